@@ -1,0 +1,241 @@
+"""oracle -- TEST INFRASTRUCTURE ONLY.
+
+ctypes/numpy front end of the plain C oracle in ``oracle.c`` (see ``oracle.h`` for
+the paper passages each function follows).  Only ``tests/``,
+``__graft_entry__.smoke()`` and ``bench.py`` (its ``cpu_baseline`` leg and its
+``--impl reference`` arm) may import this package.  It shares no code with the
+CUDA product path in ``paper_0808_2664_b200/``.
+
+All matrices are numpy float64 arrays in Fortran (column-major) order.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_HDR = os.path.join(_HERE, "oracle.h")
+_LIB = os.path.join(_HERE, "liboracle.so")
+CFLAGS = ["-O2", "-fno-fast-math", "-ffp-contract=off", "-fPIC", "-shared", "-std=c11"]
+
+
+def build(force: bool = False) -> str:
+    """Compile liboracle.so with gcc (plain C11, no BLAS)."""
+    newest = max(os.path.getmtime(_SRC), os.path.getmtime(_HDR))
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < newest:
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.run(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"], check=True)
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+_lib = None
+_i64 = ctypes.c_int64
+_pd = ctypes.POINTER(ctypes.c_double)
+_pi = ctypes.POINTER(ctypes.c_int64)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ctypes.CDLL(build())
+        _lib.orc_plan_count.restype = ctypes.c_int
+        _lib.orc_plan_fill.restype = ctypes.c_int
+    return _lib
+
+
+def _d(a: np.ndarray):
+    assert a.dtype == np.float64
+    return a.ctypes.data_as(_pd)
+
+
+def _i(a: np.ndarray):
+    assert a.dtype == np.int64
+    return a.ctypes.data_as(_pi)
+
+
+def _fortran(a) -> np.ndarray:
+    return np.asfortranarray(np.array(a, dtype=np.float64, copy=True))
+
+
+def _ld(a: np.ndarray) -> int:
+    assert a.flags.f_contiguous
+    return max(1, a.shape[0])
+
+
+# ----------------------------------------------------------------- kernels
+def house(x):
+    """Returns (v, tau, beta) with v[0] = 1 (LAPACK dlarfg convention)."""
+    x = np.array(x, dtype=np.float64, copy=True)
+    tau = ctypes.c_double()
+    beta = ctypes.c_double()
+    lib().orc_house(_i64(len(x)), _d(x), ctypes.byref(tau), ctypes.byref(beta))
+    v = x.copy()
+    v[0] = 1.0
+    return v, tau.value, beta.value
+
+
+def hqr(A):
+    """Unblocked Householder QR. Returns (F, tau): F upper = R, strictly lower = v's."""
+    F = _fortran(A)
+    m, n = F.shape
+    tau = np.zeros(n)
+    lib().orc_hqr(_i64(m), _i64(n), _d(F), _i64(_ld(F)), _d(tau))
+    return F, tau
+
+
+def combine(Ra, Rb):
+    """Structured QR of [Ra; Rb]. Returns (R, Y1, tau, flops)."""
+    a = _fortran(Ra)
+    b = _fortran(Rb)
+    n = a.shape[0]
+    tau = np.zeros(n)
+    fl = ctypes.c_double()
+    lib().orc_combine(_i64(n), _d(a), _i64(n), _d(b), _i64(n), _d(tau), ctypes.byref(fl))
+    return np.triu(a), np.triu(b), tau, fl.value
+
+
+def build_t(Y, tau):
+    """T (k x k) with H_0...H_{k-1} = I - Y T Y^T, Y unit lower trapezoidal."""
+    Y = _fortran(Y)
+    rows, k = Y.shape
+    T = np.zeros((k, k), order="F")
+    tau = np.ascontiguousarray(tau, dtype=np.float64)
+    lib().orc_build_t(_i64(rows), _i64(k), _d(Y), _i64(_ld(Y)), _d(tau), _d(T), _i64(k))
+    return T
+
+
+def build_t_node(Y1, tau):
+    Y1 = _fortran(Y1)
+    n = Y1.shape[0]
+    T = np.zeros((n, n), order="F")
+    tau = np.ascontiguousarray(tau, dtype=np.float64)
+    lib().orc_build_t_node(_i64(n), _d(Y1), _i64(n), _d(tau), _d(T), _i64(n))
+    return T
+
+
+def mgs_ld(A):
+    A = _fortran(A)
+    m, n = A.shape
+    Q = np.zeros((m, n), order="F")
+    R = np.zeros((n, n), order="F")
+    lib().orc_mgs_ld(_i64(m), _i64(n), _d(A), _i64(m), _d(Q), _i64(m), _d(R), _i64(n))
+    return Q, R
+
+
+# ------------------------------------------------------------------- plan
+@dataclass
+class Plan:
+    m: int
+    n: int
+    b: int
+    s: int
+    G: int
+    tile_row0: np.ndarray
+    tile_rows: np.ndarray
+    tile_rank: np.ndarray
+    node_a: np.ndarray
+    node_b: np.ndarray
+    node_stage: np.ndarray
+    node_level: np.ndarray
+
+    @property
+    def ntiles(self) -> int:
+        return len(self.tile_row0)
+
+    @property
+    def nnodes(self) -> int:
+        return len(self.node_a)
+
+
+def plan(m: int, n: int, b: int, s: int | None = None, G: int = 1) -> Plan:
+    s = 0 if s is None else s
+    nt, nn = _i64(), _i64()
+    rc = lib().orc_plan_count(_i64(m), _i64(n), _i64(b), _i64(s), _i64(G),
+                              ctypes.byref(nt), ctypes.byref(nn))
+    if rc != 0:
+        raise ValueError(f"invalid TSQR shape m={m} n={n} b={b} s={s} G={G}")
+    arr = [np.zeros(nt.value, np.int64) for _ in range(3)] + \
+          [np.zeros(nn.value, np.int64) for _ in range(4)]
+    rc = lib().orc_plan_fill(_i64(m), _i64(n), _i64(b), _i64(s), _i64(G), *[_i(x) for x in arr])
+    assert rc == 0
+    return Plan(m, n, b, s, G, *arr)
+
+
+# ------------------------------------------------------------------- TSQR
+@dataclass
+class Factor:
+    plan: Plan
+    A: np.ndarray          # overwritten A (tile reflectors below the tile diagonals)
+    tau_tile: np.ndarray   # ntiles x n
+    Y1: np.ndarray         # nnodes x n x n (each column-major n x n, upper)
+    tau_node: np.ndarray   # nnodes x n
+    R: np.ndarray          # n x n
+
+
+def _plan_args(p: Plan):
+    return (_i64(p.ntiles), _i(p.tile_row0), _i(p.tile_rows),
+            _i64(p.nnodes), _i(p.node_a), _i(p.node_b))
+
+
+def tsqr_factor(A, p: Plan) -> Factor:
+    F = _fortran(A)
+    m, n = F.shape
+    assert m == p.m and n == p.n
+    tau_tile = np.zeros((p.ntiles, n))
+    Y1 = np.zeros((max(p.nnodes, 1), n * n))
+    tau_node = np.zeros((max(p.nnodes, 1), n))
+    R = np.zeros((n, n), order="F")
+    lib().orc_tsqr_factor(_i64(m), _i64(n), _d(F), _i64(_ld(F)), *_plan_args(p),
+                          _d(tau_tile), _d(Y1), _d(tau_node), _d(R), _i64(n))
+    return Factor(p, F, tau_tile, Y1, tau_node, R)
+
+
+def _factor_args(f: Factor):
+    return (_d(f.A), _i64(_ld(f.A)), *_plan_args(f.plan), _d(f.tau_tile), _d(f.Y1), _d(f.tau_node))
+
+
+def tsqr_apply_qt(f: Factor, C) -> np.ndarray:
+    C = _fortran(C)
+    k = C.shape[1]
+    lib().orc_tsqr_apply_qt(_i64(f.plan.m), _i64(f.plan.n), *_factor_args(f), _d(C), _i64(_ld(C)), _i64(k))
+    return C
+
+
+def tsqr_apply_q(f: Factor, C) -> np.ndarray:
+    C = _fortran(C)
+    k = C.shape[1]
+    lib().orc_tsqr_apply_q(_i64(f.plan.m), _i64(f.plan.n), *_factor_args(f), _d(C), _i64(_ld(C)), _i64(k))
+    return C
+
+
+def tsqr_form_q(f: Factor) -> np.ndarray:
+    Q = np.zeros((f.plan.m, f.plan.n), order="F")
+    lib().orc_tsqr_form_q(_i64(f.plan.m), _i64(f.plan.n), *_factor_args(f), _d(Q), _i64(_ld(Q)))
+    return Q
+
+
+def node_y1(f: Factor, k: int) -> np.ndarray:
+    n = f.plan.n
+    return f.Y1[k].reshape(n, n, order="F")
+
+
+# --------------------------------------------------------------- checkers
+def sign_normalise(R, Q=None):
+    """R^ = diag(s) R, Q^ = Q diag(s), s = sign(diag R) (sign(0)=+1) -- reading R9."""
+    s = np.where(np.diag(R) < 0, -1.0, 1.0)
+    Rn = R * s[:, None]
+    if Q is None:
+        return Rn
+    return Rn, Q * s[None, :]
+
+
+def rel_fro(X, Y) -> float:
+    d = np.linalg.norm(np.asarray(X) - np.asarray(Y))
+    nrm = np.linalg.norm(np.asarray(Y))
+    return float(d / nrm) if nrm > 0 else float(d)

@@ -1,0 +1,418 @@
+/*
+ * oracle/oracle.c -- TEST INFRASTRUCTURE ONLY (see oracle.h).
+ *
+ * Plain loops, no BLAS, no blocking, no reordering beyond what the paper's
+ * algorithms state.  Built with  gcc -O2 -fno-fast-math -ffp-contract=off.
+ * Each function cites the passage of /root/reference/PAPER.md it follows.
+ */
+#include "oracle.h"
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define AT(a, i, j, ld) ((a)[(size_t)(i) + (size_t)(j) * (size_t)(ld)])
+
+/* House(w): Alg. QR:qnxn line 4, with LAPACK dlarfg's sign choice
+ * (reading R1) and the zero-tail rule of reading R2. */
+void orc_house(int64_t len, double *x, double *tau, double *beta)
+{
+    double alpha = x[0];
+    long double sigma2 = 0.0L;
+    for (int64_t i = 1; i < len; ++i)
+        sigma2 += (long double)x[i] * (long double)x[i];
+    if (sigma2 == 0.0L) {           /* H = I: nothing to annihilate */
+        *tau = 0.0;
+        *beta = alpha;
+        return;
+    }
+    long double norm = sqrtl((long double)alpha * (long double)alpha + sigma2);
+    double b = (double)(alpha >= 0.0 ? -norm : norm);   /* beta = -sign(alpha)||w|| */
+    *tau = (b - alpha) / b;
+    double denom = alpha - b;                            /* v = (w - beta e0)/(alpha - beta) */
+    for (int64_t i = 1; i < len; ++i)
+        x[i] = x[i] / denom;
+    *beta = b;
+}
+
+/* Unblocked Householder QR (DGEQR2): the local "sequential Householder QR" of
+ * Alg. TSQR:par line 1; reflectors overwrite the lower trapezoid,
+ * tau stored separately. */
+void orc_hqr(int64_t m, int64_t n, double *A, int64_t lda, double *tau)
+{
+    for (int64_t j = 0; j < n; ++j) {
+        double t, beta;
+        orc_house(m - j, &AT(A, j, j, lda), &t, &beta);
+        tau[j] = t;
+        /* A(j:m, j+1:n) := (I - tau v v^T) A(j:m, j+1:n), v = [1; A(j+1:m, j)] */
+        for (int64_t c = j + 1; c < n; ++c) {
+            long double w = AT(A, j, c, lda);
+            for (int64_t i = j + 1; i < m; ++i)
+                w += (long double)AT(A, i, j, lda) * (long double)AT(A, i, c, lda);
+            double tw = t * (double)w;
+            AT(A, j, c, lda) -= tw;
+            for (int64_t i = j + 1; i < m; ++i)
+                AT(A, i, c, lda) -= AT(A, i, j, lda) * tw;
+        }
+        AT(A, j, j, lda) = beta;
+    }
+}
+
+/* Alg. QR:qnxn with q = 2: index set I_j = {j, n+1:n+j}
+ * (P:1964-1965), i.e. row j of Ra and rows 0..j of Rb. */
+void orc_combine(int64_t n, double *Ra, int64_t lda, double *Rb, int64_t ldb,
+                 double *tau, double *flops)
+{
+    double fl = 0.0;
+    double *w = (double *)malloc((size_t)(n + 1) * sizeof(double));
+    for (int64_t j = 0; j < n; ++j) {
+        /* w := A(I_j, j): gather the pivot column (line 3) */
+        w[0] = AT(Ra, j, j, lda);
+        for (int64_t i = 0; i <= j; ++i) w[1 + i] = AT(Rb, i, j, ldb);
+        double t, beta;
+        orc_house(j + 2, w, &t, &beta);                           /* line 4 */
+        fl += 2.0 * (double)(j + 1) + 3.0 + (double)(j + 1);       /* norm, sqrt/div, scale */
+        /* X := (I - tau v v^T) A(I_j, j+1:n)   (lines 5-6) */
+        for (int64_t c = j + 1; c < n; ++c) {
+            long double d = AT(Ra, j, c, lda);
+            for (int64_t i = 0; i <= j; ++i)
+                d += (long double)w[1 + i] * (long double)AT(Rb, i, c, ldb);
+            double td = t * (double)d;
+            AT(Ra, j, c, lda) -= td;
+            for (int64_t i = 0; i <= j; ++i)
+                AT(Rb, i, c, ldb) -= w[1 + i] * td;
+            fl += 2.0 * (double)(j + 1) + 1.0 + 1.0 + 2.0 * (double)(j + 1) + 1.0;
+        }
+        /* scatter v(2:end) and the new diagonal (lines 7-8) */
+        AT(Ra, j, j, lda) = beta;
+        for (int64_t i = 0; i <= j; ++i) AT(Rb, i, j, ldb) = w[1 + i];
+        tau[j] = t;
+    }
+    free(w);
+    if (flops) *flops = fl;
+}
+
+/* dlarft-style T, LAPACK sign: Alg. YT:scaled computes
+ * T' with T'(j,j) = -tau_j and rho_1...rho_n = I + Y T' Y^T; we store T = -T'
+ * so that H_0...H_{k-1} = I - Y T Y^T (reading R3).  The recurrence is the
+ * paper's line "z := -tau_j (T (Y^T v_j))" with that sign flip:
+ *   T(0:j, j) = -tau_j * T(0:j, 0:j) * (Y(:,0:j)^T v_j),  T(j,j) = tau_j. */
+static void build_t_from_gram(int64_t k, const long double *G, const double *tau,
+                              double *T, int64_t ldt)
+{
+    /* G[i + j*k] = v_i^T v_j for i < j */
+    for (int64_t j = 0; j < k; ++j) {
+        for (int64_t i = 0; i < k; ++i) AT(T, i, j, ldt) = 0.0;
+        for (int64_t i = 0; i < j; ++i) {
+            long double s = 0.0L;
+            for (int64_t l = i; l < j; ++l)
+                s += (long double)AT(T, i, l, ldt) * G[l + j * k];
+            AT(T, i, j, ldt) = (double)(-(long double)tau[j] * s);
+        }
+        AT(T, j, j, ldt) = tau[j];
+    }
+}
+
+void orc_build_t(int64_t rows, int64_t k, const double *Y, int64_t ldy,
+                 const double *tau, double *T, int64_t ldt)
+{
+    long double *G = (long double *)calloc((size_t)(k * k), sizeof(long double));
+    for (int64_t j = 0; j < k; ++j)
+        for (int64_t i = 0; i < j; ++i) {
+            /* v_i = [0..0, 1 (row i), Y(i+1:, i)], v_j = [0..0, 1 (row j), Y(j+1:, j)] */
+            long double s = (long double)AT(Y, j, i, ldy);          /* v_i(j) * v_j(j)=1 */
+            for (int64_t r = j + 1; r < rows; ++r)
+                s += (long double)AT(Y, r, i, ldy) * (long double)AT(Y, r, j, ldy);
+            G[i + j * k] = s;
+        }
+    build_t_from_gram(k, G, tau, T, ldt);
+    free(G);
+}
+
+void orc_build_t_node(int64_t n, const double *Y1, int64_t ldy, const double *tau,
+                      double *T, int64_t ldt)
+{
+    long double *G = (long double *)calloc((size_t)(n * n), sizeof(long double));
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i < j; ++i) {
+            /* [e_i; y_i]^T [e_j; y_j] = y_i^T y_j, y_i nonzero in rows 0..i */
+            long double s = 0.0L;
+            for (int64_t r = 0; r <= i; ++r)
+                s += (long double)AT(Y1, r, i, ldy) * (long double)AT(Y1, r, j, ldy);
+            G[i + j * n] = s;
+        }
+    build_t_from_gram(n, G, tau, T, ldt);
+    free(G);
+}
+
+/* ------------------------------- plan ------------------------------------ */
+
+typedef struct {
+    int64_t ntiles, nnodes;
+    int64_t *tile_row0, *tile_rows, *tile_rank;
+    int64_t *node_a, *node_b, *node_stage, *node_level;
+    int count_only;
+} plan_out;
+
+static void emit_node(plan_out *p, int64_t a, int64_t b, int64_t stage, int64_t level)
+{
+    if (!p->count_only) {
+        p->node_a[p->nnodes] = a;
+        p->node_b[p->nnodes] = b;
+        p->node_stage[p->nnodes] = stage;
+        p->node_level[p->nnodes] = level;
+    }
+    p->nnodes++;
+}
+
+/* binary reduction of list[0..len) with pairing (2i, 2i+1) and the odd
+ * trailing entry promoted unchanged (Alg. TSQR:par P:1693-1696; reading R5) */
+static void reduce_binary(plan_out *p, int64_t *list, int64_t len, int64_t stage)
+{
+    int64_t level = 1;
+    while (len > 1) {
+        int64_t out = 0;
+        for (int64_t i = 0; i < len; i += 2) {
+            if (i + 1 < len) emit_node(p, list[i], list[i + 1], stage, level);
+            list[out++] = list[i];
+        }
+        len = out;
+        level++;
+    }
+}
+
+static int build_plan(int64_t m, int64_t n, int64_t b, int64_t s, int64_t G, plan_out *p)
+{
+    if (n < 1 || m < n || b < 1 || s < 0 || G < 1) return -1;
+    if ((G & (G - 1)) != 0) return -1;
+    /* row blocks (reading R6) */
+    int64_t nblk = m / b, rem = m - (m / b) * b;
+    int64_t last_rows = b;
+    if (nblk == 0) { nblk = 1; last_rows = m; }
+    else if (rem >= n) { nblk += 1; last_rows = rem; }
+    else if (rem > 0) { last_rows = b + rem; }
+    if (nblk < G) return -1;
+    int64_t *blk_row0 = (int64_t *)malloc((size_t)nblk * sizeof(int64_t));
+    int64_t *blk_rows = (int64_t *)malloc((size_t)nblk * sizeof(int64_t));
+    for (int64_t k = 0; k < nblk; ++k) {
+        blk_row0[k] = k * b;
+        blk_rows[k] = (k == nblk - 1) ? last_rows : b;
+    }
+    /* tiles */
+    int64_t *blk_tile0 = (int64_t *)malloc((size_t)(nblk + 1) * sizeof(int64_t));
+    int64_t nt = 0;
+    for (int64_t k = 0; k < nblk; ++k) {
+        blk_tile0[k] = nt;
+        int64_t h = blk_rows[k];
+        int64_t t = (s == 0) ? 1 : (h + s - 1) / s;   /* s = 0: one tile per block */
+        int64_t base = h / t, extra = h - base * t;
+        int64_t r0 = blk_row0[k];
+        for (int64_t i = 0; i < t; ++i) {
+            int64_t rows = base + (i < extra ? 1 : 0);
+            if (rows < n) { free(blk_row0); free(blk_rows); free(blk_tile0); return -1; }
+            if (!p->count_only) { p->tile_row0[nt] = r0; p->tile_rows[nt] = rows; }
+            r0 += rows;
+            nt++;
+        }
+    }
+    blk_tile0[nblk] = nt;
+    p->ntiles = nt;
+    /* ranks: contiguous runs of whole blocks */
+    int64_t *rank_blk0 = (int64_t *)malloc((size_t)(G + 1) * sizeof(int64_t));
+    {
+        int64_t base = nblk / G, extra = nblk - base * G, k0 = 0;
+        for (int64_t r = 0; r < G; ++r) {
+            rank_blk0[r] = k0;
+            k0 += base + (r < extra ? 1 : 0);
+        }
+        rank_blk0[G] = nblk;
+    }
+    if (!p->count_only)
+        for (int64_t r = 0; r < G; ++r)
+            for (int64_t k = rank_blk0[r]; k < rank_blk0[r + 1]; ++k)
+                for (int64_t t = blk_tile0[k]; t < blk_tile0[k + 1]; ++t) p->tile_rank[t] = r;
+    /* nodes */
+    int64_t *list = (int64_t *)malloc((size_t)(nt + nblk + G + 1) * sizeof(int64_t));
+    p->nnodes = 0;
+    for (int64_t r = 0; r < G; ++r) {
+        for (int64_t k = rank_blk0[r]; k < rank_blk0[r + 1]; ++k) {      /* stage 0 */
+            int64_t len = 0;
+            for (int64_t t = blk_tile0[k]; t < blk_tile0[k + 1]; ++t) list[len++] = t;
+            reduce_binary(p, list, len, 0);
+        }
+        int64_t len = 0;                                                  /* stage 1 */
+        for (int64_t k = rank_blk0[r]; k < rank_blk0[r + 1]; ++k) list[len++] = blk_tile0[k];
+        reduce_binary(p, list, len, 1);
+    }
+    {
+        int64_t len = 0;                                                  /* stage 2 */
+        for (int64_t r = 0; r < G; ++r) list[len++] = blk_tile0[rank_blk0[r]];
+        reduce_binary(p, list, len, 2);
+    }
+    free(list); free(rank_blk0); free(blk_tile0); free(blk_row0); free(blk_rows);
+    return 0;
+}
+
+int orc_plan_count(int64_t m, int64_t n, int64_t b, int64_t s, int64_t G,
+                   int64_t *ntiles, int64_t *nnodes)
+{
+    plan_out p;
+    memset(&p, 0, sizeof(p));
+    p.count_only = 1;
+    int rc = build_plan(m, n, b, s, G, &p);
+    *ntiles = p.ntiles;
+    *nnodes = p.nnodes;
+    return rc;
+}
+
+int orc_plan_fill(int64_t m, int64_t n, int64_t b, int64_t s, int64_t G,
+                  int64_t *tile_row0, int64_t *tile_rows, int64_t *tile_rank,
+                  int64_t *node_a, int64_t *node_b, int64_t *node_stage,
+                  int64_t *node_level)
+{
+    plan_out p;
+    memset(&p, 0, sizeof(p));
+    p.tile_row0 = tile_row0; p.tile_rows = tile_rows; p.tile_rank = tile_rank;
+    p.node_a = node_a; p.node_b = node_b; p.node_stage = node_stage; p.node_level = node_level;
+    return build_plan(m, n, b, s, G, &p);
+}
+
+/* ------------------------------- TSQR ------------------------------------ */
+
+/* Eqs. 1-4: every tile A_i = Q_i R_i, then stacked pairs of R's
+ * are re-factored up the tree; the implicit Q is the tree of local factors. */
+void orc_tsqr_factor(int64_t m, int64_t n, double *A, int64_t lda,
+                     int64_t ntiles, const int64_t *tile_row0, const int64_t *tile_rows,
+                     int64_t nnodes, const int64_t *node_a, const int64_t *node_b,
+                     double *tau_tile, double *Y1, double *tau_node,
+                     double *R, int64_t ldr)
+{
+    (void)m;
+    size_t nn = (size_t)(n * n);
+    double *Rsub = (double *)calloc((size_t)ntiles * nn, sizeof(double));
+    for (int64_t t = 0; t < ntiles; ++t) {                       /* Eq. 1 */
+        double *At = A + tile_row0[t];
+        orc_hqr(tile_rows[t], n, At, lda, tau_tile + t * n);
+        for (int64_t j = 0; j < n; ++j)
+            for (int64_t i = 0; i <= j; ++i) AT(Rsub + t * nn, i, j, n) = AT(At, i, j, lda);
+    }
+    for (int64_t k = 0; k < nnodes; ++k) {                       /* Eqs. 2-3 */
+        double *Ra = Rsub + node_a[k] * nn, *Rb = Rsub + node_b[k] * nn;
+        orc_combine(n, Ra, n, Rb, n, tau_node + k * n, NULL);
+        double *Yk = Y1 + k * nn;
+        for (int64_t j = 0; j < n; ++j)
+            for (int64_t i = 0; i < n; ++i) AT(Yk, i, j, n) = (i <= j) ? AT(Rb, i, j, n) : 0.0;
+    }
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i < n; ++i) AT(R, i, j, ldr) = (i <= j) ? AT(Rsub, i, j, n) : 0.0;
+    free(Rsub);
+}
+
+/* one tile reflector j applied to C rows [r0+j, r0+rows) : C -= tau v (v^T C) */
+static void apply_tile_reflector(int64_t rows, int64_t j, const double *At, int64_t lda,
+                                 double tau, double *Ct, int64_t ldc, int64_t k)
+{
+    if (tau == 0.0) return;
+    for (int64_t c = 0; c < k; ++c) {
+        long double w = AT(Ct, j, c, ldc);
+        for (int64_t i = j + 1; i < rows; ++i)
+            w += (long double)AT(At, i, j, lda) * (long double)AT(Ct, i, c, ldc);
+        double tw = tau * (double)w;
+        AT(Ct, j, c, ldc) -= tw;
+        for (int64_t i = j + 1; i < rows; ++i) AT(Ct, i, c, ldc) -= AT(At, i, j, lda) * tw;
+    }
+}
+
+/* one node reflector j (vector [e_j; Y1(0:j, j)]) applied to the head rows
+ * Ca (row j) and Cb (rows 0..j): eq. localQTupdate one column
+ * of [I; Y1] at a time. */
+static void apply_node_reflector(int64_t n, int64_t j, const double *Yk, double tau,
+                                 double *Ca, double *Cb, int64_t ldc, int64_t k)
+{
+    (void)n;
+    if (tau == 0.0) return;
+    for (int64_t c = 0; c < k; ++c) {
+        long double w = AT(Ca, j, c, ldc);
+        for (int64_t i = 0; i <= j; ++i)
+            w += (long double)AT(Yk, i, j, n) * (long double)AT(Cb, i, c, ldc);
+        double tw = tau * (double)w;
+        AT(Ca, j, c, ldc) -= tw;
+        for (int64_t i = 0; i <= j; ++i) AT(Cb, i, c, ldc) -= AT(Yk, i, j, n) * tw;
+    }
+}
+
+/* Q^T C: leaves first, then nodes bottom-up in factor order (Eq. 4 gives
+ * A = Q_leaves Q_level1 ... Q_root R; reading R4). */
+void orc_tsqr_apply_qt(int64_t m, int64_t n, const double *A, int64_t lda,
+                       int64_t ntiles, const int64_t *tile_row0, const int64_t *tile_rows,
+                       int64_t nnodes, const int64_t *node_a, const int64_t *node_b,
+                       const double *tau_tile, const double *Y1, const double *tau_node,
+                       double *C, int64_t ldc, int64_t k)
+{
+    (void)m;
+    size_t nn = (size_t)(n * n);
+    for (int64_t t = 0; t < ntiles; ++t)
+        for (int64_t j = 0; j < n; ++j)          /* Q_t^T = H_{n-1} ... H_0 : H_0 first */
+            apply_tile_reflector(tile_rows[t], j, A + tile_row0[t], lda, tau_tile[t * n + j],
+                                 C + tile_row0[t], ldc, k);
+    for (int64_t q = 0; q < nnodes; ++q)
+        for (int64_t j = 0; j < n; ++j)
+            apply_node_reflector(n, j, Y1 + q * nn, tau_node[q * n + j],
+                                 C + tile_row0[node_a[q]], C + tile_row0[node_b[q]], ldc, k);
+}
+
+void orc_tsqr_apply_q(int64_t m, int64_t n, const double *A, int64_t lda,
+                      int64_t ntiles, const int64_t *tile_row0, const int64_t *tile_rows,
+                      int64_t nnodes, const int64_t *node_a, const int64_t *node_b,
+                      const double *tau_tile, const double *Y1, const double *tau_node,
+                      double *C, int64_t ldc, int64_t k)
+{
+    (void)m;
+    size_t nn = (size_t)(n * n);
+    for (int64_t q = nnodes - 1; q >= 0; --q)
+        for (int64_t j = n - 1; j >= 0; --j)     /* Q_node = H_0 ... H_{n-1}: H_{n-1} first */
+            apply_node_reflector(n, j, Y1 + q * nn, tau_node[q * n + j],
+                                 C + tile_row0[node_a[q]], C + tile_row0[node_b[q]], ldc, k);
+    for (int64_t t = 0; t < ntiles; ++t)
+        for (int64_t j = n - 1; j >= 0; --j)
+            apply_tile_reflector(tile_rows[t], j, A + tile_row0[t], lda, tau_tile[t * n + j],
+                                 C + tile_row0[t], ldc, k);
+}
+
+void orc_tsqr_form_q(int64_t m, int64_t n, const double *A, int64_t lda,
+                     int64_t ntiles, const int64_t *tile_row0, const int64_t *tile_rows,
+                     int64_t nnodes, const int64_t *node_a, const int64_t *node_b,
+                     const double *tau_tile, const double *Y1, const double *tau_node,
+                     double *Q, int64_t ldq)
+{
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i < m; ++i) AT(Q, i, j, ldq) = (i == j) ? 1.0 : 0.0;
+    orc_tsqr_apply_q(m, n, A, lda, ntiles, tile_row0, tile_rows, nnodes, node_a, node_b,
+                     tau_tile, Y1, tau_node, Q, ldq, n);
+}
+
+/* Modified Gram-Schmidt, every operation in long double. */
+void orc_mgs_ld(int64_t m, int64_t n, const double *A, int64_t lda,
+                double *Q, int64_t ldq, double *R, int64_t ldr)
+{
+    long double *V = (long double *)malloc((size_t)(m * n) * sizeof(long double));
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i < m; ++i) V[i + j * m] = AT(A, i, j, lda);
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i < n; ++i) AT(R, i, j, ldr) = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+        long double s = 0.0L;
+        for (int64_t i = 0; i < m; ++i) s += V[i + j * m] * V[i + j * m];
+        long double r = sqrtl(s);
+        AT(R, j, j, ldr) = (double)r;
+        for (int64_t i = 0; i < m; ++i) V[i + j * m] /= r;
+        for (int64_t c = j + 1; c < n; ++c) {
+            long double d = 0.0L;
+            for (int64_t i = 0; i < m; ++i) d += V[i + j * m] * V[i + c * m];
+            AT(R, j, c, ldr) = (double)d;
+            for (int64_t i = 0; i < m; ++i) V[i + c * m] -= d * V[i + j * m];
+        }
+    }
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i < m; ++i) AT(Q, i, j, ldq) = (double)V[i + j * m];
+    free(V);
+}

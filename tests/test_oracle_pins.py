@@ -1,0 +1,376 @@
+"""Pins of the CPU oracle to things other than itself (worked examples, closed
+forms, textbook / library special cases, invariants, brute force).
+
+Every check here is independent of the oracle's own arithmetic: explicit
+reflector matrices are built with numpy from the returned (v, tau), LAPACK is
+reached through numpy/torch, MGS in long double is a different algorithm.
+Citations: P:n = /root/reference/PAPER.md line n, S:n = SPEC.md line n.
+"""
+import os
+
+import numpy as np
+import pytest
+import scipy.linalg
+
+import oracle as orc
+
+EPS = np.finfo(np.float64).eps
+
+
+def _golden_rows(path):
+    rows = []
+    with open(path) as f:
+        for line in f:
+            line = line.strip()
+            if line and not line.startswith("#"):
+                rows.append(line.split())
+    return rows
+
+
+def _rng(seed):
+    return np.random.default_rng(seed)
+
+
+def _explicit_tile_q(F, tau, rows, n):
+    """Q = H_0 H_1 ... H_{n-1} as an explicit rows x rows matrix (numpy)."""
+    Q = np.eye(rows)
+    for j in range(n):
+        v = np.zeros(rows)
+        v[j] = 1.0
+        v[j + 1:] = F[j + 1:rows, j]
+        Q = Q @ (np.eye(rows) - tau[j] * np.outer(v, v))
+    return Q
+
+
+def _explicit_node_q(Y1, tau):
+    n = Y1.shape[0]
+    Q = np.eye(2 * n)
+    for j in range(n):
+        v = np.zeros(2 * n)
+        v[j] = 1.0
+        v[n:n + j + 1] = Y1[:j + 1, j]
+        Q = Q @ (np.eye(2 * n) - tau[j] * np.outer(v, v))
+    return Q
+
+
+# --------------------------------------------------------------------- house
+def test_house_worked_example(golden_dir):
+    (row,) = _golden_rows(os.path.join(golden_dir, "house_3_4.txt"))
+    w0, w1, v0, v1, tau, beta = map(float, row)
+    v, t, b = orc.house([w0, w1])
+    assert v[0] == v0 and v[1] == v1 and t == tau and b == beta
+
+
+def test_house_special_cases():
+    # x = (c,0,0), c > 0 -> tau = 0, beta = c ; x = 0 -> tau = 0, beta = 0
+    v, t, b = orc.house([2.5, 0.0, 0.0])
+    assert t == 0.0 and b == 2.5 and list(v) == [1.0, 0.0, 0.0]
+    v, t, b = orc.house([0.0, 0.0, 0.0])
+    assert t == 0.0 and b == 0.0
+    # reading R2: a negative pivot with a zero tail is left alone (H = I)
+    v, t, b = orc.house([-3.0, 0.0])
+    assert t == 0.0 and b == -3.0
+    # sign(0) = +1 -> beta = -||x||
+    v, t, b = orc.house([0.0, 3.0, 4.0])
+    assert b == -5.0 and t == 1.0
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_house_annihilates(seed):
+    w = _rng(seed).standard_normal(7) * 10.0 ** _rng(seed + 100).integers(-5, 5)
+    v, t, b = orc.house(w)
+    H = np.eye(len(w)) - t * np.outer(v, v)
+    hw = H @ w
+    assert abs(hw[0] - b) <= 8 * EPS * np.linalg.norm(w)
+    assert np.linalg.norm(hw[1:]) <= 8 * EPS * np.linalg.norm(w)
+    assert np.linalg.norm(H.T @ H - np.eye(len(w))) <= 16 * EPS
+    assert abs(b) == pytest.approx(np.linalg.norm(w), rel=4 * EPS)
+    assert 1.0 <= t <= 2.0              # LAPACK property of dlarfg for real data
+    assert np.sign(b) == -np.sign(w[0])
+
+
+# ----------------------------------------------------------------------- hqr
+GRID = [(8, 3), (64, 6), (128, 32), (512, 64)]   # S:649 acceptance grid (n <= 64)
+
+
+@pytest.mark.parametrize("m,n", GRID)
+def test_hqr_vs_long_double_mgs(m, n):
+    A = _rng(m * 1000 + n).standard_normal((m, n))
+    F, tau = orc.hqr(A)
+    _, Rm = orc.mgs_ld(A)
+    assert orc.rel_fro(orc.sign_normalise(np.triu(F[:n])), Rm) <= 1e-13
+
+
+@pytest.mark.parametrize("m,n", GRID + [(300, 40)])
+def test_hqr_vs_lapack(m, n):
+    A = _rng(m + n).standard_normal((m, n))
+    F, tau = orc.hqr(A)
+    Rl = np.linalg.qr(A, mode="r")
+    assert orc.rel_fro(orc.sign_normalise(np.triu(F[:n])), orc.sign_normalise(Rl)) <= 1e-13
+
+
+def test_hqr_identity_columns():
+    # A = I(:,1:n) -> R = I, tau = 0 exactly
+    A = np.eye(10)[:, :4]
+    F, tau = orc.hqr(A)
+    assert np.all(tau == 0.0)
+    assert np.array_equal(np.triu(F[:4]), np.eye(4))
+
+
+@pytest.mark.parametrize("m,n", [(8, 3), (64, 6), (40, 40)])
+def test_hqr_invariants(m, n):
+    A = _rng(7 * m + n).standard_normal((m, n))
+    F, tau = orc.hqr(A)
+    Q = _explicit_tile_q(F, tau, m, n)[:, :n]
+    R = np.triu(F[:n])
+    assert np.linalg.norm(A - Q @ R) / np.linalg.norm(A) <= 1e-14
+    assert np.linalg.norm(Q.T @ Q - np.eye(n)) <= 1e-14
+    # Corollary 1 identity: R^T R = A^T A
+    assert np.linalg.norm(R.T @ R - A.T @ A) / np.linalg.norm(A) ** 2 <= 1e-14
+
+
+def test_hqr_rank_deficient_zero_column():
+    # reading R2: a zero column gives tau = 0 (H = I), no error
+    A = _rng(3).standard_normal((20, 5))
+    A[:, 2] = 0.0
+    A[:, 4] = A[:, 0]
+    F, tau = orc.hqr(A)
+    Q = _explicit_tile_q(F, tau, 20, 5)[:, :5]
+    assert np.linalg.norm(A - Q @ np.triu(F[:5])) <= 1e-14 * np.linalg.norm(A)
+    assert np.all(np.isfinite(F))
+
+
+# ------------------------------------------------------------------- combine
+def test_combine_sparsity_matches_paper(golden_dir):
+    # eq. fact_2rs, P:1051-1083 (the 5x5 example)
+    pat = _golden_rows(os.path.join(golden_dir, "fact_2rs_pattern.txt"))
+    rng = _rng(11)
+    Ra = np.triu(rng.standard_normal((5, 5)))
+    Rb = np.triu(rng.standard_normal((5, 5)))
+    R, Y1, tau, _ = orc.combine(Ra, Rb)
+    V = np.vstack([np.eye(5), Y1])
+    for i in range(10):
+        for j in range(5):
+            c = pat[i][j]
+            if c == "1":
+                assert V[i, j] == 1.0
+            elif c == ".":
+                assert V[i, j] == 0.0
+            else:
+                assert V[i, j] != 0.0
+
+
+@pytest.mark.parametrize("n", [1, 2, 8, 32, 64])
+def test_combine_vs_dense_qr(n):
+    rng = _rng(n)
+    Ra = np.triu(rng.standard_normal((n, n)))
+    Rb = np.triu(rng.standard_normal((n, n)))
+    R, Y1, tau, _ = orc.combine(Ra, Rb)
+    S = np.vstack([Ra, Rb])
+    F, _ = orc.hqr(S)                                       # dense, unstructured
+    assert orc.rel_fro(orc.sign_normalise(R), orc.sign_normalise(np.triu(F[:n]))) <= 1e-13
+    assert orc.rel_fro(orc.sign_normalise(R), orc.sign_normalise(np.linalg.qr(S, mode="r"))) <= 1e-13
+    # Y1 strictly lower is exactly zero
+    assert np.all(np.tril(Y1, -1) == 0.0)
+    # explicit node Q: Q^T [Ra; Rb] = [R; 0]
+    Q = _explicit_node_q(Y1, tau)
+    out = Q.T @ S
+    assert np.linalg.norm(out[:n] - R) <= 1e-13 * np.linalg.norm(S)
+    assert np.linalg.norm(out[n:]) <= 1e-13 * np.linalg.norm(S)
+
+
+def test_combine_identity_zero():
+    # R0 = I, R1 = 0 -> R = I, tau = 0
+    R, Y1, tau, _ = orc.combine(np.eye(6), np.zeros((6, 6)))
+    assert np.array_equal(R, np.eye(6)) and np.all(tau == 0.0) and np.all(Y1 == 0.0)
+
+
+def test_combine_flop_count():
+    # (2/3) n^3 for the structured QR of two triangles
+    _, _, _, fl = orc.combine(np.triu(np.ones((64, 64))), np.triu(np.ones((64, 64))))
+    ratio = fl / (2.0 / 3.0 * 64 ** 3)
+    assert 1.0 <= ratio <= 1.1
+
+
+# -------------------------------------------------------------------- T build
+@pytest.mark.parametrize("rows,k", [(6, 3), (40, 8), (64, 64)])
+def test_build_t_leaf(rows, k):
+    A = _rng(rows + k).standard_normal((rows, k))
+    F, tau = orc.hqr(A)
+    Y = np.tril(F, -1)
+    Y[np.arange(k), np.arange(k)] = 1.0
+    T = orc.build_t(F, tau)
+    Qexp = _explicit_tile_q(F, tau, rows, k)
+    assert np.linalg.norm(np.eye(rows) - Y @ T @ Y.T - Qexp) <= 1e-13 * rows
+    assert np.all(np.tril(T, -1) == 0.0) and np.array_equal(np.diag(T), tau)
+
+
+@pytest.mark.parametrize("n", [3, 16, 33])
+def test_build_t_node(n):
+    rng = _rng(50 + n)
+    R, Y1, tau, _ = orc.combine(np.triu(rng.standard_normal((n, n))), np.triu(rng.standard_normal((n, n))))
+    T = orc.build_t_node(Y1, tau)
+    Y = np.vstack([np.eye(n), Y1])
+    assert np.linalg.norm(np.eye(2 * n) - Y @ T @ Y.T - _explicit_node_q(Y1, tau)) <= 1e-13 * n
+    # the paper's Alg. YT:scaled T' satisfies rho_1...rho_n = I + Y T' Y^T with T' = -T (reading R3)
+    assert np.linalg.norm(np.eye(2 * n) + Y @ (-T) @ Y.T - _explicit_node_q(Y1, tau)) <= 1e-13 * n
+
+
+# ---------------------------------------------------------------------- plan
+def _plan_nodes(p):
+    return [(int(l), int(a), int(b)) for a, b, l in zip(p.node_a, p.node_b, p.node_level)]
+
+
+def test_plan_eq4_tree(golden_dir):
+    ref = [tuple(map(int, r)) for r in _golden_rows(os.path.join(golden_dir, "eq4_binary_tree_p4.txt"))]
+    p = orc.plan(4 * 32, 8, 32)
+    assert _plan_nodes(p) == ref
+
+
+def test_plan_promotion_p5(golden_dir):
+    ref = [tuple(map(int, r)) for r in _golden_rows(os.path.join(golden_dir, "build_tree_p5.txt"))]
+    p = orc.plan(5 * 32, 8, 32)
+    assert _plan_nodes(p) == ref
+    widths = [5]
+    for lev in range(1, 4):
+        widths.append(widths[-1] - int(np.sum(p.node_level == lev)))
+    assert widths == [5, 3, 2, 1]
+
+
+def test_plan_config_shapes():
+    p = orc.plan(4096, 16, 512)                  # config 1: 8 leaves, depth 3
+    assert p.ntiles == 8 and p.nnodes == 7 and p.node_level.max() == 3
+    p = orc.plan(1_000_000, 50, 4096)            # config 2: 245 blocks, last one 576 rows
+    assert p.ntiles == 245 and p.tile_rows[-1] == 576
+    assert p.node_level.max() == int(np.ceil(np.log2(245)))
+    p = orc.plan(100_000, 200, 2048)             # config 3: 49 blocks, last 1696 rows
+    assert p.ntiles == 49 and p.tile_rows[-1] == 1696
+    p = orc.plan(1_000_000, 50, 4096, 256, 8)    # runs of 31,31,31,31,31,30,30,30 blocks
+    blocks_per_rank = []
+    for r in range(8):
+        rows = p.tile_rows[p.tile_rank == r].sum()
+        blocks_per_rank.append(int(np.ceil(rows / 4096)))
+    assert blocks_per_rank == [31, 31, 31, 31, 31, 30, 30, 30]
+    # every tile is >= n rows and <= s rows; tiles cover 0..m-1 contiguously
+    assert np.all(p.tile_rows >= 50) and np.all(p.tile_rows <= 256)
+    assert p.tile_row0[0] == 0 and np.all(p.tile_row0[1:] == np.cumsum(p.tile_rows)[:-1])
+    assert p.tile_row0[-1] + p.tile_rows[-1] == 1_000_000
+    # rank stage: G - 1 nodes, depth log2 G (Table 1: log P messages)
+    assert np.sum(p.node_stage == 2) == 7 and p.node_level[p.node_stage == 2].max() == 3
+    # a binary tree over L tiles has L - 1 nodes
+    assert p.nnodes == p.ntiles - 1
+
+
+def test_plan_remainder_rules():
+    # remainder >= n becomes its own block; < n merges into the last block (reading R6)
+    p = orc.plan(1000 + 10, 16, 500)
+    assert list(p.tile_rows) == [500, 510]
+    p = orc.plan(1000 + 10, 16, 500, 200)
+    assert list(p.tile_rows) == [167, 167, 166, 170, 170, 170]
+    p = orc.plan(1000 + 16, 16, 500)
+    assert list(p.tile_rows) == [500, 500, 16]
+
+
+@pytest.mark.parametrize("args", [(5, 8, 4, 4, 1), (64, 8, 16, 16, 3), (64, 8, 32, 32, 4), (64, 8, 16, 4, 1)])
+def test_plan_rejects(args):
+    with pytest.raises(ValueError):
+        orc.plan(*args[:3], s=args[3], G=args[4])
+
+
+# ---------------------------------------------------------------------- TSQR
+@pytest.mark.parametrize("m,n,b,s,G", [
+    (64, 6, 16, 16, 4),                 # S:218 P=4 binary on 64x6
+    (4096, 16, 512, 512, 1),            # config 1
+    (3000, 24, 700, 256, 2),
+    (2048, 64, 512, 256, 4),
+    (1500, 33, 400, 128, 1),
+])
+def test_tsqr_r_vs_flat(m, n, b, s, G):
+    A = _rng(m + n + b).standard_normal((m, n))
+    f = orc.tsqr_factor(A, orc.plan(m, n, b, s, G))
+    Rflat = np.triu(orc.hqr(A)[0][:n])
+    assert np.all(np.tril(f.R, -1) == 0.0)
+    assert orc.rel_fro(orc.sign_normalise(f.R), orc.sign_normalise(Rflat)) <= 1e-13
+    assert np.linalg.norm(f.R.T @ f.R - A.T @ A) / np.linalg.norm(A) ** 2 <= 1e-14
+
+
+def test_tsqr_tree_independence():
+    # any tree gives the same R modulo signs
+    A = _rng(5).standard_normal((2048, 20))
+    Rs = [orc.sign_normalise(orc.tsqr_factor(A, orc.plan(2048, 20, b, s, G)).R)
+          for (b, s, G) in [(2048, 2048, 1), (256, 256, 1), (512, 64, 2), (128, 40, 8)]]
+    for R in Rs[1:]:
+        assert orc.rel_fro(R, Rs[0]) <= 1e-13
+
+
+def test_tsqr_r_vs_mgs_tiny():
+    A = _rng(9).standard_normal((64, 6))
+    f = orc.tsqr_factor(A, orc.plan(64, 6, 16, 16, 1))
+    _, Rm = orc.mgs_ld(A)
+    assert orc.rel_fro(orc.sign_normalise(f.R), Rm) <= 1e-13
+
+
+@pytest.mark.parametrize("m,n,b,s,G,k", [(512, 8, 128, 64, 2, 5), (1200, 16, 300, 150, 1, 16)])
+def test_tsqr_apply_qt_closed_forms(m, n, b, s, G, k):
+    rng = _rng(m * k)
+    A = rng.standard_normal((m, n))
+    p = orc.plan(m, n, b, s, G)
+    f = orc.tsqr_factor(A, p)
+    # Q^T A = [R; 0] in tree order
+    QtA = orc.tsqr_apply_qt(f, A)
+    assert np.linalg.norm(QtA[:n] - f.R) <= 1e-14 * np.linalg.norm(A) * 10
+    assert np.linalg.norm(QtA[n:]) <= 1e-14 * np.linalg.norm(A) * 10
+    C = rng.standard_normal((m, k))
+    QtC = orc.tsqr_apply_qt(f, C)
+    assert abs(np.linalg.norm(QtC) - np.linalg.norm(C)) <= 1e-14 * np.linalg.norm(C) * 10
+    back = orc.tsqr_apply_q(f, QtC)
+    assert np.linalg.norm(back - C) <= 1e-14 * np.linalg.norm(C) * 10
+    Q = orc.tsqr_form_q(f)
+    assert np.linalg.norm(QtC[:n] - Q.T @ C) <= 1e-13 * np.linalg.norm(C)
+
+
+@pytest.mark.parametrize("m,n,b,s,G", [(4096, 16, 512, 512, 1), (3000, 30, 1000, 200, 2)])
+def test_tsqr_form_q(m, n, b, s, G):
+    A = _rng(m - n).standard_normal((m, n))
+    f = orc.tsqr_factor(A, orc.plan(m, n, b, s, G))
+    Q = orc.tsqr_form_q(f)
+    assert np.linalg.norm(A - Q @ f.R) / np.linalg.norm(A) <= 1e-13
+    assert np.linalg.norm(Q.T @ Q - np.eye(n)) <= 1e-13
+    # kappa ~ 1: Q = A R^{-1} by an independent triangular solve
+    Qs = scipy.linalg.solve_triangular(f.R, A.T, trans="T", lower=False).T
+    assert np.linalg.norm(Q - Qs) / np.linalg.norm(Qs) <= 1e-12
+
+
+def test_tsqr_orthonormal_input():
+    # A with orthonormal columns: Q^ = A, R^ = I
+    Qa, _ = np.linalg.qr(_rng(1).standard_normal((1024, 12)))
+    f = orc.tsqr_factor(Qa, orc.plan(1024, 12, 256, 128, 1))
+    Rn, Qn = orc.sign_normalise(f.R, orc.tsqr_form_q(f))
+    assert np.linalg.norm(Rn - np.eye(12)) <= 1e-13
+    assert np.linalg.norm(Qn - Qa) <= 1e-13
+
+
+def test_tsqr_ill_conditioned_invariants():
+    # the C4 recipe at a small size: sigma log-spaced 1 .. 1e-10
+    rng = _rng(2)
+    n = 16
+    G = rng.standard_normal((4096, n))
+    sig = 10.0 ** (-10.0 * np.arange(n) / (n - 1))
+    V, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    A = (G * sig) @ V.T
+    f = orc.tsqr_factor(A, orc.plan(4096, n, 512, 256, 1))
+    Q = orc.tsqr_form_q(f)
+    assert np.linalg.norm(A - Q @ f.R) / np.linalg.norm(A) <= 1e-13
+    assert np.linalg.norm(Q.T @ Q - np.eye(n)) <= 1e-13
+    assert np.linalg.norm(f.R.T @ f.R - A.T @ A) / np.linalg.norm(A) ** 2 <= 1e-14
+    Rflat = np.linalg.qr(A, mode="r")
+    assert orc.rel_fro(orc.sign_normalise(f.R), orc.sign_normalise(Rflat)) <= 1e-13
+
+
+def test_mgs_ld_pins():
+    Q, R = orc.mgs_ld(np.array([[3.0], [4.0]]))
+    assert R[0, 0] == 5.0 and np.allclose(Q[:, 0], [0.6, 0.8], rtol=0, atol=1e-16)
+    A = _rng(4).standard_normal((50, 7))
+    Q, R = orc.mgs_ld(A)
+    assert orc.rel_fro(R, orc.sign_normalise(np.linalg.qr(A, mode="r"))) <= 1e-14
+    assert np.linalg.norm(Q.T @ Q - np.eye(7)) <= 1e-14
