@@ -1,0 +1,171 @@
+/*
+ * include/tsqr.h -- C-ABI of libtsqr.so, a B200-native (sm_100a) Tall-Skinny QR
+ * (TSQR) after arXiv 0808.2664 (Demmel, Grigori, Hoemmen, Langou).
+ * "P:n" = line n of the paper's LaTeX source, with its section /
+ * equation / algorithm.  DESIGN.md states the plan rules and the readings R1-R13.
+ *
+ * Conventions for every call
+ *   - Matrices are fp64, COLUMN-MAJOR: element (i,j) of X lives at X[i + j*ldx].
+ *   - Pointers named "device" must be CUDA device (or managed) memory on the
+ *     current device; "host" pointers are ordinary host memory.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Every device call is asynchronous and stream-ordered.
+ *   - Arguments are validated on the host BEFORE anything is enqueued: a status
+ *     other than TSQR_OK means nothing was enqueued and nothing was modified.
+ *   - Asynchronous device faults surface as TSQR_ERR_CUDA from a later call or
+ *     at the caller's own synchronisation.  No exception or abort crosses the ABI.
+ *   - A tree handle must be used on one device by one host thread at a time.
+ */
+#ifndef TSQR_H
+#define TSQR_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    TSQR_OK = 0,
+    TSQR_ERR_INVALID = 1,      /* null pointer, ld too small, k < 0, bad round / rank  */
+    TSQR_ERR_SHAPE = 2,        /* m < n, a tile or row block with < n rows, no block   */
+    TSQR_ERR_UNSUPPORTED = 3,  /* n > TSQR_MAX_N, tile_rows above the kernel capacity,
+                                  nranks not a power of two                             */
+    TSQR_ERR_ALLOC = 4,        /* device or host allocation failed                      */
+    TSQR_ERR_CUDA = 5          /* a CUDA runtime error (message: tsqr_last_error())     */
+} tsqr_status_t;
+
+#define TSQR_MAX_N 64          /* widest n the current kernels support */
+
+/* Plan options.
+ *  block_rows: b, the paper's row-block height (A_i of Eq. 1); the
+ *              row blocks of a rank are reduced by a binary tree (Eqs. 1-4).
+ *  tile_rows:  s, the SM-resident tile height: each row block is split into
+ *              ceil(h/s) near-equal tiles, the leaves of the tree, reduced by a
+ *              binary sub-tree inside the block ("any tree").
+ *              0 = library default for n (tsqr_plan_info reports it).
+ *  nranks, rank: the row-sharded multi-GPU layout (Alg. TSQR:par);
+ *              nranks = 1 for a single GPU.  A rank's slab must be the one
+ *              tsqr_slab() assigns.
+ *  flags:      bit 0 = synchronise and check after every launch (debug). */
+typedef struct {
+    int64_t block_rows;
+    int64_t tile_rows;
+    int32_t nranks;
+    int32_t rank;
+    int32_t flags;
+    int32_t reserved;
+} tsqr_opts_t;
+
+typedef struct tsqr_tree_s *tsqr_tree_t;   /* opaque implicit Q (D5 of SURVEY §2.2) */
+
+typedef struct {
+    int64_t m_local, n, block_rows, tile_rows;
+    int64_t ntiles;        /* leaves of the local tree                           */
+    int64_t nnodes;        /* local combine nodes (= ntiles - 1)                 */
+    int64_t nblocks;       /* row blocks of this rank                            */
+    int64_t depth;         /* levels of the local tree (tile + block stages)     */
+    int64_t cross_rounds;  /* log2(nranks): butterfly rounds (Table 1) */
+    int64_t max_tile_rows, min_tile_rows;
+    int64_t tile_capacity; /* rows one CTA keeps on chip for this n              */
+} tsqr_plan_info_t;
+
+/* ---------------------------------------------------------------- host-only
+ * These never touch a GPU and may be called on a machine without one. */
+
+const char *tsqr_status_string(tsqr_status_t s);
+/* Text of the last CUDA error seen by this thread (or "" ). */
+const char *tsqr_last_error(void);
+
+/* Rank slab of the global m x n problem: contiguous
+ * runs of whole row blocks, the first (nblocks mod nranks) ranks one block more.
+ * Outputs the slab's first global row and its row count. */
+tsqr_status_t tsqr_slab(int64_t m, int64_t n, int64_t block_rows, int32_t nranks,
+                        int32_t rank, int64_t *row0, int64_t *m_local);
+
+/* Plan summary for a rank's slab (m_local rows). */
+tsqr_status_t tsqr_plan_info(int64_t m_local, int64_t n, const tsqr_opts_t *opts,
+                             tsqr_plan_info_t *info);
+
+/* Plan arrays (host buffers sized from tsqr_plan_info): per tile its first
+ * local row and row count; per node in execution order the leftmost tiles
+ * (a, b) of its two subtrees, its stage (0 = tiles in a block, 1 = blocks) and
+ * level within the stage.  Used by the tests to compare with the oracle's plan. */
+tsqr_status_t tsqr_plan_export(int64_t m_local, int64_t n, const tsqr_opts_t *opts,
+                               int64_t *tile_row0, int64_t *tile_rows,
+                               int64_t *node_a, int64_t *node_b,
+                               int64_t *node_stage, int64_t *node_level);
+
+/* Butterfly indexing of Alg. TSQR:par: in round
+ * k = 1..log2(nranks), rank r pairs with r XOR 2^(k-1); the lower rank's R is
+ * stacked on top ("by order of processor ids").
+ * *is_lower = 1 if rank < partner.  *head_role: 1 if this rank is the leftmost
+ * rank of the lower group (its C head keeps the R coordinates), 2 if it is the
+ * leftmost of the upper group (its C head receives this node's complement),
+ * 0 otherwise.  Words per message: n(n+1)/2 (factor, Cor. 2 P:5084-5091),
+ * n*k (apply). */
+tsqr_status_t tsqr_cross_partner(int32_t nranks, int32_t rank, int32_t round,
+                                 int32_t *partner, int32_t *is_lower, int32_t *head_role);
+
+/* ---------------------------------------------------------------- device */
+
+/* Factor the rank's slab (Eqs. 1-4; Alg. TSQR:par line 1 P:1679).
+ *  A (device, m_local x n, lda >= m_local): IN the slab, OUT the tile
+ *    reflectors in place (strictly lower part of each tile) and
+ *    the node factors Y1 of eq. fact_2rs (upper triangle of the head n x n
+ *    block of each node's right subtree's first tile).  A is BORROWED by the
+ *    tree until tsqr_tree_free: do not modify or free it before then.
+ *  R (device, n x n, ldr >= n): OUT the R of the slab (nranks = 1: of A),
+ *    upper triangular, exact zeros below the diagonal.  May be NULL.
+ *  *tree: OUT a new handle; if *tree is non-NULL on entry and was built for the
+ *    same (m_local, n, opts), its device workspace is reused (no allocation).
+ * With nranks > 1 follow with tsqr_cross_factor for every round. */
+tsqr_status_t tsqr_factor(int64_t m_local, int64_t n, double *A, int64_t lda,
+                          double *R, int64_t ldr, const tsqr_opts_t *opts,
+                          void *stream, tsqr_tree_t *tree);
+
+/* Pack the tree's current R (upper triangle, column by column) into
+ * packed[n(n+1)/2] (device): the message of one butterfly round (Cor. 2). */
+tsqr_status_t tsqr_pack_r(tsqr_tree_t tree, double *packed, void *stream);
+
+/* Butterfly round `round` (1..log2 nranks) of Alg. TSQR:par:
+ * stack [R_lower; R_upper] from the tree's R and partner_packed (device,
+ * n(n+1)/2, the partner's tsqr_pack_r output of the same round), factor it with
+ * the structured combine (Alg. QR:qnxn), keep the node factor in the tree and
+ * make the new R current.  R (device, may be NULL) receives it, zeros below. */
+tsqr_status_t tsqr_cross_factor(tsqr_tree_t tree, int32_t round, const double *partner_packed,
+                                double *R, int64_t ldr, void *stream);
+
+/* C <- Q^T C over the local tree ([TR] P:1915-1938; eq. localQTupdate
+ * P:2193-2212).  C (device, m_local x k, ldc >= m_local) is overwritten in
+ * "tree order": rows 0..n-1 of the slab hold the R coordinates (for nranks = 1,
+ * Q_thin^T C); every other tile head holds its node's complement coordinates.
+ * top (device, n x k, ldtop >= n, may be NULL) receives a copy of rows 0..n-1.
+ * k = 0 is a no-op. */
+tsqr_status_t tsqr_apply_qt(tsqr_tree_t tree, double *C, int64_t ldc, int64_t k,
+                            double *top, int64_t ldtop, void *stream);
+
+/* Butterfly round of apply Q^T: top (device, n x k, ldtop) holds this rank's
+ * R coordinates, partner_top (device, n x k, ld = n) the partner's.  Both ranks
+ * apply the round's node reflectors to [top_lower; top_upper]; top becomes the
+ * new R coordinates; if head_role = 1 they are also written to C's rows
+ * 0..n-1, if head_role = 2 the complement coordinates are. */
+tsqr_status_t tsqr_cross_apply_qt(tsqr_tree_t tree, int32_t round, double *top, int64_t ldtop,
+                                  const double *partner_top, double *C, int64_t ldc,
+                                  int64_t k, void *stream);
+
+/* Explicit thin Q of the rank's slab: Q (device, m_local x n, ldq >= m_local) =
+ * rows of Q [I_n; 0].  Needs no communication: the
+ * cross-rank node factors are replicated on every rank. */
+tsqr_status_t tsqr_form_q(tsqr_tree_t tree, double *Q, int64_t ldq, void *stream);
+
+/* Release the tree's device memory (stream-ordered on the last stream used). */
+tsqr_status_t tsqr_tree_free(tsqr_tree_t tree);
+
+/* Test hook: copy the tree's tile taus (ntiles*n) and node taus (by node b
+ * index, ntiles*n; row 0 unused) to host buffers (either may be NULL).
+ * Synchronises the tree's stream. */
+tsqr_status_t tsqr_tree_export_tau(tsqr_tree_t tree, double *tau_tile_host, double *tau_node_host);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,10 @@
+"""paper_0808_2664_b200 -- B200-native (sm_100a) Tall-Skinny QR after arXiv 0808.2664.
+
+The hot path lives in libtsqr.so (csrc/, C-ABI include/tsqr.h); this package is
+the thin Python binding (api.py) plus the multi-GPU butterfly driver (dist.py)
+and the seeded input recipe (inputs.py)."""
+from .api import (Tree, apply_qt, cross_apply_qt, cross_factor, cross_partner, factor, form_q, pack_r,
+                  plan_export, plan_info, slab, tsqr)
+
+__all__ = ["Tree", "factor", "apply_qt", "form_q", "pack_r", "cross_factor", "cross_apply_qt", "plan_info",
+           "plan_export", "slab", "cross_partner", "tsqr"]

@@ -1,0 +1,182 @@
+"""User-facing API of the B200 TSQR path (torch tensors in, torch tensors out).
+
+Matrices are column-major: an m x n matrix is a float64 CUDA tensor of shape
+(n, m) whose rows are the matrix columns (stride(1) == 1, lda = stride(0)).
+Every call marshals pointers into libtsqr.so (include/tsqr.h); all arithmetic
+runs in its sm_100a kernels.  Calls are asynchronous on the current stream.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import Opts, PlanInfo, check, lib
+
+
+def _stream_ptr(stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _colmajor(t: torch.Tensor, name: str):
+    if t.dtype != torch.float64:
+        raise TypeError(f"{name} must be float64")
+    if not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor (the product path has no CPU fallback)")
+    if t.dim() != 2 or (t.shape[1] > 1 and t.stride(1) != 1):
+        raise ValueError(f"{name} must be column-major: shape (ncols, nrows) with stride(1) == 1")
+    ncols, nrows = t.shape
+    ld = t.stride(0) if ncols > 1 else max(nrows, 1)
+    return t.data_ptr(), nrows, ncols, ld
+
+
+def opts(block_rows: int = 0, tile_rows: int = 0, nranks: int = 1, rank: int = 0, debug: bool = False) -> Opts:
+    return Opts(block_rows, tile_rows, nranks, rank, 1 if debug else 0, 0)
+
+
+class Tree:
+    """Implicit Q of one rank (the tree of Householder reflectors, Eq. 4).
+    Borrows A (which holds the tile reflectors) until freed."""
+
+    def __init__(self):
+        self.handle = ctypes.c_void_p(None)
+        self.A = None
+        self.m_local = 0
+        self.n = 0
+        self.opts = None
+
+    def free(self):
+        if self.handle:
+            lib().tsqr_tree_free(self.handle)
+            self.handle = ctypes.c_void_p(None)
+        self.A = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+    def export_tau(self):
+        info = plan_info(self.m_local, self.n, self.opts)
+        L, n = info["ntiles"], self.n
+        tt = np.zeros((L, n))
+        tn = np.zeros((L, n))
+        check(lib().tsqr_tree_export_tau(self.handle, tt.ctypes.data_as(ctypes.c_void_p),
+                                          tn.ctypes.data_as(ctypes.c_void_p)), "tsqr_tree_export_tau")
+        return tt, tn
+
+
+def factor(A: torch.Tensor, block_rows: int = 0, tile_rows: int = 0, R: torch.Tensor | None = None,
+           nranks: int = 1, rank: int = 0, tree: Tree | None = None, stream=None, debug: bool = False):
+    """Factor A (column-major m_local x n) in place.  Returns (R, tree): R is n x n upper
+    triangular as a column-major (n, n) tensor.  Pass `tree` back in to reuse its workspace."""
+    pa, m, n, lda = _colmajor(A, "A")
+    if R is None:
+        R = torch.empty((n, n), dtype=torch.float64, device=A.device)
+    pr, _, _, ldr = _colmajor(R, "R")
+    o = opts(block_rows, tile_rows, nranks, rank, debug)
+    t = tree if tree is not None else Tree()
+    h = t.handle
+    check(lib().tsqr_factor(m, n, pa, lda, pr, ldr, ctypes.byref(o), _stream_ptr(stream), ctypes.byref(h)),
+          "tsqr_factor")
+    t.handle = h
+    t.A, t.m_local, t.n, t.opts = A, m, n, o
+    return R, t
+
+
+def apply_qt(tree: Tree, C: torch.Tensor, top: torch.Tensor | None = None, stream=None):
+    """C <- Q^T C in tree order (in place).  Returns (C, top)."""
+    pc, m, k, ldc = _colmajor(C, "C")
+    if m != tree.m_local:
+        raise ValueError("C must have m_local rows")
+    ptop, ldtop = None, 0
+    if top is not None:
+        ptop, _, _, ldtop = _colmajor(top, "top")
+    check(lib().tsqr_apply_qt(tree.handle, pc, ldc, k, ptop, ldtop, _stream_ptr(stream)), "tsqr_apply_qt")
+    return C, top
+
+
+def form_q(tree: Tree, Q: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Explicit thin Q rows of this rank (column-major m_local x n)."""
+    if Q is None:
+        Q = torch.empty((tree.n, tree.m_local), dtype=torch.float64, device=tree.A.device)
+    pq, m, n, ldq = _colmajor(Q, "Q")
+    check(lib().tsqr_form_q(tree.handle, pq, ldq, _stream_ptr(stream)), "tsqr_form_q")
+    return Q
+
+
+def pack_r(tree: Tree, packed: torch.Tensor, stream=None) -> torch.Tensor:
+    check(lib().tsqr_pack_r(tree.handle, packed.data_ptr(), _stream_ptr(stream)), "tsqr_pack_r")
+    return packed
+
+
+def cross_factor(tree: Tree, rnd: int, partner_packed: torch.Tensor, R: torch.Tensor | None = None, stream=None):
+    pr, ldr = None, 0
+    if R is not None:
+        pr, _, _, ldr = _colmajor(R, "R")
+    check(lib().tsqr_cross_factor(tree.handle, rnd, partner_packed.data_ptr(), pr, ldr, _stream_ptr(stream)),
+          "tsqr_cross_factor")
+    return R
+
+
+def cross_apply_qt(tree: Tree, rnd: int, top: torch.Tensor, partner_top: torch.Tensor, C: torch.Tensor,
+                   stream=None):
+    ptop, _, k, ldtop = _colmajor(top, "top")
+    pc, _, _, ldc = _colmajor(C, "C")
+    check(lib().tsqr_cross_apply_qt(tree.handle, rnd, ptop, ldtop, partner_top.data_ptr(), pc, ldc, k,
+                                    _stream_ptr(stream)), "tsqr_cross_apply_qt")
+    return top
+
+
+# ----------------------------------------------------------------- host-only
+def plan_info(m_local: int, n: int, o: Opts | None = None, **kw) -> dict:
+    o = o if o is not None else opts(**kw)
+    info = PlanInfo()
+    check(lib().tsqr_plan_info(m_local, n, ctypes.byref(o), ctypes.byref(info)), "tsqr_plan_info")
+    return {f: getattr(info, f) for f, _ in PlanInfo._fields_}
+
+
+def plan_export(m_local: int, n: int, **kw) -> dict:
+    o = opts(**kw)
+    info = plan_info(m_local, n, o)
+    L, N = info["ntiles"], info["nnodes"]
+    arrs = {k: np.zeros(L if k.startswith("tile") else max(N, 1), np.int64)
+            for k in ("tile_row0", "tile_rows", "node_a", "node_b", "node_stage", "node_level")}
+    ptr = lambda a: a.ctypes.data_as(_lib._pi64)  # noqa: E731
+    check(lib().tsqr_plan_export(m_local, n, ctypes.byref(o), *[ptr(arrs[k]) for k in
+                                 ("tile_row0", "tile_rows", "node_a", "node_b", "node_stage", "node_level")]),
+          "tsqr_plan_export")
+    for k in ("node_a", "node_b", "node_stage", "node_level"):
+        arrs[k] = arrs[k][:N]
+    return arrs
+
+
+def slab(m: int, n: int, block_rows: int, nranks: int, rank: int):
+    r0, ml = ctypes.c_int64(), ctypes.c_int64()
+    check(lib().tsqr_slab(m, n, block_rows, nranks, rank, ctypes.byref(r0), ctypes.byref(ml)), "tsqr_slab")
+    return r0.value, ml.value
+
+
+def cross_partner(nranks: int, rank: int, rnd: int):
+    p, lo, role = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    check(lib().tsqr_cross_partner(nranks, rank, rnd, ctypes.byref(p), ctypes.byref(lo), ctypes.byref(role)),
+          "tsqr_cross_partner")
+    return p.value, bool(lo.value), role.value
+
+
+# ----------------------------------------------------------------- end to end
+def tsqr(A_host: torch.Tensor, block_rows: int = 0, tile_rows: int = 0, want_q: bool = True,
+         device="cuda", stream=None):
+    """End-to-end convenience call with HOST tensors: copies A (column-major (n, m), ideally
+    pinned) to the device, factors it, forms Q, and copies R (and Q) back to host memory."""
+    A = A_host.to(device, non_blocking=True)
+    R, tree = factor(A, block_rows, tile_rows, stream=stream)
+    Q = form_q(tree, stream=stream) if want_q else None
+    R_h = R.to("cpu", non_blocking=False)
+    Q_h = Q.to("cpu", non_blocking=False) if want_q else None
+    tree.free()
+    return R_h, Q_h

@@ -1,0 +1,394 @@
+// C-ABI of libtsqr.so (include/tsqr.h): validation, tree handles, launch order.
+// Product code.  Every device call validates all arguments on the host first;
+// an error status means nothing was enqueued.
+#include "../../include/tsqr.h"
+#include "plan.h"
+#include "tsqr_kernels.h"
+
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+using namespace tsqr;
+
+static thread_local std::string g_last_error;
+
+struct tsqr_tree_s {
+    Plan plan;
+    tsqr_opts_t opts{};
+    int NP = 64;
+    int device = 0;
+    double *A = nullptr;
+    int64_t lda = 0;
+    cudaStream_t stream = nullptr;
+    // device arrays
+    int64_t *d_row0 = nullptr;
+    int *d_rows = nullptr, *d_tparent = nullptr, *d_node_a = nullptr, *d_nparent = nullptr;
+    double *d_tau_tile = nullptr, *d_tau_node = nullptr;
+    int *d_counters = nullptr;
+    double *d_cross_y1 = nullptr, *d_cross_tau = nullptr;
+    int cross_rounds = 0, cross_done = 0;
+    double *d_xbuf = nullptr;
+    int *d_step_ids = nullptr;
+    std::vector<int> step_off;   // top-down: groups [step_off[g], step_off[g+1])
+    DevPlan dplan{};
+};
+
+static tsqr_status_t cuda_fail(cudaError_t e, const char *where) {
+    g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+    return TSQR_ERR_CUDA;
+}
+
+#define CUDA_TRY(expr, where)                               \
+    do {                                                    \
+        cudaError_t _e = (expr);                            \
+        if (_e != cudaSuccess) return cuda_fail(_e, where); \
+    } while (0)
+
+static tsqr_status_t debug_sync(const tsqr_tree_s *t, cudaStream_t st, const char *where) {
+    if (t->opts.flags & 1) CUDA_TRY(cudaStreamSynchronize(st), where);
+    return TSQR_OK;
+}
+
+static void free_tree_memory(tsqr_tree_s *t) {
+    void *ptrs[] = {t->d_row0, t->d_rows, t->d_tparent, t->d_node_a, t->d_nparent, t->d_tau_tile,
+                    t->d_tau_node, t->d_counters, t->d_cross_y1, t->d_cross_tau, t->d_xbuf,
+                    t->d_step_ids};
+    for (void *p : ptrs)
+        if (p) cudaFree(p);
+}
+
+static int ilog2(int x) {
+    int r = 0;
+    while ((1 << r) < x) ++r;
+    return r;
+}
+
+extern "C" {
+
+const char *tsqr_status_string(tsqr_status_t s) {
+    switch (s) {
+        case TSQR_OK: return "ok";
+        case TSQR_ERR_INVALID: return "invalid argument";
+        case TSQR_ERR_SHAPE: return "invalid shape (m < n, or a tile / row block with fewer than n rows)";
+        case TSQR_ERR_UNSUPPORTED: return "unsupported (n > TSQR_MAX_N, tile_rows above capacity, or nranks not a power of two)";
+        case TSQR_ERR_ALLOC: return "allocation failed";
+        case TSQR_ERR_CUDA: return "CUDA error";
+    }
+    return "unknown status";
+}
+
+const char *tsqr_last_error(void) { return g_last_error.c_str(); }
+
+tsqr_status_t tsqr_slab(int64_t m, int64_t n, int64_t block_rows, int32_t nranks, int32_t rank,
+                        int64_t *row0, int64_t *m_local) {
+    if (!row0 || !m_local) return TSQR_ERR_INVALID;
+    return (tsqr_status_t)rank_slab(m, n, block_rows, nranks, rank, row0, m_local);
+}
+
+static tsqr_opts_t resolve_opts(int64_t m_local, const tsqr_opts_t *o) {
+    tsqr_opts_t r{};
+    if (o) r = *o;
+    if (r.block_rows == 0) r.block_rows = m_local;
+    if (r.nranks == 0) r.nranks = 1;
+    return r;
+}
+
+static int plan_for(int64_t m_local, int64_t n, const tsqr_opts_t *opts, Plan *p, tsqr_opts_t *ro) {
+    *ro = resolve_opts(m_local, opts);
+    if (ro->block_rows < 0) return TSQR_ERR_INVALID;
+    return build_plan(m_local, n, ro->block_rows, ro->tile_rows, ro->nranks, ro->rank, p);
+}
+
+tsqr_status_t tsqr_plan_info(int64_t m_local, int64_t n, const tsqr_opts_t *opts, tsqr_plan_info_t *info) {
+    if (!info) return TSQR_ERR_INVALID;
+    Plan p;
+    tsqr_opts_t ro;
+    int rc;
+    try { rc = plan_for(m_local, n, opts, &p, &ro); } catch (const std::bad_alloc &) { return TSQR_ERR_ALLOC; }
+    if (rc) return (tsqr_status_t)rc;
+    info->m_local = m_local;
+    info->n = n;
+    info->block_rows = p.b;
+    info->tile_rows = p.s;
+    info->ntiles = p.ntiles();
+    info->nnodes = (int64_t)p.nodes.size();
+    info->nblocks = (int64_t)p.blk_tile0.size() - 1;
+    info->depth = p.nsteps;
+    info->cross_rounds = ilog2(ro.nranks);
+    info->max_tile_rows = p.max_rows;
+    info->min_tile_rows = p.min_rows;
+    info->tile_capacity = tile_capacity(n);
+    return TSQR_OK;
+}
+
+tsqr_status_t tsqr_plan_export(int64_t m_local, int64_t n, const tsqr_opts_t *opts, int64_t *tile_row0,
+                               int64_t *tile_rows, int64_t *node_a, int64_t *node_b, int64_t *node_stage,
+                               int64_t *node_level) {
+    Plan p;
+    tsqr_opts_t ro;
+    int rc;
+    try { rc = plan_for(m_local, n, opts, &p, &ro); } catch (const std::bad_alloc &) { return TSQR_ERR_ALLOC; }
+    if (rc) return (tsqr_status_t)rc;
+    for (int t = 0; t < p.ntiles(); ++t) {
+        if (tile_row0) tile_row0[t] = p.tile_row0[t];
+        if (tile_rows) tile_rows[t] = p.tile_rows[t];
+    }
+    for (size_t i = 0; i < p.nodes.size(); ++i) {
+        if (node_a) node_a[i] = p.nodes[i].a;
+        if (node_b) node_b[i] = p.nodes[i].b;
+        if (node_stage) node_stage[i] = p.nodes[i].stage;
+        if (node_level) node_level[i] = p.nodes[i].level;
+    }
+    return TSQR_OK;
+}
+
+tsqr_status_t tsqr_cross_partner(int32_t nranks, int32_t rank, int32_t round, int32_t *partner,
+                                 int32_t *is_lower, int32_t *head_role) {
+    if (nranks < 1 || (nranks & (nranks - 1)) || rank < 0 || rank >= nranks) return TSQR_ERR_INVALID;
+    if (round < 1 || round > ilog2(nranks)) return TSQR_ERR_INVALID;
+    const int half = 1 << (round - 1);
+    const int p = rank ^ half;
+    if (partner) *partner = p;
+    if (is_lower) *is_lower = rank < p;
+    if (head_role) {
+        const int pos = rank & (2 * half - 1);          // position inside the 2^round group
+        *head_role = pos == 0 ? 1 : (pos == half ? 2 : 0);
+    }
+    return TSQR_OK;
+}
+
+static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t lda, const tsqr_opts_t *opts,
+                                 tsqr_tree_s **out) {
+    tsqr_tree_s *t = new (std::nothrow) tsqr_tree_s();
+    if (!t) return TSQR_ERR_ALLOC;
+    tsqr_opts_t ro;
+    int rc;
+    try { rc = plan_for(m_local, n, opts, &t->plan, &ro); } catch (const std::bad_alloc &) { rc = TSQR_ERR_ALLOC; }
+    if (rc) { delete t; return (tsqr_status_t)rc; }
+    t->opts = ro;
+    t->NP = padded_width(n);
+    cudaGetDevice(&t->device);
+    const Plan &p = t->plan;
+    const int L = p.ntiles();
+    // top-down form-Q schedule: node ids grouped by step, highest step first
+    std::vector<int> ids;
+    t->step_off.push_back(0);
+    for (int s = p.nsteps; s >= 1; --s) {
+        for (const auto &nd : p.nodes)
+            if (nd.step == s) ids.push_back(nd.b);
+        t->step_off.push_back((int)ids.size());
+    }
+    t->cross_rounds = ilog2(ro.nranks);
+    cudaError_t e = cudaSuccess;
+    auto alloc = [&](void **ptr, size_t bytes) {
+        if (e == cudaSuccess) e = cudaMalloc(ptr, bytes < 16 ? 16 : bytes);
+    };
+    alloc((void **)&t->d_row0, sizeof(int64_t) * L);
+    alloc((void **)&t->d_rows, sizeof(int) * L);
+    alloc((void **)&t->d_tparent, sizeof(int) * L);
+    alloc((void **)&t->d_node_a, sizeof(int) * L);
+    alloc((void **)&t->d_nparent, sizeof(int) * L);
+    alloc((void **)&t->d_tau_tile, sizeof(double) * L * n);
+    alloc((void **)&t->d_tau_node, sizeof(double) * L * n);
+    alloc((void **)&t->d_counters, sizeof(int) * L);
+    alloc((void **)&t->d_cross_y1, sizeof(double) * (t->cross_rounds + 1) * n * n);
+    alloc((void **)&t->d_cross_tau, sizeof(double) * (t->cross_rounds + 1) * n);
+    alloc((void **)&t->d_step_ids, sizeof(int) * (ids.size() + 1));
+    if (e != cudaSuccess) {
+        free_tree_memory(t);
+        delete t;
+        g_last_error = std::string("tsqr_factor alloc: ") + cudaGetErrorString(e);
+        cudaGetLastError();
+        return TSQR_ERR_ALLOC;
+    }
+    std::vector<int> rows(p.tile_rows.begin(), p.tile_rows.end());
+    e = cudaMemcpy(t->d_row0, p.tile_row0.data(), sizeof(int64_t) * L, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(t->d_rows, rows.data(), sizeof(int) * L, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(t->d_tparent, p.tile_parent.data(), sizeof(int) * L, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(t->d_node_a, p.node_a.data(), sizeof(int) * L, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(t->d_nparent, p.node_parent.data(), sizeof(int) * L, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !ids.empty())
+        e = cudaMemcpy(t->d_step_ids, ids.data(), sizeof(int) * ids.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemset(t->d_counters, 0, sizeof(int) * L);
+    if (e == cudaSuccess) e = cudaMemset(t->d_tau_node, 0, sizeof(double) * L * n);
+    if (e != cudaSuccess) {
+        free_tree_memory(t);
+        delete t;
+        return cuda_fail(e, "tsqr_factor setup");
+    }
+    t->dplan = DevPlan{t->d_row0, t->d_rows, t->d_tparent, t->d_node_a, t->d_nparent, L};
+    *out = t;
+    return TSQR_OK;
+}
+
+tsqr_status_t tsqr_factor(int64_t m_local, int64_t n, double *A, int64_t lda, double *R, int64_t ldr,
+                          const tsqr_opts_t *opts, void *stream, tsqr_tree_t *tree) {
+    if (!tree || !A) return TSQR_ERR_INVALID;
+    if (n < 1 || m_local < n) return TSQR_ERR_SHAPE;
+    if (lda < m_local) return TSQR_ERR_INVALID;
+    if (R && ldr < n) return TSQR_ERR_INVALID;
+    if (n > TSQR_MAX_N) return TSQR_ERR_UNSUPPORTED;
+    {   // validate the plan before touching the handle
+        Plan p;
+        tsqr_opts_t ro;
+        int rc;
+        try { rc = plan_for(m_local, n, opts, &p, &ro); } catch (const std::bad_alloc &) { return TSQR_ERR_ALLOC; }
+        if (rc) return (tsqr_status_t)rc;
+    }
+    tsqr_tree_s *t = *tree;
+    const tsqr_opts_t ro = resolve_opts(m_local, opts);
+    const bool reuse = t && t->plan.m_local == m_local && t->plan.n == n && t->opts.block_rows == ro.block_rows &&
+                       (ro.tile_rows == 0 || t->plan.s == ro.tile_rows) && t->opts.nranks == ro.nranks &&
+                       t->opts.rank == ro.rank;
+    if (!reuse) {
+        tsqr_tree_s *nt = nullptr;
+        tsqr_status_t s = create_tree(m_local, n, A, lda, opts, &nt);
+        if (s != TSQR_OK) return s;
+        if (t) { tsqr_tree_free(t); }
+        t = nt;
+        *tree = t;
+    }
+    t->opts.flags = ro.flags;
+    t->A = A;
+    t->lda = lda;
+    t->stream = (cudaStream_t)stream;
+    t->cross_done = 0;
+    FactorArgs f;
+    f.NP = t->NP;
+    f.max_rows = t->plan.max_rows;
+    f.A = A; f.lda = lda; f.n = (int)n;
+    f.plan = t->dplan;
+    f.tau_tile = t->d_tau_tile; f.tau_node = t->d_tau_node; f.counters = t->d_counters;
+    f.R = R; f.ldr = ldr;
+    CUDA_TRY(launch_factor(f, t->stream), "tsqr_factor launch");
+    return debug_sync(t, t->stream, "tsqr_factor");
+}
+
+tsqr_status_t tsqr_pack_r(tsqr_tree_t t, double *packed, void *stream) {
+    if (!t || !t->A || !packed) return TSQR_ERR_INVALID;
+    CUDA_TRY(launch_pack_r(t->A, t->lda, (int)t->plan.n, packed, (cudaStream_t)stream), "tsqr_pack_r");
+    t->stream = (cudaStream_t)stream;
+    return debug_sync(t, t->stream, "tsqr_pack_r");
+}
+
+tsqr_status_t tsqr_cross_factor(tsqr_tree_t t, int32_t round, const double *partner_packed, double *R,
+                                int64_t ldr, void *stream) {
+    if (!t || !t->A || !partner_packed) return TSQR_ERR_INVALID;
+    if (round != t->cross_done + 1 || round > t->cross_rounds) return TSQR_ERR_INVALID;
+    if (R && ldr < t->plan.n) return TSQR_ERR_INVALID;
+    int32_t partner, lower, role;
+    if (tsqr_cross_partner(t->opts.nranks, t->opts.rank, round, &partner, &lower, &role) != TSQR_OK)
+        return TSQR_ERR_INVALID;
+    const int n = (int)t->plan.n;
+    CUDA_TRY(launch_cross_factor(t->NP, t->A, t->lda, n, partner_packed, lower,
+                                 t->d_cross_y1 + (int64_t)(round - 1) * n * n,
+                                 t->d_cross_tau + (int64_t)(round - 1) * n, R, ldr, (cudaStream_t)stream),
+             "tsqr_cross_factor");
+    t->cross_done = round;
+    t->stream = (cudaStream_t)stream;
+    return debug_sync(t, t->stream, "tsqr_cross_factor");
+}
+
+tsqr_status_t tsqr_apply_qt(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, double *top, int64_t ldtop,
+                            void *stream) {
+    if (!t || !t->A) return TSQR_ERR_INVALID;
+    if (k < 0 || k > INT32_MAX) return TSQR_ERR_INVALID;
+    if (k == 0) return TSQR_OK;
+    if (!C || ldc < t->plan.m_local) return TSQR_ERR_INVALID;
+    if (top && ldtop < t->plan.n) return TSQR_ERR_INVALID;
+    ApplyArgs f;
+    f.NP = t->NP;
+    f.max_rows = t->plan.max_rows;
+    f.A = t->A; f.lda = t->lda; f.n = (int)t->plan.n;
+    f.plan = t->dplan;
+    f.tau_tile = t->d_tau_tile; f.tau_node = t->d_tau_node; f.counters = t->d_counters;
+    f.C = C; f.ldc = ldc; f.k = (int)k;
+    f.form_q = 0; f.xbuf = nullptr;
+    cudaStream_t st = (cudaStream_t)stream;
+    CUDA_TRY(launch_apply(f, st), "tsqr_apply_qt launch");
+    if (top) CUDA_TRY(launch_copy_block(C, ldc, top, ldtop, (int)t->plan.n, (int)k, st), "tsqr_apply_qt top");
+    t->stream = st;
+    return debug_sync(t, st, "tsqr_apply_qt");
+}
+
+tsqr_status_t tsqr_cross_apply_qt(tsqr_tree_t t, int32_t round, double *top, int64_t ldtop,
+                                  const double *partner_top, double *C, int64_t ldc, int64_t k, void *stream) {
+    if (!t || !t->A || !top || !partner_top) return TSQR_ERR_INVALID;
+    if (round < 1 || round > t->cross_done) return TSQR_ERR_INVALID;
+    if (k < 0 || k > INT32_MAX || ldtop < t->plan.n) return TSQR_ERR_INVALID;
+    int32_t partner, lower, role;
+    if (tsqr_cross_partner(t->opts.nranks, t->opts.rank, round, &partner, &lower, &role) != TSQR_OK)
+        return TSQR_ERR_INVALID;
+    if (role != 0 && (!C || ldc < t->plan.m_local)) return TSQR_ERR_INVALID;
+    if (k == 0) return TSQR_OK;
+    const int n = (int)t->plan.n;
+    CUDA_TRY(launch_cross_apply(t->NP, t->d_cross_y1 + (int64_t)(round - 1) * n * n,
+                                t->d_cross_tau + (int64_t)(round - 1) * n, top, ldtop, partner_top, lower, role,
+                                C, ldc, n, (int)k, (cudaStream_t)stream),
+             "tsqr_cross_apply_qt");
+    t->stream = (cudaStream_t)stream;
+    return debug_sync(t, t->stream, "tsqr_cross_apply_qt");
+}
+
+tsqr_status_t tsqr_form_q(tsqr_tree_t t, double *Q, int64_t ldq, void *stream) {
+    if (!t || !t->A || !Q) return TSQR_ERR_INVALID;
+    if (ldq < t->plan.m_local) return TSQR_ERR_INVALID;
+    if (t->cross_done != t->cross_rounds) return TSQR_ERR_INVALID;
+    const int n = (int)t->plan.n;
+    const int L = t->plan.ntiles();
+    cudaStream_t st = (cudaStream_t)stream;
+    if (!t->d_xbuf) {
+        cudaError_t e = cudaMalloc((void **)&t->d_xbuf, sizeof(double) * (size_t)L * n * n);
+        if (e != cudaSuccess) {
+            t->d_xbuf = nullptr;
+            cudaGetLastError();
+            g_last_error = std::string("tsqr_form_q alloc: ") + cudaGetErrorString(e);
+            return TSQR_ERR_ALLOC;
+        }
+    }
+    // root X of this rank: I (one GPU) or the butterfly path (no communication)
+    if (t->cross_rounds == 0) CUDA_TRY(launch_identity(t->d_xbuf, n, st), "tsqr_form_q identity");
+    else
+        CUDA_TRY(launch_cross_root_x(t->NP, t->d_cross_y1, t->d_cross_tau, t->cross_rounds, t->opts.rank, n,
+                                     t->d_xbuf, st),
+                 "tsqr_form_q root");
+    for (size_t g = 0; g + 1 < t->step_off.size(); ++g) {
+        const int cnt = t->step_off[g + 1] - t->step_off[g];
+        if (cnt == 0) continue;
+        CUDA_TRY(launch_formq_nodes(t->NP, t->A, t->lda, n, t->dplan, t->d_tau_node,
+                                    t->d_step_ids + t->step_off[g], cnt, t->d_xbuf, st),
+                 "tsqr_form_q nodes");
+    }
+    ApplyArgs f;
+    f.NP = t->NP;
+    f.max_rows = t->plan.max_rows;
+    f.A = t->A; f.lda = t->lda; f.n = n;
+    f.plan = t->dplan;
+    f.tau_tile = t->d_tau_tile; f.tau_node = t->d_tau_node; f.counters = t->d_counters;
+    f.C = Q; f.ldc = ldq; f.k = n;
+    f.form_q = 1; f.xbuf = t->d_xbuf;
+    CUDA_TRY(launch_apply(f, st), "tsqr_form_q leaves");
+    t->stream = st;
+    return debug_sync(t, st, "tsqr_form_q");
+}
+
+tsqr_status_t tsqr_tree_free(tsqr_tree_t t) {
+    if (!t) return TSQR_OK;
+    if (t->stream) cudaStreamSynchronize(t->stream);
+    free_tree_memory(t);
+    delete t;
+    return TSQR_OK;
+}
+
+tsqr_status_t tsqr_tree_export_tau(tsqr_tree_t t, double *tau_tile_host, double *tau_node_host) {
+    if (!t) return TSQR_ERR_INVALID;
+    const size_t bytes = sizeof(double) * (size_t)t->plan.ntiles() * t->plan.n;
+    if (t->stream) CUDA_TRY(cudaStreamSynchronize(t->stream), "tsqr_tree_export_tau");
+    if (tau_tile_host) CUDA_TRY(cudaMemcpy(tau_tile_host, t->d_tau_tile, bytes, cudaMemcpyDeviceToHost), "export");
+    if (tau_node_host) CUDA_TRY(cudaMemcpy(tau_node_host, t->d_tau_node, bytes, cudaMemcpyDeviceToHost), "export");
+    return TSQR_OK;
+}
+
+}  // extern "C"

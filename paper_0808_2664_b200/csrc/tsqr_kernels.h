@@ -1,0 +1,66 @@
+// Host-side declarations of the kernel launchers (tsqr_kernels.cu).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tsqr {
+
+struct DevPlan;
+
+// Columns of C one apply CTA keeps in registers per chunk: the C staging buffer
+// (S x KC doubles) must fit next to the S x NP Y tile in shared memory.
+template <int NP, int RT>
+struct ApplyKC {
+    static constexpr int S = (NP < 32 ? 32 / NP : 1) * RT * 8;
+    static constexpr int byS = 8192 / S;
+    static constexpr int a = NP < 32 ? NP : 32;
+    static constexpr int value = a < byS ? a : byS;
+};
+
+struct FactorArgsBase {
+    int NP = 64;
+    int64_t max_rows = 0;
+};
+
+}  // namespace tsqr
+
+#include "tsqr_device.cuh"
+
+namespace tsqr {
+
+struct FactorArgs : FactorArgsBase {
+    double *A; int64_t lda; int n;
+    DevPlan plan;
+    double *tau_tile, *tau_node; int *counters;
+    double *R; int64_t ldr;
+};
+
+struct ApplyArgs : FactorArgsBase {
+    const double *A; int64_t lda; int n;
+    DevPlan plan;
+    const double *tau_tile, *tau_node; int *counters;
+    double *C; int64_t ldc; int k;
+    int form_q;            // 1: form-Q leaf stage (C := Q, columns = n) using xbuf
+    const double *xbuf;
+};
+
+cudaError_t launch_factor(const FactorArgs &f, cudaStream_t st);
+cudaError_t launch_apply(const ApplyArgs &f, cudaStream_t st);
+cudaError_t launch_formq_nodes(int NP, const double *A, int64_t lda, int n, const DevPlan &plan,
+                               const double *tau_node, const int *ids, int count, double *xbuf,
+                               cudaStream_t st);
+cudaError_t launch_identity(double *X, int n, cudaStream_t st);
+cudaError_t launch_write_r(int NP, const double *A, int64_t lda, int n, double *R, int64_t ldr,
+                           cudaStream_t st);
+cudaError_t launch_pack_r(const double *A, int64_t lda, int n, double *packed, cudaStream_t st);
+cudaError_t launch_copy_block(const double *src, int64_t lds, double *dst, int64_t ldd, int n, int k,
+                              cudaStream_t st);
+cudaError_t launch_cross_factor(int NP, double *A, int64_t lda, int n, const double *pp, int is_lower,
+                                double *Y1, double *tau, double *R, int64_t ldr, cudaStream_t st);
+cudaError_t launch_cross_apply(int NP, const double *Y1, const double *tau, double *top, int64_t ldtop,
+                               const double *ptop, int is_lower, int role, double *C, int64_t ldc, int n,
+                               int k, cudaStream_t st);
+cudaError_t launch_cross_root_x(int NP, const double *Y1s, const double *taus, int rounds, int rank, int n,
+                                double *X0, cudaStream_t st);
+
+}  // namespace tsqr

@@ -1,0 +1,164 @@
+"""Row-sharded multi-GPU TSQR: Alg. TSQR:par as a butterfly all-reduction
+(butterfly indices P:3955-3975).
+
+One process per GPU.  Each rank factors its contiguous slab of whole row blocks
+(tsqr_slab) with the single-GPU kernels, then runs log2(G) rounds: pack the
+current R (n(n+1)/2 words, the Cor. 2 minimum), exchange it with
+partner r XOR 2^(k-1) over NCCL (torch.distributed point-to-point, NVLink), and
+run the structured combine on [R_lower; R_upper] -- both partners compute the
+same node, so R ends replicated.  Apply Q^T exchanges the n x k
+R coordinates per round; form Q needs no communication (every rank holds the
+node factors on its root-to-leaf path).
+
+The round logic is written once (`RankState`) and driven either by
+torch.distributed (`factor`, `apply_qt`) or, for tests, by an in-process
+loopback over virtual ranks (`*_virtual`).  The arithmetic is the engine's:
+`CudaEngine` calls libtsqr.so; tests substitute an oracle-backed engine.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from . import api
+
+
+class CudaEngine:
+    """The product engine: every step is a libtsqr.so call on the current stream."""
+
+    def factor_local(self, A, block_rows, tile_rows, nranks, rank):
+        return api.factor(A, block_rows, tile_rows, nranks=nranks, rank=rank)
+
+    def empty(self, shape, like):
+        return torch.empty(shape, dtype=torch.float64, device=like.device)
+
+    def pack(self, tree, out):
+        return api.pack_r(tree, out)
+
+    def cross_factor(self, tree, rnd, recv, R):
+        api.cross_factor(tree, rnd, recv, R)
+
+    def apply_local(self, tree, C, top):
+        api.apply_qt(tree, C, top)
+
+    def cross_apply(self, tree, rnd, top, partner_top, C):
+        api.cross_apply_qt(tree, rnd, top, partner_top, C)
+
+    def form_q(self, tree):
+        return api.form_q(tree)
+
+
+def rounds_of(nranks: int) -> int:
+    r = 0
+    while (1 << r) < nranks:
+        r += 1
+    if (1 << r) != nranks:
+        raise ValueError("nranks must be a power of two")
+    return r
+
+
+@dataclass
+class RankState:
+    engine: object
+    rank: int
+    nranks: int
+    n: int = 0
+    tree: object = None
+    R: object = None
+    top: object = None
+    C: object = None
+    sent: list = field(default_factory=list)      # (round, words) per message, for the count pins
+
+    # ---------------------------------------------------------------- factor
+    def factor_local(self, A, block_rows, tile_rows):
+        self.n = A.shape[0]
+        self.R, self.tree = self.engine.factor_local(A, block_rows, tile_rows, self.nranks, self.rank)
+
+    def factor_send(self, rnd):
+        buf = self.engine.empty((self.n * (self.n + 1) // 2,), self.R)
+        self.engine.pack(self.tree, buf)
+        self.sent.append((rnd, buf.numel()))
+        return buf
+
+    def factor_finish(self, rnd, recv):
+        self.engine.cross_factor(self.tree, rnd, recv, self.R)
+
+    # ----------------------------------------------------------------- apply
+    def apply_local(self, C):
+        k = C.shape[0]
+        self.C = C
+        self.top = self.engine.empty((k, self.n), C)
+        self.engine.apply_local(self.tree, C, self.top)
+
+    def apply_send(self, rnd):
+        buf = self.top.clone()
+        self.sent.append((rnd, buf.numel()))
+        return buf
+
+    def apply_finish(self, rnd, recv):
+        self.engine.cross_apply(self.tree, rnd, self.top, recv, self.C)
+
+
+def _exchange(send: torch.Tensor, partner: int, group=None) -> torch.Tensor:
+    import torch.distributed as dist
+    recv = torch.empty_like(send)
+    ops = [dist.P2POp(dist.isend, send, partner, group), dist.P2POp(dist.irecv, recv, partner, group)]
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+    return recv
+
+
+# ------------------------------------------------------ torch.distributed drivers
+def factor(A_local, block_rows: int, tile_rows: int = 0, engine=None, group=None) -> RankState:
+    """Collective over the process group: returns the rank state (R replicated in .R)."""
+    import torch.distributed as dist
+    rank, nranks = dist.get_rank(group), dist.get_world_size(group)
+    st = RankState(engine or CudaEngine(), rank, nranks)
+    st.factor_local(A_local, block_rows, tile_rows)
+    for rnd in range(1, rounds_of(nranks) + 1):
+        partner = rank ^ (1 << (rnd - 1))
+        recv = _exchange(st.factor_send(rnd), partner, group)
+        st.factor_finish(rnd, recv)
+    return st
+
+
+def apply_qt(st: RankState, C_local, group=None):
+    """Collective: C_local <- rows of Q^T C (tree order); st.top = Q_thin^T C on every rank."""
+    st.apply_local(C_local)
+    for rnd in range(1, rounds_of(st.nranks) + 1):
+        partner = st.rank ^ (1 << (rnd - 1))
+        recv = _exchange(st.apply_send(rnd), partner, group)
+        st.apply_finish(rnd, recv)
+    return C_local, st.top
+
+
+def form_q(st: RankState):
+    """Local (communication-free) explicit Q rows of this rank."""
+    return st.engine.form_q(st.tree)
+
+
+# ------------------------------------------------------- loopback (virtual) drivers
+def factor_virtual(slabs, block_rows: int, tile_rows: int = 0, engine=None) -> list:
+    """All ranks in one process, exchanging by reference between rounds (no kernel of one
+    rank ever waits on another's: each round's sends are complete before any finish)."""
+    nranks = len(slabs)
+    eng = engine or CudaEngine()
+    states = [RankState(eng, r, nranks) for r in range(nranks)]
+    for st, A in zip(states, slabs):
+        st.factor_local(A, block_rows, tile_rows)
+    for rnd in range(1, rounds_of(nranks) + 1):
+        sends = [st.factor_send(rnd) for st in states]
+        for st in states:
+            st.factor_finish(rnd, sends[st.rank ^ (1 << (rnd - 1))])
+    return states
+
+
+def apply_qt_virtual(states, C_slabs):
+    for st, C in zip(states, C_slabs):
+        st.apply_local(C)
+    for rnd in range(1, rounds_of(len(states)) + 1):
+        sends = [st.apply_send(rnd) for st in states]
+        for st in states:
+            st.apply_finish(rnd, sends[st.rank ^ (1 << (rnd - 1))])
+    return C_slabs
