@@ -19,6 +19,10 @@ int64_t tile_capacity(int64_t n) {
     }
 }
 
+// Default tile: the largest tile two CTAs per SM can keep in registers
+// (32 fp64 per thread), so one CTA's reduction latency hides behind the other's FMAs.
+int64_t default_tile_rows(int64_t n) { return tile_capacity(n) / 2; }
+
 static int64_t block_count(int64_t m, int64_t n, int64_t b, int64_t *last_rows) {
     // Reading R6: blocks of b rows; a remainder >= n is its own block, a
     // shorter one is merged into the last block.
@@ -60,7 +64,7 @@ int build_plan(int64_t m_local, int64_t n, int64_t block_rows, int64_t tile_rows
     if (block_rows < 1 || tile_rows < 0) return TSQR_ERR_INVALID;
     if (nranks < 1 || (nranks & (nranks - 1)) || rank < 0 || rank >= nranks) return TSQR_ERR_UNSUPPORTED;
     const int64_t cap = tile_capacity(n);
-    const int64_t s = tile_rows == 0 ? std::min(cap, block_rows) : tile_rows;
+    const int64_t s = tile_rows == 0 ? std::min(default_tile_rows(n), block_rows) : tile_rows;
     if (s < n) return TSQR_ERR_SHAPE;
     if (s > cap) return TSQR_ERR_UNSUPPORTED;
 

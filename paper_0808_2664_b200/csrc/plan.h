@@ -34,6 +34,7 @@ struct Plan {
 // Kernel tile capacity (rows) for a padded width, and the padded width of n.
 int padded_width(int64_t n);
 int64_t tile_capacity(int64_t n);
+int64_t default_tile_rows(int64_t n);
 
 // Returns 0 on success, else a tsqr_status_t code.
 int build_plan(int64_t m_local, int64_t n, int64_t block_rows, int64_t tile_rows,

@@ -45,25 +45,33 @@ struct Layout {
 };
 
 // ------------------------------------------------------------------ staging
-// global (rows x ncols, ld) -> smem (cap_rows x cap_cols, sld), zero padded.
-template <bool kCG>
-__device__ __forceinline__ void stage_in(double *sm, int sld, const double *g, int64_t ldg,
-                                         int rows, int ncols, int cap_rows, int cap_cols) {
-    for (int c = 0; c < cap_cols; ++c) {
-        const double *gc = g + (int64_t)c * ldg;
-        for (int r = threadIdx.x; r < cap_rows; r += kThreads) {
-            double v = 0.0;
-            if (c < ncols && r < rows) v = kCG ? __ldcg(gc + r) : gc[r];
-            sm[c * sld + r] = v;
-        }
-    }
-}
-
 __device__ __forceinline__ void stage_out(const double *sm, int sld, double *g, int64_t ldg,
                                           int rows, int ncols) {
     for (int c = 0; c < ncols; ++c) {
         double *gc = g + (int64_t)c * ldg;
         for (int r = threadIdx.x; r < rows; r += kThreads) gc[r] = sm[c * sld + r];
+    }
+}
+
+// Asynchronous global -> smem staging (cp.async, 8-byte elements, zero fill):
+// every element is in flight at once instead of one dependent load per column.
+__device__ __forceinline__ void cp_async8(double *sm, const double *g, bool valid) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(sm));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(g), "r"(valid ? 8 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
+// global (rows x ncols, ld) -> smem (cap_rows x cap_cols, sld), zero padded; the
+// caller waits with cp_async_wait_all() + __syncthreads().
+__device__ __forceinline__ void stage_in_async(double *sm, int sld, const double *g, int64_t ldg, int rows,
+                                               int ncols, int cap_rows, int cap_cols) {
+    for (int c = 0; c < cap_cols; ++c) {
+        const double *gc = g + (int64_t)(c < ncols ? c : 0) * ldg;
+        for (int r = threadIdx.x; r < cap_rows; r += kThreads) {
+            const bool ok = (c < ncols) && (r < rows);
+            cp_async8(sm + c * sld + r, ok ? gc + r : g, ok);
+        }
     }
 }
 
@@ -108,8 +116,21 @@ __device__ __forceinline__ double warp_sum_lpc(double v, int lc) {
 }
 
 // Householder scalars in the LAPACK dlarfg convention (reading R1/R2):
-// beta = -sign(alpha) sqrt(alpha^2 + sigma2), tau = (beta - alpha)/beta,
-// v = x / (alpha - beta) below the pivot.  sigma2 == 0 -> H = I.
+// beta = -sign(alpha) N, N = sqrt(alpha^2 + sigma2), tau = (beta - alpha)/beta
+// = 1 + |alpha|/N, v = x / (alpha - beta) below the pivot, i.e.
+// scale = sign(alpha) / (|alpha| + N).  sigma2 == 0 -> H = I.
+// The critical path avoids IEEE sqrt/div sequences: N = y * rsqrt(y) and the
+// reciprocal use the hardware approximations refined by Newton steps
+// (<= 2 ulp).
+__device__ __forceinline__ double rcp_nr(double d) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    double e = fma(-d, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-d, y, 1.0);
+    return fma(y, e, y);
+}
+
 struct House {
     double beta, tau, scale;
 };
@@ -120,43 +141,154 @@ __device__ __forceinline__ House householder(double alpha, double sigma2) {
         h.tau = 0.0;
         h.scale = 0.0;
     } else {
-        const double nrm = sqrt(fma(alpha, alpha, sigma2));
-        h.beta = alpha >= 0.0 ? -nrm : nrm;
-        const double d = alpha - h.beta;      // |alpha| + |beta|: no cancellation
-        h.tau = -d / h.beta;                  // (beta - alpha) / beta
-        h.scale = 1.0 / d;
+        const double y = fma(alpha, alpha, sigma2);
+        const double r = rsqrt(y);                     // MUFU + Newton, ~1 ulp
+        const double N = y * r;
+        const double aa = fabs(alpha);
+        h.beta = alpha >= 0.0 ? -N : N;
+        h.tau = fma(aa, r, 1.0);                      // 1 + |alpha| / N
+        const double inv = rcp_nr(aa + N);
+        h.scale = alpha >= 0.0 ? inv : -inv;
     }
     return h;
 }
 
+// Sum of the kWarps partials of column c in a fixed tree order (every thread
+// gets bit-identical results).
+__device__ __forceinline__ double sum_warps(const double *redb, int stride, int c) {
+    double v[kWarps];
+#pragma unroll
+    for (int q = 0; q < kWarps; ++q) v[q] = redb[q * stride + c];
+#pragma unroll
+    for (int h = kWarps / 2; h >= 1; h /= 2)
+#pragma unroll
+        for (int q = 0; q < h; ++q) v[q] = v[q] + v[q + h];
+    return v[0];
+}
+
 // ============================================================== tile QR (a2)
-// Unblocked Householder QR of the register tile a (rows x n, padded).  One
-// __syncthreads per column: partial inner products of the pivot column with
-// every column (its own one gives sigma^2 = ||x(j+1:)||^2) are reduced once;
-// w = v^T A_t follows from them by a scale (v = x/(alpha-beta)).
-// Smem: xs[S] (pivot column broadcast), red[2][kWarps][NP], rowj[2][NP], taus[NP].
+// Fetch register row i (runtime index) of this thread's tile: a jump table,
+// executed only by the one warp that holds the row (warp-uniform branch).
 template <class Lt>
+__device__ __forceinline__ double reg_row(const double (&a)[Lt::RT][Lt::CPL], int i, int cc) {
+    static_assert(Lt::RT <= 64, "reg_row covers 64 register rows");
+    switch (i) {
+        case 0: return a[0 < Lt::RT ? 0 : 0][cc];
+        case 1: return a[1 < Lt::RT ? 1 : 0][cc];
+        case 2: return a[2 < Lt::RT ? 2 : 0][cc];
+        case 3: return a[3 < Lt::RT ? 3 : 0][cc];
+        case 4: return a[4 < Lt::RT ? 4 : 0][cc];
+        case 5: return a[5 < Lt::RT ? 5 : 0][cc];
+        case 6: return a[6 < Lt::RT ? 6 : 0][cc];
+        case 7: return a[7 < Lt::RT ? 7 : 0][cc];
+        case 8: return a[8 < Lt::RT ? 8 : 0][cc];
+        case 9: return a[9 < Lt::RT ? 9 : 0][cc];
+        case 10: return a[10 < Lt::RT ? 10 : 0][cc];
+        case 11: return a[11 < Lt::RT ? 11 : 0][cc];
+        case 12: return a[12 < Lt::RT ? 12 : 0][cc];
+        case 13: return a[13 < Lt::RT ? 13 : 0][cc];
+        case 14: return a[14 < Lt::RT ? 14 : 0][cc];
+        case 15: return a[15 < Lt::RT ? 15 : 0][cc];
+        case 16: return a[16 < Lt::RT ? 16 : 0][cc];
+        case 17: return a[17 < Lt::RT ? 17 : 0][cc];
+        case 18: return a[18 < Lt::RT ? 18 : 0][cc];
+        case 19: return a[19 < Lt::RT ? 19 : 0][cc];
+        case 20: return a[20 < Lt::RT ? 20 : 0][cc];
+        case 21: return a[21 < Lt::RT ? 21 : 0][cc];
+        case 22: return a[22 < Lt::RT ? 22 : 0][cc];
+        case 23: return a[23 < Lt::RT ? 23 : 0][cc];
+        case 24: return a[24 < Lt::RT ? 24 : 0][cc];
+        case 25: return a[25 < Lt::RT ? 25 : 0][cc];
+        case 26: return a[26 < Lt::RT ? 26 : 0][cc];
+        case 27: return a[27 < Lt::RT ? 27 : 0][cc];
+        case 28: return a[28 < Lt::RT ? 28 : 0][cc];
+        case 29: return a[29 < Lt::RT ? 29 : 0][cc];
+        case 30: return a[30 < Lt::RT ? 30 : 0][cc];
+        case 31: return a[31 < Lt::RT ? 31 : 0][cc];
+        case 32: return a[32 < Lt::RT ? 32 : 0][cc];
+        case 33: return a[33 < Lt::RT ? 33 : 0][cc];
+        case 34: return a[34 < Lt::RT ? 34 : 0][cc];
+        case 35: return a[35 < Lt::RT ? 35 : 0][cc];
+        case 36: return a[36 < Lt::RT ? 36 : 0][cc];
+        case 37: return a[37 < Lt::RT ? 37 : 0][cc];
+        case 38: return a[38 < Lt::RT ? 38 : 0][cc];
+        case 39: return a[39 < Lt::RT ? 39 : 0][cc];
+        case 40: return a[40 < Lt::RT ? 40 : 0][cc];
+        case 41: return a[41 < Lt::RT ? 41 : 0][cc];
+        case 42: return a[42 < Lt::RT ? 42 : 0][cc];
+        case 43: return a[43 < Lt::RT ? 43 : 0][cc];
+        case 44: return a[44 < Lt::RT ? 44 : 0][cc];
+        case 45: return a[45 < Lt::RT ? 45 : 0][cc];
+        case 46: return a[46 < Lt::RT ? 46 : 0][cc];
+        case 47: return a[47 < Lt::RT ? 47 : 0][cc];
+        case 48: return a[48 < Lt::RT ? 48 : 0][cc];
+        case 49: return a[49 < Lt::RT ? 49 : 0][cc];
+        case 50: return a[50 < Lt::RT ? 50 : 0][cc];
+        case 51: return a[51 < Lt::RT ? 51 : 0][cc];
+        case 52: return a[52 < Lt::RT ? 52 : 0][cc];
+        case 53: return a[53 < Lt::RT ? 53 : 0][cc];
+        case 54: return a[54 < Lt::RT ? 54 : 0][cc];
+        case 55: return a[55 < Lt::RT ? 55 : 0][cc];
+        case 56: return a[56 < Lt::RT ? 56 : 0][cc];
+        case 57: return a[57 < Lt::RT ? 57 : 0][cc];
+        case 58: return a[58 < Lt::RT ? 58 : 0][cc];
+        case 59: return a[59 < Lt::RT ? 59 : 0][cc];
+        case 60: return a[60 < Lt::RT ? 60 : 0][cc];
+        case 61: return a[61 < Lt::RT ? 61 : 0][cc];
+        case 62: return a[62 < Lt::RT ? 62 : 0][cc];
+        case 63: return a[63 < Lt::RT ? 63 : 0][cc];
+        default: return 0.0;
+    }
+}
+
+// Unblocked Householder QR of the register tile a (rows x n, padded).  One
+// __syncthreads per column.  Per column j:
+//   1. the owner lane of column j publishes x = A(:, j) (rows > j; rows <= j
+//      zeroed) in smem xs;
+//   2. every thread forms partial dots x^T A(:, c) over its rows (c = j gives
+//      sigma^2 = ||x(j+1:)||^2); the thread holding row j publishes A(j, :);
+//   3. one barrier; every thread reduces the partials (same order: identical
+//      scalars), forms beta, tau and scale = 1/(alpha - beta) (dlarfg), and
+//      w_c = A(j,c) + scale x^T A(:,c) = v^T A(:,c);
+//   4. xs[j] := alpha - beta, so one rank-1 update A(:,c) -= xs * (tau*scale*w_c)
+//      also performs row j's update A(j,c) -= tau w_c, with no per-element masks.
+// Column j itself is left untouched in the loop; its final form (beta on the
+// diagonal, v = x * scale below) is applied once after the loop.
+// Smem: xs[S], red[2][kWarps][NP], rowj[2][NP], taus/betas/scales[NP].
+struct NoProbe {
+    __device__ static void mark(int, int) {}
+};
+
+template <class Lt, class Probe = NoProbe>
 __device__ void tile_qr(double (&a)[Lt::RT][Lt::CPL], int n, double *xs, double *red,
-                        double *rowj, double *taus) {
+                        double *rowj, double *taus, double *betas, double *scales) {
     constexpr int RT = Lt::RT, CPL = Lt::CPL, NP = Lt::NP;
     const int w = Lt::warp(), l = Lt::lane(), rph = Lt::rph();
     for (int j = 0; j < n; ++j) {
         const int buf = j & 1;
         double *redb = red + buf * (kWarps * NP);
         double *rjb = rowj + buf * NP;
-        const int cj = j >> 5;                       // register column of j (CPL = 2)
-        const bool owner = (Lt::colbase() == (j & 31)) && (cj < CPL);
-        // 1. broadcast the pivot column (rows > j) inside each warp
+        const int wj = j / Lt::RW, ij = (j % Lt::RW) / Lt::LPC, pj = (j % Lt::RW) % Lt::LPC;
+        Probe::mark(j, 0);
+        // 1. publish the pivot column of my warp's rows
         __syncwarp();
-        if (owner) {
+        if (Lt::colbase() == (j & 31)) {
+            double *xw = xs + w * Lt::RW;
+            if (j < 32) {
 #pragma unroll
-            for (int i = 0; i < RT; ++i) {
-                const int r = Lt::row(i);
-                const double v = (cj == 0) ? a[i][0] : a[i][CPL - 1];
-                xs[r] = r > j ? v : 0.0;
+                for (int i = 0; i < RT; ++i) xw[i * Lt::LPC + rph] = a[i][0];
+            } else {
+#pragma unroll
+                for (int i = 0; i < RT; ++i) xw[i * Lt::LPC + rph] = a[i][CPL - 1];
             }
         }
         __syncwarp();
+        if (w * Lt::RW <= j && l == 0) {                 // rows <= j of this warp are not in x
+            const int hi = min(j, w * Lt::RW + Lt::RW - 1);
+            for (int r = w * Lt::RW; r <= hi; ++r) xs[r] = 0.0;
+        }
+        __syncwarp();
+        Probe::mark(j, 1);
         // 2. partial inner products x^T A(:, c) over my rows
         double p[CPL];
         {
@@ -179,61 +311,55 @@ __device__ void tile_qr(double (&a)[Lt::RT][Lt::CPL], int n, double *xs, double 
 #pragma unroll
             for (int cc = 0; cc < CPL; ++cc) redb[w * NP + Lt::col(cc)] = p[cc];
         }
-        // row j of every column (needed for w = A(j,:) + x^T A / (alpha - beta))
-        const int wj = j / Lt::RW, ij = (j % Lt::RW) / Lt::LPC, pj = (j % Lt::RW) % Lt::LPC;
         if (w == wj && rph == pj) {
 #pragma unroll
-            for (int cc = 0; cc < CPL; ++cc) {
-                double v = 0.0;
-#pragma unroll
-                for (int i = 0; i < RT; ++i) v = (i == ij) ? a[i][cc] : v;
-                rjb[Lt::col(cc)] = v;
-            }
+            for (int cc = 0; cc < CPL; ++cc) rjb[Lt::col(cc)] = reg_row<Lt>(a, ij, cc);
         }
+        Probe::mark(j, 2);
         __syncthreads();
-        // 3. reduce across warps (same order in every thread: identical scalars)
-        double sig2 = 0.0;
-#pragma unroll
-        for (int q = 0; q < kWarps; ++q) sig2 += redb[q * NP + j];
+        Probe::mark(j, 3);
+        // 3. reduce across warps
+        const double sig2 = sum_warps(redb, NP, j);
         const double alpha = rjb[j];
         const House h = householder(alpha, sig2);
-        double u[CPL], ru[CPL];
+        double u[CPL];
 #pragma unroll
         for (int cc = 0; cc < CPL; ++cc) {
             const int c = Lt::col(cc);
-            double P = 0.0;
-#pragma unroll
-            for (int q = 0; q < kWarps; ++q) P += redb[q * NP + c];
-            const double wc = fma(P, h.scale, rjb[c]);   // v^T A(:, c)
-            const bool trail = (c > j) && (c < n);
-            u[cc] = trail ? h.tau * h.scale * wc : 0.0;  // A(r,c) -= x_r * u   (r > j)
-            ru[cc] = trail ? h.tau * wc : 0.0;            // A(j,c) -= tau * w_c
+            const double P = sum_warps(redb, NP, c);
+            const double wc = fma(P, h.scale, rjb[c]);        // v^T A(:, c)
+            u[cc] = (c > j && c < n) ? h.tau * h.scale * wc : 0.0;
         }
-        // 4. rank-1 update of the trailing columns (x re-read: saves RT registers)
+        Probe::mark(j, 4);
+        // 4. row j rides in the broadcast vector: xs[j] = alpha - beta (= 1/scale)
+        if (w == wj && l == 0) xs[j] = alpha - h.beta;
+        if (threadIdx.x == 0) {
+            taus[j] = h.tau;
+            betas[j] = h.beta;
+            scales[j] = h.scale;
+        }
+        __syncwarp();
         double x[RT];
         load_rowvec<Lt>(xs, x);
 #pragma unroll
         for (int cc = 0; cc < CPL; ++cc)
 #pragma unroll
             for (int i = 0; i < RT; ++i) a[i][cc] = fma(-x[i], u[cc], a[i][cc]);
-        if (w == wj && rph == pj) {
+        Probe::mark(j, 5);
+    }
+    __syncthreads();
+    // the pivot columns become (beta, v = x * scale) in place
 #pragma unroll
-            for (int cc = 0; cc < CPL; ++cc)
-#pragma unroll
-                for (int i = 0; i < RT; ++i)
-                    if (i == ij) a[i][cc] -= ru[cc];
-        }
-        // 5. the pivot column becomes (beta, v) in place
-        if (owner) {
+    for (int cc = 0; cc < CPL; ++cc) {
+        const int c = Lt::col(cc);
+        if (c < n) {
+            const double sc = scales[c], be = betas[c];
 #pragma unroll
             for (int i = 0; i < RT; ++i) {
                 const int r = Lt::row(i);
-                double &aij = (cj == 0) ? a[i][0] : a[i][CPL - 1];
-                if (r > j) aij = x[i] * h.scale;
-                else if (r == j) aij = h.beta;
+                a[i][cc] = r > c ? a[i][cc] * sc : (r == c ? be : a[i][cc]);
             }
         }
-        if (threadIdx.x == 0) taus[j] = h.tau;
     }
 }
 
@@ -277,9 +403,7 @@ __device__ void tile_apply(double (&c)[Lt::RT][Lt::CPL], int n, const double *Ys
         load_rowvec<Lt>(Ys + j * yld, x);
 #pragma unroll
         for (int cc = 0; cc < CPL; ++cc) {
-            double P = 0.0;
-#pragma unroll
-            for (int q = 0; q < kWarps; ++q) P += redb[q * NP + Lt::col(cc)];
+            const double P = sum_warps(redb, NP, Lt::col(cc));
             const double u = t * P;
 #pragma unroll
             for (int i = 0; i < RT; ++i) c[i][cc] = fma(-x[i], u, c[i][cc]);
@@ -340,16 +464,12 @@ __device__ void node_qr(double *Ra, double *Rb, int n, double *red, double *taus
             for (int cc = 0; cc < CPL; ++cc) redb[w * NP + Lt::col(cc)] = p[cc];
         }
         __syncthreads();
-        double sig2 = 0.0;
-#pragma unroll
-        for (int q = 0; q < kWarps; ++q) sig2 += redb[q * NP + j];
+        const double sig2 = sum_warps(redb, NP, j);
         const House h = householder(alpha, sig2);
 #pragma unroll
         for (int cc = 0; cc < CPL; ++cc) {
             const int c = Lt::col(cc);
-            double P = 0.0;
-#pragma unroll
-            for (int q = 0; q < kWarps; ++q) P += redb[q * NP + c];
+            const double P = sum_warps(redb, NP, c);
             const double wc = fma(P, h.scale, raj[cc]);
             const bool trail = (c > j) && (c < n);
             const double u = trail ? h.tau * h.scale * wc : 0.0;
@@ -414,9 +534,7 @@ __device__ void node_apply(const double *Y1, const double *tau, double *Ca, doub
 #pragma unroll
         for (int cc = 0; cc < CPL; ++cc) {
             const int c = Lt::col(cc);
-            double P = 0.0;
-#pragma unroll
-            for (int q = 0; q < kWarps; ++q) P += redb[q * NP + c];
+            const double P = sum_warps(redb, NP, c);
             const double u = t * (caj[cc] + P);
 #pragma unroll
             for (int k = 0; k < KR; ++k) cb[k][cc] = fma(-y[k], u, cb[k][cc]);
@@ -432,14 +550,25 @@ __device__ void node_apply(const double *Y1, const double *tau, double *Ca, doub
 }
 
 // Load / store an n x n upper triangle (head block of a tile) between global
-// (ld) and smem (ld NP+1, zero elsewhere).
+// (ld) and smem (ld NP+1, zero elsewhere).  Loads are issued all at once
+// (clamped addresses, select after the load) so they overlap.
 template <int NP, bool kCG>
 __device__ __forceinline__ void load_upper(double *sm, const double *g, int64_t ld, int n) {
-    for (int e = threadIdx.x; e < NP * NP; e += kThreads) {
+    constexpr int PER = (NP * NP + kThreads - 1) / kThreads;
+    double v[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int e = threadIdx.x + q * kThreads;
         const int r = e % NP, c = e / NP;
-        double v = 0.0;
-        if (r <= c && c < n) v = kCG ? __ldcg(g + r + (int64_t)c * ld) : g[r + (int64_t)c * ld];
-        sm[c * (NP + 1) + r] = v;
+        const bool ok = e < NP * NP && r <= c && c < n;
+        const double *p = ok ? g + r + (int64_t)c * ld : g;
+        v[q] = kCG ? __ldcg(p) : p[0];
+        v[q] = ok ? v[q] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int e = threadIdx.x + q * kThreads;
+        if (e < NP * NP) sm[(e / NP) * (NP + 1) + e % NP] = v[q];
     }
 }
 
@@ -454,11 +583,21 @@ __device__ __forceinline__ void store_upper(const double *sm, double *g, int64_t
 // Rectangular n x kc block between global and smem (ld NP+1).
 template <int NP, bool kCG>
 __device__ __forceinline__ void load_block(double *sm, const double *g, int64_t ld, int n, int kc) {
-    for (int e = threadIdx.x; e < NP * NP; e += kThreads) {
+    constexpr int PER = (NP * NP + kThreads - 1) / kThreads;
+    double v[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int e = threadIdx.x + q * kThreads;
         const int r = e % NP, c = e / NP;
-        double v = 0.0;
-        if (r < n && c < kc) v = kCG ? __ldcg(g + r + (int64_t)c * ld) : g[r + (int64_t)c * ld];
-        sm[c * (NP + 1) + r] = v;
+        const bool ok = e < NP * NP && r < n && c < kc;
+        const double *p = ok ? g + r + (int64_t)c * ld : g;
+        v[q] = kCG ? __ldcg(p) : p[0];
+        v[q] = ok ? v[q] : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int e = threadIdx.x + q * kThreads;
+        if (e < NP * NP) sm[(e / NP) * (NP + 1) + e % NP] = v[q];
     }
 }
 

@@ -45,10 +45,10 @@ struct FactorSmem {
     using Lt = Layout<NP, RT>;
     static constexpr int s0 = Lt::SLD * NP, s1 = 2 * NP * (NP + 1);
     static constexpr int stage = ((s0 > s1 ? s0 : s1) + 1) / 2 * 2;        // even: 16 B aligned
-    static constexpr size_t doubles = (size_t)stage + Lt::S + 2 * kWarps * NP + 2 * NP + NP + 2;
+    static constexpr size_t doubles = (size_t)stage + Lt::S + 2 * kWarps * NP + 2 * NP + 3 * NP + 2;
 };
 template <int NP, int RT>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, (RT * Layout<NP, RT>::CPL <= 32) ? 2 : 1)
 k_factor(double *A, int64_t lda, int n, DevPlan plan, double *tau_tile, double *tau_node,
          int *counters, double *R, int64_t ldr) {
     using Lt = Layout<NP, RT>;
@@ -59,18 +59,20 @@ k_factor(double *A, int64_t lda, int n, DevPlan plan, double *tau_tile, double *
     double *red = xs + Lt::S;                           // 2 * kWarps * NP
     double *rowj = red + 2 * kWarps * NP;               // 2 * NP
     double *taus = rowj + 2 * NP;                       // NP
-    int *flag = reinterpret_cast<int *>(taus + NP);
+    double *betas = taus + NP, *scales = betas + NP;    // NP, NP
+    int *flag = reinterpret_cast<int *>(scales + NP);
 
     const int t = blockIdx.x;
     const int64_t row0 = plan.tile_row0[t];
     const int rows = plan.tile_rows[t];
     double *At = A + row0;
 
-    stage_in<false>(stage, Lt::SLD, At, lda, rows, n, Lt::S, NP);
+    stage_in_async(stage, Lt::SLD, At, lda, rows, n, Lt::S, NP);
+    cp_async_wait_all();
     __syncthreads();
     double a[RT][Lt::CPL];
     smem_to_regs<Lt>(stage, a);
-    tile_qr<Lt>(a, n, xs, red, rowj, taus);
+    tile_qr<Lt>(a, n, xs, red, rowj, taus, betas, scales);
     __syncthreads();
     regs_to_smem<Lt>(stage, a);
     __syncthreads();
@@ -97,15 +99,16 @@ k_factor(double *A, int64_t lda, int n, DevPlan plan, double *tau_tile, double *
 }
 
 // ========================================================= apply Q^T (a7,a8)
-// Y tile in smem with the unit diagonal and zeros above made explicit.
+// Y tile in smem with the unit diagonal and zeros above made explicit: the
+// tile is staged with cp.async, then rows <= c of each column are overwritten.
 template <int NP, int S>
 __device__ void load_y_tile(double *Ys, int yld, const double *At, int64_t lda, int rows, int n) {
-    for (int c = 0; c < NP; ++c) {
-        for (int r = threadIdx.x; r < S; r += kThreads) {
-            double v = 0.0;
-            if (c < n && r < rows) v = (r > c) ? __ldcg(At + r + (int64_t)c * lda) : (r == c ? 1.0 : 0.0);
-            Ys[c * yld + r] = v;
-        }
+    stage_in_async(Ys, yld, At, lda, rows, n, S, NP);
+    cp_async_wait_all();
+    __syncthreads();
+    for (int e = threadIdx.x; e < NP * NP; e += kThreads) {
+        const int r = e % NP, c = e / NP;
+        if (r <= c) Ys[c * yld + r] = (r == c && c < n) ? 1.0 : 0.0;
     }
 }
 
@@ -148,7 +151,8 @@ k_apply_qt(const double *A, int64_t lda, int n, DevPlan plan, const double *tau_
     double *Ct0 = C + row0;
     for (int c0 = 0; c0 < k; c0 += KC) {
         const int kc = min(KC, k - c0);
-        stage_in<false>(Cs, Ct::SLD, Ct0 + (int64_t)c0 * ldc, ldc, rows, kc, S, KC);
+        stage_in_async(Cs, Ct::SLD, Ct0 + (int64_t)c0 * ldc, ldc, rows, kc, S, KC);
+        cp_async_wait_all();
         __syncthreads();
         double c[Ct::RT][Ct::CPL];
         smem_to_regs<Ct>(Cs, c);
@@ -233,9 +237,8 @@ k_formq_leaf(const double *A, int64_t lda, int n, DevPlan plan, const double *ta
     for (int c0 = 0; c0 < n; c0 += KC) {
         const int kc = min(KC, n - c0);
         // [X_t; 0]: the first n rows from xbuf, zeros below
-        for (int c = 0; c < KC; ++c)
-            for (int r = threadIdx.x; r < S; r += kThreads)
-                Cs[c * Ct::SLD + r] = (c < kc && r < n) ? Xt[r + (int64_t)(c0 + c) * n] : 0.0;
+        stage_in_async(Cs, Ct::SLD, Xt + (int64_t)c0 * n, n, n, kc, S, KC);
+        cp_async_wait_all();
         __syncthreads();
         double c[Ct::RT][Ct::CPL];
         smem_to_regs<Ct>(Cs, c);

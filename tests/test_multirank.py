@@ -1,0 +1,193 @@
+"""Multi-rank (row-sharded) TSQR: the butterfly driver of paper_0808_2664_b200.dist.
+
+CPU (gloo, world size 2 and 4): the SAME round logic as the product (RankState,
+torch.distributed point-to-point exchange) runs with an oracle-backed engine; its
+per-rank R, Q^T C rows and Q rows must equal the oracle's single global tree over
+the same plan (the butterfly of Alg. TSQR:par is the binary tree over
+rank roots with every rank holding a replica).
+
+GPU (marked gpu): the product CudaEngine over G virtual ranks in one process on
+one GPU (loopback exchange between rounds, no kernel ever waits on another).
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle as orc
+from paper_0808_2664_b200 import dist as tdist
+from paper_0808_2664_b200 import inputs
+
+
+# ------------------------------------------------------------ oracle engine
+def _np(t):
+    return t.numpy().T
+
+
+def _node_apply(Y1, tau, Ca, Cb, forward):
+    n = Y1.shape[0]
+    order = range(n) if forward else range(n - 1, -1, -1)
+    for j in order:
+        y = Y1[:j + 1, j]
+        w = Ca[j] + y @ Cb[:j + 1]
+        Ca[j] -= tau[j] * w
+        Cb[:j + 1] -= tau[j] * np.outer(y, w)
+
+
+class OracleTree:
+    pass
+
+
+class OracleEngine:
+    """Test-only engine: the oracle's kernels behind the product's engine interface."""
+
+    def factor_local(self, A, b, s, nranks, rank):
+        t = OracleTree()
+        ml, n = A.shape[1], A.shape[0]
+        t.f = orc.tsqr_factor(_np(A), orc.plan(ml, n, b, s, 1))
+        t.R = t.f.R.copy()
+        t.nranks, t.rank, t.n = nranks, rank, n
+        t.cross = []
+        R = torch.from_numpy(np.ascontiguousarray(t.R.T))
+        return R, t
+
+    def empty(self, shape, like):
+        return torch.empty(shape, dtype=torch.float64)
+
+    def pack(self, t, out):
+        n = t.n
+        out.numpy()[:] = np.concatenate([t.R[:c + 1, c] for c in range(n)])
+
+    def cross_factor(self, t, rnd, recv, R):
+        n = t.n
+        P = np.zeros((n, n))
+        pk = recv.numpy()
+        for c in range(n):
+            P[:c + 1, c] = pk[c * (c + 1) // 2:(c + 1) * (c + 2) // 2]
+        partner = t.rank ^ (1 << (rnd - 1))
+        Ra, Rb = (t.R, P) if t.rank < partner else (P, t.R)
+        Rn, Y1, tau, _ = orc.combine(Ra, Rb)
+        t.cross.append((Y1, tau))
+        t.R = Rn
+        R.numpy()[:] = Rn.T
+
+    def apply_local(self, t, C, top):
+        out = orc.tsqr_apply_qt(t.f, _np(C))
+        C.numpy()[:] = out.T
+        top.numpy()[:] = out[:t.n].T
+
+    def cross_apply(self, t, rnd, top, ptop, C):
+        partner = t.rank ^ (1 << (rnd - 1))
+        mine, theirs = _np(top).copy(), _np(ptop).copy()
+        Ca, Cb = (mine, theirs) if t.rank < partner else (theirs, mine)
+        Y1, tau = t.cross[rnd - 1]
+        _node_apply(Y1, tau, Ca, Cb, True)
+        top.numpy()[:] = Ca.T
+        pos = t.rank & ((1 << rnd) - 1)
+        if pos == 0:
+            C.numpy()[:, :t.n] = Ca.T
+        elif pos == 1 << (rnd - 1):
+            C.numpy()[:, :t.n] = Cb.T
+
+    def form_q(self, t):
+        n = t.n
+        X = np.eye(n)
+        for rnd in range(len(t.cross), 0, -1):
+            Y1, tau = t.cross[rnd - 1]
+            Xa, Xb = X.copy(), np.zeros((n, n))
+            _node_apply(Y1, tau, Xa, Xb, False)
+            X = Xa if ((t.rank >> (rnd - 1)) & 1) == 0 else Xb
+        ml = t.f.plan.m
+        Q0 = np.zeros((ml, n), order="F")
+        Q0[:n] = X
+        Q = orc.tsqr_apply_q(t.f, Q0)
+        return torch.from_numpy(np.ascontiguousarray(Q.T))
+
+
+# -------------------------------------------------------------- reference
+def _global_reference(m, n, b, s, G, k):
+    A = inputs.to_numpy_colmajor(inputs.gaussian(m, n, 0))
+    C = inputs.to_numpy_colmajor(inputs.gaussian(m, k, 1))
+    f = orc.tsqr_factor(A, orc.plan(m, n, b, s, G))
+    return f.R, orc.tsqr_apply_qt(f, C), orc.tsqr_form_q(f)
+
+
+def _free_port():
+    with socket.socket() as sck:
+        sck.bind(("127.0.0.1", 0))
+        return sck.getsockname()[1]
+
+
+def _worker(rank, world, port, m, n, b, s, k, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_0808_2664_b200 import api
+        row0, ml = api.slab(m, n, b, world, rank)
+        A = inputs.gaussian_rows(row0, ml, n, 0)
+        C = inputs.gaussian_rows(row0, ml, k, 1)
+        st = tdist.factor(A, b, s, engine=OracleEngine())
+        tdist.apply_qt(st, C)
+        Q = tdist.form_q(st)
+        q.put((rank, row0, ml, _np(st.R).copy(), _np(C).copy(), _np(st.top).copy(), _np(Q).copy(), st.sent))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,m,n,b,s,k", [(2, 3000, 12, 500, 250, 7), (4, 5000, 8, 300, 100, 5),
+                                             (2, 2 * 4096 + 37, 16, 4096, 512, 3)])
+def test_butterfly_gloo(world, m, n, b, s, k):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, m, n, b, s, k, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    Rref, QtC_ref, Qref = _global_reference(m, n, b, s, world, k)
+    rounds = int(np.log2(world))
+    for rank, row0, ml, R, C, top, Q, sent in sorted(res, key=lambda x: x[0]):
+        assert np.array_equal(R, Rref)                              # replicated and bitwise equal
+        assert orc.rel_fro(C, QtC_ref[row0:row0 + ml]) <= 1e-13     # tree-order rows of this rank
+        assert orc.rel_fro(top, QtC_ref[:n]) <= 1e-13              # thin part replicated
+        assert orc.rel_fro(Q, Qref[row0:row0 + ml]) <= 1e-13
+        # counts (Table 1; Cor. 2): log2 G messages of n(n+1)/2 words
+        fac = [w for r_, w in sent if True][:rounds]
+        assert len(sent) == 2 * rounds
+        assert all(w == n * (n + 1) // 2 for w in fac)
+        assert all(w == n * k for w in [w for _, w in sent][rounds:])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("G,m,n,b,s,k", [(2, 20000, 50, 4096, 256, 64), (4, 40000, 32, 4096, 512, 128),
+                                         (8, 50000, 16, 2048, 1024, 16), (8, 8 * 4096 + 100, 64, 4096, 256, 70)])
+def test_butterfly_virtual_ranks_cuda(G, m, n, b, s, k):
+    from paper_0808_2664_b200 import api
+    slabs, cs, rows = [], [], []
+    for r in range(G):
+        row0, ml = api.slab(m, n, b, G, r)
+        rows.append((row0, ml))
+        slabs.append(inputs.gaussian_rows(row0, ml, n, 0).cuda())
+        cs.append(inputs.gaussian_rows(row0, ml, k, 1).cuda())
+    states = tdist.factor_virtual(slabs, b, s)
+    tdist.apply_qt_virtual(states, cs)
+    Qs = [tdist.form_q(st) for st in states]
+    torch.cuda.synchronize()
+    Rref, QtC_ref, Qref = _global_reference(m, n, b, s, G, k)
+    for st, (row0, ml), C, Q in zip(states, rows, cs, Qs):
+        R = inputs.to_numpy_colmajor(st.R)
+        assert np.array_equal(R, inputs.to_numpy_colmajor(states[0].R))   # bitwise replicated
+        assert orc.rel_fro(orc.sign_normalise(R), orc.sign_normalise(Rref)) <= 1e-11
+        assert orc.rel_fro(inputs.to_numpy_colmajor(C), QtC_ref[row0:row0 + ml]) <= 1e-11
+        assert orc.rel_fro(inputs.to_numpy_colmajor(st.top), QtC_ref[:n]) <= 1e-11
+        assert orc.rel_fro(inputs.to_numpy_colmajor(Q), Qref[row0:row0 + ml]) <= 1e-11
+    for st in states:
+        st.tree.free()
