@@ -204,6 +204,8 @@ static int build_plan(int64_t m, int64_t n, int64_t b, int64_t s, int64_t G, pla
         blk_tile0[k] = nt;
         int64_t h = blk_rows[k];
         int64_t t = (s == 0) ? 1 : (h + s - 1) / s;   /* s = 0: one tile per block */
+        if (t > h / n) t = h / n;                      /* never a tile shorter than n */
+        if (t < 1) t = 1;
         int64_t base = h / t, extra = h - base * t;
         int64_t r0 = blk_row0[k];
         for (int64_t i = 0; i < t; ++i) {

@@ -82,9 +82,9 @@ void orc_build_t_node(int64_t n, const double *Y1, int64_t ldy, const double *ta
  * block if r >= n, else is merged into the last block (reading R6).
  * Ranks: contiguous runs of whole blocks, the first (nblocks mod G) ranks get
  * one extra block.
- * Tiles: a block of h rows is split into t = ceil(h/s) tiles of near-equal
- * height, the first (h mod t) tiles one row taller; s = 0 means one tile per
- * block (the paper's plan, tiles = row blocks).
+ * Tiles: a block of h rows is split into t = min(ceil(h/s), floor(h/n)) (at
+ * least 1) tiles of near-equal height, the first (h mod t) tiles one row
+ * taller; s = 0 means one tile per block (the paper's plan, tiles = row blocks).
  * Nodes are listed in execution order: level by level inside every block,
  * then level by level over the blocks of each rank, then the rank levels.
  * A node is the pair (a, b) of the leftmost tiles of its left and right

@@ -11,17 +11,11 @@ namespace tsqr {
 
 int padded_width(int64_t n) { return n <= 16 ? 16 : (n <= 32 ? 32 : 64); }
 
-int64_t tile_capacity(int64_t n) {
-    switch (padded_width(n)) {
-        case 16: return 1024;
-        case 32: return 512;
-        default: return 256;
-    }
-}
-
-// Default tile: the largest tile two CTAs per SM can keep in registers
-// (32 fp64 per thread), so one CTA's reduction latency hides behind the other's FMAs.
-int64_t default_tile_rows(int64_t n) { return tile_capacity(n) / 2; }
+// Tallest tile one column-owner team can keep in registers (two row groups of
+// 96-row bands), and the default tile: one 96-row band per lane, so a team is a
+// single warp (n <= 32) or two (n <= 64) and several teams share an SM.
+int64_t tile_capacity(int64_t) { return 192; }
+int64_t default_tile_rows(int64_t) { return 96; }
 
 static int64_t block_count(int64_t m, int64_t n, int64_t b, int64_t *last_rows) {
     // Reading R6: blocks of b rows; a remainder >= n is its own block, a
@@ -65,7 +59,6 @@ int build_plan(int64_t m_local, int64_t n, int64_t block_rows, int64_t tile_rows
     if (nranks < 1 || (nranks & (nranks - 1)) || rank < 0 || rank >= nranks) return TSQR_ERR_UNSUPPORTED;
     const int64_t cap = tile_capacity(n);
     const int64_t s = tile_rows == 0 ? std::min(default_tile_rows(n), block_rows) : tile_rows;
-    if (s < n) return TSQR_ERR_SHAPE;
     if (s > cap) return TSQR_ERR_UNSUPPORTED;
 
     *p = Plan();
@@ -78,11 +71,13 @@ int build_plan(int64_t m_local, int64_t n, int64_t block_rows, int64_t tile_rows
     int64_t row = 0;
     for (int64_t k = 0; k < nblk; ++k) {
         const int64_t h = (k == nblk - 1) ? last : block_rows;
-        const int64_t t = (h + s - 1) / s;        // tiles of near-equal height
+        // tiles of near-equal height, never shorter than n
+        const int64_t t = std::max<int64_t>(1, std::min<int64_t>((h + s - 1) / s, h / n));
         p->blk_tile0.push_back((int)p->tile_row0.size());
         for (int64_t i = 0; i < t; ++i) {
             const int64_t rows = h / t + (i < h % t ? 1 : 0);
             if (rows < n) return TSQR_ERR_SHAPE;
+            if (rows > cap) return TSQR_ERR_UNSUPPORTED;
             p->tile_row0.push_back(row);
             p->tile_rows.push_back(rows);
             row += rows;

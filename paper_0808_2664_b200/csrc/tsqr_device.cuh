@@ -1,21 +1,19 @@
 // Device building blocks of the B200 TSQR path (sm_100a).  Product code.
 //
-// Data layout: fp64 column-major, element (i,j) at
-// X[i + j*ld].  A tile of <= S rows x NP columns (NP = n padded to 16/32/64) is
-// held in REGISTERS by a 256-thread CTA for the whole Householder sweep:
-//   lane l of warp w owns columns  colbase(l) + 32*cc   (cc < CPL)
-//                      and rows    w*RW + i*LPC + rph(l) (i < RT)
-// so that every element is touched by exactly one thread and the per-column
-// reductions are (warp partials in registers) -> (LPC-lane shuffle) -> (one
-// __syncthreads on a double-buffered smem array).
+// Layout ("column-owner teams"): a team is one CTA of
+// CW x G warps.  Lane l of column-warp cw owns matrix column c = 32*cw + l for a
+// band of RT consecutive rows; row-group g owns rows [g*RT, (g+1)*RT).  A
+// column's band lives in that lane's registers for the whole sweep, so the
+// inner products of a Householder step (x^T A(:,c)) are per-lane sums: no
+// cross-lane reduction (G = 1), and the only synchronisation per column is the
+// publication of the pivot column (warp-level for a one-warp team).  Many small
+// teams per SM (registers, not barriers, bound the residency) hide each other's
+// reflector latency.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace tsqr {
-
-constexpr int kWarps = 8;
-constexpr int kThreads = kWarps * 32;
 
 struct DevPlan {
     const int64_t *tile_row0;   // first local row of tile t
@@ -26,35 +24,70 @@ struct DevPlan {
     int L;                      // tiles
 };
 
-template <int NP_, int RT_>
-struct Layout {
-    static constexpr int NP = NP_;
-    static constexpr int RT = RT_;                         // register rows per thread
-    static constexpr int LC = NP < 32 ? NP : 32;           // lanes with distinct columns
-    static constexpr int CPL = NP > 32 ? NP / 32 : 1;      // columns per lane
-    static constexpr int LPC = 32 / LC;                    // lanes per column (row phases)
-    static constexpr int RW = RT * LPC;                    // rows per warp
-    static constexpr int S = RW * kWarps;                  // tile capacity (rows)
-    static constexpr int SLD = S + 1;                      // odd smem ld: conflict-free
+template <int CW_, int G_, int RT_>
+struct Team {
+    static constexpr int CW = CW_;            // column warps (n <= 32*CW)
+    static constexpr int G = G_;              // row groups
+    static constexpr int RT = RT_;            // rows per lane band
+    static constexpr int NW = CW * G;         // warps per team (= CTA)
+    static constexpr int NT = NW * 32;
+    static constexpr int NPAD = CW * 32;      // columns a team can hold
+    static constexpr int S = G * RT;          // tile rows a team can hold
+    static constexpr int LDR = NPAD + 1;      // ld of n x n node blocks in smem
+    static_assert(RT % 16 == 0, "bands are processed in chunks of 16 rows");
     __device__ static int lane() { return threadIdx.x & 31; }
     __device__ static int warp() { return threadIdx.x >> 5; }
-    __device__ static int colbase() { return lane() % LC; }
-    __device__ static int rph() { return lane() / LC; }
-    __device__ static int col(int cc) { return colbase() + 32 * cc; }
-    __device__ static int row(int i) { return warp() * RW + i * LPC + rph(); }
+    __device__ static int grp() { return warp() / CW; }
+    __device__ static int col() { return (warp() % CW) * 32 + lane(); }
+    __device__ static int row0() { return grp() * RT; }
 };
 
-// ------------------------------------------------------------------ staging
-__device__ __forceinline__ void stage_out(const double *sm, int sld, double *g, int64_t ldg,
-                                          int rows, int ncols) {
-    for (int c = 0; c < ncols; ++c) {
-        double *gc = g + (int64_t)c * ldg;
-        for (int r = threadIdx.x; r < rows; r += kThreads) gc[r] = sm[c * sld + r];
-    }
+template <int NW>
+__device__ __forceinline__ void team_sync() {
+    if constexpr (NW == 1) __syncwarp();
+    else __syncthreads();
 }
 
-// Asynchronous global -> smem staging (cp.async, 8-byte elements, zero fill):
-// every element is in flight at once instead of one dependent load per column.
+// ----------------------------------------------------------- register access
+// Runtime-indexed access to a register band: a jump table (BRX) on a
+// warp-uniform index (the column step j), a handful of instructions.
+#define TSQR_C8(b)                                      \
+    case b + 0: TSQR_OP(b + 0);                         \
+    case b + 1: TSQR_OP(b + 1);                         \
+    case b + 2: TSQR_OP(b + 2);                         \
+    case b + 3: TSQR_OP(b + 3);                         \
+    case b + 4: TSQR_OP(b + 4);                         \
+    case b + 5: TSQR_OP(b + 5);                         \
+    case b + 6: TSQR_OP(b + 6);                         \
+    case b + 7: TSQR_OP(b + 7);
+#define TSQR_C128 TSQR_C8(0) TSQR_C8(8) TSQR_C8(16) TSQR_C8(24) TSQR_C8(32) TSQR_C8(40) TSQR_C8(48) \
+    TSQR_C8(56) TSQR_C8(64) TSQR_C8(72) TSQR_C8(80) TSQR_C8(88) TSQR_C8(96) TSQR_C8(104) TSQR_C8(112) TSQR_C8(120)
+
+template <int N>
+__device__ __forceinline__ double reg_get(const double (&a)[N], int i) {
+    static_assert(N <= 128, "jump table covers 128 registers");
+#define TSQR_OP(q) return a[(q) < N ? (q) : 0]
+    switch (i) {
+        TSQR_C128
+        default: return 0.0;
+    }
+#undef TSQR_OP
+}
+
+template <int N>
+__device__ __forceinline__ void reg_sub(double (&a)[N], int i, double v) {
+#define TSQR_OP(q)                              \
+    if ((q) < N) a[(q) < N ? (q) : 0] -= v;     \
+    return
+    switch (i) {
+        TSQR_C128
+        default: return;
+    }
+#undef TSQR_OP
+}
+
+// ------------------------------------------------------------------ staging
+// Asynchronous global -> smem staging (cp.async, 8-byte elements, zero fill).
 __device__ __forceinline__ void cp_async8(double *sm, const double *g, bool valid) {
     const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(sm));
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(g), "r"(valid ? 8 : 0)
@@ -62,66 +95,34 @@ __device__ __forceinline__ void cp_async8(double *sm, const double *g, bool vali
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
-// global (rows x ncols, ld) -> smem (cap_rows x cap_cols, sld), zero padded; the
-// caller waits with cp_async_wait_all() + __syncthreads().
+// global (rows x ncols, ld) -> smem (cap_rows x cap_cols, sld), zero padded.
+// The caller waits with cp_async_wait_all() and a barrier.
+template <int NT>
 __device__ __forceinline__ void stage_in_async(double *sm, int sld, const double *g, int64_t ldg, int rows,
                                                int ncols, int cap_rows, int cap_cols) {
     for (int c = 0; c < cap_cols; ++c) {
         const double *gc = g + (int64_t)(c < ncols ? c : 0) * ldg;
-        for (int r = threadIdx.x; r < cap_rows; r += kThreads) {
+        for (int r = threadIdx.x; r < cap_rows; r += NT) {
             const bool ok = (c < ncols) && (r < rows);
             cp_async8(sm + c * sld + r, ok ? gc + r : g, ok);
         }
     }
 }
 
-template <class Lt>
-__device__ __forceinline__ void smem_to_regs(const double *sm, double (&a)[Lt::RT][Lt::CPL]) {
-#pragma unroll
-    for (int cc = 0; cc < Lt::CPL; ++cc)
-#pragma unroll
-        for (int i = 0; i < Lt::RT; ++i) a[i][cc] = sm[Lt::col(cc) * Lt::SLD + Lt::row(i)];
-}
-
-template <class Lt>
-__device__ __forceinline__ void regs_to_smem(double *sm, const double (&a)[Lt::RT][Lt::CPL]) {
-#pragma unroll
-    for (int cc = 0; cc < Lt::CPL; ++cc)
-#pragma unroll
-        for (int i = 0; i < Lt::RT; ++i) sm[Lt::col(cc) * Lt::SLD + Lt::row(i)] = a[i][cc];
-}
-
-// Read this thread's RT values of a per-row vector xs[0..S) (same rows as the
-// register tile).  LPC == 1: all lanes of a warp read the same addresses
-// (broadcast), vectorised two rows per load.
-template <class Lt>
-__device__ __forceinline__ void load_rowvec(const double *xs, double (&x)[Lt::RT]) {
-    if constexpr (Lt::LPC == 1 && (Lt::RT % 2) == 0) {
-        const double2 *x2 = reinterpret_cast<const double2 *>(xs + Lt::warp() * Lt::RW);
-#pragma unroll
-        for (int i = 0; i < Lt::RT / 2; ++i) {
-            double2 v = x2[i];
-            x[2 * i] = v.x;
-            x[2 * i + 1] = v.y;
-        }
-    } else {
-#pragma unroll
-        for (int i = 0; i < Lt::RT; ++i) x[i] = xs[Lt::row(i)];
+template <int NT>
+__device__ __forceinline__ void stage_out(const double *sm, int sld, double *g, int64_t ldg, int rows, int ncols) {
+    for (int c = 0; c < ncols; ++c) {
+        double *gc = g + (int64_t)c * ldg;
+        for (int r = threadIdx.x; r < rows; r += NT) gc[r] = sm[c * sld + r];
     }
 }
 
-__device__ __forceinline__ double warp_sum_lpc(double v, int lc) {
-    for (int o = lc; o < 32; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
-// Householder scalars in the LAPACK dlarfg convention (reading R1/R2):
-// beta = -sign(alpha) N, N = sqrt(alpha^2 + sigma2), tau = (beta - alpha)/beta
-// = 1 + |alpha|/N, v = x / (alpha - beta) below the pivot, i.e.
-// scale = sign(alpha) / (|alpha| + N).  sigma2 == 0 -> H = I.
-// The critical path avoids IEEE sqrt/div sequences: N = y * rsqrt(y) and the
-// reciprocal use the hardware approximations refined by Newton steps
-// (<= 2 ulp).
+// ------------------------------------------------------------ Householder
+// LAPACK dlarfg convention (readings R1/R2): beta = -sign(alpha) N,
+// N = sqrt(alpha^2 + sigma2), tau = (beta - alpha)/beta = 1 + |alpha|/N,
+// v = x / (alpha - beta), i.e. scale = sign(alpha) / (|alpha| + N).
+// sigma2 == 0 -> H = I.  rsqrt / rcp use the hardware approximations refined by
+// Newton steps (<= 2 ulp).
 __device__ __forceinline__ double rcp_nr(double d) {
     double y;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
@@ -142,484 +143,294 @@ __device__ __forceinline__ House householder(double alpha, double sigma2) {
         h.scale = 0.0;
     } else {
         const double y = fma(alpha, alpha, sigma2);
-        const double r = rsqrt(y);                     // MUFU + Newton, ~1 ulp
+        const double r = rsqrt(y);
         const double N = y * r;
         const double aa = fabs(alpha);
         h.beta = alpha >= 0.0 ? -N : N;
-        h.tau = fma(aa, r, 1.0);                      // 1 + |alpha| / N
+        h.tau = fma(aa, r, 1.0);
         const double inv = rcp_nr(aa + N);
         h.scale = alpha >= 0.0 ? inv : -inv;
     }
     return h;
 }
 
-// Sum of the kWarps partials of column c in a fixed tree order (every thread
-// gets bit-identical results).
-__device__ __forceinline__ double sum_warps(const double *redb, int stride, int c) {
-    double v[kWarps];
+// -------------------------------------------------------------- band math
+// p = sum_i x[i] a[i] over a band; x from smem in 16-row chunks (two rows per
+// 16-byte broadcast load), 8 independent accumulators.
+template <int RT>
+__device__ __forceinline__ double band_dot(const double *x, const double (&a)[RT]) {
+    double s[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const double2 *x2 = reinterpret_cast<const double2 *>(x);
 #pragma unroll
-    for (int q = 0; q < kWarps; ++q) v[q] = redb[q * stride + c];
+    for (int k = 0; k < RT / 16; ++k) {
+        double xv[16];
 #pragma unroll
-    for (int h = kWarps / 2; h >= 1; h /= 2)
+        for (int q = 0; q < 8; ++q) {
+            const double2 v = x2[k * 8 + q];
+            xv[2 * q] = v.x;
+            xv[2 * q + 1] = v.y;
+        }
 #pragma unroll
-        for (int q = 0; q < h; ++q) v[q] = v[q] + v[q + h];
-    return v[0];
+        for (int q = 0; q < 16; ++q) s[q & 7] = fma(xv[q], a[k * 16 + q], s[q & 7]);
+    }
+    return ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
 }
 
-// ============================================================== tile QR (a2)
-// Fetch register row i (runtime index) of this thread's tile: a jump table,
-// executed only by the one warp that holds the row (warp-uniform branch).
-template <class Lt>
-__device__ __forceinline__ double reg_row(const double (&a)[Lt::RT][Lt::CPL], int i, int cc) {
-    static_assert(Lt::RT <= 64, "reg_row covers 64 register rows");
-    switch (i) {
-        case 0: return a[0 < Lt::RT ? 0 : 0][cc];
-        case 1: return a[1 < Lt::RT ? 1 : 0][cc];
-        case 2: return a[2 < Lt::RT ? 2 : 0][cc];
-        case 3: return a[3 < Lt::RT ? 3 : 0][cc];
-        case 4: return a[4 < Lt::RT ? 4 : 0][cc];
-        case 5: return a[5 < Lt::RT ? 5 : 0][cc];
-        case 6: return a[6 < Lt::RT ? 6 : 0][cc];
-        case 7: return a[7 < Lt::RT ? 7 : 0][cc];
-        case 8: return a[8 < Lt::RT ? 8 : 0][cc];
-        case 9: return a[9 < Lt::RT ? 9 : 0][cc];
-        case 10: return a[10 < Lt::RT ? 10 : 0][cc];
-        case 11: return a[11 < Lt::RT ? 11 : 0][cc];
-        case 12: return a[12 < Lt::RT ? 12 : 0][cc];
-        case 13: return a[13 < Lt::RT ? 13 : 0][cc];
-        case 14: return a[14 < Lt::RT ? 14 : 0][cc];
-        case 15: return a[15 < Lt::RT ? 15 : 0][cc];
-        case 16: return a[16 < Lt::RT ? 16 : 0][cc];
-        case 17: return a[17 < Lt::RT ? 17 : 0][cc];
-        case 18: return a[18 < Lt::RT ? 18 : 0][cc];
-        case 19: return a[19 < Lt::RT ? 19 : 0][cc];
-        case 20: return a[20 < Lt::RT ? 20 : 0][cc];
-        case 21: return a[21 < Lt::RT ? 21 : 0][cc];
-        case 22: return a[22 < Lt::RT ? 22 : 0][cc];
-        case 23: return a[23 < Lt::RT ? 23 : 0][cc];
-        case 24: return a[24 < Lt::RT ? 24 : 0][cc];
-        case 25: return a[25 < Lt::RT ? 25 : 0][cc];
-        case 26: return a[26 < Lt::RT ? 26 : 0][cc];
-        case 27: return a[27 < Lt::RT ? 27 : 0][cc];
-        case 28: return a[28 < Lt::RT ? 28 : 0][cc];
-        case 29: return a[29 < Lt::RT ? 29 : 0][cc];
-        case 30: return a[30 < Lt::RT ? 30 : 0][cc];
-        case 31: return a[31 < Lt::RT ? 31 : 0][cc];
-        case 32: return a[32 < Lt::RT ? 32 : 0][cc];
-        case 33: return a[33 < Lt::RT ? 33 : 0][cc];
-        case 34: return a[34 < Lt::RT ? 34 : 0][cc];
-        case 35: return a[35 < Lt::RT ? 35 : 0][cc];
-        case 36: return a[36 < Lt::RT ? 36 : 0][cc];
-        case 37: return a[37 < Lt::RT ? 37 : 0][cc];
-        case 38: return a[38 < Lt::RT ? 38 : 0][cc];
-        case 39: return a[39 < Lt::RT ? 39 : 0][cc];
-        case 40: return a[40 < Lt::RT ? 40 : 0][cc];
-        case 41: return a[41 < Lt::RT ? 41 : 0][cc];
-        case 42: return a[42 < Lt::RT ? 42 : 0][cc];
-        case 43: return a[43 < Lt::RT ? 43 : 0][cc];
-        case 44: return a[44 < Lt::RT ? 44 : 0][cc];
-        case 45: return a[45 < Lt::RT ? 45 : 0][cc];
-        case 46: return a[46 < Lt::RT ? 46 : 0][cc];
-        case 47: return a[47 < Lt::RT ? 47 : 0][cc];
-        case 48: return a[48 < Lt::RT ? 48 : 0][cc];
-        case 49: return a[49 < Lt::RT ? 49 : 0][cc];
-        case 50: return a[50 < Lt::RT ? 50 : 0][cc];
-        case 51: return a[51 < Lt::RT ? 51 : 0][cc];
-        case 52: return a[52 < Lt::RT ? 52 : 0][cc];
-        case 53: return a[53 < Lt::RT ? 53 : 0][cc];
-        case 54: return a[54 < Lt::RT ? 54 : 0][cc];
-        case 55: return a[55 < Lt::RT ? 55 : 0][cc];
-        case 56: return a[56 < Lt::RT ? 56 : 0][cc];
-        case 57: return a[57 < Lt::RT ? 57 : 0][cc];
-        case 58: return a[58 < Lt::RT ? 58 : 0][cc];
-        case 59: return a[59 < Lt::RT ? 59 : 0][cc];
-        case 60: return a[60 < Lt::RT ? 60 : 0][cc];
-        case 61: return a[61 < Lt::RT ? 61 : 0][cc];
-        case 62: return a[62 < Lt::RT ? 62 : 0][cc];
-        case 63: return a[63 < Lt::RT ? 63 : 0][cc];
-        default: return 0.0;
+// a[i] -= x[i] u over a band.
+template <int RT>
+__device__ __forceinline__ void band_axpy(const double *x, double u, double (&a)[RT]) {
+    const double2 *x2 = reinterpret_cast<const double2 *>(x);
+#pragma unroll
+    for (int k = 0; k < RT / 16; ++k) {
+        double xv[16];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const double2 v = x2[k * 8 + q];
+            xv[2 * q] = v.x;
+            xv[2 * q + 1] = v.y;
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) a[k * 16 + q] = fma(-xv[q], u, a[k * 16 + q]);
     }
 }
 
-// Unblocked Householder QR of the register tile a (rows x n, padded).  One
-// __syncthreads per column.  Per column j:
-//   1. the owner lane of column j publishes x = A(:, j) (rows > j; rows <= j
-//      zeroed) in smem xs;
-//   2. every thread forms partial dots x^T A(:, c) over its rows (c = j gives
-//      sigma^2 = ||x(j+1:)||^2); the thread holding row j publishes A(j, :);
-//   3. one barrier; every thread reduces the partials (same order: identical
-//      scalars), forms beta, tau and scale = 1/(alpha - beta) (dlarfg), and
-//      w_c = A(j,c) + scale x^T A(:,c) = v^T A(:,c);
-//   4. xs[j] := alpha - beta, so one rank-1 update A(:,c) -= xs * (tau*scale*w_c)
-//      also performs row j's update A(j,c) -= tau w_c, with no per-element masks.
-// Column j itself is left untouched in the loop; its final form (beta on the
-// diagonal, v = x * scale below) is applied once after the loop.
-// Smem: xs[S], red[2][kWarps][NP], rowj[2][NP], taus/betas/scales[NP].
-struct NoProbe {
-    __device__ static void mark(int, int) {}
-};
-
-template <class Lt, class Probe = NoProbe>
-__device__ void tile_qr(double (&a)[Lt::RT][Lt::CPL], int n, double *xs, double *red,
-                        double *rowj, double *taus, double *betas, double *scales) {
-    constexpr int RT = Lt::RT, CPL = Lt::CPL, NP = Lt::NP;
-    const int w = Lt::warp(), l = Lt::lane(), rph = Lt::rph();
-    for (int j = 0; j < n; ++j) {
-        const int buf = j & 1;
-        double *redb = red + buf * (kWarps * NP);
-        double *rjb = rowj + buf * NP;
-        const int wj = j / Lt::RW, ij = (j % Lt::RW) / Lt::LPC, pj = (j % Lt::RW) % Lt::LPC;
-        Probe::mark(j, 0);
-        // 1. publish the pivot column of my warp's rows
-        __syncwarp();
-        if (Lt::colbase() == (j & 31)) {
-            double *xw = xs + w * Lt::RW;
-            if (j < 32) {
+// The same over rows 0..j only (structured node blocks): chunks of 8 rows; the
+// loop stops at the first chunk past row j (warp-uniform branch).
+template <int NR>
+__device__ __forceinline__ double head_dot(const double *x, const double (&a)[NR], int j) {
+    double s[4] = {0, 0, 0, 0};
+    const double2 *x2 = reinterpret_cast<const double2 *>(x);
 #pragma unroll
-                for (int i = 0; i < RT; ++i) xw[i * Lt::LPC + rph] = a[i][0];
+    for (int k = 0; k < NR / 8; ++k) {
+        if (k * 8 > j) break;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double2 v = x2[k * 4 + q];
+            s[q] = fma(v.x, a[k * 8 + 2 * q], s[q]);
+            s[q] = fma(v.y, a[k * 8 + 2 * q + 1], s[q]);
+        }
+    }
+    return (s[0] + s[1]) + (s[2] + s[3]);
+}
+
+template <int NR>
+__device__ __forceinline__ void head_axpy(const double *x, double u, double (&a)[NR], int j) {
+    const double2 *x2 = reinterpret_cast<const double2 *>(x);
+#pragma unroll
+    for (int k = 0; k < NR / 8; ++k) {
+        if (k * 8 > j) break;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double2 v = x2[k * 4 + q];
+            a[k * 8 + 2 * q] = fma(-v.x, u, a[k * 8 + 2 * q]);
+            a[k * 8 + 2 * q + 1] = fma(-v.y, u, a[k * 8 + 2 * q + 1]);
+        }
+    }
+}
+
+// ============================================================== tile QR (a2)
+// Unblocked Householder QR (DGEQR2: the leaf QR of Alg. TSQR:par line 1,
+// P:1679-1680) of a team-resident tile.  Column j:
+//  1. the owner lanes (column j, one per row group) publish x = A(:, j) with
+//     rows <= j zeroed (double-buffered xs) and alpha = A(j, j);
+//  2. sync; every lane forms p_c = x^T A(:, c) over its band (c = j gives
+//     sigma^2 = ||A(j+1:, j)||^2); row groups add their partials (G > 1);
+//  3. every lane forms beta, tau, scale (dlarfg) and w_c = A(j,c) + scale p_c
+//     = v^T A(:, c), then A(:, c) -= x (tau scale w_c) and A(j, c) -= tau w_c.
+// Column j stays in place and becomes (beta, v = scale x) once at the end.
+// Smem: xs[2][S]; red[2][2][G][NPAD] (NW > 1); alph[2]; taus/betas/scales[NPAD].
+template <class T>
+__device__ __forceinline__ void team_tile_qr(double (&a)[T::RT], int n, double *xs, double *red, double *alph, double *taus,
+                             double *betas, double *scales) {
+    constexpr int RT = T::RT, S = T::S, G = T::G, NP = T::NPAD;
+    const int c = T::col(), g = T::grp(), r0 = T::row0();
+#pragma unroll 1
+    for (int j = 0; j < n; ++j) {
+        const int b = j & 1;
+        double *xb = xs + b * S;
+        const int gj = j / RT, ij = j - gj * RT;
+        // 1. publish the pivot column
+        if (c == j) {
+            double *xg = xb + r0;
+            if (r0 > j) {
+#pragma unroll
+                for (int i = 0; i < RT; i += 2)
+                    *reinterpret_cast<double2 *>(xg + i) = make_double2(a[i], a[i + 1]);
             } else {
 #pragma unroll
-                for (int i = 0; i < RT; ++i) xw[i * Lt::LPC + rph] = a[i][CPL - 1];
+                for (int i = 0; i < RT; ++i) xg[i] = (r0 + i > j) ? a[i] : 0.0;
+                if (g == gj) alph[b] = reg_get(a, ij);
             }
         }
-        __syncwarp();
-        if (w * Lt::RW <= j && l == 0) {                 // rows <= j of this warp are not in x
-            const int hi = min(j, w * Lt::RW + Lt::RW - 1);
-            for (int r = w * Lt::RW; r <= hi; ++r) xs[r] = 0.0;
-        }
-        __syncwarp();
-        Probe::mark(j, 1);
-        // 2. partial inner products x^T A(:, c) over my rows
-        double p[CPL];
-        {
-            double x[RT];
-            load_rowvec<Lt>(xs, x);
+        team_sync<T::NW>();
+        // 2. partial inner products over my band
+        const double p = band_dot<RT>(xb + r0, a);
+        const double rj = (g == gj) ? reg_get(a, ij) : 0.0;     // A(j, c)
+        double P, RJ, sig2, alpha;
+        if constexpr (T::NW == 1) {
+            P = p;
+            RJ = rj;
+            sig2 = __shfl_sync(0xffffffffu, p, j);
+            alpha = __shfl_sync(0xffffffffu, rj, j);
+        } else {
+            double *rp = red + (b * 2) * G * NP, *rr = rp + G * NP;
+            rp[g * NP + c] = p;
+            rr[g * NP + c] = rj;
+            team_sync<T::NW>();
+            P = 0.0;
+            RJ = 0.0;
+            sig2 = 0.0;
 #pragma unroll
-            for (int cc = 0; cc < CPL; ++cc) {
-                double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-                for (int i = 0; i < RT; i += 4) {
-                    s0 = fma(x[i], a[i][cc], s0);
-                    if (i + 1 < RT) s1 = fma(x[i + 1], a[i + 1][cc], s1);
-                    if (i + 2 < RT) s2 = fma(x[i + 2], a[i + 2][cc], s2);
-                    if (i + 3 < RT) s3 = fma(x[i + 3], a[i + 3][cc], s3);
-                }
-                p[cc] = warp_sum_lpc((s0 + s1) + (s2 + s3), Lt::LC);
+            for (int q = 0; q < G; ++q) {
+                P += rp[q * NP + c];
+                RJ += rr[q * NP + c];
+                sig2 += rp[q * NP + j];
             }
+            alpha = alph[b];
         }
-        if (rph == 0) {
-#pragma unroll
-            for (int cc = 0; cc < CPL; ++cc) redb[w * NP + Lt::col(cc)] = p[cc];
-        }
-        if (w == wj && rph == pj) {
-#pragma unroll
-            for (int cc = 0; cc < CPL; ++cc) rjb[Lt::col(cc)] = reg_row<Lt>(a, ij, cc);
-        }
-        Probe::mark(j, 2);
-        __syncthreads();
-        Probe::mark(j, 3);
-        // 3. reduce across warps
-        const double sig2 = sum_warps(redb, NP, j);
-        const double alpha = rjb[j];
+        // 3. reflector and rank-1 update
         const House h = householder(alpha, sig2);
-        double u[CPL];
-#pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) {
-            const int c = Lt::col(cc);
-            const double P = sum_warps(redb, NP, c);
-            const double wc = fma(P, h.scale, rjb[c]);        // v^T A(:, c)
-            u[cc] = (c > j && c < n) ? h.tau * h.scale * wc : 0.0;
-        }
-        Probe::mark(j, 4);
-        // 4. row j rides in the broadcast vector: xs[j] = alpha - beta (= 1/scale)
-        if (w == wj && l == 0) xs[j] = alpha - h.beta;
+        const double w = fma(P, h.scale, RJ);                     // v^T A(:, c)
+        const double u = (c > j && c < n) ? h.tau * h.scale * w : 0.0;
+        band_axpy<RT>(xb + r0, u, a);
+        if (g == gj) reg_sub(a, ij, (alpha - h.beta) * u);        // A(j,c) -= tau w_c
         if (threadIdx.x == 0) {
             taus[j] = h.tau;
             betas[j] = h.beta;
             scales[j] = h.scale;
         }
-        __syncwarp();
-        double x[RT];
-        load_rowvec<Lt>(xs, x);
-#pragma unroll
-        for (int cc = 0; cc < CPL; ++cc)
-#pragma unroll
-            for (int i = 0; i < RT; ++i) a[i][cc] = fma(-x[i], u[cc], a[i][cc]);
-        Probe::mark(j, 5);
     }
-    __syncthreads();
-    // the pivot columns become (beta, v = x * scale) in place
+    team_sync<T::NW>();
+    if (c < n) {
+        const double sc = scales[c], be = betas[c];
 #pragma unroll
-    for (int cc = 0; cc < CPL; ++cc) {
-        const int c = Lt::col(cc);
-        if (c < n) {
-            const double sc = scales[c], be = betas[c];
-#pragma unroll
-            for (int i = 0; i < RT; ++i) {
-                const int r = Lt::row(i);
-                a[i][cc] = r > c ? a[i][cc] * sc : (r == c ? be : a[i][cc]);
-            }
+        for (int i = 0; i < RT; ++i) {
+            const int r = r0 + i;
+            a[i] = r > c ? a[i] * sc : (r == c ? be : a[i]);
         }
     }
 }
 
-// ====================================================== tile reflector apply
-// C (register tile, same rows as the Y tile in smem Ys[col*yld + row], with
-// unit diagonal and zeros above it already in place) <- H_j C for
-// j = 0..n-1 (kForward: Q^T, leaf stage of apply-Q^T, [TR] P:1915-1938) or
-// j = n-1..0 (Q, leaf stage of form-Q).  One __syncthreads per reflector.
-template <class Lt, bool kForward>
-__device__ void tile_apply(double (&c)[Lt::RT][Lt::CPL], int n, const double *Ys, int yld,
-                           const double *tau, double *red) {
-    constexpr int RT = Lt::RT, CPL = Lt::CPL, NP = Lt::NP;
-    const int w = Lt::warp(), rph = Lt::rph();
-    for (int jj = 0; jj < n; ++jj) {
-        const int j = kForward ? jj : n - 1 - jj;
-        double *redb = red + (jj & 1) * (kWarps * NP);
-        double p[CPL];
-        {
-            double x[RT];
-            load_rowvec<Lt>(Ys + j * yld, x);
-#pragma unroll
-            for (int cc = 0; cc < CPL; ++cc) {
-                double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
-#pragma unroll
-                for (int i = 0; i < RT; i += 4) {
-                    s0 = fma(x[i], c[i][cc], s0);
-                    if (i + 1 < RT) s1 = fma(x[i + 1], c[i + 1][cc], s1);
-                    if (i + 2 < RT) s2 = fma(x[i + 2], c[i + 2][cc], s2);
-                    if (i + 3 < RT) s3 = fma(x[i + 3], c[i + 3][cc], s3);
-                }
-                p[cc] = warp_sum_lpc((s0 + s1) + (s2 + s3), Lt::LC);
-            }
-        }
-        if (rph == 0) {
-#pragma unroll
-            for (int cc = 0; cc < CPL; ++cc) redb[w * NP + Lt::col(cc)] = p[cc];
-        }
-        __syncthreads();
-        const double t = tau[j];
-        double x[RT];
-        load_rowvec<Lt>(Ys + j * yld, x);
-#pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) {
-            const double P = sum_warps(redb, NP, Lt::col(cc));
-            const double u = t * P;
-#pragma unroll
-            for (int i = 0; i < RT; ++i) c[i][cc] = fma(-x[i], u, c[i][cc]);
-        }
-    }
-}
-
-// ===================================================== node (structured) ops
-// Thread mapping for n x n node work: lanes own columns as in Layout<NP,*>;
-// row i of the lower block belongs to thread (w, rph) with
-//   i = (k*kWarps + w)*LPC + rph,  k < KR = NP / (kWarps*LPC).
-template <int NP>
-struct NodeLayout {
-    using Lt = Layout<NP, 1>;
-    static constexpr int CPL = Lt::CPL, LPC = Lt::LPC, LC = Lt::LC;
-    static constexpr int KR = NP / (kWarps * LPC) > 0 ? NP / (kWarps * LPC) : 1;
-    static constexpr int LD = NP + 1;
-    __device__ static int row(int k) { return (k * kWarps + Lt::warp()) * LPC + Lt::rph(); }
-};
-
+// ============================================================ node QR (a4)
 // Structured QR of [Ra; Rb] (two n x n upper triangles), Alg. QR:qnxn with q = 2
 // (P:1958-1979): reflector j acts on {row j of Ra} u {rows 0..j of Rb}.
-// Ra, Rb: smem n x n (ld NP+1), zero below the diagonal.  On exit Ra = R,
-// Rb = Y1 (upper, eq. fact_2rs), taus[j].  One __syncthreads per column.
-template <int NP>
-__device__ void node_qr(double *Ra, double *Rb, int n, double *red, double *taus) {
-    using NL = NodeLayout<NP>;
-    using Lt = typename NL::Lt;
-    constexpr int CPL = NL::CPL, KR = NL::KR, LD = NL::LD;
-    const int w = Lt::warp(), rph = Lt::rph();
-    double rb[KR][CPL];
-#pragma unroll
-    for (int k = 0; k < KR; ++k)
-#pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) rb[k][cc] = Rb[Lt::col(cc) * LD + NL::row(k)];
+// Ra: smem (ld LDR); lane c holds column c of Rb (rows 0..NPAD-1) in rb.
+// On exit Ra = R (upper), rb = Y1(:, c) (eq. fact_2rs), taus[j].  Loops over Rb
+// rows stop after row j: the triangular zeros are never touched.
+template <class T>
+__device__ __forceinline__ void team_node_qr(double *Ra, double (&rb)[T::NPAD], int n, double *xs, double *red,
+                                             double *taus, double *betas, double *scales) {
+    constexpr int NP = T::NPAD, LDR = T::LDR;
+    const int c = T::col();
+    const bool act = T::grp() == 0;          // row groups > 0 idle (they own the same columns)
+#pragma unroll 1
     for (int j = 0; j < n; ++j) {
-        double *redb = red + (j & 1) * (kWarps * NP);
-        const int cj = j >> 5;
-        const int src = (j & 31) % NL::LC + rph * NL::LC;     // lane owning (my rows, col j)
-        double x[KR];
+        const int b = j & 1;
+        double *xb = xs + b * NP;
+        if (act && c == j) {
 #pragma unroll
-        for (int k = 0; k < KR; ++k) {
-            const double v = __shfl_sync(0xffffffffu, (cj == 0) ? rb[k][0] : rb[k][CPL - 1], src);
-            x[k] = NL::row(k) <= j ? v : 0.0;
-        }
-        double p[CPL], raj[CPL];
+            for (int k = 0; k < NP / 8; ++k) {
+                if (k * 8 > j) break;
 #pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) {
-            double s = 0.0;
-#pragma unroll
-            for (int k = 0; k < KR; ++k) s = fma(x[k], rb[k][cc], s);
-            p[cc] = warp_sum_lpc(s, NL::LC);
-            raj[cc] = Ra[Lt::col(cc) * LD + j];
-        }
-        const double alpha = Ra[j * LD + j];
-        if (rph == 0) {
-#pragma unroll
-            for (int cc = 0; cc < CPL; ++cc) redb[w * NP + Lt::col(cc)] = p[cc];
-        }
-        __syncthreads();
-        const double sig2 = sum_warps(redb, NP, j);
-        const House h = householder(alpha, sig2);
-#pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) {
-            const int c = Lt::col(cc);
-            const double P = sum_warps(redb, NP, c);
-            const double wc = fma(P, h.scale, raj[cc]);
-            const bool trail = (c > j) && (c < n);
-            const double u = trail ? h.tau * h.scale * wc : 0.0;
-#pragma unroll
-            for (int k = 0; k < KR; ++k) rb[k][cc] = fma(-x[k], u, rb[k][cc]);
-            if (c == j) {
-#pragma unroll
-                for (int k = 0; k < KR; ++k) rb[k][cc] = x[k] * h.scale;   // Y1(:, j)
-            }
-            if (w == 0 && rph == 0) {
-                if (trail) Ra[c * LD + j] = raj[cc] - h.tau * wc;
-                else if (c == j) Ra[c * LD + j] = h.beta;
+                for (int q = 0; q < 8; ++q) xb[k * 8 + q] = (k * 8 + q <= j) ? rb[k * 8 + q] : 0.0;
             }
         }
-        if (threadIdx.x == 0) taus[j] = h.tau;
+        team_sync<T::NW>();
+        double p = 0.0, sig2 = 0.0;
+        if (act) p = head_dot<NP>(xb, rb, j);
+        if constexpr (T::NW == 1) {
+            sig2 = __shfl_sync(0xffffffffu, p, j);
+        } else {
+            if (act && c == j) red[b] = p;
+            team_sync<T::NW>();
+            sig2 = red[b];
+        }
+        if (act) {
+            const double alpha = Ra[j * LDR + j];
+            const double RJ = Ra[c * LDR + j];
+            const House h = householder(alpha, sig2);
+            const double w = fma(p, h.scale, RJ);
+            const bool trail = (c > j && c < n);
+            const double u = trail ? h.tau * h.scale * w : 0.0;
+            head_axpy<NP>(xb, u, rb, j);
+            if (trail) Ra[c * LDR + j] = RJ - h.tau * w;
+            if (threadIdx.x == 0) {
+                taus[j] = h.tau;
+                betas[j] = h.beta;
+                scales[j] = h.scale;
+            }
+        }
     }
-    __syncthreads();
+    team_sync<T::NW>();
+    if (act && c < n) {
+        const double sc = scales[c];
 #pragma unroll
-    for (int k = 0; k < KR; ++k)
-#pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) Rb[Lt::col(cc) * LD + NL::row(k)] = rb[k][cc];
-    __syncthreads();
+        for (int i = 0; i < NP; ++i)
+            if (i <= c) rb[i] *= sc;
+        Ra[c * LDR + c] = betas[c];
+    }
+    team_sync<T::NW>();
 }
 
-// Node reflectors applied to the head rows [Ca; Cb] (n x kc each, smem, ld NP+1,
-// kc <= NP columns): eq. localQTupdate one reflector at a time,
-// j ascending (kForward: Q^T, apply stage) or descending (Q, form-Q stage).
-// Y1: smem n x n upper (ld NP+1).  One __syncthreads per reflector.
-template <int NP, bool kForward>
-__device__ void node_apply(const double *Y1, const double *tau, double *Ca, double *Cb, int n,
-                           double *red) {
-    using NL = NodeLayout<NP>;
-    using Lt = typename NL::Lt;
-    constexpr int CPL = NL::CPL, KR = NL::KR, LD = NL::LD;
-    const int w = Lt::warp(), rph = Lt::rph();
-    double cb[KR][CPL];
-#pragma unroll
-    for (int k = 0; k < KR; ++k)
-#pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) cb[k][cc] = Cb[Lt::col(cc) * LD + NL::row(k)];
+// ======================================================= reflector applies
+// Tile reflectors on a team-resident band of C (lane = one C column),
+// j = 0..n-1 (kForward: Q^T, [TR] P:1915-1938) or n-1..0 (Q, form-Q).
+// Ys: smem, column-major (ld yld), unit diagonal and zeros above in place.
+template <class T, bool kForward>
+__device__ __forceinline__ void team_tile_apply(double (&cb)[T::RT], int n, const double *Ys, int yld, const double *tau,
+                                double *red) {
+    constexpr int RT = T::RT, G = T::G, NP = T::NPAD;
+    const int c = T::col(), g = T::grp(), r0 = T::row0();
+#pragma unroll 1
     for (int jj = 0; jj < n; ++jj) {
         const int j = kForward ? jj : n - 1 - jj;
-        double *redb = red + (jj & 1) * (kWarps * NP);
-        double y[KR];
+        const double *x = Ys + j * yld + r0;
+        double P = band_dot<RT>(x, cb);
+        if constexpr (G > 1) {
+            double *rp = red + (jj & 1) * G * NP;
+            rp[g * NP + c] = P;
+            team_sync<T::NW>();
+            P = 0.0;
 #pragma unroll
-        for (int k = 0; k < KR; ++k) y[k] = NL::row(k) <= j ? Y1[j * LD + NL::row(k)] : 0.0;
-        double p[CPL], caj[CPL];
-#pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) {
-            double s = 0.0;
-#pragma unroll
-            for (int k = 0; k < KR; ++k) s = fma(y[k], cb[k][cc], s);
-            p[cc] = warp_sum_lpc(s, NL::LC);
-            caj[cc] = Ca[Lt::col(cc) * LD + j];
+            for (int q = 0; q < G; ++q) P += rp[q * NP + c];
         }
-        if (rph == 0) {
-#pragma unroll
-            for (int cc = 0; cc < CPL; ++cc) redb[w * NP + Lt::col(cc)] = p[cc];
-        }
-        __syncthreads();
-        const double t = tau[j];
-#pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) {
-            const int c = Lt::col(cc);
-            const double P = sum_warps(redb, NP, c);
-            const double u = t * (caj[cc] + P);
-#pragma unroll
-            for (int k = 0; k < KR; ++k) cb[k][cc] = fma(-y[k], u, cb[k][cc]);
-            if (w == 0 && rph == 0) Ca[c * LD + j] = caj[cc] - u;
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int k = 0; k < KR; ++k)
-#pragma unroll
-        for (int cc = 0; cc < CPL; ++cc) Cb[Lt::col(cc) * LD + NL::row(k)] = cb[k][cc];
-    __syncthreads();
-}
-
-// Load / store an n x n upper triangle (head block of a tile) between global
-// (ld) and smem (ld NP+1, zero elsewhere).  Loads are issued all at once
-// (clamped addresses, select after the load) so they overlap.
-template <int NP, bool kCG>
-__device__ __forceinline__ void load_upper(double *sm, const double *g, int64_t ld, int n) {
-    constexpr int PER = (NP * NP + kThreads - 1) / kThreads;
-    double v[PER];
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-        const int e = threadIdx.x + q * kThreads;
-        const int r = e % NP, c = e / NP;
-        const bool ok = e < NP * NP && r <= c && c < n;
-        const double *p = ok ? g + r + (int64_t)c * ld : g;
-        v[q] = kCG ? __ldcg(p) : p[0];
-        v[q] = ok ? v[q] : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-        const int e = threadIdx.x + q * kThreads;
-        if (e < NP * NP) sm[(e / NP) * (NP + 1) + e % NP] = v[q];
+        band_axpy<RT>(x, tau[j] * P, cb);
     }
 }
 
-template <int NP>
-__device__ __forceinline__ void store_upper(const double *sm, double *g, int64_t ld, int n) {
-    for (int e = threadIdx.x; e < n * n; e += kThreads) {
-        const int r = e % n, c = e / n;
-        if (r <= c) g[r + (int64_t)c * ld] = sm[c * (NP + 1) + r];
+// Node reflectors on the head rows [Ca; Cb] (eq. localQTupdate, P:2193-2212,
+// one reflector [e_j; Y1(0:j, j)] at a time).  Y1: smem, column j at Y1 + j*LDY
+// (LDY even: 16-byte aligned columns for the broadcast loads, zeros below the
+// diagonal); Ca: smem, row j of column c at Ca[c*LDC + j] (LDC odd: conflict-free
+// per-lane access); lane c holds column c of Cb (rows 0..NR-1) in cbh.  No
+// synchronisation: every lane touches only its own column.
+template <int NR, int LDY, int LDC, bool kForward>
+__device__ __forceinline__ void team_node_apply(const double *Y1, const double *tau, double *Ca, double (&cbh)[NR],
+                                                int n, int c) {
+    static_assert(LDY % 2 == 0, "Y1 columns are read as double2");
+#pragma unroll 1
+    for (int jj = 0; jj < n; ++jj) {
+        const int j = kForward ? jj : n - 1 - jj;
+        const double *y = Y1 + j * LDY;
+        const double caj = Ca[c * LDC + j];
+        const double u = tau[j] * (caj + head_dot<NR>(y, cbh, j));
+        head_axpy<NR>(y, u, cbh, j);
+        Ca[c * LDC + j] = caj - u;
     }
 }
 
-// Rectangular n x kc block between global and smem (ld NP+1).
-template <int NP, bool kCG>
-__device__ __forceinline__ void load_block(double *sm, const double *g, int64_t ld, int n, int kc) {
-    constexpr int PER = (NP * NP + kThreads - 1) / kThreads;
-    double v[PER];
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-        const int e = threadIdx.x + q * kThreads;
-        const int r = e % NP, c = e / NP;
-        const bool ok = e < NP * NP && r < n && c < kc;
-        const double *p = ok ? g + r + (int64_t)c * ld : g;
-        v[q] = kCG ? __ldcg(p) : p[0];
-        v[q] = ok ? v[q] : 0.0;
-    }
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-        const int e = threadIdx.x + q * kThreads;
-        if (e < NP * NP) sm[(e / NP) * (NP + 1) + e % NP] = v[q];
-    }
-}
-
-template <int NP>
-__device__ __forceinline__ void store_block(const double *sm, double *g, int64_t ld, int n, int kc) {
-    for (int e = threadIdx.x; e < n * kc; e += kThreads) {
-        const int r = e % n, c = e / n;
-        g[r + (int64_t)c * ld] = sm[c * (NP + 1) + r];
-    }
-}
-
-// Ticket of the single-pass tree: returns true if this CTA is the second (last)
+// Ticket of the single-pass tree: true if this CTA is the second (last)
 // arriver at node p and must run it.  Writers fence their global stores first.
+template <int NW>
 __device__ __forceinline__ bool ticket(int *counters, int p, int *flag_smem) {
     __threadfence();
-    __syncthreads();
+    team_sync<NW>();
     if (threadIdx.x == 0) {
         const int old = atomicAdd(counters + p, 1);
         if (old == 1) counters[p] = 0;        // both arrived: reset for the next call
         *flag_smem = old;
     }
-    __syncthreads();
+    team_sync<NW>();
     const bool last = (*flag_smem == 1);
     if (last) __threadfence();
     return last;

@@ -3,44 +3,30 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
-namespace tsqr {
-
-struct DevPlan;
-
-// Columns of C one apply CTA keeps in registers per chunk: the C staging buffer
-// (S x KC doubles) must fit next to the S x NP Y tile in shared memory.
-template <int NP, int RT>
-struct ApplyKC {
-    static constexpr int S = (NP < 32 ? 32 / NP : 1) * RT * 8;
-    static constexpr int byS = 8192 / S;
-    static constexpr int a = NP < 32 ? NP : 32;
-    static constexpr int value = a < byS ? a : byS;
-};
-
-struct FactorArgsBase {
-    int NP = 64;
-    int64_t max_rows = 0;
-};
-
-}  // namespace tsqr
-
 #include "tsqr_device.cuh"
 
 namespace tsqr {
 
-struct FactorArgs : FactorArgsBase {
+// Rows one team holds for the tallest tile of a plan (64, 96, 128 or 192).
+int team_rows_for(int64_t max_rows);
+
+struct FactorArgs {
+    int NP = 64;                 // n padded to 16/32/64 (<= 32: one column warp)
+    int64_t max_rows = 0;        // tallest tile
     double *A; int64_t lda; int n;
     DevPlan plan;
     double *tau_tile, *tau_node; int *counters;
     double *R; int64_t ldr;
 };
 
-struct ApplyArgs : FactorArgsBase {
+struct ApplyArgs {
+    int NP = 64;
+    int64_t max_rows = 0;
     const double *A; int64_t lda; int n;
     DevPlan plan;
     const double *tau_tile, *tau_node; int *counters;
     double *C; int64_t ldc; int k;
-    int form_q;            // 1: form-Q leaf stage (C := Q, columns = n) using xbuf
+    int form_q;                  // 1: form-Q leaf stage (C := Q, n columns) from xbuf
     const double *xbuf;
 };
 

@@ -42,9 +42,10 @@ def _oracle_nodes(p):
 
 
 @pytest.mark.parametrize("m,n,b,s", [
-    (4096, 16, 512, 512), (1_000_000, 50, 4096, 256), (100_000, 64, 2048, 256), (5000, 50, 4096, 256),
-    (1010, 16, 500, 200), (1020, 16, 500, 200), (64, 64, 64, 64), (3000, 24, 700, 256), (777, 5, 100, 30),
-    (33_554_432 // 64, 32, 4096, 512),
+    (4096, 16, 512, 128), (1_000_000, 50, 4096, 96), (100_000, 64, 2048, 96), (5000, 50, 4096, 192),
+    (1010, 16, 500, 190), (1020, 16, 500, 190), (64, 64, 64, 64), (3000, 24, 700, 175), (777, 5, 100, 30),
+    (100, 40, 100, 30), (8 * 4096 + 100, 64, 4096, 96),
+    (33_554_432 // 64, 32, 4096, 96),
 ])
 def test_plan_matches_oracle(m, n, b, s):
     e = T.plan_export(m, n, block_rows=b, tile_rows=s)
@@ -60,7 +61,7 @@ def test_plan_matches_oracle(m, n, b, s):
 @pytest.mark.parametrize("m,n,b,G", [(1_000_000, 50, 4096, 8), (100_000, 64, 2048, 4), (33_554_432, 32, 4096, 8),
                                      (4096 * 3 + 20, 16, 4096, 2), (5000, 8, 100, 16), (5000, 40, 100, 16)])
 def test_slabs_match_oracle_ranks(m, n, b, G):
-    s = min(256, b)
+    s = min(192, b)
     p = orc.plan(m, n, b, s, G)
     for r in range(G):
         row0, ml = T.slab(m, n, b, G, r)
@@ -112,10 +113,10 @@ def test_factor_validation_without_gpu():
     assert _factor_status(100, 10, fake, 99, None, 0, o)[0] == 1         # lda < m
     assert _factor_status(100, 10, fake, 100, fake, 9, o)[0] == 1        # ldr < n
     assert _factor_status(100, 10, fake, 100, None, 0, T.api.opts(block_rows=64, tile_rows=5000))[0] == 3
-    assert _factor_status(100, 40, fake, 100, None, 0, T.api.opts(block_rows=64, tile_rows=30))[0] == 2
+    assert _factor_status(100, 40, fake, 100, None, 0, T.api.opts(block_rows=30, tile_rows=30))[0] == 2  # block < n
     assert _factor_status(1000, 10, fake, 1000, None, 0, T.api.opts(block_rows=64, nranks=3))[0] == 3
     with pytest.raises(_lib.TsqrError):
-        T.plan_info(100, 10, block_rows=64, tile_rows=7)
+        T.plan_info(100, 10, block_rows=64, tile_rows=500)
 
 
 def test_apply_validation_without_gpu():

@@ -269,9 +269,14 @@ def test_plan_remainder_rules():
     assert list(p.tile_rows) == [167, 167, 166, 170, 170, 170]
     p = orc.plan(1000 + 16, 16, 500)
     assert list(p.tile_rows) == [500, 500, 16]
+    # s < n: tiles are never shorter than n (t = min(ceil(h/s), floor(h/n)))
+    p = orc.plan(100, 40, 100, 30)
+    assert list(p.tile_rows) == [50, 50]
+    p = orc.plan(100, 64, 100, 96)
+    assert list(p.tile_rows) == [100]
 
 
-@pytest.mark.parametrize("args", [(5, 8, 4, 4, 1), (64, 8, 16, 16, 3), (64, 8, 32, 32, 4), (64, 8, 16, 4, 1)])
+@pytest.mark.parametrize("args", [(5, 8, 4, 4, 1), (64, 8, 16, 16, 3), (64, 8, 32, 32, 4), (64, 8, 4, 4, 1)])
 def test_plan_rejects(args):
     with pytest.raises(ValueError):
         orc.plan(*args[:3], s=args[3], G=args[4])
