@@ -49,41 +49,47 @@ __device__ __forceinline__ void team_sync() {
 }
 
 // ----------------------------------------------------------- register access
-// Runtime-indexed access to a register band: a jump table (BRX) on a
-// warp-uniform index (the column step j), a handful of instructions.
-#define TSQR_C8(b)                                      \
-    case b + 0: TSQR_OP(b + 0);                         \
-    case b + 1: TSQR_OP(b + 1);                         \
-    case b + 2: TSQR_OP(b + 2);                         \
-    case b + 3: TSQR_OP(b + 3);                         \
-    case b + 4: TSQR_OP(b + 4);                         \
-    case b + 5: TSQR_OP(b + 5);                         \
-    case b + 6: TSQR_OP(b + 6);                         \
-    case b + 7: TSQR_OP(b + 7);
-#define TSQR_C128 TSQR_C8(0) TSQR_C8(8) TSQR_C8(16) TSQR_C8(24) TSQR_C8(32) TSQR_C8(40) TSQR_C8(48) \
-    TSQR_C8(56) TSQR_C8(64) TSQR_C8(72) TSQR_C8(80) TSQR_C8(88) TSQR_C8(96) TSQR_C8(104) TSQR_C8(112) TSQR_C8(120)
+// Runtime-indexed access to a register band on a warp-uniform index (the column
+// step j): one switch over 8-row chunks, then branch-free selects inside the
+// chunk (no per-row jump tables, no local memory).
+template <int B, int N>
+__device__ __forceinline__ double sel8(const double (&a)[N], int lo) {
+    double r = a[B];
+#pragma unroll
+    for (int q = 1; q < 8; ++q)
+        if (B + q < N) r = (lo == q) ? a[B + q < N ? B + q : 0] : r;
+    return r;
+}
+template <int B, int N>
+__device__ __forceinline__ void sub8(double (&a)[N], int lo, double v) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+        if (B + q < N) a[B + q < N ? B + q : 0] -= (lo == q) ? v : 0.0;
+}
+
+#define TSQR_CHUNKS(OP)                                                                       \
+    switch (i >> 3) {                                                                         \
+        case 0: OP(0); case 1: OP(8); case 2: OP(16); case 3: OP(24); case 4: OP(32);         \
+        case 5: OP(40); case 6: OP(48); case 7: OP(56); case 8: OP(64); case 9: OP(72);       \
+        case 10: OP(80); case 11: OP(88); case 12: OP(96); case 13: OP(104); case 14: OP(112); \
+        case 15: OP(120);                                                                     \
+        default: break;                                                                       \
+    }
 
 template <int N>
 __device__ __forceinline__ double reg_get(const double (&a)[N], int i) {
-    static_assert(N <= 128, "jump table covers 128 registers");
-#define TSQR_OP(q) return a[(q) < N ? (q) : 0]
-    switch (i) {
-        TSQR_C128
-        default: return 0.0;
-    }
-#undef TSQR_OP
+    static_assert(N <= 128, "covers 128 registers");
+#define TSQR_G(b) if constexpr ((b) < N) return sel8<((b) < N ? (b) : 0), N>(a, i & 7); else return 0.0
+    TSQR_CHUNKS(TSQR_G)
+#undef TSQR_G
+    return 0.0;
 }
 
 template <int N>
 __device__ __forceinline__ void reg_sub(double (&a)[N], int i, double v) {
-#define TSQR_OP(q)                              \
-    if ((q) < N) a[(q) < N ? (q) : 0] -= v;     \
-    return
-    switch (i) {
-        TSQR_C128
-        default: return;
-    }
-#undef TSQR_OP
+#define TSQR_S(b) if constexpr ((b) < N) { sub8<((b) < N ? (b) : 0), N>(a, i & 7, v); return; } else return
+    TSQR_CHUNKS(TSQR_S)
+#undef TSQR_S
 }
 
 // ------------------------------------------------------------------ staging
@@ -239,9 +245,13 @@ __device__ __forceinline__ void head_axpy(const double *x, double u, double (&a)
 //     = v^T A(:, c), then A(:, c) -= x (tau scale w_c) and A(j, c) -= tau w_c.
 // Column j stays in place and becomes (beta, v = scale x) once at the end.
 // Smem: xs[2][S]; red[2][2][G][NPAD] (NW > 1); alph[2]; taus/betas/scales[NPAD].
-template <class T>
-__device__ __forceinline__ void team_tile_qr(double (&a)[T::RT], int n, double *xs, double *red, double *alph, double *taus,
-                             double *betas, double *scales) {
+struct NoProbe {
+    __device__ static void mark(int, int) {}
+};
+
+template <class T, class Probe = NoProbe>
+__device__ __forceinline__ void team_tile_qr(double (&a)[T::RT], int n, double *xs, double *red, double *alph,
+                                             double *taus, double *betas, double *scales) {
     constexpr int RT = T::RT, S = T::S, G = T::G, NP = T::NPAD;
     const int c = T::col(), g = T::grp(), r0 = T::row0();
 #pragma unroll 1
@@ -249,23 +259,30 @@ __device__ __forceinline__ void team_tile_qr(double (&a)[T::RT], int n, double *
         const int b = j & 1;
         double *xb = xs + b * S;
         const int gj = j / RT, ij = j - gj * RT;
-        // 1. publish the pivot column
-        if (c == j) {
+        Probe::mark(j, 0);
+        // 1. publish the pivot column: the owner lane stores its band unmasked
+        //    (16-byte stores, no per-element predicates), then its warp zeroes
+        //    rows <= j in parallel.  Warp-uniform branch: only the owner's warp.
+        if ((T::warp() % T::CW) == (j >> 5)) {
             double *xg = xb + r0;
-            if (r0 > j) {
+            if (T::lane() == (j & 31)) {
 #pragma unroll
                 for (int i = 0; i < RT; i += 2)
                     *reinterpret_cast<double2 *>(xg + i) = make_double2(a[i], a[i + 1]);
-            } else {
-#pragma unroll
-                for (int i = 0; i < RT; ++i) xg[i] = (r0 + i > j) ? a[i] : 0.0;
-                if (g == gj) alph[b] = reg_get(a, ij);
+            }
+            if (r0 <= j) {
+                __syncwarp();
+                const int hi = j - r0 < RT - 1 ? j - r0 : RT - 1;
+                for (int r = T::lane(); r <= hi; r += 32) xg[r] = 0.0;
             }
         }
+        Probe::mark(j, 1);
         team_sync<T::NW>();
+        Probe::mark(j, 2);
         // 2. partial inner products over my band
         const double p = band_dot<RT>(xb + r0, a);
         const double rj = (g == gj) ? reg_get(a, ij) : 0.0;     // A(j, c)
+        Probe::mark(j, 3);
         double P, RJ, sig2, alpha;
         if constexpr (T::NW == 1) {
             P = p;
@@ -280,20 +297,25 @@ __device__ __forceinline__ void team_tile_qr(double (&a)[T::RT], int n, double *
             P = 0.0;
             RJ = 0.0;
             sig2 = 0.0;
+            alpha = 0.0;
 #pragma unroll
             for (int q = 0; q < G; ++q) {
                 P += rp[q * NP + c];
                 RJ += rr[q * NP + c];
                 sig2 += rp[q * NP + j];
+                alpha += rr[q * NP + j];
             }
-            alpha = alph[b];
         }
+        Probe::mark(j, 4);
         // 3. reflector and rank-1 update
         const House h = householder(alpha, sig2);
         const double w = fma(P, h.scale, RJ);                     // v^T A(:, c)
         const double u = (c > j && c < n) ? h.tau * h.scale * w : 0.0;
+        Probe::mark(j, 5);
         band_axpy<RT>(xb + r0, u, a);
+        Probe::mark(j, 6);
         if (g == gj) reg_sub(a, ij, (alpha - h.beta) * u);        // A(j,c) -= tau w_c
+        Probe::mark(j, 7);
         if (threadIdx.x == 0) {
             taus[j] = h.tau;
             betas[j] = h.beta;
