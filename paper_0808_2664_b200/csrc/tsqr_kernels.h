@@ -3,9 +3,17 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
-#include "tsqr_device.cuh"
 
 namespace tsqr {
+
+struct DevPlan {
+    const int64_t *tile_row0;   // first local row of tile t
+    const int *tile_rows;       // rows of tile t
+    const int *tile_parent;     // node id of leaf t's first combine, -1: none
+    const int *node_a;          // by node id b: leftmost tile of the left subtree
+    const int *node_parent;     // by node id: next node, -1: local root
+    int L;                      // tiles
+};
 
 // Rows one team holds for the tallest tile of a plan (64, 96, 128 or 192).
 int team_rows_for(int64_t max_rows);
@@ -36,8 +44,6 @@ cudaError_t launch_formq_nodes(int NP, const double *A, int64_t lda, int n, cons
                                const double *tau_node, const int *ids, int count, double *xbuf,
                                cudaStream_t st);
 cudaError_t launch_identity(double *X, int n, cudaStream_t st);
-cudaError_t launch_write_r(int NP, const double *A, int64_t lda, int n, double *R, int64_t ldr,
-                           cudaStream_t st);
 cudaError_t launch_pack_r(const double *A, int64_t lda, int n, double *packed, cudaStream_t st);
 cudaError_t launch_copy_block(const double *src, int64_t lds, double *dst, int64_t ldd, int n, int k,
                               cudaStream_t st);

@@ -1,0 +1,279 @@
+// Blocked compact-WY engine of the B200 TSQR path (sm_100a).  Product code.
+//
+// A "tile" is an S x NP fp64 block in shared memory, column-major with leading
+// dimension ld (ld = 2 mod 16: conflict-free DMMA fragment loads).  Its columns
+// are processed in panels of 8 (DMMA m8n8k4 granularity):
+//
+//  * panel_qr   one warp factors the panel (8 columns x the active rows) in
+//               registers with unblocked Householder steps whose reductions are
+//               warp shuffles only (Alg. QR:qnxn / DGEQR2 order, reflector by
+//               reflector); it writes the panel's Y (unit diagonal, zeros above)
+//               to Ys and taus/betas;
+//  * build_t    T of the panel from its Gram matrix G = Y^T Y (one DMMA per 4
+//               rows) and the recurrence of Alg. YT:scaled in the
+//               LAPACK sign (reading R3): H_0...H_7 = I - Y T Y^T;
+//  * wy_update  C <- (I - Y T^T Y^T) C (kTrans, applying Q^T) or
+//               C <- (I - Y T Y^T) C (applying Q), as W = Y^T C, W <- T^(T) W,
+//               C -= Y W on FP64 DMMA; each warp handles its own 8-column blocks
+//               of C, so no cross-warp reduction is needed.
+//
+// Rows: the active rows of a panel are given as a list of 8-row blocks: a
+// dense tile uses blocks p.. (rows below the panel's first pivot), a
+// structured node [R_a; R_b] (Alg. QR:qnxn, eq. fact_2rs) uses block p of R_a
+// and blocks 0..p of R_b, so the triangular zeros are never touched.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tsqr {
+namespace wy {
+
+// D += A B for one 8x8x4 fp64 MMA (SASS DMMA.8x8x4).  Fragments (lane i):
+// A[i/4][i%4], B[k=i%4][n=i/4], C/D[i/4][2(i%4)+{0,1}].
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double rcp_nr(double d) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+    double e = fma(-d, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-d, y, 1.0);
+    return fma(y, e, y);
+}
+
+// dlarfg scalars (readings R1/R2): beta = -sign(alpha) N, N = sqrt(alpha^2 +
+// sigma2), tau = 1 + |alpha|/N, scale = 1/(alpha - beta); sigma2 == 0 -> H = I.
+struct House {
+    double beta, tau, scale;
+};
+__device__ __forceinline__ House householder(double alpha, double sigma2) {
+    House h;
+    if (sigma2 == 0.0) {
+        h.beta = alpha;
+        h.tau = 0.0;
+        h.scale = 0.0;
+    } else {
+        const double y = fma(alpha, alpha, sigma2);
+        const double r = rsqrt(y);
+        const double N = y * r;
+        const double aa = fabs(alpha);
+        h.beta = alpha >= 0.0 ? -N : N;
+        h.tau = fma(aa, r, 1.0);
+        const double inv = rcp_nr(aa + N);
+        h.scale = alpha >= 0.0 ? inv : -inv;
+    }
+    return h;
+}
+
+// Active 8-row blocks of panel p: dense (blocks p .. nrb-1) or structured node
+// (block p of R_a, then blocks na .. na+p of R_b).
+struct Rows {
+    int p, nrb, na;      // na < 0: dense
+    __device__ int count() const { return na < 0 ? nrb - p : p + 2; }
+    __device__ int block(int k) const { return na < 0 ? p + k : (k == 0 ? p : na + k - 1); }
+};
+
+// ------------------------------------------------------------------ panel QR
+// Factor columns 8p .. 8p+7 (those < n) of the tile over the active rows.
+// Lane i = 4 cl + q holds column 8p + cl, rows 8 block(k) + 2q + {0,1}.
+// On exit the tile holds R (rows <= pivot) and the reflector entries v (below)
+// in place; Ys (ld ldy) holds Y of the panel (unit diagonal, zeros above,
+// zeros outside the active rows); taus[8p..], betas[8p..] are set.
+template <int KMAX>
+__device__ __forceinline__ void panel_qr(double *tile, int ld, int n, const Rows &rows, double *Ys, int ldy,
+                                         double *taus, double *betas) {
+    const int lane = threadIdx.x & 31, cl = lane >> 2, q = lane & 3;
+    const int p = rows.p, cnt = rows.count();
+    const int col = 8 * p + cl;
+    double pv[KMAX][2];
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+        pv[k][0] = pv[k][1] = 0.0;
+        if (k < cnt) {
+            const double2 v = *reinterpret_cast<const double2 *>(tile + col * ld + 8 * rows.block(k) + 2 * q);
+            pv[k][0] = v.x;
+            pv[k][1] = v.y;
+        }
+    }
+    double scl = 0.0;
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+        const int j = 8 * p + jj;
+        if (j >= n) break;                                   // warp-uniform
+        const int src = 4 * jj + q;                          // owner of column j, same rows
+        // rows <= j of the pivot block are not part of the reflector's tail
+        const bool m0 = 2 * q > jj, m1 = 2 * q + 1 > jj;
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+            if (k < cnt) {
+                double x0 = __shfl_sync(0xffffffffu, pv[k][0], src);
+                double x1 = __shfl_sync(0xffffffffu, pv[k][1], src);
+                if (k == 0) {
+                    x0 = m0 ? x0 : 0.0;
+                    x1 = m1 ? x1 : 0.0;
+                }
+                d0 = fma(x0, pv[k][0], d0);
+                d1 = fma(x1, pv[k][1], d1);
+            }
+        double d = d0 + d1;
+        d += __shfl_xor_sync(0xffffffffu, d, 1);
+        d += __shfl_xor_sync(0xffffffffu, d, 2);             // x^T A(:, col)
+        const double sig2 = __shfl_sync(0xffffffffu, d, 4 * jj);
+        const double rj = __shfl_sync(0xffffffffu, pv[0][jj & 1], 4 * cl + (jj >> 1));   // A(j, col)
+        const double alpha = __shfl_sync(0xffffffffu, rj, 4 * jj);
+        const House h = householder(alpha, sig2);
+        const double w = fma(d, h.scale, rj);                // v^T A(:, col)
+        const double u = (cl > jj && col < n) ? h.tau * h.scale * w : 0.0;
+        // the rank-1 update re-fetches x by shuffle (keeps the panel in 2 KMAX registers)
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+            if (k < cnt) {
+                double x0 = __shfl_sync(0xffffffffu, pv[k][0], src);
+                double x1 = __shfl_sync(0xffffffffu, pv[k][1], src);
+                if (k == 0) {
+                    x0 = m0 ? x0 : 0.0;
+                    x1 = m1 ? x1 : 0.0;
+                }
+                pv[k][0] = fma(-x0, u, pv[k][0]);
+                pv[k][1] = fma(-x1, u, pv[k][1]);
+            }
+        if (q == (jj >> 1)) pv[0][jj & 1] -= (alpha - h.beta) * u;   // A(j, col) -= tau w
+        if (cl == jj) scl = h.scale;
+        if (lane == 0) {
+            taus[j] = h.tau;
+            betas[j] = h.beta;
+        }
+    }
+    __syncwarp();
+    // the pivot column of each reflector becomes (beta, v = scale * x): rows > pivot
+    if (col < n) {
+        const double be = betas[col];
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+            if (k < cnt) {
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    if (k == 0) {
+                        const int r = 2 * q + e;              // row 8p + r of the pivot block
+                        pv[0][e] = r > cl ? pv[0][e] * scl : (r == cl ? be : pv[0][e]);
+                    } else {
+                        pv[k][e] *= scl;
+                    }
+                }
+            }
+    }
+    // back to the tile, and the panel's Y (unit lower, zeros above) to Ys
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k)
+        if (k < cnt) {
+            const int rb = rows.block(k);
+            *reinterpret_cast<double2 *>(tile + col * ld + 8 * rb + 2 * q) = make_double2(pv[k][0], pv[k][1]);
+            double y0 = pv[k][0], y1 = pv[k][1];
+            if (k == 0) {
+                const int r0 = 2 * q, r1 = 2 * q + 1;
+                y0 = r0 > cl ? y0 : (r0 == cl ? 1.0 : 0.0);
+                y1 = r1 > cl ? y1 : (r1 == cl ? 1.0 : 0.0);
+            }
+            if (col >= n) y0 = y1 = 0.0;
+            *reinterpret_cast<double2 *>(Ys + cl * ldy + 8 * rb + 2 * q) = make_double2(y0, y1);
+        }
+}
+
+// ------------------------------------------------------------------ T factor
+// T (8x8, row-major Ts[r*8 + c]) of the panel whose Y is in Ys (rows given by
+// `rows`) and taus t[0..8): G = Y^T Y by DMMA, then for c = 1..7, row r < c:
+// T(r,c) = -tau_c sum_{l=r}^{c-1} T(r,l) G(l,c), T(c,c) = tau_c.  One warp.
+__device__ __forceinline__ void build_t(const double *Ys, int ldy, const Rows &rows, const double *t, double *Gs,
+                                        double *Ts) {
+    const int lane = threadIdx.x & 31;
+    double g0 = 0.0, g1 = 0.0;
+    const int cnt = rows.count();
+    for (int k = 0; k < cnt; ++k) {
+        const int rb = rows.block(k);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const double a = Ys[(lane >> 2) * ldy + 8 * rb + 4 * e + (lane & 3)];
+            dmma(g0, g1, a, a);
+        }
+    }
+    Gs[(lane >> 2) * 8 + 2 * (lane & 3)] = g0;
+    Gs[(lane >> 2) * 8 + 2 * (lane & 3) + 1] = g1;
+    __syncwarp();
+    if (lane < 8) {
+        const int r = lane;
+        double row[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) row[c] = 0.0;
+        row[r < 8 ? r : 0] = t[r];
+#pragma unroll
+        for (int c = 1; c < 8; ++c) {
+            if (r < c) {
+                double s = 0.0;
+#pragma unroll
+                for (int l = 0; l < c; ++l)
+                    if (l >= r) s = fma(row[l], Gs[l * 8 + c], s);
+                row[c] = -t[c] * s;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 8; ++c) Ts[r * 8 + c] = row[c];
+    }
+    __syncwarp();
+}
+
+// ------------------------------------------------------------------ update
+// For the calling warp's column block cb of C (columns 8cb..8cb+7, ld ldc):
+// C <- (I - Y op(T) Y^T) C over the active rows, op(T) = T^T (kTrans: Q^T) or T.
+// Wb: 8x8 per-warp scratch (row-major, stride 9).
+template <bool kTrans>
+__device__ __forceinline__ void wy_update_block(double *C, int ldc, int cb, const double *Ys, int ldy,
+                                                const Rows &rows, const double *Ts, double *Wb) {
+    const int lane = threadIdx.x & 31, lq = lane & 3, l4 = lane >> 2;
+    const int cnt = rows.count();
+    // W = Y^T C  (8 reflectors x 8 columns)
+    double w0 = 0.0, w1 = 0.0;
+    const double *cc = C + (8 * cb + l4) * ldc;
+    for (int k = 0; k < cnt; ++k) {
+        const int rb = rows.block(k);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int r = 8 * rb + 4 * e + lq;
+            dmma(w0, w1, Ys[l4 * ldy + r], cc[r]);
+        }
+    }
+    Wb[l4 * 9 + 2 * lq] = w0;
+    Wb[l4 * 9 + 2 * lq + 1] = w1;
+    __syncwarp();
+    // W' = op(T) W
+    double v0 = 0.0, v1 = 0.0;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const int kk = 4 * e + lq;
+        const double a = kTrans ? Ts[kk * 8 + l4] : Ts[l4 * 8 + kk];
+        dmma(v0, v1, a, Wb[kk * 9 + l4]);
+    }
+    __syncwarp();
+    Wb[l4 * 9 + 2 * lq] = v0;
+    Wb[l4 * 9 + 2 * lq + 1] = v1;
+    __syncwarp();
+    // C -= Y W'   as  C^T -= W'^T Y^T  (accumulator = C^T block: lane holds
+    // column 8cb + l4, rows 8rb + 2lq + {0,1})
+    const double a0 = -Wb[(lq) * 9 + l4], a1 = -Wb[(4 + lq) * 9 + l4];
+    double *cw = C + (8 * cb + l4) * ldc;
+    for (int k = 0; k < cnt; ++k) {
+        const int rb = rows.block(k);
+        double2 c2 = *reinterpret_cast<const double2 *>(cw + 8 * rb + 2 * lq);
+        dmma(c2.x, c2.y, a0, Ys[(lq)*ldy + 8 * rb + l4]);
+        dmma(c2.x, c2.y, a1, Ys[(4 + lq) * ldy + 8 * rb + l4]);
+        *reinterpret_cast<double2 *>(cw + 8 * rb + 2 * lq) = c2;
+    }
+    __syncwarp();
+}
+
+}  // namespace wy
+}  // namespace tsqr
