@@ -1,10 +1,10 @@
 // Kernels of the B200 TSQR hot path (sm_100a) on the blocked compact-WY engine
 // (wy.cuh) and their host launchers.  Product code.
 //
-//  k_factor      (a2)+(a3)+(a4)+(a6): one CTA per tile: panel QR (one warp,
-//                shuffles) -> T (a3) -> DMMA trailing update, panel by panel;
-//                then the single-pass ticketed tree: the second CTA to finish
-//                below a node runs the structured combine of [R_a; R_b]
+//  k_factor_w    (a2)+(a3)+(a4)+(a6): one warp per tile: panel QR (shuffles,
+//                Gram on the fly) -> T (a3) -> DMMA trailing update, panel by
+//                panel; then the single-pass ticketed tree: the second warp to
+//                finish below a node runs the structured combine of [R_a; R_b]
 //                (Alg. QR:qnxn on the same engine, structured row blocks) and
 //                climbs; the root writes R.
 //  k_apply_qt    (a7)+(a8): C <- Q_tile^T C panel by panel (W = Y^T C,
@@ -51,6 +51,8 @@ __device__ __forceinline__ void cp_async8(double *sm, const double *g, bool vali
                  : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
 // global (rows x ncols, ldg) -> smem (cap_rows x cap_cols, lds), zero padded.
 template <int NT>
@@ -92,7 +94,7 @@ __device__ __forceinline__ void blocked_qr(double *sm, int n, int rows) {
     zero<G::NT>(sm + SM::taus, G::NP);      // padding reflectors (columns >= n) stay H = I
     __syncthreads();
     for (int p = 0; p < npan; ++p) {
-        const wy::Rows R{p, nrb, kNode ? G::NCB : -1};
+        const wy::Rows R{p, nrb, kNode ? G::NCB : -1, p};
         if (warp == p % G::NW) {
             if (p > 0) {
                 const int lane = threadIdx.x & 31;
@@ -118,7 +120,7 @@ __device__ __forceinline__ void build_all_t(double *sm, int n, int rows) {
     const int warp = threadIdx.x >> 5;
     const int npan = (n + 7) / 8, nrb = (rows + 7) / 8;
     for (int p = warp; p < npan; p += G::NW) {
-        const wy::Rows R{p, nrb, kNode ? G::NCB : -1};
+        const wy::Rows R{p, nrb, kNode ? G::NCB : -1, p};
         wy::build_t(sm + SM::ys + 8 * p * G::LD, G::LD, R, sm + SM::taus + 8 * p, sm + SM::gs + 64 * warp,
                     sm + SM::ts + 64 * p);
     }
@@ -134,7 +136,7 @@ __device__ __forceinline__ void apply_panels(double *sm, int n, int rows, int kc
     const int npan = (n + 7) / 8, nrb = (rows + 7) / 8, ncb = (kcols + 7) / 8;
     for (int pp = 0; pp < npan; ++pp) {
         const int p = kFwd ? pp : npan - 1 - pp;
-        const wy::Rows R{p, nrb, kNode ? G::NCB : -1};
+        const wy::Rows R{p, nrb, kNode ? G::NCB : -1, p};
         for (int cb = warp; cb < ncb; cb += G::NW)
             wy::wy_update_block<kFwd>(sm + SM::tile, G::LD, cb, sm + SM::ys + 8 * p * G::LD, G::LD, R,
                                       sm + SM::ts + 64 * p, sm + SM::wb + 72 * warp);
@@ -174,59 +176,160 @@ __device__ __forceinline__ void load_node_y(double *Ys, const double *y1, int64_
     }
 }
 
-// ============================================================== factor (a2-a4)
+// ===================================================== factor, warp per tile
+// One warp owns one tile and the chain of Householder steps through it: the
+// panel chain (latency-bound) of many tiles then overlaps on each SM with no
+// block barriers.  Node combines stream R_a row block p through two 8-row
+// slots under R_b (rows [0, NP) = R_b, rows [NP, NP+16) = R_a blocks p and
+// p+1, the next one loaded into registers while panel p updates), so a node
+// needs NP + 16 rows of shared memory instead of 2 NP.
+template <int NCB_, int NRB_>
+struct WGeo {
+    static constexpr int NCB = NCB_, NRB = NRB_;
+    static constexpr int NP = 8 * NCB, S = 8 * NRB;
+    static constexpr int NROWS = S > NP + 16 ? S : NP + 16;
+    static constexpr int LD = ((NROWS + 13) / 16) * 16 + 2;     // = 2 mod 16
+    static constexpr int KMAX = NRB > NCB + 1 ? NRB : NCB + 1;
+    static constexpr int NB = 4;                                // update blocks per pass
+};
+
 template <class G>
-__global__ void __launch_bounds__(G::NT)
-k_factor(double *A, int64_t lda, int n, DevPlan plan, double *tau_tile, double *tau_node, int *counters, double *R,
-         int64_t ldr) {
-    using SM = Smem<G, G::NP, 8>;
+struct WSmem {
+    static constexpr int tile = 0;                              // NP x LD
+    static constexpr int ys = tile + G::NP * G::LD;             // 8 x LD (one panel)
+    static constexpr int ts = ys + 8 * G::LD;                   // 64
+    static constexpr int gs = ts + 64;                          // 64
+    static constexpr int wb = gs + 64;                          // 72 NB
+    static constexpr int taus = wb + 72 * G::NB;                // NP
+    static constexpr int betas = taus + G::NP;                  // NP
+    static constexpr size_t bytes = (size_t)(betas + G::NP) * sizeof(double);
+};
+
+// Householder QR of the warp's tile (dense, nrb row blocks) or of the node
+// [R_a; R_b] (kNode: R_b in rows [0, NP), R_a read and written at Ra in global
+// memory one row block per panel through the slot).
+// R_a rows 8pp..8pp+7 (upper part, zero below the diagonal), one warp: lane
+// element e = lane + 32 i, i < 16, of the 8 x (NP - 8pp) block.  L2 loads
+// (ld.global.cg): the heads are written by warps on other SMs and L1 is not
+// coherent.
+template <class G>
+__device__ __forceinline__ void slot_fetch(double (&v)[16], const double *Ra, int64_t lda, int n, int pp) {
+    const int lane = threadIdx.x & 31, w = G::NP - 8 * pp;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int e = lane + 32 * i, c = 8 * pp + (e >> 3), r = 8 * pp + (e & 7);
+        const bool ok = e < 8 * w && r <= c && c < n;
+        v[i] = ok ? __ldcg(Ra + r + (int64_t)c * lda) : 0.0;
+    }
+}
+template <class G>
+__device__ __forceinline__ void slot_put(const double (&v)[16], double *tile, int pp) {
+    const int lane = threadIdx.x & 31, w = G::NP - 8 * pp, slot = G::NP + 8 * (pp & 1);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+        const int e = lane + 32 * i;
+        if (e < 8 * w) tile[(8 * pp + (e >> 3)) * G::LD + slot + (e & 7)] = v[i];
+    }
+}
+
+template <class G, bool kNode>
+__device__ __forceinline__ void warp_qr(double *sm, int n, int nrb, double *Ra, int64_t lda) {
+    using SM = WSmem<G>;
+    const int lane = threadIdx.x & 31;
+    double *tile = sm + SM::tile, *Ys = sm + SM::ys;
+    const int npan = (n + 7) / 8;
+    double nxt[16];
+    if (kNode) {
+        slot_fetch<G>(nxt, Ra, lda, n, 0);
+        slot_put<G>(nxt, tile, 0);
+        __syncwarp();
+    }
+    for (int p = 0; p < npan; ++p) {
+        const int slot = G::NP + 8 * (p & 1);
+        const wy::Rows R = kNode ? wy::Rows{p, nrb, 0, slot / 8} : wy::Rows{p, nrb, -1, p};
+        wy::panel_qr<G::KMAX>(tile, G::LD, n, R, Ys, G::LD, sm + SM::taus, sm + SM::betas, sm + SM::gs);
+        __syncwarp();
+        if (kNode && p + 1 < npan) slot_fetch<G>(nxt, Ra, lda, n, p + 1);   // in flight during T + update
+        wy::build_t_gram(sm + SM::gs, sm + SM::taus + 8 * p, sm + SM::ts);
+        for (int cb = p + 1; cb < npan; cb += G::NB)
+            wy::wy_update_multi<true, G::NB>(tile, G::LD, cb, min(G::NB, npan - cb), Ys, G::LD, R, sm + SM::ts,
+                                              sm + SM::wb);
+        if (kNode) {                                   // R rows 8p..8p+7 of the merged subtree
+            const int w = n - 8 * p;
+            for (int e = lane; e < 8 * w; e += 32) {
+                const int i = e & 7, c = 8 * p + (e >> 3), r = 8 * p + i;
+                if (r <= c) Ra[r + (int64_t)c * lda] = tile[c * G::LD + slot + i];
+            }
+            if (p + 1 < npan) slot_put<G>(nxt, tile, p + 1);
+            __syncwarp();
+        }
+    }
+}
+
+template <class G>
+__global__ void __launch_bounds__(32)
+k_factor_w(double *A, int64_t lda, int n, DevPlan plan, double *tau_tile, double *tau_node, int *counters, double *R,
+           int64_t ldr) {
+    using SM = WSmem<G>;
     extern __shared__ __align__(16) double sm[];
-    int *flag = reinterpret_cast<int *>(sm + SM::flag);
     double *tile = sm + SM::tile;
+    const int lane = threadIdx.x;
     const int t = blockIdx.x;
     const int64_t row0 = plan.tile_row0[t];
     const int rows = plan.tile_rows[t];
     double *At = A + row0;
 
-    stage_in<G::NT>(tile, G::LD, At, lda, rows, n, G::S, G::NP);
-    __syncthreads();
-    blocked_qr<G, false>(sm, n, rows);
-    stage_out<G::NT>(tile, G::LD, At, lda, rows, n);
-    for (int j = threadIdx.x; j < n; j += G::NT) tau_tile[(int64_t)t * n + j] = sm[SM::taus + j];
+    for (int j = lane; j < G::NP; j += 32) sm[SM::taus + j] = 0.0;   // padding reflectors: H = I
+    stage_in<32>(tile, G::LD, At, lda, rows, n, G::S, G::NP);
+    __syncwarp();
+    warp_qr<G, false>(sm, n, (rows + 7) / 8, nullptr, 0);
+    stage_out<32>(tile, G::LD, At, lda, rows, n);
+    for (int j = lane; j < n; j += 32) tau_tile[(int64_t)t * n + j] = sm[SM::taus + j];
 
     int p = plan.tile_parent[t];
     bool root = (p < 0);
     while (p >= 0) {
-        // ticket: the second team to arrive at node p runs it
+        // ticket: the second warp to arrive at node p runs it
         __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            const int old = atomicAdd(counters + p, 1);
+        __syncwarp();
+        int old = 0;
+        if (lane == 0) {
+            old = atomicAdd(counters + p, 1);
             if (old == 1) counters[p] = 0;
-            *flag = old;
         }
-        __syncthreads();
-        if (*flag != 1) return;
+        old = __shfl_sync(0xffffffffu, old, 0);
+        if (old != 1) return;
         __threadfence();
-        const int a_t = plan.node_a[p];
-        const int64_t ra = plan.tile_row0[a_t], rb = plan.tile_row0[p];
-        zero<G::NT>(tile, G::NP * G::LD);
-        __syncthreads();
-        load_upper_cg<G>(tile, 0, A + ra, lda, n);
-        load_upper_cg<G>(tile, G::NP, A + rb, lda, n);
-        __syncthreads();
-        blocked_qr<G, true>(sm, n, 2 * G::NP);
-        store_upper<G>(tile, 0, A + ra, lda, n);             // R of the merged subtree
-        store_upper<G>(tile, G::NP, A + rb, lda, n);         // Y1 of the node (eq. fact_2rs)
-        for (int j = threadIdx.x; j < n; j += G::NT) tau_node[(int64_t)p * n + j] = sm[SM::taus + j];
+        const int64_t ra = plan.tile_row0[plan.node_a[p]], rb = plan.tile_row0[p];
+        for (int e0 = 0; e0 < G::NP * G::NP; e0 += 32 * 16) {     // R_b (upper) -> rows [0, NP), L2 loads
+            double v[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int e = e0 + lane + 32 * i, r = e % G::NP, c = e / G::NP;
+                const bool ok = e < G::NP * G::NP && r <= c && c < n;
+                v[i] = ok ? __ldcg(A + rb + r + (int64_t)c * lda) : 0.0;
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int e = e0 + lane + 32 * i;
+                if (e < G::NP * G::NP) tile[(e / G::NP) * G::LD + e % G::NP] = v[i];
+            }
+        }
+        __syncwarp();
+        warp_qr<G, true>(sm, n, G::NCB, A + ra, lda);
+        for (int e = lane; e < n * n; e += 32) {                   // Y1 of the node (eq. fact_2rs)
+            const int r = e % n, c = e / n;
+            if (r <= c) A[rb + r + (int64_t)c * lda] = tile[c * G::LD + r];
+        }
+        for (int j = lane; j < n; j += 32) tau_node[(int64_t)p * n + j] = sm[SM::taus + j];
         const int q = plan.node_parent[p];
         if (q < 0) root = true;
         p = q;
     }
     if (root && R != nullptr) {
         __threadfence();
-        __syncthreads();
-        for (int e = threadIdx.x; e < n * n; e += G::NT) {
+        __syncwarp();
+        for (int e = lane; e < n * n; e += 32) {
             const int r = e % n, c = e / n;
             R[r + (int64_t)c * ldr] = (r <= c) ? __ldcg(A + r + (int64_t)c * lda) : 0.0;
         }
@@ -523,25 +626,31 @@ int team_rows_for(int64_t max_rows) {
 }
 
 template <class G>
-static cudaError_t launch_factor_t(const FactorArgs &f, cudaStream_t st) {
-    const size_t sm = Smem<G, G::NP, 8>::bytes;
-    cudaError_t e = set_smem((const void *)k_factor<G>, sm);
+static cudaError_t launch_factor_w_t(const FactorArgs &f, cudaStream_t st) {
+    const size_t sm = WSmem<G>::bytes;
+    cudaError_t e = set_smem((const void *)k_factor_w<G>, sm);
     if (e != cudaSuccess) return e;
-    k_factor<G><<<f.plan.L, G::NT, sm, st>>>(f.A, f.lda, f.n, f.plan, f.tau_tile, f.tau_node, f.counters, f.R, f.ldr);
+    k_factor_w<G><<<f.plan.L, 32, sm, st>>>(f.A, f.lda, f.n, f.plan, f.tau_tile, f.tau_node, f.counters, f.R, f.ldr);
     return cudaGetLastError();
 }
 
 template <int NCB>
-static cudaError_t launch_factor_n(const FactorArgs &f, cudaStream_t st) {
-    switch (team_rows_for(f.max_rows)) {
-        case 64: return launch_factor_t<Geo<NCB, 8, NCB>>(f, st);
-        case 128: return launch_factor_t<Geo<NCB, 16, NCB>>(f, st);
-        default: return launch_factor_t<Geo<NCB, 24, NCB>>(f, st);
-    }
+static cudaError_t launch_factor_w_n(const FactorArgs &f, cudaStream_t st) {
+    if (f.max_rows <= 64) return launch_factor_w_t<WGeo<NCB, 8>>(f, st);
+    if (f.max_rows <= 96) return launch_factor_w_t<WGeo<NCB, 12>>(f, st);
+    if (f.max_rows <= 128) return launch_factor_w_t<WGeo<NCB, 16>>(f, st);
+    return launch_factor_w_t<WGeo<NCB, 24>>(f, st);
 }
 
 cudaError_t launch_factor(const FactorArgs &f, cudaStream_t st) {
-    return f.NP <= 32 ? launch_factor_n<4>(f, st) : launch_factor_n<8>(f, st);
+    const int ncb = (f.n + 7) / 8;
+    switch (ncb) {
+        case 1: case 2: return launch_factor_w_n<2>(f, st);
+        case 3: case 4: return launch_factor_w_n<4>(f, st);
+        case 5: case 6: return launch_factor_w_n<6>(f, st);
+        case 7: return launch_factor_w_n<7>(f, st);
+        default: return launch_factor_w_n<8>(f, st);
+    }
 }
 
 template <class G, int CCOLS>

@@ -70,14 +70,77 @@ __device__ __forceinline__ House householder(double alpha, double sigma2) {
 }
 
 // Active 8-row blocks of panel p: dense (blocks p .. nrb-1) or structured node
-// (block p of R_a, then blocks na .. na+p of R_b).
+// (the pivot block piv holding row block p of R_a, then blocks na .. na+p of R_b).
 struct Rows {
-    int p, nrb, na;      // na < 0: dense
+    int p, nrb, na, piv;      // na < 0: dense
     __device__ int count() const { return na < 0 ? nrb - p : p + 2; }
-    __device__ int block(int k) const { return na < 0 ? p + k : (k == 0 ? p : na + k - 1); }
+    __device__ int block(int k) const { return na < 0 ? p + k : (k == 0 ? piv : na + k - 1); }
 };
 
 // ------------------------------------------------------------------ panel QR
+// The Householder column steps of one panel on KM register blocks, branch-free:
+// blocks beyond the active count hold zeros and stay zero (x = 0 there).
+//
+// Gs (if not null) receives the panel's Gram entries G(l, jj) = y_l^T y_jj for
+// l < jj (row-major 8x8): with y_c = (0.., 1, scl_c x_c) and d_l = x_jj^T x_l
+// over the rows below pivot jj (the dot this step computes anyway),
+// G(l, jj) = scl_l (x_l[jj] + scl_jj d_l).
+template <int KM>
+__device__ __forceinline__ void panel_steps(double (*pv)[2], int p, int n, double *taus, double *betas,
+                                            double &scl, double *Gs) {
+    const int lane = threadIdx.x & 31, cl = lane >> 2, q = lane & 3;
+    const int col = 8 * p + cl;
+    const int jend = min(8, n - 8 * p);
+#pragma unroll 1
+    for (int jj = 0; jj < jend; ++jj) {                      // rolled: keeps the loop in the I-cache
+        const int src = 4 * jj + q;                          // owner of column 8p + jj, same rows
+        // rows <= pivot of the pivot block are not part of the reflector's tail
+        const bool m0 = 2 * q > jj, m1 = 2 * q + 1 > jj;
+        double x[KM][2];
+#pragma unroll
+        for (int k = 0; k < KM; ++k) {
+            x[k][0] = __shfl_sync(0xffffffffu, pv[k][0], src);
+            x[k][1] = __shfl_sync(0xffffffffu, pv[k][1], src);
+        }
+        x[0][0] = m0 ? x[0][0] : 0.0;
+        x[0][1] = m1 ? x[0][1] : 0.0;
+        double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+        for (int k = 0; k < KM; k += 2) {
+            d0 = fma(x[k][0], pv[k][0], d0);
+            d1 = fma(x[k][1], pv[k][1], d1);
+            if (k + 1 < KM) {
+                d2 = fma(x[k + 1][0], pv[k + 1][0], d2);
+                d3 = fma(x[k + 1][1], pv[k + 1][1], d3);
+            }
+        }
+        double d = (d0 + d1) + (d2 + d3);
+        d += __shfl_xor_sync(0xffffffffu, d, 1);
+        d += __shfl_xor_sync(0xffffffffu, d, 2);             // x^T A(:, col)
+        const double pj = (jj & 1) ? pv[0][1] : pv[0][0];
+        const double rj = __shfl_sync(0xffffffffu, pj, 4 * cl + (jj >> 1));   // A(8p + jj, col)
+        const double sig2 = __shfl_sync(0xffffffffu, d, 4 * jj);
+        const double alpha = __shfl_sync(0xffffffffu, rj, 4 * jj);
+        const House h = householder(alpha, sig2);
+        const double w = fma(d, h.scale, rj);                // v^T A(:, col)
+        const double u = (cl > jj && col < n) ? h.tau * h.scale * w : 0.0;
+#pragma unroll
+        for (int k = 0; k < KM; ++k) {
+            pv[k][0] = fma(-x[k][0], u, pv[k][0]);
+            pv[k][1] = fma(-x[k][1], u, pv[k][1]);
+        }
+        const double dr = (q == (jj >> 1)) ? (alpha - h.beta) * u : 0.0;   // A(j, col) -= tau w
+        if (jj & 1) pv[0][1] -= dr;
+        else pv[0][0] -= dr;
+        if (Gs != nullptr && q == 0 && cl < jj) Gs[cl * 8 + jj] = scl * fma(h.scale, d, rj);
+        scl = (cl == jj) ? h.scale : scl;
+        if (lane == 0) {
+            taus[8 * p + jj] = h.tau;
+            betas[8 * p + jj] = h.beta;
+        }
+    }
+}
+
 // Factor columns 8p .. 8p+7 (those < n) of the tile over the active rows.
 // Lane i = 4 cl + q holds column 8p + cl, rows 8 block(k) + 2q + {0,1}.
 // On exit the tile holds R (rows <= pivot) and the reflector entries v (below)
@@ -85,7 +148,7 @@ struct Rows {
 // zeros outside the active rows); taus[8p..], betas[8p..] are set.
 template <int KMAX>
 __device__ __forceinline__ void panel_qr(double *tile, int ld, int n, const Rows &rows, double *Ys, int ldy,
-                                         double *taus, double *betas) {
+                                         double *taus, double *betas, double *Gs = nullptr) {
     const int lane = threadIdx.x & 31, cl = lane >> 2, q = lane & 3;
     const int p = rows.p, cnt = rows.count();
     const int col = 8 * p + cl;
@@ -100,55 +163,14 @@ __device__ __forceinline__ void panel_qr(double *tile, int ld, int n, const Rows
         }
     }
     double scl = 0.0;
-#pragma unroll
-    for (int jj = 0; jj < 8; ++jj) {
-        const int j = 8 * p + jj;
-        if (j >= n) break;                                   // warp-uniform
-        const int src = 4 * jj + q;                          // owner of column j, same rows
-        // rows <= j of the pivot block are not part of the reflector's tail
-        const bool m0 = 2 * q > jj, m1 = 2 * q + 1 > jj;
-        double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-        for (int k = 0; k < KMAX; ++k)
-            if (k < cnt) {
-                double x0 = __shfl_sync(0xffffffffu, pv[k][0], src);
-                double x1 = __shfl_sync(0xffffffffu, pv[k][1], src);
-                if (k == 0) {
-                    x0 = m0 ? x0 : 0.0;
-                    x1 = m1 ? x1 : 0.0;
-                }
-                d0 = fma(x0, pv[k][0], d0);
-                d1 = fma(x1, pv[k][1], d1);
-            }
-        double d = d0 + d1;
-        d += __shfl_xor_sync(0xffffffffu, d, 1);
-        d += __shfl_xor_sync(0xffffffffu, d, 2);             // x^T A(:, col)
-        const double sig2 = __shfl_sync(0xffffffffu, d, 4 * jj);
-        const double rj = __shfl_sync(0xffffffffu, pv[0][jj & 1], 4 * cl + (jj >> 1));   // A(j, col)
-        const double alpha = __shfl_sync(0xffffffffu, rj, 4 * jj);
-        const House h = householder(alpha, sig2);
-        const double w = fma(d, h.scale, rj);                // v^T A(:, col)
-        const double u = (cl > jj && col < n) ? h.tau * h.scale * w : 0.0;
-        // the rank-1 update re-fetches x by shuffle (keeps the panel in 2 KMAX registers)
-#pragma unroll
-        for (int k = 0; k < KMAX; ++k)
-            if (k < cnt) {
-                double x0 = __shfl_sync(0xffffffffu, pv[k][0], src);
-                double x1 = __shfl_sync(0xffffffffu, pv[k][1], src);
-                if (k == 0) {
-                    x0 = m0 ? x0 : 0.0;
-                    x1 = m1 ? x1 : 0.0;
-                }
-                pv[k][0] = fma(-x0, u, pv[k][0]);
-                pv[k][1] = fma(-x1, u, pv[k][1]);
-            }
-        if (q == (jj >> 1)) pv[0][jj & 1] -= (alpha - h.beta) * u;   // A(j, col) -= tau w
-        if (cl == jj) scl = h.scale;
-        if (lane == 0) {
-            taus[j] = h.tau;
-            betas[j] = h.beta;
-        }
+    if (Gs != nullptr) {
+        Gs[lane] = 0.0;
+        Gs[lane + 32] = 0.0;
+        __syncwarp();
     }
+    constexpr int KH = (KMAX + 1) / 2;
+    if (KH < KMAX && cnt <= KH) panel_steps<KH>(pv, p, n, taus, betas, scl, Gs);
+    else panel_steps<KMAX>(pv, p, n, taus, betas, scl, Gs);
     __syncwarp();
     // the pivot column of each reflector becomes (beta, v = scale * x): rows > pivot
     if (col < n) {
@@ -226,6 +248,29 @@ __device__ __forceinline__ void build_t(const double *Ys, int ldy, const Rows &r
     __syncwarp();
 }
 
+// T from the Gram entries panel_qr left in Gs (row-major, G(l, c) for l < c),
+// same recurrence as build_t; lanes r < 8 own row r of T (static indexing:
+// T(r, l) = 0 for l < r, so the sum may run over all l < c).
+__device__ __forceinline__ void build_t_gram(const double *Gs, const double *t, double *Ts) {
+    const int r = threadIdx.x & 31;
+    if (r < 8) {
+        double row[8];
+        const double tr = t[r];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) row[c] = (c == r) ? tr : 0.0;
+#pragma unroll
+        for (int c = 1; c < 8; ++c) {
+            double s = 0.0;
+#pragma unroll
+            for (int l = 0; l < c; ++l) s = fma(row[l], Gs[l * 8 + c], s);
+            if (r < c) row[c] = -t[c] * s;
+        }
+#pragma unroll
+        for (int c = 0; c < 8; c += 2) *reinterpret_cast<double2 *>(Ts + r * 8 + c) = make_double2(row[c], row[c + 1]);
+    }
+    __syncwarp();
+}
+
 // ------------------------------------------------------------------ update
 // For the calling warp's column block cb of C (columns 8cb..8cb+7, ld ldc):
 // C <- (I - Y op(T) Y^T) C over the active rows, op(T) = T^T (kTrans: Q^T) or T.
@@ -271,6 +316,78 @@ __device__ __forceinline__ void wy_update_block(double *C, int ldc, int cb, cons
         dmma(c2.x, c2.y, a0, Ys[(lq)*ldy + 8 * rb + l4]);
         dmma(c2.x, c2.y, a1, Ys[(4 + lq) * ldy + 8 * rb + l4]);
         *reinterpret_cast<double2 *>(cw + 8 * rb + 2 * lq) = c2;
+    }
+    __syncwarp();
+}
+
+// wy_update_block on nb <= NB column blocks cb0, cb0+1, .. at once (one warp):
+// the Y fragments are loaded once for all blocks and the NB DMMA chains
+// interleave.  Wb: NB x 72 scratch.  nb is warp-uniform.
+template <bool kTrans, int NB>
+__device__ __forceinline__ void wy_update_multi(double *C, int ldc, int cb0, int nb, const double *Ys, int ldy,
+                                                const Rows &rows, const double *Ts, double *Wb) {
+    const int lane = threadIdx.x & 31, lq = lane & 3, l4 = lane >> 2;
+    const int cnt = rows.count();
+    double w[NB][2];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) w[b][0] = w[b][1] = 0.0;
+    const double *cc = C + (8 * cb0 + l4) * ldc;
+    for (int k = 0; k < cnt; ++k) {
+        const int rb = rows.block(k);
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int r = 8 * rb + 4 * e + lq;
+            const double a = Ys[l4 * ldy + r];
+#pragma unroll
+            for (int b = 0; b < NB; ++b)
+                if (b < nb) dmma(w[b][0], w[b][1], a, cc[8 * b * ldc + r]);
+        }
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        Wb[72 * b + l4 * 9 + 2 * lq] = w[b][0];
+        Wb[72 * b + l4 * 9 + 2 * lq + 1] = w[b][1];
+    }
+    __syncwarp();
+    double a2[2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+        const int kk = 4 * e + lq;
+        a2[e] = kTrans ? Ts[kk * 8 + l4] : Ts[l4 * 8 + kk];
+    }
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        w[b][0] = w[b][1] = 0.0;
+        if (b < nb) {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) dmma(w[b][0], w[b][1], a2[e], Wb[72 * b + (4 * e + lq) * 9 + l4]);
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        Wb[72 * b + l4 * 9 + 2 * lq] = w[b][0];
+        Wb[72 * b + l4 * 9 + 2 * lq + 1] = w[b][1];
+    }
+    __syncwarp();
+    double a0[NB], a1[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        a0[b] = -Wb[72 * b + lq * 9 + l4];
+        a1[b] = -Wb[72 * b + (4 + lq) * 9 + l4];
+    }
+    double *cw = C + (8 * cb0 + l4) * ldc;
+    for (int k = 0; k < cnt; ++k) {
+        const int rb = rows.block(k);
+        const double y0 = Ys[lq * ldy + 8 * rb + l4], y1 = Ys[(4 + lq) * ldy + 8 * rb + l4];
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+            if (b < nb) {
+                double2 c2 = *reinterpret_cast<const double2 *>(cw + 8 * b * ldc + 8 * rb + 2 * lq);
+                dmma(c2.x, c2.y, a0[b], y0);
+                dmma(c2.x, c2.y, a1[b], y1);
+                *reinterpret_cast<double2 *>(cw + 8 * b * ldc + 8 * rb + 2 * lq) = c2;
+            }
     }
     __syncwarp();
 }

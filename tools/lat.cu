@@ -38,17 +38,26 @@ __global__ void k(double *out, long long *cyc, double a, double b) {
     t0 = clock64();
     for (int i = 0; i < N / 8; ++i) { __syncthreads(); x = x * a; }
     t1 = clock64(); if (threadIdx.x == 0) cyc[9] = (t1 - t0) * 8;
+    {
+        double d0 = x, d1 = x * 0.5;
+        t0 = clock64();
+        for (int i = 0; i < N; ++i)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                         : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+        t1 = clock64(); if (threadIdx.x == 0) cyc[10] = t1 - t0;
+        x += d0 + d1;
+    }
     out[threadIdx.x] = x;
 }
 int main() {
     double *o; long long *c; cudaMalloc(&o, 4096 * 8); cudaMallocManaged(&c, 16 * 8);
     const char *names[] = {"dfma", "dadd", "shfl64+dmul", "sts+lds+dmul", "rsqrt(double)", "sqrt(double)", "div 1/x",
-                           "rcp.approx.f64", "rsqrt.approx.f64", "bar.sync(256)+dmul"};
+                           "rcp.approx.f64", "rsqrt.approx.f64", "bar.sync(256)+dmul", "dmma chain"};
     for (int thr : {32, 256}) {
         k<<<1, thr>>>(o, c, 1.0000001, 1e-9);
         k<<<1, thr>>>(o, c, 1.0000001, 1e-9);
         cudaDeviceSynchronize();
         printf("threads=%d\n", thr);
-        for (int i = 0; i < 10; ++i) printf("  %-20s %.1f cycles/op\n", names[i], c[i] / double(N));
+        for (int i = 0; i < 11; ++i) printf("  %-20s %.1f cycles/op\n", names[i], c[i] / double(N));
     }
 }
