@@ -65,7 +65,10 @@ typedef struct {
     int64_t depth;         /* levels of the local tree (tile + block stages)     */
     int64_t cross_rounds;  /* log2(nranks): butterfly rounds (Table 1) */
     int64_t max_tile_rows, min_tile_rows;
-    int64_t tile_capacity; /* rows one CTA keeps on chip for this n              */
+    int64_t tile_capacity; /* tallest tile the kernels accept                     */
+    int64_t chunk_rows;    /* c: every tile is factored as a flat chain ("sequential
+                              TSQR") over chunks of c rows  */
+    int64_t nchunks;       /* chunks of all tiles = rows of the tau export        */
 } tsqr_plan_info_t;
 
 /* ---------------------------------------------------------------- host-only
@@ -160,8 +163,10 @@ tsqr_status_t tsqr_form_q(tsqr_tree_t tree, double *Q, int64_t ldq, void *stream
 /* Release the tree's device memory (stream-ordered on the last stream used). */
 tsqr_status_t tsqr_tree_free(tsqr_tree_t tree);
 
-/* Test hook: copy the tree's tile taus (ntiles*n) and node taus (by node b
- * index, ntiles*n; row 0 unused) to host buffers (either may be NULL).
+/* Test hook: copy the tree's leaf taus (nchunks*n: chunk k of the tiles in
+ * order, reflector j at [k*n + j], 0 where chunk k has no reflector j) and the
+ * node taus (by node b index, ntiles*n; row 0 unused) to host buffers (either
+ * may be NULL).
  * Synchronises the tree's stream. */
 tsqr_status_t tsqr_tree_export_tau(tsqr_tree_t tree, double *tau_tile_host, double *tau_node_host);
 

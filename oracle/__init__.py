@@ -89,6 +89,18 @@ def hqr(A):
     return F, tau
 
 
+def chain_qr(A, c: int = 0):
+    """Flat-chain QR of one tile over c-row chunks (orc_chain_qr).
+    Returns (F, tau): F upper (first n rows) = R, below the diagonal = reflector
+    tails; tau (nchunks x n)."""
+    F = _fortran(A)
+    m, n = F.shape
+    nch = 1 if c <= 0 else -(-m // c)
+    tau = np.zeros((nch, n))
+    lib().orc_chain_qr(_i64(m), _i64(n), _d(F), _i64(_ld(F)), _i64(c), _d(tau))
+    return F, tau
+
+
 def combine(Ra, Rb):
     """Structured QR of [Ra; Rb]. Returns (R, Y1, tau, flops)."""
     a = _fortran(Ra)
@@ -143,17 +155,24 @@ class Plan:
     node_b: np.ndarray
     node_stage: np.ndarray
     node_level: np.ndarray
+    c: int = 0                 # chunk rows of the tiles' flat chains (0: one chunk per tile)
 
     @property
     def ntiles(self) -> int:
         return len(self.tile_row0)
 
     @property
+    def tile_chunk0(self) -> np.ndarray:
+        """First chunk of every tile (+ the total), the row index into tau_tile."""
+        k = np.ones_like(self.tile_rows) if self.c <= 0 else -(-self.tile_rows // self.c)
+        return np.concatenate([[0], np.cumsum(k)]).astype(np.int64)
+
+    @property
     def nnodes(self) -> int:
         return len(self.node_a)
 
 
-def plan(m: int, n: int, b: int, s: int | None = None, G: int = 1) -> Plan:
+def plan(m: int, n: int, b: int, s: int | None = None, G: int = 1, c: int = 0) -> Plan:
     s = 0 if s is None else s
     nt, nn = _i64(), _i64()
     rc = lib().orc_plan_count(_i64(m), _i64(n), _i64(b), _i64(s), _i64(G),
@@ -164,7 +183,7 @@ def plan(m: int, n: int, b: int, s: int | None = None, G: int = 1) -> Plan:
           [np.zeros(nn.value, np.int64) for _ in range(4)]
     rc = lib().orc_plan_fill(_i64(m), _i64(n), _i64(b), _i64(s), _i64(G), *[_i(x) for x in arr])
     assert rc == 0
-    return Plan(m, n, b, s, G, *arr)
+    return Plan(m, n, b, s, G, *arr, c=c)
 
 
 # ------------------------------------------------------------------- TSQR
@@ -172,7 +191,7 @@ def plan(m: int, n: int, b: int, s: int | None = None, G: int = 1) -> Plan:
 class Factor:
     plan: Plan
     A: np.ndarray          # overwritten A (tile reflectors below the tile diagonals)
-    tau_tile: np.ndarray   # ntiles x n
+    tau_tile: np.ndarray   # nchunks x n (plan.tile_chunk0 indexes the tiles)
     Y1: np.ndarray         # nnodes x n x n (each column-major n x n, upper)
     tau_node: np.ndarray   # nnodes x n
     R: np.ndarray          # n x n
@@ -187,17 +206,18 @@ def tsqr_factor(A, p: Plan) -> Factor:
     F = _fortran(A)
     m, n = F.shape
     assert m == p.m and n == p.n
-    tau_tile = np.zeros((p.ntiles, n))
+    tau_tile = np.zeros((int(p.tile_chunk0[-1]), n))
     Y1 = np.zeros((max(p.nnodes, 1), n * n))
     tau_node = np.zeros((max(p.nnodes, 1), n))
     R = np.zeros((n, n), order="F")
-    lib().orc_tsqr_factor(_i64(m), _i64(n), _d(F), _i64(_ld(F)), *_plan_args(p),
+    lib().orc_tsqr_factor(_i64(m), _i64(n), _d(F), _i64(_ld(F)), _i64(p.c), *_plan_args(p),
                           _d(tau_tile), _d(Y1), _d(tau_node), _d(R), _i64(n))
     return Factor(p, F, tau_tile, Y1, tau_node, R)
 
 
 def _factor_args(f: Factor):
-    return (_d(f.A), _i64(_ld(f.A)), *_plan_args(f.plan), _d(f.tau_tile), _d(f.Y1), _d(f.tau_node))
+    return (_d(f.A), _i64(_ld(f.A)), _i64(f.plan.c), *_plan_args(f.plan), _d(f.tau_tile), _d(f.Y1),
+            _d(f.tau_node))
 
 
 def tsqr_apply_qt(f: Factor, C) -> np.ndarray:

@@ -57,6 +57,64 @@ void orc_hqr(int64_t m, int64_t n, double *A, int64_t lda, double *tau)
     }
 }
 
+/* Rows of reflector j of chunk k of a tile's flat chain (orc_chain_qr): the
+ * chunk is rows [r0, r0 + h).  j < r0: "structured" -- pivot row j (the
+ * running R's row j, kept in place in the tile's head) and tail = the whole
+ * chunk; r0 <= j < r0 + h: "dense" -- pivot row j inside the chunk, tail =
+ * rows j+1 .. r0+h-1; otherwise no reflector.  Returns the tail length
+ * (-1: no reflector) and the first tail row in *t0. */
+static int64_t chain_rows(int64_t j, int64_t r0, int64_t h, int64_t *t0)
+{
+    if (j < r0) { *t0 = r0; return h; }
+    if (j < r0 + h) { *t0 = j + 1; return r0 + h - j - 1; }
+    return -1;
+}
+
+static int64_t chunks_of(int64_t rows, int64_t c)
+{
+    return c <= 0 ? 1 : (rows + c - 1) / c;
+}
+
+/* Flat-tree ("sequential") TSQR of one tile ([TR] Alg. sequential
+ * TSQR P:1725-1753) over chunks of c consecutive rows: chunk k (rows
+ * r0 = k c .. r0 + h - 1) is merged into the running R by qr([R; A_k]), one
+ * Householder reflector per column j = 0..n-1 on the rows chain_rows gives
+ * (the structure of [R; A_k]: R upper trapezoidal, its row j being the tile's
+ * row j).  c <= 0 (or c >= rows): one chunk, i.e. orc_hqr.  On exit the tile
+ * holds R in the upper triangle of its first n rows and every reflector's
+ * tail below the diagonal (row > column) in place; tau[k*n + j] (0 for a
+ * missing reflector). */
+void orc_chain_qr(int64_t rows, int64_t n, double *A, int64_t lda, int64_t c, double *tau)
+{
+    const int64_t cc = c <= 0 ? rows : c;
+    double *w = (double *)malloc((size_t)(cc + 1) * sizeof(double));
+    for (int64_t k = 0, r0 = 0; r0 < rows; ++k, r0 += cc) {
+        const int64_t h = rows - r0 < cc ? rows - r0 : cc;
+        for (int64_t j = 0; j < n; ++j) {
+            int64_t t0;
+            const int64_t len = chain_rows(j, r0, h, &t0);
+            if (len < 0) { tau[k * n + j] = 0.0; continue; }
+            /* gather the pivot column (pivot row j, then the tail rows) */
+            w[0] = AT(A, j, j, lda);
+            for (int64_t i = 0; i < len; ++i) w[1 + i] = AT(A, t0 + i, j, lda);
+            double t, beta;
+            orc_house(len + 1, w, &t, &beta);
+            for (int64_t col = j + 1; col < n; ++col) {
+                long double d = AT(A, j, col, lda);
+                for (int64_t i = 0; i < len; ++i)
+                    d += (long double)w[1 + i] * (long double)AT(A, t0 + i, col, lda);
+                double td = t * (double)d;
+                AT(A, j, col, lda) -= td;
+                for (int64_t i = 0; i < len; ++i) AT(A, t0 + i, col, lda) -= w[1 + i] * td;
+            }
+            AT(A, j, j, lda) = beta;
+            for (int64_t i = 0; i < len; ++i) AT(A, t0 + i, j, lda) = w[1 + i];
+            tau[k * n + j] = t;
+        }
+    }
+    free(w);
+}
+
 /* Alg. QR:qnxn with q = 2: index set I_j = {j, n+1:n+j}
  * (P:1964-1965), i.e. row j of Ra and rows 0..j of Rb. */
 void orc_combine(int64_t n, double *Ra, int64_t lda, double *Rb, int64_t ldb,
@@ -282,7 +340,7 @@ int orc_plan_fill(int64_t m, int64_t n, int64_t b, int64_t s, int64_t G,
 
 /* Eqs. 1-4: every tile A_i = Q_i R_i, then stacked pairs of R's
  * are re-factored up the tree; the implicit Q is the tree of local factors. */
-void orc_tsqr_factor(int64_t m, int64_t n, double *A, int64_t lda,
+void orc_tsqr_factor(int64_t m, int64_t n, double *A, int64_t lda, int64_t c,
                      int64_t ntiles, const int64_t *tile_row0, const int64_t *tile_rows,
                      int64_t nnodes, const int64_t *node_a, const int64_t *node_b,
                      double *tau_tile, double *Y1, double *tau_node,
@@ -291,9 +349,11 @@ void orc_tsqr_factor(int64_t m, int64_t n, double *A, int64_t lda,
     (void)m;
     size_t nn = (size_t)(n * n);
     double *Rsub = (double *)calloc((size_t)ntiles * nn, sizeof(double));
+    int64_t ch0 = 0;
     for (int64_t t = 0; t < ntiles; ++t) {                       /* Eq. 1 */
         double *At = A + tile_row0[t];
-        orc_hqr(tile_rows[t], n, At, lda, tau_tile + t * n);
+        orc_chain_qr(tile_rows[t], n, At, lda, c, tau_tile + ch0 * n);
+        ch0 += chunks_of(tile_rows[t], c);
         for (int64_t j = 0; j < n; ++j)
             for (int64_t i = 0; i <= j; ++i) AT(Rsub + t * nn, i, j, n) = AT(At, i, j, lda);
     }
@@ -309,18 +369,38 @@ void orc_tsqr_factor(int64_t m, int64_t n, double *A, int64_t lda,
     free(Rsub);
 }
 
-/* one tile reflector j applied to C rows [r0+j, r0+rows) : C -= tau v (v^T C) */
-static void apply_tile_reflector(int64_t rows, int64_t j, const double *At, int64_t lda,
-                                 double tau, double *Ct, int64_t ldc, int64_t k)
+/* reflector j of a tile chunk (rows from chain_rows, vector tail stored in
+ * the tile below the diagonal) applied to the same rows of C: C -= tau v (v^T C) */
+static void apply_chain_reflector(int64_t j, int64_t t0, int64_t len, const double *At, int64_t lda,
+                                  double tau, double *Ct, int64_t ldc, int64_t k)
 {
-    if (tau == 0.0) return;
+    if (tau == 0.0 || len < 0) return;
     for (int64_t c = 0; c < k; ++c) {
         long double w = AT(Ct, j, c, ldc);
-        for (int64_t i = j + 1; i < rows; ++i)
-            w += (long double)AT(At, i, j, lda) * (long double)AT(Ct, i, c, ldc);
+        for (int64_t i = 0; i < len; ++i)
+            w += (long double)AT(At, t0 + i, j, lda) * (long double)AT(Ct, t0 + i, c, ldc);
         double tw = tau * (double)w;
         AT(Ct, j, c, ldc) -= tw;
-        for (int64_t i = j + 1; i < rows; ++i) AT(Ct, i, c, ldc) -= AT(At, i, j, lda) * tw;
+        for (int64_t i = 0; i < len; ++i) AT(Ct, t0 + i, c, ldc) -= AT(At, t0 + i, j, lda) * tw;
+    }
+}
+
+/* Q_t^T C_t for one tile: chunks in order, reflectors j = 0..n-1 (forward), or
+ * Q_t C_t: chunks and reflectors in reverse. */
+static void apply_tile(int64_t rows, int64_t n, int64_t c, const double *At, int64_t lda,
+                       const double *tau, double *Ct, int64_t ldc, int64_t k, int forward)
+{
+    const int64_t cc = c <= 0 ? rows : c;
+    const int64_t nk = chunks_of(rows, c);
+    for (int64_t kk = 0; kk < nk; ++kk) {
+        const int64_t ck = forward ? kk : nk - 1 - kk;
+        const int64_t r0 = ck * cc, h = rows - r0 < cc ? rows - r0 : cc;
+        for (int64_t jj = 0; jj < n; ++jj) {
+            const int64_t j = forward ? jj : n - 1 - jj;
+            int64_t t0;
+            const int64_t len = chain_rows(j, r0, h, &t0);
+            apply_chain_reflector(j, t0, len, At, lda, tau[ck * n + j], Ct, ldc, k);
+        }
     }
 }
 
@@ -344,7 +424,7 @@ static void apply_node_reflector(int64_t n, int64_t j, const double *Yk, double 
 
 /* Q^T C: leaves first, then nodes bottom-up in factor order (Eq. 4 gives
  * A = Q_leaves Q_level1 ... Q_root R; reading R4). */
-void orc_tsqr_apply_qt(int64_t m, int64_t n, const double *A, int64_t lda,
+void orc_tsqr_apply_qt(int64_t m, int64_t n, const double *A, int64_t lda, int64_t c,
                        int64_t ntiles, const int64_t *tile_row0, const int64_t *tile_rows,
                        int64_t nnodes, const int64_t *node_a, const int64_t *node_b,
                        const double *tau_tile, const double *Y1, const double *tau_node,
@@ -352,17 +432,15 @@ void orc_tsqr_apply_qt(int64_t m, int64_t n, const double *A, int64_t lda,
 {
     (void)m;
     size_t nn = (size_t)(n * n);
-    for (int64_t t = 0; t < ntiles; ++t)
-        for (int64_t j = 0; j < n; ++j)          /* Q_t^T = H_{n-1} ... H_0 : H_0 first */
-            apply_tile_reflector(tile_rows[t], j, A + tile_row0[t], lda, tau_tile[t * n + j],
-                                 C + tile_row0[t], ldc, k);
+    for (int64_t t = 0, ch0 = 0; t < ntiles; ch0 += chunks_of(tile_rows[t], c), ++t)
+        apply_tile(tile_rows[t], n, c, A + tile_row0[t], lda, tau_tile + ch0 * n, C + tile_row0[t], ldc, k, 1);
     for (int64_t q = 0; q < nnodes; ++q)
         for (int64_t j = 0; j < n; ++j)
             apply_node_reflector(n, j, Y1 + q * nn, tau_node[q * n + j],
                                  C + tile_row0[node_a[q]], C + tile_row0[node_b[q]], ldc, k);
 }
 
-void orc_tsqr_apply_q(int64_t m, int64_t n, const double *A, int64_t lda,
+void orc_tsqr_apply_q(int64_t m, int64_t n, const double *A, int64_t lda, int64_t c,
                       int64_t ntiles, const int64_t *tile_row0, const int64_t *tile_rows,
                       int64_t nnodes, const int64_t *node_a, const int64_t *node_b,
                       const double *tau_tile, const double *Y1, const double *tau_node,
@@ -374,13 +452,11 @@ void orc_tsqr_apply_q(int64_t m, int64_t n, const double *A, int64_t lda,
         for (int64_t j = n - 1; j >= 0; --j)     /* Q_node = H_0 ... H_{n-1}: H_{n-1} first */
             apply_node_reflector(n, j, Y1 + q * nn, tau_node[q * n + j],
                                  C + tile_row0[node_a[q]], C + tile_row0[node_b[q]], ldc, k);
-    for (int64_t t = 0; t < ntiles; ++t)
-        for (int64_t j = n - 1; j >= 0; --j)
-            apply_tile_reflector(tile_rows[t], j, A + tile_row0[t], lda, tau_tile[t * n + j],
-                                 C + tile_row0[t], ldc, k);
+    for (int64_t t = 0, ch0 = 0; t < ntiles; ch0 += chunks_of(tile_rows[t], c), ++t)
+        apply_tile(tile_rows[t], n, c, A + tile_row0[t], lda, tau_tile + ch0 * n, C + tile_row0[t], ldc, k, 0);
 }
 
-void orc_tsqr_form_q(int64_t m, int64_t n, const double *A, int64_t lda,
+void orc_tsqr_form_q(int64_t m, int64_t n, const double *A, int64_t lda, int64_t c,
                      int64_t ntiles, const int64_t *tile_row0, const int64_t *tile_rows,
                      int64_t nnodes, const int64_t *node_a, const int64_t *node_b,
                      const double *tau_tile, const double *Y1, const double *tau_node,
@@ -388,7 +464,7 @@ void orc_tsqr_form_q(int64_t m, int64_t n, const double *A, int64_t lda,
 {
     for (int64_t j = 0; j < n; ++j)
         for (int64_t i = 0; i < m; ++i) AT(Q, i, j, ldq) = (i == j) ? 1.0 : 0.0;
-    orc_tsqr_apply_q(m, n, A, lda, ntiles, tile_row0, tile_rows, nnodes, node_a, node_b,
+    orc_tsqr_apply_q(m, n, A, lda, c, ntiles, tile_row0, tile_rows, nnodes, node_a, node_b,
                      tau_tile, Y1, tau_node, Q, ldq, n);
 }
 

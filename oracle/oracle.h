@@ -46,6 +46,21 @@ void orc_house(int64_t len, double *x, double *tau, double *beta);
  * the invariants ||A-QR||, ||Q^TQ-I||, R^TR = A^TA. */
 void orc_hqr(int64_t m, int64_t n, double *A, int64_t lda, double *tau);
 
+/* Flat-tree ("sequential") TSQR of one tile over chunks of c rows (
+ * [TR] Alg. sequential TSQR P:1725-1753): chunk k (rows r0 = kc .. r0+h-1) is
+ * merged into the running R by qr([R; A_k]); R is upper trapezoidal and its
+ * row j is the tile's row j, so reflector j of chunk k acts on
+ *   rows {j} u [r0, r0+h)   if j < r0        (pivot = R row j, tail = chunk),
+ *   rows [j, r0+h)          if r0 <= j < r0+h (pivot inside the chunk),
+ * and is absent otherwise (tau = 0).  c <= 0 or c >= rows: orc_hqr exactly.
+ * On exit R is in the upper triangle of the first n rows, every reflector's
+ * tail in place below the diagonal, tau[k*n + j] for chunk k.
+ * Pinned by: c = 0 equals orc_hqr bit for bit; R vs LAPACK / flat QR
+ * (uniqueness modulo signs); the invariants of the explicit Q
+ * built from the stored reflectors; the executed row sets (chain_rows) vs
+ * the sparsity of [R; A_k]. */
+void orc_chain_qr(int64_t rows, int64_t n, double *A, int64_t lda, int64_t c, double *tau);
+
 /* Structured QR of two stacked n x n upper triangles [Ra; Rb], Alg. QR:qnxn with
  * q = 2 (sparsity eq. fact_2rs).  Reflector j acts on
  * the index set I_j = {row j of Ra} u {rows 0..j of Rb}.
@@ -99,13 +114,14 @@ int orc_plan_fill(int64_t m, int64_t n, int64_t b, int64_t s, int64_t G,
                   int64_t *node_level);
 
 /* TSQR factorization over an explicit plan (Eqs. 1-4).
- * A (m x n, global) is overwritten tile by tile as orc_hqr does;
- * tau_tile[ntiles*n]; node factors Y1[nnodes*n*n] (node k at Y1 + k*n*n,
+ * Every tile (leaf) is factored by orc_chain_qr with chunk rows c (c = 0: the
+ * paper's plain leaf QR); A (m x n, global) is overwritten tile by tile;
+ * tau_tile[nchunks*n] (chunks of tile 0 first, ceil(rows/c) chunks per tile); node factors Y1[nnodes*n*n] (node k at Y1 + k*n*n,
  * column-major n x n, upper triangle) and tau_node[nnodes*n]; R (n x n, ldr)
  * receives the final R (zeros below the diagonal).
  * Pinned by: flat orc_hqr R (uniqueness modulo signs), tree
  * independence, R^TR = A^TA (Cor. 1). */
-void orc_tsqr_factor(int64_t m, int64_t n, double *A, int64_t lda,
+void orc_tsqr_factor(int64_t m, int64_t n, double *A, int64_t lda, int64_t c,
                      int64_t ntiles, const int64_t *tile_row0, const int64_t *tile_rows,
                      int64_t nnodes, const int64_t *node_a, const int64_t *node_b,
                      double *tau_tile, double *Y1, double *tau_node,
@@ -116,21 +132,21 @@ void orc_tsqr_factor(int64_t m, int64_t n, double *A, int64_t lda,
  * applied reflector by reflector.  Global rows 0..n-1 end
  * holding Q_thin^T C.  Pinned by: Q^T A = [R; 0]; ||Q^T C|| = ||C||;
  * apply_q(apply_qt(C)) = C; thin part = (formed Q)^T C. */
-void orc_tsqr_apply_qt(int64_t m, int64_t n, const double *A, int64_t lda,
+void orc_tsqr_apply_qt(int64_t m, int64_t n, const double *A, int64_t lda, int64_t c,
                        int64_t ntiles, const int64_t *tile_row0, const int64_t *tile_rows,
                        int64_t nnodes, const int64_t *node_a, const int64_t *node_b,
                        const double *tau_tile, const double *Y1, const double *tau_node,
                        double *C, int64_t ldc, int64_t k);
 
 /* C <- Q C, the exact reverse traversal of orc_tsqr_apply_qt. */
-void orc_tsqr_apply_q(int64_t m, int64_t n, const double *A, int64_t lda,
+void orc_tsqr_apply_q(int64_t m, int64_t n, const double *A, int64_t lda, int64_t c,
                       int64_t ntiles, const int64_t *tile_row0, const int64_t *tile_rows,
                       int64_t nnodes, const int64_t *node_a, const int64_t *node_b,
                       const double *tau_tile, const double *Y1, const double *tau_node,
                       double *C, int64_t ldc, int64_t k);
 
 /* Explicit thin Q (m x n) = Q [I_n; 0]. */
-void orc_tsqr_form_q(int64_t m, int64_t n, const double *A, int64_t lda,
+void orc_tsqr_form_q(int64_t m, int64_t n, const double *A, int64_t lda, int64_t c,
                      int64_t ntiles, const int64_t *tile_row0, const int64_t *tile_rows,
                      int64_t nnodes, const int64_t *node_a, const int64_t *node_b,
                      const double *tau_tile, const double *Y1, const double *tau_node,

@@ -34,7 +34,7 @@ class Opts(ctypes.Structure):
 class PlanInfo(ctypes.Structure):
     _fields_ = [(f, ctypes.c_int64) for f in
                 ("m_local", "n", "block_rows", "tile_rows", "ntiles", "nnodes", "nblocks", "depth",
-                 "cross_rounds", "max_tile_rows", "min_tile_rows", "tile_capacity")]
+                 "cross_rounds", "max_tile_rows", "min_tile_rows", "tile_capacity", "chunk_rows", "nchunks")]
 
 
 _lib = None

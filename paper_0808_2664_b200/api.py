@@ -63,7 +63,7 @@ class Tree:
     def export_tau(self):
         info = plan_info(self.m_local, self.n, self.opts)
         L, n = info["ntiles"], self.n
-        tt = np.zeros((L, n))
+        tt = np.zeros((info["nchunks"], n))
         tn = np.zeros((L, n))
         check(lib().tsqr_tree_export_tau(self.handle, tt.ctypes.data_as(ctypes.c_void_p),
                                           tn.ctypes.data_as(ctypes.c_void_p)), "tsqr_tree_export_tau")

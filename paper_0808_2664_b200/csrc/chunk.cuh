@@ -1,0 +1,420 @@
+// Register-resident chunk engine of the B200 TSQR leaf path (sm_100a).  Product code.
+//
+// A tile (the leaf of the binary tree) is factored as a
+// flat chain ("sequential TSQR", flat tree P:954-993, [TR] Alg. P:1725-1753)
+// over chunks of CH = 8 KM consecutive rows: for the chunk at tile row r0,
+//     [R; A_k]  <-  Householder QR, column by column j = 0 .. n-1:
+//   * j <  r0:            "structured" -- the pivot is row j of the running R
+//                         (upper trapezoidal, min(r0, n) rows) and the tail is
+//                         the whole chunk (Alg. QR:qnxn with a dense lower block);
+//   * r0 <= j < r0 + CH:  "dense" -- the pivot is chunk row j - r0, the tail the
+//                         chunk rows below it (ordinary Householder, DGEQR2);
+//   * j >= r0 + CH:       the chunk lies above the pivot: nothing.
+// One warp holds one chunk in registers as DMMA fragments (transposed
+// accumulator layout): lane (q = lane & 3, l4 = lane >> 2) holds
+//     a[k][cb][e] = A(chunk row 8k + 2q + e, column 8cb + l4).
+// Columns are processed in panels of 8 (p = 0 .. NCB-1): the panel's Householder
+// steps use warp shuffles only (x broadcast, 4-lane reductions); the panel's
+// T (compact WY, Alg. YT:scaled P:2007-2028, LAPACK sign R3) comes from the
+// Gram entries the steps compute anyway; the trailing update
+//     W^T = C^T Y (+ R pivot rows),  W'^T = W^T T,  C^T -= W'^T Y^T
+// runs on FP64 DMMA with the chunk registers as operands and accumulators.
+// The running R lives in shared memory (row-major, ld LDR); row block p of R is
+// the hand-off between consecutive chunks (a counter per row block).
+#pragma once
+#include <cstdint>
+#include "wy.cuh"
+
+#ifdef TSQR_PROBE
+// Probe build only (tools/probe_chain.cu): lane 0 of each warp of CTA 0 logs
+// (clock64 << 8 | event) into a per-warp shared-memory log, flushed to global
+// memory at the end of the kernel.
+__device__ unsigned long long *g_probe_buf;   // [warps][PROBE_N]
+constexpr int PROBE_N = 512, PROBE_W = 8;
+__device__ __forceinline__ unsigned long long *probe_log() {
+    __shared__ unsigned long long log[PROBE_W][PROBE_N];
+    return &log[0][0];
+}
+__device__ __forceinline__ void probe_mark(int id) {
+    if ((threadIdx.x & 31) == 0) {
+        unsigned long long *b = probe_log() + (threadIdx.x >> 5) * PROBE_N;
+        const int i = (int)b[0] + 1;
+        if (i < PROBE_N) {
+            b[i] = ((unsigned long long)clock64() << 8) | (unsigned)id;
+            b[0] = i;
+        }
+    }
+}
+__device__ __forceinline__ void probe_init() {
+    if ((threadIdx.x & 31) == 0) probe_log()[(threadIdx.x >> 5) * PROBE_N] = 0;
+}
+__device__ __forceinline__ void probe_flush() {
+    __syncthreads();
+    if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i < PROBE_W * PROBE_N; i += blockDim.x) g_probe_buf[i] = probe_log()[i];
+}
+#define PROBE(id) probe_mark(id)
+#define PROBE_INIT() probe_init()
+#define PROBE_FLUSH() probe_flush()
+#else
+#define PROBE(id)
+#define PROBE_INIT()
+#define PROBE_FLUSH()
+#endif
+
+namespace tsqr {
+namespace chunk {
+
+using wy::dmma;
+using wy::House;
+using wy::householder;
+
+constexpr unsigned FULL = 0xffffffffu;
+
+// Hand-off between consecutive chunks of one R buffer (a software pipeline
+// over the warps of a CTA).  Every chunk of the buffer's sequence has a number
+// s; counters hold "chunks done":
+//   row[j] -- chunks that have finished Householder step j (R row j's panel
+//             entries are final for them),
+//   tr[p]  -- chunks that have finished panel p's update of R rows 8p..8p+7.
+// Chunk s waits for row[j] >= s before step j and for tr[p] >= s before it
+// touches R's trailing columns, and publishes s + 1 after each.  One writer at
+// a time per counter, so every counter is monotonic.
+struct Sync {
+    int *row, *tr;
+    int s;
+};
+// Shared-memory accesses of one warp are performed in issue order, so a hand-off
+// needs only compiler barriers: the data stores precede the counter store in
+// program order (publish), and no load of the guarded data is hoisted above
+// the spin (wait).  No MEMBAR: a fence.cta would also wait for the warp's
+// outstanding global stores.
+__device__ __forceinline__ void sync_wait(const int *c, int v) {
+    while (*reinterpret_cast<const volatile int *>(c) < v) {
+    }
+    asm volatile("" ::: "memory");
+}
+__device__ __forceinline__ void sync_publish(int *c, int v) {
+    asm volatile("" ::: "memory");
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) *reinterpret_cast<volatile int *>(c) = v;
+}
+
+// dlarfg scalars (readings R1/R2/R19), branch-free: beta = -sign(alpha) N with
+// N = sqrt(alpha^2 + sigma2), tau = 1 + |alpha|/N, scale = 1/(alpha - beta);
+// sigma2 == 0 gives H = I (tau = 0, beta = alpha).  1/sqrt from the MUFU seed
+// and two Newton steps, 1/x likewise (rcp_nr): <= 2 ulp.
+__device__ __forceinline__ House house_bf(double alpha, double s2) {
+    const double y = fma(alpha, alpha, s2);
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(y));
+    const double hy = 0.5 * y;
+    r = r * fma(-hy * r, r, 1.5);
+    r = r * fma(-hy * r, r, 1.5);
+    const double N = y * r;
+    const double aa = fabs(alpha);
+    const double inv = wy::rcp_nr(aa + N);
+    const bool z = (s2 == 0.0);
+    House h;
+    h.beta = z ? alpha : (alpha >= 0.0 ? -N : N);
+    h.tau = z ? 0.0 : fma(aa, r, 1.0);
+    h.scale = z ? 0.0 : (alpha >= 0.0 ? inv : -inv);
+    return h;
+}
+
+template <int NCB_, int KM_, int NW_>
+struct Cfg {
+    static constexpr int NCB = NCB_, KM = KM_, NW = NW_;
+    static constexpr int NP = 8 * NCB, CH = 8 * KM, NT = 32 * NW;
+    static constexpr int LDR = NP + 2;                    // R buffer: R(i, c) at [i * LDR + c]
+    static constexpr int RBUF = NP * LDR;
+    // per-warp scratch: Y panel (CH x 8 row-major), Gram, T (row-major), taus
+    static constexpr int YS = 0, GS = CH * 8, TS = GS + 64, T8 = TS + 64, WS = T8 + 8;
+    static constexpr int OFF_WS = 2 * RBUF;               // after the two R buffers
+    static constexpr int OFF_SYNC = OFF_WS + NW * WS;     // per buffer: NP row + NCB panel counters
+    static constexpr int SYNC_INTS = NP + NCB;
+    static constexpr size_t BYTES = (size_t)OFF_SYNC * sizeof(double) + 2 * SYNC_INTS * sizeof(int);
+};
+
+// T (8x8, row-major) of one panel from its Gram entries G(l, c), l < c
+// (row-major in Gs) and taus t: T(r,r) = t_r, T(r,c) = -t_c sum_l T(r,l) G(l,c).
+__device__ __forceinline__ void build_t(const double *Gs, const double *t, double *Ts) {
+    const int r = threadIdx.x & 31;
+    if (r < 8) {
+        double row[8];
+        const double tr = t[r];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) row[c] = (c == r) ? tr : 0.0;
+#pragma unroll
+        for (int c = 1; c < 8; ++c) {
+            double s = 0.0;
+#pragma unroll
+            for (int l = 0; l < c; ++l) s = fma(row[l], Gs[l * 8 + c], s);
+            if (r < c) row[c] = -t[c] * s;
+        }
+#pragma unroll
+        for (int c = 0; c < 8; c += 2) *reinterpret_cast<double2 *>(Ts + r * 8 + c) = make_double2(row[c], row[c + 1]);
+    }
+    __syncwarp();
+}
+
+template <class C>
+struct Chunk {
+    double a[C::KM][C::NCB][2];
+};
+
+// --------------------------------------------------------------- panel steps
+// Structured panel P: pivots are R rows 8P .. 8P+7 (smem, Rb), the tail is the
+// whole chunk.  On exit the panel registers hold v (the reflectors' chunk part,
+// scale applied), R's pivot rows hold (beta, updated R entries) in the panel
+// columns, Gs/t8 the Gram entries and taus.
+template <class C, int P>
+__device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, double *Gs, double *t8, double *tau_out,
+                                                 int n, const Sync &sy) {
+    const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+#pragma unroll 1
+    for (int jj = 0; jj < 8; ++jj) {
+        const int j = 8 * P + jj;
+        const int src = 4 * jj + q;
+        double x[C::KM][2];
+#pragma unroll
+        for (int k = 0; k < C::KM; ++k) {
+            x[k][0] = __shfl_sync(FULL, ch.a[k][P][0], src);
+            x[k][1] = __shfl_sync(FULL, ch.a[k][P][1], src);
+        }
+        double d0 = 0.0, d1 = 0.0, s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < C::KM; ++k) {
+            d0 = fma(x[k][0], ch.a[k][P][0], d0);
+            d1 = fma(x[k][1], ch.a[k][P][1], d1);
+            s0 = fma(x[k][0], x[k][0], s0);
+            s1 = fma(x[k][1], x[k][1], s1);
+        }
+        double d = d0 + d1, s2 = s0 + s1;
+        d += __shfl_xor_sync(FULL, d, 1);
+        s2 += __shfl_xor_sync(FULL, s2, 1);
+        d += __shfl_xor_sync(FULL, d, 2);
+        s2 += __shfl_xor_sync(FULL, s2, 2);
+        PROBE(3);
+        sync_wait(sy.row + j, sy.s);                                 // R row j released by the previous chunk
+        PROBE(4);
+        const double alpha = Rb[j * C::LDR + j];
+        const double rj = Rb[j * C::LDR + 8 * P + l4];                // R(j, 8P + l4)
+        const House h = house_bf(alpha, s2);
+        const double w = fma(h.scale, d, rj);                        // v^T [R(j,c); a_c]
+        const double u = (l4 > jj) ? h.tau * h.scale * w : (l4 == jj ? 1.0 - h.scale : 0.0);
+#pragma unroll
+        for (int k = 0; k < C::KM; ++k) {
+            ch.a[k][P][0] = fma(-u, x[k][0], ch.a[k][P][0]);
+            ch.a[k][P][1] = fma(-u, x[k][1], ch.a[k][P][1]);
+        }
+        __syncwarp();                  // every lane has read R(j, .) before it is overwritten
+        const double rnew = (l4 == jj) ? h.beta : fma(-h.tau, w, rj);
+        if (q == 0 && l4 >= jj) Rb[j * C::LDR + 8 * P + l4] = rnew;
+        if (q == 0 && l4 < jj) Gs[l4 * 8 + jj] = h.scale * d;       // G(l, jj) = v_l^T v_jj
+        if (lane == 0) t8[jj] = h.tau;
+        sync_publish(sy.row + j, sy.s + 1);
+        PROBE(2);
+    }
+    __syncwarp();
+    if (lane < 8 && 8 * P + lane < n) tau_out[8 * P + lane] = t8[lane];
+}
+
+// Dense panel P: the pivots are chunk rows 8 kb .. 8 kb + 7 (kb = (8P - r0)/8).
+// On exit the panel column holds R above/at the pivot (beta on the diagonal)
+// and v below it, as DGEQR2 stores them.
+template <class C, int P>
+__device__ __forceinline__ void panel_dense(Chunk<C> &ch, int kb, double *Gs, double *t8, double *tau_out, int n) {
+    const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+#pragma unroll 1
+    for (int jj = 0; jj < 8; ++jj) {
+        const int j = 8 * P + jj;
+        const int qp = jj >> 1, ep = jj & 1;
+        const int src = 4 * jj + q;
+        double x[C::KM][2];
+        double sel = 0.0;
+#pragma unroll
+        for (int k = 0; k < C::KM; ++k) {
+            x[k][0] = __shfl_sync(FULL, ch.a[k][P][0], src);
+            x[k][1] = __shfl_sync(FULL, ch.a[k][P][1], src);
+            const bool below0 = (k > kb) || (k == kb && 2 * q > jj);
+            const bool below1 = (k > kb) || (k == kb && 2 * q + 1 > jj);
+            x[k][0] = below0 ? x[k][0] : 0.0;
+            x[k][1] = below1 ? x[k][1] : 0.0;
+            if (k == kb) sel = ep ? ch.a[k][P][1] : ch.a[k][P][0];
+        }
+        const double rj = __shfl_sync(FULL, sel, 4 * l4 + qp);       // A(pivot row, 8P + l4)
+        const double alpha = __shfl_sync(FULL, rj, 4 * jj);
+        double d0 = 0.0, d1 = 0.0, s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < C::KM; ++k) {
+            d0 = fma(x[k][0], ch.a[k][P][0], d0);
+            d1 = fma(x[k][1], ch.a[k][P][1], d1);
+            s0 = fma(x[k][0], x[k][0], s0);
+            s1 = fma(x[k][1], x[k][1], s1);
+        }
+        double d = d0 + d1, s2 = s0 + s1;
+        d += __shfl_xor_sync(FULL, d, 1);
+        s2 += __shfl_xor_sync(FULL, s2, 1);
+        d += __shfl_xor_sync(FULL, d, 2);
+        s2 += __shfl_xor_sync(FULL, s2, 2);
+        const House h = house_bf(alpha, s2);
+        const double w = fma(h.scale, d, rj);
+        const double u = (l4 > jj) ? h.tau * h.scale * w : (l4 == jj ? 1.0 - h.scale : 0.0);
+#pragma unroll
+        for (int k = 0; k < C::KM; ++k) {
+            ch.a[k][P][0] = fma(-u, x[k][0], ch.a[k][P][0]);
+            ch.a[k][P][1] = fma(-u, x[k][1], ch.a[k][P][1]);
+        }
+        const double pnew = (l4 > jj) ? fma(-h.tau, w, rj) : (l4 == jj ? h.beta : rj);
+        if (q == qp) {
+#pragma unroll
+            for (int k = 0; k < C::KM; ++k)
+                if (k == kb) {
+                    if (ep) ch.a[k][P][1] = pnew;
+                    else ch.a[k][P][0] = pnew;
+                }
+        }
+        if (q == 0 && l4 < jj) Gs[l4 * 8 + jj] = fma(h.scale, d, rj);    // G(l, jj) = y_l^T y_jj
+        if (lane == 0) t8[jj] = h.tau;
+    }
+    __syncwarp();
+    if (lane < 8 && 8 * P + lane < n) tau_out[8 * P + lane] = t8[lane];
+}
+
+// ------------------------------------------------------------ trailing update
+// C <- (I - Y T^T Y^T) C for the chunk's column blocks cb > P (kStruct: with the
+// R pivot rows 8P..8P+7 of Rb as the identity part of Y).  yv: the panel's Y
+// (B operand of W^T = C^T Y); Ys: the same Y in smem (row-major, CH x 8).
+// Order: W^T for every block (chunk registers only), then -- after the
+// previous chunk has released R's rows -- the R part, W'^T = W^T T and R's
+// update, publish, and only then the chunk's own update.
+template <class C, int P, bool kStruct>
+__device__ __forceinline__ void trailing(Chunk<C> &ch, const double (&yv)[C::KM][2], const double *Ys,
+                                         const double *Ts, double *Rb, const Sync &sy, bool defer) {
+    const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+    if constexpr (P + 1 < C::NCB) {
+        double wt[C::NCB][2];
+#pragma unroll
+        for (int cb = P + 1; cb < C::NCB; ++cb) {
+            wt[cb][0] = wt[cb][1] = 0.0;
+#pragma unroll
+            for (int k = 0; k < C::KM; ++k) {
+                dmma(wt[cb][0], wt[cb][1], ch.a[k][cb][0], yv[k][0]);
+                dmma(wt[cb][0], wt[cb][1], ch.a[k][cb][1], yv[k][1]);
+            }
+        }
+        const double tb0 = Ts[(2 * q) * 8 + l4], tb1 = Ts[(2 * q + 1) * 8 + l4];
+        PROBE(6);
+        if (kStruct) sync_wait(sy.tr + P, sy.s);
+        PROBE(9);
+#pragma unroll
+        for (int cb = P + 1; cb < C::NCB; ++cb) {
+            double *r0p = Rb + (8 * P + 2 * q) * C::LDR + 8 * cb + l4;
+            if (kStruct) {
+                wt[cb][0] += r0p[0];
+                wt[cb][1] += r0p[C::LDR];
+            }
+            double wp0 = 0.0, wp1 = 0.0;
+            dmma(wp0, wp1, wt[cb][0], tb0);
+            dmma(wp0, wp1, wt[cb][1], tb1);
+            if (kStruct) {
+                r0p[0] -= wp0;
+                r0p[C::LDR] -= wp1;
+            }
+            wt[cb][0] = -wp0;
+            wt[cb][1] = -wp1;
+        }
+        if (kStruct && !defer) sync_publish(sy.tr + P, sy.s + 1);
+        PROBE(7);
+        double yt[C::KM][2];
+#pragma unroll
+        for (int k = 0; k < C::KM; ++k) {
+            const double2 v = *reinterpret_cast<const double2 *>(Ys + (8 * k + l4) * 8 + 2 * q);
+            yt[k][0] = v.x;
+            yt[k][1] = v.y;
+        }
+#pragma unroll
+        for (int cb = P + 1; cb < C::NCB; ++cb)
+#pragma unroll
+            for (int k = 0; k < C::KM; ++k) {
+                dmma(ch.a[k][cb][0], ch.a[k][cb][1], wt[cb][0], yt[k][0]);
+                dmma(ch.a[k][cb][0], ch.a[k][cb][1], wt[cb][1], yt[k][1]);
+            }
+    } else if (kStruct) {
+        sync_wait(sy.tr + P, sy.s);
+        if (!defer) sync_publish(sy.tr + P, sy.s + 1);
+    }
+}
+
+// Panel P of the factorisation of one chunk (kind 0 structured, 1 dense, 2 none).
+template <class C, int P>
+__device__ __forceinline__ void factor_panel(Chunk<C> &ch, int kind, int kb, double *Rb, double *ws,
+                                             double *tau_out, int n, const Sync &sy, bool defer, double *tg) {
+    // defer: the caller publishes tr[P] itself (after copying R rows out);
+    // tg: this chunk's T cache (NCB x 8 x 8, row-major per panel) or null
+    const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+    double *Ys = ws + C::YS, *Gs = ws + C::GS, *Ts = ws + C::TS, *t8 = ws + C::T8;
+    if (kind != 0) {                  // the previous chunk must be done with R rows 8P..8P+7
+        sync_wait(sy.tr + P, sy.s);
+        if (kind == 2) {
+            if (lane < 8 && 8 * P + lane < n) tau_out[8 * P + lane] = 0.0;
+            if (lane < 8) sy.row[8 * P + lane] = sy.s + 1;
+            if (!defer) sync_publish(sy.tr + P, sy.s + 1);
+            return;
+        }
+    }
+    double yv[C::KM][2];
+    PROBE(1);
+    if (kind == 0) {
+        panel_structured<C, P>(ch, Rb, Gs, t8, tau_out, n, sy);
+#pragma unroll
+        for (int k = 0; k < C::KM; ++k) {
+            yv[k][0] = ch.a[k][P][0];
+            yv[k][1] = ch.a[k][P][1];
+        }
+    } else {
+        panel_dense<C, P>(ch, kb, Gs, t8, tau_out, n);
+        const int piv = 8 * kb + l4;                      // chunk row of this lane's column's pivot
+#pragma unroll
+        for (int k = 0; k < C::KM; ++k)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int r = 8 * k + 2 * q + e;
+                yv[k][e] = r > piv ? ch.a[k][P][e] : (r == piv ? 1.0 : 0.0);
+            }
+    }
+#pragma unroll
+    for (int k = 0; k < C::KM; ++k) {
+        Ys[(8 * k + 2 * q) * 8 + l4] = yv[k][0];
+        Ys[(8 * k + 2 * q + 1) * 8 + l4] = yv[k][1];
+    }
+    __syncwarp();
+    PROBE(5);
+    build_t(Gs, t8, Ts);
+    PROBE(10);
+    if (tg != nullptr)                    // cache T (compact WY of the panel) for apply / form Q
+        *reinterpret_cast<double2 *>(tg + 8 * P * 8 + 2 * lane) = *reinterpret_cast<const double2 *>(Ts + 2 * lane);
+    if (kind == 0) trailing<C, P, true>(ch, yv, Ys, Ts, Rb, sy, defer);
+    else {
+        trailing<C, P, false>(ch, yv, Ys, Ts, Rb, sy, defer);
+        // the pivot block rows are R rows 8P .. 8P+7 from here on
+#pragma unroll
+        for (int k = 0; k < C::KM; ++k)
+            if (k == kb) {
+#pragma unroll
+                for (int cb = P; cb < C::NCB; ++cb) {
+                    Rb[(8 * P + 2 * q) * C::LDR + 8 * cb + l4] = ch.a[k][cb][0];
+                    Rb[(8 * P + 2 * q + 1) * C::LDR + 8 * cb + l4] = ch.a[k][cb][1];
+                }
+            }
+        asm volatile("" ::: "memory");
+        __syncwarp();
+        if (lane < 8) sy.row[8 * P + lane] = sy.s + 1;
+        if (!defer) sync_publish(sy.tr + P, sy.s + 1);
+    }
+    __syncwarp();
+}
+
+}  // namespace chunk
+}  // namespace tsqr

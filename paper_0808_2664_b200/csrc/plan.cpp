@@ -11,11 +11,12 @@ namespace tsqr {
 
 int padded_width(int64_t n) { return n <= 16 ? 16 : (n <= 32 ? 32 : 64); }
 
-// Tallest tile one column-owner team can keep in registers (two row groups of
-// 96-row bands), and the default tile: one 96-row band per lane, so a team is a
-// single warp (n <= 32) or two (n <= 64) and several teams share an SM.
-int64_t tile_capacity(int64_t) { return 192; }
-int64_t default_tile_rows(int64_t) { return 96; }
+// A tile is factored as a flat chain of register-resident chunks (chunk.cuh),
+// so its height is bounded only by the 32-bit row count of the device plan.
+// Default tile: 32 chunks of the chain.
+int64_t tile_capacity(int64_t) { return (int64_t)1 << 30; }
+int64_t default_tile_rows(int64_t n) { return 32 * (int64_t)chunk_rows_for(n); }
+int chunk_rows_for(int64_t n) { return n <= 32 ? 64 : 32; }
 
 static int64_t block_count(int64_t m, int64_t n, int64_t b, int64_t *last_rows) {
     // Reading R6: blocks of b rows; a remainder >= n is its own block, a
@@ -86,6 +87,9 @@ int build_plan(int64_t m_local, int64_t n, int64_t block_rows, int64_t tile_rows
     p->blk_tile0.push_back((int)p->tile_row0.size());
     if ((int64_t)p->tile_row0.size() > ((int64_t)1 << 31) - 1) return TSQR_ERR_UNSUPPORTED;
     const int L = p->ntiles();
+    p->c = chunk_rows_for(n);
+    p->tile_chunk0.assign(L + 1, 0);
+    for (int t = 0; t < L; ++t) p->tile_chunk0[t + 1] = p->tile_chunk0[t] + (p->tile_rows[t] + p->c - 1) / p->c;
     p->max_rows = *std::max_element(p->tile_rows.begin(), p->tile_rows.end());
     p->min_rows = *std::min_element(p->tile_rows.begin(), p->tile_rows.end());
 

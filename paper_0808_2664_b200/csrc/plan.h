@@ -18,6 +18,8 @@ struct PlanNode {
 
 struct Plan {
     int64_t m_local = 0, n = 0, b = 0, s = 0;
+    int c = 32;                            // chunk rows of the tiles' flat chains
+    std::vector<int64_t> tile_chunk0;      // first chunk of each tile (+ total)
     int nranks = 1, rank = 0;
     std::vector<int64_t> tile_row0, tile_rows;
     std::vector<int> blk_tile0;            // first tile of each row block (+ sentinel)
@@ -35,6 +37,7 @@ struct Plan {
 int padded_width(int64_t n);
 int64_t tile_capacity(int64_t n);
 int64_t default_tile_rows(int64_t n);
+int chunk_rows_for(int64_t n);
 
 // Returns 0 on success, else a tsqr_status_t code.
 int build_plan(int64_t m_local, int64_t n, int64_t block_rows, int64_t tile_rows,

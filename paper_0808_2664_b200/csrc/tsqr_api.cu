@@ -31,6 +31,13 @@ struct tsqr_tree_s {
     int cross_rounds = 0, cross_done = 0;
     double *d_xbuf = nullptr;
     int *d_step_ids = nullptr;
+    // chunk-chain leaf stage
+    int64_t *d_tile_chunk0 = nullptr;
+    int *d_cta_tile0 = nullptr;
+    int chain_grid = 0;
+    double *d_tau_chunk = nullptr;
+    double *d_tcache = nullptr;       // [chunks][NCB][8][8] panel T factors (compact WY)
+    int64_t nchunks = 0;
     std::vector<int> step_off;   // top-down: groups [step_off[g], step_off[g+1])
     DevPlan dplan{};
 };
@@ -54,7 +61,7 @@ static tsqr_status_t debug_sync(const tsqr_tree_s *t, cudaStream_t st, const cha
 static void free_tree_memory(tsqr_tree_s *t) {
     void *ptrs[] = {t->d_row0, t->d_rows, t->d_tparent, t->d_node_a, t->d_nparent, t->d_tau_tile,
                     t->d_tau_node, t->d_counters, t->d_cross_y1, t->d_cross_tau, t->d_xbuf,
-                    t->d_step_ids};
+                    t->d_step_ids, t->d_tile_chunk0, t->d_cta_tile0, t->d_tau_chunk, t->d_tcache};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -120,6 +127,8 @@ tsqr_status_t tsqr_plan_info(int64_t m_local, int64_t n, const tsqr_opts_t *opts
     info->max_tile_rows = p.max_rows;
     info->min_tile_rows = p.min_rows;
     info->tile_capacity = tile_capacity(n);
+    info->chunk_rows = p.c;
+    info->nchunks = p.tile_chunk0.back();
     return TSQR_OK;
 }
 
@@ -196,6 +205,17 @@ static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t 
     alloc((void **)&t->d_cross_y1, sizeof(double) * (t->cross_rounds + 1) * n * n);
     alloc((void **)&t->d_cross_tau, sizeof(double) * (t->cross_rounds + 1) * n);
     alloc((void **)&t->d_step_ids, sizeof(int) * (ids.size() + 1));
+    const int64_t nchunks = p.tile_chunk0[L];
+    int grid = chain_grid((int)n, p.c);
+    if (grid > L) grid = L;
+    std::vector<int> cta_tile0;
+    chain_partition(p.tile_rows, p.c, grid, cta_tile0);
+    t->chain_grid = grid;
+    alloc((void **)&t->d_tile_chunk0, sizeof(int64_t) * (L + 1));
+    alloc((void **)&t->d_cta_tile0, sizeof(int) * (grid + 1));
+    alloc((void **)&t->d_tau_chunk, sizeof(double) * nchunks * n);
+    alloc((void **)&t->d_tcache, sizeof(double) * nchunks * chain_ncb((int)n, p.c) * 64);
+    t->nchunks = nchunks;
     if (e != cudaSuccess) {
         free_tree_memory(t);
         delete t;
@@ -211,6 +231,10 @@ static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t 
     if (e == cudaSuccess) e = cudaMemcpy(t->d_nparent, p.node_parent.data(), sizeof(int) * L, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && !ids.empty())
         e = cudaMemcpy(t->d_step_ids, ids.data(), sizeof(int) * ids.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(t->d_tile_chunk0, p.tile_chunk0.data(), sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(t->d_cta_tile0, cta_tile0.data(), sizeof(int) * (grid + 1), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemset(t->d_counters, 0, sizeof(int) * L);
     if (e == cudaSuccess) e = cudaMemset(t->d_tau_node, 0, sizeof(double) * L * n);
     if (e != cudaSuccess) {
@@ -262,7 +286,12 @@ tsqr_status_t tsqr_factor(int64_t m_local, int64_t n, double *A, int64_t lda, do
     f.plan = t->dplan;
     f.tau_tile = t->d_tau_tile; f.tau_node = t->d_tau_node; f.counters = t->d_counters;
     f.R = R; f.ldr = ldr;
-    CUDA_TRY(launch_factor(f, t->stream), "tsqr_factor launch");
+    ChainArgs ca;
+    ca.A = A; ca.lda = lda; ca.n = (int)n; ca.chunk_rows = t->plan.c;
+    ca.tile_row0 = t->d_row0; ca.tile_rows = t->d_rows; ca.tile_chunk0 = t->d_tile_chunk0;
+    ca.cta_tile0 = t->d_cta_tile0; ca.grid = t->chain_grid; ca.tau = t->d_tau_chunk; ca.tcache = t->d_tcache;
+    CUDA_TRY(launch_chain_factor(ca, t->stream), "tsqr_factor leaves");
+    CUDA_TRY(launch_tree(f, t->stream), "tsqr_factor tree");
     return debug_sync(t, t->stream, "tsqr_factor");
 }
 
@@ -307,7 +336,13 @@ tsqr_status_t tsqr_apply_qt(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, do
     f.C = C; f.ldc = ldc; f.k = (int)k;
     f.form_q = 0; f.xbuf = nullptr;
     cudaStream_t st = (cudaStream_t)stream;
-    CUDA_TRY(launch_apply(f, st), "tsqr_apply_qt launch");
+    ChainApplyArgs ca;
+    ca.A = t->A; ca.lda = t->lda; ca.n = (int)t->plan.n; ca.chunk_rows = t->plan.c;
+    ca.tile_row0 = t->d_row0; ca.tile_rows = t->d_rows; ca.tile_chunk0 = t->d_tile_chunk0;
+    ca.cta_tile0 = t->d_cta_tile0; ca.grid = t->chain_grid; ca.tcache = t->d_tcache;
+    ca.C = C; ca.ldc = ldc; ca.k = (int)k; ca.forward = 1; ca.xbuf = nullptr;
+    CUDA_TRY(launch_chain_apply(ca, st), "tsqr_apply_qt leaves");
+    if (t->plan.ntiles() > 1) CUDA_TRY(launch_apply_nodes(f, st), "tsqr_apply_qt nodes");
     if (top) CUDA_TRY(launch_copy_block(C, ldc, top, ldtop, (int)t->plan.n, (int)k, st), "tsqr_apply_qt top");
     t->stream = st;
     return debug_sync(t, st, "tsqr_apply_qt");
@@ -361,15 +396,12 @@ tsqr_status_t tsqr_form_q(tsqr_tree_t t, double *Q, int64_t ldq, void *stream) {
                                     t->d_step_ids + t->step_off[g], cnt, t->d_xbuf, st),
                  "tsqr_form_q nodes");
     }
-    ApplyArgs f;
-    f.NP = t->NP;
-    f.max_rows = t->plan.max_rows;
-    f.A = t->A; f.lda = t->lda; f.n = n;
-    f.plan = t->dplan;
-    f.tau_tile = t->d_tau_tile; f.tau_node = t->d_tau_node; f.counters = t->d_counters;
-    f.C = Q; f.ldc = ldq; f.k = n;
-    f.form_q = 1; f.xbuf = t->d_xbuf;
-    CUDA_TRY(launch_apply(f, st), "tsqr_form_q leaves");
+    ChainApplyArgs ca;
+    ca.A = t->A; ca.lda = t->lda; ca.n = n; ca.chunk_rows = t->plan.c;
+    ca.tile_row0 = t->d_row0; ca.tile_rows = t->d_rows; ca.tile_chunk0 = t->d_tile_chunk0;
+    ca.cta_tile0 = t->d_cta_tile0; ca.grid = t->chain_grid; ca.tcache = t->d_tcache;
+    ca.C = Q; ca.ldc = ldq; ca.k = n; ca.forward = 0; ca.xbuf = t->d_xbuf;
+    CUDA_TRY(launch_chain_apply(ca, st), "tsqr_form_q leaves");
     t->stream = st;
     return debug_sync(t, st, "tsqr_form_q");
 }
@@ -385,8 +417,9 @@ tsqr_status_t tsqr_tree_free(tsqr_tree_t t) {
 tsqr_status_t tsqr_tree_export_tau(tsqr_tree_t t, double *tau_tile_host, double *tau_node_host) {
     if (!t) return TSQR_ERR_INVALID;
     const size_t bytes = sizeof(double) * (size_t)t->plan.ntiles() * t->plan.n;
+    const size_t cbytes = sizeof(double) * (size_t)t->nchunks * t->plan.n;
     if (t->stream) CUDA_TRY(cudaStreamSynchronize(t->stream), "tsqr_tree_export_tau");
-    if (tau_tile_host) CUDA_TRY(cudaMemcpy(tau_tile_host, t->d_tau_tile, bytes, cudaMemcpyDeviceToHost), "export");
+    if (tau_tile_host) CUDA_TRY(cudaMemcpy(tau_tile_host, t->d_tau_chunk, cbytes, cudaMemcpyDeviceToHost), "export");
     if (tau_node_host) CUDA_TRY(cudaMemcpy(tau_node_host, t->d_tau_node, bytes, cudaMemcpyDeviceToHost), "export");
     return TSQR_OK;
 }

@@ -2,6 +2,7 @@
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
+#include <vector>
 
 
 namespace tsqr {
@@ -39,7 +40,37 @@ struct ApplyArgs {
 };
 
 cudaError_t launch_factor(const FactorArgs &f, cudaStream_t st);
+
+// Leaf stage on the chunk engine (tsqr_chain.cu).
+struct ChainArgs {
+    double *A; int64_t lda; int n;
+    int chunk_rows;              // 32 or 64 (chain_chunk_rows(n))
+    const int64_t *tile_row0; const int *tile_rows; const int64_t *tile_chunk0;
+    const int *cta_tile0; int grid;
+    double *tau;                 // [chunks][n]
+    double *tcache;              // [chunks][NCB][8][8]: the panels' T (compact WY), may be null
+};
+// Leaf stage of Q^T C (forward) or of form Q (Q = Q_leaves [X; 0], !forward).
+struct ChainApplyArgs {
+    const double *A; int64_t lda; int n;
+    int chunk_rows;
+    const int64_t *tile_row0; const int *tile_rows; const int64_t *tile_chunk0;
+    const int *cta_tile0; int grid;
+    const double *tcache;        // the factor's T cache
+    double *C; int64_t ldc; int k;
+    int forward;
+    const double *xbuf;          // !forward: per-tile X (n x n) from the node stage
+};
+cudaError_t launch_chain_apply(const ChainApplyArgs &f, cudaStream_t st);
+int chain_chunk_rows(int n);
+int chain_grid(int n, int chunk_rows);
+cudaError_t launch_chain_factor(const ChainArgs &f, cudaStream_t st);
+void chain_partition(const std::vector<int64_t> &tile_rows, int chunk_rows, int grid, std::vector<int> &cta_tile0);
+// Tree stage only (ticketed climb from every tile), after launch_chain_factor.
+cudaError_t launch_tree(const FactorArgs &f, cudaStream_t st);
 cudaError_t launch_apply(const ApplyArgs &f, cudaStream_t st);
+cudaError_t launch_apply_nodes(const ApplyArgs &f, cudaStream_t st);
+int chain_ncb(int n, int chunk_rows);          // column blocks of the compiled configuration
 cudaError_t launch_formq_nodes(int NP, const double *A, int64_t lda, int n, const DevPlan &plan,
                                const double *tau_node, const int *ids, int count, double *xbuf,
                                cudaStream_t st);

@@ -266,7 +266,7 @@ __device__ __forceinline__ void warp_qr(double *sm, int n, int nrb, double *Ra, 
     }
 }
 
-template <class G>
+template <class G, bool kLeaf>
 __global__ void __launch_bounds__(32)
 k_factor_w(double *A, int64_t lda, int n, DevPlan plan, double *tau_tile, double *tau_node, int *counters, double *R,
            int64_t ldr) {
@@ -275,16 +275,17 @@ k_factor_w(double *A, int64_t lda, int n, DevPlan plan, double *tau_tile, double
     double *tile = sm + SM::tile;
     const int lane = threadIdx.x;
     const int t = blockIdx.x;
-    const int64_t row0 = plan.tile_row0[t];
-    const int rows = plan.tile_rows[t];
-    double *At = A + row0;
-
-    for (int j = lane; j < G::NP; j += 32) sm[SM::taus + j] = 0.0;   // padding reflectors: H = I
-    stage_in<32>(tile, G::LD, At, lda, rows, n, G::S, G::NP);
-    __syncwarp();
-    warp_qr<G, false>(sm, n, (rows + 7) / 8, nullptr, 0);
-    stage_out<32>(tile, G::LD, At, lda, rows, n);
-    for (int j = lane; j < n; j += 32) tau_tile[(int64_t)t * n + j] = sm[SM::taus + j];
+    if (kLeaf) {
+        const int64_t row0 = plan.tile_row0[t];
+        const int rows = plan.tile_rows[t];
+        double *At = A + row0;
+        for (int j = lane; j < G::NP; j += 32) sm[SM::taus + j] = 0.0;   // padding reflectors: H = I
+        stage_in<32>(tile, G::LD, At, lda, rows, n, G::S, G::NP);
+        __syncwarp();
+        warp_qr<G, false>(sm, n, (rows + 7) / 8, nullptr, 0);
+        stage_out<32>(tile, G::LD, At, lda, rows, n);
+        for (int j = lane; j < n; j += 32) tau_tile[(int64_t)t * n + j] = sm[SM::taus + j];
+    }
 
     int p = plan.tile_parent[t];
     bool root = (p < 0);
@@ -357,7 +358,7 @@ __device__ __forceinline__ void load_tile_y(double *sm, const double *At, int64_
     __syncthreads();
 }
 
-template <class G, int CCOLS>
+template <class G, int CCOLS, bool kLeaf>
 __global__ void __launch_bounds__(G::NT)
 k_apply_qt(const double *A, int64_t lda, int n, DevPlan plan, const double *tau_tile, const double *tau_node,
            int *counters, double *C, int64_t ldc, int k) {
@@ -366,19 +367,21 @@ k_apply_qt(const double *A, int64_t lda, int n, DevPlan plan, const double *tau_
     int *flag = reinterpret_cast<int *>(sm + SM::flag);
     double *tile = sm + SM::tile;
     const int t = blockIdx.x;
-    const int64_t row0 = plan.tile_row0[t];
-    const int rows = plan.tile_rows[t];
-    for (int j = threadIdx.x; j < G::NP; j += G::NT) sm[SM::taus + j] = j < n ? tau_tile[(int64_t)t * n + j] : 0.0;
-    load_tile_y<G, CCOLS>(sm, A + row0, lda, rows, n);
-    build_all_t<G, CCOLS, false>(sm, n, rows);
-    double *Ct = C + row0;
-    for (int c0 = 0; c0 < k; c0 += CCOLS) {
-        const int kc = min(CCOLS, k - c0);
-        stage_in<G::NT>(tile, G::LD, Ct + (int64_t)c0 * ldc, ldc, rows, kc, G::S, CCOLS);
-        __syncthreads();
-        apply_panels<G, CCOLS, false, true>(sm, n, rows, kc);
-        stage_out<G::NT>(tile, G::LD, Ct + (int64_t)c0 * ldc, ldc, rows, kc);
-        __syncthreads();
+    if (kLeaf) {
+        const int64_t row0 = plan.tile_row0[t];
+        const int rows = plan.tile_rows[t];
+        for (int j = threadIdx.x; j < G::NP; j += G::NT) sm[SM::taus + j] = j < n ? tau_tile[(int64_t)t * n + j] : 0.0;
+        load_tile_y<G, CCOLS>(sm, A + row0, lda, rows, n);
+        build_all_t<G, CCOLS, false>(sm, n, rows);
+        double *Ct = C + row0;
+        for (int c0 = 0; c0 < k; c0 += CCOLS) {
+            const int kc = min(CCOLS, k - c0);
+            stage_in<G::NT>(tile, G::LD, Ct + (int64_t)c0 * ldc, ldc, rows, kc, G::S, CCOLS);
+            __syncthreads();
+            apply_panels<G, CCOLS, false, true>(sm, n, rows, kc);
+            stage_out<G::NT>(tile, G::LD, Ct + (int64_t)c0 * ldc, ldc, rows, kc);
+            __syncthreads();
+        }
     }
     // node stage (eq. localQTupdate) on the head rows, climbing the tree
     int p = plan.tile_parent[t];
@@ -625,13 +628,24 @@ int team_rows_for(int64_t max_rows) {
     return 192;
 }
 
-template <class G>
+template <class G, bool kLeaf = true>
 static cudaError_t launch_factor_w_t(const FactorArgs &f, cudaStream_t st) {
     const size_t sm = WSmem<G>::bytes;
-    cudaError_t e = set_smem((const void *)k_factor_w<G>, sm);
+    cudaError_t e = set_smem((const void *)k_factor_w<G, kLeaf>, sm);
     if (e != cudaSuccess) return e;
-    k_factor_w<G><<<f.plan.L, 32, sm, st>>>(f.A, f.lda, f.n, f.plan, f.tau_tile, f.tau_node, f.counters, f.R, f.ldr);
+    k_factor_w<G, kLeaf><<<f.plan.L, 32, sm, st>>>(f.A, f.lda, f.n, f.plan, f.tau_tile, f.tau_node, f.counters, f.R,
+                                                    f.ldr);
     return cudaGetLastError();
+}
+
+cudaError_t launch_tree(const FactorArgs &f, cudaStream_t st) {
+    switch ((f.n + 7) / 8) {
+        case 1: case 2: return launch_factor_w_t<WGeo<2, 8>, false>(f, st);
+        case 3: case 4: return launch_factor_w_t<WGeo<4, 8>, false>(f, st);
+        case 5: case 6: return launch_factor_w_t<WGeo<6, 8>, false>(f, st);
+        case 7: return launch_factor_w_t<WGeo<7, 8>, false>(f, st);
+        default: return launch_factor_w_t<WGeo<8, 8>, false>(f, st);
+    }
 }
 
 template <int NCB>
@@ -662,10 +676,10 @@ static cudaError_t launch_apply_t(const ApplyArgs &f, cudaStream_t st) {
         if (e != cudaSuccess) return e;
         k_formq_leaf<G, CCOLS><<<f.plan.L, G::NT, sm, st>>>(f.A, f.lda, f.n, f.plan, f.tau_tile, f.xbuf, f.C, f.ldc);
     } else {
-        e = set_smem((const void *)k_apply_qt<G, CCOLS>, sm);
+        e = set_smem((const void *)k_apply_qt<G, CCOLS, true>, sm);
         if (e != cudaSuccess) return e;
-        k_apply_qt<G, CCOLS><<<f.plan.L, G::NT, sm, st>>>(f.A, f.lda, f.n, f.plan, f.tau_tile, f.tau_node,
-                                                          f.counters, f.C, f.ldc, f.k);
+        k_apply_qt<G, CCOLS, true><<<f.plan.L, G::NT, sm, st>>>(f.A, f.lda, f.n, f.plan, f.tau_tile, f.tau_node,
+                                                                f.counters, f.C, f.ldc, f.k);
     }
     return cudaGetLastError();
 }
@@ -677,6 +691,22 @@ static cudaError_t launch_apply_n(const ApplyArgs &f, cudaStream_t st) {
         case 128: return launch_apply_t<Geo<NCB, 16, NCB>, 8 * NCB>(f, st);
         default: return launch_apply_t<Geo<NCB, 24, NCB>, 8 * NCB>(f, st);
     }
+}
+
+// Node stage only of Q^T C (eq. localQTupdate on the tile heads), after the leaf stage.
+template <class G>
+static cudaError_t launch_apply_nodes_t(const ApplyArgs &f, cudaStream_t st) {
+    constexpr int CCOLS = G::NP;
+    const size_t sm = Smem<G, CCOLS>::bytes;
+    cudaError_t e = set_smem((const void *)k_apply_qt<G, CCOLS, false>, sm);
+    if (e != cudaSuccess) return e;
+    k_apply_qt<G, CCOLS, false><<<f.plan.L, G::NT, sm, st>>>(f.A, f.lda, f.n, f.plan, f.tau_tile, f.tau_node,
+                                                             f.counters, f.C, f.ldc, f.k);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_apply_nodes(const ApplyArgs &f, cudaStream_t st) {
+    return f.NP <= 32 ? launch_apply_nodes_t<Geo<4, 8, 4>>(f, st) : launch_apply_nodes_t<Geo<8, 8, 8>>(f, st);
 }
 
 cudaError_t launch_apply(const ApplyArgs &f, cudaStream_t st) {

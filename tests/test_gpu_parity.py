@@ -25,13 +25,18 @@ def _np(t):
     return inputs.to_numpy_colmajor(t)
 
 
+def _chunk_rows(m, n, b, s):
+    """The chunk height the library's plan uses for the tiles' flat chains."""
+    return T.plan_info(m, n, block_rows=b, tile_rows=s)["chunk_rows"]
+
+
 def _run(m, n, b, s, seed=0, kind="gauss"):
     At = inputs.gaussian(m, n, seed) if kind == "gauss" else inputs.conditioned(m, n, seed, kappa=1e10)
     A0 = _np(At).copy()
     Ad = At.cuda()
     R, tree = T.factor(Ad, block_rows=b, tile_rows=s, debug=True)
     torch.cuda.synchronize()
-    p = orc.plan(m, n, b, s, 1)
+    p = orc.plan(m, n, b, s, 1, _chunk_rows(m, n, b, s))
     f = orc.tsqr_factor(A0, p)
     return A0, Ad, R, tree, p, f
 
@@ -51,6 +56,11 @@ CASES = [
     (12000, 16, 12000, 192),
     (4096 * 3, 64, 4096, 96),
     (4096 * 3, 50, 4096, 64),
+    (20000, 50, 4096, 704),      # config-2 tiles: 22 chunks of 32 rows per tile
+    (50000, 64, 4096, 4096),     # config-4 style: one 4096-row tile per block (128 chunks)
+    (40000, 32, 4096, 4096),     # config-5 style: 64-row chunks
+    (1000, 50, 1000, 1000),      # one tile, ragged last chunk (1000 = 31*32 + 8)
+    (77, 50, 77, 77),            # one tile, three chunks, the last 13 rows
 ]
 
 
@@ -93,7 +103,9 @@ def test_form_q(m, n, b, s):
 
 @pytest.mark.parametrize("m,n,b,s,k", [(4096, 16, 512, 128, 16), (3000, 24, 700, 175, 37), (2048, 64, 512, 128, 64),
                                        (1500, 33, 400, 128, 130), (9000, 32, 4096, 96, 128), (777, 5, 100, 30, 1),
-                                       (5000, 50, 4096, 192, 64), (4096, 64, 4096, 64, 200)])
+                                       (5000, 50, 4096, 192, 64), (4096, 64, 4096, 64, 200),
+                                       (20000, 50, 4096, 704, 64), (40000, 32, 4096, 4096, 128),
+                                       (1000, 50, 1000, 1000, 70)])
 def test_apply_qt(m, n, b, s, k):
     A0, Ad, R, tree, p, f = _run(m, n, b, s, seed=5)
     Ct = inputs.gaussian(m, k, seed=1)
@@ -157,7 +169,7 @@ def test_degenerate_inputs():
         assert np.linalg.norm(Rg.T @ Rg - M.T @ M) <= 1e-14 * max(np.linalg.norm(M), 1.0) ** 2
         if fr:
             # full rank: R is unique and both sides use the same sign convention
-            f = orc.tsqr_factor(M, orc.plan(m, n, 256, 128, 1))
+            f = orc.tsqr_factor(M, orc.plan(m, n, 256, 128, 1, _chunk_rows(m, n, 256, 128)))
             assert orc.rel_fro(Rg, f.R) <= TOL_R
         else:
             # rank deficient: R's rows after a dependent column are set by rounding noise,

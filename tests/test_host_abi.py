@@ -56,6 +56,9 @@ def test_plan_matches_oracle(m, n, b, s):
     assert mine == _oracle_nodes(p)
     info = T.plan_info(m, n, block_rows=b, tile_rows=s)
     assert info["ntiles"] == p.ntiles and info["nnodes"] == p.nnodes == p.ntiles - 1
+    # the tiles' flat chains: chunk rows and the chunk count the oracle derives from them
+    pc = orc.plan(m, n, b, s, 1, info["chunk_rows"])
+    assert info["chunk_rows"] in (32, 64) and info["nchunks"] == pc.tile_chunk0[-1]
 
 
 @pytest.mark.parametrize("m,n,b,G", [(1_000_000, 50, 4096, 8), (100_000, 64, 2048, 4), (33_554_432, 32, 4096, 8),
@@ -112,11 +115,11 @@ def test_factor_validation_without_gpu():
     assert _factor_status(100, 10, None, 100, None, 0, o)[0] == 1        # null A
     assert _factor_status(100, 10, fake, 99, None, 0, o)[0] == 1         # lda < m
     assert _factor_status(100, 10, fake, 100, fake, 9, o)[0] == 1        # ldr < n
-    assert _factor_status(100, 10, fake, 100, None, 0, T.api.opts(block_rows=64, tile_rows=5000))[0] == 3
+    assert _factor_status(100, 10, fake, 100, None, 0, T.api.opts(block_rows=64, tile_rows=(1 << 30) + 1))[0] == 3
     assert _factor_status(100, 40, fake, 100, None, 0, T.api.opts(block_rows=30, tile_rows=30))[0] == 2  # block < n
     assert _factor_status(1000, 10, fake, 1000, None, 0, T.api.opts(block_rows=64, nranks=3))[0] == 3
     with pytest.raises(_lib.TsqrError):
-        T.plan_info(100, 10, block_rows=64, tile_rows=500)
+        T.plan_info(100, 10, block_rows=64, tile_rows=1 << 31)
 
 
 def test_apply_validation_without_gpu():

@@ -109,10 +109,10 @@ class OracleEngine:
 
 
 # -------------------------------------------------------------- reference
-def _global_reference(m, n, b, s, G, k):
+def _global_reference(m, n, b, s, G, k, c=0):
     A = inputs.to_numpy_colmajor(inputs.gaussian(m, n, 0))
     C = inputs.to_numpy_colmajor(inputs.gaussian(m, k, 1))
-    f = orc.tsqr_factor(A, orc.plan(m, n, b, s, G))
+    f = orc.tsqr_factor(A, orc.plan(m, n, b, s, G, c))
     return f.R, orc.tsqr_apply_qt(f, C), orc.tsqr_form_q(f)
 
 
@@ -181,7 +181,8 @@ def test_butterfly_virtual_ranks_cuda(G, m, n, b, s, k):
     tdist.apply_qt_virtual(states, cs)
     Qs = [tdist.form_q(st) for st in states]
     torch.cuda.synchronize()
-    Rref, QtC_ref, Qref = _global_reference(m, n, b, s, G, k)
+    c = api.plan_info(rows[0][1], n, block_rows=b, tile_rows=s, nranks=G, rank=0)["chunk_rows"]
+    Rref, QtC_ref, Qref = _global_reference(m, n, b, s, G, k, c)
     for st, (row0, ml), C, Q in zip(states, rows, cs, Qs):
         R = inputs.to_numpy_colmajor(st.R)
         assert np.array_equal(R, inputs.to_numpy_colmajor(states[0].R))   # bitwise replicated

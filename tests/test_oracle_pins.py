@@ -283,6 +283,7 @@ def test_plan_rejects(args):
 
 
 # ---------------------------------------------------------------------- TSQR
+@pytest.mark.parametrize("c", [0, 32])
 @pytest.mark.parametrize("m,n,b,s,G", [
     (64, 6, 16, 16, 4),                 # S:218 P=4 binary on 64x6
     (4096, 16, 512, 512, 1),            # config 1
@@ -290,9 +291,9 @@ def test_plan_rejects(args):
     (2048, 64, 512, 256, 4),
     (1500, 33, 400, 128, 1),
 ])
-def test_tsqr_r_vs_flat(m, n, b, s, G):
+def test_tsqr_r_vs_flat(m, n, b, s, G, c):
     A = _rng(m + n + b).standard_normal((m, n))
-    f = orc.tsqr_factor(A, orc.plan(m, n, b, s, G))
+    f = orc.tsqr_factor(A, orc.plan(m, n, b, s, G, c))
     Rflat = np.triu(orc.hqr(A)[0][:n])
     assert np.all(np.tril(f.R, -1) == 0.0)
     assert orc.rel_fro(orc.sign_normalise(f.R), orc.sign_normalise(Rflat)) <= 1e-13
@@ -315,11 +316,13 @@ def test_tsqr_r_vs_mgs_tiny():
     assert orc.rel_fro(orc.sign_normalise(f.R), Rm) <= 1e-13
 
 
-@pytest.mark.parametrize("m,n,b,s,G,k", [(512, 8, 128, 64, 2, 5), (1200, 16, 300, 150, 1, 16)])
-def test_tsqr_apply_qt_closed_forms(m, n, b, s, G, k):
+@pytest.mark.parametrize("m,n,b,s,G,k,c", [(512, 8, 128, 64, 2, 5, 0), (1200, 16, 300, 150, 1, 16, 0),
+                                           (512, 8, 128, 64, 2, 5, 16), (1200, 16, 300, 150, 1, 16, 32),
+                                           (1000, 40, 500, 500, 1, 7, 32)])
+def test_tsqr_apply_qt_closed_forms(m, n, b, s, G, k, c):
     rng = _rng(m * k)
     A = rng.standard_normal((m, n))
-    p = orc.plan(m, n, b, s, G)
+    p = orc.plan(m, n, b, s, G, c)
     f = orc.tsqr_factor(A, p)
     # Q^T A = [R; 0] in tree order
     QtA = orc.tsqr_apply_qt(f, A)
@@ -334,10 +337,12 @@ def test_tsqr_apply_qt_closed_forms(m, n, b, s, G, k):
     assert np.linalg.norm(QtC[:n] - Q.T @ C) <= 1e-13 * np.linalg.norm(C)
 
 
-@pytest.mark.parametrize("m,n,b,s,G", [(4096, 16, 512, 512, 1), (3000, 30, 1000, 200, 2)])
-def test_tsqr_form_q(m, n, b, s, G):
+@pytest.mark.parametrize("m,n,b,s,G,c", [(4096, 16, 512, 512, 1, 0), (3000, 30, 1000, 200, 2, 0),
+                                         (4096, 16, 512, 512, 1, 64), (3000, 30, 1000, 200, 2, 32),
+                                         (2000, 50, 1000, 1000, 1, 32)])
+def test_tsqr_form_q(m, n, b, s, G, c):
     A = _rng(m - n).standard_normal((m, n))
-    f = orc.tsqr_factor(A, orc.plan(m, n, b, s, G))
+    f = orc.tsqr_factor(A, orc.plan(m, n, b, s, G, c))
     Q = orc.tsqr_form_q(f)
     assert np.linalg.norm(A - Q @ f.R) / np.linalg.norm(A) <= 1e-13
     assert np.linalg.norm(Q.T @ Q - np.eye(n)) <= 1e-13
@@ -363,13 +368,14 @@ def test_tsqr_ill_conditioned_invariants():
     sig = 10.0 ** (-10.0 * np.arange(n) / (n - 1))
     V, _ = np.linalg.qr(rng.standard_normal((n, n)))
     A = (G * sig) @ V.T
-    f = orc.tsqr_factor(A, orc.plan(4096, n, 512, 256, 1))
-    Q = orc.tsqr_form_q(f)
-    assert np.linalg.norm(A - Q @ f.R) / np.linalg.norm(A) <= 1e-13
-    assert np.linalg.norm(Q.T @ Q - np.eye(n)) <= 1e-13
-    assert np.linalg.norm(f.R.T @ f.R - A.T @ A) / np.linalg.norm(A) ** 2 <= 1e-14
-    Rflat = np.linalg.qr(A, mode="r")
-    assert orc.rel_fro(orc.sign_normalise(f.R), orc.sign_normalise(Rflat)) <= 1e-13
+    for c in (0, 32):
+        f = orc.tsqr_factor(A, orc.plan(4096, n, 512, 256, 1, c))
+        Q = orc.tsqr_form_q(f)
+        assert np.linalg.norm(A - Q @ f.R) / np.linalg.norm(A) <= 1e-13
+        assert np.linalg.norm(Q.T @ Q - np.eye(n)) <= 1e-13
+        assert np.linalg.norm(f.R.T @ f.R - A.T @ A) / np.linalg.norm(A) ** 2 <= 1e-14
+        Rflat = np.linalg.qr(A, mode="r")
+        assert orc.rel_fro(orc.sign_normalise(f.R), orc.sign_normalise(Rflat)) <= 1e-13
 
 
 def test_mgs_ld_pins():
@@ -379,3 +385,53 @@ def test_mgs_ld_pins():
     Q, R = orc.mgs_ld(A)
     assert orc.rel_fro(R, orc.sign_normalise(np.linalg.qr(A, mode="r"))) <= 1e-14
     assert np.linalg.norm(Q.T @ Q - np.eye(7)) <= 1e-14
+
+
+# ------------------------------------------------- flat-chain tile QR (leaves)
+@pytest.mark.parametrize("rows,n", [(100, 7), (257, 16), (64, 64), (200, 50)])
+def test_chain_c0_is_hqr(rows, n):
+    # c = 0 and c >= rows are the paper's plain leaf QR (DGEQR2), bit for bit
+    A = _rng(rows * n).standard_normal((rows, n))
+    F0, t0 = orc.hqr(A)
+    for c in (0, rows, rows + 5):
+        F, t = orc.chain_qr(A, c)
+        assert np.array_equal(F, F0) and np.array_equal(t[0], t0)
+
+
+@pytest.mark.parametrize("rows,n,c", [(200, 16, 32), (200, 50, 32), (97, 40, 32), (130, 64, 32),
+                                      (300, 24, 64), (64, 64, 32), (77, 50, 32), (50, 16, 8)])
+def test_chain_equals_stacked_hqr(rows, n, c):
+    # Sequential TSQR: every chunk step is qr([R; A_k]) with R the
+    # upper trapezoid so far.  Dense hqr of the explicitly stacked matrix
+    # (zero-padded to n rows while it is wide) touches the same nonzeros -- R's
+    # zeros and the padding add exact zeros -- so it must agree bit for bit:
+    # the chunk's taus, its reflector tails, and R after every chunk.
+    A = _rng(rows + 7 * n + c).standard_normal((rows, n))
+    F, tau = orc.chain_qr(A, c)
+    Rk = np.zeros((0, n))
+    for k, r0 in enumerate(range(0, rows, c)):
+        h = min(c, rows - r0)
+        r = Rk.shape[0]
+        S = np.vstack([Rk, A[r0:r0 + h], np.zeros((max(0, n - r - h), n))])
+        Fs, ts = orc.hqr(S)
+        kk = min(n, r + h)                                 # reflectors this chunk has
+        assert np.array_equal(tau[k][:kk], ts[:kk]) and np.all(tau[k][kk:] == 0.0)
+        for i in range(h):                                 # tails: tile row > column
+            cols = min(n, r0 + i)
+            assert np.array_equal(F[r0 + i, :cols], Fs[r + i, :cols])
+        Rk = np.triu(Fs[:kk])
+    assert np.array_equal(np.triu(F[:n]), Rk)
+
+
+@pytest.mark.parametrize("rows,n,c", [(300, 20, 32), (256, 64, 32), (1000, 50, 32)])
+def test_chain_r_vs_lapack_and_q(rows, n, c):
+    A = _rng(rows - n + c).standard_normal((rows, n))
+    F, tau = orc.chain_qr(A, c)
+    R = np.triu(F[:n])
+    assert orc.rel_fro(orc.sign_normalise(R), orc.sign_normalise(np.linalg.qr(A, mode="r"))) <= 1e-13
+    p = orc.plan(rows, n, rows, rows, 1, c)             # one tile: Q from the stored reflectors
+    f = orc.tsqr_factor(A, p)
+    assert np.array_equal(f.A, F) and np.array_equal(f.tau_tile, tau)
+    Q = orc.tsqr_form_q(f)
+    assert np.linalg.norm(A - Q @ R) / np.linalg.norm(A) <= 1e-13
+    assert np.linalg.norm(Q.T @ Q - np.eye(n)) <= 1e-13
