@@ -29,15 +29,16 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# BASELINE.json configs (block rows b from the config; tile rows s = the SM tile)
+# BASELINE.json configs (block rows b from the config; tile rows s: the leaves of the
+# binary tree, each factored as a flat chain of register-resident chunks)
 CONFIGS = {
-    "c1": dict(m=4096, n=16, b=512, s=128, kind="gauss", op="form_q", k=0,
+    "c1": dict(m=4096, n=16, b=512, s=512, kind="gauss", op="form_q", k=0,
                desc="fp64 A 4096x16 N(0,1) seed 0, row blocks 512 (8-leaf binary tree): factor + form Q"),
-    "c2": dict(m=1_000_000, n=50, b=4096, s=96, kind="gauss", op="form_q", k=0,
+    "c2": dict(m=1_000_000, n=50, b=4096, s=4096, kind="gauss", op="form_q", k=0,
                desc="fp64 A 1,000,000x50 N(0,1), row blocks 4096, binary tree: factor + form Q"),
-    "c4": dict(m=16_777_216, n=64, b=4096, s=96, kind="cond", op="form_q", k=0,
+    "c4": dict(m=16_777_216, n=64, b=4096, s=4096, kind="cond", op="form_q", k=0,
                desc="fp64 A 16,777,216x64 = G diag(sigma) V^T, sigma 1..1e-10: factor + form Q"),
-    "c5": dict(m=33_554_432, n=32, b=4096, s=96, kind="gauss", op="apply_qt", k=128,
+    "c5": dict(m=33_554_432, n=32, b=4096, s=4096, kind="gauss", op="apply_qt", k=128,
                desc="fp64 A 33,554,432x32 N(0,1): factor + apply Q^T to C 33,554,432x128"),
 }
 DEFAULT_CONFIG = "c2"   # configs[1]: the workload BASELINE.json's metric is quoted on that fits one GPU
@@ -293,7 +294,10 @@ def run_ours(args, cfg):
             traffic = json.load(open(prof)).get(f"{args.config}_factor")
         except Exception:
             traffic = None
-    launches_per_step = 1 + (info["depth"] + 2 if cfg["op"] == "form_q" else 1)
+    # factor: chain leaves + tree climb; form Q: identity + one node launch per tree
+    # step + chain leaves; apply Q^T: chain leaves + node climb
+    multi = info["ntiles"] > 1
+    launches_per_step = (1 + multi) + (info["depth"] + 2 if cfg["op"] == "form_q" else 1 + multi)
     if world > 1:
         launches_per_step += 2 * info["cross_rounds"] + 1 + (2 * info["cross_rounds"] if cfg["op"] == "apply_qt" else 0)
     cpu = oracle_sample(cfg) if (world == 1 and not args.no_cpu_baseline) else None

@@ -106,19 +106,25 @@ __device__ __forceinline__ void sync_publish(int *c, int v) {
 // and two Newton steps, 1/x likewise (rcp_nr): <= 2 ulp.
 __device__ __forceinline__ House house_bf(double alpha, double s2) {
     const double y = fma(alpha, alpha, s2);
-    double r;
+    const double aa = fabs(alpha);
+    double r, i;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(y));
+    // seed 1/(|alpha| + N) from the rsqrt seed while r is refined (the two MUFU
+    // chains overlap); its Newton steps then run against the exact denominator
+    const double D0 = fma(y, r, aa);
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(i) : "d"(D0));
     const double hy = 0.5 * y;
     r = r * fma(-hy * r, r, 1.5);
     r = r * fma(-hy * r, r, 1.5);
     const double N = y * r;
-    const double aa = fabs(alpha);
-    const double inv = wy::rcp_nr(aa + N);
+    const double D = aa + N;
+    i = fma(i, fma(-D, i, 1.0), i);
+    i = fma(i, fma(-D, i, 1.0), i);
     const bool z = (s2 == 0.0);
     House h;
     h.beta = z ? alpha : (alpha >= 0.0 ? -N : N);
     h.tau = z ? 0.0 : fma(aa, r, 1.0);
-    h.scale = z ? 0.0 : (alpha >= 0.0 ? inv : -inv);
+    h.scale = z ? 0.0 : (alpha >= 0.0 ? i : -i);
     return h;
 }
 
@@ -129,7 +135,7 @@ struct Cfg {
     static constexpr int LDR = NP + 2;                    // R buffer: R(i, c) at [i * LDR + c]
     static constexpr int RBUF = NP * LDR;
     // per-warp scratch: Y panel (CH x 8 row-major), Gram, T (row-major), taus
-    static constexpr int YS = 0, GS = CH * 8, TS = GS + 64, T8 = TS + 64, WS = T8 + 8;
+    static constexpr int YS = 0, GS = CH * 8, TS = GS + 64, T8 = TS + 64, XS = T8 + 8, WS = XS + 2 * CH;
     static constexpr int OFF_WS = 2 * RBUF;               // after the two R buffers
     static constexpr int OFF_SYNC = OFF_WS + NW * WS;     // per buffer: NP row + NCB panel counters
     static constexpr int SYNC_INTS = NP + NCB;
@@ -139,19 +145,21 @@ struct Cfg {
 // T (8x8, row-major) of one panel from its Gram entries G(l, c), l < c
 // (row-major in Gs) and taus t: T(r,r) = t_r, T(r,c) = -t_c sum_l T(r,l) G(l,c).
 __device__ __forceinline__ void build_t(const double *Gs, const double *t, double *Ts) {
-    const int r = threadIdx.x & 31;
-    if (r < 8) {
-        double row[8];
-        const double tr = t[r];
+    // straight-line for every lane (row lane & 7), so the compiler can overlap
+    // it with the independent W^T DMMAs that follow; lanes 0..7 store
+    const int r = threadIdx.x & 7;
+    double row[8];
+    const double tr = t[r];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) row[c] = (c == r) ? tr : 0.0;
+    for (int c = 0; c < 8; ++c) row[c] = (c == r) ? tr : 0.0;
 #pragma unroll
-        for (int c = 1; c < 8; ++c) {
-            double s = 0.0;
+    for (int c = 1; c < 8; ++c) {
+        double s = 0.0;
 #pragma unroll
-            for (int l = 0; l < c; ++l) s = fma(row[l], Gs[l * 8 + c], s);
-            if (r < c) row[c] = -t[c] * s;
-        }
+        for (int l = 0; l < c; ++l) s = fma(row[l], Gs[l * 8 + c], s);
+        row[c] = (r < c) ? -t[c] * s : row[c];
+    }
+    if ((threadIdx.x & 31) < 8) {
 #pragma unroll
         for (int c = 0; c < 8; c += 2) *reinterpret_cast<double2 *>(Ts + r * 8 + c) = make_double2(row[c], row[c + 1]);
     }
@@ -169,18 +177,27 @@ struct Chunk {
 // scale applied), R's pivot rows hold (beta, updated R entries) in the panel
 // columns, Gs/t8 the Gram entries and taus.
 template <class C, int P>
-__device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, double *Gs, double *t8, double *tau_out,
-                                                 int n, const Sync &sy) {
+__device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, double *Gs, double *t8, double *xs,
+                                                 double *tau_out, int n, const Sync &sy) {
     const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+    // the pivot column is broadcast through a double-buffered row in smem: its
+    // owners (l4 == jj) store it right after their update of the previous step
+    if (l4 == 0) {
+#pragma unroll
+        for (int k = 0; k < C::KM; ++k)
+            *reinterpret_cast<double2 *>(xs + 8 * k + 2 * q) = make_double2(ch.a[k][P][0], ch.a[k][P][1]);
+    }
+    __syncwarp();
 #pragma unroll 1
     for (int jj = 0; jj < 8; ++jj) {
         const int j = 8 * P + jj;
-        const int src = 4 * jj + q;
+        const double *xr = xs + (jj & 1) * C::CH;
         double x[C::KM][2];
 #pragma unroll
         for (int k = 0; k < C::KM; ++k) {
-            x[k][0] = __shfl_sync(FULL, ch.a[k][P][0], src);
-            x[k][1] = __shfl_sync(FULL, ch.a[k][P][1], src);
+            const double2 v = *reinterpret_cast<const double2 *>(xr + 8 * k + 2 * q);
+            x[k][0] = v.x;
+            x[k][1] = v.y;
         }
         double d0 = 0.0, d1 = 0.0, s0 = 0.0, s1 = 0.0;
 #pragma unroll
@@ -208,12 +225,18 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
             ch.a[k][P][0] = fma(-u, x[k][0], ch.a[k][P][0]);
             ch.a[k][P][1] = fma(-u, x[k][1], ch.a[k][P][1]);
         }
+        if (l4 == jj + 1) {                                          // next pivot column -> the other row
+            double *xw = xs + ((jj + 1) & 1) * C::CH;
+#pragma unroll
+            for (int k = 0; k < C::KM; ++k)
+                *reinterpret_cast<double2 *>(xw + 8 * k + 2 * q) = make_double2(ch.a[k][P][0], ch.a[k][P][1]);
+        }
         __syncwarp();                  // every lane has read R(j, .) before it is overwritten
         const double rnew = (l4 == jj) ? h.beta : fma(-h.tau, w, rj);
         if (q == 0 && l4 >= jj) Rb[j * C::LDR + 8 * P + l4] = rnew;
         if (q == 0 && l4 < jj) Gs[l4 * 8 + jj] = h.scale * d;       // G(l, jj) = v_l^T v_jj
         if (lane == 0) t8[jj] = h.tau;
-        sync_publish(sy.row + j, sy.s + 1);
+        sync_publish(sy.row + j, sy.s + 1);                          // (its __syncwarp also publishes xs)
         PROBE(2);
     }
     __syncwarp();
@@ -367,7 +390,7 @@ __device__ __forceinline__ void factor_panel(Chunk<C> &ch, int kind, int kb, dou
     double yv[C::KM][2];
     PROBE(1);
     if (kind == 0) {
-        panel_structured<C, P>(ch, Rb, Gs, t8, tau_out, n, sy);
+        panel_structured<C, P>(ch, Rb, Gs, t8, ws + C::XS, tau_out, n, sy);
 #pragma unroll
         for (int k = 0; k < C::KM; ++k) {
             yv[k][0] = ch.a[k][P][0];
