@@ -16,6 +16,8 @@ int padded_width(int64_t n) { return n <= 16 ? 16 : (n <= 32 ? 32 : 64); }
 // Default tile: 32 chunks of the chain.
 int64_t tile_capacity(int64_t) { return (int64_t)1 << 30; }
 int64_t default_tile_rows(int64_t n) { return 32 * (int64_t)chunk_rows_for(n); }
+// chunk.cuh: 64 doubles of chunk per lane -- KM = 8 row blocks (64 rows) for
+// n <= 32, KM = 4 (32 rows) for n <= 64
 int chunk_rows_for(int64_t n) { return n <= 32 ? 64 : 32; }
 
 static int64_t block_count(int64_t m, int64_t n, int64_t b, int64_t *last_rows) {

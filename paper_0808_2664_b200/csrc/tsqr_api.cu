@@ -206,7 +206,7 @@ static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t 
     alloc((void **)&t->d_cross_tau, sizeof(double) * (t->cross_rounds + 1) * n);
     alloc((void **)&t->d_step_ids, sizeof(int) * (ids.size() + 1));
     const int64_t nchunks = p.tile_chunk0[L];
-    int grid = chain_grid((int)n, p.c);
+    int grid = chain_grid((int)n);
     if (grid > L) grid = L;
     std::vector<int> cta_tile0;
     chain_partition(p.tile_rows, p.c, grid, cta_tile0);
@@ -214,7 +214,7 @@ static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t 
     alloc((void **)&t->d_tile_chunk0, sizeof(int64_t) * (L + 1));
     alloc((void **)&t->d_cta_tile0, sizeof(int) * (grid + 1));
     alloc((void **)&t->d_tau_chunk, sizeof(double) * nchunks * n);
-    alloc((void **)&t->d_tcache, sizeof(double) * nchunks * chain_ncb((int)n, p.c) * 64);
+    alloc((void **)&t->d_tcache, sizeof(double) * nchunks * chain_ncb((int)n) * 64);
     t->nchunks = nchunks;
     if (e != cudaSuccess) {
         free_tree_memory(t);
@@ -341,7 +341,7 @@ tsqr_status_t tsqr_apply_qt(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, do
     ca.tile_row0 = t->d_row0; ca.tile_rows = t->d_rows; ca.tile_chunk0 = t->d_tile_chunk0;
     ca.cta_tile0 = t->d_cta_tile0; ca.grid = t->chain_grid; ca.tcache = t->d_tcache;
     ca.C = C; ca.ldc = ldc; ca.k = (int)k; ca.forward = 1; ca.xbuf = nullptr;
-    CUDA_TRY(launch_chain_apply(ca, st), "tsqr_apply_qt leaves");
+    CUDA_TRY(launch_cs_apply(ca, st), "tsqr_apply_qt leaves");
     if (t->plan.ntiles() > 1) CUDA_TRY(launch_apply_nodes(f, st), "tsqr_apply_qt nodes");
     if (top) CUDA_TRY(launch_copy_block(C, ldc, top, ldtop, (int)t->plan.n, (int)k, st), "tsqr_apply_qt top");
     t->stream = st;
@@ -401,7 +401,7 @@ tsqr_status_t tsqr_form_q(tsqr_tree_t t, double *Q, int64_t ldq, void *stream) {
     ca.tile_row0 = t->d_row0; ca.tile_rows = t->d_rows; ca.tile_chunk0 = t->d_tile_chunk0;
     ca.cta_tile0 = t->d_cta_tile0; ca.grid = t->chain_grid; ca.tcache = t->d_tcache;
     ca.C = Q; ca.ldc = ldq; ca.k = n; ca.forward = 0; ca.xbuf = t->d_xbuf;
-    CUDA_TRY(launch_chain_apply(ca, st), "tsqr_form_q leaves");
+    CUDA_TRY(launch_cs_apply(ca, st), "tsqr_form_q leaves");
     t->stream = st;
     return debug_sync(t, st, "tsqr_form_q");
 }

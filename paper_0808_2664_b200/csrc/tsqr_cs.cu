@@ -1,0 +1,431 @@
+// Leaf-stage factor kernel on the column-split chunk engine (cs.cuh).  Product code.
+//
+//  k_cs_factor  (a2)+(a3)+(a6 per tile): persistent CTAs of NGRP groups of NG
+//      warps; CTA i owns a contiguous run of tiles, group g takes every NGRP-th
+//      of them; a group walks its tiles' chunks in order (the flat chain), its
+//      warps splitting every chunk's columns.  The last chunk of a tile writes
+//      the tile's R into the upper triangle of the tile's head rows.
+#include "tsqr_kernels.h"
+#include "cs.cuh"
+
+#include <algorithm>
+#include <vector>
+
+namespace tsqr {
+using namespace cs;
+
+// With one column block per warp (NG = NCB), warp W of a group owns block W
+// of every chunk: it applies Y_0 .. Y_{W-1} of the chunk to its block as they
+// are published, then factors panel W and publishes Y_W, T_W.
+template <class C, bool kDense>
+__device__ __forceinline__ void cs_warp_chunk(Regs<C> &rg, int W, int s, double *Rb, double *Ybase, int *ready,
+                                              int *done, double *ws, double *tau_out, double *tg, int n) {
+    const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+#pragma unroll 1
+    for (int P = 0; P < W; ++P) {
+        wait_ge(ready + P, s + 1);
+        apply_block<C, kDense>(rg, P, Ybase + P * C::YSLOT, Rb, W);
+        if (kDense) rows_to_r<C>(rg, P, Rb, W);        // chunk rows 8P.. of block W are R rows now
+        bump(done + P);
+    }
+    double *ys = Ybase + W * C::YSLOT;
+    double *Gs = ws + C::GS, *t8 = ws + C::T8, *Ts = ws + C::TS, *xs = ws + C::XS;
+    wait_ge(done + W, s * (C::NCB - 1 - W));           // the slot's previous Y_W has been applied everywhere
+    panel_steps<C, kDense>(rg, W, Rb, Gs, t8, xs);
+    build_t(Gs, t8, Ts);
+    // publish Y_W (unit diagonal and zeros above it for a dense panel) and T_W
+#pragma unroll
+    for (int k = 0; k < C::KM; ++k)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int r = 8 * k + 2 * q + e;
+            double y = rg.a[k][0][e];
+            if (kDense) y = (k > W || (k == W && 2 * q + e > l4)) ? y : ((k == W && 2 * q + e == l4) ? 1.0 : 0.0);
+            ys[r * 8 + l4] = y;
+        }
+    *reinterpret_cast<double2 *>(ys + C::CH * 8 + 2 * lane) = *reinterpret_cast<const double2 *>(Ts + 2 * lane);
+    if (tg != nullptr)
+        *reinterpret_cast<double2 *>(tg + W * 64 + 2 * lane) = *reinterpret_cast<const double2 *>(Ts + 2 * lane);
+    if (lane < 8 && 8 * W + lane < n) tau_out[8 * W + lane] = t8[lane];
+    if (kDense) rows_to_r<C>(rg, W, Rb, W);            // chunk rows 8W.. are R rows from here on
+    publish(ready + W, s + 1);
+}
+
+template <class C>
+__global__ void __launch_bounds__(C::NT, 1)
+k_cs_factor(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *tile_rows,
+            const int64_t *tile_chunk0, const int *cta_tile0, double *tau, double *tcache) {
+    extern __shared__ __align__(16) double sm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int q = lane & 3, l4 = lane >> 2;
+    const int grp = warp / C::NG, wl = warp % C::NG;
+    double *Rb = sm + C::OFF_R + grp * C::RBUF;
+    double *Ybase = sm + C::OFF_Y + grp * C::NCB * C::YSLOT;
+    double *ws = sm + C::OFF_W + warp * C::WSCR;
+    int *sync = reinterpret_cast<int *>(sm + C::OFF_SYNC);
+    for (int i = threadIdx.x; i < C::NGRP * 2 * C::NCB; i += C::NT) sync[i] = 0;
+    __syncthreads();
+    int *ready = sync + grp * 2 * C::NCB, *done = ready + C::NCB;
+    const int tb = cta_tile0[blockIdx.x], te = cta_tile0[blockIdx.x + 1];
+    int s = 0;
+    for (int t = tb + grp; t < te; t += C::NGRP) {
+        const int h = tile_rows[t];
+        const int nch = (h + C::CH - 1) / C::CH;
+        const int64_t row0 = tile_row0[t];
+        for (int c = 0; c < nch; ++c, ++s) {
+            const int r0 = c * C::CH, hk = min(C::CH, h - r0);
+            Regs<C> rg;
+            const double *src = A + row0 + r0;
+#pragma unroll
+            for (int j = 0; j < C::NBW; ++j) {
+                const int b = C::blk(wl, j);
+                const int col = 8 * b + l4;
+                const bool okc = b >= 0 && col < n;
+                const double *pc = src + (int64_t)(okc ? col : 0) * lda;
+#pragma unroll
+                for (int k = 0; k < C::KM; ++k) {
+                    const int r = 8 * k + 2 * q;
+                    rg.a[k][j][0] = (okc && r < hk) ? __ldg(pc + r) : 0.0;
+                    rg.a[k][j][1] = (okc && r + 1 < hk) ? __ldg(pc + r + 1) : 0.0;
+                }
+            }
+            double *tau_out = tau + (tile_chunk0[t] + c) * n;
+            double *tg = tcache ? tcache + (tile_chunk0[t] + c) * (C::NCB * 64) : nullptr;
+            static_assert(C::NG == C::NCB && C::NBW == 1, "one column block per warp");
+            if (c == 0) cs_warp_chunk<C, true>(rg, wl, s, Rb, Ybase, ready, done, ws, tau_out, tg, n);
+            else cs_warp_chunk<C, false>(rg, wl, s, Rb, Ybase, ready, done, ws, tau_out, tg, n);
+            double *dst = A + row0 + r0;
+#pragma unroll
+            for (int j = 0; j < C::NBW; ++j) {
+                const int b = C::blk(wl, j);
+                const int col = 8 * b + l4;
+                if (b < 0 || col >= n) continue;
+#pragma unroll
+                for (int k = 0; k < C::KM; ++k)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int r = 8 * k + 2 * q + e;
+                        if (r < hk && r0 + r > col) dst[r + (int64_t)col * lda] = rg.a[k][j][e];
+                    }
+            }
+            if (c == nch - 1) {                        // the tile's R (my columns) -> its head rows
+                __syncwarp();
+                for (int j = 0; j < C::NBW; ++j) {
+                    const int b = C::blk(wl, j);
+                    if (b < 0) continue;
+                    for (int e = lane; e < 8 * C::NP; e += 32) {
+                        const int i = e % C::NP, col = 8 * b + e / C::NP;
+                        if (i <= col && col < n) A[row0 + i + (int64_t)col * lda] = Rb[i * C::LDR + col];
+                    }
+                }
+            }
+        }
+    }
+}
+
+// ============================================================ apply / form Q
+// k_cs_apply<C, kFwd>: the leaf stage of C <- Q^T C (kFwd, (a7)) or of the
+// explicit Q = Q_leaves [X; 0] (!kFwd, (a10)) on the factor's chunk chains
+// (C: the factor's chunk configuration).  The 8 warps of a CTA work on the same
+// chunk; warp w owns an 8-column slab of C (column block w of the current
+// pass) for the chunk's CH rows (registers, DMMA accumulator layout) and the
+// slab's "R-row coordinates" C_R (NP x 8, registers: cr[p] = C_R rows
+// 8p..8p+7), which play the role R plays in the factor.  Chunk by chunk
+// (forward order for Q^T, reverse for Q) the CTA stages the chunk's Y (CH x NP
+// from its rows of A) and its panels' T (the factor's cache) into a
+// double-buffered smem slot with cp.async, one __syncthreads per chunk; every
+// warp then applies the chunk's block reflectors panel by panel to
+// [C_R rows 8p..8p+7; its chunk slab].
+template <class C>
+struct ApplyCs {
+    static constexpr int NW = 8, NT = 256;
+    static constexpr int YS = C::CH * C::NP + C::NCB * 64;     // Y (row-major CH x NP) + T's
+    static constexpr size_t BYTES = (size_t)2 * YS * sizeof(double);
+};
+
+__device__ __forceinline__ void cp8(double *sm, const double *g, bool ok) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(sm));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 8 : 0) : "memory");
+}
+
+// Stage the chunk's Y (zero outside [0, hk) x [0, n) and on/above the pivot
+// of a column whose pivot lies in the chunk -- chunk row col - r0; fix_dense
+// then adds the unit diagonal) and its T's.
+template <class C>
+__device__ __forceinline__ void stage_chunk(double *slot, const double *Ak, int64_t lda, int hk, int n,
+                                            const double *tch, int r0) {
+    for (int i = threadIdx.x; i < C::CH * C::NP; i += 256) {
+        const int col = i / C::CH, row = i % C::CH;
+        const bool ok = row < hk && col < n && row > col - r0;
+        cp8(slot + row * C::NP + col, Ak + row + (int64_t)(ok ? col : 0) * lda, ok);
+    }
+    for (int i = threadIdx.x; i < C::NCB * 64; i += 256) cp8(slot + C::CH * C::NP + i, tch + i, true);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+template <class C>
+__device__ __forceinline__ void fix_dense(double *slot, int n, int r0) {
+    for (int c = threadIdx.x; c < C::NP; c += 256)
+        if (c < n && c >= r0 && c < r0 + C::CH) slot[(c - r0) * C::NP + c] = 1.0;
+}
+
+template <class C, bool kFwd>
+__device__ __forceinline__ void cs_apply_panel(double (&cc)[C::KM][2], double (&cr)[C::NCB][2], int p, int r0,
+                                               const double *slot) {
+    const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+    constexpr int KM = C::KM, NP = C::NP;
+    if (8 * p >= r0 + C::CH) return;           // no reflector of panel p in this chunk
+    const bool dense = 8 * p >= r0;            // pivots inside the chunk: row block kb
+    const int kb = dense ? (8 * p - r0) >> 3 : -1;
+    const double *ys = slot + 8 * p;
+    const double *Tg = slot + C::CH * NP + 64 * p;
+    double crp0 = 0.0, crp1 = 0.0;
+#pragma unroll
+    for (int i = 0; i < C::NCB; ++i) {
+        crp0 = (i == p) ? cr[i][0] : crp0;
+        crp1 = (i == p) ? cr[i][1] : crp1;
+    }
+    if (!kFwd && dense) {                     // Q: the pivot rows take their R-row coordinates back
+#pragma unroll
+        for (int k = 0; k < KM; ++k) {
+            cc[k][0] = (k == kb) ? crp0 : cc[k][0];
+            cc[k][1] = (k == kb) ? crp1 : cc[k][1];
+        }
+    }
+    double w0[2] = {0.0, 0.0}, w1[2] = {0.0, 0.0};
+#pragma unroll
+    for (int k = 0; k < KM; ++k) {
+        const double y0 = ys[(8 * k + 2 * q) * NP + l4], y1 = ys[(8 * k + 2 * q + 1) * NP + l4];
+        dmma(w0[k & 1], w1[k & 1], cc[k][0], y0);
+        dmma(w0[k & 1], w1[k & 1], cc[k][1], y1);
+    }
+    double wt0 = w0[0] + w0[1], wt1 = w1[0] + w1[1];
+    if (!dense) {
+        wt0 += crp0;
+        wt1 += crp1;
+    }
+    const double tb0 = kFwd ? Tg[(2 * q) * 8 + l4] : Tg[l4 * 8 + 2 * q];
+    const double tb1 = kFwd ? Tg[(2 * q + 1) * 8 + l4] : Tg[l4 * 8 + 2 * q + 1];
+    double p0 = 0.0, p1 = 0.0;
+    dmma(p0, p1, wt0, tb0);
+    dmma(p0, p1, wt1, tb1);
+    if (!dense) {
+        crp0 -= p0;
+        crp1 -= p1;
+    }
+#pragma unroll
+    for (int k = 0; k < KM; ++k) {
+        const double y0 = ys[(8 * k + l4) * NP + 2 * q], y1 = ys[(8 * k + l4) * NP + 2 * q + 1];
+        dmma(cc[k][0], cc[k][1], -p0, y0);
+        dmma(cc[k][0], cc[k][1], -p1, y1);
+    }
+    if (kFwd && dense) {                      // Q^T: the pivot rows become R-row coordinates
+#pragma unroll
+        for (int k = 0; k < KM; ++k) {
+            crp0 = (k == kb) ? cc[k][0] : crp0;
+            crp1 = (k == kb) ? cc[k][1] : crp1;
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < C::NCB; ++i) {
+        cr[i][0] = (i == p) ? crp0 : cr[i][0];
+        cr[i][1] = (i == p) ? crp1 : cr[i][1];
+    }
+}
+
+template <class C, bool kFwd>
+__global__ void __launch_bounds__(256, 1)
+k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const int *tile_rows,
+           const int64_t *tile_chunk0, const int *cta_tile0, const double *tcache, double *Cm, int64_t ldc, int k,
+           const double *xbuf) {
+    using AC = ApplyCs<C>;
+    extern __shared__ __align__(16) double sm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+    const int tb = cta_tile0[blockIdx.x], te = cta_tile0[blockIdx.x + 1];
+    const int npass = (k + 63) / 64;
+    const int np = (n + 7) / 8;
+    // the CTA's work list: (tile, pass) items, each a chain over the tile's chunks
+    int cur = 0;                                                  // staging parity
+    bool staged = false;
+    auto chunk_of = [&](int t, int cc_) {
+        const int nch = (tile_rows[t] + C::CH - 1) / C::CH;
+        return kFwd ? cc_ : nch - 1 - cc_;
+    };
+    for (int t = tb; t < te; ++t) {
+        const int h = tile_rows[t];
+        const int nch = (h + C::CH - 1) / C::CH;
+        const int64_t row0 = tile_row0[t];
+        for (int pass = 0; pass < npass; ++pass) {
+            const int col = 64 * pass + 8 * warp + l4;            // this lane's column of C
+            const bool okc = col < k;
+            double cr[C::NCB][2];
+#pragma unroll
+            for (int i = 0; i < C::NCB; ++i) {
+                cr[i][0] = cr[i][1] = 0.0;
+                if (!kFwd) {                                      // C_R := X (rows < n, columns < n)
+                    const int r = 8 * i + 2 * q;
+                    const double *X = xbuf + (int64_t)t * n * n;
+                    cr[i][0] = (okc && r < n) ? X[r + (int64_t)col * n] : 0.0;
+                    cr[i][1] = (okc && r + 1 < n) ? X[r + 1 + (int64_t)col * n] : 0.0;
+                }
+            }
+            for (int cc_ = 0; cc_ < nch; ++cc_) {
+                const int c = chunk_of(t, cc_);
+                const int r0 = c * C::CH, hk = min(C::CH, h - r0);
+                const bool dense = r0 < C::NP;                    // a head chunk (holds pivots)
+                if (!staged)
+                    stage_chunk<C>(sm + cur * AC::YS, A + row0 + r0, lda, hk, n,
+                                   tcache + (tile_chunk0[t] + c) * (C::NCB * 64), r0);
+                // prefetch the next chunk of the work list into the other slot
+                int tn = t, pn = pass, cn = cc_ + 1;
+                if (cn == nch) { cn = 0; if (++pn == npass) { pn = 0; ++tn; } }
+                if (tn < te) {
+                    const int cnn = chunk_of(tn, cn), hn = tile_rows[tn], r0n = cnn * C::CH;
+                    stage_chunk<C>(sm + (cur ^ 1) * AC::YS, A + tile_row0[tn] + r0n, lda, min(C::CH, hn - r0n), n,
+                                   tcache + (tile_chunk0[tn] + cnn) * (C::NCB * 64), r0n);
+                    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+                    staged = true;
+                } else {
+                    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+                    staged = false;
+                }
+                __syncthreads();
+                double *slot = sm + cur * AC::YS;
+                if (dense) {
+                    fix_dense<C>(slot, n, r0);
+                    __syncthreads();
+                }
+                double *Ck = Cm + row0 + r0;
+                double ccv[C::KM][2];
+#pragma unroll
+                for (int kk = 0; kk < C::KM; ++kk) {
+                    const int r = 8 * kk + 2 * q;
+                    ccv[kk][0] = (kFwd && okc && r < hk) ? Ck[r + (int64_t)col * ldc] : 0.0;
+                    ccv[kk][1] = (kFwd && okc && r + 1 < hk) ? Ck[r + 1 + (int64_t)col * ldc] : 0.0;
+                }
+#pragma unroll 1
+                for (int pp = 0; pp < np; ++pp)
+                    cs_apply_panel<C, kFwd>(ccv, cr, kFwd ? pp : np - 1 - pp, r0, slot);
+#pragma unroll
+                for (int kk = 0; kk < C::KM; ++kk)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int r = 8 * kk + 2 * q + e;
+                        if (okc && r < hk && (!kFwd || r0 + r >= n)) Ck[r + (int64_t)col * ldc] = ccv[kk][e];
+                    }
+                __syncthreads();                                  // the slot may be refilled
+                cur ^= 1;
+            }
+            if (kFwd && okc) {                                    // the tile's head rows receive C_R
+#pragma unroll
+                for (int i = 0; i < C::NCB; ++i)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int r = 8 * i + 2 * q + e;
+                        if (r < n) Cm[row0 + r + (int64_t)col * ldc] = cr[i][e];
+                    }
+            }
+        }
+    }
+}
+
+// ================================================================= launchers
+template <class C>
+static cudaError_t cs_setup(size_t *bytes) {
+    *bytes = C::BYTES;
+    return cudaFuncSetAttribute((const void *)k_cs_factor<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)C::BYTES);
+}
+
+template <class F>
+static cudaError_t cs_dispatch(int n, F &&fn) {
+    const int ncb = (n + 7) / 8;
+    switch (ncb) {
+        case 1: case 2: return fn(Cfg<2, 32, 2, 4>());
+        case 3: case 4: return fn(Cfg<4, 32, 4, 2>());
+        case 5: case 6: return fn(Cfg<6, 32, 6, 1>());
+        case 7: return fn(Cfg<7, 32, 7, 1>());
+        default: return fn(Cfg<8, 32, 8, 1>());
+    }
+}
+
+int cs_chunk_rows(int n) {
+    int ch = 0;
+    cs_dispatch(n, [&](auto c) {
+        ch = decltype(c)::CH;
+        return cudaSuccess;
+    });
+    return ch;
+}
+int cs_ncb(int n) {
+    int v = 0;
+    cs_dispatch(n, [&](auto c) {
+        v = decltype(c)::NCB;
+        return cudaSuccess;
+    });
+    return v;
+}
+
+int cs_grid(int n) {
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cs_dispatch(n, [&](auto c) {
+        using C = decltype(c);
+        size_t b;
+        cudaError_t r = cs_setup<C>(&b);
+        if (r != cudaSuccess) return r;
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cs_factor<C>, C::NT, b);
+    });
+    if (e != cudaSuccess || occ < 1) occ = 1;
+    return sms * occ;
+}
+
+int cs_groups(int n) {
+    int g = 1;
+    cs_dispatch(n, [&](auto c) {
+        g = decltype(c)::NGRP;
+        return cudaSuccess;
+    });
+    return g;
+}
+
+// The apply kernel on the chain factor's representation (chunk.cuh, 32-row chunks).
+template <class F>
+static cudaError_t chain_cfg_dispatch(int n, F &&fn) {
+    const int ncb = (n + 7) / 8;
+    switch (ncb) {
+        case 1: case 2: return fn(chunk::Cfg<2, 8, 8>());
+        case 3: case 4: return fn(chunk::Cfg<4, 8, 8>());
+        case 5: case 6: return fn(chunk::Cfg<6, 4, 8>());
+        case 7: return fn(chunk::Cfg<7, 4, 8>());
+        default: return fn(chunk::Cfg<8, 4, 8>());
+    }
+}
+
+cudaError_t launch_cs_apply(const ChainApplyArgs &f, cudaStream_t st) {
+    return chain_cfg_dispatch(f.n, [&](auto c) {
+        using C = decltype(c);
+        using AC = ApplyCs<C>;
+        auto kern = f.forward ? k_cs_apply<C, true> : k_cs_apply<C, false>;
+        cudaError_t e = cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)AC::BYTES);
+        if (e != cudaSuccess) return e;
+        kern<<<f.grid, AC::NT, AC::BYTES, st>>>(f.A, f.lda, f.n, f.tile_row0, f.tile_rows, f.tile_chunk0, f.cta_tile0,
+                                                f.tcache, f.C, f.ldc, f.k, f.xbuf);
+        return cudaGetLastError();
+    });
+}
+
+cudaError_t launch_cs_factor(const ChainArgs &f, cudaStream_t st) {
+    return cs_dispatch(f.n, [&](auto c) {
+        using C = decltype(c);
+        size_t sm;
+        cudaError_t e = cs_setup<C>(&sm);
+        if (e != cudaSuccess) return e;
+        k_cs_factor<C><<<f.grid, C::NT, sm, st>>>(f.A, f.lda, f.n, f.tile_row0, f.tile_rows, f.tile_chunk0,
+                                                  f.cta_tile0, f.tau, f.tcache);
+        return cudaGetLastError();
+    });
+}
+
+}  // namespace tsqr

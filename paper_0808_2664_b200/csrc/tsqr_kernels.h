@@ -61,16 +61,21 @@ struct ChainApplyArgs {
     int forward;
     const double *xbuf;          // !forward: per-tile X (n x n) from the node stage
 };
-cudaError_t launch_chain_apply(const ChainApplyArgs &f, cudaStream_t st);
+// Chain engine (tsqr_chain.cu): chunk rows, column blocks, persistent grid, factor.
 int chain_chunk_rows(int n);
-int chain_grid(int n, int chunk_rows);
+int chain_ncb(int n);
+int chain_grid(int n);
 cudaError_t launch_chain_factor(const ChainArgs &f, cudaStream_t st);
+// Leaf stage of Q^T C / form Q on the chain representation (tsqr_cs.cu).
+cudaError_t launch_cs_apply(const ChainApplyArgs &f, cudaStream_t st);
+// Column-split factor (tsqr_cs.cu, 256-row chunks; kept for experiments).
+int cs_grid(int n);
+cudaError_t launch_cs_factor(const ChainArgs &f, cudaStream_t st);
 void chain_partition(const std::vector<int64_t> &tile_rows, int chunk_rows, int grid, std::vector<int> &cta_tile0);
 // Tree stage only (ticketed climb from every tile), after launch_chain_factor.
 cudaError_t launch_tree(const FactorArgs &f, cudaStream_t st);
 cudaError_t launch_apply(const ApplyArgs &f, cudaStream_t st);
 cudaError_t launch_apply_nodes(const ApplyArgs &f, cudaStream_t st);
-int chain_ncb(int n, int chunk_rows);          // column blocks of the compiled configuration
 cudaError_t launch_formq_nodes(int NP, const double *A, int64_t lda, int n, const DevPlan &plan,
                                const double *tau_node, const int *ids, int count, double *xbuf,
                                cudaStream_t st);
