@@ -7,7 +7,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtsqr.so")
+# developer override (A/B builds of the same sources); the default is the in-tree build
+LIB_PATH = os.environ.get("TSQR_LIBRARY", os.path.join(HERE, "libtsqr.so"))
 
 TSQR_OK = 0
 STATUS = {0: "TSQR_OK", 1: "TSQR_ERR_INVALID", 2: "TSQR_ERR_SHAPE", 3: "TSQR_ERR_UNSUPPORTED",

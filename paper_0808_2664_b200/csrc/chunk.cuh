@@ -139,7 +139,10 @@ struct Cfg {
     static constexpr int OFF_WS = 2 * RBUF;               // after the two R buffers
     static constexpr int OFF_SYNC = OFF_WS + NW * WS;     // per buffer: NP row + NCB panel counters
     static constexpr int SYNC_INTS = NP + NCB;
-    static constexpr size_t BYTES = (size_t)OFF_SYNC * sizeof(double) + 2 * SYNC_INTS * sizeof(int);
+    static constexpr int OFF_STG = (OFF_SYNC + (2 * SYNC_INTS + 1) / 2 + 1) & ~1;   // 16-byte aligned; per warp:
+                                                                                   // the next chunk (col-major CH x NP)
+    static constexpr int STG = CH * NP;
+    static constexpr size_t BYTES = (size_t)(OFF_STG + NW * STG) * sizeof(double);
 };
 
 // T (8x8, row-major) of one panel from its Gram entries G(l, c), l < c
@@ -220,6 +223,12 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
         const House h = house_bf(alpha, s2);
         const double w = fma(h.scale, d, rj);                        // v^T [R(j,c); a_c]
         const double u = (l4 > jj) ? h.tau * h.scale * w : (l4 == jj ? 1.0 - h.scale : 0.0);
+        // hand R row j to the next chunk first (its step j waits for it), then
+        // update this chunk's panel
+        const double rnew = (l4 == jj) ? h.beta : fma(-h.tau, w, rj);
+        __syncwarp();                  // every lane has read R(j, .) before it is overwritten
+        if (q == 0 && l4 >= jj) Rb[j * C::LDR + 8 * P + l4] = rnew;
+        sync_publish(sy.row + j, sy.s + 1);
 #pragma unroll
         for (int k = 0; k < C::KM; ++k) {
             ch.a[k][P][0] = fma(-u, x[k][0], ch.a[k][P][0]);
@@ -231,12 +240,9 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
             for (int k = 0; k < C::KM; ++k)
                 *reinterpret_cast<double2 *>(xw + 8 * k + 2 * q) = make_double2(ch.a[k][P][0], ch.a[k][P][1]);
         }
-        __syncwarp();                  // every lane has read R(j, .) before it is overwritten
-        const double rnew = (l4 == jj) ? h.beta : fma(-h.tau, w, rj);
-        if (q == 0 && l4 >= jj) Rb[j * C::LDR + 8 * P + l4] = rnew;
         if (q == 0 && l4 < jj) Gs[l4 * 8 + jj] = h.scale * d;       // G(l, jj) = v_l^T v_jj
         if (lane == 0) t8[jj] = h.tau;
-        sync_publish(sy.row + j, sy.s + 1);                          // (its __syncwarp also publishes xs)
+        __syncwarp();                                                // xs of the next step
         PROBE(2);
     }
     __syncwarp();
@@ -314,7 +320,8 @@ __device__ __forceinline__ void panel_dense(Chunk<C> &ch, int kb, double *Gs, do
 // update, publish, and only then the chunk's own update.
 template <class C, int P, bool kStruct>
 __device__ __forceinline__ void trailing(Chunk<C> &ch, const double (&yv)[C::KM][2], const double *Ys,
-                                         const double *Ts, double *Rb, const Sync &sy, bool defer) {
+                                         const double *Gs, const double *t8, double *Ts, double *tg, double *Rb,
+                                         const Sync &sy, bool defer) {
     const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
     if constexpr (P + 1 < C::NCB) {
         double wt[C::NCB][2];
@@ -327,6 +334,10 @@ __device__ __forceinline__ void trailing(Chunk<C> &ch, const double (&yv)[C::KM]
                 dmma(wt[cb][0], wt[cb][1], ch.a[k][cb][1], yv[k][1]);
             }
         }
+        // T while the W^T DMMAs drain (it only needs the panel's Gram and taus)
+        build_t(Gs, t8, Ts);
+        if (tg != nullptr)
+            *reinterpret_cast<double2 *>(tg + 8 * P * 8 + 2 * lane) = *reinterpret_cast<const double2 *>(Ts + 2 * lane);
         const double tb0 = Ts[(2 * q) * 8 + l4], tb1 = Ts[(2 * q + 1) * 8 + l4];
         PROBE(6);
         if (kStruct) sync_wait(sy.tr + P, sy.s);
@@ -364,9 +375,14 @@ __device__ __forceinline__ void trailing(Chunk<C> &ch, const double (&yv)[C::KM]
                 dmma(ch.a[k][cb][0], ch.a[k][cb][1], wt[cb][0], yt[k][0]);
                 dmma(ch.a[k][cb][0], ch.a[k][cb][1], wt[cb][1], yt[k][1]);
             }
-    } else if (kStruct) {
-        sync_wait(sy.tr + P, sy.s);
-        if (!defer) sync_publish(sy.tr + P, sy.s + 1);
+    } else {
+        build_t(Gs, t8, Ts);
+        if (tg != nullptr)
+            *reinterpret_cast<double2 *>(tg + 8 * P * 8 + 2 * lane) = *reinterpret_cast<const double2 *>(Ts + 2 * lane);
+        if (kStruct) {
+            sync_wait(sy.tr + P, sy.s);
+            if (!defer) sync_publish(sy.tr + P, sy.s + 1);
+        }
     }
 }
 
@@ -414,13 +430,11 @@ __device__ __forceinline__ void factor_panel(Chunk<C> &ch, int kind, int kb, dou
     }
     __syncwarp();
     PROBE(5);
-    build_t(Gs, t8, Ts);
-    PROBE(10);
-    if (tg != nullptr)                    // cache T (compact WY of the panel) for apply / form Q
-        *reinterpret_cast<double2 *>(tg + 8 * P * 8 + 2 * lane) = *reinterpret_cast<const double2 *>(Ts + 2 * lane);
-    if (kind == 0) trailing<C, P, true>(ch, yv, Ys, Ts, Rb, sy, defer);
+    // T (compact WY of the panel; cached in tg for apply / form Q) is built
+    // inside trailing(), overlapped with the W^T DMMAs
+    if (kind == 0) trailing<C, P, true>(ch, yv, Ys, Gs, t8, Ts, tg, Rb, sy, defer);
     else {
-        trailing<C, P, false>(ch, yv, Ys, Ts, Rb, sy, defer);
+        trailing<C, P, false>(ch, yv, Ys, Gs, t8, Ts, tg, Rb, sy, defer);
         // the pivot block rows are R rows 8P .. 8P+7 from here on
 #pragma unroll
         for (int k = 0; k < C::KM; ++k)

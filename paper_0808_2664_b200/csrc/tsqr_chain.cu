@@ -37,6 +37,22 @@ __device__ __forceinline__ void chunk_panels(Chunk<C> &ch, int r0, bool last, do
     if constexpr (P + 1 < C::NCB) chunk_panels<C, P + 1>(ch, r0, last, Rb, sy, ws, tau_out, n, Ahead, lda, tg);
 }
 
+// Prefetch a chunk (rows [r0, r0 + hk) of the tile at A + row0, all n columns)
+// into the warp's staging buffer (col-major CH x NP, zero-filled) with cp.async.
+template <class C>
+__device__ __forceinline__ void prefetch_chunk(double *stg, const double *src, int64_t lda, int hk, int n) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll 4
+    for (int i = lane; i < C::CH * C::NP; i += 32) {
+        const int col = i / C::CH, row = i % C::CH;
+        const bool ok = row < hk && col < n;
+        const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(stg + i));
+        const double *g = src + (ok ? row + (int64_t)col * lda : 0);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 8 : 0) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+}
+
 template <class C>
 __global__ void __launch_bounds__(C::NT, 1)
 k_chain_factor(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *tile_rows,
@@ -49,45 +65,82 @@ k_chain_factor(double *A, int64_t lda, int n, const int64_t *tile_row0, const in
     PROBE_INIT();
     __syncthreads();
     double *ws = sm + C::OFF_WS + warp * C::WS;
+    double *stg = sm + C::OFF_STG + warp * C::STG;
     const int tb = cta_tile0[blockIdx.x], te = cta_tile0[blockIdx.x + 1];
+    // Walk the CTA's chunk sequence (all warps identically); this warp owns
+    // every NW-th chunk.  When the warp finds its next chunk it computes the
+    // previous one (pend), whose data was prefetched into its staging buffer,
+    // and streams the new one in meanwhile.
     int cnt[2] = {0, 0};
     int g = 0;
-    for (int t = tb; t < te; ++t) {
-        const int b = (t - tb) & 1;
-        const int h = tile_rows[t];
-        const int nch = (h + C::CH - 1) / C::CH;
-        const int64_t row0 = tile_row0[t];
-        for (int c = 0; c < nch; ++c, ++g) {
+    int pt = -1, pc = 0, ps = 0, pb = 0;                  // the pending chunk
+    int t = tb, c = 0, b = 0, nch = tb < te ? (tile_rows[tb] + C::CH - 1) / C::CH : 0;
+    for (;;) {
+        // advance to this warp's next chunk (or the end)
+        int nt = -1, ncix = 0, ns = 0, nb = 0;
+        while (t < te) {
+            if (c == nch) {
+                ++t;
+                c = 0;
+                if (t >= te) break;
+                b = (t - tb) & 1;
+                nch = (tile_rows[t] + C::CH - 1) / C::CH;
+                continue;
+            }
             const int s = cnt[b]++;
-            if (g % C::NW != warp) continue;
-            const int r0 = c * C::CH, hk = min(C::CH, h - r0);
-            Chunk<C> ch;
-            const double *src = A + row0 + r0;
-#pragma unroll
-            for (int k = 0; k < C::KM; ++k)
-#pragma unroll
-                for (int cb = 0; cb < C::NCB; ++cb) {
-                    const int r = 8 * k + 2 * q, col = 8 * cb + l4;
-                    const double *p = src + r + (int64_t)col * lda;
-                    ch.a[k][cb][0] = (col < n && r < hk) ? __ldg(p) : 0.0;
-                    ch.a[k][cb][1] = (col < n && r + 1 < hk) ? __ldg(p + 1) : 0.0;
-                }
-            PROBE(0);
-            double *tau_out = tau + (tile_chunk0[t] + c) * n;
-            const Sync sy{sync + b * C::SYNC_INTS, sync + b * C::SYNC_INTS + C::NP, s};
-            double *tg = tcache ? tcache + (tile_chunk0[t] + c) * (C::NCB * 64) : nullptr;
-            chunk_panels<C, 0>(ch, r0, c == nch - 1, sm + b * C::RBUF, sy, ws, tau_out, n, A + row0, lda, tg);
-            double *dst = A + row0 + r0;
-#pragma unroll
-            for (int k = 0; k < C::KM; ++k)
-#pragma unroll
-                for (int cb = 0; cb < C::NCB; ++cb)
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int r = 8 * k + 2 * q + e, col = 8 * cb + l4;
-                        if (col < n && r < hk && r0 + r > col) dst[r + (int64_t)col * lda] = ch.a[k][cb][e];
-                    }
+            const bool mine = (g % C::NW == warp);
+            ++g;
+            const int cc = c++;
+            if (mine) {
+                nt = t; ncix = cc; ns = s; nb = b;
+                break;
+            }
         }
+        if (pt < 0) {                                     // first chunk: stream it in
+            if (nt < 0) break;
+            const int r0 = ncix * C::CH;
+            prefetch_chunk<C>(stg, A + tile_row0[nt] + r0, lda, min(C::CH, tile_rows[nt] - r0), n);
+            pt = nt; pc = ncix; ps = ns; pb = nb;
+            continue;
+        }
+        // compute the pending chunk
+        const int h = tile_rows[pt];
+        const int pnch = (h + C::CH - 1) / C::CH;
+        const int64_t row0 = tile_row0[pt];
+        const int r0 = pc * C::CH, hk = min(C::CH, h - r0);
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncwarp();
+        Chunk<C> ch;
+#pragma unroll
+        for (int k = 0; k < C::KM; ++k)
+#pragma unroll
+            for (int cb = 0; cb < C::NCB; ++cb) {
+                const double2 v = *reinterpret_cast<const double2 *>(stg + (8 * cb + l4) * C::CH + 8 * k + 2 * q);
+                ch.a[k][cb][0] = v.x;
+                ch.a[k][cb][1] = v.y;
+            }
+        __syncwarp();
+        if (nt >= 0) {                                    // the next chunk streams in meanwhile
+            const int r0n = ncix * C::CH;
+            prefetch_chunk<C>(stg, A + tile_row0[nt] + r0n, lda, min(C::CH, tile_rows[nt] - r0n), n);
+        }
+        PROBE(0);
+        double *tau_out = tau + (tile_chunk0[pt] + pc) * n;
+        const Sync sy{sync + pb * C::SYNC_INTS, sync + pb * C::SYNC_INTS + C::NP, ps};
+        double *tg = tcache ? tcache + (tile_chunk0[pt] + pc) * (C::NCB * 64) : nullptr;
+        chunk_panels<C, 0>(ch, r0, pc == pnch - 1, sm + pb * C::RBUF, sy, ws, tau_out, n, A + row0, lda, tg);
+        double *dst = A + row0 + r0;
+#pragma unroll
+        for (int k = 0; k < C::KM; ++k)
+#pragma unroll
+            for (int cb = 0; cb < C::NCB; ++cb)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int r = 8 * k + 2 * q + e, col = 8 * cb + l4;
+                    if (col < n && r < hk && r0 + r > col) dst[r + (int64_t)col * lda] = ch.a[k][cb][e];
+                }
+        if (nt < 0) break;
+        pt = nt; pc = ncix; ps = ns; pb = nb;
     }
     PROBE_FLUSH();
 }
