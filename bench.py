@@ -36,6 +36,9 @@ CONFIGS = {
                desc="fp64 A 4096x16 N(0,1) seed 0, row blocks 512 (8-leaf binary tree): factor + form Q"),
     "c2": dict(m=1_000_000, n=50, b=4096, s=4096, kind="gauss", op="form_q", k=0,
                desc="fp64 A 1,000,000x50 N(0,1), row blocks 4096, binary tree: factor + form Q"),
+    "c3": dict(m=100_000, n=200, b=2048, s=2048, kind="gauss", op="apply_qt", k=64,
+               desc="fp64 A 100,000x200 N(0,1), row blocks 2048 (blocked compact-WY leaves): factor + apply Q^T "
+                    "to C 100,000x64"),
     "c4": dict(m=16_777_216, n=64, b=4096, s=4096, kind="cond", op="form_q", k=0,
                desc="fp64 A 16,777,216x64 = G diag(sigma) V^T, sigma 1..1e-10: factor + form Q"),
     "c5": dict(m=33_554_432, n=32, b=4096, s=4096, kind="gauss", op="apply_qt", k=128,

@@ -33,7 +33,9 @@ typedef enum {
     TSQR_ERR_CUDA = 5          /* a CUDA runtime error (message: tsqr_last_error())     */
 } tsqr_status_t;
 
-#define TSQR_MAX_N 64          /* widest n the current kernels support */
+#define TSQR_MAX_N 256         /* widest n the kernels support: n <= 64 on the
+                                  register-resident chunk chains, 64 < n <= 256 on
+                                  the wide engine (tiles of at most 2304 rows)   */
 
 /* Plan options.
  *  block_rows: b, the paper's row-block height (A_i of Eq. 1); the

@@ -13,7 +13,7 @@ LIB_PATH = os.environ.get("TSQR_LIBRARY", os.path.join(HERE, "libtsqr.so"))
 TSQR_OK = 0
 STATUS = {0: "TSQR_OK", 1: "TSQR_ERR_INVALID", 2: "TSQR_ERR_SHAPE", 3: "TSQR_ERR_UNSUPPORTED",
           4: "TSQR_ERR_ALLOC", 5: "TSQR_ERR_CUDA"}
-MAX_N = 64
+MAX_N = 256
 
 # every symbol include/tsqr.h declares
 SYMBOLS = ["tsqr_status_string", "tsqr_last_error", "tsqr_slab", "tsqr_plan_info", "tsqr_plan_export",

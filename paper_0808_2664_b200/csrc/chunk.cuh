@@ -222,7 +222,11 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
         const double rj = Rb[j * C::LDR + 8 * P + l4];                // R(j, 8P + l4)
         const House h = house_bf(alpha, s2);
         const double w = fma(h.scale, d, rj);                        // v^T [R(j,c); a_c]
-        const double u = (l4 > jj) ? h.tau * h.scale * w : (l4 == jj ? 1.0 - h.scale : 0.0);
+        // a <- a - u x (u = tau scale w) for the trailing columns; the pivot
+        // column becomes v = scale x, formed as scale x + (a - x) with a - x
+        // exactly 0 (a - (1 - scale) x would cancel when scale << 1)
+        const double u = (l4 > jj) ? h.tau * h.scale * w : (l4 == jj ? 1.0 : 0.0);
+        const double g = (l4 == jj) ? h.scale : 0.0;
         // hand R row j to the next chunk first (its step j waits for it), then
         // update this chunk's panel
         const double rnew = (l4 == jj) ? h.beta : fma(-h.tau, w, rj);
@@ -231,8 +235,8 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
         sync_publish(sy.row + j, sy.s + 1);
 #pragma unroll
         for (int k = 0; k < C::KM; ++k) {
-            ch.a[k][P][0] = fma(-u, x[k][0], ch.a[k][P][0]);
-            ch.a[k][P][1] = fma(-u, x[k][1], ch.a[k][P][1]);
+            ch.a[k][P][0] = fma(g, x[k][0], fma(-u, x[k][0], ch.a[k][P][0]));
+            ch.a[k][P][1] = fma(g, x[k][1], fma(-u, x[k][1], ch.a[k][P][1]));
         }
         if (l4 == jj + 1) {                                          // next pivot column -> the other row
             double *xw = xs + ((jj + 1) & 1) * C::CH;
@@ -289,11 +293,12 @@ __device__ __forceinline__ void panel_dense(Chunk<C> &ch, int kb, double *Gs, do
         s2 += __shfl_xor_sync(FULL, s2, 2);
         const House h = house_bf(alpha, s2);
         const double w = fma(h.scale, d, rj);
-        const double u = (l4 > jj) ? h.tau * h.scale * w : (l4 == jj ? 1.0 - h.scale : 0.0);
+        const double u = (l4 > jj) ? h.tau * h.scale * w : (l4 == jj ? 1.0 : 0.0);
+        const double g = (l4 == jj) ? h.scale : 0.0;                 // pivot column: v = scale x exactly
 #pragma unroll
         for (int k = 0; k < C::KM; ++k) {
-            ch.a[k][P][0] = fma(-u, x[k][0], ch.a[k][P][0]);
-            ch.a[k][P][1] = fma(-u, x[k][1], ch.a[k][P][1]);
+            ch.a[k][P][0] = fma(g, x[k][0], fma(-u, x[k][0], ch.a[k][P][0]));
+            ch.a[k][P][1] = fma(g, x[k][1], fma(-u, x[k][1], ch.a[k][P][1]));
         }
         const double pnew = (l4 > jj) ? fma(-h.tau, w, rj) : (l4 == jj ? h.beta : rj);
         if (q == qp) {

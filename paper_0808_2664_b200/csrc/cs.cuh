@@ -137,7 +137,8 @@ __device__ __forceinline__ void panel_steps(Regs<C> &rg, int P, double *Rb, doub
         }
         const House h = house_bf(alpha, s2);
         const double w = fma(h.scale, dd, rj);
-        const double u = (l4 > jj) ? h.tau * h.scale * w : (l4 == jj ? 1.0 - h.scale : 0.0);
+        const double u = (l4 > jj) ? h.tau * h.scale * w : (l4 == jj ? 1.0 : 0.0);
+        const double g = (l4 == jj) ? h.scale : 0.0;                 // pivot column: v = scale x exactly
         const double pnew = (l4 > jj) ? fma(-h.tau, w, rj) : (l4 == jj ? h.beta : rj);
         const bool nxt = (l4 == jj + 1);
         double *xw = xs + ((jj + 1) & 1) * C::CH;
@@ -149,7 +150,7 @@ __device__ __forceinline__ void panel_steps(Regs<C> &rg, int P, double *Rb, doub
                 xv.x = (k > P || (k == P && 2 * q > jj)) ? xv.x : 0.0;
                 xv.y = (k > P || (k == P && 2 * q + 1 > jj)) ? xv.y : 0.0;
             }
-            double a0 = fma(-u, xv.x, rg.a[k][0][0]), a1 = fma(-u, xv.y, rg.a[k][0][1]);
+            double a0 = fma(g, xv.x, fma(-u, xv.x, rg.a[k][0][0])), a1 = fma(g, xv.y, fma(-u, xv.y, rg.a[k][0][1]));
             if (kDense) {                                                // the pivot row
                 const bool pr = (k == P) && (q == (jj >> 1));
                 a0 = (pr && !(jj & 1)) ? pnew : a0;

@@ -14,11 +14,13 @@ int padded_width(int64_t n) { return n <= 16 ? 16 : (n <= 32 ? 32 : 64); }
 // A tile is factored as a flat chain of register-resident chunks (chunk.cuh),
 // so its height is bounded only by the 32-bit row count of the device plan.
 // Default tile: 32 chunks of the chain.
-int64_t tile_capacity(int64_t) { return (int64_t)1 << 30; }
-int64_t default_tile_rows(int64_t n) { return 32 * (int64_t)chunk_rows_for(n); }
+// Wide n (> 64): the leaf is one blocked QR of the whole tile by one CTA, at
+// most 2304 logical rows (tsqr_wide.cu), default 2048.
+int64_t tile_capacity(int64_t n) { return n > 64 ? 2304 : (int64_t)1 << 30; }
+int64_t default_tile_rows(int64_t n) { return n > 64 ? 2048 : 32 * (int64_t)chunk_rows_for(n); }
 // chunk.cuh: 64 doubles of chunk per lane -- KM = 8 row blocks (64 rows) for
 // n <= 32, KM = 4 (32 rows) for n <= 64
-int chunk_rows_for(int64_t n) { return n <= 32 ? 64 : 32; }
+int chunk_rows_for(int64_t n) { return n <= 32 ? 64 : (n <= 64 ? 32 : 0); }   // 0: one chunk per tile
 
 static int64_t block_count(int64_t m, int64_t n, int64_t b, int64_t *last_rows) {
     // Reading R6: blocks of b rows; a remainder >= n is its own block, a
@@ -91,7 +93,8 @@ int build_plan(int64_t m_local, int64_t n, int64_t block_rows, int64_t tile_rows
     const int L = p->ntiles();
     p->c = chunk_rows_for(n);
     p->tile_chunk0.assign(L + 1, 0);
-    for (int t = 0; t < L; ++t) p->tile_chunk0[t + 1] = p->tile_chunk0[t] + (p->tile_rows[t] + p->c - 1) / p->c;
+    for (int t = 0; t < L; ++t)
+        p->tile_chunk0[t + 1] = p->tile_chunk0[t] + (p->c > 0 ? (p->tile_rows[t] + p->c - 1) / p->c : 1);
     p->max_rows = *std::max_element(p->tile_rows.begin(), p->tile_rows.end());
     p->min_rows = *std::min_element(p->tile_rows.begin(), p->tile_rows.end());
 

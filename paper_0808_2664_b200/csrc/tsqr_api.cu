@@ -5,6 +5,7 @@
 #include "plan.h"
 #include "tsqr_kernels.h"
 
+#include <algorithm>
 #include <cstring>
 #include <new>
 #include <string>
@@ -38,6 +39,11 @@ struct tsqr_tree_s {
     double *d_tau_chunk = nullptr;
     double *d_tcache = nullptr;       // [chunks][NCB][8][8] panel T factors (compact WY)
     int64_t nchunks = 0;
+    // wide n (> 64): per-node T cache, butterfly T caches, a stacking buffer
+    bool wide = false;
+    int npan = 0;
+    double *d_tcache_node = nullptr, *d_cross_tcache = nullptr, *d_wtmp = nullptr;
+    int64_t wtmp_size = 0;
     std::vector<int> step_off;   // top-down: groups [step_off[g], step_off[g+1])
     DevPlan dplan{};
 };
@@ -61,9 +67,25 @@ static tsqr_status_t debug_sync(const tsqr_tree_s *t, cudaStream_t st, const cha
 static void free_tree_memory(tsqr_tree_s *t) {
     void *ptrs[] = {t->d_row0, t->d_rows, t->d_tparent, t->d_node_a, t->d_nparent, t->d_tau_tile,
                     t->d_tau_node, t->d_counters, t->d_cross_y1, t->d_cross_tau, t->d_xbuf,
-                    t->d_step_ids, t->d_tile_chunk0, t->d_cta_tile0, t->d_tau_chunk, t->d_tcache};
+                    t->d_step_ids, t->d_tile_chunk0, t->d_cta_tile0, t->d_tau_chunk, t->d_tcache,
+                    t->d_tcache_node, t->d_cross_tcache, t->d_wtmp};
     for (void *p : ptrs)
         if (p) cudaFree(p);
+}
+
+// The wide path's stacking buffer (2n x max(n, cols) doubles), grown on demand.
+static tsqr_status_t wide_tmp(tsqr_tree_s *t, int64_t cols) {
+    const int64_t need = 2 * t->plan.n * std::max<int64_t>(cols, t->plan.n);
+    if (t->d_wtmp && t->wtmp_size >= need) return TSQR_OK;
+    if (t->d_wtmp) cudaFree(t->d_wtmp);
+    t->d_wtmp = nullptr;
+    if (cudaMalloc((void **)&t->d_wtmp, sizeof(double) * need) != cudaSuccess) {
+        cudaGetLastError();
+        t->wtmp_size = 0;
+        return TSQR_ERR_ALLOC;
+    }
+    t->wtmp_size = need;
+    return TSQR_OK;
 }
 
 static int ilog2(int x) {
@@ -206,15 +228,27 @@ static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t 
     alloc((void **)&t->d_cross_tau, sizeof(double) * (t->cross_rounds + 1) * n);
     alloc((void **)&t->d_step_ids, sizeof(int) * (ids.size() + 1));
     const int64_t nchunks = p.tile_chunk0[L];
-    int grid = chain_grid((int)n);
-    if (grid > L) grid = L;
-    std::vector<int> cta_tile0;
-    chain_partition(p.tile_rows, p.c, grid, cta_tile0);
+    t->wide = n > 64;
+    t->npan = (int)((n + 7) / 8);
+    int grid = 1;
+    std::vector<int> cta_tile0(2, 0);
+    if (!t->wide) {
+        grid = chain_grid((int)n);
+        if (grid > L) grid = L;
+        chain_partition(p.tile_rows, p.c, grid, cta_tile0);
+    } else {
+        cta_tile0[1] = L;
+    }
     t->chain_grid = grid;
     alloc((void **)&t->d_tile_chunk0, sizeof(int64_t) * (L + 1));
     alloc((void **)&t->d_cta_tile0, sizeof(int) * (grid + 1));
     alloc((void **)&t->d_tau_chunk, sizeof(double) * nchunks * n);
-    alloc((void **)&t->d_tcache, sizeof(double) * nchunks * chain_ncb((int)n) * 64);
+    const int ncb_cache = t->wide ? t->npan : chain_ncb((int)n);
+    alloc((void **)&t->d_tcache, sizeof(double) * nchunks * ncb_cache * 64);
+    if (t->wide) {
+        alloc((void **)&t->d_tcache_node, sizeof(double) * L * t->npan * 64);
+        alloc((void **)&t->d_cross_tcache, sizeof(double) * (ilog2(ro.nranks) + 1) * t->npan * 64);
+    }
     t->nchunks = nchunks;
     if (e != cudaSuccess) {
         free_tree_memory(t);
@@ -290,6 +324,20 @@ tsqr_status_t tsqr_factor(int64_t m_local, int64_t n, double *A, int64_t lda, do
     ca.A = A; ca.lda = lda; ca.n = (int)n; ca.chunk_rows = t->plan.c;
     ca.tile_row0 = t->d_row0; ca.tile_rows = t->d_rows; ca.tile_chunk0 = t->d_tile_chunk0;
     ca.cta_tile0 = t->d_cta_tile0; ca.grid = t->chain_grid; ca.tau = t->d_tau_chunk; ca.tcache = t->d_tcache;
+    if (t->wide) {
+        const int L = t->plan.ntiles();
+        CUDA_TRY(launch_wide_leaves(A, lda, (int)n, t->d_row0, t->d_rows, L, t->d_tau_chunk, t->d_tcache, t->stream),
+                 "tsqr_factor leaves");
+        for (size_t g = t->step_off.size() - 1; g-- > 0;) {         // tree steps bottom-up
+            const int cnt = t->step_off[g + 1] - t->step_off[g];
+            if (cnt == 0) continue;
+            CUDA_TRY(launch_wide_nodes(A, lda, (int)n, t->d_row0, t->d_node_a, t->d_step_ids + t->step_off[g], cnt,
+                                       t->d_tau_node, t->d_tcache_node, t->stream),
+                     "tsqr_factor tree");
+        }
+        if (R) CUDA_TRY(launch_extract_r(A, lda, (int)n, R, ldr, t->stream), "tsqr_factor R");
+        return debug_sync(t, t->stream, "tsqr_factor");
+    }
     CUDA_TRY(launch_chain_factor(ca, t->stream), "tsqr_factor leaves");
     CUDA_TRY(launch_tree(f, t->stream), "tsqr_factor tree");
     return debug_sync(t, t->stream, "tsqr_factor");
@@ -311,10 +359,21 @@ tsqr_status_t tsqr_cross_factor(tsqr_tree_t t, int32_t round, const double *part
     if (tsqr_cross_partner(t->opts.nranks, t->opts.rank, round, &partner, &lower, &role) != TSQR_OK)
         return TSQR_ERR_INVALID;
     const int n = (int)t->plan.n;
-    CUDA_TRY(launch_cross_factor(t->NP, t->A, t->lda, n, partner_packed, lower,
-                                 t->d_cross_y1 + (int64_t)(round - 1) * n * n,
-                                 t->d_cross_tau + (int64_t)(round - 1) * n, R, ldr, (cudaStream_t)stream),
-             "tsqr_cross_factor");
+    if (t->wide) {
+        tsqr_status_t ws = wide_tmp(t, n);
+        if (ws != TSQR_OK) return ws;
+        CUDA_TRY(launch_wide_cross_factor(t->A, t->lda, n, partner_packed, lower, t->d_wtmp,
+                                          t->d_cross_y1 + (int64_t)(round - 1) * n * n,
+                                          t->d_cross_tau + (int64_t)(round - 1) * n,
+                                          t->d_cross_tcache + (int64_t)(round - 1) * t->npan * 64, R, ldr,
+                                          (cudaStream_t)stream),
+                 "tsqr_cross_factor");
+    } else {
+        CUDA_TRY(launch_cross_factor(t->NP, t->A, t->lda, n, partner_packed, lower,
+                                     t->d_cross_y1 + (int64_t)(round - 1) * n * n,
+                                     t->d_cross_tau + (int64_t)(round - 1) * n, R, ldr, (cudaStream_t)stream),
+                 "tsqr_cross_factor");
+    }
     t->cross_done = round;
     t->stream = (cudaStream_t)stream;
     return debug_sync(t, t->stream, "tsqr_cross_factor");
@@ -341,8 +400,22 @@ tsqr_status_t tsqr_apply_qt(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, do
     ca.tile_row0 = t->d_row0; ca.tile_rows = t->d_rows; ca.tile_chunk0 = t->d_tile_chunk0;
     ca.cta_tile0 = t->d_cta_tile0; ca.grid = t->chain_grid; ca.tcache = t->d_tcache;
     ca.C = C; ca.ldc = ldc; ca.k = (int)k; ca.forward = 1; ca.xbuf = nullptr;
-    CUDA_TRY(launch_cs_apply(ca, st), "tsqr_apply_qt leaves");
-    if (t->plan.ntiles() > 1) CUDA_TRY(launch_apply_nodes(f, st), "tsqr_apply_qt nodes");
+    if (t->wide) {
+        const int n = (int)t->plan.n;
+        CUDA_TRY(launch_wide_apply_leaves(t->A, t->lda, n, t->d_row0, t->d_rows, t->plan.ntiles(), t->d_tcache, C,
+                                          ldc, (int)k, 1, st),
+                 "tsqr_apply_qt leaves");
+        for (size_t g = t->step_off.size() - 1; g-- > 0;) {         // tree steps bottom-up
+            const int cnt = t->step_off[g + 1] - t->step_off[g];
+            if (cnt == 0) continue;
+            CUDA_TRY(launch_wide_apply_nodes(t->A, t->lda, n, t->d_row0, t->d_node_a, t->d_step_ids + t->step_off[g],
+                                             cnt, t->d_tcache_node, C, ldc, (int)k, 1, 0, st),
+                     "tsqr_apply_qt nodes");
+        }
+    } else {
+        CUDA_TRY(launch_cs_apply(ca, st), "tsqr_apply_qt leaves");
+        if (t->plan.ntiles() > 1) CUDA_TRY(launch_apply_nodes(f, st), "tsqr_apply_qt nodes");
+    }
     if (top) CUDA_TRY(launch_copy_block(C, ldc, top, ldtop, (int)t->plan.n, (int)k, st), "tsqr_apply_qt top");
     t->stream = st;
     return debug_sync(t, st, "tsqr_apply_qt");
@@ -359,10 +432,20 @@ tsqr_status_t tsqr_cross_apply_qt(tsqr_tree_t t, int32_t round, double *top, int
     if (role != 0 && (!C || ldc < t->plan.m_local)) return TSQR_ERR_INVALID;
     if (k == 0) return TSQR_OK;
     const int n = (int)t->plan.n;
-    CUDA_TRY(launch_cross_apply(t->NP, t->d_cross_y1 + (int64_t)(round - 1) * n * n,
-                                t->d_cross_tau + (int64_t)(round - 1) * n, top, ldtop, partner_top, lower, role,
-                                C, ldc, n, (int)k, (cudaStream_t)stream),
-             "tsqr_cross_apply_qt");
+    if (t->wide) {
+        tsqr_status_t ws = wide_tmp(t, k);
+        if (ws != TSQR_OK) return ws;
+        CUDA_TRY(launch_wide_cross_apply(t->d_cross_y1 + (int64_t)(round - 1) * n * n,
+                                         t->d_cross_tcache + (int64_t)(round - 1) * t->npan * 64, top, ldtop,
+                                         partner_top, lower, role, C, ldc, n, (int)k, t->d_wtmp,
+                                         (cudaStream_t)stream),
+                 "tsqr_cross_apply_qt");
+    } else {
+        CUDA_TRY(launch_cross_apply(t->NP, t->d_cross_y1 + (int64_t)(round - 1) * n * n,
+                                    t->d_cross_tau + (int64_t)(round - 1) * n, top, ldtop, partner_top, lower, role,
+                                    C, ldc, n, (int)k, (cudaStream_t)stream),
+                 "tsqr_cross_apply_qt");
+    }
     t->stream = (cudaStream_t)stream;
     return debug_sync(t, t->stream, "tsqr_cross_apply_qt");
 }
@@ -382,6 +465,26 @@ tsqr_status_t tsqr_form_q(tsqr_tree_t t, double *Q, int64_t ldq, void *stream) {
             g_last_error = std::string("tsqr_form_q alloc: ") + cudaGetErrorString(e);
             return TSQR_ERR_ALLOC;
         }
+    }
+    if (t->wide) {
+        tsqr_status_t ws = wide_tmp(t, n);
+        if (ws != TSQR_OK) return ws;
+        CUDA_TRY(cudaMemsetAsync(t->d_xbuf, 0, sizeof(double) * (size_t)L * n * n, st), "tsqr_form_q");
+        CUDA_TRY(launch_wide_cross_root_x(t->d_cross_y1, t->d_cross_tcache, (int64_t)t->npan * 64, t->cross_rounds,
+                                          t->opts.rank, n, t->d_wtmp, t->d_xbuf, st),
+                 "tsqr_form_q root");
+        for (size_t g = 0; g + 1 < t->step_off.size(); ++g) {         // tree steps top-down
+            const int cnt = t->step_off[g + 1] - t->step_off[g];
+            if (cnt == 0) continue;
+            CUDA_TRY(launch_wide_apply_nodes(t->A, t->lda, n, t->d_row0, t->d_node_a, t->d_step_ids + t->step_off[g],
+                                             cnt, t->d_tcache_node, t->d_xbuf, n, n, 0, 1, st),
+                     "tsqr_form_q nodes");
+        }
+        CUDA_TRY(launch_wide_formq_init(t->d_row0, t->d_rows, L, n, t->d_xbuf, Q, ldq, st), "tsqr_form_q");
+        CUDA_TRY(launch_wide_apply_leaves(t->A, t->lda, n, t->d_row0, t->d_rows, L, t->d_tcache, Q, ldq, n, 0, st),
+                 "tsqr_form_q leaves");
+        t->stream = st;
+        return debug_sync(t, st, "tsqr_form_q");
     }
     // root X of this rank: I (one GPU) or the butterfly path (no communication)
     if (t->cross_rounds == 0) CUDA_TRY(launch_identity(t->d_xbuf, n, st), "tsqr_form_q identity");

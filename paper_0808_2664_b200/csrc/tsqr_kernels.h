@@ -68,6 +68,33 @@ int chain_grid(int n);
 cudaError_t launch_chain_factor(const ChainArgs &f, cudaStream_t st);
 // Leaf stage of Q^T C / form Q on the chain representation (tsqr_cs.cu).
 cudaError_t launch_cs_apply(const ChainApplyArgs &f, cudaStream_t st);
+// Wide-n engine (tsqr_wide.cu, 64 < n <= 256): one CTA per leaf / node problem.
+int wide_max_rows();
+cudaError_t launch_wide_leaves(double *A, int64_t lda, int n, const int64_t *row0, const int *rows, int L,
+                               double *tau, double *tcache, cudaStream_t st);
+cudaError_t launch_wide_nodes(double *A, int64_t lda, int n, const int64_t *row0, const int *node_a, const int *ids,
+                              int count, double *tau_node, double *tcache_node, cudaStream_t st);
+cudaError_t launch_wide_node1(double *Ra, int64_t lda, double *Rb, int64_t ldb, int n, double *tau, double *tcache,
+                              cudaStream_t st);
+cudaError_t launch_wide_apply_leaves(const double *A, int64_t lda, int n, const int64_t *row0, const int *rows,
+                                     int L, const double *tcache, double *C, int64_t ldc, int k, int forward,
+                                     cudaStream_t st);
+cudaError_t launch_wide_apply_nodes(const double *A, int64_t lda, int n, const int64_t *row0, const int *node_a,
+                                    const int *ids, int count, const double *tcache_node, double *C, int64_t ldc,
+                                    int k, int forward, int xbuf_mode, cudaStream_t st);
+cudaError_t launch_wide_apply_node1(const double *Y1, int64_t ldy, int n, const double *tcache, double *Ca,
+                                    int64_t ldca, double *Cb, int64_t ldcb, int k, int forward, cudaStream_t st);
+cudaError_t launch_wide_formq_init(const int64_t *row0, const int *rows, int L, int n, const double *xbuf, double *Q,
+                                   int64_t ldq, cudaStream_t st);
+cudaError_t launch_extract_r(const double *A, int64_t lda, int n, double *R, int64_t ldr, cudaStream_t st);
+cudaError_t launch_wide_cross_factor(double *A, int64_t lda, int n, const double *packed, int is_lower, double *tmp,
+                                     double *Y1, double *tau, double *tcache, double *R, int64_t ldr,
+                                     cudaStream_t st);
+cudaError_t launch_wide_cross_apply(const double *Y1, const double *tcache, double *top, int64_t ldtop,
+                                    const double *ptop, int is_lower, int role, double *C, int64_t ldc, int n, int k,
+                                    double *tmp, cudaStream_t st);
+cudaError_t launch_wide_cross_root_x(const double *Y1s, const double *tcaches, int64_t tstride, int rounds, int rank,
+                                     int n, double *tmp, double *X0, cudaStream_t st);
 // Column-split factor (tsqr_cs.cu, 256-row chunks; kept for experiments).
 int cs_grid(int n);
 cudaError_t launch_cs_factor(const ChainArgs &f, cudaStream_t st);

@@ -1,0 +1,566 @@
+// Wide-n engine of the B200 TSQR path (64 < n <= 256, config 3's n = 200).  Product code.
+//
+// For wide n the running R of a flat chain (n x n, 320 KB at n = 200) does not
+// fit on chip, so every leaf is factored by a blocked compact-WY Householder QR
+// of the whole tile (the paper's leaf, DGEQR2 order, Alg. TSQR:par line 1
+// P:1679-1680; compact WY Alg. YT:scaled P:2007-2028) by one CTA, with the tile
+// in global memory (L2-resident):
+//   panel p (8 columns): loaded row-split over the 8 warps (each warp a fixed
+//       range of up to 288 logical rows, DMMA-fragment layout), Householder
+//       steps with warp-shuffle + one __syncthreads cross-warp reduction per
+//       column, written back (R above, v below the diagonal), T built;
+//   trailing update, column-split: warp w owns column blocks w, w+8, ...; it
+//       streams W^T = C^T Y over the rows (FP64 DMMA), W'^T = W^T T and
+//       C -= Y W' -- no cross-warp reduction at all.
+// A tree node (Alg. QR:qnxn, [R_a; R_b], eq. fact_2rs) is the same kernel on
+// the stacked logical rows [R_a rows 0..n-1; R_b rows 0..n-1] with masks: R_a
+// row i holds column c only for i <= c, R_b row r only for r <= c; everything
+// else reads as zero and is never written.  The zeros are exact, so this is
+// the structured combine itself (same beta, tau, v), touching only the
+// upper triangles: R lands in R_a's, the node's Y1 in R_b's.
+// k_wide_apply applies the stored reflectors (Q^T: panels forward with T^T;
+// Q: backward with T) to C rows mapped the same way, column-split, no barriers.
+#include "tsqr_kernels.h"
+#include "wy.cuh"
+
+namespace tsqr {
+namespace wide {
+
+using wy::dmma;
+using wy::House;
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int NW = 8, NT = 256, KMW = 36, RW = 8 * KMW;   // rows per warp (logical)
+constexpr int MAXR = NW * RW;                               // 2304 logical rows
+
+// branch-free dlarfg scalars (readings R1/R2/R19), as chunk::house_bf
+__device__ __forceinline__ House house(double alpha, double s2) {
+    const double y = fma(alpha, alpha, s2);
+    const double aa = fabs(alpha);
+    double r, i;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(y));
+    const double D0 = fma(y, r, aa);
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(i) : "d"(D0));
+    const double hy = 0.5 * y;
+    r = r * fma(-hy * r, r, 1.5);
+    r = r * fma(-hy * r, r, 1.5);
+    const double N = y * r;
+    const double D = aa + N;
+    i = fma(i, fma(-D, i, 1.0), i);
+    i = fma(i, fma(-D, i, 1.0), i);
+    const bool z = (s2 == 0.0);
+    House h;
+    h.beta = z ? alpha : (alpha >= 0.0 ? -N : N);
+    h.tau = z ? 0.0 : fma(aa, r, 1.0);
+    h.scale = z ? 0.0 : (alpha >= 0.0 ? i : -i);
+    return h;
+}
+
+// A problem: logical rows [0, hA) -> segment A rows (the first nA exist),
+// [hA, hA + hB) -> segment B rows.  A node pads its R_a segment to hA = NP
+// rows so that R_b starts on an 8-row block; the padding rows never exist.
+struct Prob {
+    double *a;       // segment A (ld lda)
+    double *b;       // segment B (ld ldb), may be null when hB = 0
+    int64_t lda, ldb;
+    int hA, hB, nA;
+    int node;        // 1: [R_a; R_b] upper-triangle masks
+};
+
+__device__ __forceinline__ double *rowp(const Prob &P, int r, int c) {
+    return r < P.hA ? P.a + r + (int64_t)c * P.lda : P.b + (r - P.hA) + (int64_t)c * P.ldb;
+}
+__device__ __forceinline__ bool row_exists(const Prob &P, int r) {
+    return r < P.hA ? r < P.nA : r - P.hA < P.hB;
+}
+// Is logical element (r, c) part of the problem's matrix (else it reads as 0
+// and is never written)?
+__device__ __forceinline__ bool present(const Prob &P, int r, int c, int n) {
+    if (c >= n || !row_exists(P, r)) return false;
+    if (!P.node) return true;
+    return r < P.hA ? r <= c : (r - P.hA) <= c;
+}
+// Y(r, j) of reflector j (pivot = logical row j) from the stored factor.
+__device__ __forceinline__ double yval(const Prob &P, int r, int j, int n) {
+    if (j >= n || r < j) return 0.0;
+    if (r == j) return 1.0;
+    return present(P, r, j, n) ? *rowp(P, r, j) : 0.0;
+}
+
+struct Smem {
+    double part[2][NW][9];     // per-step partial dots (8 columns) + sigma^2, double-buffered
+    double piv[2][8];          // the pivot row's panel values
+    double Gs[64], Ts[64], t8[8];
+    double xs[NW][2][RW];      // per-warp pivot-column broadcast (double-buffered)
+};
+
+// One problem: blocked Householder QR in place; tau[n], tcache[npan][64].
+__device__ void wide_qr(const Prob &P, int n, double *tau, double *tcache, Smem &S) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+    const int H = P.hA + P.hB;
+    const int npan = (n + 7) / 8;
+    const int rbase = warp * RW;
+    for (int p = 0; p < npan; ++p) {
+        const int c = 8 * p + l4;
+        // ---- load the panel (this warp's logical rows)
+        double a[KMW][2];
+#pragma unroll
+        for (int k = 0; k < KMW; ++k)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int r = rbase + 8 * k + 2 * q + e;
+                a[k][e] = present(P, r, c, n) ? *rowp(P, r, c) : 0.0;
+            }
+        double *xs0 = S.xs[warp][0], *xs1 = S.xs[warp][1];
+        if (l4 == 0) {
+#pragma unroll
+            for (int k = 0; k < KMW; ++k)
+                *reinterpret_cast<double2 *>(xs0 + 8 * k + 2 * q) = make_double2(a[k][0], a[k][1]);
+        }
+        __syncwarp();
+#pragma unroll 1
+        for (int jj = 0; jj < 8; ++jj) {
+            const int j = 8 * p + jj;                         // pivot = logical row j
+            const int par = jj & 1;
+            const double *xr = par ? xs1 : xs0;
+            double d[4] = {0.0, 0.0, 0.0, 0.0}, s[4] = {0.0, 0.0, 0.0, 0.0};
+            double pv = 0.0;                                  // this lane's entry of the pivot row
+            bool haspiv = false;
+#pragma unroll
+            for (int k = 0; k < KMW; ++k) {
+                const double2 xv = *reinterpret_cast<const double2 *>(xr + 8 * k + 2 * q);
+                const int r = rbase + 8 * k + 2 * q;
+                const double x0 = r > j ? xv.x : 0.0, x1 = r + 1 > j ? xv.y : 0.0;
+                d[k & 3] = fma(x0, a[k][0], d[k & 3]);
+                d[(k + 2) & 3] = fma(x1, a[k][1], d[(k + 2) & 3]);
+                s[k & 3] = fma(x0, x0, s[k & 3]);
+                s[(k + 2) & 3] = fma(x1, x1, s[(k + 2) & 3]);
+                if (r == j) { pv = a[k][0]; haspiv = true; }
+                if (r + 1 == j) { pv = a[k][1]; haspiv = true; }
+            }
+            double dd = (d[0] + d[1]) + (d[2] + d[3]), s2 = (s[0] + s[1]) + (s[2] + s[3]);
+            dd += __shfl_xor_sync(FULL, dd, 1);
+            s2 += __shfl_xor_sync(FULL, s2, 1);
+            dd += __shfl_xor_sync(FULL, dd, 2);
+            s2 += __shfl_xor_sync(FULL, s2, 2);
+            if (q == 0) S.part[par][warp][l4] = dd;
+            if (lane == 0) S.part[par][warp][8] = s2;
+            if (haspiv) S.piv[par][l4] = pv;
+            __syncthreads();
+            dd = 0.0;
+            s2 = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                dd += S.part[par][w][l4];
+                s2 += S.part[par][w][8];
+            }
+            const double rj = S.piv[par][l4], alpha = S.piv[par][jj];
+            const House h = house(alpha, s2);
+            const double wv = fma(h.scale, dd, rj);
+            const double u = (l4 > jj) ? h.tau * h.scale * wv : (l4 == jj ? 1.0 : 0.0);
+            const double g = (l4 == jj) ? h.scale : 0.0;             // pivot column: v = scale x exactly
+            const double pnew = (l4 > jj) ? fma(-h.tau, wv, rj) : (l4 == jj ? h.beta : rj);
+            double *xw = par ? xs0 : xs1;
+#pragma unroll
+            for (int k = 0; k < KMW; ++k) {
+                const double2 xv = *reinterpret_cast<const double2 *>(xr + 8 * k + 2 * q);
+                const int r = rbase + 8 * k + 2 * q;
+                const double x0 = r > j ? xv.x : 0.0, x1 = r + 1 > j ? xv.y : 0.0;
+                double a0 = fma(g, x0, fma(-u, x0, a[k][0])), a1 = fma(g, x1, fma(-u, x1, a[k][1]));
+                a0 = (r == j) ? pnew : a0;
+                a1 = (r + 1 == j) ? pnew : a1;
+                a[k][0] = a0;
+                a[k][1] = a1;
+                if (l4 == jj + 1) *reinterpret_cast<double2 *>(xw + 8 * k + 2 * q) = make_double2(a0, a1);
+            }
+            if (warp == 0 && q == 0 && l4 < jj) S.Gs[l4 * 8 + jj] = fma(h.scale, dd, rj);
+            if (threadIdx.x == 0) S.t8[jj] = h.tau;
+            __syncwarp();
+        }
+        // ---- write the panel back; T; taus
+#pragma unroll
+        for (int k = 0; k < KMW; ++k)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int r = rbase + 8 * k + 2 * q + e;
+                if (present(P, r, c, n)) *rowp(P, r, c) = a[k][e];
+            }
+        __syncthreads();
+        if (warp == 0) {
+            const int rr = lane & 7;
+            double row[8];
+            const double tr = S.t8[rr];
+#pragma unroll
+            for (int cc = 0; cc < 8; ++cc) row[cc] = (cc == rr) ? tr : 0.0;
+#pragma unroll
+            for (int cc = 1; cc < 8; ++cc) {
+                double sacc = 0.0;
+#pragma unroll
+                for (int l = 0; l < cc; ++l) sacc = fma(row[l], S.Gs[l * 8 + cc], sacc);
+                row[cc] = (rr < cc) ? -S.t8[cc] * sacc : row[cc];
+            }
+            if (lane < 8) {
+#pragma unroll
+                for (int cc = 0; cc < 8; ++cc) {
+                    S.Ts[lane * 8 + cc] = row[cc];
+                    tcache[p * 64 + lane * 8 + cc] = row[cc];
+                }
+                if (8 * p + lane < n) tau[8 * p + lane] = S.t8[lane];
+            }
+        }
+        __syncthreads();
+        // ---- trailing update, column-split over the warps
+        const double tb0 = S.Ts[(2 * q) * 8 + l4], tb1 = S.Ts[(2 * q + 1) * 8 + l4];
+        const int rb0 = P.node ? 0 : p;                        // first logical row block touched
+        const int nrb = (H + 7) / 8;
+        for (int cb = p + 1 + warp; cb < npan; cb += NW) {
+            const int col = 8 * cb + l4;
+            double w0[2] = {0.0, 0.0}, w1[2] = {0.0, 0.0};
+            for (int k = rb0; k < nrb; ++k) {
+                if (P.node && !(k == p || (k >= P.hA / 8 && k - P.hA / 8 <= p))) continue;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int r = 8 * k + 2 * q + e;
+                    const double cv = present(P, r, col, n) ? *rowp(P, r, col) : 0.0;
+                    const double yv = yval(P, r, 8 * p + l4, n);
+                    dmma(w0[k & 1], w1[k & 1], cv, yv);
+                }
+            }
+            double p0 = 0.0, p1 = 0.0;
+            dmma(p0, p1, w0[0] + w0[1], tb0);
+            dmma(p0, p1, w1[0] + w1[1], tb1);
+            for (int k = rb0; k < nrb; ++k) {
+                if (P.node && !(k == p || (k >= P.hA / 8 && k - P.hA / 8 <= p))) continue;
+                const int r0 = 8 * k + 2 * q;
+                const bool ok0 = present(P, r0, col, n), ok1 = present(P, r0 + 1, col, n);
+                double c0 = ok0 ? *rowp(P, r0, col) : 0.0, c1 = ok1 ? *rowp(P, r0 + 1, col) : 0.0;
+                const double y0 = yval(P, 8 * k + l4, 8 * p + 2 * q, n), y1 = yval(P, 8 * k + l4, 8 * p + 2 * q + 1, n);
+                dmma(c0, c1, -p0, y0);
+                dmma(c0, c1, -p1, y1);
+                if (ok0) *rowp(P, r0, col) = c0;
+                if (ok1) *rowp(P, r0 + 1, col) = c1;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Apply the problem's stored reflectors to C (rows mapped like the problem's,
+// every element present): Q^T (kFwd, panels forward, T^T) or Q (backward, T).
+template <bool kFwd>
+__device__ void wide_apply(const Prob &P, const Prob &Cp, int n, int k, const double *tcache) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+    const int H = P.hA + P.hB;
+    const int npan = (n + 7) / 8;
+    const int nrb = (H + 7) / 8;
+    auto cptr = [&](int r, int col) -> double * {
+        return r < Cp.hA ? Cp.a + r + (int64_t)col * Cp.lda : Cp.b + (r - Cp.hA) + (int64_t)col * Cp.ldb;
+    };
+    for (int cb = warp; cb < (k + 7) / 8; cb += NW) {
+        const int col = 8 * cb + l4;
+        const bool okc = col < k;
+        for (int pp = 0; pp < npan; ++pp) {
+            const int p = kFwd ? pp : npan - 1 - pp;
+            const double *Tg = tcache + p * 64;
+            const double tb0 = kFwd ? Tg[(2 * q) * 8 + l4] : Tg[l4 * 8 + 2 * q];
+            const double tb1 = kFwd ? Tg[(2 * q + 1) * 8 + l4] : Tg[l4 * 8 + 2 * q + 1];
+            const int rb0 = P.node ? 0 : p;
+            double w0[2] = {0.0, 0.0}, w1[2] = {0.0, 0.0};
+            for (int kk = rb0; kk < nrb; ++kk) {
+                if (P.node && !(kk == p || (kk >= P.hA / 8 && kk - P.hA / 8 <= p))) continue;
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int r = 8 * kk + 2 * q + e;
+                    const double cv = (okc && row_exists(Cp, r)) ? *cptr(r, col) : 0.0;
+                    dmma(w0[kk & 1], w1[kk & 1], cv, yval(P, r, 8 * p + l4, n));
+                }
+            }
+            double p0 = 0.0, p1 = 0.0;
+            dmma(p0, p1, w0[0] + w0[1], tb0);
+            dmma(p0, p1, w1[0] + w1[1], tb1);
+            for (int kk = rb0; kk < nrb; ++kk) {
+                if (P.node && !(kk == p || (kk >= P.hA / 8 && kk - P.hA / 8 <= p))) continue;
+                const int r0 = 8 * kk + 2 * q;
+                const bool e0 = okc && row_exists(Cp, r0), e1 = okc && row_exists(Cp, r0 + 1);
+                double c0 = e0 ? *cptr(r0, col) : 0.0, c1 = e1 ? *cptr(r0 + 1, col) : 0.0;
+                dmma(c0, c1, -p0, yval(P, 8 * kk + l4, 8 * p + 2 * q, n));
+                dmma(c0, c1, -p1, yval(P, 8 * kk + l4, 8 * p + 2 * q + 1, n));
+                if (e0) *cptr(r0, col) = c0;
+                if (e1) *cptr(r0 + 1, col) = c1;
+            }
+        }
+    }
+}
+
+}  // namespace wide
+
+using namespace wide;
+
+// Leaves: problem t = tile t (one CTA each).
+__global__ void __launch_bounds__(NT, 1)
+k_wide_leaves(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *tile_rows, double *tau_tile,
+              double *tcache_tile) {
+    extern __shared__ __align__(16) double smraw[];
+    Smem &S = *reinterpret_cast<Smem *>(smraw);
+    const int t = blockIdx.x;
+    const int npan = (n + 7) / 8;
+    Prob P{A + tile_row0[t], nullptr, lda, 0, tile_rows[t], 0, tile_rows[t], 0};
+    wide_qr(P, n, tau_tile + (int64_t)t * n, tcache_tile + (int64_t)t * npan * 64, S);
+}
+
+// Tree nodes of one step: node ids[i] = b (right subtree's first tile), its
+// left child's first tile node_a[b]; [R_a; R_b] in the tiles' head rows.
+__global__ void __launch_bounds__(NT, 1)
+k_wide_nodes(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *node_a, const int *ids,
+             double *tau_node, double *tcache_node) {
+    extern __shared__ __align__(16) double smraw[];
+    Smem &S = *reinterpret_cast<Smem *>(smraw);
+    const int b = ids[blockIdx.x];
+    const int npan = (n + 7) / 8;
+    Prob P{A + tile_row0[node_a[b]], A + tile_row0[b], lda, lda, 8 * npan, n, n, 1};
+    wide_qr(P, n, tau_node + (int64_t)b * n, tcache_node + (int64_t)b * npan * 64, S);
+}
+
+// A single stacked node [Ra (ld lda); Rb (ld ldb)] (the cross-GPU rounds).
+__global__ void __launch_bounds__(NT, 1)
+k_wide_node1(double *Ra, int64_t lda, double *Rb, int64_t ldb, int n, double *tau, double *tcache) {
+    extern __shared__ __align__(16) double smraw[];
+    Smem &S = *reinterpret_cast<Smem *>(smraw);
+    Prob P{Ra, Rb, lda, ldb, 8 * ((n + 7) / 8), n, n, 1};
+    wide_qr(P, n, tau, tcache, S);
+}
+
+// Q^T C / Q C on the leaves (forward: all tiles; C rows = the tile's rows).
+template <bool kFwd>
+__global__ void __launch_bounds__(NT, 1)
+k_wide_apply_leaves(const double *A, int64_t lda, int n, const int64_t *tile_row0, const int *tile_rows,
+                    const double *tcache_tile, double *C, int64_t ldc, int k) {
+    const int t = blockIdx.x;
+    const int npan = (n + 7) / 8;
+    Prob P{const_cast<double *>(A) + tile_row0[t], nullptr, lda, 0, tile_rows[t], 0, tile_rows[t], 0};
+    Prob Cp{C + tile_row0[t], nullptr, ldc, 0, tile_rows[t], 0, tile_rows[t], 0};
+    wide_apply<kFwd>(P, Cp, n, k, tcache_tile + (int64_t)t * npan * 64);
+}
+
+// Q^T / Q of one tree step's nodes on C's head rows (or on xbuf blocks for form Q).
+template <bool kFwd>
+__global__ void __launch_bounds__(NT, 1)
+k_wide_apply_nodes(const double *A, int64_t lda, int n, const int64_t *tile_row0, const int *node_a,
+                   const int *ids, const double *tcache_node, double *C, int64_t ldc, int k, int xbuf_mode) {
+    const int b = ids[blockIdx.x];
+    const int a = node_a[b];
+    const int npan = (n + 7) / 8;
+    const int hA = 8 * npan;
+    Prob P{const_cast<double *>(A) + tile_row0[a], const_cast<double *>(A) + tile_row0[b], lda, lda, hA, n, n, 1};
+    Prob Cp = xbuf_mode ? Prob{C + (int64_t)a * n * n, C + (int64_t)b * n * n, n, n, hA, n, n, 0}
+                        : Prob{C + tile_row0[a], C + tile_row0[b], ldc, ldc, hA, n, n, 0};
+    wide_apply<kFwd>(P, Cp, n, k, tcache_node + (int64_t)b * npan * 64);
+}
+
+// One stacked node's reflectors (Y1 in Rb-storage, ld ldy) applied to [Ca; Cb].
+template <bool kFwd>
+__global__ void __launch_bounds__(NT, 1)
+k_wide_apply_node1(const double *Ra_dummy, const double *Y1, int64_t ldy, int n, const double *tcache, double *Ca,
+                   int64_t ldca, double *Cb, int64_t ldcb, int k) {
+    const int hA = 8 * ((n + 7) / 8);
+    Prob P{const_cast<double *>(Ra_dummy), const_cast<double *>(Y1), 1, ldy, hA, n, n, 1};
+    Prob Cp{Ca, Cb, ldca, ldcb, hA, n, n, 0};
+    wide_apply<kFwd>(P, Cp, n, k, tcache);
+}
+
+// [X; 0] for form Q: rows 0..n-1 of every tile's Q slab <- xbuf[t], the rest 0.
+__global__ void k_wide_formq_init(const int64_t *tile_row0, const int *tile_rows, int n, const double *xbuf,
+                                  double *Q, int64_t ldq) {
+    const int t = blockIdx.x;
+    const int h = tile_rows[t];
+    for (int64_t e = threadIdx.x; e < (int64_t)h * n; e += blockDim.x) {
+        const int r = (int)(e % h), c = (int)(e / h);
+        Q[tile_row0[t] + r + (int64_t)c * ldq] = r < n ? xbuf[(int64_t)t * n * n + r + (int64_t)c * n] : 0.0;
+    }
+}
+
+// ================================================================= launchers
+static size_t wide_smem() { return sizeof(Smem); }
+static cudaError_t wide_attr(const void *fn) {
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wide_smem());
+}
+int wide_max_rows() { return MAXR; }
+
+cudaError_t launch_wide_leaves(double *A, int64_t lda, int n, const int64_t *row0, const int *rows, int L,
+                               double *tau, double *tcache, cudaStream_t st) {
+    cudaError_t e = wide_attr((const void *)k_wide_leaves);
+    if (e != cudaSuccess) return e;
+    k_wide_leaves<<<L, NT, wide_smem(), st>>>(A, lda, n, row0, rows, tau, tcache);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_wide_nodes(double *A, int64_t lda, int n, const int64_t *row0, const int *node_a, const int *ids,
+                              int count, double *tau_node, double *tcache_node, cudaStream_t st) {
+    cudaError_t e = wide_attr((const void *)k_wide_nodes);
+    if (e != cudaSuccess) return e;
+    k_wide_nodes<<<count, NT, wide_smem(), st>>>(A, lda, n, row0, node_a, ids, tau_node, tcache_node);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_wide_node1(double *Ra, int64_t lda, double *Rb, int64_t ldb, int n, double *tau, double *tcache,
+                              cudaStream_t st) {
+    cudaError_t e = wide_attr((const void *)k_wide_node1);
+    if (e != cudaSuccess) return e;
+    k_wide_node1<<<1, NT, wide_smem(), st>>>(Ra, lda, Rb, ldb, n, tau, tcache);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_wide_apply_leaves(const double *A, int64_t lda, int n, const int64_t *row0, const int *rows,
+                                     int L, const double *tcache, double *C, int64_t ldc, int k, int forward,
+                                     cudaStream_t st) {
+    if (forward) k_wide_apply_leaves<true><<<L, NT, 0, st>>>(A, lda, n, row0, rows, tcache, C, ldc, k);
+    else k_wide_apply_leaves<false><<<L, NT, 0, st>>>(A, lda, n, row0, rows, tcache, C, ldc, k);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_wide_apply_nodes(const double *A, int64_t lda, int n, const int64_t *row0, const int *node_a,
+                                    const int *ids, int count, const double *tcache_node, double *C, int64_t ldc,
+                                    int k, int forward, int xbuf_mode, cudaStream_t st) {
+    if (forward)
+        k_wide_apply_nodes<true><<<count, NT, 0, st>>>(A, lda, n, row0, node_a, ids, tcache_node, C, ldc, k, xbuf_mode);
+    else
+        k_wide_apply_nodes<false><<<count, NT, 0, st>>>(A, lda, n, row0, node_a, ids, tcache_node, C, ldc, k, xbuf_mode);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_wide_apply_node1(const double *Y1, int64_t ldy, int n, const double *tcache, double *Ca,
+                                    int64_t ldca, double *Cb, int64_t ldcb, int k, int forward, cudaStream_t st) {
+    if (forward) k_wide_apply_node1<true><<<1, NT, 0, st>>>(Y1, Y1, ldy, n, tcache, Ca, ldca, Cb, ldcb, k);
+    else k_wide_apply_node1<false><<<1, NT, 0, st>>>(Y1, Y1, ldy, n, tcache, Ca, ldca, Cb, ldcb, k);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_wide_formq_init(const int64_t *row0, const int *rows, int L, int n, const double *xbuf, double *Q,
+                                   int64_t ldq, cudaStream_t st) {
+    k_wide_formq_init<<<L, 256, 0, st>>>(row0, rows, n, xbuf, Q, ldq);
+    return cudaGetLastError();
+}
+
+}  // namespace tsqr
+
+namespace tsqr {
+
+// ------------------------------------------------------------ small helpers
+// R (n x n, ldr) <- upper triangle of A's head rows, exact zeros below.
+__global__ void k_extract_r(const double *A, int64_t lda, int n, double *R, int64_t ldr) {
+    for (int e = threadIdx.x + blockIdx.x * blockDim.x; e < n * n; e += blockDim.x * gridDim.x) {
+        const int r = e % n, c = e / n;
+        R[r + (int64_t)c * ldr] = r <= c ? A[r + (int64_t)c * lda] : 0.0;
+    }
+}
+cudaError_t launch_extract_r(const double *A, int64_t lda, int n, double *R, int64_t ldr, cudaStream_t st) {
+    k_extract_r<<<(n * n + 255) / 256, 256, 0, st>>>(A, lda, n, R, ldr);
+    return cudaGetLastError();
+}
+
+// Butterfly round, wide n: tmp (2n x n, ld 2n) <- [R_lower; R_upper] from this
+// rank's head (upper triangle) and the partner's packed R.
+__global__ void k_wide_stack(const double *Ahead, int64_t lda, const double *packed, int is_lower, int n,
+                             double *tmp) {
+    for (int e = threadIdx.x + blockIdx.x * blockDim.x; e < n * n; e += blockDim.x * gridDim.x) {
+        const int r = e % n, c = e / n;
+        const double mine = r <= c ? Ahead[r + (int64_t)c * lda] : 0.0;
+        const double theirs = r <= c ? packed[(int64_t)c * (c + 1) / 2 + r] : 0.0;
+        tmp[r + (int64_t)c * 2 * n] = is_lower ? mine : theirs;
+        tmp[n + r + (int64_t)c * 2 * n] = is_lower ? theirs : mine;
+    }
+}
+// After the node: this rank's head (upper) and R <- the new R; Y1 (ld n) <- the
+// bottom's upper triangle.
+__global__ void k_wide_unstack(const double *tmp, int n, double *Ahead, int64_t lda, double *R, int64_t ldr,
+                               double *Y1) {
+    for (int e = threadIdx.x + blockIdx.x * blockDim.x; e < n * n; e += blockDim.x * gridDim.x) {
+        const int r = e % n, c = e / n;
+        const double rv = r <= c ? tmp[r + (int64_t)c * 2 * n] : 0.0;
+        if (r <= c) Ahead[r + (int64_t)c * lda] = rv;
+        if (R) R[r + (int64_t)c * ldr] = rv;
+        Y1[r + (int64_t)c * n] = r <= c ? tmp[n + r + (int64_t)c * 2 * n] : 0.0;
+    }
+}
+cudaError_t launch_wide_cross_factor(double *A, int64_t lda, int n, const double *packed, int is_lower, double *tmp,
+                                     double *Y1, double *tau, double *tcache, double *R, int64_t ldr,
+                                     cudaStream_t st) {
+    const int blocks = (n * n + 255) / 256;
+    k_wide_stack<<<blocks, 256, 0, st>>>(A, lda, packed, is_lower, n, tmp);
+    cudaError_t e = launch_wide_node1(tmp, 2 * n, tmp + n, 2 * n, n, tau, tcache, st);
+    if (e != cudaSuccess) return e;
+    k_wide_unstack<<<blocks, 256, 0, st>>>(tmp, n, A, lda, R, ldr, Y1);
+    return cudaGetLastError();
+}
+
+// Butterfly round of Q^T C, wide n: tmp (2n x k, ld 2n) <- [top_lower; top_upper],
+// the round's node reflectors applied, then top <- tmp's top half and C's head
+// rows per head_role (1: the R coordinates, 2: the complement).
+__global__ void k_wide_stack_c(const double *top, int64_t ldtop, const double *ptop, int is_lower, int n, int k,
+                               double *tmp) {
+    for (int64_t e = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; e < (int64_t)n * k; e += (int64_t)blockDim.x * gridDim.x) {
+        const int r = (int)(e % n);
+        const int64_t c = e / n;
+        const double mine = top[r + c * ldtop], theirs = ptop[r + c * n];
+        tmp[r + c * 2 * n] = is_lower ? mine : theirs;
+        tmp[n + r + c * 2 * n] = is_lower ? theirs : mine;
+    }
+}
+__global__ void k_wide_unstack_c(const double *tmp, int n, int k, double *top, int64_t ldtop, int role, double *C,
+                                 int64_t ldc) {
+    for (int64_t e = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; e < (int64_t)n * k; e += (int64_t)blockDim.x * gridDim.x) {
+        const int r = (int)(e % n);
+        const int64_t c = e / n;
+        const double ra = tmp[r + c * 2 * n];
+        top[r + c * ldtop] = ra;
+        if (role == 1) C[r + c * ldc] = ra;
+        if (role == 2) C[r + c * ldc] = tmp[n + r + c * 2 * n];
+    }
+}
+cudaError_t launch_wide_cross_apply(const double *Y1, const double *tcache, double *top, int64_t ldtop,
+                                    const double *ptop, int is_lower, int role, double *C, int64_t ldc, int n, int k,
+                                    double *tmp, cudaStream_t st) {
+    const int64_t tot = (int64_t)n * k;
+    const int blocks = (int)((tot + 255) / 256 < 4096 ? (tot + 255) / 256 : 4096);
+    k_wide_stack_c<<<blocks, 256, 0, st>>>(top, ldtop, ptop, is_lower, n, k, tmp);
+    cudaError_t e = launch_wide_apply_node1(Y1, n, n, tcache, tmp, 2 * n, tmp + n, 2 * n, k, 1, st);
+    if (e != cudaSuccess) return e;
+    k_wide_unstack_c<<<blocks, 256, 0, st>>>(tmp, n, k, top, ldtop, role, C, ldc);
+    return cudaGetLastError();
+}
+
+// Root X of this rank for form Q, wide n: top-down over the butterfly rounds,
+// [X_lower; X_upper] = Q_round [X; 0], keep this rank's half.
+__global__ void k_wide_x_init(double *tmp, int n) {
+    for (int e = threadIdx.x + blockIdx.x * blockDim.x; e < 2 * n * n; e += blockDim.x * gridDim.x) {
+        const int r = e % (2 * n), c = e / (2 * n);
+        tmp[e] = (r == c) ? 1.0 : 0.0;
+    }
+}
+__global__ void k_wide_x_pick(double *tmp, int n, int upper, double *X0, int last) {
+    for (int e = threadIdx.x + blockIdx.x * blockDim.x; e < n * n; e += blockDim.x * gridDim.x) {
+        const int r = e % n, c = e / n;
+        const double v = tmp[(upper ? n : 0) + r + (int64_t)c * 2 * n];
+        tmp[r + (int64_t)c * 2 * n] = v;
+        tmp[n + r + (int64_t)c * 2 * n] = 0.0;
+        if (last) X0[r + (int64_t)c * n] = v;
+    }
+}
+cudaError_t launch_wide_cross_root_x(const double *Y1s, const double *tcaches, int64_t tstride, int rounds, int rank,
+                                     int n, double *tmp, double *X0, cudaStream_t st) {
+    const int blocks = (2 * n * n + 255) / 256;
+    k_wide_x_init<<<blocks, 256, 0, st>>>(tmp, n);
+    if (rounds == 0) {
+        k_wide_x_pick<<<blocks, 256, 0, st>>>(tmp, n, 0, X0, 1);
+        return cudaGetLastError();
+    }
+    for (int kr = rounds; kr >= 1; --kr) {
+        cudaError_t e = launch_wide_apply_node1(Y1s + (int64_t)(kr - 1) * n * n, n, n, tcaches + (kr - 1) * tstride,
+                                                tmp, 2 * n, tmp + n, 2 * n, n, 0, st);
+        if (e != cudaSuccess) return e;
+        const int upper = ((rank >> (kr - 1)) & 1) != 0;
+        k_wide_x_pick<<<blocks, 256, 0, st>>>(tmp, n, upper, X0, kr == 1);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace tsqr

@@ -61,6 +61,11 @@ CASES = [
     (40000, 32, 4096, 4096),     # config-5 style: 64-row chunks
     (1000, 50, 1000, 1000),      # one tile, ragged last chunk (1000 = 31*32 + 8)
     (77, 50, 77, 77),            # one tile, three chunks, the last 13 rows
+    # wide n (> 64): one blocked compact-WY QR per tile, masked dense node combines
+    (300, 200, 300, 300),        # a single 300 x 200 tile
+    (5000, 100, 2048, 2048),     # n not a multiple of 8, three tiles (last 904 rows)
+    (20000, 200, 2048, 2048),    # config-3 shape at m = 20,000: ten tiles
+    (3000, 65, 1000, 1000),      # n = 65: nine padded columns
 ]
 
 
@@ -105,7 +110,8 @@ def test_form_q(m, n, b, s):
                                        (1500, 33, 400, 128, 130), (9000, 32, 4096, 96, 128), (777, 5, 100, 30, 1),
                                        (5000, 50, 4096, 192, 64), (4096, 64, 4096, 64, 200),
                                        (20000, 50, 4096, 704, 64), (40000, 32, 4096, 4096, 128),
-                                       (1000, 50, 1000, 1000, 70)])
+                                       (1000, 50, 1000, 1000, 70), (20000, 200, 2048, 2048, 64),
+                                       (5000, 100, 2048, 2048, 13)])
 def test_apply_qt(m, n, b, s, k):
     A0, Ad, R, tree, p, f = _run(m, n, b, s, seed=5)
     Ct = inputs.gaussian(m, k, seed=1)
@@ -189,4 +195,22 @@ def test_tree_reuse_and_repeat_determinism():
     torch.cuda.synchronize()
     assert tree.handle.value == h                     # workspace reused
     assert torch.equal(R1, R2) and torch.equal(A1, A2)  # bitwise deterministic
+    tree.free()
+
+
+def test_config3_full_size():
+    # BASELINE config 3: 100,000 x 200, block rows 2048 (49 tiles), apply Q^T to C (k = 64)
+    m, n, b, k = 100_000, 200, 2048, 64
+    A0, Ad, R, tree, p, f = _run(m, n, b, b, seed=0)
+    Rg = _np(R)
+    assert orc.rel_fro(orc.sign_normalise(Rg), orc.sign_normalise(f.R)) <= TOL_R
+    assert np.linalg.norm(Rg.T @ Rg - A0.T @ A0) / np.linalg.norm(A0) ** 2 <= 1e-14
+    Ct = inputs.gaussian(m, k, seed=1)
+    C0 = _np(Ct).copy()
+    Cd = Ct.cuda()
+    T.apply_qt(tree, Cd)
+    torch.cuda.synchronize()
+    Cg = _np(Cd)
+    Co = orc.tsqr_apply_qt(f, C0)
+    assert orc.rel_fro(Cg, Co) <= TOL_R
     tree.free()

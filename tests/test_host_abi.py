@@ -111,7 +111,9 @@ def test_factor_validation_without_gpu():
     o = T.api.opts(block_rows=64, tile_rows=64)
     fake = ctypes.c_void_p(0x1000)
     assert _factor_status(10, 20, fake, 10, None, 0, o)[0] == 2          # m < n
-    assert _factor_status(100, 65, fake, 100, None, 0, o)[0] == 3        # n > TSQR_MAX_N
+    assert _factor_status(300, 257, fake, 300, None, 0, o)[0] == 3       # n > TSQR_MAX_N
+    # wide n (> 64): one CTA per tile, at most 2304 rows
+    assert _factor_status(5000, 65, fake, 5000, None, 0, T.api.opts(block_rows=5000, tile_rows=2400))[0] == 3
     assert _factor_status(100, 10, None, 100, None, 0, o)[0] == 1        # null A
     assert _factor_status(100, 10, fake, 99, None, 0, o)[0] == 1         # lda < m
     assert _factor_status(100, 10, fake, 100, fake, 9, o)[0] == 1        # ldr < n

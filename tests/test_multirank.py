@@ -168,7 +168,8 @@ def test_butterfly_gloo(world, m, n, b, s, k):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("G,m,n,b,s,k", [(2, 20000, 50, 4096, 96, 64), (4, 40000, 32, 4096, 192, 128),
-                                         (8, 50000, 16, 2048, 128, 16), (8, 8 * 4096 + 100, 64, 4096, 96, 70), (2, 2 * 4096 + 30, 32, 4096, 64, 32)])
+                                         (8, 50000, 16, 2048, 128, 16), (8, 8 * 4096 + 100, 64, 4096, 96, 70), (2, 2 * 4096 + 30, 32, 4096, 64, 32),
+                                         (2, 12000, 200, 2048, 2048, 64), (4, 16000, 100, 2048, 2048, 20)])
 def test_butterfly_virtual_ranks_cuda(G, m, n, b, s, k):
     from paper_0808_2664_b200 import api
     slabs, cs, rows = [], [], []
