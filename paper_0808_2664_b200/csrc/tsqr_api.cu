@@ -32,10 +32,12 @@ struct tsqr_tree_s {
     int cross_rounds = 0, cross_done = 0;
     double *d_xbuf = nullptr;
     int *d_step_ids = nullptr;
+    int *d_pipe_nodes = nullptr, *d_prod_l = nullptr, *d_prod_r = nullptr, *d_pipe_flags = nullptr;
+    int pipe_count = 0, pipe_root = -1;
     // chunk-chain leaf stage
     int64_t *d_tile_chunk0 = nullptr;
-    int *d_cta_tile0 = nullptr;
-    int chain_grid = 0;
+    int *d_cta_tile0 = nullptr, *d_apply_cta_tile0 = nullptr;
+    int chain_grid = 0, apply_grid = 0;
     double *d_tau_chunk = nullptr;
     double *d_tcache = nullptr;       // [chunks][NCB][8][8] panel T factors (compact WY)
     int64_t nchunks = 0;
@@ -67,7 +69,8 @@ static tsqr_status_t debug_sync(const tsqr_tree_s *t, cudaStream_t st, const cha
 static void free_tree_memory(tsqr_tree_s *t) {
     void *ptrs[] = {t->d_row0, t->d_rows, t->d_tparent, t->d_node_a, t->d_nparent, t->d_tau_tile,
                     t->d_tau_node, t->d_counters, t->d_cross_y1, t->d_cross_tau, t->d_xbuf,
-                    t->d_step_ids, t->d_tile_chunk0, t->d_cta_tile0, t->d_tau_chunk, t->d_tcache,
+                    t->d_step_ids, t->d_pipe_nodes, t->d_prod_l, t->d_prod_r, t->d_pipe_flags,
+                    t->d_tile_chunk0, t->d_cta_tile0, t->d_apply_cta_tile0, t->d_tau_chunk, t->d_tcache,
                     t->d_tcache_node, t->d_cross_tcache, t->d_wtmp};
     for (void *p : ptrs)
         if (p) cudaFree(p);
@@ -227,6 +230,20 @@ static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t 
     alloc((void **)&t->d_cross_y1, sizeof(double) * (t->cross_rounds + 1) * n * n);
     alloc((void **)&t->d_cross_tau, sizeof(double) * (t->cross_rounds + 1) * n);
     alloc((void **)&t->d_step_ids, sizeof(int) * (ids.size() + 1));
+    // pipelined tree (n <= 64): nodes bottom-up; each child's producing node
+    std::vector<int> pipe(ids.rbegin(), ids.rend()), prod_l(L, -1), prod_r(L, -1), last(L, -1);
+    for (int b : pipe) {
+        const int a = p.node_a[b];
+        prod_l[b] = last[a];
+        prod_r[b] = last[b];
+        last[a] = b;
+    }
+    t->pipe_count = (int)pipe.size();
+    t->pipe_root = L > 1 ? last[0] : -1;
+    alloc((void **)&t->d_pipe_nodes, sizeof(int) * L);
+    alloc((void **)&t->d_prod_l, sizeof(int) * L);
+    alloc((void **)&t->d_prod_r, sizeof(int) * L);
+    alloc((void **)&t->d_pipe_flags, sizeof(int) * L * 8);
     const int64_t nchunks = p.tile_chunk0[L];
     t->wide = n > 64;
     t->npan = (int)((n + 7) / 8);
@@ -240,6 +257,16 @@ static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t 
         cta_tile0[1] = L;
     }
     t->chain_grid = grid;
+    int agrid = 1;                         // the apply / form-Q kernels' own split (higher occupancy)
+    std::vector<int> apply_tile0(2, 0);
+    if (!t->wide) {
+        agrid = std::min(L, cs_apply_grid((int)n));
+        chain_partition(p.tile_rows, p.c, agrid, apply_tile0);
+    } else {
+        apply_tile0[1] = L;
+    }
+    t->apply_grid = agrid;
+    alloc((void **)&t->d_apply_cta_tile0, sizeof(int) * (agrid + 1));
     alloc((void **)&t->d_tile_chunk0, sizeof(int64_t) * (L + 1));
     alloc((void **)&t->d_cta_tile0, sizeof(int) * (grid + 1));
     alloc((void **)&t->d_tau_chunk, sizeof(double) * nchunks * n);
@@ -265,10 +292,16 @@ static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t 
     if (e == cudaSuccess) e = cudaMemcpy(t->d_nparent, p.node_parent.data(), sizeof(int) * L, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && !ids.empty())
         e = cudaMemcpy(t->d_step_ids, ids.data(), sizeof(int) * ids.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && !pipe.empty())
+        e = cudaMemcpy(t->d_pipe_nodes, pipe.data(), sizeof(int) * pipe.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(t->d_prod_l, prod_l.data(), sizeof(int) * L, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(t->d_prod_r, prod_r.data(), sizeof(int) * L, cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
         e = cudaMemcpy(t->d_tile_chunk0, p.tile_chunk0.data(), sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
         e = cudaMemcpy(t->d_cta_tile0, cta_tile0.data(), sizeof(int) * (grid + 1), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess)
+        e = cudaMemcpy(t->d_apply_cta_tile0, apply_tile0.data(), sizeof(int) * (agrid + 1), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemset(t->d_counters, 0, sizeof(int) * L);
     if (e == cudaSuccess) e = cudaMemset(t->d_tau_node, 0, sizeof(double) * L * n);
     if (e != cudaSuccess) {
@@ -339,7 +372,13 @@ tsqr_status_t tsqr_factor(int64_t m_local, int64_t n, double *A, int64_t lda, do
         return debug_sync(t, t->stream, "tsqr_factor");
     }
     CUDA_TRY(launch_chain_factor(ca, t->stream), "tsqr_factor leaves");
-    CUDA_TRY(launch_tree(f, t->stream), "tsqr_factor tree");
+    if (t->pipe_count == 0) {
+        if (R) CUDA_TRY(launch_extract_r(A, lda, (int)n, R, ldr, t->stream), "tsqr_factor R");
+    } else {
+        CUDA_TRY(launch_tree_pipe(A, lda, (int)n, t->d_row0, t->d_node_a, t->d_pipe_nodes, t->pipe_count, t->d_prod_l,
+                                  t->d_prod_r, t->d_pipe_flags, t->d_tau_node, t->pipe_root, R, ldr, t->stream),
+                 "tsqr_factor tree");
+    }
     return debug_sync(t, t->stream, "tsqr_factor");
 }
 
@@ -398,7 +437,7 @@ tsqr_status_t tsqr_apply_qt(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, do
     ChainApplyArgs ca;
     ca.A = t->A; ca.lda = t->lda; ca.n = (int)t->plan.n; ca.chunk_rows = t->plan.c;
     ca.tile_row0 = t->d_row0; ca.tile_rows = t->d_rows; ca.tile_chunk0 = t->d_tile_chunk0;
-    ca.cta_tile0 = t->d_cta_tile0; ca.grid = t->chain_grid; ca.tcache = t->d_tcache;
+    ca.cta_tile0 = t->d_apply_cta_tile0; ca.grid = t->apply_grid; ca.tcache = t->d_tcache;
     ca.C = C; ca.ldc = ldc; ca.k = (int)k; ca.forward = 1; ca.xbuf = nullptr;
     if (t->wide) {
         const int n = (int)t->plan.n;
@@ -502,7 +541,7 @@ tsqr_status_t tsqr_form_q(tsqr_tree_t t, double *Q, int64_t ldq, void *stream) {
     ChainApplyArgs ca;
     ca.A = t->A; ca.lda = t->lda; ca.n = n; ca.chunk_rows = t->plan.c;
     ca.tile_row0 = t->d_row0; ca.tile_rows = t->d_rows; ca.tile_chunk0 = t->d_tile_chunk0;
-    ca.cta_tile0 = t->d_cta_tile0; ca.grid = t->chain_grid; ca.tcache = t->d_tcache;
+    ca.cta_tile0 = t->d_apply_cta_tile0; ca.grid = t->apply_grid; ca.tcache = t->d_tcache;
     ca.C = Q; ca.ldc = ldq; ca.k = n; ca.forward = 0; ca.xbuf = t->d_xbuf;
     CUDA_TRY(launch_cs_apply(ca, st), "tsqr_form_q leaves");
     t->stream = st;

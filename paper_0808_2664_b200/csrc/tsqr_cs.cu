@@ -154,17 +154,17 @@ __device__ __forceinline__ void cp8(double *sm, const double *g, bool ok) {
 template <class C>
 __device__ __forceinline__ void stage_chunk(double *slot, const double *Ak, int64_t lda, int hk, int n,
                                             const double *tch, int r0) {
-    for (int i = threadIdx.x; i < C::CH * C::NP; i += 256) {
+    for (int i = threadIdx.x; i < C::CH * C::NP; i += blockDim.x) {
         const int col = i / C::CH, row = i % C::CH;
         const bool ok = row < hk && col < n && row > col - r0;
         cp8(slot + row * C::NP + col, Ak + row + (int64_t)(ok ? col : 0) * lda, ok);
     }
-    for (int i = threadIdx.x; i < C::NCB * 64; i += 256) cp8(slot + C::CH * C::NP + i, tch + i, true);
+    for (int i = threadIdx.x; i < C::NCB * 64; i += blockDim.x) cp8(slot + C::CH * C::NP + i, tch + i, true);
     asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 template <class C>
 __device__ __forceinline__ void fix_dense(double *slot, int n, int r0) {
-    for (int c = threadIdx.x; c < C::NP; c += 256)
+    for (int c = threadIdx.x; c < C::NP; c += blockDim.x)
         if (c < n && c >= r0 && c < r0 + C::CH) slot[(c - r0) * C::NP + c] = 1.0;
 }
 
@@ -232,8 +232,22 @@ __device__ __forceinline__ void cs_apply_panel(double (&cc)[C::KM][2], double (&
     }
 }
 
+// this lane's slab of C (column col, rows 8kk+2q+{0,1}) for chunk c of a tile
+template <class C>
+__device__ __forceinline__ void load_cslab(double (&v)[C::KM][2], const double *Cm, int64_t ldc, int k, int64_t row0,
+                                           int h, int c, int col, int q) {
+    const int r0 = c * C::CH, hk = min(C::CH, h - r0);
+    const double *Ck = Cm + row0 + r0 + (int64_t)(col < k ? col : 0) * ldc;
+#pragma unroll
+    for (int kk = 0; kk < C::KM; ++kk) {
+        const int r = 8 * kk + 2 * q;
+        v[kk][0] = (col < k && r < hk) ? Ck[r] : 0.0;
+        v[kk][1] = (col < k && r + 1 < hk) ? Ck[r + 1] : 0.0;
+    }
+}
+
 template <class C, bool kFwd>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, 2)
 k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const int *tile_rows,
            const int64_t *tile_chunk0, const int *cta_tile0, const double *tcache, double *Cm, int64_t ldc, int k,
            const double *xbuf) {
@@ -241,7 +255,8 @@ k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const 
     extern __shared__ __align__(16) double sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
     const int tb = cta_tile0[blockIdx.x], te = cta_tile0[blockIdx.x + 1];
-    const int npass = (k + 63) / 64;
+    const int pw = blockDim.x >> 2;                               // columns per pass (8 per warp)
+    const int npass = (k + pw - 1) / pw;
     const int np = (n + 7) / 8;
     // the CTA's work list: (tile, pass) items, each a chain over the tile's chunks
     int cur = 0;                                                  // staging parity
@@ -250,12 +265,14 @@ k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const 
         const int nch = (tile_rows[t] + C::CH - 1) / C::CH;
         return kFwd ? cc_ : nch - 1 - cc_;
     };
+    double ccv[C::KM][2];
+    if (kFwd && tb < te) load_cslab<C>(ccv, Cm, ldc, k, tile_row0[tb], tile_rows[tb], chunk_of(tb, 0), 8 * warp + l4, q);
     for (int t = tb; t < te; ++t) {
         const int h = tile_rows[t];
         const int nch = (h + C::CH - 1) / C::CH;
         const int64_t row0 = tile_row0[t];
         for (int pass = 0; pass < npass; ++pass) {
-            const int col = 64 * pass + 8 * warp + l4;            // this lane's column of C
+            const int col = pw * pass + 8 * warp + l4;            // this lane's column of C
             const bool okc = col < k;
             double cr[C::NCB][2];
 #pragma unroll
@@ -275,18 +292,25 @@ k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                 if (!staged)
                     stage_chunk<C>(sm + cur * AC::YS, A + row0 + r0, lda, hk, n,
                                    tcache + (tile_chunk0[t] + c) * (C::NCB * 64), r0);
-                // prefetch the next chunk of the work list into the other slot
+                // prefetch the next chunk of the work list: Y/T into the other
+                // slot, C into registers
                 int tn = t, pn = pass, cn = cc_ + 1;
                 if (cn == nch) { cn = 0; if (++pn == npass) { pn = 0; ++tn; } }
+                double ccn[C::KM][2];
                 if (tn < te) {
                     const int cnn = chunk_of(tn, cn), hn = tile_rows[tn], r0n = cnn * C::CH;
                     stage_chunk<C>(sm + (cur ^ 1) * AC::YS, A + tile_row0[tn] + r0n, lda, min(C::CH, hn - r0n), n,
                                    tcache + (tile_chunk0[tn] + cnn) * (C::NCB * 64), r0n);
+                    if (kFwd) load_cslab<C>(ccn, Cm, ldc, k, tile_row0[tn], hn, cnn, pw * pn + 8 * warp + l4, q);
                     asm volatile("cp.async.wait_group 1;\n" ::: "memory");
                     staged = true;
                 } else {
                     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
                     staged = false;
+                }
+                if (!kFwd) {
+#pragma unroll
+                    for (int kk = 0; kk < C::KM; ++kk) ccv[kk][0] = ccv[kk][1] = 0.0;
                 }
                 __syncthreads();
                 double *slot = sm + cur * AC::YS;
@@ -295,13 +319,6 @@ k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                     __syncthreads();
                 }
                 double *Ck = Cm + row0 + r0;
-                double ccv[C::KM][2];
-#pragma unroll
-                for (int kk = 0; kk < C::KM; ++kk) {
-                    const int r = 8 * kk + 2 * q;
-                    ccv[kk][0] = (kFwd && okc && r < hk) ? Ck[r + (int64_t)col * ldc] : 0.0;
-                    ccv[kk][1] = (kFwd && okc && r + 1 < hk) ? Ck[r + 1 + (int64_t)col * ldc] : 0.0;
-                }
 #pragma unroll 1
                 for (int pp = 0; pp < np; ++pp)
                     cs_apply_panel<C, kFwd>(ccv, cr, kFwd ? pp : np - 1 - pp, r0, slot);
@@ -312,6 +329,13 @@ k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                         const int r = 8 * kk + 2 * q + e;
                         if (okc && r < hk && (!kFwd || r0 + r >= n)) Ck[r + (int64_t)col * ldc] = ccv[kk][e];
                     }
+                if (kFwd && tn < te) {
+#pragma unroll
+                    for (int kk = 0; kk < C::KM; ++kk) {
+                        ccv[kk][0] = ccn[kk][0];
+                        ccv[kk][1] = ccn[kk][1];
+                    }
+                }
                 __syncthreads();                                  // the slot may be refilled
                 cur ^= 1;
             }
@@ -402,6 +426,22 @@ static cudaError_t chain_cfg_dispatch(int n, F &&fn) {
     }
 }
 
+int cs_apply_grid(int n) {
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = chain_cfg_dispatch(n, [&](auto c) {
+        using C = decltype(c);
+        using AC = ApplyCs<C>;
+        cudaError_t r = cudaFuncSetAttribute((const void *)k_cs_apply<C, true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AC::BYTES);
+        if (r != cudaSuccess) return r;
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cs_apply<C, true>, AC::NT, AC::BYTES);
+    });
+    if (e != cudaSuccess || occ < 1) occ = 1;
+    return sms * occ;
+}
+
 cudaError_t launch_cs_apply(const ChainApplyArgs &f, cudaStream_t st) {
     return chain_cfg_dispatch(f.n, [&](auto c) {
         using C = decltype(c);
@@ -410,7 +450,8 @@ cudaError_t launch_cs_apply(const ChainApplyArgs &f, cudaStream_t st) {
         cudaError_t e = cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)AC::BYTES);
         if (e != cudaSuccess) return e;
-        kern<<<f.grid, AC::NT, AC::BYTES, st>>>(f.A, f.lda, f.n, f.tile_row0, f.tile_rows, f.tile_chunk0, f.cta_tile0,
+        const int nw = f.k >= 64 ? 8 : (f.k + 7) / 8;           // one warp per 8-column slab
+        kern<<<f.grid, 32 * (nw < 1 ? 1 : nw), AC::BYTES, st>>>(f.A, f.lda, f.n, f.tile_row0, f.tile_rows, f.tile_chunk0, f.cta_tile0,
                                                 f.tcache, f.C, f.ldc, f.k, f.xbuf);
         return cudaGetLastError();
     });

@@ -65,6 +65,7 @@ struct ChainApplyArgs {
 int chain_chunk_rows(int n);
 int chain_ncb(int n);
 int chain_grid(int n);
+int cs_apply_grid(int n);   // SMs x resident apply CTAs
 cudaError_t launch_chain_factor(const ChainArgs &f, cudaStream_t st);
 // Leaf stage of Q^T C / form Q on the chain representation (tsqr_cs.cu).
 cudaError_t launch_cs_apply(const ChainApplyArgs &f, cudaStream_t st);
@@ -101,6 +102,11 @@ cudaError_t launch_cs_factor(const ChainArgs &f, cudaStream_t st);
 void chain_partition(const std::vector<int64_t> &tile_rows, int chunk_rows, int grid, std::vector<int> &cta_tile0);
 // Tree stage only (ticketed climb from every tile), after launch_chain_factor.
 cudaError_t launch_tree(const FactorArgs &f, cudaStream_t st);
+// Pipelined node combines for n <= 64 (tsqr_tree.cu): nodes (ids, bottom-up),
+// prod_l/prod_r = producing node of each child (-1: leaf), flags L x NCB ints.
+cudaError_t launch_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *node_a,
+                             const int *nodes, int count, const int *prod_l, const int *prod_r, int *flags,
+                             double *tau_node, int root, double *R, int64_t ldr, cudaStream_t st);
 cudaError_t launch_apply(const ApplyArgs &f, cudaStream_t st);
 cudaError_t launch_apply_nodes(const ApplyArgs &f, cudaStream_t st);
 cudaError_t launch_formq_nodes(int NP, const double *A, int64_t lda, int n, const DevPlan &plan,

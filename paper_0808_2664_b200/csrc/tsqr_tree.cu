@@ -1,0 +1,246 @@
+// Pipelined reduction tree for n <= 64 (a4, a6).  Product code.
+//
+// Every tree node (Alg. QR:qnxn with q = 2 on [R_a; R_b], eq. fact_2rs;
+// Alg. TSQR:par P:1681-1692) is one warp.  R_b's upper block-triangle lives in
+// the warp's registers as DMMA fragments (blocks k <= cb of 8x8, the zero
+// blocks never exist); the pivot rows 8P..8P+7 of R_a of panel P sit in a small
+// per-warp smem buffer.  Panel P of a node needs only row block P of each
+// child's R (R's rows 8P..8P+7 are final once the child has finished its panel
+// P), so a node starts panel P as soon as both children have published it:
+// the levels of the tree overlap, and the critical path is about
+// (depth + panels) panel latencies instead of depth x node latencies.
+// Outputs per panel: the node's R rows 8P..8P+7 -> the left subtree's head
+// (tile a), Y1 columns 8P..8P+7 -> the right subtree's head (tile b), both
+// upper triangles only (the leaf reflectors below stay); tau -> tau_node.
+// Nodes are numbered bottom-up, so a node depends only on lower-numbered
+// nodes, which were dispatched earlier (blocks are dispatched in order): the
+// spin-waits cannot deadlock.
+#include "tsqr_kernels.h"
+#include "chunk.cuh"
+
+namespace tsqr {
+namespace tree {
+
+using chunk::build_t;
+using chunk::House;
+using chunk::house_bf;
+using wy::dmma;
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int NW = 8;
+
+template <int NCB_>
+struct TCfg {
+    static constexpr int NCB = NCB_, NP = 8 * NCB;
+    static constexpr int LDA = NP + 2;                      // R_a row block (8 x NP, row-major)
+    static constexpr int RA = 0, YS = RA + 8 * LDA, GS = YS + NP * 8, TS = GS + 64, T8 = TS + 64, XS = T8 + 8;
+    static constexpr int WS = XS + 2 * NP;                  // per warp (doubles)
+    static constexpr size_t BYTES = (size_t)NW * WS * sizeof(double);
+};
+
+template <class C>
+struct NodeRegs {
+    double a[C::NCB][C::NCB][2];     // only k <= cb is ever touched
+};
+
+__device__ __forceinline__ void wait_flag(const int *f) {
+    if ((threadIdx.x & 31) == 0) {
+        while (*reinterpret_cast<const volatile int *>(f) == 0) __nanosleep(64);
+    }
+    __syncwarp();
+    __threadfence();
+}
+
+template <class C, int P>
+__device__ __forceinline__ void node_panel(NodeRegs<C> &rg, double *Ahead_a, double *Ahead_b, int64_t lda, int n,
+                                           double *ws, double *tau_out, const int *fl, const int *fr, int *fme,
+                                           double *R, int64_t ldr) {
+    const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+    double *Ra = ws + C::RA, *Ys = ws + C::YS, *Gs = ws + C::GS, *Ts = ws + C::TS, *t8 = ws + C::T8, *xs = ws + C::XS;
+    if (fl) wait_flag(fl + P);
+    if (fr) wait_flag(fr + P);
+    // R_a rows 8P..8P+7 (upper part) -> smem; R_b row block P (upper part) -> registers
+    double ra[2 * C::NCB];              // all loads in flight before the first use
+#pragma unroll
+    for (int u = 0; u < 2 * C::NCB; ++u) {
+        const int e = lane + 32 * u, r = e & 7, c = e >> 3, i = 8 * P + r;
+        ra[u] = (c >= i && c < n) ? __ldcg(Ahead_a + i + (int64_t)c * lda) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 2 * C::NCB; ++u) {
+        const int e = lane + 32 * u;
+        Ra[(e & 7) * C::LDA + (e >> 3)] = ra[u];
+    }
+#pragma unroll
+    for (int cb = P; cb < C::NCB; ++cb)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int i = 8 * P + 2 * q + e, c = 8 * cb + l4;
+            rg.a[P][cb][e] = (c >= i && c < n) ? __ldcg(Ahead_b + i + (int64_t)c * lda) : 0.0;
+        }
+    // pivot column broadcast row (x = column 8P of R_b rows 0..8P+7)
+    if (l4 == 0) {
+#pragma unroll
+        for (int k = 0; k <= P; ++k)
+            *reinterpret_cast<double2 *>(xs + 8 * k + 2 * q) = make_double2(rg.a[k][P][0], rg.a[k][P][1]);
+    }
+    __syncwarp();
+#pragma unroll 1
+    for (int jj = 0; jj < 8; ++jj) {
+        const double *xr = xs + (jj & 1) * C::NP;
+        double d0 = 0.0, d1 = 0.0, s0 = 0.0, s1 = 0.0;
+        double x[P + 1][2];
+#pragma unroll
+        for (int k = 0; k <= P; ++k) {
+            const double2 v = *reinterpret_cast<const double2 *>(xr + 8 * k + 2 * q);
+            x[k][0] = v.x;
+            x[k][1] = v.y;
+            d0 = fma(x[k][0], rg.a[k][P][0], d0);
+            d1 = fma(x[k][1], rg.a[k][P][1], d1);
+            s0 = fma(x[k][0], x[k][0], s0);
+            s1 = fma(x[k][1], x[k][1], s1);
+        }
+        double d = d0 + d1, s2 = s0 + s1;
+        d += __shfl_xor_sync(FULL, d, 1);
+        s2 += __shfl_xor_sync(FULL, s2, 1);
+        d += __shfl_xor_sync(FULL, d, 2);
+        s2 += __shfl_xor_sync(FULL, s2, 2);
+        const double alpha = Ra[jj * C::LDA + 8 * P + jj];
+        const double rj = Ra[jj * C::LDA + 8 * P + l4];
+        const House h = house_bf(alpha, s2);
+        const double w = fma(h.scale, d, rj);
+        const double u = (l4 > jj) ? h.tau * h.scale * w : (l4 == jj ? 1.0 : 0.0);
+        const double g = (l4 == jj) ? h.scale : 0.0;
+        const double rnew = (l4 == jj) ? h.beta : fma(-h.tau, w, rj);
+#pragma unroll
+        for (int k = 0; k <= P; ++k) {
+            rg.a[k][P][0] = fma(g, x[k][0], fma(-u, x[k][0], rg.a[k][P][0]));
+            rg.a[k][P][1] = fma(g, x[k][1], fma(-u, x[k][1], rg.a[k][P][1]));
+        }
+        if (l4 == jj + 1) {
+            double *xw = xs + ((jj + 1) & 1) * C::NP;
+#pragma unroll
+            for (int k = 0; k <= P; ++k)
+                *reinterpret_cast<double2 *>(xw + 8 * k + 2 * q) = make_double2(rg.a[k][P][0], rg.a[k][P][1]);
+        }
+        __syncwarp();
+        if (q == 0 && l4 >= jj) Ra[jj * C::LDA + 8 * P + l4] = rnew;
+        if (q == 0 && l4 < jj) Gs[l4 * 8 + jj] = h.scale * d;
+        if (lane == 0) t8[jj] = h.tau;
+        __syncwarp();
+    }
+    if (lane < 8 && 8 * P + lane < n) tau_out[8 * P + lane] = t8[lane];
+    // Y of the panel (rows 0..8P+7 of R_b, i.e. Y1's columns 8P..8P+7) for the update
+#pragma unroll
+    for (int k = 0; k <= P; ++k) {
+        Ys[(8 * k + 2 * q) * 8 + l4] = rg.a[k][P][0];
+        Ys[(8 * k + 2 * q + 1) * 8 + l4] = rg.a[k][P][1];
+    }
+    __syncwarp();
+    build_t(Gs, t8, Ts);
+    if constexpr (P + 1 < C::NCB) {
+        const double tb0 = Ts[(2 * q) * 8 + l4], tb1 = Ts[(2 * q + 1) * 8 + l4];
+#pragma unroll
+        for (int cb = P + 1; cb < C::NCB; ++cb) {
+            double w0 = 0.0, w1 = 0.0;
+#pragma unroll
+            for (int k = 0; k <= P; ++k) {
+                dmma(w0, w1, rg.a[k][cb][0], rg.a[k][P][0]);
+                dmma(w0, w1, rg.a[k][cb][1], rg.a[k][P][1]);
+            }
+            double *rp = Ra + (2 * q) * C::LDA + 8 * cb + l4;
+            w0 += rp[0];
+            w1 += rp[C::LDA];
+            double p0 = 0.0, p1 = 0.0;
+            dmma(p0, p1, w0, tb0);
+            dmma(p0, p1, w1, tb1);
+            rp[0] -= p0;
+            rp[C::LDA] -= p1;
+#pragma unroll
+            for (int k = 0; k <= P; ++k) {
+                const double2 yt = *reinterpret_cast<const double2 *>(Ys + (8 * k + l4) * 8 + 2 * q);
+                dmma(rg.a[k][cb][0], rg.a[k][cb][1], -p0, yt.x);
+                dmma(rg.a[k][cb][0], rg.a[k][cb][1], -p1, yt.y);
+            }
+        }
+    }
+    __syncwarp();
+    // publish: R rows 8P..8P+7 -> tile a's head, Y1 columns 8P..8P+7 -> tile b's head
+#pragma unroll
+    for (int u = 0; u < 2 * C::NCB; ++u) {
+        const int e = lane + 32 * u, r = e & 7, c = e >> 3, i = 8 * P + r;
+        if (c >= i && c < n) Ahead_a[i + (int64_t)c * lda] = Ra[r * C::LDA + c];
+        if (R && i < n && c < n) R[i + (int64_t)c * ldr] = c >= i ? Ra[r * C::LDA + c] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k <= P; ++k)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const int i = 8 * k + 2 * q + e, c = 8 * P + l4;
+            if (i <= c && c < n) Ahead_b[i + (int64_t)c * lda] = rg.a[k][P][e];
+        }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) *reinterpret_cast<volatile int *>(fme + P) = 1;
+    if constexpr (P + 1 < C::NCB) node_panel<C, P + 1>(rg, Ahead_a, Ahead_b, lda, n, ws, tau_out, fl, fr, fme, R, ldr);
+}
+
+}  // namespace tree
+
+using namespace tree;
+
+// nodes[i]: node id (b) in bottom-up order; prod_l / prod_r: the node ids that
+// produce the left / right child's R (-1: a leaf tile, ready); flags[b][NCB].
+template <class C>
+__global__ void __launch_bounds__(NW * 32)
+k_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *node_a, const int *nodes, int count,
+            const int *prod_l, const int *prod_r, int *flags, double *tau_node, int root, double *R, int64_t ldr) {
+    extern __shared__ __align__(16) double sm[];
+    const int warp = threadIdx.x >> 5;
+    const int i = blockIdx.x * NW + warp;
+    if (i >= count) return;
+    const int b = nodes[i], a = node_a[b];
+    double *ws = sm + warp * C::WS;
+    NodeRegs<C> rg;
+#pragma unroll
+    for (int k = 0; k < C::NCB; ++k)
+#pragma unroll
+        for (int cb = 0; cb < C::NCB; ++cb) rg.a[k][cb][0] = rg.a[k][cb][1] = 0.0;
+    const int pl = prod_l[b], pr = prod_r[b];
+    node_panel<C, 0>(rg, A + tile_row0[a], A + tile_row0[b], lda, n, ws, tau_node + (int64_t)b * n,
+                     pl >= 0 ? flags + pl * C::NCB : nullptr, pr >= 0 ? flags + pr * C::NCB : nullptr,
+                     flags + b * C::NCB, b == root ? R : nullptr, ldr);
+}
+
+template <class F>
+static cudaError_t tree_dispatch(int n, F &&fn) {
+    switch ((n + 7) / 8) {
+        case 1: return fn(TCfg<1>());
+        case 2: return fn(TCfg<2>());
+        case 3: return fn(TCfg<3>());
+        case 4: return fn(TCfg<4>());
+        case 5: return fn(TCfg<5>());
+        case 6: return fn(TCfg<6>());
+        case 7: return fn(TCfg<7>());
+        default: return fn(TCfg<8>());
+    }
+}
+
+cudaError_t launch_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *node_a,
+                             const int *nodes, int count, const int *prod_l, const int *prod_r, int *flags,
+                             double *tau_node, int root, double *R, int64_t ldr, cudaStream_t st) {
+    if (count == 0) return cudaSuccess;
+    return tree_dispatch(n, [&](auto c) {
+        using C = decltype(c);
+        cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)(count + 1) * C::NCB, st);  // ids <= count
+        if (e != cudaSuccess) return e;
+        e = cudaFuncSetAttribute((const void *)k_tree_pipe<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)C::BYTES);
+        if (e != cudaSuccess) return e;
+        k_tree_pipe<C><<<(count + NW - 1) / NW, NW * 32, C::BYTES, st>>>(A, lda, n, tile_row0, node_a, nodes, count,
+                                                                         prod_l, prod_r, flags, tau_node, root, R,
+                                                                         ldr);
+        return cudaGetLastError();
+    });
+}
+
+}  // namespace tsqr
