@@ -90,6 +90,9 @@ struct Sync {
 // the spin (wait).  No MEMBAR: a fence.cta would also wait for the warp's
 // outstanding global stores.
 __device__ __forceinline__ void sync_wait(const int *c, int v) {
+#ifdef TSQR_NOWAIT                         // timing experiment only (results invalid)
+    return;
+#endif
     while (*reinterpret_cast<const volatile int *>(c) < v) {
     }
     asm volatile("" ::: "memory");
@@ -216,7 +219,9 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
         d += __shfl_xor_sync(FULL, d, 2);
         s2 += __shfl_xor_sync(FULL, s2, 2);
         PROBE(3);
+#ifndef TSQR_NOWAIT_ROW                    // timing experiment only (results invalid)
         sync_wait(sy.row + j, sy.s);                                 // R row j released by the previous chunk
+#endif
         PROBE(4);
         const double alpha = Rb[j * C::LDR + j];
         const double rj = Rb[j * C::LDR + 8 * P + l4];                // R(j, 8P + l4)

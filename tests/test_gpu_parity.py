@@ -60,7 +60,12 @@ CASES = [
     (50000, 64, 4096, 4096),     # config-4 style: one 4096-row tile per block (128 chunks)
     (40000, 32, 4096, 4096),     # config-5 style: 64-row chunks
     (1000, 50, 1000, 1000),      # one tile, ragged last chunk (1000 = 31*32 + 8)
-    (77, 50, 77, 77),            # one tile, three chunks, the last 13 rows
+    (77, 50, 77, 77),            # one tile: chunks of 40 rows, the last 37
+    (2000, 40, 1000, 500),       # 48-row chunks (33 <= n <= 48), ragged 20-row last chunk
+    (2400, 48, 2400, 480),       # n = 48: ten 48-row chunks per tile
+    (3003, 56, 3003, 1001),      # n = 56: 40-row chunks, 1001 = 25*40 + 1
+    (41, 41, 41, 41),            # m = n = 41: one chunk shorter than its 48 rows
+    (4000, 49, 4000, 1000),      # n = 49: 40-row chunks, pivots in chunk 1 (rows 40..48)
     # wide n (> 64): one blocked compact-WY QR per tile, masked dense node combines
     (300, 200, 300, 300),        # a single 300 x 200 tile
     (5000, 100, 2048, 2048),     # n not a multiple of 8, three tiles (last 904 rows)

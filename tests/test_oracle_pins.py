@@ -399,7 +399,8 @@ def test_chain_c0_is_hqr(rows, n):
 
 
 @pytest.mark.parametrize("rows,n,c", [(200, 16, 32), (200, 50, 32), (97, 40, 32), (130, 64, 32),
-                                      (300, 24, 64), (64, 64, 32), (77, 50, 32), (50, 16, 8)])
+                                      (300, 24, 64), (64, 64, 32), (77, 50, 32), (50, 16, 8),
+                                      (203, 50, 40), (170, 44, 48)])
 def test_chain_equals_stacked_hqr(rows, n, c):
     # Sequential TSQR: every chunk step is qr([R; A_k]) with R the
     # upper trapezoid so far.  Dense hqr of the explicitly stacked matrix
@@ -423,7 +424,7 @@ def test_chain_equals_stacked_hqr(rows, n, c):
     assert np.array_equal(np.triu(F[:n]), Rk)
 
 
-@pytest.mark.parametrize("rows,n,c", [(300, 20, 32), (256, 64, 32), (1000, 50, 32)])
+@pytest.mark.parametrize("rows,n,c", [(300, 20, 32), (256, 64, 32), (1000, 50, 32), (1000, 50, 40), (700, 40, 48)])
 def test_chain_r_vs_lapack_and_q(rows, n, c):
     A = _rng(rows - n + c).standard_normal((rows, n))
     F, tau = orc.chain_qr(A, c)
