@@ -243,7 +243,7 @@ static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t 
     alloc((void **)&t->d_pipe_nodes, sizeof(int) * L);
     alloc((void **)&t->d_prod_l, sizeof(int) * L);
     alloc((void **)&t->d_prod_r, sizeof(int) * L);
-    alloc((void **)&t->d_pipe_flags, sizeof(int) * L * 8);
+    alloc((void **)&t->d_pipe_flags, sizeof(int) * L * 32);   // L x panels (<= 28 wide, 8 narrow)
     const int64_t nchunks = p.tile_chunk0[L];
     t->wide = n > 64;
     t->npan = (int)((n + 7) / 8);
@@ -361,12 +361,19 @@ tsqr_status_t tsqr_factor(int64_t m_local, int64_t n, double *A, int64_t lda, do
         const int L = t->plan.ntiles();
         CUDA_TRY(launch_wide_leaves(A, lda, (int)n, t->d_row0, t->d_rows, L, t->d_tau_chunk, t->d_tcache, t->stream),
                  "tsqr_factor leaves");
-        for (size_t g = t->step_off.size() - 1; g-- > 0;) {         // tree steps bottom-up
-            const int cnt = t->step_off[g + 1] - t->step_off[g];
-            if (cnt == 0) continue;
-            CUDA_TRY(launch_wide_nodes(A, lda, (int)n, t->d_row0, t->d_node_a, t->d_step_ids + t->step_off[g], cnt,
-                                       t->d_tau_node, t->d_tcache_node, t->stream),
+        if (wide_tree_pipe_ok((int)n)) {
+            CUDA_TRY(launch_wide_tree_pipe(A, lda, (int)n, t->d_row0, t->d_node_a, t->d_pipe_nodes, t->pipe_count,
+                                           t->d_prod_l, t->d_prod_r, t->d_pipe_flags, t->d_tau_node,
+                                           t->d_tcache_node, t->stream),
                      "tsqr_factor tree");
+        } else {
+            for (size_t g = t->step_off.size() - 1; g-- > 0;) {     // tree steps bottom-up
+                const int cnt = t->step_off[g + 1] - t->step_off[g];
+                if (cnt == 0) continue;
+                CUDA_TRY(launch_wide_nodes(A, lda, (int)n, t->d_row0, t->d_node_a, t->d_step_ids + t->step_off[g],
+                                           cnt, t->d_tau_node, t->d_tcache_node, t->stream),
+                         "tsqr_factor tree");
+            }
         }
         if (R) CUDA_TRY(launch_extract_r(A, lda, (int)n, R, ldr, t->stream), "tsqr_factor R");
         return debug_sync(t, t->stream, "tsqr_factor");

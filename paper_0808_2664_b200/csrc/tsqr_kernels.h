@@ -107,6 +107,11 @@ cudaError_t launch_tree(const FactorArgs &f, cudaStream_t st);
 cudaError_t launch_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *node_a,
                              const int *nodes, int count, const int *prod_l, const int *prod_r, int *flags,
                              double *tau_node, int root, double *R, int64_t ldr, cudaStream_t st);
+// The same for 64 < n <= 224: one CTA per node (flags L x 28 ints).
+bool wide_tree_pipe_ok(int n);
+cudaError_t launch_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *node_a,
+                                  const int *nodes, int count, const int *prod_l, const int *prod_r, int *flags,
+                                  double *tau_node, double *tcache_node, cudaStream_t st);
 cudaError_t launch_apply(const ApplyArgs &f, cudaStream_t st);
 cudaError_t launch_apply_nodes(const ApplyArgs &f, cudaStream_t st);
 cudaError_t launch_formq_nodes(int NP, const double *A, int64_t lda, int n, const DevPlan &plan,

@@ -243,4 +243,189 @@ cudaError_t launch_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_
     });
 }
 
+
+// =====================================================================
+// Pipelined reduction tree for 64 < n <= 224 (a4, a6): one CTA per node.
+// R_b's upper block-triangle sits in shared memory as 8x8 column-major blocks
+// (block (k, cb), k <= cb; element (r, c) at [8c + r], which is exactly the
+// DMMA fragment order: lane (q, l4) reads rows 2q, 2q+1 of column l4 as one
+// double2), R_a's pivot rows of the current panel likewise (one block per
+// column block).  Panel P: wait for both children's panel P, load R_a's and
+// R_b's row block P (the only rows of them reflectors < 8P have not touched),
+// warp 0 runs the 8 structured Householder steps on column block P (rows
+// 0..8P+7 of R_b), builds T, then all warps update the trailing column blocks
+// with DMMA (W^T = R_a rows + Y^T R_b, W'^T = W^T T, R_a rows -= W'^T,
+// R_b -= Y W'^T).  The node's R rows 8P..8P+7 go to the left subtree's head,
+// Y1's columns 8P..8P+7 to the right subtree's head, then the panel flag.
+namespace wtree {
+
+constexpr int NT = 256;
+constexpr int MAX_NPAN = 28;
+
+__host__ __device__ constexpr int nblk(int npan) { return npan * (npan + 1) / 2; }
+__host__ __device__ inline size_t smem_doubles(int npan) { return (size_t)(nblk(npan) + npan) * 64 + 64 + 64 + 8 + 2 * 8 * npan; }
+
+__device__ __forceinline__ double *blk(double *Rb, int k, int cb) { return Rb + 64 * (cb * (cb + 1) / 2 + k); }
+
+__device__ __forceinline__ void wait_flag_cta(const int *f) {
+    if (threadIdx.x == 0) {
+        while (*reinterpret_cast<const volatile int *>(f) == 0) __nanosleep(100);
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+}  // namespace wtree
+
+__global__ void __launch_bounds__(wtree::NT, 1)
+k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *node_a, const int *nodes,
+                 int count, const int *prod_l, const int *prod_r, int *flags, double *tau_node, double *tcache_node) {
+    using namespace wtree;
+    extern __shared__ __align__(16) double sm[];
+    const int npan = (n + 7) / 8;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+    double *Rb = sm;                                 // nblk(npan) blocks
+    double *Ra = Rb + 64 * nblk(npan);               // npan blocks: R_a's pivot rows of the panel
+    double *Gs = Ra + 64 * npan, *Ts = Gs + 64, *t8 = Ts + 64, *xs = t8 + 8;   // xs: 2 x 8 npan
+    const int b = nodes[blockIdx.x], a = node_a[b];
+    double *Ha = A + tile_row0[a], *Hb = A + tile_row0[b];
+    const int pl = prod_l[b], pr = prod_r[b];
+    double *tau_out = tau_node + (int64_t)b * n;
+    double *tc = tcache_node + (int64_t)b * npan * 64;
+    for (int P = 0; P < npan; ++P) {
+        if (pl >= 0) wait_flag_cta(flags + pl * MAX_NPAN + P);
+        if (pr >= 0) wait_flag_cta(flags + pr * MAX_NPAN + P);
+        // row block P of R_a and R_b (upper part), column blocks P..npan-1
+        for (int e = threadIdx.x; e < 64 * (npan - P); e += NT) {
+            const int cb = P + (e >> 6), cl = (e >> 3) & 7, r = e & 7;
+            const int i = 8 * P + r, c = 8 * cb + cl;
+            const bool ok = c >= i && c < n;
+            Ra[64 * cb + 8 * cl + r] = ok ? __ldcg(Ha + i + (int64_t)c * lda) : 0.0;
+            blk(Rb, P, cb)[8 * cl + r] = ok ? __ldcg(Hb + i + (int64_t)c * lda) : 0.0;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            // pivot column (column 8P of R_b, rows 0..8P+7) -> xs[0]
+            for (int k = 0; k <= P; ++k)
+                if (l4 == 0)
+                    *reinterpret_cast<double2 *>(xs + 8 * k + 2 * q) =
+                        *reinterpret_cast<const double2 *>(blk(Rb, k, P) + 2 * q);
+            __syncwarp();
+            double *RaP = Ra + 64 * P;
+#pragma unroll 1
+            for (int jj = 0; jj < 8; ++jj) {
+                const double *xr = xs + (jj & 1) * 8 * npan;
+                double d0 = 0.0, d1 = 0.0, s0 = 0.0, s1 = 0.0;
+#pragma unroll 4
+                for (int k = 0; k <= P; ++k) {
+                    const double2 x = *reinterpret_cast<const double2 *>(xr + 8 * k + 2 * q);
+                    const double2 v = *reinterpret_cast<const double2 *>(blk(Rb, k, P) + 8 * l4 + 2 * q);
+                    d0 = fma(x.x, v.x, d0);
+                    d1 = fma(x.y, v.y, d1);
+                    s0 = fma(x.x, x.x, s0);
+                    s1 = fma(x.y, x.y, s1);
+                }
+                double d = d0 + d1, s2 = s0 + s1;
+                d += __shfl_xor_sync(tree::FULL, d, 1);
+                s2 += __shfl_xor_sync(tree::FULL, s2, 1);
+                d += __shfl_xor_sync(tree::FULL, d, 2);
+                s2 += __shfl_xor_sync(tree::FULL, s2, 2);
+                const double alpha = RaP[8 * jj + jj];
+                const double rj = RaP[8 * l4 + jj];
+                const House h = house_bf(alpha, s2);
+                const double w = fma(h.scale, d, rj);
+                const double u = (l4 > jj) ? h.tau * h.scale * w : (l4 == jj ? 1.0 : 0.0);
+                const double g = (l4 == jj) ? h.scale : 0.0;
+                const double rnew = (l4 == jj) ? h.beta : fma(-h.tau, w, rj);
+                double *xw = xs + ((jj + 1) & 1) * 8 * npan;
+#pragma unroll 4
+                for (int k = 0; k <= P; ++k) {
+                    const double2 x = *reinterpret_cast<const double2 *>(xr + 8 * k + 2 * q);
+                    double2 *vp = reinterpret_cast<double2 *>(blk(Rb, k, P) + 8 * l4 + 2 * q);
+                    double2 v = *vp;
+                    v.x = fma(g, x.x, fma(-u, x.x, v.x));
+                    v.y = fma(g, x.y, fma(-u, x.y, v.y));
+                    *vp = v;
+                    if (l4 == jj + 1) *reinterpret_cast<double2 *>(xw + 8 * k + 2 * q) = v;
+                }
+                __syncwarp();
+                if (q == 0 && l4 >= jj) RaP[8 * l4 + jj] = rnew;
+                if (q == 0 && l4 < jj) Gs[l4 * 8 + jj] = h.scale * d;
+                if (lane == 0) t8[jj] = h.tau;
+                __syncwarp();
+            }
+            if (lane < 8 && 8 * P + lane < n) tau_out[8 * P + lane] = t8[lane];
+            build_t(Gs, t8, Ts);
+            *reinterpret_cast<double2 *>(tc + 64 * P + 2 * lane) = *reinterpret_cast<const double2 *>(Ts + 2 * lane);
+        }
+        __syncthreads();
+        // trailing column blocks, split over the warps
+        {
+            const double tb0 = Ts[(2 * q) * 8 + l4], tb1 = Ts[(2 * q + 1) * 8 + l4];
+            for (int cb = P + 1 + warp; cb < npan; cb += NT / 32) {
+                double w0[2] = {0.0, 0.0}, w1[2] = {0.0, 0.0};
+#pragma unroll 4
+                for (int k = 0; k <= P; ++k) {
+                    const double2 c = *reinterpret_cast<const double2 *>(blk(Rb, k, cb) + 8 * l4 + 2 * q);
+                    const double2 y = *reinterpret_cast<const double2 *>(blk(Rb, k, P) + 8 * l4 + 2 * q);
+                    dmma(w0[k & 1], w1[k & 1], c.x, y.x);
+                    dmma(w0[k & 1], w1[k & 1], c.y, y.y);
+                }
+                double2 *rp = reinterpret_cast<double2 *>(Ra + 64 * cb + 8 * l4 + 2 * q);
+                double2 rv = *rp;
+                const double wt0 = w0[0] + w0[1] + rv.x, wt1 = w1[0] + w1[1] + rv.y;
+                double p0 = 0.0, p1 = 0.0;
+                dmma(p0, p1, wt0, tb0);
+                dmma(p0, p1, wt1, tb1);
+                rv.x -= p0;
+                rv.y -= p1;
+                *rp = rv;
+#pragma unroll 4
+                for (int k = 0; k <= P; ++k) {
+                    const double *yb = blk(Rb, k, P);
+                    const double yt0 = yb[8 * (2 * q) + l4], yt1 = yb[8 * (2 * q + 1) + l4];
+                    double2 *cp = reinterpret_cast<double2 *>(blk(Rb, k, cb) + 8 * l4 + 2 * q);
+                    double2 c = *cp;
+                    dmma(c.x, c.y, -p0, yt0);
+                    dmma(c.x, c.y, -p1, yt1);
+                    *cp = c;
+                }
+            }
+        }
+        __syncthreads();
+        // publish: R rows 8P..8P+7 -> tile a's head, Y1 columns 8P..8P+7 -> tile b's head
+        for (int e = threadIdx.x; e < 64 * (npan - P); e += NT) {
+            const int cb = P + (e >> 6), cl = (e >> 3) & 7, r = e & 7;
+            const int i = 8 * P + r, c = 8 * cb + cl;
+            if (c >= i && c < n) Ha[i + (int64_t)c * lda] = Ra[64 * cb + 8 * cl + r];
+        }
+        for (int e = threadIdx.x; e < 64 * (P + 1); e += NT) {
+            const int k = e >> 6, cl = (e >> 3) & 7, r = e & 7;
+            const int i = 8 * k + r, c = 8 * P + cl;
+            if (i <= c && c < n) Hb[i + (int64_t)c * lda] = blk(Rb, k, P)[8 * cl + r];
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) *reinterpret_cast<volatile int *>(flags + b * MAX_NPAN + P) = 1;
+    }
+}
+
+bool wide_tree_pipe_ok(int n) { return (n + 7) / 8 <= wtree::MAX_NPAN; }
+
+cudaError_t launch_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *node_a,
+                                  const int *nodes, int count, const int *prod_l, const int *prod_r, int *flags,
+                                  double *tau_node, double *tcache_node, cudaStream_t st) {
+    if (count == 0) return cudaSuccess;
+    const int npan = (n + 7) / 8;
+    if (npan > wtree::MAX_NPAN) return cudaErrorInvalidValue;
+    const size_t bytes = wtree::smem_doubles(npan) * sizeof(double);
+    cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)(count + 1) * wtree::MAX_NPAN, st);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute((const void *)k_wide_tree_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+    k_wide_tree_pipe<<<count, wtree::NT, bytes, st>>>(A, lda, n, tile_row0, node_a, nodes, count, prod_l, prod_r,
+                                                      flags, tau_node, tcache_node);
+    return cudaGetLastError();
+}
+
 }  // namespace tsqr
