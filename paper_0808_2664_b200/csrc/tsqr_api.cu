@@ -359,7 +359,8 @@ tsqr_status_t tsqr_factor(int64_t m_local, int64_t n, double *A, int64_t lda, do
     ca.cta_tile0 = t->d_cta_tile0; ca.grid = t->chain_grid; ca.tau = t->d_tau_chunk; ca.tcache = t->d_tcache;
     if (t->wide) {
         const int L = t->plan.ntiles();
-        CUDA_TRY(launch_wide_leaves(A, lda, (int)n, t->d_row0, t->d_rows, L, t->d_tau_chunk, t->d_tcache, t->stream),
+        CUDA_TRY(launch_wide_leaves(A, lda, (int)n, t->d_row0, t->d_rows, L, (int)t->plan.max_rows, t->d_tau_chunk,
+                                    t->d_tcache, t->stream),
                  "tsqr_factor leaves");
         if (wide_tree_pipe_ok((int)n)) {
             CUDA_TRY(launch_wide_tree_pipe(A, lda, (int)n, t->d_row0, t->d_node_a, t->d_pipe_nodes, t->pipe_count,

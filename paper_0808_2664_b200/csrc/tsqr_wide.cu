@@ -291,20 +291,218 @@ __device__ void wide_apply(const Prob &P, const Prob &Cp, int n, int k, const do
     }
 }
 
+
+// ------------------------------------------------------------------ leaves
+// The leaf path (plain tiles, no masks): the panel's Y is staged in shared
+// memory (row-major H x 8, zero-padded to a whole row block), so the column-
+// split trailing update / apply streams only C from global memory, with 8 row
+// blocks of loads in flight per lane.
+constexpr int UNR = 8;
+
+// C <- (I - Y T' Y^T) C on columns [c_lo, c_hi) and rows [8 rb0, H) of C
+// (T' = T^T for Q^T, kFwd; T for Q), Y = Ys (rows >= 8 rb0 valid, zero past H).
+template <bool kFwd>
+__device__ __forceinline__ void apply_panel_cols(const double *Ys, const double *Tg, double *C, int64_t ldc, int H,
+                                                 int rb0, int c_lo, int c_hi) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+    const double tb0 = kFwd ? Tg[(2 * q) * 8 + l4] : Tg[l4 * 8 + 2 * q];
+    const double tb1 = kFwd ? Tg[(2 * q + 1) * 8 + l4] : Tg[l4 * 8 + 2 * q + 1];
+    const int nrb = (H + 7) / 8;
+    for (int cb = c_lo / 8 + warp; 8 * cb < c_hi; cb += NW) {
+        const int col = 8 * cb + l4;
+        const bool okc = col < c_hi;
+        double *cp = C + (int64_t)(okc ? col : c_lo) * ldc;
+        double w0[2] = {0.0, 0.0}, w1[2] = {0.0, 0.0};
+        for (int k0 = rb0; k0 < nrb; k0 += UNR) {
+            double cv[UNR][2];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const int r = 8 * (k0 + u) + 2 * q;
+                cv[u][0] = (okc && r < H) ? cp[r] : 0.0;
+                cv[u][1] = (okc && r + 1 < H) ? cp[r + 1] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                if (k0 + u < nrb) {
+                    const int r = 8 * (k0 + u) + 2 * q;
+                    dmma(w0[u & 1], w1[u & 1], cv[u][0], Ys[r * 8 + l4]);
+                    dmma(w0[u & 1], w1[u & 1], cv[u][1], Ys[(r + 1) * 8 + l4]);
+                }
+            }
+        }
+        double p0 = 0.0, p1 = 0.0;
+        dmma(p0, p1, w0[0] + w0[1], tb0);
+        dmma(p0, p1, w1[0] + w1[1], tb1);
+        for (int k0 = rb0; k0 < nrb; k0 += UNR) {
+            double cv[UNR][2];
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const int r = 8 * (k0 + u) + 2 * q;
+                cv[u][0] = (okc && r < H) ? cp[r] : 0.0;
+                cv[u][1] = (okc && r + 1 < H) ? cp[r + 1] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                if (k0 + u < nrb) {
+                    const double2 y = *reinterpret_cast<const double2 *>(Ys + (8 * (k0 + u) + l4) * 8 + 2 * q);
+                    dmma(cv[u][0], cv[u][1], -p0, y.x);
+                    dmma(cv[u][0], cv[u][1], -p1, y.y);
+                    const int r = 8 * (k0 + u) + 2 * q;
+                    if (okc && r < H) cp[r] = cv[u][0];
+                    if (okc && r + 1 < H) cp[r + 1] = cv[u][1];
+                }
+            }
+        }
+    }
+}
+
+struct LeafSmem {
+    double part[2][NW][9];
+    double piv[2][8];
+    double Gs[64], Ts[64], t8[8];
+    double xs[NW][2][RW];
+    double Ys[MAXR * 8];
+};
+
+// Blocked compact-WY QR of one tile (H rows, H <= 64 KM): the panel is
+// row-split over the warps (warp w: rows [w 8KM, (w+1) 8KM)), one
+// __syncthreads per Householder step for the cross-warp sums; T per panel;
+// the trailing update column-split (apply_panel_cols).
+template <int KM>
+__device__ void wide_leaf_qr(double *At, int64_t lda, int H, int n, double *tau, double *tcache, LeafSmem &S) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+    const int npan = (n + 7) / 8;
+    const int rbase = warp * 8 * KM;
+    const int Hp = 8 * ((H + 7) / 8);
+    for (int p = 0; p < npan; ++p) {
+        const int c = 8 * p + l4;
+        double *colp = At + (int64_t)(c < n ? c : 0) * lda;
+        double a[KM][2];
+#pragma unroll
+        for (int k = 0; k < KM; ++k)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int r = rbase + 8 * k + 2 * q + e;
+                a[k][e] = (c < n && r < H) ? colp[r] : 0.0;
+            }
+        double *xs0 = S.xs[warp][0], *xs1 = S.xs[warp][1];
+        if (l4 == 0) {
+#pragma unroll
+            for (int k = 0; k < KM; ++k)
+                *reinterpret_cast<double2 *>(xs0 + 8 * k + 2 * q) = make_double2(a[k][0], a[k][1]);
+        }
+        __syncwarp();
+#pragma unroll 1
+        for (int jj = 0; jj < 8; ++jj) {
+            const int j = 8 * p + jj;
+            const int par = jj & 1;
+            const double *xr = par ? xs1 : xs0;
+            double d[4] = {0.0, 0.0, 0.0, 0.0}, s[4] = {0.0, 0.0, 0.0, 0.0};
+            double pv = 0.0;
+            bool haspiv = false;
+#pragma unroll
+            for (int k = 0; k < KM; ++k) {
+                const double2 xv = *reinterpret_cast<const double2 *>(xr + 8 * k + 2 * q);
+                const int r = rbase + 8 * k + 2 * q;
+                const double x0 = r > j ? xv.x : 0.0, x1 = r + 1 > j ? xv.y : 0.0;
+                d[k & 3] = fma(x0, a[k][0], d[k & 3]);
+                d[(k + 2) & 3] = fma(x1, a[k][1], d[(k + 2) & 3]);
+                s[k & 3] = fma(x0, x0, s[k & 3]);
+                s[(k + 2) & 3] = fma(x1, x1, s[(k + 2) & 3]);
+                if (r == j) { pv = a[k][0]; haspiv = true; }
+                if (r + 1 == j) { pv = a[k][1]; haspiv = true; }
+            }
+            double dd = (d[0] + d[1]) + (d[2] + d[3]), s2 = (s[0] + s[1]) + (s[2] + s[3]);
+            dd += __shfl_xor_sync(FULL, dd, 1);
+            s2 += __shfl_xor_sync(FULL, s2, 1);
+            dd += __shfl_xor_sync(FULL, dd, 2);
+            s2 += __shfl_xor_sync(FULL, s2, 2);
+            if (q == 0) S.part[par][warp][l4] = dd;
+            if (lane == 0) S.part[par][warp][8] = s2;
+            if (haspiv) S.piv[par][l4] = pv;
+            __syncthreads();
+            dd = 0.0;
+            s2 = 0.0;
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                dd += S.part[par][w][l4];
+                s2 += S.part[par][w][8];
+            }
+            const double rj = S.piv[par][l4], alpha = S.piv[par][jj];
+            const House h = house(alpha, s2);
+            const double wv = fma(h.scale, dd, rj);
+            const double u = (l4 > jj) ? h.tau * h.scale * wv : (l4 == jj ? 1.0 : 0.0);
+            const double g = (l4 == jj) ? h.scale : 0.0;
+            const double pnew = (l4 > jj) ? fma(-h.tau, wv, rj) : (l4 == jj ? h.beta : rj);
+            double *xw = par ? xs0 : xs1;
+#pragma unroll
+            for (int k = 0; k < KM; ++k) {
+                const double2 xv = *reinterpret_cast<const double2 *>(xr + 8 * k + 2 * q);
+                const int r = rbase + 8 * k + 2 * q;
+                const double x0 = r > j ? xv.x : 0.0, x1 = r + 1 > j ? xv.y : 0.0;
+                double a0 = fma(g, x0, fma(-u, x0, a[k][0])), a1 = fma(g, x1, fma(-u, x1, a[k][1]));
+                a0 = (r == j) ? pnew : a0;
+                a1 = (r + 1 == j) ? pnew : a1;
+                a[k][0] = a0;
+                a[k][1] = a1;
+                if (l4 == jj + 1) *reinterpret_cast<double2 *>(xw + 8 * k + 2 * q) = make_double2(a0, a1);
+            }
+            if (warp == 0 && q == 0 && l4 < jj) S.Gs[l4 * 8 + jj] = fma(h.scale, dd, rj);
+            if (threadIdx.x == 0) S.t8[jj] = h.tau;
+            __syncwarp();
+        }
+        // write the panel back; Y of the panel -> Ys (rows >= 8p, zero past H)
+#pragma unroll
+        for (int k = 0; k < KM; ++k)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int r = rbase + 8 * k + 2 * q + e;
+                if (c < n && r < H) colp[r] = a[k][e];
+                if (r >= 8 * p && r < Hp) S.Ys[r * 8 + l4] = (c >= n || r < c || r >= H) ? 0.0 : (r == c ? 1.0 : a[k][e]);
+            }
+        __syncthreads();
+        if (warp == 0) {
+            const int rr = lane & 7;
+            double row[8];
+            const double tr = S.t8[rr];
+#pragma unroll
+            for (int cc = 0; cc < 8; ++cc) row[cc] = (cc == rr) ? tr : 0.0;
+#pragma unroll
+            for (int cc = 1; cc < 8; ++cc) {
+                double sacc = 0.0;
+#pragma unroll
+                for (int l = 0; l < cc; ++l) sacc = fma(row[l], S.Gs[l * 8 + cc], sacc);
+                row[cc] = (rr < cc) ? -S.t8[cc] * sacc : row[cc];
+            }
+            if (lane < 8) {
+#pragma unroll
+                for (int cc = 0; cc < 8; ++cc) {
+                    S.Ts[lane * 8 + cc] = row[cc];
+                    tcache[p * 64 + lane * 8 + cc] = row[cc];
+                }
+                if (8 * p + lane < n) tau[8 * p + lane] = S.t8[lane];
+            }
+        }
+        __syncthreads();
+        if (p + 1 < npan) apply_panel_cols<true>(S.Ys, S.Ts, At, lda, H, p, 8 * (p + 1), n);
+        __syncthreads();
+    }
+}
 }  // namespace wide
 
 using namespace wide;
 
-// Leaves: problem t = tile t (one CTA each).
+// Leaves: tile t (one CTA each), row-split panels sized to the tile.
+template <int KM>
 __global__ void __launch_bounds__(NT, 1)
 k_wide_leaves(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *tile_rows, double *tau_tile,
               double *tcache_tile) {
     extern __shared__ __align__(16) double smraw[];
-    Smem &S = *reinterpret_cast<Smem *>(smraw);
+    LeafSmem &S = *reinterpret_cast<LeafSmem *>(smraw);
     const int t = blockIdx.x;
     const int npan = (n + 7) / 8;
-    Prob P{A + tile_row0[t], nullptr, lda, 0, tile_rows[t], 0, tile_rows[t], 0};
-    wide_qr(P, n, tau_tile + (int64_t)t * n, tcache_tile + (int64_t)t * npan * 64, S);
+    wide_leaf_qr<KM>(A + tile_row0[t], lda, tile_rows[t], n, tau_tile + (int64_t)t * n,
+                     tcache_tile + (int64_t)t * npan * 64, S);
 }
 
 // Tree nodes of one step: node ids[i] = b (right subtree's first tile), its
@@ -329,16 +527,33 @@ k_wide_node1(double *Ra, int64_t lda, double *Rb, int64_t ldb, int n, double *ta
     wide_qr(P, n, tau, tcache, S);
 }
 
-// Q^T C / Q C on the leaves (forward: all tiles; C rows = the tile's rows).
+// Q^T C / Q C on the leaves (forward: all tiles; C rows = the tile's rows):
+// panel by panel (forward for Q^T, backward for Q) the panel's Y is staged in
+// shared memory from the stored factor, then the column-split update.
 template <bool kFwd>
 __global__ void __launch_bounds__(NT, 1)
 k_wide_apply_leaves(const double *A, int64_t lda, int n, const int64_t *tile_row0, const int *tile_rows,
                     const double *tcache_tile, double *C, int64_t ldc, int k) {
+    extern __shared__ __align__(16) double smraw[];
+    double *Ys = smraw, *Ts = smraw + MAXR * 8;
     const int t = blockIdx.x;
     const int npan = (n + 7) / 8;
-    Prob P{const_cast<double *>(A) + tile_row0[t], nullptr, lda, 0, tile_rows[t], 0, tile_rows[t], 0};
-    Prob Cp{C + tile_row0[t], nullptr, ldc, 0, tile_rows[t], 0, tile_rows[t], 0};
-    wide_apply<kFwd>(P, Cp, n, k, tcache_tile + (int64_t)t * npan * 64);
+    const int H = tile_rows[t];
+    const int Hp = 8 * ((H + 7) / 8);
+    const double *At = A + tile_row0[t];
+    const double *tc = tcache_tile + (int64_t)t * npan * 64;
+    for (int pp = 0; pp < npan; ++pp) {
+        const int p = kFwd ? pp : npan - 1 - pp;
+        const int h0 = 8 * p, hs = Hp - h0;
+        for (int e = threadIdx.x; e < 8 * hs; e += NT) {
+            const int r = h0 + e % hs, jj = e / hs, c = 8 * p + jj;
+            Ys[r * 8 + jj] = (c >= n || r < c || r >= H) ? 0.0 : (r == c ? 1.0 : At[r + (int64_t)c * lda]);
+        }
+        if (threadIdx.x < 64) Ts[threadIdx.x] = tc[64 * p + threadIdx.x];
+        __syncthreads();
+        apply_panel_cols<kFwd>(Ys, Ts, C + tile_row0[t], ldc, H, p, 0, k);
+        __syncthreads();
+    }
 }
 
 // Q^T / Q of one tree step's nodes on C's head rows (or on xbuf blocks for form Q).
@@ -385,12 +600,26 @@ static cudaError_t wide_attr(const void *fn) {
 }
 int wide_max_rows() { return MAXR; }
 
-cudaError_t launch_wide_leaves(double *A, int64_t lda, int n, const int64_t *row0, const int *rows, int L,
-                               double *tau, double *tcache, cudaStream_t st) {
-    cudaError_t e = wide_attr((const void *)k_wide_leaves);
+static size_t leaf_smem() { return sizeof(LeafSmem); }
+static size_t apply_leaf_smem() { return sizeof(double) * (MAXR * 8 + 64); }
+
+template <int KM>
+static cudaError_t launch_leaves_km(double *A, int64_t lda, int n, const int64_t *row0, const int *rows, int L,
+                                   double *tau, double *tcache, cudaStream_t st) {
+    cudaError_t e = cudaFuncSetAttribute((const void *)k_wide_leaves<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)leaf_smem());
     if (e != cudaSuccess) return e;
-    k_wide_leaves<<<L, NT, wide_smem(), st>>>(A, lda, n, row0, rows, tau, tcache);
+    k_wide_leaves<KM><<<L, NT, leaf_smem(), st>>>(A, lda, n, row0, rows, tau, tcache);
     return cudaGetLastError();
+}
+
+// max_rows: the tallest tile (selects the per-warp row range, 64 KM >= max_rows)
+cudaError_t launch_wide_leaves(double *A, int64_t lda, int n, const int64_t *row0, const int *rows, int L,
+                               int max_rows, double *tau, double *tcache, cudaStream_t st) {
+    if (max_rows <= 512) return launch_leaves_km<8>(A, lda, n, row0, rows, L, tau, tcache, st);
+    if (max_rows <= 1024) return launch_leaves_km<16>(A, lda, n, row0, rows, L, tau, tcache, st);
+    if (max_rows <= 1536) return launch_leaves_km<24>(A, lda, n, row0, rows, L, tau, tcache, st);
+    return launch_leaves_km<KMW>(A, lda, n, row0, rows, L, tau, tcache, st);
 }
 
 cudaError_t launch_wide_nodes(double *A, int64_t lda, int n, const int64_t *row0, const int *node_a, const int *ids,
@@ -412,8 +641,11 @@ cudaError_t launch_wide_node1(double *Ra, int64_t lda, double *Rb, int64_t ldb, 
 cudaError_t launch_wide_apply_leaves(const double *A, int64_t lda, int n, const int64_t *row0, const int *rows,
                                      int L, const double *tcache, double *C, int64_t ldc, int k, int forward,
                                      cudaStream_t st) {
-    if (forward) k_wide_apply_leaves<true><<<L, NT, 0, st>>>(A, lda, n, row0, rows, tcache, C, ldc, k);
-    else k_wide_apply_leaves<false><<<L, NT, 0, st>>>(A, lda, n, row0, rows, tcache, C, ldc, k);
+    const void *fn = forward ? (const void *)k_wide_apply_leaves<true> : (const void *)k_wide_apply_leaves<false>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)apply_leaf_smem());
+    if (e != cudaSuccess) return e;
+    if (forward) k_wide_apply_leaves<true><<<L, NT, apply_leaf_smem(), st>>>(A, lda, n, row0, rows, tcache, C, ldc, k);
+    else k_wide_apply_leaves<false><<<L, NT, apply_leaf_smem(), st>>>(A, lda, n, row0, rows, tcache, C, ldc, k);
     return cudaGetLastError();
 }
 
