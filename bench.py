@@ -34,9 +34,9 @@ sys.path.insert(0, ROOT)
 CONFIGS = {
     "c1": dict(m=4096, n=16, b=512, s=512, kind="gauss", op="form_q", k=0,
                desc="fp64 A 4096x16 N(0,1) seed 0, row blocks 512 (8-leaf binary tree): factor + form Q"),
-    "c2": dict(m=1_000_000, n=50, b=4096, s=4096, kind="gauss", op="form_q", k=0,
+    "c2": dict(m=1_000_000, n=50, b=4096, s=1024, kind="gauss", op="form_q", k=0,
                desc="fp64 A 1,000,000x50 N(0,1), row blocks 4096, binary tree: factor + form Q"),
-    "c3": dict(m=100_000, n=200, b=2048, s=2048, kind="gauss", op="apply_qt", k=64,
+    "c3": dict(m=100_000, n=200, b=2048, s=400, kind="gauss", op="apply_qt", k=64,
                desc="fp64 A 100,000x200 N(0,1), row blocks 2048 (blocked compact-WY leaves): factor + apply Q^T "
                     "to C 100,000x64"),
     "c4": dict(m=16_777_216, n=64, b=4096, s=4096, kind="cond", op="form_q", k=0,
@@ -51,6 +51,21 @@ DEFAULT_CONFIG = "c2"   # configs[1]: the workload BASELINE.json's metric is quo
 # 148 SMs x 64 FP64 FMA/clk x 2 flop x 1.965 GHz = 37.23 TFLOP/s (tools/peaks.cu measured
 # DMMA 37.18, DFMA 34.2 TFLOP/s on this pool).
 FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+
+
+def kernel_launches(info, n, op, world):
+    """Kernels of this repo launched per step (tsqr_api.cu's dispatch): factor, then the second op."""
+    multi = info["ntiles"] > 1
+    rounds = info["cross_rounds"] if world > 1 else 0
+    if n <= 64:
+        fac = 1 + 1                                   # chain leaves + pipelined tree (or R extraction)
+        second = (1 + multi) if op == "apply_qt" else (info["depth"] + 2)   # leaves+nodes | identity+node steps+leaves
+    else:
+        fac = 1 + multi + 1                           # leaves + pipelined tree + R extraction
+        second = (1 + info["depth"]) if op == "apply_qt" else (info["depth"] + 4)
+    # butterfly rounds: pack + combine per round on the factor; apply exchanges the head per round
+    cross = 2 * rounds + (1 if rounds else 0) + (2 * rounds if op == "apply_qt" else 0)
+    return fac + second + cross
 
 
 def measured_peaks():
@@ -193,12 +208,14 @@ def run_ours(args, cfg):
     tree = None
     st = None
 
+    engine = tdist.CudaEngine(stage_timing=True) if world > 1 else None
+
     def step():
         nonlocal tree, st
         if world == 1:
-            _, tree = T.factor(A, b, s, R=R, tree=tree)
+            _, tree = T.factor(A, b, s, R=R, tree=tree, stage_timing=True)
         else:
-            st = tdist.factor(A, b, s)
+            st = tdist.factor(A, b, s, engine=engine)
             tree = st.tree
         ev_f.record(stream)
         if cfg["op"] == "form_q":
@@ -224,7 +241,7 @@ def run_ours(args, cfg):
 
     clocks = ClockSampler(dev.index)
     clocks.start()
-    t_factor, t_step = [], []
+    t_factor, t_step, t_leaf, t_tree = [], [], [], []
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -237,16 +254,20 @@ def run_ours(args, cfg):
         ev_e.synchronize()
         t_factor.append(ev_s.elapsed_time(ev_f))
         t_step.append(ev_s.elapsed_time(ev_e))
+        lm, tm = tree.stage_ms()                          # the leaf kernel's own launch (device events)
+        t_leaf.append(lm)
+        t_tree.append(tm)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     wall = time.perf_counter() - wall0
     clk = clocks.stop()
     tf, ts = statistics.mean(t_factor), statistics.mean(t_step)
+    tl, tt = statistics.mean(t_leaf), statistics.mean(t_tree)
     if world > 1:
-        x = torch.tensor([tf, ts], dtype=torch.float64, device=dev)
+        x = torch.tensor([tf, ts, tl, tt], dtype=torch.float64, device=dev)
         dist.all_reduce(x, op=dist.ReduceOp.MAX)
-        tf, ts = x.tolist()
+        tf, ts, tl, tt = x.tolist()
 
     # ---- e2e through the public API with pinned host buffers (host <-> device inside)
     e2e = None
@@ -285,7 +306,12 @@ def run_ours(args, cfg):
         return 0
 
     flops = 2.0 * m * n * n
-    achieved = flops / (tf * 1e-3) / 1e12           # TFLOP/s of the whole job
+    # dominant kernel = the leaf stage (a2+a3), one launch per step: its algorithmic flops are
+    # the Householder QR flops of every local tile, sum(2 h n^2 - 2 n^3/3),
+    # over its own launch time from device events on the factor's stream (tsqr_tree_stage_ms)
+    tiles = T.plan_export(ml, n, block_rows=b, tile_rows=s, nranks=world, rank=rank)["tile_rows"]
+    leaf_flops = float(sum(2.0 * h * n * n - 2.0 * n ** 3 / 3 for h in tiles)) * world
+    achieved = leaf_flops / (tl * 1e-3) / 1e12      # TFLOP/s of the leaf kernel (all ranks)
     peak = FP64_PEAK_TFLOPS * world
     pk = measured_peaks()
     bw = pk.get("hbm_gbs", 6555.8)
@@ -297,12 +323,7 @@ def run_ours(args, cfg):
             traffic = json.load(open(prof)).get(f"{args.config}_factor")
         except Exception:
             traffic = None
-    # factor: chain leaves + tree climb; form Q: identity + one node launch per tree
-    # step + chain leaves; apply Q^T: chain leaves + node climb
-    multi = info["ntiles"] > 1
-    launches_per_step = (1 + multi) + (info["depth"] + 2 if cfg["op"] == "form_q" else 1 + multi)
-    if world > 1:
-        launches_per_step += 2 * info["cross_rounds"] + 1 + (2 * info["cross_rounds"] if cfg["op"] == "apply_qt" else 0)
+    launches_per_step = kernel_launches(info, n, cfg["op"], world)
     cpu = oracle_sample(cfg) if (world == 1 and not args.no_cpu_baseline) else None
     line = {
         "metric": METRIC, "value": flops / (tf * 1e-3) / 1e9, "unit": "GFLOP/s", "n_gpus": world,
@@ -313,10 +334,13 @@ def run_ours(args, cfg):
                    "cross_rounds": info["cross_rounds"], "second_op": cfg["op"], "k": k,
                    "l2": "inputs larger than L2 (A = %.0f MB > 126 MB), pristine A restored before each step"
                          % (8e-6 * m * n),
-                   "value_timing": "CUDA events around tsqr_factor (one kernel launch) per step, mean of K, max over ranks"},
+                   "value_timing": "CUDA events around tsqr_factor (leaf kernel + tree kernel) per step, mean of K, "
+                                   "max over ranks"},
         "roofline": {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (DESIGN.md); measured DMMA 37.18",
+                     "kernel": "leaf stage (k_chain_factor n<=64 / k_wide_leaves n>64), one launch per step",
+                     "kernel_ms": tl, "kernel_flops_per_launch": leaf_flops / world, "tree_ms": tt,
                      "frac_of_max_roofline": t_roof / (tf * 1e-3)},
         "ms_factor": tf, "second_op_ms": ts - tf,
         "second_op_gflops": (2.0 * m * n * n - 2.0 * n ** 3 / 3 if cfg["op"] == "form_q" else 4.0 * m * n * k)

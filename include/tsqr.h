@@ -47,7 +47,9 @@ typedef enum {
  *  nranks, rank: the row-sharded multi-GPU layout (Alg. TSQR:par);
  *              nranks = 1 for a single GPU.  A rank's slab must be the one
  *              tsqr_slab() assigns.
- *  flags:      bit 0 = synchronise and check after every launch (debug). */
+ *  flags:      bit 0 = synchronise and check after every launch (debug);
+ *              bit 1 = record CUDA events around tsqr_factor's leaf and tree
+ *              stages on its stream (read back with tsqr_tree_stage_ms). */
 typedef struct {
     int64_t block_rows;
     int64_t tile_rows;
@@ -171,6 +173,12 @@ tsqr_status_t tsqr_tree_free(tsqr_tree_t tree);
  * may be NULL).
  * Synchronises the tree's stream. */
 tsqr_status_t tsqr_tree_export_tau(tsqr_tree_t tree, double *tau_tile_host, double *tau_node_host);
+
+/* Measurement hook: device time (ms) of the last tsqr_factor's leaf stage
+ * (a2+a3: the dominant kernel) and of its tree stage (a4+a6), from CUDA events
+ * recorded on the factor's stream when opts.flags bit 1 was set (else
+ * TSQR_ERR_INVALID).  Either pointer may be NULL.  Waits for the last event. */
+tsqr_status_t tsqr_tree_stage_ms(tsqr_tree_t tree, float *leaf_ms, float *tree_ms);
 
 #ifdef __cplusplus
 }

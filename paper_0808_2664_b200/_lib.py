@@ -18,7 +18,8 @@ MAX_N = 256
 # every symbol include/tsqr.h declares
 SYMBOLS = ["tsqr_status_string", "tsqr_last_error", "tsqr_slab", "tsqr_plan_info", "tsqr_plan_export",
            "tsqr_cross_partner", "tsqr_factor", "tsqr_pack_r", "tsqr_cross_factor", "tsqr_apply_qt",
-           "tsqr_cross_apply_qt", "tsqr_form_q", "tsqr_tree_free", "tsqr_tree_export_tau"]
+           "tsqr_cross_apply_qt", "tsqr_form_q", "tsqr_tree_free", "tsqr_tree_export_tau",
+           "tsqr_tree_stage_ms"]
 
 
 class TsqrError(RuntimeError):
@@ -73,6 +74,7 @@ def lib():
         "tsqr_form_q": [_vp, _vp, _i64, _vp],
         "tsqr_tree_free": [_vp],
         "tsqr_tree_export_tau": [_vp, _vp, _vp],
+        "tsqr_tree_stage_ms": [_vp, _vp, _vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)

@@ -33,8 +33,9 @@ def _colmajor(t: torch.Tensor, name: str):
     return t.data_ptr(), nrows, ncols, ld
 
 
-def opts(block_rows: int = 0, tile_rows: int = 0, nranks: int = 1, rank: int = 0, debug: bool = False) -> Opts:
-    return Opts(block_rows, tile_rows, nranks, rank, 1 if debug else 0, 0)
+def opts(block_rows: int = 0, tile_rows: int = 0, nranks: int = 1, rank: int = 0, debug: bool = False,
+         stage_timing: bool = False) -> Opts:
+    return Opts(block_rows, tile_rows, nranks, rank, (1 if debug else 0) | (2 if stage_timing else 0), 0)
 
 
 class Tree:
@@ -60,6 +61,12 @@ class Tree:
         except Exception:
             pass
 
+    def stage_ms(self):
+        """(leaf_ms, tree_ms) of the last factor run with stage_timing=True (device events)."""
+        a, b = ctypes.c_float(), ctypes.c_float()
+        check(lib().tsqr_tree_stage_ms(self.handle, ctypes.byref(a), ctypes.byref(b)), "tsqr_tree_stage_ms")
+        return a.value, b.value
+
     def export_tau(self):
         info = plan_info(self.m_local, self.n, self.opts)
         L, n = info["ntiles"], self.n
@@ -71,14 +78,15 @@ class Tree:
 
 
 def factor(A: torch.Tensor, block_rows: int = 0, tile_rows: int = 0, R: torch.Tensor | None = None,
-           nranks: int = 1, rank: int = 0, tree: Tree | None = None, stream=None, debug: bool = False):
+           nranks: int = 1, rank: int = 0, tree: Tree | None = None, stream=None, debug: bool = False,
+           stage_timing: bool = False):
     """Factor A (column-major m_local x n) in place.  Returns (R, tree): R is n x n upper
     triangular as a column-major (n, n) tensor.  Pass `tree` back in to reuse its workspace."""
     pa, m, n, lda = _colmajor(A, "A")
     if R is None:
         R = torch.empty((n, n), dtype=torch.float64, device=A.device)
     pr, _, _, ldr = _colmajor(R, "R")
-    o = opts(block_rows, tile_rows, nranks, rank, debug)
+    o = opts(block_rows, tile_rows, nranks, rank, debug, stage_timing)
     t = tree if tree is not None else Tree()
     h = t.handle
     check(lib().tsqr_factor(m, n, pa, lda, pr, ldr, ctypes.byref(o), _stream_ptr(stream), ctypes.byref(h)),

@@ -34,6 +34,8 @@ struct tsqr_tree_s {
     int *d_step_ids = nullptr;
     int *d_pipe_nodes = nullptr, *d_prod_l = nullptr, *d_prod_r = nullptr, *d_pipe_flags = nullptr;
     int pipe_count = 0, pipe_root = -1;
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};   // stage timing (opts.flags bit 1)
+    bool ev_recorded = false;
     // chunk-chain leaf stage
     int64_t *d_tile_chunk0 = nullptr;
     int *d_cta_tile0 = nullptr, *d_apply_cta_tile0 = nullptr;
@@ -346,6 +348,12 @@ tsqr_status_t tsqr_factor(int64_t m_local, int64_t n, double *A, int64_t lda, do
     t->lda = lda;
     t->stream = (cudaStream_t)stream;
     t->cross_done = 0;
+    const bool timed = (ro.flags & 2) != 0;
+    t->ev_recorded = false;
+    if (timed)
+        for (cudaEvent_t &e : t->ev)
+            if (!e) CUDA_TRY(cudaEventCreate(&e), "tsqr_factor events");
+    auto mark = [&](int i) -> cudaError_t { return timed ? cudaEventRecord(t->ev[i], t->stream) : cudaSuccess; };
     FactorArgs f;
     f.NP = t->NP;
     f.max_rows = t->plan.max_rows;
@@ -359,9 +367,11 @@ tsqr_status_t tsqr_factor(int64_t m_local, int64_t n, double *A, int64_t lda, do
     ca.cta_tile0 = t->d_cta_tile0; ca.grid = t->chain_grid; ca.tau = t->d_tau_chunk; ca.tcache = t->d_tcache;
     if (t->wide) {
         const int L = t->plan.ntiles();
+        CUDA_TRY(mark(0), "tsqr_factor events");
         CUDA_TRY(launch_wide_leaves(A, lda, (int)n, t->d_row0, t->d_rows, L, (int)t->plan.max_rows, t->d_tau_chunk,
                                     t->d_tcache, t->stream),
                  "tsqr_factor leaves");
+        CUDA_TRY(mark(1), "tsqr_factor events");
         if (wide_tree_pipe_ok((int)n)) {
             CUDA_TRY(launch_wide_tree_pipe(A, lda, (int)n, t->d_row0, t->d_node_a, t->d_pipe_nodes, t->pipe_count,
                                            t->d_prod_l, t->d_prod_r, t->d_pipe_flags, t->d_tau_node,
@@ -377,9 +387,13 @@ tsqr_status_t tsqr_factor(int64_t m_local, int64_t n, double *A, int64_t lda, do
             }
         }
         if (R) CUDA_TRY(launch_extract_r(A, lda, (int)n, R, ldr, t->stream), "tsqr_factor R");
+        CUDA_TRY(mark(2), "tsqr_factor events");
+        t->ev_recorded = timed;
         return debug_sync(t, t->stream, "tsqr_factor");
     }
+    CUDA_TRY(mark(0), "tsqr_factor events");
     CUDA_TRY(launch_chain_factor(ca, t->stream), "tsqr_factor leaves");
+    CUDA_TRY(mark(1), "tsqr_factor events");
     if (t->pipe_count == 0) {
         if (R) CUDA_TRY(launch_extract_r(A, lda, (int)n, R, ldr, t->stream), "tsqr_factor R");
     } else {
@@ -387,6 +401,8 @@ tsqr_status_t tsqr_factor(int64_t m_local, int64_t n, double *A, int64_t lda, do
                                   t->d_prod_r, t->d_pipe_flags, t->d_tau_node, t->pipe_root, R, ldr, t->stream),
                  "tsqr_factor tree");
     }
+    CUDA_TRY(mark(2), "tsqr_factor events");
+    t->ev_recorded = timed;
     return debug_sync(t, t->stream, "tsqr_factor");
 }
 
@@ -449,7 +465,7 @@ tsqr_status_t tsqr_apply_qt(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, do
     ca.C = C; ca.ldc = ldc; ca.k = (int)k; ca.forward = 1; ca.xbuf = nullptr;
     if (t->wide) {
         const int n = (int)t->plan.n;
-        CUDA_TRY(launch_wide_apply_leaves(t->A, t->lda, n, t->d_row0, t->d_rows, t->plan.ntiles(), t->d_tcache, C,
+        CUDA_TRY(launch_wide_apply_leaves(t->A, t->lda, n, t->d_row0, t->d_rows, t->plan.ntiles(), (int)t->plan.max_rows, t->d_tcache, C,
                                           ldc, (int)k, 1, st),
                  "tsqr_apply_qt leaves");
         for (size_t g = t->step_off.size() - 1; g-- > 0;) {         // tree steps bottom-up
@@ -528,7 +544,7 @@ tsqr_status_t tsqr_form_q(tsqr_tree_t t, double *Q, int64_t ldq, void *stream) {
                      "tsqr_form_q nodes");
         }
         CUDA_TRY(launch_wide_formq_init(t->d_row0, t->d_rows, L, n, t->d_xbuf, Q, ldq, st), "tsqr_form_q");
-        CUDA_TRY(launch_wide_apply_leaves(t->A, t->lda, n, t->d_row0, t->d_rows, L, t->d_tcache, Q, ldq, n, 0, st),
+        CUDA_TRY(launch_wide_apply_leaves(t->A, t->lda, n, t->d_row0, t->d_rows, L, (int)t->plan.max_rows, t->d_tcache, Q, ldq, n, 0, st),
                  "tsqr_form_q leaves");
         t->stream = st;
         return debug_sync(t, st, "tsqr_form_q");
@@ -559,8 +575,21 @@ tsqr_status_t tsqr_form_q(tsqr_tree_t t, double *Q, int64_t ldq, void *stream) {
 tsqr_status_t tsqr_tree_free(tsqr_tree_t t) {
     if (!t) return TSQR_OK;
     if (t->stream) cudaStreamSynchronize(t->stream);
+    for (cudaEvent_t &e : t->ev)
+        if (e) cudaEventDestroy(e);
     free_tree_memory(t);
     delete t;
+    return TSQR_OK;
+}
+
+tsqr_status_t tsqr_tree_stage_ms(tsqr_tree_t t, float *leaf_ms, float *tree_ms) {
+    if (!t || !t->ev_recorded) return TSQR_ERR_INVALID;
+    CUDA_TRY(cudaEventSynchronize(t->ev[2]), "tsqr_tree_stage_ms");
+    float a = 0.f, b = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&a, t->ev[0], t->ev[1]), "tsqr_tree_stage_ms");
+    CUDA_TRY(cudaEventElapsedTime(&b, t->ev[1], t->ev[2]), "tsqr_tree_stage_ms");
+    if (leaf_ms) *leaf_ms = a;
+    if (tree_ms) *tree_ms = b;
     return TSQR_OK;
 }
 

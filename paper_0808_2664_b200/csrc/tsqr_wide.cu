@@ -299,8 +299,51 @@ __device__ void wide_apply(const Prob &P, const Prob &Cp, int n, int k, const do
 // blocks of loads in flight per lane.
 constexpr int UNR = 8;
 
+// one group of U row blocks of this lane's column of C (rows 8k+2q+{0,1})
+template <int U>
+__device__ __forceinline__ void load_grp(double (&cv)[U][2], const double *cp, bool okc, int H, int k0) {
+    const int q = threadIdx.x & 3;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int r = 8 * (k0 + u) + 2 * q;
+        cv[u][0] = (okc && r < H) ? cp[r] : 0.0;
+        cv[u][1] = (okc && r + 1 < H) ? cp[r + 1] : 0.0;
+    }
+}
+template <int U>
+__device__ __forceinline__ void w_grp(double (&w0)[2], double (&w1)[2], const double (&cv)[U][2], const double *Ys,
+                                      int nrb, int k0) {
+    const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        if (k0 + u < nrb) {
+            const int r = 8 * (k0 + u) + 2 * q;
+            dmma(w0[u & 1], w1[u & 1], cv[u][0], Ys[r * 8 + l4]);
+            dmma(w0[u & 1], w1[u & 1], cv[u][1], Ys[(r + 1) * 8 + l4]);
+        }
+    }
+}
+template <int U>
+__device__ __forceinline__ void upd_grp(double (&cv)[U][2], double *cp, bool okc, int H, const double *Ys, int nrb,
+                                        int k0, double p0, double p1) {
+    const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        if (k0 + u < nrb) {
+            const double2 y = *reinterpret_cast<const double2 *>(Ys + (8 * (k0 + u) + l4) * 8 + 2 * q);
+            dmma(cv[u][0], cv[u][1], -p0, y.x);
+            dmma(cv[u][0], cv[u][1], -p1, y.y);
+            const int r = 8 * (k0 + u) + 2 * q;
+            if (okc && r < H) cp[r] = cv[u][0];
+            if (okc && r + 1 < H) cp[r + 1] = cv[u][1];
+        }
+    }
+}
+
 // C <- (I - Y T' Y^T) C on columns [c_lo, c_hi) and rows [8 rb0, H) of C
 // (T' = T^T for Q^T, kFwd; T for Q), Y = Ys (rows >= 8 rb0 valid, zero past H).
+// Both passes over the rows are software-pipelined: the next group of UNR row
+// blocks is loaded while the current one is consumed.
 template <bool kFwd>
 __device__ __forceinline__ void apply_panel_cols(const double *Ys, const double *Tg, double *C, int64_t ldc, int H,
                                                  int rb0, int c_lo, int c_hi) {
@@ -313,55 +356,37 @@ __device__ __forceinline__ void apply_panel_cols(const double *Ys, const double 
         const bool okc = col < c_hi;
         double *cp = C + (int64_t)(okc ? col : c_lo) * ldc;
         double w0[2] = {0.0, 0.0}, w1[2] = {0.0, 0.0};
-        for (int k0 = rb0; k0 < nrb; k0 += UNR) {
-            double cv[UNR][2];
-#pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                const int r = 8 * (k0 + u) + 2 * q;
-                cv[u][0] = (okc && r < H) ? cp[r] : 0.0;
-                cv[u][1] = (okc && r + 1 < H) ? cp[r + 1] : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                if (k0 + u < nrb) {
-                    const int r = 8 * (k0 + u) + 2 * q;
-                    dmma(w0[u & 1], w1[u & 1], cv[u][0], Ys[r * 8 + l4]);
-                    dmma(w0[u & 1], w1[u & 1], cv[u][1], Ys[(r + 1) * 8 + l4]);
-                }
-            }
+        double ca[UNR][2], cb2[UNR][2];
+        load_grp<UNR>(ca, cp, okc, H, rb0);
+        for (int k0 = rb0; k0 < nrb; k0 += 2 * UNR) {
+            if (k0 + UNR < nrb) load_grp<UNR>(cb2, cp, okc, H, k0 + UNR);
+            w_grp<UNR>(w0, w1, ca, Ys, nrb, k0);
+            if (k0 + UNR >= nrb) break;
+            if (k0 + 2 * UNR < nrb) load_grp<UNR>(ca, cp, okc, H, k0 + 2 * UNR);
+            w_grp<UNR>(w0, w1, cb2, Ys, nrb, k0 + UNR);
         }
         double p0 = 0.0, p1 = 0.0;
         dmma(p0, p1, w0[0] + w0[1], tb0);
         dmma(p0, p1, w1[0] + w1[1], tb1);
-        for (int k0 = rb0; k0 < nrb; k0 += UNR) {
-            double cv[UNR][2];
-#pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                const int r = 8 * (k0 + u) + 2 * q;
-                cv[u][0] = (okc && r < H) ? cp[r] : 0.0;
-                cv[u][1] = (okc && r + 1 < H) ? cp[r + 1] : 0.0;
-            }
-#pragma unroll
-            for (int u = 0; u < UNR; ++u) {
-                if (k0 + u < nrb) {
-                    const double2 y = *reinterpret_cast<const double2 *>(Ys + (8 * (k0 + u) + l4) * 8 + 2 * q);
-                    dmma(cv[u][0], cv[u][1], -p0, y.x);
-                    dmma(cv[u][0], cv[u][1], -p1, y.y);
-                    const int r = 8 * (k0 + u) + 2 * q;
-                    if (okc && r < H) cp[r] = cv[u][0];
-                    if (okc && r + 1 < H) cp[r + 1] = cv[u][1];
-                }
-            }
+        load_grp<UNR>(ca, cp, okc, H, rb0);
+        for (int k0 = rb0; k0 < nrb; k0 += 2 * UNR) {
+            if (k0 + UNR < nrb) load_grp<UNR>(cb2, cp, okc, H, k0 + UNR);
+            upd_grp<UNR>(ca, cp, okc, H, Ys, nrb, k0, p0, p1);
+            if (k0 + UNR >= nrb) break;
+            if (k0 + 2 * UNR < nrb) load_grp<UNR>(ca, cp, okc, H, k0 + 2 * UNR);
+            upd_grp<UNR>(cb2, cp, okc, H, Ys, nrb, k0 + UNR, p0, p1);
         }
     }
 }
 
+template <int KM>
 struct LeafSmem {
     double part[2][NW][9];
     double piv[2][8];
     double Gs[64], Ts[64], t8[8];
-    double xs[NW][2][RW];
-    double Ys[MAXR * 8];
+    double xs[NW][2][8 * KM];
+    double Ys[8];              // H_pad x 8 (the launch sizes it to the tallest tile)
+    static size_t bytes(int max_rows) { return sizeof(LeafSmem) + sizeof(double) * 8 * ((max_rows + 7) / 8 * 8); }
 };
 
 // Blocked compact-WY QR of one tile (H rows, H <= 64 KM): the panel is
@@ -369,7 +394,7 @@ struct LeafSmem {
 // __syncthreads per Householder step for the cross-warp sums; T per panel;
 // the trailing update column-split (apply_panel_cols).
 template <int KM>
-__device__ void wide_leaf_qr(double *At, int64_t lda, int H, int n, double *tau, double *tcache, LeafSmem &S) {
+__device__ void wide_leaf_qr(double *At, int64_t lda, int H, int n, double *tau, double *tcache, LeafSmem<KM> &S) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
     const int npan = (n + 7) / 8;
     const int rbase = warp * 8 * KM;
@@ -494,11 +519,11 @@ using namespace wide;
 
 // Leaves: tile t (one CTA each), row-split panels sized to the tile.
 template <int KM>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, KM <= 8 ? 2 : 1)
 k_wide_leaves(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *tile_rows, double *tau_tile,
               double *tcache_tile) {
     extern __shared__ __align__(16) double smraw[];
-    LeafSmem &S = *reinterpret_cast<LeafSmem *>(smraw);
+    LeafSmem<KM> &S = *reinterpret_cast<LeafSmem<KM> *>(smraw);
     const int t = blockIdx.x;
     const int npan = (n + 7) / 8;
     wide_leaf_qr<KM>(A + tile_row0[t], lda, tile_rows[t], n, tau_tile + (int64_t)t * n,
@@ -531,15 +556,15 @@ k_wide_node1(double *Ra, int64_t lda, double *Rb, int64_t ldb, int n, double *ta
 // panel by panel (forward for Q^T, backward for Q) the panel's Y is staged in
 // shared memory from the stored factor, then the column-split update.
 template <bool kFwd>
-__global__ void __launch_bounds__(NT, 1)
+__global__ void __launch_bounds__(NT, 2)
 k_wide_apply_leaves(const double *A, int64_t lda, int n, const int64_t *tile_row0, const int *tile_rows,
                     const double *tcache_tile, double *C, int64_t ldc, int k) {
     extern __shared__ __align__(16) double smraw[];
-    double *Ys = smraw, *Ts = smraw + MAXR * 8;
     const int t = blockIdx.x;
     const int npan = (n + 7) / 8;
     const int H = tile_rows[t];
     const int Hp = 8 * ((H + 7) / 8);
+    double *Ts = smraw, *Ys = smraw + 64;
     const double *At = A + tile_row0[t];
     const double *tc = tcache_tile + (int64_t)t * npan * 64;
     for (int pp = 0; pp < npan; ++pp) {
@@ -571,6 +596,106 @@ k_wide_apply_nodes(const double *A, int64_t lda, int n, const int64_t *tile_row0
     wide_apply<kFwd>(P, Cp, n, k, tcache_node + (int64_t)b * npan * 64);
 }
 
+// Q^T / Q of one tree step's nodes for npan <= 28: the node's Y1 (upper
+// block triangle of the right subtree's head, 8x8 column-major blocks) and
+// its panels' T are staged in shared memory once; every warp then owns an
+// 8-column slab of C and runs all panels alone: C_b's head rows (n x 8) in
+// registers, C_a's row block P read and written back per panel (the identity
+// part of the node's reflectors).  No barrier after the staging.
+constexpr int NPAN_NODE = 28;
+template <bool kFwd>
+__global__ void __launch_bounds__(NT, 1)
+k_wide_apply_nodes_reg(const double *A, int64_t lda, int n, const int64_t *tile_row0, const int *node_a,
+                       const int *ids, const double *tcache_node, double *C, int64_t ldc, int k, int xbuf_mode) {
+    extern __shared__ __align__(16) double smraw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+    const int b = ids[blockIdx.x], a = node_a[b];
+    const int npan = (n + 7) / 8;
+    const int nb = npan * (npan + 1) / 2;
+    double *Yb = smraw, *Tn = smraw + 64 * nb;
+    const double *Hb = A + tile_row0[b];
+#pragma unroll 8
+    for (int e = threadIdx.x; e < 64 * nb; e += NT) {            // loads independent of each other
+        const int bi = e >> 6, cl = (e >> 3) & 7, r = e & 7;
+        int cb = (int)((sqrtf(8.0f * bi + 1.0f) - 1.0f) * 0.5f);   // bi = cb(cb+1)/2 + kk, kk <= cb
+        cb += (cb + 1) * (cb + 2) / 2 <= bi;
+        cb -= cb * (cb + 1) / 2 > bi;
+        const int kk = bi - cb * (cb + 1) / 2;
+        const int i = 8 * kk + r, c = 8 * cb + cl;
+        Yb[e] = (i <= c && c < n) ? __ldg(Hb + i + (int64_t)c * lda) : 0.0;
+    }
+    const double *tc = tcache_node + (int64_t)b * npan * 64;
+    for (int e = threadIdx.x; e < 64 * npan; e += NT) Tn[e] = tc[e];
+    __syncthreads();
+    double *Ca, *Cb;
+    int64_t ld;
+    if (xbuf_mode) {
+        Ca = C + (int64_t)a * n * n; Cb = C + (int64_t)b * n * n; ld = n;
+    } else {
+        Ca = C + tile_row0[a]; Cb = C + tile_row0[b]; ld = ldc;
+    }
+    for (int cbw = warp; 8 * cbw < k; cbw += NW) {
+        const int col = 8 * cbw + l4;
+        const bool okc = col < k;
+        const int64_t co = (int64_t)(okc ? col : 0) * ld;
+        double cb[NPAN_NODE][2];
+#pragma unroll
+        for (int kk = 0; kk < NPAN_NODE; ++kk)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int r = 8 * kk + 2 * q + e;
+                cb[kk][e] = (okc && kk < npan && r < n) ? Cb[r + co] : 0.0;
+            }
+        // C_a's row block of the next panel is prefetched one panel ahead
+        const int P0 = kFwd ? 0 : npan - 1;
+        double na0 = (okc && 8 * P0 + 2 * q < n) ? Ca[8 * P0 + 2 * q + co] : 0.0;
+        double na1 = (okc && 8 * P0 + 2 * q + 1 < n) ? Ca[8 * P0 + 2 * q + 1 + co] : 0.0;
+        for (int pp = 0; pp < npan; ++pp) {
+            const int P = kFwd ? pp : npan - 1 - pp;
+            const double *Tg = Tn + 64 * P;
+            const double tb0 = kFwd ? Tg[(2 * q) * 8 + l4] : Tg[l4 * 8 + 2 * q];
+            const double tb1 = kFwd ? Tg[(2 * q + 1) * 8 + l4] : Tg[l4 * 8 + 2 * q + 1];
+            const int ra = 8 * P + 2 * q;
+            const double ca0 = na0, ca1 = na1;
+            if (pp + 1 < npan) {
+                const int rn = 8 * (kFwd ? P + 1 : P - 1) + 2 * q;
+                na0 = (okc && rn < n) ? Ca[rn + co] : 0.0;
+                na1 = (okc && rn + 1 < n) ? Ca[rn + 1 + co] : 0.0;
+            }
+            const double *yP = Yb + 64 * (P * (P + 1) / 2);           // block (0, P); block (kk, P) at + 64 kk
+            double w0[2] = {0.0, 0.0}, w1[2] = {0.0, 0.0};
+#pragma unroll
+            for (int kk = 0; kk < NPAN_NODE; ++kk) {
+                if (kk <= P) {
+                    const double2 y = *reinterpret_cast<const double2 *>(yP + 64 * kk + 8 * l4 + 2 * q);
+                    dmma(w0[kk & 1], w1[kk & 1], cb[kk][0], y.x);
+                    dmma(w0[kk & 1], w1[kk & 1], cb[kk][1], y.y);
+                }
+            }
+            double p0 = 0.0, p1 = 0.0;
+            dmma(p0, p1, w0[0] + w0[1] + ca0, tb0);
+            dmma(p0, p1, w1[0] + w1[1] + ca1, tb1);
+            if (okc && ra < n) Ca[ra + co] = ca0 - p0;
+            if (okc && ra + 1 < n) Ca[ra + 1 + co] = ca1 - p1;
+#pragma unroll
+            for (int kk = 0; kk < NPAN_NODE; ++kk) {
+                if (kk <= P) {
+                    const double *yb = yP + 64 * kk;
+                    dmma(cb[kk][0], cb[kk][1], -p0, yb[8 * (2 * q) + l4]);
+                    dmma(cb[kk][0], cb[kk][1], -p1, yb[8 * (2 * q + 1) + l4]);
+                }
+            }
+        }
+#pragma unroll
+        for (int kk = 0; kk < NPAN_NODE; ++kk)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int r = 8 * kk + 2 * q + e;
+                if (okc && kk < npan && r < n) Cb[r + co] = cb[kk][e];
+            }
+    }
+}
+
 // One stacked node's reflectors (Y1 in Rb-storage, ld ldy) applied to [Ca; Cb].
 template <bool kFwd>
 __global__ void __launch_bounds__(NT, 1)
@@ -600,26 +725,26 @@ static cudaError_t wide_attr(const void *fn) {
 }
 int wide_max_rows() { return MAXR; }
 
-static size_t leaf_smem() { return sizeof(LeafSmem); }
-static size_t apply_leaf_smem() { return sizeof(double) * (MAXR * 8 + 64); }
+static size_t apply_leaf_smem(int max_rows) { return sizeof(double) * (8 * ((max_rows + 7) / 8 * 8) + 64); }
 
 template <int KM>
 static cudaError_t launch_leaves_km(double *A, int64_t lda, int n, const int64_t *row0, const int *rows, int L,
-                                   double *tau, double *tcache, cudaStream_t st) {
+                                   int max_rows, double *tau, double *tcache, cudaStream_t st) {
+    const size_t bytes = LeafSmem<KM>::bytes(max_rows);
     cudaError_t e = cudaFuncSetAttribute((const void *)k_wide_leaves<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)leaf_smem());
+                                         (int)bytes);
     if (e != cudaSuccess) return e;
-    k_wide_leaves<KM><<<L, NT, leaf_smem(), st>>>(A, lda, n, row0, rows, tau, tcache);
+    k_wide_leaves<KM><<<L, NT, bytes, st>>>(A, lda, n, row0, rows, tau, tcache);
     return cudaGetLastError();
 }
 
 // max_rows: the tallest tile (selects the per-warp row range, 64 KM >= max_rows)
 cudaError_t launch_wide_leaves(double *A, int64_t lda, int n, const int64_t *row0, const int *rows, int L,
                                int max_rows, double *tau, double *tcache, cudaStream_t st) {
-    if (max_rows <= 512) return launch_leaves_km<8>(A, lda, n, row0, rows, L, tau, tcache, st);
-    if (max_rows <= 1024) return launch_leaves_km<16>(A, lda, n, row0, rows, L, tau, tcache, st);
-    if (max_rows <= 1536) return launch_leaves_km<24>(A, lda, n, row0, rows, L, tau, tcache, st);
-    return launch_leaves_km<KMW>(A, lda, n, row0, rows, L, tau, tcache, st);
+    if (max_rows <= 512) return launch_leaves_km<8>(A, lda, n, row0, rows, L, max_rows, tau, tcache, st);
+    if (max_rows <= 1024) return launch_leaves_km<16>(A, lda, n, row0, rows, L, max_rows, tau, tcache, st);
+    if (max_rows <= 1536) return launch_leaves_km<24>(A, lda, n, row0, rows, L, max_rows, tau, tcache, st);
+    return launch_leaves_km<KMW>(A, lda, n, row0, rows, L, max_rows, tau, tcache, st);
 }
 
 cudaError_t launch_wide_nodes(double *A, int64_t lda, int n, const int64_t *row0, const int *node_a, const int *ids,
@@ -639,19 +764,34 @@ cudaError_t launch_wide_node1(double *Ra, int64_t lda, double *Rb, int64_t ldb, 
 }
 
 cudaError_t launch_wide_apply_leaves(const double *A, int64_t lda, int n, const int64_t *row0, const int *rows,
-                                     int L, const double *tcache, double *C, int64_t ldc, int k, int forward,
-                                     cudaStream_t st) {
+                                     int L, int max_rows, const double *tcache, double *C, int64_t ldc, int k,
+                                     int forward, cudaStream_t st) {
+    const size_t bytes = apply_leaf_smem(max_rows);
     const void *fn = forward ? (const void *)k_wide_apply_leaves<true> : (const void *)k_wide_apply_leaves<false>;
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)apply_leaf_smem());
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;
-    if (forward) k_wide_apply_leaves<true><<<L, NT, apply_leaf_smem(), st>>>(A, lda, n, row0, rows, tcache, C, ldc, k);
-    else k_wide_apply_leaves<false><<<L, NT, apply_leaf_smem(), st>>>(A, lda, n, row0, rows, tcache, C, ldc, k);
+    if (forward) k_wide_apply_leaves<true><<<L, NT, bytes, st>>>(A, lda, n, row0, rows, tcache, C, ldc, k);
+    else k_wide_apply_leaves<false><<<L, NT, bytes, st>>>(A, lda, n, row0, rows, tcache, C, ldc, k);
     return cudaGetLastError();
 }
 
 cudaError_t launch_wide_apply_nodes(const double *A, int64_t lda, int n, const int64_t *row0, const int *node_a,
                                     const int *ids, int count, const double *tcache_node, double *C, int64_t ldc,
                                     int k, int forward, int xbuf_mode, cudaStream_t st) {
+    const int npan = (n + 7) / 8;
+    if (npan <= NPAN_NODE) {
+        const size_t bytes = sizeof(double) * 64 * (npan * (npan + 1) / 2 + npan);
+        const void *fn = forward ? (const void *)k_wide_apply_nodes_reg<true> : (const void *)k_wide_apply_nodes_reg<false>;
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        if (e != cudaSuccess) return e;
+        if (forward)
+            k_wide_apply_nodes_reg<true><<<count, NT, bytes, st>>>(A, lda, n, row0, node_a, ids, tcache_node, C, ldc, k,
+                                                                   xbuf_mode);
+        else
+            k_wide_apply_nodes_reg<false><<<count, NT, bytes, st>>>(A, lda, n, row0, node_a, ids, tcache_node, C, ldc,
+                                                                    k, xbuf_mode);
+        return cudaGetLastError();
+    }
     if (forward)
         k_wide_apply_nodes<true><<<count, NT, 0, st>>>(A, lda, n, row0, node_a, ids, tcache_node, C, ldc, k, xbuf_mode);
     else

@@ -25,10 +25,14 @@ from . import api
 
 
 class CudaEngine:
-    """The product engine: every step is a libtsqr.so call on the current stream."""
+    """The product engine: every step is a libtsqr.so call on the current stream.
+    stage_timing: record device events around the local leaf / tree stages (Tree.stage_ms)."""
+
+    def __init__(self, stage_timing: bool = False):
+        self.stage_timing = stage_timing
 
     def factor_local(self, A, block_rows, tile_rows, nranks, rank):
-        return api.factor(A, block_rows, tile_rows, nranks=nranks, rank=rank)
+        return api.factor(A, block_rows, tile_rows, nranks=nranks, rank=rank, stage_timing=self.stage_timing)
 
     def empty(self, shape, like):
         return torch.empty(shape, dtype=torch.float64, device=like.device)
