@@ -1,0 +1,51 @@
+"""Key counters of one kernel in an ncu --set full report, as text for profiles/ (tools only).
+usage: python tools/ncu_summary.py report.ncu-rep [label]"""
+import csv
+import io
+import subprocess
+import sys
+
+KEYS = [
+    ("gpu__time_duration.sum", "duration"),
+    ("dram__bytes_read.sum", "DRAM read"),
+    ("dram__bytes_write.sum", "DRAM write"),
+    ("dram__throughput.avg.pct_of_peak_sustained_elapsed", "DRAM throughput % of peak"),
+    ("lts__t_bytes.sum", "L2 bytes"),
+    ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe active % (active cycles)"),
+    ("sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active", "DMMA subpipe active %"),
+    ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput % (elapsed)"),
+    ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
+    ("launch__grid_size", "grid"),
+    ("launch__block_size", "block"),
+    ("launch__registers_per_thread", "registers/thread"),
+    ("launch__shared_mem_per_block_dynamic", "dynamic smem/block"),
+    ("launch__occupancy_limit_registers", "occupancy limit (registers)"),
+    ("smsp__average_warps_issue_stalled_wait_per_issue_active.ratio", "stall wait / issue"),
+    ("smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio", "stall long_scoreboard / issue"),
+    ("smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio", "stall short_scoreboard / issue"),
+    ("smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio", "stall barrier / issue"),
+    ("smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio", "stall math throttle / issue"),
+]
+
+
+def main():
+    rep = sys.argv[1]
+    label = sys.argv[2] if len(sys.argv) > 2 else rep
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h, units = rows[0], rows[1]
+    print(label)
+    for r in rows[2:]:
+        name = r[h.index("Kernel Name")]
+        print(f"kernel: {name}")
+        for key, desc in KEYS:
+            if key in h:
+                i = h.index(key)
+                print(f"  {desc:36s} {r[i]:>16s} {units[i]}   ({key})")
+        rd = h.index("dram__bytes_read.sum")
+        wr = h.index("dram__bytes_write.sum")
+        print(f"  DRAM read + write per launch: {r[rd]} + {r[wr]} {units[rd]}")
+
+
+if __name__ == "__main__":
+    main()
