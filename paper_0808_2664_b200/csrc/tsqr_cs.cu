@@ -139,7 +139,12 @@ k_cs_factor(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *
 template <class C>
 struct ApplyCs {
     static constexpr int NW = 8, NT = 256;
-    static constexpr int YS = C::CH * C::NP + C::NCB * 64;     // Y (row-major CH x NP) + T's
+    // Y twice, so that both DMMA operand reads are bank-conflict free: row-major Yr (CH x NP,
+    // row stride LDY = NP + 2) for W^T = C^T Y (rows 2q+e, column l4 of a lane) and column-major
+    // Yt (NP x CH, stride LDT = CH + 2) for C -= Y W' (rows l4, columns 2q+e); then the T's
+    static constexpr int LDY = C::NP + 2, LDT = C::CH + 2;
+    static constexpr int OFF_YT = C::CH * LDY, OFF_T = OFF_YT + C::NP * LDT;
+    static constexpr int YS = OFF_T + C::NCB * 64;
     static constexpr size_t BYTES = (size_t)2 * YS * sizeof(double);
 };
 
@@ -157,27 +162,33 @@ __device__ __forceinline__ void stage_chunk(double *slot, const double *Ak, int6
     for (int i = threadIdx.x; i < C::CH * C::NP; i += blockDim.x) {
         const int col = i / C::CH, row = i % C::CH;
         const bool ok = row < hk && col < n && row > col - r0;
-        cp8(slot + row * C::NP + col, Ak + row + (int64_t)(ok ? col : 0) * lda, ok);
+        const double *src = Ak + row + (int64_t)(ok ? col : 0) * lda;
+        cp8(slot + row * ApplyCs<C>::LDY + col, src, ok);
+        cp8(slot + ApplyCs<C>::OFF_YT + col * ApplyCs<C>::LDT + row, src, ok);
     }
-    for (int i = threadIdx.x; i < C::NCB * 64; i += blockDim.x) cp8(slot + C::CH * C::NP + i, tch + i, true);
+    for (int i = threadIdx.x; i < C::NCB * 64; i += blockDim.x) cp8(slot + ApplyCs<C>::OFF_T + i, tch + i, true);
     asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 template <class C>
 __device__ __forceinline__ void fix_dense(double *slot, int n, int r0) {
     for (int c = threadIdx.x; c < C::NP; c += blockDim.x)
-        if (c < n && c >= r0 && c < r0 + C::CH) slot[(c - r0) * C::NP + c] = 1.0;
+        if (c < n && c >= r0 && c < r0 + C::CH) {
+            slot[(c - r0) * ApplyCs<C>::LDY + c] = 1.0;
+            slot[ApplyCs<C>::OFF_YT + c * ApplyCs<C>::LDT + (c - r0)] = 1.0;
+        }
 }
 
 template <class C, bool kFwd>
 __device__ __forceinline__ void cs_apply_panel(double (&cc)[C::KM][2], double (&cr)[C::NCB][2], int p, int r0,
                                                const double *slot) {
     const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
-    constexpr int KM = C::KM, NP = C::NP;
+    constexpr int KM = C::KM, NP = ApplyCs<C>::LDY, LDT = ApplyCs<C>::LDT;   // Yr / Yt strides
     if (8 * p >= r0 + C::CH) return;           // no reflector of panel p in this chunk
     const bool dense = 8 * p >= r0;            // pivots inside the chunk: row block kb
     const int kb = dense ? (8 * p - r0) >> 3 : -1;
     const double *ys = slot + 8 * p;
-    const double *Tg = slot + C::CH * NP + 64 * p;
+    const double *Tg = slot + ApplyCs<C>::OFF_T + 64 * p;
+    const double *yt = slot + ApplyCs<C>::OFF_YT + 8 * p * LDT;       // Yt column 8p
     double crp0 = 0.0, crp1 = 0.0;
 #pragma unroll
     for (int i = 0; i < C::NCB; ++i) {
@@ -214,7 +225,7 @@ __device__ __forceinline__ void cs_apply_panel(double (&cc)[C::KM][2], double (&
     }
 #pragma unroll
     for (int k = 0; k < KM; ++k) {
-        const double y0 = ys[(8 * k + l4) * NP + 2 * q], y1 = ys[(8 * k + l4) * NP + 2 * q + 1];
+        const double y0 = yt[(2 * q) * LDT + 8 * k + l4], y1 = yt[(2 * q + 1) * LDT + 8 * k + l4];
         dmma(cc[k][0], cc[k][1], -p0, y0);
         dmma(cc[k][0], cc[k][1], -p1, y1);
     }
