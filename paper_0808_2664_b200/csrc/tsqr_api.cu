@@ -274,10 +274,8 @@ static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t 
     alloc((void **)&t->d_tau_chunk, sizeof(double) * nchunks * n);
     const int ncb_cache = t->wide ? t->npan : chain_ncb((int)n);
     alloc((void **)&t->d_tcache, sizeof(double) * nchunks * ncb_cache * 64);
-    if (t->wide) {
-        alloc((void **)&t->d_tcache_node, sizeof(double) * L * t->npan * 64);
-        alloc((void **)&t->d_cross_tcache, sizeof(double) * (ilog2(ro.nranks) + 1) * t->npan * 64);
-    }
+    alloc((void **)&t->d_tcache_node, sizeof(double) * L * t->npan * 64);    // node panel T's (both engines)
+    if (t->wide) alloc((void **)&t->d_cross_tcache, sizeof(double) * (ilog2(ro.nranks) + 1) * t->npan * 64);
     t->nchunks = nchunks;
     if (e != cudaSuccess) {
         free_tree_memory(t);
@@ -354,13 +352,6 @@ tsqr_status_t tsqr_factor(int64_t m_local, int64_t n, double *A, int64_t lda, do
         for (cudaEvent_t &e : t->ev)
             if (!e) CUDA_TRY(cudaEventCreate(&e), "tsqr_factor events");
     auto mark = [&](int i) -> cudaError_t { return timed ? cudaEventRecord(t->ev[i], t->stream) : cudaSuccess; };
-    FactorArgs f;
-    f.NP = t->NP;
-    f.max_rows = t->plan.max_rows;
-    f.A = A; f.lda = lda; f.n = (int)n;
-    f.plan = t->dplan;
-    f.tau_tile = t->d_tau_tile; f.tau_node = t->d_tau_node; f.counters = t->d_counters;
-    f.R = R; f.ldr = ldr;
     ChainArgs ca;
     ca.A = A; ca.lda = lda; ca.n = (int)n; ca.chunk_rows = t->plan.c;
     ca.tile_row0 = t->d_row0; ca.tile_rows = t->d_rows; ca.tile_chunk0 = t->d_tile_chunk0;
@@ -398,7 +389,8 @@ tsqr_status_t tsqr_factor(int64_t m_local, int64_t n, double *A, int64_t lda, do
         if (R) CUDA_TRY(launch_extract_r(A, lda, (int)n, R, ldr, t->stream), "tsqr_factor R");
     } else {
         CUDA_TRY(launch_tree_pipe(A, lda, (int)n, t->d_row0, t->d_node_a, t->d_pipe_nodes, t->pipe_count, t->d_prod_l,
-                                  t->d_prod_r, t->d_pipe_flags, t->d_tau_node, t->pipe_root, R, ldr, t->stream),
+                                  t->d_prod_r, t->d_pipe_flags, t->d_tau_node, t->pipe_root, R, ldr,
+                                  t->d_tcache_node, t->stream),
                  "tsqr_factor tree");
     }
     CUDA_TRY(mark(2), "tsqr_factor events");
@@ -449,14 +441,6 @@ tsqr_status_t tsqr_apply_qt(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, do
     if (k == 0) return TSQR_OK;
     if (!C || ldc < t->plan.m_local) return TSQR_ERR_INVALID;
     if (top && ldtop < t->plan.n) return TSQR_ERR_INVALID;
-    ApplyArgs f;
-    f.NP = t->NP;
-    f.max_rows = t->plan.max_rows;
-    f.A = t->A; f.lda = t->lda; f.n = (int)t->plan.n;
-    f.plan = t->dplan;
-    f.tau_tile = t->d_tau_tile; f.tau_node = t->d_tau_node; f.counters = t->d_counters;
-    f.C = C; f.ldc = ldc; f.k = (int)k;
-    f.form_q = 0; f.xbuf = nullptr;
     cudaStream_t st = (cudaStream_t)stream;
     ChainApplyArgs ca;
     ca.A = t->A; ca.lda = t->lda; ca.n = (int)t->plan.n; ca.chunk_rows = t->plan.c;
@@ -477,7 +461,14 @@ tsqr_status_t tsqr_apply_qt(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, do
         }
     } else {
         CUDA_TRY(launch_cs_apply(ca, st), "tsqr_apply_qt leaves");
-        if (t->plan.ntiles() > 1) CUDA_TRY(launch_apply_nodes(f, st), "tsqr_apply_qt nodes");
+        for (size_t g = t->step_off.size() - 1; g-- > 0;) {         // tree steps bottom-up
+            const int cnt = t->step_off[g + 1] - t->step_off[g];
+            if (cnt == 0) continue;
+            CUDA_TRY(launch_wide_apply_nodes(t->A, t->lda, (int)t->plan.n, t->d_row0, t->d_node_a,
+                                             t->d_step_ids + t->step_off[g], cnt, t->d_tcache_node, C, ldc, (int)k, 1,
+                                             0, st),
+                     "tsqr_apply_qt nodes");
+        }
     }
     if (top) CUDA_TRY(launch_copy_block(C, ldc, top, ldtop, (int)t->plan.n, (int)k, st), "tsqr_apply_qt top");
     t->stream = st;
@@ -550,16 +541,18 @@ tsqr_status_t tsqr_form_q(tsqr_tree_t t, double *Q, int64_t ldq, void *stream) {
         return debug_sync(t, st, "tsqr_form_q");
     }
     // root X of this rank: I (one GPU) or the butterfly path (no communication)
+    // the node stages read X_b = 0 below every subtree's X ([X; 0])
+    if (L > 1) CUDA_TRY(cudaMemsetAsync(t->d_xbuf, 0, sizeof(double) * (size_t)L * n * n, st), "tsqr_form_q");
     if (t->cross_rounds == 0) CUDA_TRY(launch_identity(t->d_xbuf, n, st), "tsqr_form_q identity");
     else
         CUDA_TRY(launch_cross_root_x(t->NP, t->d_cross_y1, t->d_cross_tau, t->cross_rounds, t->opts.rank, n,
                                      t->d_xbuf, st),
                  "tsqr_form_q root");
-    for (size_t g = 0; g + 1 < t->step_off.size(); ++g) {
+    for (size_t g = 0; g + 1 < t->step_off.size(); ++g) {         // tree steps top-down
         const int cnt = t->step_off[g + 1] - t->step_off[g];
         if (cnt == 0) continue;
-        CUDA_TRY(launch_formq_nodes(t->NP, t->A, t->lda, n, t->dplan, t->d_tau_node,
-                                    t->d_step_ids + t->step_off[g], cnt, t->d_xbuf, st),
+        CUDA_TRY(launch_wide_apply_nodes(t->A, t->lda, n, t->d_row0, t->d_node_a, t->d_step_ids + t->step_off[g],
+                                         cnt, t->d_tcache_node, t->d_xbuf, n, n, 0, 1, st),
                  "tsqr_form_q nodes");
     }
     ChainApplyArgs ca;

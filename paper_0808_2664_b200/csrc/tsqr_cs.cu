@@ -1,127 +1,13 @@
-// Leaf-stage factor kernel on the column-split chunk engine (cs.cuh).  Product code.
-//
-//  k_cs_factor  (a2)+(a3)+(a6 per tile): persistent CTAs of NGRP groups of NG
-//      warps; CTA i owns a contiguous run of tiles, group g takes every NGRP-th
-//      of them; a group walks its tiles' chunks in order (the flat chain), its
-//      warps splitting every chunk's columns.  The last chunk of a tile writes
-//      the tile's R into the upper triangle of the tile's head rows.
+// Leaf stage of the apply / form-Q kernels (a7, a10) on the chunk-chain
+// factor's representation (chunk.cuh).  Product code.
 #include "tsqr_kernels.h"
-#include "cs.cuh"
+#include "chunk.cuh"
 
 #include <algorithm>
 #include <vector>
 
 namespace tsqr {
-using namespace cs;
-
-// With one column block per warp (NG = NCB), warp W of a group owns block W
-// of every chunk: it applies Y_0 .. Y_{W-1} of the chunk to its block as they
-// are published, then factors panel W and publishes Y_W, T_W.
-template <class C, bool kDense>
-__device__ __forceinline__ void cs_warp_chunk(Regs<C> &rg, int W, int s, double *Rb, double *Ybase, int *ready,
-                                              int *done, double *ws, double *tau_out, double *tg, int n) {
-    const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
-#pragma unroll 1
-    for (int P = 0; P < W; ++P) {
-        wait_ge(ready + P, s + 1);
-        apply_block<C, kDense>(rg, P, Ybase + P * C::YSLOT, Rb, W);
-        if (kDense) rows_to_r<C>(rg, P, Rb, W);        // chunk rows 8P.. of block W are R rows now
-        bump(done + P);
-    }
-    double *ys = Ybase + W * C::YSLOT;
-    double *Gs = ws + C::GS, *t8 = ws + C::T8, *Ts = ws + C::TS, *xs = ws + C::XS;
-    wait_ge(done + W, s * (C::NCB - 1 - W));           // the slot's previous Y_W has been applied everywhere
-    panel_steps<C, kDense>(rg, W, Rb, Gs, t8, xs);
-    build_t(Gs, t8, Ts);
-    // publish Y_W (unit diagonal and zeros above it for a dense panel) and T_W
-#pragma unroll
-    for (int k = 0; k < C::KM; ++k)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-            const int r = 8 * k + 2 * q + e;
-            double y = rg.a[k][0][e];
-            if (kDense) y = (k > W || (k == W && 2 * q + e > l4)) ? y : ((k == W && 2 * q + e == l4) ? 1.0 : 0.0);
-            ys[r * 8 + l4] = y;
-        }
-    *reinterpret_cast<double2 *>(ys + C::CH * 8 + 2 * lane) = *reinterpret_cast<const double2 *>(Ts + 2 * lane);
-    if (tg != nullptr)
-        *reinterpret_cast<double2 *>(tg + W * 64 + 2 * lane) = *reinterpret_cast<const double2 *>(Ts + 2 * lane);
-    if (lane < 8 && 8 * W + lane < n) tau_out[8 * W + lane] = t8[lane];
-    if (kDense) rows_to_r<C>(rg, W, Rb, W);            // chunk rows 8W.. are R rows from here on
-    publish(ready + W, s + 1);
-}
-
-template <class C>
-__global__ void __launch_bounds__(C::NT, 1)
-k_cs_factor(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *tile_rows,
-            const int64_t *tile_chunk0, const int *cta_tile0, double *tau, double *tcache) {
-    extern __shared__ __align__(16) double sm[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int q = lane & 3, l4 = lane >> 2;
-    const int grp = warp / C::NG, wl = warp % C::NG;
-    double *Rb = sm + C::OFF_R + grp * C::RBUF;
-    double *Ybase = sm + C::OFF_Y + grp * C::NCB * C::YSLOT;
-    double *ws = sm + C::OFF_W + warp * C::WSCR;
-    int *sync = reinterpret_cast<int *>(sm + C::OFF_SYNC);
-    for (int i = threadIdx.x; i < C::NGRP * 2 * C::NCB; i += C::NT) sync[i] = 0;
-    __syncthreads();
-    int *ready = sync + grp * 2 * C::NCB, *done = ready + C::NCB;
-    const int tb = cta_tile0[blockIdx.x], te = cta_tile0[blockIdx.x + 1];
-    int s = 0;
-    for (int t = tb + grp; t < te; t += C::NGRP) {
-        const int h = tile_rows[t];
-        const int nch = (h + C::CH - 1) / C::CH;
-        const int64_t row0 = tile_row0[t];
-        for (int c = 0; c < nch; ++c, ++s) {
-            const int r0 = c * C::CH, hk = min(C::CH, h - r0);
-            Regs<C> rg;
-            const double *src = A + row0 + r0;
-#pragma unroll
-            for (int j = 0; j < C::NBW; ++j) {
-                const int b = C::blk(wl, j);
-                const int col = 8 * b + l4;
-                const bool okc = b >= 0 && col < n;
-                const double *pc = src + (int64_t)(okc ? col : 0) * lda;
-#pragma unroll
-                for (int k = 0; k < C::KM; ++k) {
-                    const int r = 8 * k + 2 * q;
-                    rg.a[k][j][0] = (okc && r < hk) ? __ldg(pc + r) : 0.0;
-                    rg.a[k][j][1] = (okc && r + 1 < hk) ? __ldg(pc + r + 1) : 0.0;
-                }
-            }
-            double *tau_out = tau + (tile_chunk0[t] + c) * n;
-            double *tg = tcache ? tcache + (tile_chunk0[t] + c) * (C::NCB * 64) : nullptr;
-            static_assert(C::NG == C::NCB && C::NBW == 1, "one column block per warp");
-            if (c == 0) cs_warp_chunk<C, true>(rg, wl, s, Rb, Ybase, ready, done, ws, tau_out, tg, n);
-            else cs_warp_chunk<C, false>(rg, wl, s, Rb, Ybase, ready, done, ws, tau_out, tg, n);
-            double *dst = A + row0 + r0;
-#pragma unroll
-            for (int j = 0; j < C::NBW; ++j) {
-                const int b = C::blk(wl, j);
-                const int col = 8 * b + l4;
-                if (b < 0 || col >= n) continue;
-#pragma unroll
-                for (int k = 0; k < C::KM; ++k)
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int r = 8 * k + 2 * q + e;
-                        if (r < hk && r0 + r > col) dst[r + (int64_t)col * lda] = rg.a[k][j][e];
-                    }
-            }
-            if (c == nch - 1) {                        // the tile's R (my columns) -> its head rows
-                __syncwarp();
-                for (int j = 0; j < C::NBW; ++j) {
-                    const int b = C::blk(wl, j);
-                    if (b < 0) continue;
-                    for (int e = lane; e < 8 * C::NP; e += 32) {
-                        const int i = e % C::NP, col = 8 * b + e / C::NP;
-                        if (i <= col && col < n) A[row0 + i + (int64_t)col * lda] = Rb[i * C::LDR + col];
-                    }
-                }
-            }
-        }
-    }
-}
+using namespace chunk;
 
 // ============================================================ apply / form Q
 // k_cs_apply<C, kFwd>: the leaf stage of C <- Q^T C (kFwd, (a7)) or of the
@@ -364,66 +250,6 @@ k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const 
 }
 
 // ================================================================= launchers
-template <class C>
-static cudaError_t cs_setup(size_t *bytes) {
-    *bytes = C::BYTES;
-    return cudaFuncSetAttribute((const void *)k_cs_factor<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)C::BYTES);
-}
-
-template <class F>
-static cudaError_t cs_dispatch(int n, F &&fn) {
-    const int ncb = (n + 7) / 8;
-    switch (ncb) {
-        case 1: case 2: return fn(Cfg<2, 32, 2, 4>());
-        case 3: case 4: return fn(Cfg<4, 32, 4, 2>());
-        case 5: case 6: return fn(Cfg<6, 32, 6, 1>());
-        case 7: return fn(Cfg<7, 32, 7, 1>());
-        default: return fn(Cfg<8, 32, 8, 1>());
-    }
-}
-
-int cs_chunk_rows(int n) {
-    int ch = 0;
-    cs_dispatch(n, [&](auto c) {
-        ch = decltype(c)::CH;
-        return cudaSuccess;
-    });
-    return ch;
-}
-int cs_ncb(int n) {
-    int v = 0;
-    cs_dispatch(n, [&](auto c) {
-        v = decltype(c)::NCB;
-        return cudaSuccess;
-    });
-    return v;
-}
-
-int cs_grid(int n) {
-    int dev = 0, sms = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cs_dispatch(n, [&](auto c) {
-        using C = decltype(c);
-        size_t b;
-        cudaError_t r = cs_setup<C>(&b);
-        if (r != cudaSuccess) return r;
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cs_factor<C>, C::NT, b);
-    });
-    if (e != cudaSuccess || occ < 1) occ = 1;
-    return sms * occ;
-}
-
-int cs_groups(int n) {
-    int g = 1;
-    cs_dispatch(n, [&](auto c) {
-        g = decltype(c)::NGRP;
-        return cudaSuccess;
-    });
-    return g;
-}
-
 // The apply kernel on the chain factor's representation (chunk.cuh, 32-row chunks).
 template <class F>
 static cudaError_t chain_cfg_dispatch(int n, F &&fn) {
@@ -464,18 +290,6 @@ cudaError_t launch_cs_apply(const ChainApplyArgs &f, cudaStream_t st) {
         const int nw = f.k >= 64 ? 8 : (f.k + 7) / 8;           // one warp per 8-column slab
         kern<<<f.grid, 32 * (nw < 1 ? 1 : nw), AC::BYTES, st>>>(f.A, f.lda, f.n, f.tile_row0, f.tile_rows, f.tile_chunk0, f.cta_tile0,
                                                 f.tcache, f.C, f.ldc, f.k, f.xbuf);
-        return cudaGetLastError();
-    });
-}
-
-cudaError_t launch_cs_factor(const ChainArgs &f, cudaStream_t st) {
-    return cs_dispatch(f.n, [&](auto c) {
-        using C = decltype(c);
-        size_t sm;
-        cudaError_t e = cs_setup<C>(&sm);
-        if (e != cudaSuccess) return e;
-        k_cs_factor<C><<<f.grid, C::NT, sm, st>>>(f.A, f.lda, f.n, f.tile_row0, f.tile_rows, f.tile_chunk0,
-                                                  f.cta_tile0, f.tau, f.tcache);
         return cudaGetLastError();
     });
 }

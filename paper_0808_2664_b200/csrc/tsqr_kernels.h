@@ -16,30 +16,6 @@ struct DevPlan {
     int L;                      // tiles
 };
 
-// Rows one team holds for the tallest tile of a plan (64, 96, 128 or 192).
-int team_rows_for(int64_t max_rows);
-
-struct FactorArgs {
-    int NP = 64;                 // n padded to 16/32/64 (<= 32: one column warp)
-    int64_t max_rows = 0;        // tallest tile
-    double *A; int64_t lda; int n;
-    DevPlan plan;
-    double *tau_tile, *tau_node; int *counters;
-    double *R; int64_t ldr;
-};
-
-struct ApplyArgs {
-    int NP = 64;
-    int64_t max_rows = 0;
-    const double *A; int64_t lda; int n;
-    DevPlan plan;
-    const double *tau_tile, *tau_node; int *counters;
-    double *C; int64_t ldc; int k;
-    int form_q;                  // 1: form-Q leaf stage (C := Q, n columns) from xbuf
-    const double *xbuf;
-};
-
-cudaError_t launch_factor(const FactorArgs &f, cudaStream_t st);
 
 // Leaf stage on the chunk engine (tsqr_chain.cu).
 struct ChainArgs {
@@ -96,27 +72,19 @@ cudaError_t launch_wide_cross_apply(const double *Y1, const double *tcache, doub
                                     double *tmp, cudaStream_t st);
 cudaError_t launch_wide_cross_root_x(const double *Y1s, const double *tcaches, int64_t tstride, int rounds, int rank,
                                      int n, double *tmp, double *X0, cudaStream_t st);
-// Column-split factor (tsqr_cs.cu, 256-row chunks; kept for experiments).
-int cs_grid(int n);
-cudaError_t launch_cs_factor(const ChainArgs &f, cudaStream_t st);
+// Balanced contiguous split of the tiles over `grid` persistent CTAs by chunk count.
 void chain_partition(const std::vector<int64_t> &tile_rows, int chunk_rows, int grid, std::vector<int> &cta_tile0);
-// Tree stage only (ticketed climb from every tile), after launch_chain_factor.
-cudaError_t launch_tree(const FactorArgs &f, cudaStream_t st);
 // Pipelined node combines for n <= 64 (tsqr_tree.cu): nodes (ids, bottom-up),
 // prod_l/prod_r = producing node of each child (-1: leaf), flags L x NCB ints.
 cudaError_t launch_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *node_a,
                              const int *nodes, int count, const int *prod_l, const int *prod_r, int *flags,
-                             double *tau_node, int root, double *R, int64_t ldr, cudaStream_t st);
+                             double *tau_node, int root, double *R, int64_t ldr, double *tcache_node,
+                             cudaStream_t st);
 // The same for 64 < n <= 224: one CTA per node (flags L x 28 ints).
 bool wide_tree_pipe_ok(int n);
 cudaError_t launch_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *node_a,
                                   const int *nodes, int count, const int *prod_l, const int *prod_r, int *flags,
                                   double *tau_node, double *tcache_node, cudaStream_t st);
-cudaError_t launch_apply(const ApplyArgs &f, cudaStream_t st);
-cudaError_t launch_apply_nodes(const ApplyArgs &f, cudaStream_t st);
-cudaError_t launch_formq_nodes(int NP, const double *A, int64_t lda, int n, const DevPlan &plan,
-                               const double *tau_node, const int *ids, int count, double *xbuf,
-                               cudaStream_t st);
 cudaError_t launch_identity(double *X, int n, cudaStream_t st);
 cudaError_t launch_pack_r(const double *A, int64_t lda, int n, double *packed, cudaStream_t st);
 cudaError_t launch_copy_block(const double *src, int64_t lds, double *dst, int64_t ldd, int n, int k,

@@ -53,7 +53,7 @@ __device__ __forceinline__ void wait_flag(const int *f) {
 template <class C, int P>
 __device__ __forceinline__ void node_panel(NodeRegs<C> &rg, double *Ahead_a, double *Ahead_b, int64_t lda, int n,
                                            double *ws, double *tau_out, const int *fl, const int *fr, int *fme,
-                                           double *R, int64_t ldr) {
+                                           double *R, int64_t ldr, double *tc) {
     const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
     double *Ra = ws + C::RA, *Ys = ws + C::YS, *Gs = ws + C::GS, *Ts = ws + C::TS, *t8 = ws + C::T8, *xs = ws + C::XS;
     if (fl) wait_flag(fl + P);
@@ -137,6 +137,7 @@ __device__ __forceinline__ void node_panel(NodeRegs<C> &rg, double *Ahead_a, dou
     }
     __syncwarp();
     build_t(Gs, t8, Ts);
+    *reinterpret_cast<double2 *>(tc + 64 * P + 2 * lane) = *reinterpret_cast<const double2 *>(Ts + 2 * lane);
     if constexpr (P + 1 < C::NCB) {
         const double tb0 = Ts[(2 * q) * 8 + l4], tb1 = Ts[(2 * q + 1) * 8 + l4];
 #pragma unroll
@@ -181,7 +182,7 @@ __device__ __forceinline__ void node_panel(NodeRegs<C> &rg, double *Ahead_a, dou
     __threadfence();
     __syncwarp();
     if (lane == 0) *reinterpret_cast<volatile int *>(fme + P) = 1;
-    if constexpr (P + 1 < C::NCB) node_panel<C, P + 1>(rg, Ahead_a, Ahead_b, lda, n, ws, tau_out, fl, fr, fme, R, ldr);
+    if constexpr (P + 1 < C::NCB) node_panel<C, P + 1>(rg, Ahead_a, Ahead_b, lda, n, ws, tau_out, fl, fr, fme, R, ldr, tc);
 }
 
 }  // namespace tree
@@ -193,7 +194,8 @@ using namespace tree;
 template <class C>
 __global__ void __launch_bounds__(NW * 32)
 k_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *node_a, const int *nodes, int count,
-            const int *prod_l, const int *prod_r, int *flags, double *tau_node, int root, double *R, int64_t ldr) {
+            const int *prod_l, const int *prod_r, int *flags, double *tau_node, int root, double *R, int64_t ldr,
+            double *tcache_node) {
     extern __shared__ __align__(16) double sm[];
     const int warp = threadIdx.x >> 5;
     const int i = blockIdx.x * NW + warp;
@@ -208,7 +210,7 @@ k_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *
     const int pl = prod_l[b], pr = prod_r[b];
     node_panel<C, 0>(rg, A + tile_row0[a], A + tile_row0[b], lda, n, ws, tau_node + (int64_t)b * n,
                      pl >= 0 ? flags + pl * C::NCB : nullptr, pr >= 0 ? flags + pr * C::NCB : nullptr,
-                     flags + b * C::NCB, b == root ? R : nullptr, ldr);
+                     flags + b * C::NCB, b == root ? R : nullptr, ldr, tcache_node + (int64_t)b * C::NCB * 64);
 }
 
 template <class F>
@@ -227,7 +229,8 @@ static cudaError_t tree_dispatch(int n, F &&fn) {
 
 cudaError_t launch_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *node_a,
                              const int *nodes, int count, const int *prod_l, const int *prod_r, int *flags,
-                             double *tau_node, int root, double *R, int64_t ldr, cudaStream_t st) {
+                             double *tau_node, int root, double *R, int64_t ldr, double *tcache_node,
+                             cudaStream_t st) {
     if (count == 0) return cudaSuccess;
     return tree_dispatch(n, [&](auto c) {
         using C = decltype(c);
@@ -238,7 +241,7 @@ cudaError_t launch_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_
         if (e != cudaSuccess) return e;
         k_tree_pipe<C><<<(count + NW - 1) / NW, NW * 32, C::BYTES, st>>>(A, lda, n, tile_row0, node_a, nodes, count,
                                                                          prod_l, prod_r, flags, tau_node, root, R,
-                                                                         ldr);
+                                                                         ldr, tcache_node);
         return cudaGetLastError();
     });
 }

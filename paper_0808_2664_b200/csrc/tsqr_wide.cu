@@ -23,6 +23,8 @@
 #include "tsqr_kernels.h"
 #include "wy.cuh"
 
+#include <type_traits>
+
 namespace tsqr {
 namespace wide {
 
@@ -603,7 +605,7 @@ k_wide_apply_nodes(const double *A, int64_t lda, int n, const int64_t *tile_row0
 // registers, C_a's row block P read and written back per panel (the identity
 // part of the node's reflectors).  No barrier after the staging.
 constexpr int NPAN_NODE = 28;
-template <bool kFwd>
+template <bool kFwd, int NPAN_NODE>
 __global__ void __launch_bounds__(NT, 1)
 k_wide_apply_nodes_reg(const double *A, int64_t lda, int n, const int64_t *tile_row0, const int *node_a,
                        const int *ids, const double *tcache_node, double *C, int64_t ldc, int k, int xbuf_mode) {
@@ -781,16 +783,20 @@ cudaError_t launch_wide_apply_nodes(const double *A, int64_t lda, int n, const i
     const int npan = (n + 7) / 8;
     if (npan <= NPAN_NODE) {
         const size_t bytes = sizeof(double) * 64 * (npan * (npan + 1) / 2 + npan);
-        const void *fn = forward ? (const void *)k_wide_apply_nodes_reg<true> : (const void *)k_wide_apply_nodes_reg<false>;
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-        if (e != cudaSuccess) return e;
-        if (forward)
-            k_wide_apply_nodes_reg<true><<<count, NT, bytes, st>>>(A, lda, n, row0, node_a, ids, tcache_node, C, ldc, k,
-                                                                   xbuf_mode);
-        else
-            k_wide_apply_nodes_reg<false><<<count, NT, bytes, st>>>(A, lda, n, row0, node_a, ids, tcache_node, C, ldc,
-                                                                    k, xbuf_mode);
-        return cudaGetLastError();
+        auto go = [&](auto kf, auto np) -> cudaError_t {
+            constexpr bool F = decltype(kf)::value;
+            constexpr int NPM = decltype(np)::value;
+            cudaError_t e = cudaFuncSetAttribute((const void *)k_wide_apply_nodes_reg<F, NPM>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+            if (e != cudaSuccess) return e;
+            k_wide_apply_nodes_reg<F, NPM><<<count, NT, bytes, st>>>(A, lda, n, row0, node_a, ids, tcache_node, C, ldc,
+                                                                     k, xbuf_mode);
+            return cudaGetLastError();
+        };
+        using T8 = std::integral_constant<int, 8>;
+        using T28 = std::integral_constant<int, NPAN_NODE>;
+        if (forward) return npan <= 8 ? go(std::true_type(), T8()) : go(std::true_type(), T28());
+        return npan <= 8 ? go(std::false_type(), T8()) : go(std::false_type(), T28());
     }
     if (forward)
         k_wide_apply_nodes<true><<<count, NT, 0, st>>>(A, lda, n, row0, node_a, ids, tcache_node, C, ldc, k, xbuf_mode);
