@@ -455,7 +455,7 @@ tsqr_status_t tsqr_apply_qt(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, do
         for (size_t g = t->step_off.size() - 1; g-- > 0;) {         // tree steps bottom-up
             const int cnt = t->step_off[g + 1] - t->step_off[g];
             if (cnt == 0) continue;
-            CUDA_TRY(launch_wide_apply_nodes(t->A, t->lda, n, t->d_row0, t->d_node_a, t->d_step_ids + t->step_off[g],
+            CUDA_TRY(launch_node_apply(t->A, t->lda, n, t->d_row0, t->d_node_a, t->d_step_ids + t->step_off[g],
                                              cnt, t->d_tcache_node, C, ldc, (int)k, 1, 0, st),
                      "tsqr_apply_qt nodes");
         }
@@ -464,7 +464,7 @@ tsqr_status_t tsqr_apply_qt(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, do
         for (size_t g = t->step_off.size() - 1; g-- > 0;) {         // tree steps bottom-up
             const int cnt = t->step_off[g + 1] - t->step_off[g];
             if (cnt == 0) continue;
-            CUDA_TRY(launch_wide_apply_nodes(t->A, t->lda, (int)t->plan.n, t->d_row0, t->d_node_a,
+            CUDA_TRY(launch_node_apply(t->A, t->lda, (int)t->plan.n, t->d_row0, t->d_node_a,
                                              t->d_step_ids + t->step_off[g], cnt, t->d_tcache_node, C, ldc, (int)k, 1,
                                              0, st),
                      "tsqr_apply_qt nodes");
@@ -530,7 +530,7 @@ tsqr_status_t tsqr_form_q(tsqr_tree_t t, double *Q, int64_t ldq, void *stream) {
         for (size_t g = 0; g + 1 < t->step_off.size(); ++g) {         // tree steps top-down
             const int cnt = t->step_off[g + 1] - t->step_off[g];
             if (cnt == 0) continue;
-            CUDA_TRY(launch_wide_apply_nodes(t->A, t->lda, n, t->d_row0, t->d_node_a, t->d_step_ids + t->step_off[g],
+            CUDA_TRY(launch_node_apply(t->A, t->lda, n, t->d_row0, t->d_node_a, t->d_step_ids + t->step_off[g],
                                              cnt, t->d_tcache_node, t->d_xbuf, n, n, 0, 1, st),
                      "tsqr_form_q nodes");
         }
@@ -551,7 +551,7 @@ tsqr_status_t tsqr_form_q(tsqr_tree_t t, double *Q, int64_t ldq, void *stream) {
     for (size_t g = 0; g + 1 < t->step_off.size(); ++g) {         // tree steps top-down
         const int cnt = t->step_off[g + 1] - t->step_off[g];
         if (cnt == 0) continue;
-        CUDA_TRY(launch_wide_apply_nodes(t->A, t->lda, n, t->d_row0, t->d_node_a, t->d_step_ids + t->step_off[g],
+        CUDA_TRY(launch_node_apply(t->A, t->lda, n, t->d_row0, t->d_node_a, t->d_step_ids + t->step_off[g],
                                          cnt, t->d_tcache_node, t->d_xbuf, n, n, 0, 1, st),
                  "tsqr_form_q nodes");
     }

@@ -56,7 +56,7 @@ cudaError_t launch_wide_node1(double *Ra, int64_t lda, double *Rb, int64_t ldb, 
 cudaError_t launch_wide_apply_leaves(const double *A, int64_t lda, int n, const int64_t *row0, const int *rows,
                                      int L, int max_rows, const double *tcache, double *C, int64_t ldc, int k,
                                      int forward, cudaStream_t st);
-cudaError_t launch_wide_apply_nodes(const double *A, int64_t lda, int n, const int64_t *row0, const int *node_a,
+cudaError_t launch_node_apply(const double *A, int64_t lda, int n, const int64_t *row0, const int *node_a,
                                     const int *ids, int count, const double *tcache_node, double *C, int64_t ldc,
                                     int k, int forward, int xbuf_mode, cudaStream_t st);
 cudaError_t launch_wide_apply_node1(const double *Y1, int64_t ldy, int n, const double *tcache, double *Ca,

@@ -607,7 +607,7 @@ k_wide_apply_nodes(const double *A, int64_t lda, int n, const int64_t *tile_row0
 constexpr int NPAN_NODE = 28;
 template <bool kFwd, int NPAN_NODE>
 __global__ void __launch_bounds__(NT, 1)
-k_wide_apply_nodes_reg(const double *A, int64_t lda, int n, const int64_t *tile_row0, const int *node_a,
+k_node_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const int *node_a,
                        const int *ids, const double *tcache_node, double *C, int64_t ldc, int k, int xbuf_mode) {
     extern __shared__ __align__(16) double smraw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
@@ -777,7 +777,7 @@ cudaError_t launch_wide_apply_leaves(const double *A, int64_t lda, int n, const 
     return cudaGetLastError();
 }
 
-cudaError_t launch_wide_apply_nodes(const double *A, int64_t lda, int n, const int64_t *row0, const int *node_a,
+cudaError_t launch_node_apply(const double *A, int64_t lda, int n, const int64_t *row0, const int *node_a,
                                     const int *ids, int count, const double *tcache_node, double *C, int64_t ldc,
                                     int k, int forward, int xbuf_mode, cudaStream_t st) {
     const int npan = (n + 7) / 8;
@@ -786,10 +786,10 @@ cudaError_t launch_wide_apply_nodes(const double *A, int64_t lda, int n, const i
         auto go = [&](auto kf, auto np) -> cudaError_t {
             constexpr bool F = decltype(kf)::value;
             constexpr int NPM = decltype(np)::value;
-            cudaError_t e = cudaFuncSetAttribute((const void *)k_wide_apply_nodes_reg<F, NPM>,
+            cudaError_t e = cudaFuncSetAttribute((const void *)k_node_apply<F, NPM>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
             if (e != cudaSuccess) return e;
-            k_wide_apply_nodes_reg<F, NPM><<<count, NT, bytes, st>>>(A, lda, n, row0, node_a, ids, tcache_node, C, ldc,
+            k_node_apply<F, NPM><<<count, NT, bytes, st>>>(A, lda, n, row0, node_a, ids, tcache_node, C, ldc,
                                                                      k, xbuf_mode);
             return cudaGetLastError();
         };
