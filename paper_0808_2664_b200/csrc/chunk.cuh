@@ -172,6 +172,18 @@ __device__ __forceinline__ void build_t(const double *Gs, const double *t, doubl
     __syncwarp();
 }
 
+// Columns past n are padding: their Householder steps would be identities
+// (tau = 0, zero reflector), so the panels stop after column n-1 and give the
+// remaining columns tau = 0 and zero Gram entries, which makes their rows and
+// columns of T zero exactly as the skipped steps would have.
+__device__ __forceinline__ void pad_steps(double *Gs, double *t8, int jn) {
+    const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+    for (int c = jn; c < 8; ++c) {
+        if (q == 0 && l4 < c) Gs[l4 * 8 + c] = 0.0;
+        if (lane == 0) t8[c] = 0.0;
+    }
+}
+
 template <class C>
 struct Chunk {
     double a[C::KM][C::NCB][2];
@@ -194,8 +206,9 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
             *reinterpret_cast<double2 *>(xs + 8 * k + 2 * q) = make_double2(ch.a[k][P][0], ch.a[k][P][1]);
     }
     __syncwarp();
+    const int jn = (P + 1 < C::NCB) ? 8 : n - 8 * P;      // only the last panel has padding columns
 #pragma unroll 1
-    for (int jj = 0; jj < 8; ++jj) {
+    for (int jj = 0; jj < jn; ++jj) {
         const int j = 8 * P + jj;
         const double *xr = xs + (jj & 1) * C::CH;
         double x[C::KM][2];
@@ -254,6 +267,7 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
         __syncwarp();                                                // xs of the next step
         PROBE(2);
     }
+    pad_steps(Gs, t8, jn);
     __syncwarp();
     if (lane < 8 && 8 * P + lane < n) tau_out[8 * P + lane] = t8[lane];
 }
@@ -264,8 +278,9 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
 template <class C, int P>
 __device__ __forceinline__ void panel_dense(Chunk<C> &ch, int kb, double *Gs, double *t8, double *tau_out, int n) {
     const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+    const int jn = (P + 1 < C::NCB) ? 8 : n - 8 * P;      // only the last panel has padding columns
 #pragma unroll 1
-    for (int jj = 0; jj < 8; ++jj) {
+    for (int jj = 0; jj < jn; ++jj) {
         const int j = 8 * P + jj;
         const int qp = jj >> 1, ep = jj & 1;
         const int src = 4 * jj + q;
@@ -317,6 +332,7 @@ __device__ __forceinline__ void panel_dense(Chunk<C> &ch, int kb, double *Gs, do
         if (q == 0 && l4 < jj) Gs[l4 * 8 + jj] = fma(h.scale, d, rj);    // G(l, jj) = y_l^T y_jj
         if (lane == 0) t8[jj] = h.tau;
     }
+    pad_steps(Gs, t8, jn);
     __syncwarp();
     if (lane < 8 && 8 * P + lane < n) tau_out[8 * P + lane] = t8[lane];
 }

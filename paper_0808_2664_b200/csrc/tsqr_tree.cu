@@ -84,8 +84,9 @@ __device__ __forceinline__ void node_panel(NodeRegs<C> &rg, double *Ahead_a, dou
             *reinterpret_cast<double2 *>(xs + 8 * k + 2 * q) = make_double2(rg.a[k][P][0], rg.a[k][P][1]);
     }
     __syncwarp();
+    const int jn = (P + 1 < C::NCB) ? 8 : n - 8 * P;
 #pragma unroll 1
-    for (int jj = 0; jj < 8; ++jj) {
+    for (int jj = 0; jj < jn; ++jj) {
         const double *xr = xs + (jj & 1) * C::NP;
         double d0 = 0.0, d1 = 0.0, s0 = 0.0, s1 = 0.0;
         double x[P + 1][2];
@@ -128,6 +129,8 @@ __device__ __forceinline__ void node_panel(NodeRegs<C> &rg, double *Ahead_a, dou
         if (lane == 0) t8[jj] = h.tau;
         __syncwarp();
     }
+    chunk::pad_steps(Gs, t8, jn);
+    __syncwarp();
     if (lane < 8 && 8 * P + lane < n) tau_out[8 * P + lane] = t8[lane];
     // Y of the panel (rows 0..8P+7 of R_b, i.e. Y1's columns 8P..8P+7) for the update
 #pragma unroll
@@ -315,8 +318,9 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                         *reinterpret_cast<const double2 *>(blk(Rb, k, P) + 2 * q);
             __syncwarp();
             double *RaP = Ra + 64 * P;
+            const int jn = min(8, n - 8 * P);
 #pragma unroll 1
-            for (int jj = 0; jj < 8; ++jj) {
+            for (int jj = 0; jj < jn; ++jj) {
                 const double *xr = xs + (jj & 1) * 8 * npan;
                 double d0 = 0.0, d1 = 0.0, s0 = 0.0, s1 = 0.0;
 #pragma unroll 4
@@ -357,6 +361,8 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                 if (lane == 0) t8[jj] = h.tau;
                 __syncwarp();
             }
+            chunk::pad_steps(Gs, t8, jn);
+            __syncwarp();
             if (lane < 8 && 8 * P + lane < n) tau_out[8 * P + lane] = t8[lane];
             build_t(Gs, t8, Ts);
             *reinterpret_cast<double2 *>(tc + 64 * P + 2 * lane) = *reinterpret_cast<const double2 *>(Ts + 2 * lane);

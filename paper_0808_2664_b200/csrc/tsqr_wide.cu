@@ -119,8 +119,9 @@ __device__ void wide_qr(const Prob &P, int n, double *tau, double *tcache, Smem 
                 *reinterpret_cast<double2 *>(xs0 + 8 * k + 2 * q) = make_double2(a[k][0], a[k][1]);
         }
         __syncwarp();
+        const int jn = min(8, n - 8 * p);
 #pragma unroll 1
-        for (int jj = 0; jj < 8; ++jj) {
+        for (int jj = 0; jj < jn; ++jj) {
             const int j = 8 * p + jj;                         // pivot = logical row j
             const int par = jj & 1;
             const double *xr = par ? xs1 : xs0;
@@ -177,6 +178,12 @@ __device__ void wide_qr(const Prob &P, int n, double *tau, double *tcache, Smem 
             if (warp == 0 && q == 0 && l4 < jj) S.Gs[l4 * 8 + jj] = fma(h.scale, dd, rj);
             if (threadIdx.x == 0) S.t8[jj] = h.tau;
             __syncwarp();
+        }
+        if (warp == 0) {                         // padding columns past n: identity steps
+            for (int c2 = jn; c2 < 8; ++c2) {
+                if (q == 0 && l4 < c2) S.Gs[l4 * 8 + c2] = 0.0;
+                if (lane == 0) S.t8[c2] = 0.0;
+            }
         }
         // ---- write the panel back; T; taus
 #pragma unroll
@@ -419,8 +426,9 @@ __device__ void wide_leaf_qr(double *At, int64_t lda, int H, int n, double *tau,
                 *reinterpret_cast<double2 *>(xs0 + 8 * k + 2 * q) = make_double2(a[k][0], a[k][1]);
         }
         __syncwarp();
+        const int jn = min(8, n - 8 * p);
 #pragma unroll 1
-        for (int jj = 0; jj < 8; ++jj) {
+        for (int jj = 0; jj < jn; ++jj) {
             const int j = 8 * p + jj;
             const int par = jj & 1;
             const double *xr = par ? xs1 : xs0;
@@ -477,6 +485,12 @@ __device__ void wide_leaf_qr(double *At, int64_t lda, int H, int n, double *tau,
             if (warp == 0 && q == 0 && l4 < jj) S.Gs[l4 * 8 + jj] = fma(h.scale, dd, rj);
             if (threadIdx.x == 0) S.t8[jj] = h.tau;
             __syncwarp();
+        }
+        if (warp == 0) {                         // padding columns past n: identity steps
+            for (int c2 = jn; c2 < 8; ++c2) {
+                if (q == 0 && l4 < c2) S.Gs[l4 * 8 + c2] = 0.0;
+                if (lane == 0) S.t8[c2] = 0.0;
+            }
         }
         // write the panel back; Y of the panel -> Ys (rows >= 8p, zero past H)
 #pragma unroll
