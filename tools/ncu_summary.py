@@ -44,7 +44,7 @@ def main():
                 print(f"  {desc:36s} {r[i]:>16s} {units[i]}   ({key})")
         rd = h.index("dram__bytes_read.sum")
         wr = h.index("dram__bytes_write.sum")
-        print(f"  DRAM read + write per launch: {r[rd]} + {r[wr]} {units[rd]}")
+        print(f"  DRAM read + write per launch: {r[rd]} {units[rd]} + {r[wr]} {units[wr]}")
 
 
 if __name__ == "__main__":
