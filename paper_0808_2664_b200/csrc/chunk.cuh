@@ -118,10 +118,13 @@ __device__ __forceinline__ House house_bf(double alpha, double s2) {
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(i) : "d"(D0));
     const double hy = 0.5 * y;
     r = r * fma(-hy * r, r, 1.5);
+    // first Newton step of 1/D against D1 = |alpha| + y r1 (r once refined),
+    // overlapped with r's second step; the last one runs against the exact D
+    const double D1 = fma(y, r, aa);
+    i = fma(i, fma(-D1, i, 1.0), i);
     r = r * fma(-hy * r, r, 1.5);
     const double N = y * r;
     const double D = aa + N;
-    i = fma(i, fma(-D, i, 1.0), i);
     i = fma(i, fma(-D, i, 1.0), i);
     const bool z = (s2 == 0.0);
     House h;
@@ -170,6 +173,18 @@ __device__ __forceinline__ void build_t(const double *Gs, const double *t, doubl
         for (int c = 0; c < 8; c += 2) *reinterpret_cast<double2 *>(Ts + r * 8 + c) = make_double2(row[c], row[c + 1]);
     }
     __syncwarp();
+}
+
+// Sums of a value over the 4 lanes q of each column l4 (lane = 4 l4 + q), on
+// the tensor pipe instead of two shuffle rounds: D = A 1 with A[l4][q] the
+// lane's partial (one m8n8k4 DMMA per sum, both issued back to back); every
+// lane of column l4 receives its column's sum.
+__device__ __forceinline__ void quad_sums(double &d, double &s2, double pd, double ps) {
+    double d1 = 0.0, s1 = 0.0;
+    d = 0.0;
+    s2 = 0.0;
+    dmma(d, d1, pd, 1.0);
+    dmma(s2, s1, ps, 1.0);
 }
 
 // Columns past n are padding: their Householder steps would be identities
@@ -226,11 +241,8 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
             s0 = fma(x[k][0], x[k][0], s0);
             s1 = fma(x[k][1], x[k][1], s1);
         }
-        double d = d0 + d1, s2 = s0 + s1;
-        d += __shfl_xor_sync(FULL, d, 1);
-        s2 += __shfl_xor_sync(FULL, s2, 1);
-        d += __shfl_xor_sync(FULL, d, 2);
-        s2 += __shfl_xor_sync(FULL, s2, 2);
+        double d, s2;
+        quad_sums(d, s2, d0 + d1, s0 + s1);
         PROBE(3);
 #ifndef TSQR_NOWAIT_ROW                    // timing experiment only (results invalid)
         sync_wait(sy.row + j, sy.s);                                 // R row j released by the previous chunk
@@ -306,11 +318,8 @@ __device__ __forceinline__ void panel_dense(Chunk<C> &ch, int kb, double *Gs, do
             s0 = fma(x[k][0], x[k][0], s0);
             s1 = fma(x[k][1], x[k][1], s1);
         }
-        double d = d0 + d1, s2 = s0 + s1;
-        d += __shfl_xor_sync(FULL, d, 1);
-        s2 += __shfl_xor_sync(FULL, s2, 1);
-        d += __shfl_xor_sync(FULL, d, 2);
-        s2 += __shfl_xor_sync(FULL, s2, 2);
+        double d, s2;
+        quad_sums(d, s2, d0 + d1, s0 + s1);
         const House h = house_bf(alpha, s2);
         const double w = fma(h.scale, d, rj);
         const double u = (l4 > jj) ? h.tau * h.scale * w : (l4 == jj ? 1.0 : 0.0);

@@ -100,11 +100,8 @@ __device__ __forceinline__ void node_panel(NodeRegs<C> &rg, double *Ahead_a, dou
             s0 = fma(x[k][0], x[k][0], s0);
             s1 = fma(x[k][1], x[k][1], s1);
         }
-        double d = d0 + d1, s2 = s0 + s1;
-        d += __shfl_xor_sync(FULL, d, 1);
-        s2 += __shfl_xor_sync(FULL, s2, 1);
-        d += __shfl_xor_sync(FULL, d, 2);
-        s2 += __shfl_xor_sync(FULL, s2, 2);
+        double d, s2;
+        chunk::quad_sums(d, s2, d0 + d1, s0 + s1);
         const double alpha = Ra[jj * C::LDA + 8 * P + jj];
         const double rj = Ra[jj * C::LDA + 8 * P + l4];
         const House h = house_bf(alpha, s2);
@@ -332,11 +329,8 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                     s0 = fma(x.x, x.x, s0);
                     s1 = fma(x.y, x.y, s1);
                 }
-                double d = d0 + d1, s2 = s0 + s1;
-                d += __shfl_xor_sync(tree::FULL, d, 1);
-                s2 += __shfl_xor_sync(tree::FULL, s2, 1);
-                d += __shfl_xor_sync(tree::FULL, d, 2);
-                s2 += __shfl_xor_sync(tree::FULL, s2, 2);
+                double d, s2;
+                chunk::quad_sums(d, s2, d0 + d1, s0 + s1);
                 const double alpha = RaP[8 * jj + jj];
                 const double rj = RaP[8 * l4 + jj];
                 const House h = house_bf(alpha, s2);
