@@ -244,12 +244,24 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
         double d, s2;
         quad_sums(d, s2, d0 + d1, s0 + s1);
         PROBE(3);
-#ifndef TSQR_NOWAIT_ROW                    // timing experiment only (results invalid)
-        sync_wait(sy.row + j, sy.s);                                 // R row j released by the previous chunk
-#endif
+        // R row j released by the previous chunk: the counter and the row are
+        // read together (a warp's shared-memory accesses are performed in
+        // issue order, so a row read issued after a counter read that sees
+        // the release sees the row); only if the counter is short do we spin
+        // and read the row again
+        double alpha, rj;                                            // R(j, j), R(j, 8P + l4)
+        {
+            const volatile double *rr = Rb + j * C::LDR;
+            const int c0 = *reinterpret_cast<const volatile int *>(sy.row + j);
+            alpha = rr[j];
+            rj = rr[8 * P + l4];
+            if (c0 < sy.s) {
+                sync_wait(sy.row + j, sy.s);
+                alpha = rr[j];
+                rj = rr[8 * P + l4];
+            }
+        }
         PROBE(4);
-        const double alpha = Rb[j * C::LDR + j];
-        const double rj = Rb[j * C::LDR + 8 * P + l4];                // R(j, 8P + l4)
         const House h = house_bf(alpha, s2);
         const double w = fma(h.scale, d, rj);                        // v^T [R(j,c); a_c]
         // a <- a - u x (u = tau scale w) for the trailing columns; the pivot
