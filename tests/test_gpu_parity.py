@@ -71,6 +71,11 @@ CASES = [
     (5000, 100, 2048, 2048),     # n not a multiple of 8, three tiles (last 904 rows)
     (20000, 200, 2048, 2048),    # config-3 shape at m = 20,000: ten tiles
     (3000, 65, 1000, 1000),      # n = 65: nine padded columns
+    (2000, 224, 1000, 1000),     # n = 224: the widest pipelined tree (28 panels in smem)
+    (3000, 256, 1500, 1500),     # n = 256 (TSQR_MAX_N): masked dense node kernel, one launch per step
+    (700, 57, 700, 100),         # n = 57: 32-row chunks, last panel has one real column
+    (500, 63, 500, 250),         # n = 63
+    (300, 9, 300, 40),           # n = 9: 64-row chunks taller than the 40-row tiles' chunks
 ]
 
 
