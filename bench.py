@@ -191,9 +191,9 @@ def run_ours(args, cfg):
     N = args.gpus
     rank, world = 0, 1
     if N > 1:
-        dist.init_process_group("nccl")
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", os.environ.get("RANK", "0"))))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
         rank, world = dist.get_rank(), dist.get_world_size()
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
     dev = torch.device("cuda", torch.cuda.current_device())
     m, n, b, s, k = cfg["m"], cfg["n"], cfg["b"], cfg["s"], cfg["k"]
     row0, ml = T.slab(m, n, b, world, rank)
