@@ -299,12 +299,29 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
         if (pl >= 0) wait_flag_cta(flags + pl * MAX_NPAN + P);
         if (pr >= 0) wait_flag_cta(flags + pr * MAX_NPAN + P);
         // row block P of R_a and R_b (upper part), column blocks P..npan-1
-        for (int e = threadIdx.x; e < 64 * (npan - P); e += NT) {
-            const int cb = P + (e >> 6), cl = (e >> 3) & 7, r = e & 7;
-            const int i = 8 * P + r, c = 8 * cb + cl;
-            const bool ok = c >= i && c < n;
-            Ra[64 * cb + 8 * cl + r] = ok ? __ldcg(Ha + i + (int64_t)c * lda) : 0.0;
-            blk(Rb, P, cb)[8 * cl + r] = ok ? __ldcg(Hb + i + (int64_t)c * lda) : 0.0;
+        // L2 loads (ld.cg: the rows were written by other CTAs of this launch;
+        // L1 may hold stale lines), all of a thread's loads in flight at once
+        {
+            constexpr int MAXL = (64 * MAX_NPAN + NT - 1) / NT;
+            double va[MAXL], vb[MAXL];
+#pragma unroll
+            for (int u = 0; u < MAXL; ++u) {
+                const int e = threadIdx.x + u * NT;
+                const int cb = P + (e >> 6), cl = (e >> 3) & 7, r = e & 7;
+                const int i = 8 * P + r, c = 8 * cb + cl;
+                const bool ok = e < 64 * (npan - P) && c >= i && c < n;
+                va[u] = ok ? __ldcg(Ha + i + (int64_t)c * lda) : 0.0;
+                vb[u] = ok ? __ldcg(Hb + i + (int64_t)c * lda) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < MAXL; ++u) {
+                const int e = threadIdx.x + u * NT;
+                if (e < 64 * (npan - P)) {
+                    const int cb = P + (e >> 6), cl = (e >> 3) & 7, r = e & 7;
+                    Ra[64 * cb + 8 * cl + r] = va[u];
+                    blk(Rb, P, cb)[8 * cl + r] = vb[u];
+                }
+            }
         }
         __syncthreads();
         if (warp == 0) {

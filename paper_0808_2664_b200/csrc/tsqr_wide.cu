@@ -301,6 +301,12 @@ __device__ void wide_apply(const Prob &P, const Prob &Cp, int n, int k, const do
 }
 
 
+// 8-byte global -> shared copy (zero-filled when !ok)
+__device__ __forceinline__ void cp_async8(double *sm, const double *g, bool ok) {
+    const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(sm));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 8 : 0) : "memory");
+}
+
 // ------------------------------------------------------------------ leaves
 // The leaf path (plain tiles, no masks): the panel's Y is staged in shared
 // memory (row-major H x 8, zero-padded to a whole row block), so the column-
@@ -574,26 +580,46 @@ k_wide_node1(double *Ra, int64_t lda, double *Rb, int64_t ldb, int n, double *ta
 template <bool kFwd>
 __global__ void __launch_bounds__(NT, 2)
 k_wide_apply_leaves(const double *A, int64_t lda, int n, const int64_t *tile_row0, const int *tile_rows,
-                    const double *tcache_tile, double *C, int64_t ldc, int k) {
+                    const double *tcache_tile, double *C, int64_t ldc, int k, int two_slots) {
     extern __shared__ __align__(16) double smraw[];
     const int t = blockIdx.x;
     const int npan = (n + 7) / 8;
     const int H = tile_rows[t];
     const int Hp = 8 * ((H + 7) / 8);
-    double *Ts = smraw, *Ys = smraw + 64;
+    double *Ts = smraw, *Ys = smraw + 128;                       // 2 slots each
     const double *At = A + tile_row0[t];
     const double *tc = tcache_tile + (int64_t)t * npan * 64;
-    for (int pp = 0; pp < npan; ++pp) {
-        const int p = kFwd ? pp : npan - 1 - pp;
+    // panel p's Y staged with cp.async (zero-filled off the reflectors, unit
+    // diagonal patched after the wait), the next panel's copy in flight while
+    // this one is applied (two slots)
+    auto stage = [&](int p, int slot) {
+        double *Y = Ys + slot * Hp * 8, *T = Ts + slot * 64;
         const int h0 = 8 * p, hs = Hp - h0;
         for (int e = threadIdx.x; e < 8 * hs; e += NT) {
             const int r = h0 + e % hs, jj = e / hs, c = 8 * p + jj;
-            Ys[r * 8 + jj] = (c >= n || r < c || r >= H) ? 0.0 : (r == c ? 1.0 : At[r + (int64_t)c * lda]);
+            const bool ok = c < n && r > c && r < H;
+            cp_async8(Y + r * 8 + jj, At + (ok ? r + (int64_t)c * lda : 0), ok);
         }
-        if (threadIdx.x < 64) Ts[threadIdx.x] = tc[64 * p + threadIdx.x];
+        if (threadIdx.x < 64) cp_async8(T + threadIdx.x, tc + 64 * p + threadIdx.x, true);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    stage(kFwd ? 0 : npan - 1, 0);
+    for (int pp = 0; pp < npan; ++pp) {
+        const int p = kFwd ? pp : npan - 1 - pp, slot = two_slots ? (pp & 1) : 0;
+        if (two_slots && pp + 1 < npan) {
+            stage(kFwd ? p + 1 : p - 1, slot ^ 1);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
         __syncthreads();
-        apply_panel_cols<kFwd>(Ys, Ts, C + tile_row0[t], ldc, H, p, 0, k);
+        double *Y = Ys + slot * Hp * 8;
+        if (threadIdx.x < 8 && 8 * p + threadIdx.x < n && 8 * p + threadIdx.x < H)
+            Y[(8 * p + threadIdx.x) * 8 + threadIdx.x] = 1.0;
         __syncthreads();
+        apply_panel_cols<kFwd>(Y, Ts + slot * 64, C + tile_row0[t], ldc, H, p, 0, k);
+        __syncthreads();
+        if (!two_slots && pp + 1 < npan) stage(kFwd ? p + 1 : p - 1, 0);
     }
 }
 
@@ -630,18 +656,20 @@ k_node_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, cons
     const int nb = npan * (npan + 1) / 2;
     double *Yb = smraw, *Tn = smraw + 64 * nb;
     const double *Hb = A + tile_row0[b];
-#pragma unroll 8
-    for (int e = threadIdx.x; e < 64 * nb; e += NT) {            // loads independent of each other
+    // Y1 and the T's staged with cp.async: every copy of the CTA in flight at once
+    for (int e = threadIdx.x; e < 64 * nb; e += NT) {
         const int bi = e >> 6, cl = (e >> 3) & 7, r = e & 7;
         int cb = (int)((sqrtf(8.0f * bi + 1.0f) - 1.0f) * 0.5f);   // bi = cb(cb+1)/2 + kk, kk <= cb
         cb += (cb + 1) * (cb + 2) / 2 <= bi;
         cb -= cb * (cb + 1) / 2 > bi;
         const int kk = bi - cb * (cb + 1) / 2;
         const int i = 8 * kk + r, c = 8 * cb + cl;
-        Yb[e] = (i <= c && c < n) ? __ldg(Hb + i + (int64_t)c * lda) : 0.0;
+        const bool ok = i <= c && c < n;
+        cp_async8(Yb + e, Hb + (ok ? i + (int64_t)c * lda : 0), ok);
     }
     const double *tc = tcache_node + (int64_t)b * npan * 64;
-    for (int e = threadIdx.x; e < 64 * npan; e += NT) Tn[e] = tc[e];
+    for (int e = threadIdx.x; e < 64 * npan; e += NT) cp_async8(Tn + e, tc + e, true);
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncthreads();
     double *Ca, *Cb;
     int64_t ld;
@@ -741,7 +769,9 @@ static cudaError_t wide_attr(const void *fn) {
 }
 int wide_max_rows() { return MAXR; }
 
-static size_t apply_leaf_smem(int max_rows) { return sizeof(double) * (8 * ((max_rows + 7) / 8 * 8) + 64); }
+static size_t apply_leaf_smem(int max_rows, int slots) {
+    return sizeof(double) * (slots * 8 * ((max_rows + 7) / 8 * 8) + 128);
+}
 
 template <int KM>
 static cudaError_t launch_leaves_km(double *A, int64_t lda, int n, const int64_t *row0, const int *rows, int L,
@@ -782,12 +812,15 @@ cudaError_t launch_wide_node1(double *Ra, int64_t lda, double *Rb, int64_t ldb, 
 cudaError_t launch_wide_apply_leaves(const double *A, int64_t lda, int n, const int64_t *row0, const int *rows,
                                      int L, int max_rows, const double *tcache, double *C, int64_t ldc, int k,
                                      int forward, cudaStream_t st) {
-    const size_t bytes = apply_leaf_smem(max_rows);
+    const int slots = apply_leaf_smem(max_rows, 2) <= 227 * 1024 ? 2 : 1;   // prefetch the next panel's Y if it fits
+    const size_t bytes = apply_leaf_smem(max_rows, slots);
     const void *fn = forward ? (const void *)k_wide_apply_leaves<true> : (const void *)k_wide_apply_leaves<false>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;
-    if (forward) k_wide_apply_leaves<true><<<L, NT, bytes, st>>>(A, lda, n, row0, rows, tcache, C, ldc, k);
-    else k_wide_apply_leaves<false><<<L, NT, bytes, st>>>(A, lda, n, row0, rows, tcache, C, ldc, k);
+    if (forward)
+        k_wide_apply_leaves<true><<<L, NT, bytes, st>>>(A, lda, n, row0, rows, tcache, C, ldc, k, slots == 2);
+    else
+        k_wide_apply_leaves<false><<<L, NT, bytes, st>>>(A, lda, n, row0, rows, tcache, C, ldc, k, slots == 2);
     return cudaGetLastError();
 }
 
