@@ -18,6 +18,8 @@
 #include "tsqr_kernels.h"
 #include "chunk.cuh"
 
+#include <vector>
+
 namespace tsqr {
 namespace tree {
 
@@ -266,9 +268,29 @@ constexpr int NT = 256;
 constexpr int MAX_NPAN = 28;
 
 __host__ __device__ constexpr int nblk(int npan) { return npan * (npan + 1) / 2; }
-__host__ __device__ inline size_t smem_doubles(int npan) { return (size_t)(nblk(npan) + npan) * 64 + 64 + 64 + 8 + 2 * 8 * npan; }
+// Block (k, cb) of R_b (k <= cb) is live from panel k (its row block arrives)
+// to panel cb (its column is published as Y1), so at panel P only the blocks
+// with k <= P <= cb exist: at most max_P (P+1)(npan-P) of them, about a
+// quarter of the triangle.  A host-side greedy colouring of these intervals
+// (by start panel) gives every block a slot that no live block shares;
+// the tables for every npan <= MAX_NPAN sit in constant memory, block (k, cb)
+// of width npan at c_slot[slot_off(npan) + cb(cb+1)/2 + k].
+__host__ __device__ constexpr int slot_off(int npan) { return (npan - 1) * npan * (npan + 1) / 6; }   // sum nblk(j<npan)
+constexpr int SLOT_TABLE = slot_off(MAX_NPAN + 1);
+__constant__ unsigned short c_slot[SLOT_TABLE];
 
-__device__ __forceinline__ double *blk(double *Rb, int k, int cb) { return Rb + 64 * (cb * (cb + 1) / 2 + k); }
+__host__ __device__ inline int max_live(int npan) {
+    int m = 0;
+    for (int P = 0; P < npan; ++P) m = (P + 1) * (npan - P) > m ? (P + 1) * (npan - P) : m;
+    return m;
+}
+__host__ __device__ inline size_t smem_doubles(int npan) {
+    return (size_t)(max_live(npan) + npan) * 64 + 64 + 64 + 8 + 2 * 8 * npan;
+}
+
+__device__ __forceinline__ double *blk(double *Rb, int so, int k, int cb) {
+    return Rb + 64 * c_slot[so + cb * (cb + 1) / 2 + k];
+}
 
 __device__ __forceinline__ void wait_flag_cta(const int *f) {
     if (threadIdx.x == 0) {
@@ -287,10 +309,11 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
     extern __shared__ __align__(16) double sm[];
     const int npan = (n + 7) / 8;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
-    double *Rb = sm;                                 // nblk(npan) blocks
-    double *Ra = Rb + 64 * nblk(npan);               // npan blocks: R_a's pivot rows of the panel
+    double *Rb = sm;                                 // max_live(npan) block slots (see c_slot)
+    double *Ra = Rb + 64 * max_live(npan);           // npan blocks: R_a's pivot rows of the panel
     double *Gs = Ra + 64 * npan, *Ts = Gs + 64, *t8 = Ts + 64, *xs = t8 + 8;   // xs: 2 x 8 npan
     const int b = nodes[blockIdx.x], a = node_a[b];
+    const int so = slot_off(npan);
     double *Ha = A + tile_row0[a], *Hb = A + tile_row0[b];
     const int pl = prod_l[b], pr = prod_r[b];
     double *tau_out = tau_node + (int64_t)b * n;
@@ -319,7 +342,7 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                 if (e < 64 * (npan - P)) {
                     const int cb = P + (e >> 6), cl = (e >> 3) & 7, r = e & 7;
                     Ra[64 * cb + 8 * cl + r] = va[u];
-                    blk(Rb, P, cb)[8 * cl + r] = vb[u];
+                    blk(Rb, so, P, cb)[8 * cl + r] = vb[u];
                 }
             }
         }
@@ -329,7 +352,7 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
             for (int k = 0; k <= P; ++k)
                 if (l4 == 0)
                     *reinterpret_cast<double2 *>(xs + 8 * k + 2 * q) =
-                        *reinterpret_cast<const double2 *>(blk(Rb, k, P) + 2 * q);
+                        *reinterpret_cast<const double2 *>(blk(Rb, so, k, P) + 2 * q);
             __syncwarp();
             double *RaP = Ra + 64 * P;
             const int jn = min(8, n - 8 * P);
@@ -340,7 +363,7 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
 #pragma unroll 4
                 for (int k = 0; k <= P; ++k) {
                     const double2 x = *reinterpret_cast<const double2 *>(xr + 8 * k + 2 * q);
-                    const double2 v = *reinterpret_cast<const double2 *>(blk(Rb, k, P) + 8 * l4 + 2 * q);
+                    const double2 v = *reinterpret_cast<const double2 *>(blk(Rb, so, k, P) + 8 * l4 + 2 * q);
                     d0 = fma(x.x, v.x, d0);
                     d1 = fma(x.y, v.y, d1);
                     s0 = fma(x.x, x.x, s0);
@@ -359,7 +382,7 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
 #pragma unroll 4
                 for (int k = 0; k <= P; ++k) {
                     const double2 x = *reinterpret_cast<const double2 *>(xr + 8 * k + 2 * q);
-                    double2 *vp = reinterpret_cast<double2 *>(blk(Rb, k, P) + 8 * l4 + 2 * q);
+                    double2 *vp = reinterpret_cast<double2 *>(blk(Rb, so, k, P) + 8 * l4 + 2 * q);
                     double2 v = *vp;
                     v.x = fma(g, x.x, fma(-u, x.x, v.x));
                     v.y = fma(g, x.y, fma(-u, x.y, v.y));
@@ -386,8 +409,8 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                 double w0[2] = {0.0, 0.0}, w1[2] = {0.0, 0.0};
 #pragma unroll 4
                 for (int k = 0; k <= P; ++k) {
-                    const double2 c = *reinterpret_cast<const double2 *>(blk(Rb, k, cb) + 8 * l4 + 2 * q);
-                    const double2 y = *reinterpret_cast<const double2 *>(blk(Rb, k, P) + 8 * l4 + 2 * q);
+                    const double2 c = *reinterpret_cast<const double2 *>(blk(Rb, so, k, cb) + 8 * l4 + 2 * q);
+                    const double2 y = *reinterpret_cast<const double2 *>(blk(Rb, so, k, P) + 8 * l4 + 2 * q);
                     dmma(w0[k & 1], w1[k & 1], c.x, y.x);
                     dmma(w0[k & 1], w1[k & 1], c.y, y.y);
                 }
@@ -402,9 +425,9 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                 *rp = rv;
 #pragma unroll 4
                 for (int k = 0; k <= P; ++k) {
-                    const double *yb = blk(Rb, k, P);
+                    const double *yb = blk(Rb, so, k, P);
                     const double yt0 = yb[8 * (2 * q) + l4], yt1 = yb[8 * (2 * q + 1) + l4];
-                    double2 *cp = reinterpret_cast<double2 *>(blk(Rb, k, cb) + 8 * l4 + 2 * q);
+                    double2 *cp = reinterpret_cast<double2 *>(blk(Rb, so, k, cb) + 8 * l4 + 2 * q);
                     double2 c = *cp;
                     dmma(c.x, c.y, -p0, yt0);
                     dmma(c.x, c.y, -p1, yt1);
@@ -422,7 +445,7 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
         for (int e = threadIdx.x; e < 64 * (P + 1); e += NT) {
             const int k = e >> 6, cl = (e >> 3) & 7, r = e & 7;
             const int i = 8 * k + r, c = 8 * P + cl;
-            if (i <= c && c < n) Hb[i + (int64_t)c * lda] = blk(Rb, k, P)[8 * cl + r];
+            if (i <= c && c < n) Hb[i + (int64_t)c * lda] = blk(Rb, so, k, P)[8 * cl + r];
         }
         __threadfence();
         __syncthreads();
@@ -438,6 +461,25 @@ cudaError_t launch_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *
     if (count == 0) return cudaSuccess;
     const int npan = (n + 7) / 8;
     if (npan > wtree::MAX_NPAN) return cudaErrorInvalidValue;
+    static bool tables = false;                      // slot colourings, once per process
+    if (!tables) {
+        std::vector<unsigned short> tab(wtree::SLOT_TABLE);
+        for (int np = 1; np <= wtree::MAX_NPAN; ++np) {
+            std::vector<int> end;                        // per slot: last panel of its occupant
+            for (int k = 0; k < np; ++k)                 // blocks by start panel k, then by cb
+                for (int cb = k; cb < np; ++cb) {
+                    int sl = 0;
+                    while (sl < (int)end.size() && end[sl] >= k) ++sl;
+                    if (sl == (int)end.size()) end.push_back(cb);
+                    else end[sl] = cb;
+                    tab[wtree::slot_off(np) + cb * (cb + 1) / 2 + k] = (unsigned short)sl;
+                }
+            if ((int)end.size() > wtree::max_live(np)) return cudaErrorInvalidValue;
+        }
+        cudaError_t e = cudaMemcpyToSymbol(wtree::c_slot, tab.data(), sizeof(unsigned short) * tab.size());
+        if (e != cudaSuccess) return e;
+        tables = true;
+    }
     const size_t bytes = wtree::smem_doubles(npan) * sizeof(double);
     cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)(count + 1) * wtree::MAX_NPAN, st);
     if (e != cudaSuccess) return e;
