@@ -264,6 +264,17 @@ cudaError_t launch_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_
 // Y1's columns 8P..8P+7 to the right subtree's head, then the panel flag.
 namespace wtree {
 
+#ifdef TSQR_TREE_PROBE
+__device__ unsigned long long g_tprobe[32 * 8];
+#define TPROBE(i) do { if (threadIdx.x == 0 && blockIdx.x == 0) { unsigned long long t; \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); g_tprobe[P * 8 + (i)] = t; } } while (0)
+#define SPROBE(i) do { if (threadIdx.x == 0 && blockIdx.x == 0 && P == 20 && jj < 4) { unsigned long long t; \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); g_tprobe[208 + jj * 8 + (i)] = t; } } while (0)
+#else
+#define TPROBE(i)
+#define SPROBE(i)
+#endif
+
 constexpr int NT = 256;
 constexpr int MAX_NPAN = 28;
 
@@ -285,7 +296,7 @@ __host__ __device__ inline int max_live(int npan) {
     return m;
 }
 __host__ __device__ inline size_t smem_doubles(int npan) {
-    return (size_t)(max_live(npan) + npan) * 64 + 64 + 64 + 8 + 2 * 8 * npan;
+    return (size_t)(max_live(npan) + npan + 1) * 64 + 64 + 64 + 8 + 2 * 8 * npan + 8 * 9;
 }
 
 __device__ __forceinline__ double *blk(double *Rb, int so, int k, int cb) {
@@ -310,8 +321,13 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
     const int npan = (n + 7) / 8;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
     double *Rb = sm;                                 // max_live(npan) block slots (see c_slot)
-    double *Ra = Rb + 64 * max_live(npan);           // npan blocks: R_a's pivot rows of the panel
-    double *Gs = Ra + 64 * npan, *Ts = Gs + 64, *t8 = Ts + 64, *xs = t8 + 8;   // xs: 2 x 8 npan
+    // npan + 1 blocks shared by the panel's column of R_b, contiguous (PB(k) =
+    // Wb + 64 k, k <= P: the steps, T, the update's Y and the Y1 publish read it
+    // without slot lookups) and R_a's pivot rows (Ra(cb) = Wb + 64 (cb + 1), cb >= P)
+    double *Wb = Rb + 64 * max_live(npan);
+    double *Ra = Wb + 64;                            // Ra + 64 cb = Wb + 64 (cb + 1)
+    double *Gs = Wb + 64 * (npan + 1), *Ts = Gs + 64, *t8 = Ts + 64, *xs = t8 + 8;   // xs: 2 x 8 npan
+    double *part = xs + 2 * 8 * npan;                // per-warp partial dots of a step (8 x 9)
     const int b = nodes[blockIdx.x], a = node_a[b];
     const int so = slot_off(npan);
     double *Ha = A + tile_row0[a], *Hb = A + tile_row0[b];
@@ -319,6 +335,7 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
     double *tau_out = tau_node + (int64_t)b * n;
     double *tc = tcache_node + (int64_t)b * npan * 64;
     for (int P = 0; P < npan; ++P) {
+        TPROBE(0);
         if (pl >= 0) wait_flag_cta(flags + pl * MAX_NPAN + P);
         if (pr >= 0) wait_flag_cta(flags + pr * MAX_NPAN + P);
         // row block P of R_a and R_b (upper part), column blocks P..npan-1
@@ -342,35 +359,58 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                 if (e < 64 * (npan - P)) {
                     const int cb = P + (e >> 6), cl = (e >> 3) & 7, r = e & 7;
                     Ra[64 * cb + 8 * cl + r] = va[u];
-                    blk(Rb, so, P, cb)[8 * cl + r] = vb[u];
+                    (cb == P ? Wb + 64 * P : blk(Rb, so, P, cb))[8 * cl + r] = vb[u];
                 }
+            }
+            // the panel's column blocks (k, P), k < P, from their slots into PB
+            for (int e = threadIdx.x; e < 32 * P; e += NT) {
+                const int k = e >> 5, o = 2 * (e & 31);
+                *reinterpret_cast<double2 *>(Wb + 64 * k + o) =
+                    *reinterpret_cast<const double2 *>(blk(Rb, so, k, P) + o);
             }
         }
         __syncthreads();
-        if (warp == 0) {
-            // pivot column (column 8P of R_b, rows 0..8P+7) -> xs[0]
-            for (int k = 0; k <= P; ++k)
-                if (l4 == 0)
-                    *reinterpret_cast<double2 *>(xs + 8 * k + 2 * q) =
-                        *reinterpret_cast<const double2 *>(blk(Rb, so, k, P) + 2 * q);
-            __syncwarp();
-            double *RaP = Ra + 64 * P;
+        TPROBE(1);
+        // the 8 structured Householder steps of panel P, all warps: warp w owns
+        // the panel's row blocks k = w, w + 8, ... (k <= P); per step the warps'
+        // partial dots meet in smem, every warp sums them in the same order and
+        // runs the same dlarfg, then updates its own blocks
+        double *RaP = Ra + 64 * P;
+        for (int k = warp; k <= P; k += NT / 32)          // pivot column 8P -> xs[0]
+            if (l4 == 0)
+                *reinterpret_cast<double2 *>(xs + 8 * k + 2 * q) =
+                    *reinterpret_cast<const double2 *>(Wb + 64 * k + 2 * q);
+        __syncthreads();
+        {
             const int jn = min(8, n - 8 * P);
 #pragma unroll 1
             for (int jj = 0; jj < jn; ++jj) {
                 const double *xr = xs + (jj & 1) * 8 * npan;
+                double *xw = xs + ((jj + 1) & 1) * 8 * npan;
+                SPROBE(0);
                 double d0 = 0.0, d1 = 0.0, s0 = 0.0, s1 = 0.0;
 #pragma unroll 4
-                for (int k = 0; k <= P; ++k) {
+                for (int k = warp; k <= P; k += NT / 32) {
                     const double2 x = *reinterpret_cast<const double2 *>(xr + 8 * k + 2 * q);
-                    const double2 v = *reinterpret_cast<const double2 *>(blk(Rb, so, k, P) + 8 * l4 + 2 * q);
+                    const double2 v = *reinterpret_cast<const double2 *>(Wb + 64 * k + 8 * l4 + 2 * q);
                     d0 = fma(x.x, v.x, d0);
                     d1 = fma(x.y, v.y, d1);
                     s0 = fma(x.x, x.x, s0);
                     s1 = fma(x.y, x.y, s1);
                 }
-                double d, s2;
-                chunk::quad_sums(d, s2, d0 + d1, s0 + s1);
+                double dw, sw;
+                chunk::quad_sums(dw, sw, d0 + d1, s0 + s1);
+                if (q == 0) part[warp * 9 + l4] = dw;
+                if (lane == 0) part[warp * 9 + 8] = sw;
+                __syncthreads();
+                SPROBE(1);
+                double d = 0.0, s2 = 0.0;
+#pragma unroll
+                for (int w2 = 0; w2 < NT / 32; ++w2) {
+                    d += part[w2 * 9 + l4];
+                    s2 += part[w2 * 9 + 8];
+                }
+                SPROBE(2);
                 const double alpha = RaP[8 * jj + jj];
                 const double rj = RaP[8 * l4 + jj];
                 const House h = house_bf(alpha, s2);
@@ -378,30 +418,36 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                 const double u = (l4 > jj) ? h.tau * h.scale * w : (l4 == jj ? 1.0 : 0.0);
                 const double g = (l4 == jj) ? h.scale : 0.0;
                 const double rnew = (l4 == jj) ? h.beta : fma(-h.tau, w, rj);
-                double *xw = xs + ((jj + 1) & 1) * 8 * npan;
+                SPROBE(3);
 #pragma unroll 4
-                for (int k = 0; k <= P; ++k) {
+                for (int k = warp; k <= P; k += NT / 32) {
                     const double2 x = *reinterpret_cast<const double2 *>(xr + 8 * k + 2 * q);
-                    double2 *vp = reinterpret_cast<double2 *>(blk(Rb, so, k, P) + 8 * l4 + 2 * q);
+                    double2 *vp = reinterpret_cast<double2 *>(Wb + 64 * k + 8 * l4 + 2 * q);
                     double2 v = *vp;
                     v.x = fma(g, x.x, fma(-u, x.x, v.x));
                     v.y = fma(g, x.y, fma(-u, x.y, v.y));
                     *vp = v;
                     if (l4 == jj + 1) *reinterpret_cast<double2 *>(xw + 8 * k + 2 * q) = v;
                 }
-                __syncwarp();
-                if (q == 0 && l4 >= jj) RaP[8 * l4 + jj] = rnew;
-                if (q == 0 && l4 < jj) Gs[l4 * 8 + jj] = h.scale * d;
-                if (lane == 0) t8[jj] = h.tau;
-                __syncwarp();
+                SPROBE(4);
+                if (warp == 0) {          // row jj of R_a (no other warp reads it again this panel)
+                    if (q == 0 && l4 >= jj) RaP[8 * l4 + jj] = rnew;
+                    if (q == 0 && l4 < jj) Gs[l4 * 8 + jj] = h.scale * d;
+                    if (lane == 0) t8[jj] = h.tau;
+                }
+                __syncthreads();          // xw complete; part free for the next step
             }
-            chunk::pad_steps(Gs, t8, jn);
-            __syncwarp();
-            if (lane < 8 && 8 * P + lane < n) tau_out[8 * P + lane] = t8[lane];
-            build_t(Gs, t8, Ts);
-            *reinterpret_cast<double2 *>(tc + 64 * P + 2 * lane) = *reinterpret_cast<const double2 *>(Ts + 2 * lane);
+            if (warp == 0) {
+                chunk::pad_steps(Gs, t8, jn);
+                __syncwarp();
+                if (lane < 8 && 8 * P + lane < n) tau_out[8 * P + lane] = t8[lane];
+                build_t(Gs, t8, Ts);
+                *reinterpret_cast<double2 *>(tc + 64 * P + 2 * lane) =
+                    *reinterpret_cast<const double2 *>(Ts + 2 * lane);
+            }
         }
         __syncthreads();
+        TPROBE(2);
         // trailing column blocks, split over the warps
         {
             const double tb0 = Ts[(2 * q) * 8 + l4], tb1 = Ts[(2 * q + 1) * 8 + l4];
@@ -410,7 +456,7 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
 #pragma unroll 4
                 for (int k = 0; k <= P; ++k) {
                     const double2 c = *reinterpret_cast<const double2 *>(blk(Rb, so, k, cb) + 8 * l4 + 2 * q);
-                    const double2 y = *reinterpret_cast<const double2 *>(blk(Rb, so, k, P) + 8 * l4 + 2 * q);
+                    const double2 y = *reinterpret_cast<const double2 *>(Wb + 64 * k + 8 * l4 + 2 * q);
                     dmma(w0[k & 1], w1[k & 1], c.x, y.x);
                     dmma(w0[k & 1], w1[k & 1], c.y, y.y);
                 }
@@ -425,7 +471,7 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                 *rp = rv;
 #pragma unroll 4
                 for (int k = 0; k <= P; ++k) {
-                    const double *yb = blk(Rb, so, k, P);
+                    const double *yb = Wb + 64 * k;
                     const double yt0 = yb[8 * (2 * q) + l4], yt1 = yb[8 * (2 * q + 1) + l4];
                     double2 *cp = reinterpret_cast<double2 *>(blk(Rb, so, k, cb) + 8 * l4 + 2 * q);
                     double2 c = *cp;
@@ -436,6 +482,7 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
             }
         }
         __syncthreads();
+        TPROBE(3);
         // publish: R rows 8P..8P+7 -> tile a's head, Y1 columns 8P..8P+7 -> tile b's head
         for (int e = threadIdx.x; e < 64 * (npan - P); e += NT) {
             const int cb = P + (e >> 6), cl = (e >> 3) & 7, r = e & 7;
@@ -445,13 +492,20 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
         for (int e = threadIdx.x; e < 64 * (P + 1); e += NT) {
             const int k = e >> 6, cl = (e >> 3) & 7, r = e & 7;
             const int i = 8 * k + r, c = 8 * P + cl;
-            if (i <= c && c < n) Hb[i + (int64_t)c * lda] = blk(Rb, so, k, P)[8 * cl + r];
+            if (i <= c && c < n) Hb[i + (int64_t)c * lda] = Wb[64 * k + 8 * cl + r];
         }
         __threadfence();
         __syncthreads();
+        TPROBE(4);
         if (threadIdx.x == 0) *reinterpret_cast<volatile int *>(flags + b * MAX_NPAN + P) = 1;
     }
 }
+
+#ifdef TSQR_TREE_PROBE
+extern "C" int tsqr_tree_probe_dump(unsigned long long *host) {
+    return (int)cudaMemcpyFromSymbol(host, wtree::g_tprobe, sizeof(unsigned long long) * 32 * 8);
+}
+#endif
 
 bool wide_tree_pipe_ok(int n) { return (n + 7) / 8 <= wtree::MAX_NPAN; }
 
