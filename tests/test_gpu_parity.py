@@ -206,21 +206,3 @@ def test_tree_reuse_and_repeat_determinism():
     assert tree.handle.value == h                     # workspace reused
     assert torch.equal(R1, R2) and torch.equal(A1, A2)  # bitwise deterministic
     tree.free()
-
-
-def test_config3_full_size():
-    # BASELINE config 3: 100,000 x 200, block rows 2048 (49 tiles), apply Q^T to C (k = 64)
-    m, n, b, k = 100_000, 200, 2048, 64
-    A0, Ad, R, tree, p, f = _run(m, n, b, b, seed=0)
-    Rg = _np(R)
-    assert orc.rel_fro(orc.sign_normalise(Rg), orc.sign_normalise(f.R)) <= TOL_R
-    assert np.linalg.norm(Rg.T @ Rg - A0.T @ A0) / np.linalg.norm(A0) ** 2 <= 1e-14
-    Ct = inputs.gaussian(m, k, seed=1)
-    C0 = _np(Ct).copy()
-    Cd = Ct.cuda()
-    T.apply_qt(tree, Cd)
-    torch.cuda.synchronize()
-    Cg = _np(Cd)
-    Co = orc.tsqr_apply_qt(f, C0)
-    assert orc.rel_fro(Cg, Co) <= TOL_R
-    tree.free()
