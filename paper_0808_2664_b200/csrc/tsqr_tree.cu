@@ -430,12 +430,12 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                     if (l4 == jj + 1) *reinterpret_cast<double2 *>(xw + 8 * k + 2 * q) = v;
                 }
                 SPROBE(4);
-                if (warp == 0) {          // row jj of R_a (no other warp reads it again this panel)
-                    if (q == 0 && l4 >= jj) RaP[8 * l4 + jj] = rnew;
+                if (warp == 0) {
                     if (q == 0 && l4 < jj) Gs[l4 * 8 + jj] = h.scale * d;
                     if (lane == 0) t8[jj] = h.tau;
                 }
-                __syncthreads();          // xw complete; part free for the next step
+                __syncthreads();          // xw complete; part free; every warp has read R_a row jj
+                if (warp == 0 && q == 0 && l4 >= jj) RaP[8 * l4 + jj] = rnew;   // read again only after the panel
             }
             if (warp == 0) {
                 chunk::pad_steps(Gs, t8, jn);

@@ -396,13 +396,143 @@ __device__ __forceinline__ void apply_panel_cols(const double *Ys, const double 
 
 template <int KM>
 struct LeafSmem {
+    // KM <= 16: panels are applied to the trailing columns in pairs (16
+    // reflectors per pass over C: half the passes); Y of a pair is H x 16
+    static constexpr bool TWO = KM <= 16;
+    static constexpr int YW = TWO ? 16 : 8;
     double part[2][NW][9];
     double piv[2][8];
-    double Gs[64], Ts[64], t8[8];
+    double Gs[64], Ts[3][64], t8[8];           // T of panel p (slot p & 1), T01 of a pair
+    double gp[NW][64];                         // per-warp partial Gram Y0^T Y1 of a pair
     double xs[NW][2][8 * KM];
-    double Ys[8];              // H_pad x 8 (the launch sizes it to the tallest tile)
-    static size_t bytes(int max_rows) { return sizeof(LeafSmem) + sizeof(double) * 8 * ((max_rows + 7) / 8 * 8); }
+    double Ys[8];              // H_pad x YW (the launch sizes it to the tallest tile)
+    static size_t bytes(int max_rows) { return sizeof(LeafSmem) + sizeof(double) * YW * ((max_rows + 7) / 8 * 8); }
 };
+
+// C <- (I - Y T16^T Y^T) C for a pair of panels (Y = [Y0 Y1], H x 16 in Ys,
+// T16 = [T0 T01; 0 T1], LAPACK's forward compact WY of 16 reflectors) on the
+// columns [c_lo, c_hi) and rows [8 rb0, H) of C: one W pass and one update
+// pass over C for 16 reflectors, each software-pipelined like apply_panel_cols.
+template <int U>
+__device__ __forceinline__ void w_grp16(double (&w0)[2], double (&w1)[2], double (&v0)[2], double (&v1)[2],
+                                        const double (&cv)[U][2], const double *Ys, int nrb, int k0) {
+    const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        if (k0 + u < nrb) {
+            const int r = 8 * (k0 + u) + 2 * q;
+            dmma(w0[u & 1], w1[u & 1], cv[u][0], Ys[r * 16 + l4]);
+            dmma(w0[u & 1], w1[u & 1], cv[u][1], Ys[(r + 1) * 16 + l4]);
+            dmma(v0[u & 1], v1[u & 1], cv[u][0], Ys[r * 16 + 8 + l4]);
+            dmma(v0[u & 1], v1[u & 1], cv[u][1], Ys[(r + 1) * 16 + 8 + l4]);
+        }
+    }
+}
+template <int U>
+__device__ __forceinline__ void upd_grp16(double (&cv)[U][2], double *cp, bool okc, int H, const double *Ys,
+                                          int nrb, int k0, double p0, double p1, double r0, double r1) {
+    const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        if (k0 + u < nrb) {
+            const double2 y = *reinterpret_cast<const double2 *>(Ys + (8 * (k0 + u) + l4) * 16 + 2 * q);
+            const double2 z = *reinterpret_cast<const double2 *>(Ys + (8 * (k0 + u) + l4) * 16 + 8 + 2 * q);
+            dmma(cv[u][0], cv[u][1], -p0, y.x);
+            dmma(cv[u][0], cv[u][1], -p1, y.y);
+            dmma(cv[u][0], cv[u][1], -r0, z.x);
+            dmma(cv[u][0], cv[u][1], -r1, z.y);
+            const int r = 8 * (k0 + u) + 2 * q;
+            if (okc && r < H) cp[r] = cv[u][0];
+            if (okc && r + 1 < H) cp[r + 1] = cv[u][1];
+        }
+    }
+}
+__device__ __forceinline__ void apply_pair_cols(const double *Ys, const double *T0, const double *T1,
+                                                const double *T01, double *C, int64_t ldc, int H, int rb0, int c_lo,
+                                                int c_hi) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+    // B operands T(2q+e, l4) of the three 8x8 blocks (forward: Q^T uses T16^T on the left of Y^T)
+    const double a0 = T0[(2 * q) * 8 + l4], a1 = T0[(2 * q + 1) * 8 + l4];
+    const double b0 = T1[(2 * q) * 8 + l4], b1 = T1[(2 * q + 1) * 8 + l4];
+    const double x0 = T01[(2 * q) * 8 + l4], x1 = T01[(2 * q + 1) * 8 + l4];
+    const int nrb = (H + 7) / 8;
+    constexpr int U = 4;                       // row blocks per load group (register budget of 2 CTAs/SM)
+    for (int cb = c_lo / 8 + warp; 8 * cb < c_hi; cb += NW) {
+        const int col = 8 * cb + l4;
+        const bool okc = col < c_hi;
+        double *cp = C + (int64_t)(okc ? col : c_lo) * ldc;
+        double w0[2] = {0.0, 0.0}, w1[2] = {0.0, 0.0}, v0[2] = {0.0, 0.0}, v1[2] = {0.0, 0.0};
+        double ca[U][2], cb2[U][2];
+        load_grp<U>(ca, cp, okc, H, rb0);
+        for (int k0 = rb0; k0 < nrb; k0 += 2 * U) {
+            if (k0 + U < nrb) load_grp<U>(cb2, cp, okc, H, k0 + U);
+            w_grp16<U>(w0, w1, v0, v1, ca, Ys, nrb, k0);
+            if (k0 + U >= nrb) break;
+            if (k0 + 2 * U < nrb) load_grp<U>(ca, cp, okc, H, k0 + 2 * U);
+            w_grp16<U>(w0, w1, v0, v1, cb2, Ys, nrb, k0 + U);
+        }
+        // P0 = W0^T T0, P1 = W0^T T01 + W1^T T1 (W^T = C^T [Y0 Y1], fragments of 8 columns)
+        const double we = w0[0] + w0[1], wo = w1[0] + w1[1], ve = v0[0] + v0[1], vo = v1[0] + v1[1];
+        double p0 = 0.0, p1 = 0.0, r0 = 0.0, r1 = 0.0;
+        dmma(p0, p1, we, a0);
+        dmma(p0, p1, wo, a1);
+        dmma(r0, r1, we, x0);
+        dmma(r0, r1, wo, x1);
+        dmma(r0, r1, ve, b0);
+        dmma(r0, r1, vo, b1);
+        load_grp<U>(ca, cp, okc, H, rb0);
+        for (int k0 = rb0; k0 < nrb; k0 += 2 * U) {
+            if (k0 + U < nrb) load_grp<U>(cb2, cp, okc, H, k0 + U);
+            upd_grp16<U>(ca, cp, okc, H, Ys, nrb, k0, p0, p1, r0, r1);
+            if (k0 + U >= nrb) break;
+            if (k0 + 2 * U < nrb) load_grp<U>(ca, cp, okc, H, k0 + 2 * U);
+            upd_grp16<U>(cb2, cp, okc, H, Ys, nrb, k0 + U, p0, p1, r0, r1);
+        }
+    }
+}
+
+// apply_panel_cols on a Y stored with row stride YW (one panel's 8 columns at Ys + off)
+template <int YW>
+__device__ __forceinline__ void apply_one_cols(const double *Ys, const double *Tg, double *C, int64_t ldc, int H,
+                                               int rb0, int c_lo, int c_hi) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+    const double tb0 = Tg[(2 * q) * 8 + l4], tb1 = Tg[(2 * q + 1) * 8 + l4];
+    const int nrb = (H + 7) / 8;
+    for (int cb = c_lo / 8 + warp; 8 * cb < c_hi; cb += NW) {
+        const int col = 8 * cb + l4;
+        const bool okc = col < c_hi;
+        double *cp = C + (int64_t)(okc ? col : c_lo) * ldc;
+        double w0[2] = {0.0, 0.0}, w1[2] = {0.0, 0.0};
+        for (int k0 = rb0; k0 < nrb; k0 += UNR) {
+            double cv[UNR][2];
+            load_grp<UNR>(cv, cp, okc, H, k0);
+#pragma unroll
+            for (int u = 0; u < UNR; ++u)
+                if (k0 + u < nrb) {
+                    const int r = 8 * (k0 + u) + 2 * q;
+                    dmma(w0[u & 1], w1[u & 1], cv[u][0], Ys[r * YW + l4]);
+                    dmma(w0[u & 1], w1[u & 1], cv[u][1], Ys[(r + 1) * YW + l4]);
+                }
+        }
+        double p0 = 0.0, p1 = 0.0;
+        dmma(p0, p1, w0[0] + w0[1], tb0);
+        dmma(p0, p1, w1[0] + w1[1], tb1);
+        for (int k0 = rb0; k0 < nrb; k0 += UNR) {
+            double cv[UNR][2];
+            load_grp<UNR>(cv, cp, okc, H, k0);
+#pragma unroll
+            for (int u = 0; u < UNR; ++u)
+                if (k0 + u < nrb) {
+                    const int r8 = 8 * (k0 + u) + l4;
+                    dmma(cv[u][0], cv[u][1], -p0, Ys[r8 * YW + 2 * q]);
+                    dmma(cv[u][0], cv[u][1], -p1, Ys[r8 * YW + 2 * q + 1]);
+                    const int r = 8 * (k0 + u) + 2 * q;
+                    if (okc && r < H) cp[r] = cv[u][0];
+                    if (okc && r + 1 < H) cp[r + 1] = cv[u][1];
+                }
+        }
+    }
+}
 
 // Blocked compact-WY QR of one tile (H rows, H <= 64 KM): the panel is
 // row-split over the warps (warp w: rows [w 8KM, (w+1) 8KM)), one
@@ -414,8 +544,12 @@ __device__ void wide_leaf_qr(double *At, int64_t lda, int H, int n, double *tau,
     const int npan = (n + 7) / 8;
     const int rbase = warp * 8 * KM;
     const int Hp = 8 * ((H + 7) / 8);
+    constexpr bool TWO = LeafSmem<KM>::TWO;
+    constexpr int YW = LeafSmem<KM>::YW;
     for (int p = 0; p < npan; ++p) {
         const int c = 8 * p + l4;
+        const int yo = TWO ? 8 * (p & 1) : 0;            // this panel's 8 columns of Ys
+        double *Tp = S.Ts[TWO ? (p & 1) : 0];
         double *colp = At + (int64_t)(c < n ? c : 0) * lda;
         double a[KM][2];
 #pragma unroll
@@ -505,7 +639,8 @@ __device__ void wide_leaf_qr(double *At, int64_t lda, int H, int n, double *tau,
             for (int e = 0; e < 2; ++e) {
                 const int r = rbase + 8 * k + 2 * q + e;
                 if (c < n && r < H) colp[r] = a[k][e];
-                if (r >= 8 * p && r < Hp) S.Ys[r * 8 + l4] = (c >= n || r < c || r >= H) ? 0.0 : (r == c ? 1.0 : a[k][e]);
+                if (r >= 8 * (TWO ? (p & ~1) : p) && r < Hp)     // a pair's Y1 is zero on Y0's first rows
+                    S.Ys[r * YW + yo + l4] = (c >= n || r < c || r >= H) ? 0.0 : (r == c ? 1.0 : a[k][e]);
             }
         __syncthreads();
         if (warp == 0) {
@@ -524,14 +659,63 @@ __device__ void wide_leaf_qr(double *At, int64_t lda, int H, int n, double *tau,
             if (lane < 8) {
 #pragma unroll
                 for (int cc = 0; cc < 8; ++cc) {
-                    S.Ts[lane * 8 + cc] = row[cc];
+                    Tp[lane * 8 + cc] = row[cc];
                     tcache[p * 64 + lane * 8 + cc] = row[cc];
                 }
                 if (8 * p + lane < n) tau[8 * p + lane] = S.t8[lane];
             }
         }
         __syncthreads();
-        if (p + 1 < npan) apply_panel_cols<true>(S.Ys, S.Ts, At, lda, H, p, 8 * (p + 1), n);
+        if (p + 1 == npan) break;
+        if (!TWO) {
+            apply_one_cols<YW>(S.Ys, Tp, At, lda, H, p, 8 * (p + 1), n);
+        } else if ((p & 1) == 0) {
+            // first panel of a pair: update only the pair's second column block
+            apply_one_cols<YW>(S.Ys, Tp, At, lda, H, p, 8 * (p + 1), min(n, 8 * (p + 2)));
+        } else {
+            // second panel of a pair: T01 = -T0 (Y0^T Y1) T1, then the 16-reflector update
+            {
+                double g0 = 0.0, g1 = 0.0;
+                for (int k = p + warp; k < Hp / 8; k += NW) {         // Y1 is zero above row 8p
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int r = 8 * k + 2 * q + e;
+                        dmma(g0, g1, S.Ys[r * 16 + l4], S.Ys[r * 16 + 8 + l4]);
+                    }
+                }
+                *reinterpret_cast<double2 *>(&S.gp[warp][8 * l4 + 2 * q]) = make_double2(g0, g1);
+            }
+            __syncthreads();
+            if (warp == 0) {
+                // lane (i, j0): T01(i, j0 + e) = -sum_a T0(i, a) sum_b G(a, b) T1(b, j0 + e),
+                // G = Y0^T Y1 = sum of the warps' partials
+                const int i = lane >> 2, j0 = 2 * (lane & 3);
+                double t01[2] = {0.0, 0.0};
+                // T01(i, j) = - sum_a T0(i, a) sum_b G(a, b) T1(b, j)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int j = j0 + e;
+                    double acc = 0.0;
+#pragma unroll
+                    for (int a = 0; a < 8; ++a) {
+                        double gb = 0.0;
+#pragma unroll
+                        for (int bb = 0; bb < 8; ++bb) {
+                            double gab = 0.0;
+#pragma unroll
+                            for (int w = 0; w < NW; ++w) gab += S.gp[w][8 * a + bb];
+                            gb = fma(gab, S.Ts[1][bb * 8 + j], gb);
+                        }
+                        acc = fma(S.Ts[0][i * 8 + a], gb, acc);
+                    }
+                    t01[e] = -acc;
+                }
+                S.Ts[2][i * 8 + j0] = t01[0];
+                S.Ts[2][i * 8 + j0 + 1] = t01[1];
+            }
+            __syncthreads();
+            if (p + 1 < npan) apply_pair_cols(S.Ys, S.Ts[0], S.Ts[1], S.Ts[2], At, lda, H, p - 1, 8 * (p + 1), n);
+        }
         __syncthreads();
     }
 }
