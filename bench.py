@@ -215,7 +215,7 @@ def run_ours(args, cfg):
         if world == 1:
             _, tree = T.factor(A, b, s, R=R, tree=tree, stage_timing=True)
         else:
-            st = tdist.factor(A, b, s, engine=engine)
+            st = tdist.factor(A, b, s, engine=engine, tree=tree)   # workspace reused across steps
             tree = st.tree
         ev_f.record(stream)
         if cfg["op"] == "form_q":

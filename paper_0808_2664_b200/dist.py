@@ -31,8 +31,9 @@ class CudaEngine:
     def __init__(self, stage_timing: bool = False):
         self.stage_timing = stage_timing
 
-    def factor_local(self, A, block_rows, tile_rows, nranks, rank):
-        return api.factor(A, block_rows, tile_rows, nranks=nranks, rank=rank, stage_timing=self.stage_timing)
+    def factor_local(self, A, block_rows, tile_rows, nranks, rank, tree=None):
+        return api.factor(A, block_rows, tile_rows, nranks=nranks, rank=rank, tree=tree,
+                          stage_timing=self.stage_timing)
 
     def empty(self, shape, like):
         return torch.empty(shape, dtype=torch.float64, device=like.device)
@@ -75,9 +76,12 @@ class RankState:
     sent: list = field(default_factory=list)      # (round, words) per message, for the count pins
 
     # ---------------------------------------------------------------- factor
-    def factor_local(self, A, block_rows, tile_rows):
+    def factor_local(self, A, block_rows, tile_rows, tree=None):
         self.n = A.shape[0]
-        self.R, self.tree = self.engine.factor_local(A, block_rows, tile_rows, self.nranks, self.rank)
+        if tree is None:
+            self.R, self.tree = self.engine.factor_local(A, block_rows, tile_rows, self.nranks, self.rank)
+        else:                                        # reuse a previous factor's workspace
+            self.R, self.tree = self.engine.factor_local(A, block_rows, tile_rows, self.nranks, self.rank, tree=tree)
 
     def factor_send(self, rnd):
         buf = self.engine.empty((self.n * (self.n + 1) // 2,), self.R)
@@ -114,12 +118,13 @@ def _exchange(send: torch.Tensor, partner: int, group=None) -> torch.Tensor:
 
 
 # ------------------------------------------------------ torch.distributed drivers
-def factor(A_local, block_rows: int, tile_rows: int = 0, engine=None, group=None) -> RankState:
-    """Collective over the process group: returns the rank state (R replicated in .R)."""
+def factor(A_local, block_rows: int, tile_rows: int = 0, engine=None, group=None, tree=None) -> RankState:
+    """Collective over the process group: returns the rank state (R replicated in .R).
+    tree: a previous factor's tree of the same shape, whose workspace is reused."""
     import torch.distributed as dist
     rank, nranks = dist.get_rank(group), dist.get_world_size(group)
     st = RankState(engine or CudaEngine(), rank, nranks)
-    st.factor_local(A_local, block_rows, tile_rows)
+    st.factor_local(A_local, block_rows, tile_rows, tree)
     for rnd in range(1, rounds_of(nranks) + 1):
         partner = rank ^ (1 << (rnd - 1))
         recv = _exchange(st.factor_send(rnd), partner, group)
