@@ -90,9 +90,6 @@ struct Sync {
 // the spin (wait).  No MEMBAR: a fence.cta would also wait for the warp's
 // outstanding global stores.
 __device__ __forceinline__ void sync_wait(const int *c, int v) {
-#ifdef TSQR_NOWAIT                         // timing experiment only (results invalid)
-    return;
-#endif
     while (*reinterpret_cast<const volatile int *>(c) < v) {
     }
     asm volatile("" ::: "memory");

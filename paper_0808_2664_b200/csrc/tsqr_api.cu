@@ -25,9 +25,8 @@ struct tsqr_tree_s {
     cudaStream_t stream = nullptr;
     // device arrays
     int64_t *d_row0 = nullptr;
-    int *d_rows = nullptr, *d_tparent = nullptr, *d_node_a = nullptr, *d_nparent = nullptr;
-    double *d_tau_tile = nullptr, *d_tau_node = nullptr;
-    int *d_counters = nullptr;
+    int *d_rows = nullptr, *d_node_a = nullptr;
+    double *d_tau_node = nullptr;
     double *d_cross_y1 = nullptr, *d_cross_tau = nullptr;
     int cross_rounds = 0, cross_done = 0;
     double *d_xbuf = nullptr;
@@ -49,7 +48,6 @@ struct tsqr_tree_s {
     double *d_tcache_node = nullptr, *d_cross_tcache = nullptr, *d_wtmp = nullptr;
     int64_t wtmp_size = 0;
     std::vector<int> step_off;   // top-down: groups [step_off[g], step_off[g+1])
-    DevPlan dplan{};
 };
 
 static tsqr_status_t cuda_fail(cudaError_t e, const char *where) {
@@ -69,8 +67,8 @@ static tsqr_status_t debug_sync(const tsqr_tree_s *t, cudaStream_t st, const cha
 }
 
 static void free_tree_memory(tsqr_tree_s *t) {
-    void *ptrs[] = {t->d_row0, t->d_rows, t->d_tparent, t->d_node_a, t->d_nparent, t->d_tau_tile,
-                    t->d_tau_node, t->d_counters, t->d_cross_y1, t->d_cross_tau, t->d_xbuf,
+    void *ptrs[] = {t->d_row0, t->d_rows, t->d_node_a,
+                    t->d_tau_node, t->d_cross_y1, t->d_cross_tau, t->d_xbuf,
                     t->d_step_ids, t->d_pipe_nodes, t->d_prod_l, t->d_prod_r, t->d_pipe_flags,
                     t->d_tile_chunk0, t->d_cta_tile0, t->d_apply_cta_tile0, t->d_tau_chunk, t->d_tcache,
                     t->d_tcache_node, t->d_cross_tcache, t->d_wtmp};
@@ -223,12 +221,8 @@ static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t 
     };
     alloc((void **)&t->d_row0, sizeof(int64_t) * L);
     alloc((void **)&t->d_rows, sizeof(int) * L);
-    alloc((void **)&t->d_tparent, sizeof(int) * L);
     alloc((void **)&t->d_node_a, sizeof(int) * L);
-    alloc((void **)&t->d_nparent, sizeof(int) * L);
-    alloc((void **)&t->d_tau_tile, sizeof(double) * L * n);
     alloc((void **)&t->d_tau_node, sizeof(double) * L * n);
-    alloc((void **)&t->d_counters, sizeof(int) * L);
     alloc((void **)&t->d_cross_y1, sizeof(double) * (t->cross_rounds + 1) * n * n);
     alloc((void **)&t->d_cross_tau, sizeof(double) * (t->cross_rounds + 1) * n);
     alloc((void **)&t->d_step_ids, sizeof(int) * (ids.size() + 1));
@@ -287,9 +281,7 @@ static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t 
     std::vector<int> rows(p.tile_rows.begin(), p.tile_rows.end());
     e = cudaMemcpy(t->d_row0, p.tile_row0.data(), sizeof(int64_t) * L, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(t->d_rows, rows.data(), sizeof(int) * L, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(t->d_tparent, p.tile_parent.data(), sizeof(int) * L, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(t->d_node_a, p.node_a.data(), sizeof(int) * L, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(t->d_nparent, p.node_parent.data(), sizeof(int) * L, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && !ids.empty())
         e = cudaMemcpy(t->d_step_ids, ids.data(), sizeof(int) * ids.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess && !pipe.empty())
@@ -302,14 +294,12 @@ static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t 
         e = cudaMemcpy(t->d_cta_tile0, cta_tile0.data(), sizeof(int) * (grid + 1), cudaMemcpyHostToDevice);
     if (e == cudaSuccess)
         e = cudaMemcpy(t->d_apply_cta_tile0, apply_tile0.data(), sizeof(int) * (agrid + 1), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemset(t->d_counters, 0, sizeof(int) * L);
     if (e == cudaSuccess) e = cudaMemset(t->d_tau_node, 0, sizeof(double) * L * n);
     if (e != cudaSuccess) {
         free_tree_memory(t);
         delete t;
         return cuda_fail(e, "tsqr_factor setup");
     }
-    t->dplan = DevPlan{t->d_row0, t->d_rows, t->d_tparent, t->d_node_a, t->d_nparent, L};
     *out = t;
     return TSQR_OK;
 }

@@ -1,4 +1,5 @@
-// Host-side declarations of the kernel launchers (tsqr_kernels.cu).
+// Host-side declarations of the kernel launchers (tsqr_chain.cu, tsqr_cs.cu,
+// tsqr_tree.cu, tsqr_wide.cu, tsqr_wy.cu), called by the C-ABI in tsqr_api.cu.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -7,14 +8,6 @@
 
 namespace tsqr {
 
-struct DevPlan {
-    const int64_t *tile_row0;   // first local row of tile t
-    const int *tile_rows;       // rows of tile t
-    const int *tile_parent;     // node id of leaf t's first combine, -1: none
-    const int *node_a;          // by node id b: leftmost tile of the left subtree
-    const int *node_parent;     // by node id: next node, -1: local root
-    int L;                      // tiles
-};
 
 
 // Leaf stage on the chunk engine (tsqr_chain.cu).
