@@ -891,13 +891,25 @@ k_node_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, cons
                 na1 = (okc && rn + 1 < n) ? Ca[rn + 1 + co] : 0.0;
             }
             const double *yP = Yb + 64 * (P * (P + 1) / 2);           // block (0, P); block (kk, P) at + 64 kk
+            // groups of 4 blocks behind one uniform branch each; inside a group the
+            // blocks past P read block P (a valid address) and are zeroed by a
+            // select, so there is no per-block branch (their DMMAs add exact zeros)
             double w0[2] = {0.0, 0.0}, w1[2] = {0.0, 0.0};
 #pragma unroll
-            for (int kk = 0; kk < NPAN_NODE; ++kk) {
-                if (kk <= P) {
-                    const double2 y = *reinterpret_cast<const double2 *>(yP + 64 * kk + 8 * l4 + 2 * q);
-                    dmma(w0[kk & 1], w1[kk & 1], cb[kk][0], y.x);
-                    dmma(w0[kk & 1], w1[kk & 1], cb[kk][1], y.y);
+            for (int g = 0; g < NPAN_NODE; g += 4) {
+                if (g <= P) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int kk = g + u;
+                        if (kk < NPAN_NODE) {
+                            const bool ok = kk <= P;
+                            double2 y = *reinterpret_cast<const double2 *>(yP + 64 * (ok ? kk : P) + 8 * l4 + 2 * q);
+                            y.x = ok ? y.x : 0.0;
+                            y.y = ok ? y.y : 0.0;
+                            dmma(w0[u & 1], w1[u & 1], cb[kk][0], y.x);
+                            dmma(w0[u & 1], w1[u & 1], cb[kk][1], y.y);
+                        }
+                    }
                 }
             }
             double p0 = 0.0, p1 = 0.0;
@@ -906,11 +918,19 @@ k_node_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, cons
             if (okc && ra < n) Ca[ra + co] = ca0 - p0;
             if (okc && ra + 1 < n) Ca[ra + 1 + co] = ca1 - p1;
 #pragma unroll
-            for (int kk = 0; kk < NPAN_NODE; ++kk) {
-                if (kk <= P) {
-                    const double *yb = yP + 64 * kk;
-                    dmma(cb[kk][0], cb[kk][1], -p0, yb[8 * (2 * q) + l4]);
-                    dmma(cb[kk][0], cb[kk][1], -p1, yb[8 * (2 * q + 1) + l4]);
+            for (int g = 0; g < NPAN_NODE; g += 4) {
+                if (g <= P) {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int kk = g + u;
+                        if (kk < NPAN_NODE) {
+                            const bool ok = kk <= P;
+                            const double *yb = yP + 64 * (ok ? kk : P);
+                            const double y0 = ok ? yb[8 * (2 * q) + l4] : 0.0, y1 = ok ? yb[8 * (2 * q + 1) + l4] : 0.0;
+                            dmma(cb[kk][0], cb[kk][1], -p0, y0);
+                            dmma(cb[kk][0], cb[kk][1], -p1, y1);
+                        }
+                    }
                 }
             }
         }
