@@ -66,7 +66,9 @@ __device__ __forceinline__ void fix_dense(double *slot, int n, int r0) {
 
 template <class C, bool kFwd>
 __device__ __forceinline__ void cs_apply_panel(double (&cc)[C::KM][2], double (&cr)[C::NCB][2], int p, int r0,
-                                               const double *slot) {
+                                               const double *slot, bool &czero) {
+    // czero (form Q only): the chunk's rows of C are still all zero -- they become
+    // nonzero with the first panel applied to the chunk -- so W^T = C^T Y is skipped
     const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
     constexpr int KM = C::KM, NP = ApplyCs<C>::LDY, LDT = ApplyCs<C>::LDT;   // Yr / Yt strides
     if (8 * p >= r0 + C::CH) return;           // no reflector of panel p in this chunk
@@ -89,12 +91,15 @@ __device__ __forceinline__ void cs_apply_panel(double (&cc)[C::KM][2], double (&
         }
     }
     double w0[2] = {0.0, 0.0}, w1[2] = {0.0, 0.0};
+    if (!(kFwd == false && czero && !dense)) {
 #pragma unroll
-    for (int k = 0; k < KM; ++k) {
-        const double y0 = ys[(8 * k + 2 * q) * NP + l4], y1 = ys[(8 * k + 2 * q + 1) * NP + l4];
-        dmma(w0[k & 1], w1[k & 1], cc[k][0], y0);
-        dmma(w0[k & 1], w1[k & 1], cc[k][1], y1);
+        for (int k = 0; k < KM; ++k) {
+            const double y0 = ys[(8 * k + 2 * q) * NP + l4], y1 = ys[(8 * k + 2 * q + 1) * NP + l4];
+            dmma(w0[k & 1], w1[k & 1], cc[k][0], y0);
+            dmma(w0[k & 1], w1[k & 1], cc[k][1], y1);
+        }
     }
+    czero = false;
     double wt0 = w0[0] + w0[1], wt1 = w1[0] + w1[1];
     if (!dense) {
         wt0 += crp0;
@@ -216,9 +221,10 @@ k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                     __syncthreads();
                 }
                 double *Ck = Cm + row0 + r0;
+                bool czero = !kFwd;
 #pragma unroll 1
                 for (int pp = 0; pp < np; ++pp)
-                    cs_apply_panel<C, kFwd>(ccv, cr, kFwd ? pp : np - 1 - pp, r0, slot);
+                    cs_apply_panel<C, kFwd>(ccv, cr, kFwd ? pp : np - 1 - pp, r0, slot, czero);
 #pragma unroll
                 for (int kk = 0; kk < C::KM; ++kk)
 #pragma unroll
