@@ -239,7 +239,7 @@ static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t 
     alloc((void **)&t->d_pipe_nodes, sizeof(int) * L);
     alloc((void **)&t->d_prod_l, sizeof(int) * L);
     alloc((void **)&t->d_prod_r, sizeof(int) * L);
-    alloc((void **)&t->d_pipe_flags, sizeof(int) * L * 32);   // L x panels (<= 28 wide, 8 narrow)
+    alloc((void **)&t->d_pipe_flags, sizeof(int) * (L * 32 + 1));   // L x panels (<= 28 wide, 8 narrow) + ticket
     const int64_t nchunks = p.tile_chunk0[L];
     t->wide = n > 64;
     t->npan = (int)((n + 7) / 8);

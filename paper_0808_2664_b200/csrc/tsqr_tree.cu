@@ -13,8 +13,9 @@
 // (tile a), Y1 columns 8P..8P+7 -> the right subtree's head (tile b), both
 // upper triangles only (the leaf reflectors below stay); tau -> tau_node.
 // Nodes are numbered bottom-up, so a node depends only on lower-numbered
-// nodes, which were dispatched earlier (blocks are dispatched in order): the
-// spin-waits cannot deadlock.
+// nodes; blocks take their node range from a ticket counter when they start,
+// so a lower-numbered node always belongs to a block that is already resident
+// or finished: the spin-waits cannot deadlock.
 #include "tsqr_kernels.h"
 #include "chunk.cuh"
 
@@ -200,7 +201,13 @@ k_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *
             double *tcache_node) {
     extern __shared__ __align__(16) double sm[];
     const int warp = threadIdx.x >> 5;
-    const int i = blockIdx.x * NW + warp;
+    // logical block index from a ticket taken at start, so that every node a
+    // resident warp waits on belongs to a block that started earlier (is resident
+    // or done) whatever order the hardware dispatches blocks in
+    __shared__ int s_ticket;
+    if (threadIdx.x == 0) s_ticket = atomicAdd(flags + (count + 1) * C::NCB, 1);
+    __syncthreads();
+    const int i = s_ticket * NW + warp;
     if (i >= count) return;
     const int b = nodes[i], a = node_a[b];
     double *ws = sm + warp * C::WS;
@@ -236,7 +243,8 @@ cudaError_t launch_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_
     if (count == 0) return cudaSuccess;
     return tree_dispatch(n, [&](auto c) {
         using C = decltype(c);
-        cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)(count + 1) * C::NCB, st);  // ids <= count
+        // node flags (ids <= count) and the block ticket counter after them
+        cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * ((size_t)(count + 1) * C::NCB + 1), st);
         if (e != cudaSuccess) return e;
         e = cudaFuncSetAttribute((const void *)k_tree_pipe<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)C::BYTES);
@@ -328,7 +336,10 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
     double *Ra = Wb + 64;                            // Ra + 64 cb = Wb + 64 (cb + 1)
     double *Gs = Wb + 64 * (npan + 1), *Ts = Gs + 64, *t8 = Ts + 64, *xs = t8 + 8;   // xs: 2 x 8 npan
     double *part = xs + 2 * 8 * npan;                // per-warp partial dots of a step (8 x 9)
-    const int b = nodes[blockIdx.x], a = node_a[b];
+    __shared__ int s_ticket;                         // logical block index (see k_tree_pipe)
+    if (threadIdx.x == 0) s_ticket = atomicAdd(flags + (count + 1) * MAX_NPAN, 1);
+    __syncthreads();
+    const int b = nodes[s_ticket], a = node_a[b];
     const int so = slot_off(npan);
     double *Ha = A + tile_row0[a], *Hb = A + tile_row0[b];
     const int pl = prod_l[b], pr = prod_r[b];
@@ -535,7 +546,7 @@ cudaError_t launch_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *
         tables = true;
     }
     const size_t bytes = wtree::smem_doubles(npan) * sizeof(double);
-    cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)(count + 1) * wtree::MAX_NPAN, st);
+    cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * ((size_t)(count + 1) * wtree::MAX_NPAN + 1), st);
     if (e != cudaSuccess) return e;
     e = cudaFuncSetAttribute((const void *)k_wide_tree_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;
