@@ -53,14 +53,26 @@ __device__ __forceinline__ void wait_flag(const int *f) {
     __threadfence();
 }
 
+#ifdef TSQR_NTREE_PROBE
+__device__ unsigned long long g_ntprobe[8 * 8 * 2];
+#define NTPROBE(i) do { if ((threadIdx.x & 31) == 0 && (fme == g_nt_root || fme == g_nt_leaf)) { \
+    unsigned long long t_; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_)); \
+    g_ntprobe[(fme == g_nt_root ? 64 : 0) + P * 8 + (i)] = t_; } } while (0)
+__device__ int *g_nt_root, *g_nt_leaf;
+#else
+#define NTPROBE(i)
+#endif
+
 template <class C, int P>
 __device__ __forceinline__ void node_panel(NodeRegs<C> &rg, double *Ahead_a, double *Ahead_b, int64_t lda, int n,
                                            double *ws, double *tau_out, const int *fl, const int *fr, int *fme,
                                            double *R, int64_t ldr, double *tc) {
     const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
     double *Ra = ws + C::RA, *Ys = ws + C::YS, *Gs = ws + C::GS, *Ts = ws + C::TS, *t8 = ws + C::T8, *xs = ws + C::XS;
+    NTPROBE(0);
     if (fl) wait_flag(fl + P);
     if (fr) wait_flag(fr + P);
+    NTPROBE(1);
     // R_a rows 8P..8P+7 (upper part) -> smem; R_b row block P (upper part) -> registers
     double ra[2 * C::NCB];              // all loads in flight before the first use
 #pragma unroll
@@ -139,6 +151,7 @@ __device__ __forceinline__ void node_panel(NodeRegs<C> &rg, double *Ahead_a, dou
         Ys[(8 * k + 2 * q + 1) * 8 + l4] = rg.a[k][P][1];
     }
     __syncwarp();
+    NTPROBE(2);
     build_t(Gs, t8, Ts);
     *reinterpret_cast<double2 *>(tc + 64 * P + 2 * lane) = *reinterpret_cast<const double2 *>(Ts + 2 * lane);
     if constexpr (P + 1 < C::NCB) {
@@ -182,9 +195,11 @@ __device__ __forceinline__ void node_panel(NodeRegs<C> &rg, double *Ahead_a, dou
             const int i = 8 * k + 2 * q + e, c = 8 * P + l4;
             if (i <= c && c < n) Ahead_b[i + (int64_t)c * lda] = rg.a[k][P][e];
         }
+    NTPROBE(3);
     __threadfence();
     __syncwarp();
     if (lane == 0) *reinterpret_cast<volatile int *>(fme + P) = 1;
+    NTPROBE(4);
     if constexpr (P + 1 < C::NCB) node_panel<C, P + 1>(rg, Ahead_a, Ahead_b, lda, n, ws, tau_out, fl, fr, fme, R, ldr, tc);
 }
 
@@ -217,6 +232,10 @@ k_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *
 #pragma unroll
         for (int cb = 0; cb < C::NCB; ++cb) rg.a[k][cb][0] = rg.a[k][cb][1] = 0.0;
     const int pl = prod_l[b], pr = prod_r[b];
+#ifdef TSQR_NTREE_PROBE
+    if (i == 0 && (threadIdx.x & 31) == 0) g_nt_leaf = flags + b * C::NCB;
+    if (b == root && (threadIdx.x & 31) == 0) g_nt_root = flags + b * C::NCB;
+#endif
     node_panel<C, 0>(rg, A + tile_row0[a], A + tile_row0[b], lda, n, ws, tau_node + (int64_t)b * n,
                      pl >= 0 ? flags + pl * C::NCB : nullptr, pr >= 0 ? flags + pr * C::NCB : nullptr,
                      flags + b * C::NCB, b == root ? R : nullptr, ldr, tcache_node + (int64_t)b * C::NCB * 64);
@@ -512,6 +531,11 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
     }
 }
 
+#ifdef TSQR_NTREE_PROBE
+extern "C" int tsqr_ntree_probe_dump(unsigned long long *host) {
+    return (int)cudaMemcpyFromSymbol(host, g_ntprobe, sizeof(unsigned long long) * 128);
+}
+#endif
 #ifdef TSQR_TREE_PROBE
 extern "C" int tsqr_tree_probe_dump(unsigned long long *host) {
     return (int)cudaMemcpyFromSymbol(host, wtree::g_tprobe, sizeof(unsigned long long) * 32 * 8);
