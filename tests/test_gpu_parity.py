@@ -76,6 +76,10 @@ CASES = [
     (700, 57, 700, 100),         # n = 57: 32-row chunks, last panel has one real column
     (500, 63, 500, 250),         # n = 63
     (300, 9, 300, 40),           # n = 9: 64-row chunks taller than the 40-row tiles' chunks
+    (200, 200, 200, 200),        # wide m = n: one square tile, no tree
+    (65, 65, 65, 65),            # n = 65 square
+    (128, 64, 128, 64),          # tiles exactly n rows tall (two 64-row tiles)
+    (7000, 128, 3500, 512),      # n = 128 (16 panels, pairs), tiles of 500 rows, two blocks
 ]
 
 
