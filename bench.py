@@ -365,7 +365,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.config is None:
-        args.config = DEFAULT_CONFIG if args.gpus == 1 or True else "c2"
+        args.config = DEFAULT_CONFIG
     if args.warmup < 3:
         args.warmup = 3
     cfg = CONFIGS[args.config]
