@@ -269,37 +269,51 @@ def run_ours(args, cfg):
         dist.all_reduce(x, op=dist.ReduceOp.MAX)
         tf, ts, tl, tt = x.tolist()
 
-    # ---- e2e through the public API with pinned host buffers (host <-> device inside)
-    e2e = None
-    if world == 1:
-        A_h = A0.cpu().pin_memory()
-        R_h = torch.empty((n, n), dtype=torch.float64).pin_memory()
-        out_h = torch.empty((n, ml) if cfg["op"] == "form_q" else (k, ml), dtype=torch.float64).pin_memory()
-        C_h = C0.cpu().pin_memory() if C0 is not None else None
-        e_s, e_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        te = []
-        for it in range(max(2, min(args.steps, 10)) + 1):
-            e_s.record(stream)
-            A.copy_(A_h, non_blocking=True)
-            if C_h is not None:
-                C.copy_(C_h, non_blocking=True)
+    # ---- e2e through the public API with pinned host buffers (host <-> device inside);
+    # every rank copies its own slab, the time is the max over ranks
+    A_h = A0.cpu().pin_memory()
+    R_h = torch.empty((n, n), dtype=torch.float64).pin_memory()
+    out_h = torch.empty((n, ml) if cfg["op"] == "form_q" else (k, ml), dtype=torch.float64).pin_memory()
+    C_h = C0.cpu().pin_memory() if C0 is not None else None
+    e_s, e_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    te = []
+    for it in range(max(2, min(args.steps, 10)) + 1):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e_s.record(stream)
+        A.copy_(A_h, non_blocking=True)
+        if C_h is not None:
+            C.copy_(C_h, non_blocking=True)
+        if world == 1:
             _, tree = T.factor(A, b, s, R=R, tree=tree)
-            if cfg["op"] == "form_q":
-                T.form_q(tree, Q)
-                out_h.copy_(Q, non_blocking=True)
-            else:
+            Rr = R
+        else:
+            st = tdist.factor(A, b, s, engine=engine, tree=tree)
+            tree, Rr = st.tree, st.R
+        if cfg["op"] == "form_q":
+            T.form_q(tree, Q)                            # no communication (butterfly replication)
+            out_h.copy_(Q, non_blocking=True)
+        else:
+            if world == 1:
                 T.apply_qt(tree, C)
-                out_h.copy_(C, non_blocking=True)
-            R_h.copy_(R, non_blocking=True)
-            e_e.record(stream)
-            e_e.synchronize()
-            if it > 0:
-                te.append(e_s.elapsed_time(e_e))
-        t_e2e = statistics.mean(te)
-        h2d = 8 * m * n + (8 * m * k if C_h is not None else 0)
-        d2h = 8 * n * n + (8 * m * n if cfg["op"] == "form_q" else 8 * m * k)
-        e2e = {"value": 2.0 * m * n * n / (t_e2e * 1e-3) / 1e9, "unit": "GFLOP/s (2mn^2 over the whole e2e step)",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e}
+            else:
+                tdist.apply_qt(st, C)
+            out_h.copy_(C, non_blocking=True)
+        R_h.copy_(Rr, non_blocking=True)
+        e_e.record(stream)
+        e_e.synchronize()
+        if it > 0:
+            te.append(e_s.elapsed_time(e_e))
+    t_e2e = statistics.mean(te)
+    if world > 1:
+        x = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        t_e2e = x.item()
+    h2d = 8 * m * n + (8 * m * k if C_h is not None else 0)                 # all ranks' slabs
+    d2h = 8 * n * n * world + (8 * m * n if cfg["op"] == "form_q" else 8 * m * k)
+    e2e = {"value": 2.0 * m * n * n / (t_e2e * 1e-3) / 1e9, "unit": "GFLOP/s (2mn^2 over the whole e2e step)",
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e}
 
     if rank != 0:
         dist.destroy_process_group()
