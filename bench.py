@@ -68,6 +68,15 @@ def kernel_launches(info, n, op, world):
     return fac + second + cross
 
 
+def max_over_ranks(vals, dev):
+    """Element-wise max over the process group (device tensor for NCCL, host for gloo)."""
+    import torch
+    import torch.distributed as dist
+    x = torch.tensor(vals, dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(x, op=dist.ReduceOp.MAX)
+    return x.tolist()
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -191,8 +200,16 @@ def run_ours(args, cfg):
     N = args.gpus
     rank, world = 0, 1
     if N > 1:
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", os.environ.get("RANK", "0"))))
-        dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
+        # TSQR_BENCH_BACKEND=gloo + TSQR_BENCH_ONE_GPU=1: a functional check of the multi-rank
+        # path with every rank on one GPU (the butterfly's messages staged through the host);
+        # never a scaling measurement
+        backend = os.environ.get("TSQR_BENCH_BACKEND", "nccl")
+        local = 0 if os.environ.get("TSQR_BENCH_ONE_GPU") else int(os.environ.get("LOCAL_RANK", os.environ.get("RANK", "0")))
+        torch.cuda.set_device(local)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
+        else:
+            dist.init_process_group(backend)
         rank, world = dist.get_rank(), dist.get_world_size()
     dev = torch.device("cuda", torch.cuda.current_device())
     m, n, b, s, k = cfg["m"], cfg["n"], cfg["b"], cfg["s"], cfg["k"]
@@ -265,9 +282,7 @@ def run_ours(args, cfg):
     tf, ts = statistics.mean(t_factor), statistics.mean(t_step)
     tl, tt = statistics.mean(t_leaf), statistics.mean(t_tree)
     if world > 1:
-        x = torch.tensor([tf, ts, tl, tt], dtype=torch.float64, device=dev)
-        dist.all_reduce(x, op=dist.ReduceOp.MAX)
-        tf, ts, tl, tt = x.tolist()
+        tf, ts, tl, tt = max_over_ranks([tf, ts, tl, tt], dev)
 
     # ---- e2e through the public API with pinned host buffers (host <-> device inside);
     # every rank copies its own slab, the time is the max over ranks
@@ -307,9 +322,7 @@ def run_ours(args, cfg):
             te.append(e_s.elapsed_time(e_e))
     t_e2e = statistics.mean(te)
     if world > 1:
-        x = torch.tensor([t_e2e], dtype=torch.float64, device=dev)
-        dist.all_reduce(x, op=dist.ReduceOp.MAX)
-        t_e2e = x.item()
+        t_e2e = max_over_ranks([t_e2e], dev)[0]
     h2d = 8 * m * n + (8 * m * k if C_h is not None else 0)                 # all ranks' slabs
     d2h = 8 * n * n * world + (8 * m * n if cfg["op"] == "form_q" else 8 * m * k)
     e2e = {"value": 2.0 * m * n * n / (t_e2e * 1e-3) / 1e9, "unit": "GFLOP/s (2mn^2 over the whole e2e step)",

@@ -110,6 +110,9 @@ class RankState:
 
 def _exchange(send: torch.Tensor, partner: int, group=None) -> torch.Tensor:
     import torch.distributed as dist
+    if send.is_cuda and dist.get_backend(group) == "gloo":
+        # gloo moves host memory only: stage a device buffer through the host
+        return _exchange(send.cpu(), partner, group).to(send.device)
     recv = torch.empty_like(send)
     ops = [dist.P2POp(dist.isend, send, partner, group), dist.P2POp(dist.irecv, recv, partner, group)]
     for req in dist.batch_isend_irecv(ops):
