@@ -46,6 +46,7 @@ struct tsqr_tree_s {
     bool wide = false;
     int npan = 0;
     double *d_tcache_node = nullptr, *d_cross_tcache = nullptr, *d_wtmp = nullptr;
+    double *d_tcache_pair = nullptr;   // wide leaves: T01 of each pair of panels (tiles <= 1024 rows)
     int64_t wtmp_size = 0;
     std::vector<int> step_off;   // top-down: groups [step_off[g], step_off[g+1])
 };
@@ -71,7 +72,7 @@ static void free_tree_memory(tsqr_tree_s *t) {
                     t->d_tau_node, t->d_cross_y1, t->d_cross_tau, t->d_xbuf,
                     t->d_step_ids, t->d_pipe_nodes, t->d_prod_l, t->d_prod_r, t->d_pipe_flags,
                     t->d_tile_chunk0, t->d_cta_tile0, t->d_apply_cta_tile0, t->d_tau_chunk, t->d_tcache,
-                    t->d_tcache_node, t->d_cross_tcache, t->d_wtmp};
+                    t->d_tcache_node, t->d_cross_tcache, t->d_wtmp, t->d_tcache_pair};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -269,7 +270,10 @@ static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t 
     const int ncb_cache = t->wide ? t->npan : chain_ncb((int)n);
     alloc((void **)&t->d_tcache, sizeof(double) * nchunks * ncb_cache * 64);
     alloc((void **)&t->d_tcache_node, sizeof(double) * L * t->npan * 64);    // node panel T's (both engines)
-    if (t->wide) alloc((void **)&t->d_cross_tcache, sizeof(double) * (ilog2(ro.nranks) + 1) * t->npan * 64);
+    if (t->wide) {
+        alloc((void **)&t->d_cross_tcache, sizeof(double) * (ilog2(ro.nranks) + 1) * t->npan * 64);
+        alloc((void **)&t->d_tcache_pair, sizeof(double) * L * ((t->npan + 1) / 2) * 64);
+    }
     t->nchunks = nchunks;
     if (e != cudaSuccess) {
         free_tree_memory(t);
@@ -350,7 +354,7 @@ tsqr_status_t tsqr_factor(int64_t m_local, int64_t n, double *A, int64_t lda, do
         const int L = t->plan.ntiles();
         CUDA_TRY(mark(0), "tsqr_factor events");
         CUDA_TRY(launch_wide_leaves(A, lda, (int)n, t->d_row0, t->d_rows, L, (int)t->plan.max_rows, t->d_tau_chunk,
-                                    t->d_tcache, t->stream),
+                                    t->d_tcache, t->d_tcache_pair, t->stream),
                  "tsqr_factor leaves");
         CUDA_TRY(mark(1), "tsqr_factor events");
         if (wide_tree_pipe_ok((int)n)) {
@@ -439,8 +443,9 @@ tsqr_status_t tsqr_apply_qt(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, do
     ca.C = C; ca.ldc = ldc; ca.k = (int)k; ca.forward = 1; ca.xbuf = nullptr;
     if (t->wide) {
         const int n = (int)t->plan.n;
-        CUDA_TRY(launch_wide_apply_leaves(t->A, t->lda, n, t->d_row0, t->d_rows, t->plan.ntiles(), (int)t->plan.max_rows, t->d_tcache, C,
-                                          ldc, (int)k, 1, st),
+        CUDA_TRY(launch_wide_apply_leaves(t->A, t->lda, n, t->d_row0, t->d_rows, t->plan.ntiles(),
+                                          (int)t->plan.max_rows, t->d_tcache, t->d_tcache_pair, C, ldc, (int)k, 1,
+                                          st),
                  "tsqr_apply_qt leaves");
         for (size_t g = t->step_off.size() - 1; g-- > 0;) {         // tree steps bottom-up
             const int cnt = t->step_off[g + 1] - t->step_off[g];
@@ -525,7 +530,8 @@ tsqr_status_t tsqr_form_q(tsqr_tree_t t, double *Q, int64_t ldq, void *stream) {
                      "tsqr_form_q nodes");
         }
         CUDA_TRY(launch_wide_formq_init(t->d_row0, t->d_rows, L, n, t->d_xbuf, Q, ldq, st), "tsqr_form_q");
-        CUDA_TRY(launch_wide_apply_leaves(t->A, t->lda, n, t->d_row0, t->d_rows, L, (int)t->plan.max_rows, t->d_tcache, Q, ldq, n, 0, st),
+        CUDA_TRY(launch_wide_apply_leaves(t->A, t->lda, n, t->d_row0, t->d_rows, L, (int)t->plan.max_rows,
+                                          t->d_tcache, t->d_tcache_pair, Q, ldq, n, 0, st),
                  "tsqr_form_q leaves");
         t->stream = st;
         return debug_sync(t, st, "tsqr_form_q");

@@ -41,14 +41,14 @@ cudaError_t launch_cs_apply(const ChainApplyArgs &f, cudaStream_t st);
 // Wide-n engine (tsqr_wide.cu, 64 < n <= 256): one CTA per leaf / node problem.
 int wide_max_rows();
 cudaError_t launch_wide_leaves(double *A, int64_t lda, int n, const int64_t *row0, const int *rows, int L,
-                               int max_rows, double *tau, double *tcache, cudaStream_t st);
+                               int max_rows, double *tau, double *tcache, double *tpair, cudaStream_t st);
 cudaError_t launch_wide_nodes(double *A, int64_t lda, int n, const int64_t *row0, const int *node_a, const int *ids,
                               int count, double *tau_node, double *tcache_node, cudaStream_t st);
 cudaError_t launch_wide_node1(double *Ra, int64_t lda, double *Rb, int64_t ldb, int n, double *tau, double *tcache,
                               cudaStream_t st);
 cudaError_t launch_wide_apply_leaves(const double *A, int64_t lda, int n, const int64_t *row0, const int *rows,
-                                     int L, int max_rows, const double *tcache, double *C, int64_t ldc, int k,
-                                     int forward, cudaStream_t st);
+                                     int L, int max_rows, const double *tcache, const double *tpair, double *C,
+                                     int64_t ldc, int k, int forward, cudaStream_t st);
 cudaError_t launch_node_apply(const double *A, int64_t lda, int n, const int64_t *row0, const int *node_a,
                                     const int *ids, int count, const double *tcache_node, double *C, int64_t ldc,
                                     int k, int forward, int xbuf_mode, cudaStream_t st);

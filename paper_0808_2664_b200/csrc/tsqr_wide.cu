@@ -447,14 +447,15 @@ __device__ __forceinline__ void upd_grp16(double (&cv)[U][2], double *cp, bool o
         }
     }
 }
+template <bool kFwd = true>
 __device__ __forceinline__ void apply_pair_cols(const double *Ys, const double *T0, const double *T1,
                                                 const double *T01, double *C, int64_t ldc, int H, int rb0, int c_lo,
                                                 int c_hi) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
-    // B operands T(2q+e, l4) of the three 8x8 blocks (forward: Q^T uses T16^T on the left of Y^T)
-    const double a0 = T0[(2 * q) * 8 + l4], a1 = T0[(2 * q + 1) * 8 + l4];
-    const double b0 = T1[(2 * q) * 8 + l4], b1 = T1[(2 * q + 1) * 8 + l4];
-    const double x0 = T01[(2 * q) * 8 + l4], x1 = T01[(2 * q + 1) * 8 + l4];
+    // B operands: T(2q+e, l4) of the three 8x8 blocks for Q^T (P = W^T T16), T(l4, 2q+e) for Q
+    // (P = W^T T16^T, T16^T = [T0^T 0; T01^T T1^T])
+    auto tb = [&](const double *T, int e) { return kFwd ? T[(2 * q + e) * 8 + l4] : T[l4 * 8 + 2 * q + e]; };
+    const double a0 = tb(T0, 0), a1 = tb(T0, 1), b0 = tb(T1, 0), b1 = tb(T1, 1), x0 = tb(T01, 0), x1 = tb(T01, 1);
     const int nrb = (H + 7) / 8;
     constexpr int U = 4;                       // row blocks per load group (register budget of 2 CTAs/SM)
     for (int cb = c_lo / 8 + warp; 8 * cb < c_hi; cb += NW) {
@@ -476,8 +477,13 @@ __device__ __forceinline__ void apply_pair_cols(const double *Ys, const double *
         double p0 = 0.0, p1 = 0.0, r0 = 0.0, r1 = 0.0;
         dmma(p0, p1, we, a0);
         dmma(p0, p1, wo, a1);
-        dmma(r0, r1, we, x0);
-        dmma(r0, r1, wo, x1);
+        if (kFwd) {                            // P1 = W0^T T01 + W1^T T1
+            dmma(r0, r1, we, x0);
+            dmma(r0, r1, wo, x1);
+        } else {                               // P0 += W1^T T01^T
+            dmma(p0, p1, ve, x0);
+            dmma(p0, p1, vo, x1);
+        }
         dmma(r0, r1, ve, b0);
         dmma(r0, r1, vo, b1);
         load_grp<U>(ca, cp, okc, H, rb0);
@@ -492,11 +498,12 @@ __device__ __forceinline__ void apply_pair_cols(const double *Ys, const double *
 }
 
 // apply_panel_cols on a Y stored with row stride YW (one panel's 8 columns at Ys + off)
-template <int YW>
+template <int YW, bool kFwd = true>
 __device__ __forceinline__ void apply_one_cols(const double *Ys, const double *Tg, double *C, int64_t ldc, int H,
                                                int rb0, int c_lo, int c_hi) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
-    const double tb0 = Tg[(2 * q) * 8 + l4], tb1 = Tg[(2 * q + 1) * 8 + l4];
+    const double tb0 = kFwd ? Tg[(2 * q) * 8 + l4] : Tg[l4 * 8 + 2 * q];
+    const double tb1 = kFwd ? Tg[(2 * q + 1) * 8 + l4] : Tg[l4 * 8 + 2 * q + 1];
     const int nrb = (H + 7) / 8;
     for (int cb = c_lo / 8 + warp; 8 * cb < c_hi; cb += NW) {
         const int col = 8 * cb + l4;
@@ -539,7 +546,8 @@ __device__ __forceinline__ void apply_one_cols(const double *Ys, const double *T
 // __syncthreads per Householder step for the cross-warp sums; T per panel;
 // the trailing update column-split (apply_panel_cols).
 template <int KM>
-__device__ void wide_leaf_qr(double *At, int64_t lda, int H, int n, double *tau, double *tcache, LeafSmem<KM> &S) {
+__device__ void wide_leaf_qr(double *At, int64_t lda, int H, int n, double *tau, double *tcache, double *tpair,
+                             LeafSmem<KM> &S) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
     const int npan = (n + 7) / 8;
     const int rbase = warp * 8 * KM;
@@ -666,13 +674,13 @@ __device__ void wide_leaf_qr(double *At, int64_t lda, int H, int n, double *tau,
             }
         }
         __syncthreads();
-        if (p + 1 == npan) break;
         if (!TWO) {
-            apply_one_cols<YW>(S.Ys, Tp, At, lda, H, p, 8 * (p + 1), n);
+            if (p + 1 < npan) apply_one_cols<YW>(S.Ys, Tp, At, lda, H, p, 8 * (p + 1), n);
         } else if ((p & 1) == 0) {
             // first panel of a pair: update only the pair's second column block
-            apply_one_cols<YW>(S.Ys, Tp, At, lda, H, p, 8 * (p + 1), min(n, 8 * (p + 2)));
+            if (p + 1 < npan) apply_one_cols<YW>(S.Ys, Tp, At, lda, H, p, 8 * (p + 1), min(n, 8 * (p + 2)));
         } else {
+            // (also for the last pair: the apply / form-Q kernels use its T01)
             // second panel of a pair: T01 = -T0 (Y0^T Y1) T1, then the 16-reflector update
             {
                 double g0 = 0.0, g1 = 0.0;
@@ -712,6 +720,8 @@ __device__ void wide_leaf_qr(double *At, int64_t lda, int H, int n, double *tau,
                 }
                 S.Ts[2][i * 8 + j0] = t01[0];
                 S.Ts[2][i * 8 + j0 + 1] = t01[1];
+                tpair[(p >> 1) * 64 + i * 8 + j0] = t01[0];     // for the paired apply / form Q
+                tpair[(p >> 1) * 64 + i * 8 + j0 + 1] = t01[1];
             }
             __syncthreads();
             if (p + 1 < npan) apply_pair_cols(S.Ys, S.Ts[0], S.Ts[1], S.Ts[2], At, lda, H, p - 1, 8 * (p + 1), n);
@@ -727,13 +737,13 @@ using namespace wide;
 template <int KM>
 __global__ void __launch_bounds__(NT, KM <= 8 ? 2 : 1)
 k_wide_leaves(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *tile_rows, double *tau_tile,
-              double *tcache_tile) {
+              double *tcache_tile, double *tpair_tile) {
     extern __shared__ __align__(16) double smraw[];
     LeafSmem<KM> &S = *reinterpret_cast<LeafSmem<KM> *>(smraw);
     const int t = blockIdx.x;
     const int npan = (n + 7) / 8;
     wide_leaf_qr<KM>(A + tile_row0[t], lda, tile_rows[t], n, tau_tile + (int64_t)t * n,
-                     tcache_tile + (int64_t)t * npan * 64, S);
+                     tcache_tile + (int64_t)t * npan * 64, tpair_tile + (int64_t)t * ((npan + 1) / 2) * 64, S);
 }
 
 // Tree nodes of one step: node ids[i] = b (right subtree's first tile), its
@@ -764,46 +774,58 @@ k_wide_node1(double *Ra, int64_t lda, double *Rb, int64_t ldb, int n, double *ta
 template <bool kFwd>
 __global__ void __launch_bounds__(NT, 2)
 k_wide_apply_leaves(const double *A, int64_t lda, int n, const int64_t *tile_row0, const int *tile_rows,
-                    const double *tcache_tile, double *C, int64_t ldc, int k, int two_slots) {
+                    const double *tcache_tile, const double *tpair_tile, int pairs, double *C, int64_t ldc, int k,
+                    int two_slots) {
+    // Panels are applied in the factor's pairs when it cached their T01 (pairs:
+    // tiles <= 1024 rows): Y of a pair (H x 16, row stride 16) and its T0, T1,
+    // T01 staged with cp.async, the next group's copy in flight in a second slot
+    // when it fits; one 16-reflector pass over C per pair (apply_pair_cols).
     extern __shared__ __align__(16) double smraw[];
     const int t = blockIdx.x;
     const int npan = (n + 7) / 8;
     const int H = tile_rows[t];
     const int Hp = 8 * ((H + 7) / 8);
-    double *Ts = smraw, *Ys = smraw + 128;                       // 2 slots each
+    double *Ts = smraw, *Ys = smraw + 2 * 192;                   // 2 slots: T0 T1 T01 | Y
     const double *At = A + tile_row0[t];
     const double *tc = tcache_tile + (int64_t)t * npan * 64;
-    // panel p's Y staged with cp.async (zero-filled off the reflectors, unit
-    // diagonal patched after the wait), the next panel's copy in flight while
-    // this one is applied (two slots)
-    auto stage = [&](int p, int slot) {
-        double *Y = Ys + slot * Hp * 8, *T = Ts + slot * 64;
-        const int h0 = 8 * p, hs = Hp - h0;
-        for (int e = threadIdx.x; e < 8 * hs; e += NT) {
-            const int r = h0 + e % hs, jj = e / hs, c = 8 * p + jj;
+    const double *tp = tpair_tile + (int64_t)t * ((npan + 1) / 2) * 64;
+    const int gw = pairs ? 2 : 1;                               // panels per group
+    const int yw = 8 * gw;                                      // Y's row stride
+    const int ngrp = (npan + gw - 1) / gw;
+    auto stage = [&](int g, int slot) {
+        double *Y = Ys + slot * Hp * yw, *T = Ts + slot * 192;
+        const int p0 = gw * g, np = min(gw, npan - p0), h0 = 8 * p0, hs = Hp - h0;
+        for (int e = threadIdx.x; e < 8 * np * hs; e += NT) {
+            const int r = h0 + e % hs, jj = e / hs, c = 8 * p0 + jj;
             const bool ok = c < n && r > c && r < H;
-            cp_async8(Y + r * 8 + jj, At + (ok ? r + (int64_t)c * lda : 0), ok);
+            cp_async8(Y + r * yw + jj, At + (ok ? r + (int64_t)c * lda : 0), ok);
         }
-        if (threadIdx.x < 64) cp_async8(T + threadIdx.x, tc + 64 * p + threadIdx.x, true);
+        if (threadIdx.x < 64 * np) cp_async8(T + threadIdx.x, tc + 64 * p0 + threadIdx.x, true);
+        if (np == 2 && threadIdx.x < 64) cp_async8(T + 128 + threadIdx.x, tp + 64 * g + threadIdx.x, true);
         asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
-    stage(kFwd ? 0 : npan - 1, 0);
-    for (int pp = 0; pp < npan; ++pp) {
-        const int p = kFwd ? pp : npan - 1 - pp, slot = two_slots ? (pp & 1) : 0;
-        if (two_slots && pp + 1 < npan) {
-            stage(kFwd ? p + 1 : p - 1, slot ^ 1);
+    stage(kFwd ? 0 : ngrp - 1, 0);
+    for (int gg = 0; gg < ngrp; ++gg) {
+        const int g = kFwd ? gg : ngrp - 1 - gg, slot = two_slots ? (gg & 1) : 0;
+        if (two_slots && gg + 1 < ngrp) {
+            stage(kFwd ? g + 1 : g - 1, slot ^ 1);
             asm volatile("cp.async.wait_group 1;\n" ::: "memory");
         } else {
             asm volatile("cp.async.wait_group 0;\n" ::: "memory");
         }
         __syncthreads();
-        double *Y = Ys + slot * Hp * 8;
-        if (threadIdx.x < 8 && 8 * p + threadIdx.x < n && 8 * p + threadIdx.x < H)
-            Y[(8 * p + threadIdx.x) * 8 + threadIdx.x] = 1.0;
+        const int p0 = gw * g, np = min(gw, npan - p0);
+        double *Y = Ys + slot * Hp * yw, *T = Ts + slot * 192;
+        if (threadIdx.x < 8 * np) {                             // the unit diagonals
+            const int c = 8 * p0 + threadIdx.x;
+            if (c < n && c < H) Y[c * yw + threadIdx.x] = 1.0;
+        }
         __syncthreads();
-        apply_panel_cols<kFwd>(Y, Ts + slot * 64, C + tile_row0[t], ldc, H, p, 0, k);
+        if (np == 2) apply_pair_cols<kFwd>(Y, T, T + 64, T + 128, C + tile_row0[t], ldc, H, p0, 0, k);
+        else if (pairs) apply_one_cols<16, kFwd>(Y, T, C + tile_row0[t], ldc, H, p0, 0, k);
+        else apply_one_cols<8, kFwd>(Y, T, C + tile_row0[t], ldc, H, p0, 0, k);
         __syncthreads();
-        if (!two_slots && pp + 1 < npan) stage(kFwd ? p + 1 : p - 1, 0);
+        if (!two_slots && gg + 1 < ngrp) stage(kFwd ? g + 1 : g - 1, 0);
     }
 }
 
@@ -974,27 +996,28 @@ static cudaError_t wide_attr(const void *fn) {
 int wide_max_rows() { return MAXR; }
 
 static size_t apply_leaf_smem(int max_rows, int slots) {
-    return sizeof(double) * (slots * 8 * ((max_rows + 7) / 8 * 8) + 128);
+    const int yw = max_rows <= 1024 ? 16 : 8;                // pairs of panels only for tiles <= 1024 rows
+    return sizeof(double) * (slots * yw * ((max_rows + 7) / 8 * 8) + 2 * 192);
 }
 
 template <int KM>
 static cudaError_t launch_leaves_km(double *A, int64_t lda, int n, const int64_t *row0, const int *rows, int L,
-                                   int max_rows, double *tau, double *tcache, cudaStream_t st) {
+                                   int max_rows, double *tau, double *tcache, double *tpair, cudaStream_t st) {
     const size_t bytes = LeafSmem<KM>::bytes(max_rows);
     cudaError_t e = cudaFuncSetAttribute((const void *)k_wide_leaves<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)bytes);
     if (e != cudaSuccess) return e;
-    k_wide_leaves<KM><<<L, NT, bytes, st>>>(A, lda, n, row0, rows, tau, tcache);
+    k_wide_leaves<KM><<<L, NT, bytes, st>>>(A, lda, n, row0, rows, tau, tcache, tpair);
     return cudaGetLastError();
 }
 
 // max_rows: the tallest tile (selects the per-warp row range, 64 KM >= max_rows)
 cudaError_t launch_wide_leaves(double *A, int64_t lda, int n, const int64_t *row0, const int *rows, int L,
-                               int max_rows, double *tau, double *tcache, cudaStream_t st) {
-    if (max_rows <= 512) return launch_leaves_km<8>(A, lda, n, row0, rows, L, max_rows, tau, tcache, st);
-    if (max_rows <= 1024) return launch_leaves_km<16>(A, lda, n, row0, rows, L, max_rows, tau, tcache, st);
-    if (max_rows <= 1536) return launch_leaves_km<24>(A, lda, n, row0, rows, L, max_rows, tau, tcache, st);
-    return launch_leaves_km<KMW>(A, lda, n, row0, rows, L, max_rows, tau, tcache, st);
+                               int max_rows, double *tau, double *tcache, double *tpair, cudaStream_t st) {
+    if (max_rows <= 512) return launch_leaves_km<8>(A, lda, n, row0, rows, L, max_rows, tau, tcache, tpair, st);
+    if (max_rows <= 1024) return launch_leaves_km<16>(A, lda, n, row0, rows, L, max_rows, tau, tcache, tpair, st);
+    if (max_rows <= 1536) return launch_leaves_km<24>(A, lda, n, row0, rows, L, max_rows, tau, tcache, tpair, st);
+    return launch_leaves_km<KMW>(A, lda, n, row0, rows, L, max_rows, tau, tcache, tpair, st);
 }
 
 cudaError_t launch_wide_nodes(double *A, int64_t lda, int n, const int64_t *row0, const int *node_a, const int *ids,
@@ -1014,17 +1037,20 @@ cudaError_t launch_wide_node1(double *Ra, int64_t lda, double *Rb, int64_t ldb, 
 }
 
 cudaError_t launch_wide_apply_leaves(const double *A, int64_t lda, int n, const int64_t *row0, const int *rows,
-                                     int L, int max_rows, const double *tcache, double *C, int64_t ldc, int k,
-                                     int forward, cudaStream_t st) {
-    const int slots = apply_leaf_smem(max_rows, 2) <= 227 * 1024 ? 2 : 1;   // prefetch the next panel's Y if it fits
+                                     int L, int max_rows, const double *tcache, const double *tpair, double *C,
+                                     int64_t ldc, int k, int forward, cudaStream_t st) {
+    const int pairs = max_rows <= 1024;                      // the factor cached T01 (wide_leaf_qr, KM <= 16)
+    const int slots = apply_leaf_smem(max_rows, 2) <= 227 * 1024 ? 2 : 1;   // prefetch the next group if it fits
     const size_t bytes = apply_leaf_smem(max_rows, slots);
     const void *fn = forward ? (const void *)k_wide_apply_leaves<true> : (const void *)k_wide_apply_leaves<false>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;
     if (forward)
-        k_wide_apply_leaves<true><<<L, NT, bytes, st>>>(A, lda, n, row0, rows, tcache, C, ldc, k, slots == 2);
+        k_wide_apply_leaves<true><<<L, NT, bytes, st>>>(A, lda, n, row0, rows, tcache, tpair, pairs, C, ldc, k,
+                                                        slots == 2);
     else
-        k_wide_apply_leaves<false><<<L, NT, bytes, st>>>(A, lda, n, row0, rows, tcache, C, ldc, k, slots == 2);
+        k_wide_apply_leaves<false><<<L, NT, bytes, st>>>(A, lda, n, row0, rows, tcache, tpair, pairs, C, ldc, k,
+                                                         slots == 2);
     return cudaGetLastError();
 }
 
