@@ -1,18 +1,16 @@
-// Kernels of the B200 TSQR hot path (sm_100a) on the blocked compact-WY engine
-// (wy.cuh) and their host launchers.  Product code.
+// Butterfly-round kernels (a5, a8 and a9 across ranks, n <= 64) on the blocked
+// compact-WY tile engine (wy.cuh), plus small utility kernels, and their host
+// launchers.  Product code.
 //
-//  k_factor_w    (a2)+(a3)+(a4)+(a6): one warp per tile: panel QR (shuffles,
-//                Gram on the fly) -> T (a3) -> DMMA trailing update, panel by
-//                panel; then the single-pass ticketed tree: the second warp to
-//                finish below a node runs the structured combine of [R_a; R_b]
-//                (Alg. QR:qnxn on the same engine, structured row blocks) and
-//                climbs; the root writes R.
-//  k_apply_qt    (a7)+(a8): C <- Q_tile^T C panel by panel (W = Y^T C,
-//                W <- T^T W, C -= Y W on DMMA), then the ticketed climb applying
-//                each node's [I; Y1] reflectors to the head rows.
-//  k_formq_node  (a9): one top-down tree step [X_a; X_b] = Q_node [X; 0].
-//  k_formq_leaf  (a10): Q_t = Q_tile [X_t; 0].
-//  k_cross_*     (a5): butterfly round compute.
+//  k_cross_factor  (a5): one round's node [R_lower; R_upper] of the cross-GPU
+//                  butterfly (Alg. TSQR:par P:1667-1707): structured combine of
+//                  this rank's R and the partner's packed R, identical on both.
+//  k_cross_apply   (a8): the round's reflectors applied to the stacked heads of
+//                  Q^T C (this rank's and the partner's), keeping this rank's half.
+//  k_cross_root_x  (a9): the root X of this rank for form Q, from the replicated
+//                  round factors (no communication).
+//  k_identity, k_pack_r, k_copy_block: X = I, R -> packed upper triangle, and
+//                  block copies for the exchanges.
 #include "tsqr_kernels.h"
 #include "wy.cuh"
 
