@@ -131,18 +131,21 @@ __device__ __forceinline__ House house_bf(double alpha, double s2) {
     return h;
 }
 
-template <int NCB_, int KM_, int NW_>
+template <int NCB_, int KM_, int NW_, int NBUF_ = 2>
 struct Cfg {
-    static constexpr int NCB = NCB_, KM = KM_, NW = NW_;
+    // NBUF: R buffers; with 2 the tiles of a CTA alternate and the next tile's head
+    // chunk never waits for the previous tile; with 1 (to make room for taller
+    // chunks) it follows the previous tile's last chunk panel by panel
+    static constexpr int NCB = NCB_, KM = KM_, NW = NW_, NBUF = NBUF_;
     static constexpr int NP = 8 * NCB, CH = 8 * KM, NT = 32 * NW;
     static constexpr int LDR = NP + 2;                    // R buffer: R(i, c) at [i * LDR + c]
     static constexpr int RBUF = NP * LDR;
     // per-warp scratch: Y panel (CH x 8 row-major), Gram, T (row-major), taus
     static constexpr int YS = 0, GS = CH * 8, TS = GS + 64, T8 = TS + 64, XS = T8 + 8, WS = XS + 2 * CH;
-    static constexpr int OFF_WS = 2 * RBUF;               // after the two R buffers
+    static constexpr int OFF_WS = NBUF * RBUF;            // after the R buffers
     static constexpr int OFF_SYNC = OFF_WS + NW * WS;     // per buffer: NP row + NCB panel counters
     static constexpr int SYNC_INTS = NP + NCB;
-    static constexpr int OFF_STG = (OFF_SYNC + (2 * SYNC_INTS + 1) / 2 + 1) & ~1;   // 16-byte aligned; per warp:
+    static constexpr int OFF_STG = (OFF_SYNC + (NBUF * SYNC_INTS + 1) / 2 + 1) & ~1;   // 16-byte aligned; per warp:
                                                                                    // the next chunk (col-major CH x NP)
     static constexpr int STG = CH * NP;
     static constexpr size_t BYTES = (size_t)(OFF_STG + NW * STG) * sizeof(double);

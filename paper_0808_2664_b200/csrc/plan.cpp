@@ -20,10 +20,10 @@ int64_t tile_capacity(int64_t n) { return n > 64 ? 2304 : (int64_t)1 << 30; }
 int64_t default_tile_rows(int64_t n) { return n > 64 ? 2048 : 32 * (int64_t)chunk_rows_for(n); }
 // chunk.cuh: the chunk is register-resident (KM x NCB DMMA fragments per lane),
 // as tall as the register file and the staging buffers allow at 8 warps/SM:
-// KM = 8 (64 rows) for n <= 32, 6 (48) for n <= 48, 5 (40) for n <= 56, 4 (32)
-// for n <= 64
+// KM = 8 (64 rows) for n <= 32, 6 (48) for n <= 48, 5 (40) for n <= 64 (for
+// 56 < n <= 64 with a single R buffer, tsqr_chain.cu)
 int chunk_rows_for(int64_t n) {
-    return n <= 32 ? 64 : (n <= 48 ? 48 : (n <= 56 ? 40 : (n <= 64 ? 32 : 0)));   // 0: one chunk per tile
+    return n <= 32 ? 64 : (n <= 48 ? 48 : (n <= 64 ? 40 : 0));   // 0: one chunk per tile
 }
 
 static int64_t block_count(int64_t m, int64_t n, int64_t b, int64_t *last_rows) {

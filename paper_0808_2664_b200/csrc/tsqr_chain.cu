@@ -61,7 +61,7 @@ k_chain_factor(double *A, int64_t lda, int n, const int64_t *tile_row0, const in
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int q = lane & 3, l4 = lane >> 2;
     int *sync = reinterpret_cast<int *>(sm + C::OFF_SYNC);
-    for (int i = threadIdx.x; i < 2 * C::SYNC_INTS; i += C::NT) sync[i] = 0;
+    for (int i = threadIdx.x; i < C::NBUF * C::SYNC_INTS; i += C::NT) sync[i] = 0;
     PROBE_INIT();
     __syncthreads();
     double *ws = sm + C::OFF_WS + warp * C::WS;
@@ -83,7 +83,7 @@ k_chain_factor(double *A, int64_t lda, int n, const int64_t *tile_row0, const in
                 ++t;
                 c = 0;
                 if (t >= te) break;
-                b = (t - tb) & 1;
+                b = C::NBUF == 2 ? (t - tb) & 1 : 0;
                 nch = (tile_rows[t] + C::CH - 1) / C::CH;
                 continue;
             }
@@ -155,7 +155,7 @@ static cudaError_t chain_dispatch(int n, F &&fn) {
         case 3: case 4: return fn(Cfg<4, 8, 8>());
         case 5: case 6: return fn(Cfg<6, 6, 8>());
         case 7: return fn(Cfg<7, 5, 8>());
-        default: return fn(Cfg<8, 4, 8>());
+        default: return fn(Cfg<8, 5, 8, 1>());          // one R buffer: room for 40-row chunks
     }
 }
 
