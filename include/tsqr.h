@@ -159,6 +159,17 @@ tsqr_status_t tsqr_cross_apply_qt(tsqr_tree_t tree, int32_t round, double *top, 
                                   const double *partner_top, double *C, int64_t ldc,
                                   int64_t k, void *stream);
 
+/* C <- Q C, the inverse of tsqr_apply_qt (the reverse traversal: node stages
+ * top-down with T in place of T^T, then the leaves' reflectors in reverse order;
+ * [TR] P:1919-1925 with an arbitrary C in place of [I_n; 0]).
+ * C (device, m_local x k, ldc >= m_local) is read in tree order -- rows 0..n-1
+ * of the slab are the R coordinates, every other tile head its node's
+ * complement coordinates -- so tsqr_apply_q(tsqr_apply_qt(C)) = C, and C =
+ * [X; 0] gives Q[X; 0] (X = I: the explicit thin Q of tsqr_form_q).  Local tree
+ * only: a tree with butterfly rounds (nranks > 1) returns TSQR_ERR_INVALID.
+ * k = 0 is a no-op. */
+tsqr_status_t tsqr_apply_q(tsqr_tree_t tree, double *C, int64_t ldc, int64_t k, void *stream);
+
 /* Explicit thin Q of the rank's slab: Q (device, m_local x n, ldq >= m_local) =
  * rows of Q [I_n; 0].  Needs no communication: the
  * cross-rank node factors are replicated on every rank. */

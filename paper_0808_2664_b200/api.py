@@ -108,6 +108,15 @@ def apply_qt(tree: Tree, C: torch.Tensor, top: torch.Tensor | None = None, strea
     return C, top
 
 
+def apply_q(tree: Tree, C: torch.Tensor, stream=None) -> torch.Tensor:
+    """C <- Q C in place, C in tree order (the inverse of apply_qt; one-rank trees)."""
+    pc, m, k, ldc = _colmajor(C, "C")
+    if m != tree.m_local:
+        raise ValueError("C must have m_local rows")
+    check(lib().tsqr_apply_q(tree.handle, pc, ldc, k, _stream_ptr(stream)), "tsqr_apply_q")
+    return C
+
+
 def form_q(tree: Tree, Q: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """Explicit thin Q rows of this rank (column-major m_local x n)."""
     if Q is None:

@@ -499,6 +499,40 @@ tsqr_status_t tsqr_cross_apply_qt(tsqr_tree_t t, int32_t round, double *top, int
     return debug_sync(t, t->stream, "tsqr_cross_apply_qt");
 }
 
+tsqr_status_t tsqr_apply_q(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, void *stream) {
+    if (!t || !t->A) return TSQR_ERR_INVALID;
+    if (k < 0 || k > INT32_MAX) return TSQR_ERR_INVALID;
+    if (t->cross_rounds != 0) {
+        g_last_error = "tsqr_apply_q: trees with butterfly rounds are not supported";
+        return TSQR_ERR_INVALID;
+    }
+    if (k == 0) return TSQR_OK;
+    if (!C || ldc < t->plan.m_local) return TSQR_ERR_INVALID;
+    const int n = (int)t->plan.n;
+    cudaStream_t st = (cudaStream_t)stream;
+    for (size_t g = 0; g + 1 < t->step_off.size(); ++g) {             // tree steps top-down
+        const int cnt = t->step_off[g + 1] - t->step_off[g];
+        if (cnt == 0) continue;
+        CUDA_TRY(launch_node_apply(t->A, t->lda, n, t->d_row0, t->d_node_a, t->d_step_ids + t->step_off[g], cnt,
+                                   t->d_tcache_node, C, ldc, (int)k, 0, 0, st),
+                 "tsqr_apply_q nodes");
+    }
+    if (t->wide) {
+        CUDA_TRY(launch_wide_apply_leaves(t->A, t->lda, n, t->d_row0, t->d_rows, t->plan.ntiles(),
+                                          (int)t->plan.max_rows, t->d_tcache, t->d_tcache_pair, C, ldc, (int)k, 0, st),
+                 "tsqr_apply_q leaves");
+    } else {
+        ChainApplyArgs ca;
+        ca.A = t->A; ca.lda = t->lda; ca.n = n; ca.chunk_rows = t->plan.c;
+        ca.tile_row0 = t->d_row0; ca.tile_rows = t->d_rows; ca.tile_chunk0 = t->d_tile_chunk0;
+        ca.cta_tile0 = t->d_apply_cta_tile0; ca.grid = t->apply_grid; ca.tcache = t->d_tcache;
+        ca.C = C; ca.ldc = ldc; ca.k = (int)k; ca.forward = 0; ca.xbuf = nullptr;
+        CUDA_TRY(launch_cs_apply(ca, st), "tsqr_apply_q leaves");
+    }
+    t->stream = st;
+    return debug_sync(t, st, "tsqr_apply_q");
+}
+
 tsqr_status_t tsqr_form_q(tsqr_tree_t t, double *Q, int64_t ldq, void *stream) {
     if (!t || !t->A || !Q) return TSQR_ERR_INVALID;
     if (ldq < t->plan.m_local) return TSQR_ERR_INVALID;

@@ -10,8 +10,9 @@ namespace tsqr {
 using namespace chunk;
 
 // ============================================================ apply / form Q
-// k_cs_apply<C, kFwd>: the leaf stage of C <- Q^T C (kFwd, (a7)) or of the
-// explicit Q = Q_leaves [X; 0] (!kFwd, (a10)) on the factor's chunk chains
+// k_cs_apply<C, kFwd, kX>: the leaf stage of C <- Q^T C (kFwd, (a7)), of the
+// explicit Q = Q_leaves [X; 0] (!kFwd, kX, (a10)) or of C <- Q C (!kFwd, !kX:
+// the reverse traversal) on the factor's chunk chains
 // (C: the factor's chunk configuration).  The 8 warps of a CTA work on the same
 // chunk; warp w owns an 8-column slab of C (column block w of the current
 // pass) for the chunk's CH rows (registers, DMMA accumulator layout) and the
@@ -148,7 +149,7 @@ __device__ __forceinline__ void load_cslab(double (&v)[C::KM][2], const double *
     }
 }
 
-template <class C, bool kFwd>
+template <class C, bool kFwd, bool kX>
 __global__ void __launch_bounds__(256, 2)
 k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const int *tile_rows,
            const int64_t *tile_chunk0, const int *cta_tile0, const double *tcache, double *Cm, int64_t ldc, int k,
@@ -168,7 +169,7 @@ k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const 
         return kFwd ? cc_ : nch - 1 - cc_;
     };
     double ccv[C::KM][2];
-    if (kFwd && tb < te) load_cslab<C>(ccv, Cm, ldc, k, tile_row0[tb], tile_rows[tb], chunk_of(tb, 0), 8 * warp + l4, q);
+    if (!kX && tb < te) load_cslab<C>(ccv, Cm, ldc, k, tile_row0[tb], tile_rows[tb], chunk_of(tb, 0), 8 * warp + l4, q);
     for (int t = tb; t < te; ++t) {
         const int h = tile_rows[t];
         const int nch = (h + C::CH - 1) / C::CH;
@@ -180,11 +181,18 @@ k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const 
 #pragma unroll
             for (int i = 0; i < C::NCB; ++i) {
                 cr[i][0] = cr[i][1] = 0.0;
-                if (!kFwd) {                                      // C_R := X (rows < n, columns < n)
-                    const int r = 8 * i + 2 * q;
+                const int r = 8 * i + 2 * q;
+                if (kX) {                                         // C_R := X (rows < n, columns < n)
                     const double *X = xbuf + (int64_t)t * n * n;
                     cr[i][0] = (okc && r < n) ? X[r + (int64_t)col * n] : 0.0;
                     cr[i][1] = (okc && r + 1 < n) ? X[r + 1 + (int64_t)col * n] : 0.0;
+                } else if (!kFwd) {
+                    // Q C: C_R := the tile's head rows, including the padding rows n..8np-1 of
+                    // the last panel's row block: they are passive in C_R (zero Y columns and T
+                    // rows) and the dense chunk takes the whole row block back
+                    const double *Ch = Cm + row0 + (int64_t)col * ldc;
+                    cr[i][0] = (okc && r < h) ? Ch[r] : 0.0;
+                    cr[i][1] = (okc && r + 1 < h) ? Ch[r + 1] : 0.0;
                 }
             }
             for (int cc_ = 0; cc_ < nch; ++cc_) {
@@ -203,14 +211,14 @@ k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                     const int cnn = chunk_of(tn, cn), hn = tile_rows[tn], r0n = cnn * C::CH;
                     stage_chunk<C>(sm + (cur ^ 1) * AC::YS, A + tile_row0[tn] + r0n, lda, min(C::CH, hn - r0n), n,
                                    tcache + (tile_chunk0[tn] + cnn) * (C::NCB * 64), r0n);
-                    if (kFwd) load_cslab<C>(ccn, Cm, ldc, k, tile_row0[tn], hn, cnn, pw * pn + 8 * warp + l4, q);
+                    if (!kX) load_cslab<C>(ccn, Cm, ldc, k, tile_row0[tn], hn, cnn, pw * pn + 8 * warp + l4, q);
                     asm volatile("cp.async.wait_group 1;\n" ::: "memory");
                     staged = true;
                 } else {
                     asm volatile("cp.async.wait_group 0;\n" ::: "memory");
                     staged = false;
                 }
-                if (!kFwd) {
+                if (kX) {
 #pragma unroll
                     for (int kk = 0; kk < C::KM; ++kk) ccv[kk][0] = ccv[kk][1] = 0.0;
                 }
@@ -221,7 +229,7 @@ k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                     __syncthreads();
                 }
                 double *Ck = Cm + row0 + r0;
-                bool czero = !kFwd;
+                bool czero = kX;
 #pragma unroll 1
                 for (int pp = 0; pp < np; ++pp)
                     cs_apply_panel<C, kFwd>(ccv, cr, kFwd ? pp : np - 1 - pp, r0, slot, czero);
@@ -232,7 +240,7 @@ k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                         const int r = 8 * kk + 2 * q + e;
                         if (okc && r < hk && (!kFwd || r0 + r >= n)) Ck[r + (int64_t)col * ldc] = ccv[kk][e];
                     }
-                if (kFwd && tn < te) {
+                if (!kX && tn < te) {
 #pragma unroll
                     for (int kk = 0; kk < C::KM; ++kk) {
                         ccv[kk][0] = ccn[kk][0];
@@ -276,10 +284,10 @@ int cs_apply_grid(int n) {
     cudaError_t e = chain_cfg_dispatch(n, [&](auto c) {
         using C = decltype(c);
         using AC = ApplyCs<C>;
-        cudaError_t r = cudaFuncSetAttribute((const void *)k_cs_apply<C, true>,
+        cudaError_t r = cudaFuncSetAttribute((const void *)k_cs_apply<C, true, false>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AC::BYTES);
         if (r != cudaSuccess) return r;
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cs_apply<C, true>, AC::NT, AC::BYTES);
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_cs_apply<C, true, false>, AC::NT, AC::BYTES);
     });
     if (e != cudaSuccess || occ < 1) occ = 1;
     return sms * occ;
@@ -289,7 +297,8 @@ cudaError_t launch_cs_apply(const ChainApplyArgs &f, cudaStream_t st) {
     return chain_cfg_dispatch(f.n, [&](auto c) {
         using C = decltype(c);
         using AC = ApplyCs<C>;
-        auto kern = f.forward ? k_cs_apply<C, true> : k_cs_apply<C, false>;
+        auto kern = f.forward ? k_cs_apply<C, true, false>
+                              : (f.xbuf ? k_cs_apply<C, false, true> : k_cs_apply<C, false, false>);
         cudaError_t e = cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)AC::BYTES);
         if (e != cudaSuccess) return e;

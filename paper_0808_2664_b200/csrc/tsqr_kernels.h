@@ -28,7 +28,8 @@ struct ChainApplyArgs {
     const double *tcache;        // the factor's T cache
     double *C; int64_t ldc; int k;
     int forward;
-    const double *xbuf;          // !forward: per-tile X (n x n) from the node stage
+    const double *xbuf;          // !forward: per-tile X (n x n) from the node stage (form Q);
+                                 // nullptr: C <- Q C in place (the head rows hold C_R)
 };
 // Chain engine (tsqr_chain.cu): chunk rows, column blocks, persistent grid, factor.
 int chain_chunk_rows(int n);

@@ -210,3 +210,32 @@ def test_tree_reuse_and_repeat_determinism():
     assert tree.handle.value == h                     # workspace reused
     assert torch.equal(R1, R2) and torch.equal(A1, A2)  # bitwise deterministic
     tree.free()
+
+
+@pytest.mark.parametrize("m,n,b,s,k", [(4096, 16, 512, 128, 16), (3000, 24, 700, 175, 37), (2048, 64, 512, 128, 64),
+                                       (1500, 33, 400, 128, 130), (5000, 50, 4096, 192, 64), (777, 5, 100, 30, 1),
+                                       (3003, 56, 3003, 1001, 20), (4000, 49, 4000, 1000, 9), (700, 57, 700, 100, 57),
+                                       (50, 50, 50, 50, 8), (300, 9, 300, 40, 11), (5000, 100, 2048, 2048, 13),
+                                       (3000, 65, 1000, 1000, 65), (7000, 128, 3500, 512, 40), (300, 200, 300, 300, 7)])
+def test_apply_q(m, n, b, s, k):
+    """C <- Q C (the reverse traversal) against the oracle's apply_q on the same plan,
+    the round trip Q (Q^T C) = C, and Q [I; 0] = the explicit Q of form_q."""
+    A0, Ad, R, tree, p, f = _run(m, n, b, s, seed=11)
+    Ct = inputs.gaussian(m, k, seed=4)
+    C0 = _np(Ct).copy()
+    Cd = Ct.cuda()
+    T.apply_q(tree, Cd)
+    torch.cuda.synchronize()
+    Cg = _np(Cd)
+    assert orc.rel_fro(Cg, orc.tsqr_apply_q(f, C0.copy())) <= TOL_R
+    assert abs(np.linalg.norm(Cg) - np.linalg.norm(C0)) <= 1e-13 * np.linalg.norm(C0)
+    T.apply_qt(tree, Cd)                                      # back to C
+    torch.cuda.synchronize()
+    assert np.linalg.norm(_np(Cd) - C0) <= 1e-13 * np.linalg.norm(C0)
+    E = torch.zeros((n, m), dtype=torch.float64, device="cuda")
+    E[:, :n] = torch.eye(n, dtype=torch.float64, device="cuda")
+    T.apply_q(tree, E)
+    Q = T.form_q(tree)
+    torch.cuda.synchronize()
+    assert (torch.linalg.norm(E - Q) / torch.linalg.norm(Q)).item() <= 1e-14
+    tree.free()
