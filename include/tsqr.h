@@ -165,10 +165,23 @@ tsqr_status_t tsqr_cross_apply_qt(tsqr_tree_t tree, int32_t round, double *top, 
  * C (device, m_local x k, ldc >= m_local) is read in tree order -- rows 0..n-1
  * of the slab are the R coordinates, every other tile head its node's
  * complement coordinates -- so tsqr_apply_q(tsqr_apply_qt(C)) = C, and C =
- * [X; 0] gives Q[X; 0] (X = I: the explicit thin Q of tsqr_form_q).  Local tree
- * only: a tree with butterfly rounds (nranks > 1) returns TSQR_ERR_INVALID.
+ * [X; 0] gives Q[X; 0] (X = I: the explicit thin Q of tsqr_form_q).  With
+ * butterfly rounds (nranks > 1) the rounds go first, top-down, through
+ * tsqr_cross_apply_q; this call is then the local tree's part.
  * k = 0 is a no-op. */
 tsqr_status_t tsqr_apply_q(tsqr_tree_t tree, double *C, int64_t ldc, int64_t k, void *stream);
+
+/* Butterfly round of apply Q, rounds log2(nranks) .. 1 in that order, called by
+ * the two group heads of the round only (head_role 1 or 2 of
+ * tsqr_cross_partner; any other rank gets TSQR_ERR_INVALID and has nothing to
+ * do).  top (device, n x k, ldtop) holds this rank's C head rows (the group's R
+ * coordinates for head_role 1, the node's complement for head_role 2),
+ * partner_top (device, n x k, ld = n) the partner's; both compute
+ * Q_node [lower; upper] and keep their own half, written to top and to C's rows
+ * 0..n-1 (C: device, m_local x k, ldc >= m_local). */
+tsqr_status_t tsqr_cross_apply_q(tsqr_tree_t tree, int32_t round, double *top, int64_t ldtop,
+                                 const double *partner_top, double *C, int64_t ldc,
+                                 int64_t k, void *stream);
 
 /* Explicit thin Q of the rank's slab: Q (device, m_local x n, ldq >= m_local) =
  * rows of Q [I_n; 0].  Needs no communication: the

@@ -18,7 +18,7 @@ MAX_N = 256
 # every symbol include/tsqr.h declares
 SYMBOLS = ["tsqr_status_string", "tsqr_last_error", "tsqr_slab", "tsqr_plan_info", "tsqr_plan_export",
            "tsqr_cross_partner", "tsqr_factor", "tsqr_pack_r", "tsqr_cross_factor", "tsqr_apply_qt",
-           "tsqr_cross_apply_qt", "tsqr_apply_q", "tsqr_form_q", "tsqr_tree_free", "tsqr_tree_export_tau",
+           "tsqr_cross_apply_qt", "tsqr_apply_q", "tsqr_cross_apply_q", "tsqr_form_q", "tsqr_tree_free", "tsqr_tree_export_tau",
            "tsqr_tree_stage_ms"]
 
 
@@ -72,6 +72,7 @@ def lib():
         "tsqr_apply_qt": [_vp, _vp, _i64, _i64, _vp, _i64, _vp],
         "tsqr_cross_apply_qt": [_vp, _i32, _vp, _i64, _vp, _vp, _i64, _i64, _vp],
         "tsqr_apply_q": [_vp, _vp, _i64, _i64, _vp],
+        "tsqr_cross_apply_q": [_vp, _i32, _vp, _i64, _vp, _vp, _i64, _i64, _vp],
         "tsqr_form_q": [_vp, _vp, _i64, _vp],
         "tsqr_tree_free": [_vp],
         "tsqr_tree_export_tau": [_vp, _vp, _vp],

@@ -149,6 +149,17 @@ def cross_apply_qt(tree: Tree, rnd: int, top: torch.Tensor, partner_top: torch.T
     return top
 
 
+def cross_apply_q(tree: Tree, rnd: int, top: torch.Tensor, partner_top: torch.Tensor, C: torch.Tensor,
+                  stream=None):
+    """Butterfly round rnd of C <- Q C (group heads only): top <- this rank's half of
+    Q_node [lower; upper], also written to C's head rows."""
+    ptop, _, k, ldtop = _colmajor(top, "top")
+    pc, _, _, ldc = _colmajor(C, "C")
+    check(lib().tsqr_cross_apply_q(tree.handle, rnd, ptop, ldtop, partner_top.data_ptr(), pc, ldc, k,
+                                   _stream_ptr(stream)), "tsqr_cross_apply_q")
+    return top
+
+
 # ----------------------------------------------------------------- host-only
 def plan_info(m_local: int, n: int, o: Opts | None = None, **kw) -> dict:
     o = o if o is not None else opts(**kw)

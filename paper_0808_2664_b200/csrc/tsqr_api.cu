@@ -486,26 +486,52 @@ tsqr_status_t tsqr_cross_apply_qt(tsqr_tree_t t, int32_t round, double *top, int
         if (ws != TSQR_OK) return ws;
         CUDA_TRY(launch_wide_cross_apply(t->d_cross_y1 + (int64_t)(round - 1) * n * n,
                                          t->d_cross_tcache + (int64_t)(round - 1) * t->npan * 64, top, ldtop,
-                                         partner_top, lower, role, C, ldc, n, (int)k, t->d_wtmp,
+                                         partner_top, lower, role, C, ldc, n, (int)k, t->d_wtmp, 1,
                                          (cudaStream_t)stream),
                  "tsqr_cross_apply_qt");
     } else {
         CUDA_TRY(launch_cross_apply(t->NP, t->d_cross_y1 + (int64_t)(round - 1) * n * n,
                                     t->d_cross_tau + (int64_t)(round - 1) * n, top, ldtop, partner_top, lower, role,
-                                    C, ldc, n, (int)k, (cudaStream_t)stream),
+                                    C, ldc, n, (int)k, 1, (cudaStream_t)stream),
                  "tsqr_cross_apply_qt");
     }
     t->stream = (cudaStream_t)stream;
     return debug_sync(t, t->stream, "tsqr_cross_apply_qt");
 }
 
+tsqr_status_t tsqr_cross_apply_q(tsqr_tree_t t, int32_t round, double *top, int64_t ldtop,
+                                 const double *partner_top, double *C, int64_t ldc, int64_t k, void *stream) {
+    if (!t || !t->A || !top || !partner_top) return TSQR_ERR_INVALID;
+    if (round < 1 || round > t->cross_done) return TSQR_ERR_INVALID;
+    if (k < 0 || k > INT32_MAX || ldtop < t->plan.n) return TSQR_ERR_INVALID;
+    if (!C || ldc < t->plan.m_local) return TSQR_ERR_INVALID;
+    int32_t partner, lower, role;
+    if (tsqr_cross_partner(t->opts.nranks, t->opts.rank, round, &partner, &lower, &role) != TSQR_OK)
+        return TSQR_ERR_INVALID;
+    if (role == 0) return TSQR_ERR_INVALID;        // only the group heads take part in this round
+    if (k == 0) return TSQR_OK;
+    const int n = (int)t->plan.n;
+    if (t->wide) {
+        tsqr_status_t ws = wide_tmp(t, k);
+        if (ws != TSQR_OK) return ws;
+        CUDA_TRY(launch_wide_cross_apply(t->d_cross_y1 + (int64_t)(round - 1) * n * n,
+                                         t->d_cross_tcache + (int64_t)(round - 1) * t->npan * 64, top, ldtop,
+                                         partner_top, lower, role, C, ldc, n, (int)k, t->d_wtmp, 0,
+                                         (cudaStream_t)stream),
+                 "tsqr_cross_apply_q");
+    } else {
+        CUDA_TRY(launch_cross_apply(t->NP, t->d_cross_y1 + (int64_t)(round - 1) * n * n,
+                                    t->d_cross_tau + (int64_t)(round - 1) * n, top, ldtop, partner_top, lower, role,
+                                    C, ldc, n, (int)k, 0, (cudaStream_t)stream),
+                 "tsqr_cross_apply_q");
+    }
+    t->stream = (cudaStream_t)stream;
+    return debug_sync(t, t->stream, "tsqr_cross_apply_q");
+}
+
 tsqr_status_t tsqr_apply_q(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, void *stream) {
     if (!t || !t->A) return TSQR_ERR_INVALID;
     if (k < 0 || k > INT32_MAX) return TSQR_ERR_INVALID;
-    if (t->cross_rounds != 0) {
-        g_last_error = "tsqr_apply_q: trees with butterfly rounds are not supported";
-        return TSQR_ERR_INVALID;
-    }
     if (k == 0) return TSQR_OK;
     if (!C || ldc < t->plan.m_local) return TSQR_ERR_INVALID;
     const int n = (int)t->plan.n;

@@ -63,7 +63,7 @@ cudaError_t launch_wide_cross_factor(double *A, int64_t lda, int n, const double
                                      cudaStream_t st);
 cudaError_t launch_wide_cross_apply(const double *Y1, const double *tcache, double *top, int64_t ldtop,
                                     const double *ptop, int is_lower, int role, double *C, int64_t ldc, int n, int k,
-                                    double *tmp, cudaStream_t st);
+                                    double *tmp, int forward, cudaStream_t st);
 cudaError_t launch_wide_cross_root_x(const double *Y1s, const double *tcaches, int64_t tstride, int rounds, int rank,
                                      int n, double *tmp, double *X0, cudaStream_t st);
 // Balanced contiguous split of the tiles over `grid` persistent CTAs by chunk count.
@@ -87,7 +87,7 @@ cudaError_t launch_cross_factor(int NP, double *A, int64_t lda, int n, const dou
                                 double *Y1, double *tau, double *R, int64_t ldr, cudaStream_t st);
 cudaError_t launch_cross_apply(int NP, const double *Y1, const double *tau, double *top, int64_t ldtop,
                                const double *ptop, int is_lower, int role, double *C, int64_t ldc, int n,
-                               int k, cudaStream_t st);
+                               int k, int forward, cudaStream_t st);
 cudaError_t launch_cross_root_x(int NP, const double *Y1s, const double *taus, int rounds, int rank, int n,
                                 double *X0, cudaStream_t st);
 

@@ -1165,20 +1165,21 @@ __global__ void k_wide_unstack_c(const double *tmp, int n, int k, double *top, i
     for (int64_t e = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; e < (int64_t)n * k; e += (int64_t)blockDim.x * gridDim.x) {
         const int r = (int)(e % n);
         const int64_t c = e / n;
-        const double ra = tmp[r + c * 2 * n];
+        const double ra = tmp[(role == 3 ? n : 0) + r + c * 2 * n];     // role 3 (Q C): the upper half
         top[r + c * ldtop] = ra;
-        if (role == 1) C[r + c * ldc] = ra;
+        if (role == 1 || role == 3) C[r + c * ldc] = ra;
         if (role == 2) C[r + c * ldc] = tmp[n + r + c * 2 * n];
     }
 }
 cudaError_t launch_wide_cross_apply(const double *Y1, const double *tcache, double *top, int64_t ldtop,
                                     const double *ptop, int is_lower, int role, double *C, int64_t ldc, int n, int k,
-                                    double *tmp, cudaStream_t st) {
+                                    double *tmp, int forward, cudaStream_t st) {
     const int64_t tot = (int64_t)n * k;
     const int blocks = (int)((tot + 255) / 256 < 4096 ? (tot + 255) / 256 : 4096);
     k_wide_stack_c<<<blocks, 256, 0, st>>>(top, ldtop, ptop, is_lower, n, k, tmp);
-    cudaError_t e = launch_wide_apply_node1(Y1, n, n, tcache, tmp, 2 * n, tmp + n, 2 * n, k, 1, st);
+    cudaError_t e = launch_wide_apply_node1(Y1, n, n, tcache, tmp, 2 * n, tmp + n, 2 * n, k, forward, st);
     if (e != cudaSuccess) return e;
+    if (!forward) role = is_lower ? 1 : 3;                  // Q C: keep this rank's half
     k_wide_unstack_c<<<blocks, 256, 0, st>>>(tmp, n, k, top, ldtop, role, C, ldc);
     return cudaGetLastError();
 }

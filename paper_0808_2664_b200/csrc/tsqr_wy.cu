@@ -6,7 +6,8 @@
 //                  butterfly (Alg. TSQR:par P:1667-1707): structured combine of
 //                  this rank's R and the partner's packed R, identical on both.
 //  k_cross_apply   (a8): the round's reflectors applied to the stacked heads of
-//                  Q^T C (this rank's and the partner's), keeping this rank's half.
+//                  Q^T C (this rank's and the partner's), keeping the R coordinates;
+//                  or of Q C (reverse traversal), keeping this rank's half.
 //  k_cross_root_x  (a9): the root X of this rank for form Q, from the replicated
 //                  round factors (no communication).
 //  k_identity, k_pack_r, k_copy_block: X = I, R -> packed upper triangle, and
@@ -318,7 +319,7 @@ k_cross_factor(double *A, int64_t lda, int n, const double *partner_packed, int 
 }
 
 // Butterfly round of apply Q^T on the R coordinates (n x k tops).
-template <class G>
+template <class G, bool kFwd>
 __global__ void __launch_bounds__(G::NT)
 k_cross_apply(const double *Y1g, const double *taug, double *top, int64_t ldtop, const double *partner_top,
               int is_lower, int head_role, double *C, int64_t ldc, int n, int k) {
@@ -345,12 +346,13 @@ k_cross_apply(const double *Y1g, const double *taug, double *top, int64_t ldtop,
             tile[c * G::LD + r] = v;
         }
         __syncthreads();
-        apply_panels<G, G::NP, true, true>(sm, n, 2 * G::NP, kc);
+        apply_panels<G, G::NP, true, kFwd>(sm, n, 2 * G::NP, kc);
         for (int e = threadIdx.x; e < kc * n; e += G::NT) {
             const int r = e % n, c = e / n;
-            const double ra = tile[c * G::LD + r];
+            // Q^T: the new R coordinates; Q C (!kFwd): this rank's half of the result
+            const double ra = tile[c * G::LD + (kFwd || is_lower ? 0 : G::NP) + r];
             top[r + (int64_t)(c0 + c) * ldtop] = ra;
-            if (head_role == 1) C[r + (int64_t)(c0 + c) * ldc] = ra;
+            if (!kFwd || head_role == 1) C[r + (int64_t)(c0 + c) * ldc] = ra;
             if (head_role == 2) C[r + (int64_t)(c0 + c) * ldc] = tile[c * G::LD + G::NP + r];
         }
         __syncthreads();
@@ -444,19 +446,21 @@ cudaError_t launch_cross_factor(int NP, double *A, int64_t lda, int n, const dou
 template <class G>
 static cudaError_t launch_cross_apply_t(const double *Y1, const double *tau, double *top, int64_t ldtop,
                                         const double *ptop, int is_lower, int role, double *C, int64_t ldc, int n,
-                                        int k, cudaStream_t st) {
+                                        int k, int forward, cudaStream_t st) {
     const size_t sm = Smem<G, G::NP>::bytes;
-    cudaError_t e = set_smem((const void *)k_cross_apply<G>, sm);
+    auto kern = forward ? k_cross_apply<G, true> : k_cross_apply<G, false>;
+    cudaError_t e = set_smem((const void *)kern, sm);
     if (e != cudaSuccess) return e;
-    k_cross_apply<G><<<1, G::NT, sm, st>>>(Y1, tau, top, ldtop, ptop, is_lower, role, C, ldc, n, k);
+    kern<<<1, G::NT, sm, st>>>(Y1, tau, top, ldtop, ptop, is_lower, role, C, ldc, n, k);
     return cudaGetLastError();
 }
 
 cudaError_t launch_cross_apply(int NP, const double *Y1, const double *tau, double *top, int64_t ldtop,
                                const double *ptop, int is_lower, int role, double *C, int64_t ldc, int n, int k,
-                               cudaStream_t st) {
-    return NP <= 32 ? launch_cross_apply_t<Geo<4, 8, 4>>(Y1, tau, top, ldtop, ptop, is_lower, role, C, ldc, n, k, st)
-                    : launch_cross_apply_t<Geo<8, 8, 8>>(Y1, tau, top, ldtop, ptop, is_lower, role, C, ldc, n, k, st);
+                               int forward, cudaStream_t st) {
+    return NP <= 32
+               ? launch_cross_apply_t<Geo<4, 8, 4>>(Y1, tau, top, ldtop, ptop, is_lower, role, C, ldc, n, k, forward, st)
+               : launch_cross_apply_t<Geo<8, 8, 8>>(Y1, tau, top, ldtop, ptop, is_lower, role, C, ldc, n, k, forward, st);
 }
 
 template <class G>

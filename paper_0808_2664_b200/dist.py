@@ -7,7 +7,8 @@ current R (n(n+1)/2 words, the Cor. 2 minimum), exchange it with
 partner r XOR 2^(k-1) over NCCL (torch.distributed point-to-point, NVLink), and
 run the structured combine on [R_lower; R_upper] -- both partners compute the
 same node, so R ends replicated.  Apply Q^T exchanges the n x k
-R coordinates per round; form Q needs no communication (every rank holds the
+R coordinates per round, apply Q (its inverse) the same between the group heads;
+form Q needs no communication (every rank holds the
 node factors on its root-to-leaf path).
 
 The round logic is written once (`RankState`) and driven either by
@@ -50,8 +51,21 @@ class CudaEngine:
     def cross_apply(self, tree, rnd, top, partner_top, C):
         api.cross_apply_qt(tree, rnd, top, partner_top, C)
 
+    def cross_apply_q(self, tree, rnd, top, partner_top, C):
+        api.cross_apply_q(tree, rnd, top, partner_top, C)
+
+    def apply_q_local(self, tree, C):
+        api.apply_q(tree, C)
+
     def form_q(self, tree):
         return api.form_q(tree)
+
+
+def head_role(rank: int, rnd: int) -> int:
+    """1: leftmost rank of the 2^rnd group (lower half), 2: leftmost of its upper half, 0: other
+    (tsqr_cross_partner's head_role)."""
+    pos = rank & ((1 << rnd) - 1)
+    return 1 if pos == 0 else (2 if pos == 1 << (rnd - 1) else 0)
 
 
 def rounds_of(nranks: int) -> int:
@@ -107,6 +121,22 @@ class RankState:
     def apply_finish(self, rnd, recv):
         self.engine.cross_apply(self.tree, rnd, self.top, recv, self.C)
 
+    # ------------------------------------------------------ apply Q (reverse)
+    # Rounds log2 G .. 1: in round k only the two group heads take part -- the
+    # lower holds the group's R coordinates, the upper this node's complement
+    # (both in their C head rows, where apply_qt left them); each keeps its half of
+    # Q_node [lower; upper], which is its subgroup's R coordinates one round down.
+    def apply_q_send(self, rnd, C):
+        if head_role(self.rank, rnd) == 0:
+            return None
+        buf = C[:, :self.n].contiguous()                  # n x k head rows, ld n
+        self.sent.append((-rnd, buf.numel()))
+        return buf
+
+    def apply_q_finish(self, rnd, recv, C):
+        mine = C[:, :self.n].contiguous()                 # the sent buffer may be the partner's recv
+        self.engine.cross_apply_q(self.tree, rnd, mine, recv, C)
+
 
 def _exchange(send: torch.Tensor, partner: int, group=None) -> torch.Tensor:
     import torch.distributed as dist
@@ -145,6 +175,18 @@ def apply_qt(st: RankState, C_local, group=None):
     return C_local, st.top
 
 
+def apply_q(st: RankState, C_local, group=None):
+    """Collective: C_local <- rows of Q C, C in tree order (the inverse of apply_qt)."""
+    for rnd in range(rounds_of(st.nranks), 0, -1):
+        send = st.apply_q_send(rnd, C_local)
+        if send is None:
+            continue
+        recv = _exchange(send, st.rank ^ (1 << (rnd - 1)), group)
+        st.apply_q_finish(rnd, recv, C_local)
+    st.engine.apply_q_local(st.tree, C_local)
+    return C_local
+
+
 def form_q(st: RankState):
     """Local (communication-free) explicit Q rows of this rank."""
     return st.engine.form_q(st.tree)
@@ -173,4 +215,15 @@ def apply_qt_virtual(states, C_slabs):
         sends = [st.apply_send(rnd) for st in states]
         for st in states:
             st.apply_finish(rnd, sends[st.rank ^ (1 << (rnd - 1))])
+    return C_slabs
+
+
+def apply_q_virtual(states, C_slabs):
+    for rnd in range(rounds_of(len(states)), 0, -1):
+        sends = [st.apply_q_send(rnd, C) for st, C in zip(states, C_slabs)]
+        for st, C in zip(states, C_slabs):
+            if sends[st.rank] is not None:
+                st.apply_q_finish(rnd, sends[st.rank ^ (1 << (rnd - 1))], C)
+    for st, C in zip(states, C_slabs):
+        st.engine.apply_q_local(st.tree, C)
     return C_slabs

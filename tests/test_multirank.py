@@ -93,6 +93,20 @@ class OracleEngine:
         elif pos == 1 << (rnd - 1):
             C.numpy()[:, :t.n] = Cb.T
 
+    def cross_apply_q(self, t, rnd, top, ptop, C):
+        partner = t.rank ^ (1 << (rnd - 1))
+        mine, theirs = _np(top).copy(), _np(ptop).copy()
+        Ca, Cb = (mine, theirs) if t.rank < partner else (theirs, mine)
+        Y1, tau = t.cross[rnd - 1]
+        _node_apply(Y1, tau, Ca, Cb, False)
+        keep = Ca if t.rank < partner else Cb
+        top.numpy()[:] = keep.T
+        C.numpy()[:, :t.n] = keep.T
+
+    def apply_q_local(self, t, C):
+        out = orc.tsqr_apply_q(t.f, _np(C))
+        C.numpy()[:] = out.T
+
     def form_q(self, t):
         n = t.n
         X = np.eye(n)
@@ -113,7 +127,8 @@ def _global_reference(m, n, b, s, G, k, c=0):
     A = inputs.to_numpy_colmajor(inputs.gaussian(m, n, 0))
     C = inputs.to_numpy_colmajor(inputs.gaussian(m, k, 1))
     f = orc.tsqr_factor(A, orc.plan(m, n, b, s, G, c))
-    return f.R, orc.tsqr_apply_qt(f, C), orc.tsqr_form_q(f)
+    Z = inputs.to_numpy_colmajor(inputs.gaussian(m, k, 2))
+    return f.R, orc.tsqr_apply_qt(f, C.copy()), orc.tsqr_form_q(f), orc.tsqr_apply_q(f, Z)
 
 
 def _free_port():
@@ -132,9 +147,16 @@ def _worker(rank, world, port, m, n, b, s, k, q):
         A = inputs.gaussian_rows(row0, ml, n, 0)
         C = inputs.gaussian_rows(row0, ml, k, 1)
         st = tdist.factor(A, b, s, engine=OracleEngine())
+        C0 = C.clone()
         tdist.apply_qt(st, C)
+        QtC = C.clone()
+        tdist.apply_q(st, C)                                   # back to C0
+        back = _np(C).copy()
+        Z = inputs.gaussian_rows(row0, ml, k, 2)
+        tdist.apply_q(st, Z)
         Q = tdist.form_q(st)
-        q.put((rank, row0, ml, _np(st.R).copy(), _np(C).copy(), _np(st.top).copy(), _np(Q).copy(), st.sent))
+        q.put((rank, row0, ml, _np(st.R).copy(), _np(QtC).copy(), _np(st.top).copy(), _np(Q).copy(), st.sent,
+               back, _np(C0).copy(), _np(Z).copy()))
     finally:
         dist.destroy_process_group()
 
@@ -152,18 +174,47 @@ def test_butterfly_gloo(world, m, n, b, s, k):
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    Rref, QtC_ref, Qref = _global_reference(m, n, b, s, world, k)
+    Rref, QtC_ref, Qref, QZ_ref = _global_reference(m, n, b, s, world, k)
     rounds = int(np.log2(world))
-    for rank, row0, ml, R, C, top, Q, sent in sorted(res, key=lambda x: x[0]):
+    for rank, row0, ml, R, C, top, Q, sent, back, C0, QZ in sorted(res, key=lambda x: x[0]):
         assert np.array_equal(R, Rref)                              # replicated and bitwise equal
         assert orc.rel_fro(C, QtC_ref[row0:row0 + ml]) <= 1e-13     # tree-order rows of this rank
         assert orc.rel_fro(top, QtC_ref[:n]) <= 1e-13              # thin part replicated
         assert orc.rel_fro(Q, Qref[row0:row0 + ml]) <= 1e-13
+        assert orc.rel_fro(back, C0) <= 1e-13                       # apply_q(apply_qt(C)) = C
+        assert orc.rel_fro(QZ, QZ_ref[row0:row0 + ml]) <= 1e-13     # Q Z = the global tree's
+        # apply Q: a rank exchanges only in the rounds where it is a group head
+        heads = [r for r in range(1, rounds + 1) if tdist.head_role(rank, r)]
+        assert sorted(-r for r, _ in sent if r < 0) == sorted(2 * heads)
+        sent = [x for x in sent if x[0] > 0]
         # counts (Table 1; Cor. 2): log2 G messages of n(n+1)/2 words
         fac = [w for r_, w in sent if True][:rounds]
         assert len(sent) == 2 * rounds
         assert all(w == n * (n + 1) // 2 for w in fac)
         assert all(w == n * k for w in [w for _, w in sent][rounds:])
+
+
+@pytest.mark.parametrize("G,m,n,b,s,k", [(2, 20000, 12, 4096, 512, 5), (4, 9000, 8, 1000, 250, 3)])
+def test_butterfly_virtual_oracle(G, m, n, b, s, k):
+    """The loopback driver (the one the GPU tests use) with the oracle engine: apply Q^T,
+    apply Q (each round's sent buffer is also the partner's receive buffer) and the
+    round trip, against the global tree."""
+    from paper_0808_2664_b200 import api
+    rows = [api.slab(m, n, b, G, r) for r in range(G)]
+    eng = OracleEngine()
+    states = tdist.factor_virtual([inputs.gaussian_rows(r0, ml, n, 0) for r0, ml in rows], b, s, engine=eng)
+    cs = [inputs.gaussian_rows(r0, ml, k, 1) for r0, ml in rows]
+    c0 = [C.clone() for C in cs]
+    zs = [inputs.gaussian_rows(r0, ml, k, 2) for r0, ml in rows]
+    tdist.apply_qt_virtual(states, cs)
+    Rref, QtC_ref, Qref, QZ_ref = _global_reference(m, n, b, s, G, k)
+    for (r0, ml), C in zip(rows, cs):
+        assert orc.rel_fro(_np(C), QtC_ref[r0:r0 + ml]) <= 1e-13
+    tdist.apply_q_virtual(states, cs)
+    tdist.apply_q_virtual(states, zs)
+    for (r0, ml), C, C0, Z in zip(rows, cs, c0, zs):
+        assert orc.rel_fro(_np(C), _np(C0)) <= 1e-13
+        assert orc.rel_fro(_np(Z), QZ_ref[r0:r0 + ml]) <= 1e-13
 
 
 @pytest.mark.gpu
@@ -179,17 +230,24 @@ def test_butterfly_virtual_ranks_cuda(G, m, n, b, s, k):
         slabs.append(inputs.gaussian_rows(row0, ml, n, 0).cuda())
         cs.append(inputs.gaussian_rows(row0, ml, k, 1).cuda())
     states = tdist.factor_virtual(slabs, b, s)
+    c0 = [C.clone() for C in cs]
     tdist.apply_qt_virtual(states, cs)
     Qs = [tdist.form_q(st) for st in states]
+    qtc = [C.clone() for C in cs]
+    tdist.apply_q_virtual(states, cs)                               # back to C
+    zs = [inputs.gaussian_rows(row0, ml, k, 2).cuda() for row0, ml in rows]
+    tdist.apply_q_virtual(states, zs)
     torch.cuda.synchronize()
     c = api.plan_info(rows[0][1], n, block_rows=b, tile_rows=s, nranks=G, rank=0)["chunk_rows"]
-    Rref, QtC_ref, Qref = _global_reference(m, n, b, s, G, k, c)
-    for st, (row0, ml), C, Q in zip(states, rows, cs, Qs):
+    Rref, QtC_ref, Qref, QZ_ref = _global_reference(m, n, b, s, G, k, c)
+    for st, (row0, ml), C, Q, C0, Cb, Z in zip(states, rows, qtc, Qs, c0, cs, zs):
         R = inputs.to_numpy_colmajor(st.R)
         assert np.array_equal(R, inputs.to_numpy_colmajor(states[0].R))   # bitwise replicated
         assert orc.rel_fro(orc.sign_normalise(R), orc.sign_normalise(Rref)) <= 1e-11
         assert orc.rel_fro(inputs.to_numpy_colmajor(C), QtC_ref[row0:row0 + ml]) <= 1e-11
         assert orc.rel_fro(inputs.to_numpy_colmajor(st.top), QtC_ref[:n]) <= 1e-11
         assert orc.rel_fro(inputs.to_numpy_colmajor(Q), Qref[row0:row0 + ml]) <= 1e-11
+        assert orc.rel_fro(inputs.to_numpy_colmajor(Cb), inputs.to_numpy_colmajor(C0)) <= 1e-13
+        assert orc.rel_fro(inputs.to_numpy_colmajor(Z), QZ_ref[row0:row0 + ml]) <= 1e-11
     for st in states:
         st.tree.free()
