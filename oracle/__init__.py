@@ -245,6 +245,64 @@ def node_y1(f: Factor, k: int) -> np.ndarray:
     return f.Y1[k].reshape(n, n, order="F")
 
 
+# ------------------------------------------------------------------- CAQR
+@dataclass
+class CaqrFactor:
+    m: int
+    N: int
+    panel: int
+    panels: list           # (c0, Factor of the panel's TSQR over rows c0..m-1)
+    R: np.ndarray          # N x N upper triangular
+
+
+def caqr_factor(A, panel: int, b: int, s: int | None = None, chunk=lambda w: 0) -> CaqrFactor:
+    """Right-looking CAQR with TSQR panels on one processor column: "CAQR simply implements
+    the right-looking QR factorization using ... TSQR as the panel factorization" (Sec. 3,
+    P:2944-2946); Alg. CAQR:j ([TR] P:3992-4048) with one process row: panel j (columns
+    c0..c0+w-1, rows c0..m-1) is factored by TSQR (line 1), then Q_j^T is applied to the
+    trailing columns (line 3 and the tree stages of lines 4-9, i.e. tsqr_apply_qt); rows
+    c0..c0+w-1 of the updated trailing block are R's row block, rows c0+w.. (tree order)
+    are the next panel's input.  chunk(w) gives the leaves' chunk height for a panel of
+    width w (the plan parameter c of reading R20)."""
+    W = np.array(A, dtype=np.float64, order="F", copy=True)
+    m, N = W.shape
+    R = np.zeros((N, N), order="F")
+    panels = []
+    for c0 in range(0, N, panel):
+        w = min(panel, N - c0)
+        f = tsqr_factor(np.array(W[c0:, c0:c0 + w], order="F"), plan(m - c0, w, b, s, 1, chunk(w)))
+        R[c0:c0 + w, c0:c0 + w] = f.R
+        if c0 + w < N:
+            T = tsqr_apply_qt(f, np.array(W[c0:, c0 + w:], order="F"))
+            W[c0:, c0 + w:] = T
+            R[c0:c0 + w, c0 + w:] = T[:w]
+        panels.append((c0, f))
+    return CaqrFactor(m, N, panel, panels, R)
+
+
+def caqr_apply_qt(cf: CaqrFactor, C) -> np.ndarray:
+    """C <- Q^T C = Q_p^T ... Q_1^T C, Q_j acting on rows c0_j..m-1 (tree order)."""
+    C = np.array(C, dtype=np.float64, order="F", copy=True)
+    for c0, f in cf.panels:
+        C[c0:] = tsqr_apply_qt(f, np.array(C[c0:], order="F"))
+    return C
+
+
+def caqr_apply_q(cf: CaqrFactor, C) -> np.ndarray:
+    """C <- Q C = Q_1 ... Q_p C (the panels in reverse order)."""
+    C = np.array(C, dtype=np.float64, order="F", copy=True)
+    for c0, f in reversed(cf.panels):
+        C[c0:] = tsqr_apply_q(f, np.array(C[c0:], order="F"))
+    return C
+
+
+def caqr_form_q(cf: CaqrFactor) -> np.ndarray:
+    """Explicit thin Q = Q [I_N; 0] (m x N)."""
+    E = np.zeros((cf.m, cf.N), order="F")
+    E[:cf.N] = np.eye(cf.N)
+    return caqr_apply_q(cf, E)
+
+
 # --------------------------------------------------------------- checkers
 def sign_normalise(R, Q=None):
     """R^ = diag(s) R, Q^ = Q diag(s), s = sign(diag R) (sign(0)=+1) -- reading R9."""

@@ -436,3 +436,36 @@ def test_chain_r_vs_lapack_and_q(rows, n, c):
     Q = orc.tsqr_form_q(f)
     assert np.linalg.norm(A - Q @ R) / np.linalg.norm(A) <= 1e-13
     assert np.linalg.norm(Q.T @ Q - np.eye(n)) <= 1e-13
+
+
+# ------------------------------------------------------------------- CAQR
+@pytest.mark.parametrize("m,N,panel,b,s,c", [(600, 40, 16, 200, 100, 0), (777, 37, 10, 250, 90, 16),
+                                              (300, 300, 64, 300, 300, 0), (1000, 70, 70, 400, 200, 0)])
+def test_caqr_pins(m, N, panel, b, s, c):
+    """CAQR (Sec. 3; Alg. CAQR:j [TR] P:3992-4048) pinned to LAPACK's R (unique up to
+    signs for a full-rank A), A = QR, Q^T Q = I, the inverse pair apply_q(apply_qt(C)) = C and the
+    thin part of Q^T C = R^-T A^T C."""
+    rng = np.random.default_rng(3)
+    A = np.asfortranarray(rng.standard_normal((m, N)))
+    cf = orc.caqr_factor(A, panel, b, s, chunk=lambda w: min(c, 8 * ((w + 7) // 8)) if c else 0)
+    R = cf.R
+    assert np.all(np.tril(R, -1) == 0.0)
+    Rl = scipy.linalg.qr(A, mode="r")[0][:N]
+    assert orc.rel_fro(orc.sign_normalise(R), orc.sign_normalise(Rl)) <= 1e-12
+    Q = orc.caqr_form_q(cf)
+    assert np.linalg.norm(A - Q @ R) / np.linalg.norm(A) <= 1e-14
+    assert np.linalg.norm(Q.T @ Q - np.eye(N)) <= 1e-13
+    C = rng.standard_normal((m, 5))
+    QtC = orc.caqr_apply_qt(cf, C)
+    assert np.linalg.norm(orc.caqr_apply_q(cf, QtC) - C) <= 1e-13 * np.linalg.norm(C)
+    thin = scipy.linalg.solve_triangular(R, A.T @ C, trans="T")
+    assert orc.rel_fro(QtC[:N], thin) <= 1e-12
+
+
+def test_caqr_single_panel_is_tsqr():
+    """panel >= N: CAQR is exactly one TSQR (same plan, bitwise)."""
+    A = np.asfortranarray(np.random.default_rng(4).standard_normal((900, 24)))
+    cf = orc.caqr_factor(A, 32, 300, 100)
+    f = orc.tsqr_factor(A.copy(order="F"), orc.plan(900, 24, 300, 100, 1, 0))
+    assert np.array_equal(cf.R, f.R)
+    assert np.array_equal(orc.caqr_form_q(cf), orc.tsqr_form_q(f))
