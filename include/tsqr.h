@@ -188,6 +188,43 @@ tsqr_status_t tsqr_cross_apply_q(tsqr_tree_t tree, int32_t round, double *top, i
  * cross-rank node factors are replicated on every rank. */
 tsqr_status_t tsqr_form_q(tsqr_tree_t tree, double *Q, int64_t ldq, void *stream);
 
+/* ---------------------------------------------------------------- CAQR
+ * Right-looking QR of an m x N matrix (N may exceed TSQR_MAX_N) with TSQR
+ * panels: "CAQR simply implements the right-looking QR factorization using ...
+ * TSQR as the panel factorization" (Sec. 3); Alg. CAQR:j ([TR]
+ * P:3992-4048) on one GPU (one process row).  Panel j = columns c0..c0+w-1
+ * (c0 = j*panel_cols, w = min(panel_cols, N - c0)) is factored by tsqr_factor
+ * over rows c0..m-1 (line 1), then Q_j^T is applied to the trailing columns by
+ * tsqr_apply_qt (line 3 and the tree stages, lines 4-9); rows c0..c0+w-1 of the
+ * update are R's row block, rows c0+w.. (panel j's tree order) the next panel.
+ * Q = Q_1 diag(I, Q_2) ... ; Q_j acts on rows c0_j..m-1. */
+typedef struct tsqr_caqr_s *tsqr_caqr_t;
+
+/* A (device, m x N, lda >= m, m >= N): IN the matrix, OUT the panels' reflectors
+ * and the trailing updates; BORROWED until tsqr_caqr_free.  R (device, N x N,
+ * ldr >= N): OUT upper triangular, exact zeros below.  opts: as tsqr_factor's,
+ * used for every panel (nranks must be 0 or 1: TSQR_ERR_UNSUPPORTED otherwise).
+ * panel_cols in [1, TSQR_MAX_N].  *caqr: OUT a new handle, or IN a handle of the
+ * same (m, N, panel_cols, block_rows, tile_rows) whose panel trees are reused
+ * (TSQR_ERR_INVALID for another shape).  Errors of a panel's TSQR are returned
+ * as they are (e.g. TSQR_ERR_SHAPE when a panel's row block has < w rows). */
+tsqr_status_t tsqr_caqr_factor(int64_t m, int64_t N, double *A, int64_t lda, int64_t panel_cols,
+                               double *R, int64_t ldr, const tsqr_opts_t *opts, void *stream,
+                               tsqr_caqr_t *caqr);
+
+/* C <- Q^T C (C: device, m x k, ldc >= m), the panels' trees in order, each in
+ * its own tree order on rows c0_j..m-1: rows 0..N-1 become Q_thin^T C. */
+tsqr_status_t tsqr_caqr_apply_qt(tsqr_caqr_t caqr, double *C, int64_t ldc, int64_t k, void *stream);
+
+/* C <- Q C, the inverse of tsqr_caqr_apply_qt (panels in reverse order). */
+tsqr_status_t tsqr_caqr_apply_q(tsqr_caqr_t caqr, double *C, int64_t ldc, int64_t k, void *stream);
+
+/* Explicit thin Q (device, m x N, ldq >= m) = Q [I_N; 0]. */
+tsqr_status_t tsqr_caqr_form_q(tsqr_caqr_t caqr, double *Q, int64_t ldq, void *stream);
+
+/* Release the handle and its panel trees. */
+tsqr_status_t tsqr_caqr_free(tsqr_caqr_t caqr);
+
 /* Release the tree's device memory (stream-ordered on the last stream used). */
 tsqr_status_t tsqr_tree_free(tsqr_tree_t tree);
 

@@ -19,7 +19,8 @@ MAX_N = 256
 SYMBOLS = ["tsqr_status_string", "tsqr_last_error", "tsqr_slab", "tsqr_plan_info", "tsqr_plan_export",
            "tsqr_cross_partner", "tsqr_factor", "tsqr_pack_r", "tsqr_cross_factor", "tsqr_apply_qt",
            "tsqr_cross_apply_qt", "tsqr_apply_q", "tsqr_cross_apply_q", "tsqr_form_q", "tsqr_tree_free", "tsqr_tree_export_tau",
-           "tsqr_tree_stage_ms"]
+           "tsqr_tree_stage_ms", "tsqr_caqr_factor", "tsqr_caqr_apply_qt", "tsqr_caqr_apply_q",
+           "tsqr_caqr_form_q", "tsqr_caqr_free"]
 
 
 class TsqrError(RuntimeError):
@@ -77,6 +78,11 @@ def lib():
         "tsqr_tree_free": [_vp],
         "tsqr_tree_export_tau": [_vp, _vp, _vp],
         "tsqr_tree_stage_ms": [_vp, _vp, _vp],
+        "tsqr_caqr_factor": [_i64, _i64, _vp, _i64, _i64, _vp, _i64, ctypes.POINTER(Opts), _vp, ctypes.POINTER(_vp)],
+        "tsqr_caqr_apply_qt": [_vp, _vp, _i64, _i64, _vp],
+        "tsqr_caqr_apply_q": [_vp, _vp, _i64, _i64, _vp],
+        "tsqr_caqr_form_q": [_vp, _vp, _i64, _vp],
+        "tsqr_caqr_free": [_vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)

@@ -160,6 +160,70 @@ def cross_apply_q(tree: Tree, rnd: int, top: torch.Tensor, partner_top: torch.Te
     return top
 
 
+# ------------------------------------------------------------------- CAQR
+class Caqr:
+    """Right-looking CAQR with TSQR panels (tsqr_caqr_*): one panel tree per panel_cols
+    columns.  Borrows A until freed."""
+
+    def __init__(self):
+        self.handle = ctypes.c_void_p(None)
+        self.A = None
+        self.m = self.N = self.panel = 0
+
+    def free(self):
+        if self.handle:
+            lib().tsqr_caqr_free(self.handle)
+            self.handle = ctypes.c_void_p(None)
+        self.A = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def caqr(A: torch.Tensor, panel_cols: int, block_rows: int = 0, tile_rows: int = 0, R: torch.Tensor | None = None,
+         handle: Caqr | None = None, stream=None, debug: bool = False):
+    """QR of A (column-major m x N) in place by CAQR.  Returns (R, handle)."""
+    pa, m, N, lda = _colmajor(A, "A")
+    if R is None:
+        R = torch.empty((N, N), dtype=torch.float64, device=A.device)
+    pr, _, _, ldr = _colmajor(R, "R")
+    o = opts(block_rows, tile_rows, 1, 0, debug)
+    c = handle if handle is not None else Caqr()
+    h = c.handle
+    check(lib().tsqr_caqr_factor(m, N, pa, lda, panel_cols, pr, ldr, ctypes.byref(o), _stream_ptr(stream),
+                                 ctypes.byref(h)), "tsqr_caqr_factor")
+    c.handle = h
+    c.A, c.m, c.N, c.panel = A, m, N, panel_cols
+    return R, c
+
+
+def caqr_apply_qt(c: Caqr, C: torch.Tensor, stream=None) -> torch.Tensor:
+    pc, m, k, ldc = _colmajor(C, "C")
+    if m != c.m:
+        raise ValueError("C must have m rows")
+    check(lib().tsqr_caqr_apply_qt(c.handle, pc, ldc, k, _stream_ptr(stream)), "tsqr_caqr_apply_qt")
+    return C
+
+
+def caqr_apply_q(c: Caqr, C: torch.Tensor, stream=None) -> torch.Tensor:
+    pc, m, k, ldc = _colmajor(C, "C")
+    if m != c.m:
+        raise ValueError("C must have m rows")
+    check(lib().tsqr_caqr_apply_q(c.handle, pc, ldc, k, _stream_ptr(stream)), "tsqr_caqr_apply_q")
+    return C
+
+
+def caqr_form_q(c: Caqr, Q: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    if Q is None:
+        Q = torch.empty((c.N, c.m), dtype=torch.float64, device=c.A.device)
+    pq, _, _, ldq = _colmajor(Q, "Q")
+    check(lib().tsqr_caqr_form_q(c.handle, pq, ldq, _stream_ptr(stream)), "tsqr_caqr_form_q")
+    return Q
+
+
 # ----------------------------------------------------------------- host-only
 def plan_info(m_local: int, n: int, o: Opts | None = None, **kw) -> dict:
     o = o if o is not None else opts(**kw)
