@@ -232,7 +232,7 @@ def run_ours(args, cfg):
         if world == 1:
             _, tree = T.factor(A, b, s, R=R, tree=tree, stage_timing=True)
         else:
-            st = tdist.factor(A, b, s, engine=engine, tree=tree)   # workspace reused across steps
+            st = tdist.factor(A, b, s, engine=engine, tree=tree, cross=args.cross)   # workspace reused
             tree = st.tree
         ev_f.record(stream)
         if cfg["op"] == "form_q":
@@ -304,7 +304,7 @@ def run_ours(args, cfg):
             _, tree = T.factor(A, b, s, R=R, tree=tree)
             Rr = R
         else:
-            st = tdist.factor(A, b, s, engine=engine, tree=tree)
+            st = tdist.factor(A, b, s, engine=engine, tree=tree, cross=args.cross)
             tree, Rr = st.tree, st.R
         if cfg["op"] == "form_q":
             T.form_q(tree, Q)                            # no communication (butterfly replication)
@@ -358,7 +358,7 @@ def run_ours(args, cfg):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.config, "desc": cfg["desc"], "m": m, "n": n, "block_rows": b,
                    "tile_rows": info["tile_rows"], "ntiles_per_rank": info["ntiles"], "tree_depth": info["depth"],
-                   "cross_rounds": info["cross_rounds"], "second_op": cfg["op"], "k": k,
+                   "cross_rounds": info["cross_rounds"], "cross": args.cross if world > 1 else None, "second_op": cfg["op"], "k": k,
                    "l2": "inputs larger than L2 (A = %.0f MB > 126 MB), pristine A restored before each step"
                          % (8e-6 * m * n),
                    "value_timing": "CUDA events around tsqr_factor (leaf kernel + tree kernel) per step, mean of K, "
@@ -390,6 +390,8 @@ def main():
     ap.add_argument("--config", default=None)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cross", default="butterfly", choices=["butterfly", "allgather"],
+                    help="N > 1: the cross-GPU R-combine as log2 N pairwise rounds or one all-gather")
     args = ap.parse_args()
     if args.config is None:
         args.config = DEFAULT_CONFIG

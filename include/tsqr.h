@@ -141,6 +141,17 @@ tsqr_status_t tsqr_pack_r(tsqr_tree_t tree, double *packed, void *stream);
 tsqr_status_t tsqr_cross_factor(tsqr_tree_t tree, int32_t round, const double *partner_packed,
                                 double *R, int64_t ldr, void *stream);
 
+/* All rounds of the butterfly at once from an all-gather of the leaf R's (one
+ * collective instead of log2(nranks) exchanges; "any tree"
+ * P:928-932): all_packed (device, nranks * n(n+1)/2) holds every rank's
+ * tsqr_pack_r output, rank i at offset i*n(n+1)/2.  Each rank recomputes the
+ * sibling groups' R's it needs (nranks - 1 - log2(nranks) extra combines) with
+ * the same kernels, then runs its own rounds as tsqr_cross_factor would: the
+ * tree ends in the same state and R is bitwise the butterfly's.  Only on a tree
+ * with no round done yet.  R (device, may be NULL) receives the final R. */
+tsqr_status_t tsqr_cross_factor_gathered(tsqr_tree_t tree, const double *all_packed, double *R,
+                                         int64_t ldr, void *stream);
+
 /* C <- Q^T C over the local tree ([TR] P:1915-1938; eq. localQTupdate
  * P:2193-2212).  C (device, m_local x k, ldc >= m_local) is overwritten in
  * "tree order": rows 0..n-1 of the slab hold the R coordinates (for nranks = 1,

@@ -17,7 +17,7 @@ MAX_N = 256
 
 # every symbol include/tsqr.h declares
 SYMBOLS = ["tsqr_status_string", "tsqr_last_error", "tsqr_slab", "tsqr_plan_info", "tsqr_plan_export",
-           "tsqr_cross_partner", "tsqr_factor", "tsqr_pack_r", "tsqr_cross_factor", "tsqr_apply_qt",
+           "tsqr_cross_partner", "tsqr_factor", "tsqr_pack_r", "tsqr_cross_factor", "tsqr_cross_factor_gathered", "tsqr_apply_qt",
            "tsqr_cross_apply_qt", "tsqr_apply_q", "tsqr_cross_apply_q", "tsqr_form_q", "tsqr_tree_free", "tsqr_tree_export_tau",
            "tsqr_tree_stage_ms", "tsqr_caqr_factor", "tsqr_caqr_apply_qt", "tsqr_caqr_apply_q",
            "tsqr_caqr_form_q", "tsqr_caqr_free"]
@@ -70,6 +70,7 @@ def lib():
         "tsqr_factor": [_i64, _i64, _vp, _i64, _vp, _i64, ctypes.POINTER(Opts), _vp, ctypes.POINTER(_vp)],
         "tsqr_pack_r": [_vp, _vp, _vp],
         "tsqr_cross_factor": [_vp, _i32, _vp, _vp, _i64, _vp],
+        "tsqr_cross_factor_gathered": [_vp, _vp, _vp, _i64, _vp],
         "tsqr_apply_qt": [_vp, _vp, _i64, _i64, _vp, _i64, _vp],
         "tsqr_cross_apply_qt": [_vp, _i32, _vp, _i64, _vp, _vp, _i64, _i64, _vp],
         "tsqr_apply_q": [_vp, _vp, _i64, _i64, _vp],

@@ -140,6 +140,16 @@ def cross_factor(tree: Tree, rnd: int, partner_packed: torch.Tensor, R: torch.Te
     return R
 
 
+def cross_factor_gathered(tree: Tree, all_packed: torch.Tensor, R: torch.Tensor | None = None, stream=None):
+    """Every butterfly round from the all-gathered packed leaf R's (rank i at i*n(n+1)/2)."""
+    pr, ldr = None, 0
+    if R is not None:
+        pr, _, _, ldr = _colmajor(R, "R")
+    check(lib().tsqr_cross_factor_gathered(tree.handle, all_packed.data_ptr(), pr, ldr, _stream_ptr(stream)),
+          "tsqr_cross_factor_gathered")
+    return R
+
+
 def cross_apply_qt(tree: Tree, rnd: int, top: torch.Tensor, partner_top: torch.Tensor, C: torch.Tensor,
                    stream=None):
     ptop, _, k, ldtop = _colmajor(top, "top")

@@ -47,6 +47,7 @@ struct tsqr_tree_s {
     int npan = 0;
     double *d_tcache_node = nullptr, *d_cross_tcache = nullptr, *d_wtmp = nullptr;
     double *d_tcache_pair = nullptr;   // wide leaves: T01 of each pair of panels (tiles <= 1024 rows)
+    double *d_gather = nullptr;        // all-gathered cross variant: n x n scratch + G packed group R's
     int64_t wtmp_size = 0;
     std::vector<int> step_off;   // top-down: groups [step_off[g], step_off[g+1])
 };
@@ -72,7 +73,7 @@ static void free_tree_memory(tsqr_tree_s *t) {
                     t->d_tau_node, t->d_cross_y1, t->d_cross_tau, t->d_xbuf,
                     t->d_step_ids, t->d_pipe_nodes, t->d_prod_l, t->d_prod_r, t->d_pipe_flags,
                     t->d_tile_chunk0, t->d_cta_tile0, t->d_apply_cta_tile0, t->d_tau_chunk, t->d_tcache,
-                    t->d_tcache_node, t->d_cross_tcache, t->d_wtmp, t->d_tcache_pair};
+                    t->d_tcache_node, t->d_cross_tcache, t->d_wtmp, t->d_tcache_pair, t->d_gather};
     for (void *p : ptrs)
         if (p) cudaFree(p);
 }
@@ -426,6 +427,73 @@ tsqr_status_t tsqr_cross_factor(tsqr_tree_t t, int32_t round, const double *part
     t->cross_done = round;
     t->stream = (cudaStream_t)stream;
     return debug_sync(t, t->stream, "tsqr_cross_factor");
+}
+
+// Packed R of rank group g at butterfly level r (ranks g*2^r .. (g+1)*2^r - 1) from the
+// all-gathered leaf R's, by the same structured-combine kernels as the butterfly rounds
+// (so bitwise the R the group's ranks hold after round r).  Slot: heap index (G >> r) + g.
+static tsqr_status_t gathered_group_r(tsqr_tree_s *t, const double *all, int r, int g, const double **out,
+                                      cudaStream_t st) {
+    const int n = (int)t->plan.n, G = t->opts.nranks;
+    const int64_t np = (int64_t)n * (n + 1) / 2;
+    if (r == 0) {
+        *out = all + (int64_t)g * np;
+        return TSQR_OK;
+    }
+    const double *lo = nullptr, *hi = nullptr;
+    tsqr_status_t s = gathered_group_r(t, all, r - 1, 2 * g, &lo, st);
+    if (s == TSQR_OK) s = gathered_group_r(t, all, r - 1, 2 * g + 1, &hi, st);
+    if (s != TSQR_OK) return s;
+    double *scr = t->d_gather, *dst = t->d_gather + (int64_t)n * n + (int64_t)((G >> r) + g) * np;
+    const int jr = t->cross_rounds;                 // the spare round slot takes the node factors
+    CUDA_TRY(launch_unpack_r(lo, n, scr, n, st), "tsqr_cross_factor_gathered");
+    if (t->wide) {
+        CUDA_TRY(launch_wide_cross_factor(scr, n, n, hi, 1, t->d_wtmp, t->d_cross_y1 + (int64_t)jr * n * n,
+                                          t->d_cross_tau + (int64_t)jr * n,
+                                          t->d_cross_tcache + (int64_t)jr * t->npan * 64, nullptr, 0, st),
+                 "tsqr_cross_factor_gathered");
+    } else {
+        CUDA_TRY(launch_cross_factor(t->NP, scr, n, n, hi, 1, t->d_cross_y1 + (int64_t)jr * n * n,
+                                     t->d_cross_tau + (int64_t)jr * n, nullptr, 0, st),
+                 "tsqr_cross_factor_gathered");
+    }
+    CUDA_TRY(launch_pack_r(scr, n, n, dst, st), "tsqr_cross_factor_gathered");
+    *out = dst;
+    return TSQR_OK;
+}
+
+tsqr_status_t tsqr_cross_factor_gathered(tsqr_tree_t t, const double *all_packed, double *R, int64_t ldr,
+                                         void *stream) {
+    if (!t || !t->A || !all_packed) return TSQR_ERR_INVALID;
+    if (t->cross_done != 0) return TSQR_ERR_INVALID;
+    if (R && ldr < t->plan.n) return TSQR_ERR_INVALID;
+    const int n = (int)t->plan.n, G = t->opts.nranks;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (t->cross_rounds == 0) {
+        if (R) CUDA_TRY(launch_extract_r(t->A, t->lda, n, R, ldr, st), "tsqr_cross_factor_gathered");
+        return debug_sync(t, st, "tsqr_cross_factor_gathered");
+    }
+    if (!t->d_gather) {
+        const size_t words = (size_t)n * n + (size_t)G * n * (n + 1) / 2;
+        if (cudaMalloc((void **)&t->d_gather, sizeof(double) * words) != cudaSuccess) {
+            cudaGetLastError();
+            t->d_gather = nullptr;
+            return TSQR_ERR_ALLOC;
+        }
+    }
+    if (t->wide) {
+        tsqr_status_t ws = wide_tmp(t, n);
+        if (ws != TSQR_OK) return ws;
+    }
+    for (int r = 1; r <= t->cross_rounds; ++r) {
+        // this rank's node of round r: its own R (the tree's current R) and the sibling group's
+        const int sib = (t->opts.rank >> (r - 1)) ^ 1;
+        const double *sp = nullptr;
+        tsqr_status_t s = gathered_group_r(t, all_packed, r - 1, sib, &sp, st);
+        if (s == TSQR_OK) s = tsqr_cross_factor(t, r, sp, r == t->cross_rounds ? R : nullptr, ldr, stream);
+        if (s != TSQR_OK) return s;
+    }
+    return TSQR_OK;
 }
 
 tsqr_status_t tsqr_apply_qt(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, double *top, int64_t ldtop,

@@ -81,6 +81,7 @@ cudaError_t launch_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *
                                   double *tau_node, double *tcache_node, cudaStream_t st);
 cudaError_t launch_identity(double *X, int n, cudaStream_t st);
 cudaError_t launch_pack_r(const double *A, int64_t lda, int n, double *packed, cudaStream_t st);
+cudaError_t launch_unpack_r(const double *packed, int n, double *A, int64_t lda, cudaStream_t st);
 cudaError_t launch_copy_block(const double *src, int64_t lds, double *dst, int64_t ldd, int n, int k,
                               cudaStream_t st);
 cudaError_t launch_cross_factor(int NP, double *A, int64_t lda, int n, const double *pp, int is_lower,

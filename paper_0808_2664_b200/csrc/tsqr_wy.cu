@@ -278,6 +278,13 @@ __global__ void k_pack_r(const double *A, int64_t lda, int n, double *packed) {
     }
 }
 
+__global__ void k_unpack_r(const double *packed, int n, double *A, int64_t lda) {
+    for (int e = threadIdx.x + blockIdx.x * blockDim.x; e < n * n; e += blockDim.x * gridDim.x) {
+        const int r = e % n, c = e / n;
+        A[r + (int64_t)c * lda] = r <= c ? packed[(int64_t)c * (c + 1) / 2 + r] : 0.0;
+    }
+}
+
 __global__ void k_copy_block(const double *src, int64_t lds, double *dst, int64_t ldd, int n, int k) {
     for (int64_t e = threadIdx.x + (int64_t)blockIdx.x * blockDim.x; e < (int64_t)n * k;
          e += (int64_t)blockDim.x * gridDim.x) {
@@ -414,6 +421,11 @@ cudaError_t launch_identity(double *X, int n, cudaStream_t st) {
 
 cudaError_t launch_pack_r(const double *A, int64_t lda, int n, double *packed, cudaStream_t st) {
     k_pack_r<<<(n * n + 255) / 256, 256, 0, st>>>(A, lda, n, packed);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_unpack_r(const double *packed, int n, double *A, int64_t lda, cudaStream_t st) {
+    k_unpack_r<<<(n * n + 255) / 256, 256, 0, st>>>(packed, n, A, lda);
     return cudaGetLastError();
 }
 

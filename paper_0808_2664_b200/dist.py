@@ -45,6 +45,9 @@ class CudaEngine:
     def cross_factor(self, tree, rnd, recv, R):
         api.cross_factor(tree, rnd, recv, R)
 
+    def cross_factor_gathered(self, tree, all_packed, R):
+        api.cross_factor_gathered(tree, all_packed, R)
+
     def apply_local(self, tree, C, top):
         api.apply_qt(tree, C, top)
 
@@ -106,6 +109,10 @@ class RankState:
     def factor_finish(self, rnd, recv):
         self.engine.cross_factor(self.tree, rnd, recv, self.R)
 
+    def factor_gathered_finish(self, all_packed):
+        # every round from the all-gathered leaf R's (the factor_send(0) of every rank)
+        self.engine.cross_factor_gathered(self.tree, all_packed, self.R)
+
     # ----------------------------------------------------------------- apply
     def apply_local(self, C):
         k = C.shape[0]
@@ -150,14 +157,37 @@ def _exchange(send: torch.Tensor, partner: int, group=None) -> torch.Tensor:
     return recv
 
 
+def _all_gather(send: torch.Tensor, group=None) -> torch.Tensor:
+    import torch.distributed as dist
+    if send.is_cuda and dist.get_backend(group) == "gloo":
+        return _all_gather(send.cpu(), group).to(send.device)
+    G = dist.get_world_size(group)
+    if dist.get_backend(group) == "nccl":
+        out = torch.empty((G * send.numel(),), dtype=send.dtype, device=send.device)
+        dist.all_gather_into_tensor(out, send, group=group)
+        return out
+    parts = [torch.empty_like(send) for _ in range(G)]
+    dist.all_gather(parts, send, group=group)
+    return torch.cat(parts)
+
+
 # ------------------------------------------------------ torch.distributed drivers
-def factor(A_local, block_rows: int, tile_rows: int = 0, engine=None, group=None, tree=None) -> RankState:
+def factor(A_local, block_rows: int, tile_rows: int = 0, engine=None, group=None, tree=None,
+           cross: str = "butterfly") -> RankState:
     """Collective over the process group: returns the rank state (R replicated in .R).
-    tree: a previous factor's tree of the same shape, whose workspace is reused."""
+    tree: a previous factor's tree of the same shape, whose workspace is reused.
+    cross: "butterfly" (log2 G pairwise exchanges) or "allgather" (one all-gather of the
+    packed leaf R's, the rounds recomputed locally; bitwise the same R and tree state)."""
     import torch.distributed as dist
     rank, nranks = dist.get_rank(group), dist.get_world_size(group)
     st = RankState(engine or CudaEngine(), rank, nranks)
     st.factor_local(A_local, block_rows, tile_rows, tree)
+    if cross == "allgather":
+        if nranks > 1:
+            st.factor_gathered_finish(_all_gather(st.factor_send(0), group))
+        return st
+    if cross != "butterfly":
+        raise ValueError("cross must be 'butterfly' or 'allgather'")
     for rnd in range(1, rounds_of(nranks) + 1):
         partner = rank ^ (1 << (rnd - 1))
         recv = _exchange(st.factor_send(rnd), partner, group)
@@ -193,7 +223,7 @@ def form_q(st: RankState):
 
 
 # ------------------------------------------------------- loopback (virtual) drivers
-def factor_virtual(slabs, block_rows: int, tile_rows: int = 0, engine=None) -> list:
+def factor_virtual(slabs, block_rows: int, tile_rows: int = 0, engine=None, cross: str = "butterfly") -> list:
     """All ranks in one process, exchanging by reference between rounds (no kernel of one
     rank ever waits on another's: each round's sends are complete before any finish)."""
     nranks = len(slabs)
@@ -201,6 +231,12 @@ def factor_virtual(slabs, block_rows: int, tile_rows: int = 0, engine=None) -> l
     states = [RankState(eng, r, nranks) for r in range(nranks)]
     for st, A in zip(states, slabs):
         st.factor_local(A, block_rows, tile_rows)
+    if cross == "allgather":
+        if nranks > 1:
+            all_packed = torch.cat([st.factor_send(0) for st in states])
+            for st in states:
+                st.factor_gathered_finish(all_packed)
+        return states
     for rnd in range(1, rounds_of(nranks) + 1):
         sends = [st.factor_send(rnd) for st in states]
         for st in states:

@@ -75,6 +75,27 @@ class OracleEngine:
         t.R = Rn
         R.numpy()[:] = Rn.T
 
+    def cross_factor_gathered(self, t, all_packed, R):
+        n, G = t.n, t.nranks
+        npk = n * (n + 1) // 2
+        packs = all_packed.numpy().reshape(G, npk)
+
+        def unpack(pk):
+            P = np.zeros((n, n))
+            for c in range(n):
+                P[:c + 1, c] = pk[c * (c + 1) // 2:(c + 1) * (c + 2) // 2]
+            return P
+
+        def group(r, g):                      # R of ranks g*2^r .. (g+1)*2^r - 1
+            if r == 0:
+                return unpack(packs[g])
+            return orc.combine(group(r - 1, 2 * g), group(r - 1, 2 * g + 1))[0]
+
+        for rnd in range(1, int(np.log2(G)) + 1):
+            P = group(rnd - 1, (t.rank >> (rnd - 1)) ^ 1)
+            pk = torch.from_numpy(np.concatenate([P[:c + 1, c] for c in range(n)]))
+            self.cross_factor(t, rnd, pk, R)
+
     def apply_local(self, t, C, top):
         out = orc.tsqr_apply_qt(t.f, _np(C))
         C.numpy()[:] = out.T
@@ -137,7 +158,7 @@ def _free_port():
         return sck.getsockname()[1]
 
 
-def _worker(rank, world, port, m, n, b, s, k, q):
+def _worker(rank, world, port, m, n, b, s, k, q, cross="butterfly"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -146,7 +167,7 @@ def _worker(rank, world, port, m, n, b, s, k, q):
         row0, ml = api.slab(m, n, b, world, rank)
         A = inputs.gaussian_rows(row0, ml, n, 0)
         C = inputs.gaussian_rows(row0, ml, k, 1)
-        st = tdist.factor(A, b, s, engine=OracleEngine())
+        st = tdist.factor(A, b, s, engine=OracleEngine(), cross=cross)
         C0 = C.clone()
         tdist.apply_qt(st, C)
         QtC = C.clone()
@@ -161,13 +182,15 @@ def _worker(rank, world, port, m, n, b, s, k, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,m,n,b,s,k", [(2, 3000, 12, 500, 250, 7), (4, 5000, 8, 300, 100, 5),
-                                             (2, 2 * 4096 + 37, 16, 4096, 512, 3)])
-def test_butterfly_gloo(world, m, n, b, s, k):
+@pytest.mark.parametrize("world,m,n,b,s,k,cross", [(2, 3000, 12, 500, 250, 7, "butterfly"),
+                                                   (4, 5000, 8, 300, 100, 5, "butterfly"),
+                                                   (2, 2 * 4096 + 37, 16, 4096, 512, 3, "butterfly"),
+                                                   (4, 5000, 8, 300, 100, 5, "allgather")])
+def test_butterfly_gloo(world, m, n, b, s, k, cross):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, m, n, b, s, k, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, m, n, b, s, k, q, cross)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]
@@ -186,6 +209,10 @@ def test_butterfly_gloo(world, m, n, b, s, k):
         # apply Q: a rank exchanges only in the rounds where it is a group head
         heads = [r for r in range(1, rounds + 1) if tdist.head_role(rank, r)]
         assert sorted(-r for r, _ in sent if r < 0) == sorted(2 * heads)
+        if cross == "allgather":                                    # one all-gather of the packed R
+            assert [w for r_, w in sent if r_ == 0] == [n * (n + 1) // 2]
+            assert [w for r_, w in sent if r_ > 0] == [n * k] * rounds
+            continue
         sent = [x for x in sent if x[0] > 0]
         # counts (Table 1; Cor. 2): log2 G messages of n(n+1)/2 words
         fac = [w for r_, w in sent if True][:rounds]
@@ -215,6 +242,30 @@ def test_butterfly_virtual_oracle(G, m, n, b, s, k):
     for (r0, ml), C, C0, Z in zip(rows, cs, c0, zs):
         assert orc.rel_fro(_np(C), _np(C0)) <= 1e-13
         assert orc.rel_fro(_np(Z), QZ_ref[r0:r0 + ml]) <= 1e-13
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("G,m,n,b,s", [(8, 50000, 16, 2048, 128), (4, 40000, 50, 4096, 192), (2, 12000, 200, 2048, 2048),
+                                       (8, 8 * 4096 + 100, 64, 4096, 96), (4, 16000, 100, 2048, 2048)])
+def test_allgather_cross_equals_butterfly_cuda(G, m, n, b, s):
+    """The all-gather variant of the cross-GPU combine leaves every rank's tree in the butterfly's
+    state: R, Q^T C and Q bitwise equal."""
+    from paper_0808_2664_b200 import api
+    rows = [api.slab(m, n, b, G, r) for r in range(G)]
+    out = {}
+    for cross in ("butterfly", "allgather"):
+        slabs = [inputs.gaussian_rows(r0, ml, n, 0).cuda() for r0, ml in rows]
+        cs = [inputs.gaussian_rows(r0, ml, 7, 1).cuda() for r0, ml in rows]
+        states = tdist.factor_virtual(slabs, b, s, cross=cross)
+        tdist.apply_qt_virtual(states, cs)
+        Qs = [tdist.form_q(st) for st in states]
+        torch.cuda.synchronize()
+        out[cross] = ([st.R.clone() for st in states], cs, Qs)
+        for st in states:
+            st.tree.free()
+    for x, y in zip(out["butterfly"], out["allgather"]):
+        for a_, b_ in zip(x, y):
+            assert torch.equal(a_, b_)
 
 
 @pytest.mark.gpu

@@ -10,3 +10,6 @@ done
 timeout -s KILL 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv python bench.py --config c2 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/launch_c2.csv 2>&1
 timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:k_chain_factor -c 1 -o gpurun_out/chain_factor_c2 python tools/prof_one.py c2 form_q 1 > gpurun_out/ncu_c2.log 2>&1
 timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:k_wide_leaves -c 1 -o gpurun_out/wide_leaves_c3 python tools/prof_one.py c3 factor 1 > gpurun_out/ncu_c3.log 2>&1
+[ -n "$NCU_C4" ] && timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:k_chain_factor -c 1 -o gpurun_out/chain_factor_c4 python tools/prof_one.py c4 factor 1 > gpurun_out/ncu_c4.log 2>&1
+[ -n "$CUSOLVER" ] && PYTHONPATH=$PWD timeout -s KILL 300 python tools/caqr_time.py 1000000 50 64 4096 1024 > gpurun_out/cusolver_c2.txt 2>&1
+exit 0
