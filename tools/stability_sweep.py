@@ -44,13 +44,12 @@ for e in range(0, 16, 2):
     R = torch.empty((n, n), dtype=torch.float64, device="cuda")
     Q = torch.empty((n, m), dtype=torch.float64, device="cuda")
     W = A.clone()
-    tree = None
+    hold = {"tree": None}
 
     def tsqr():
-        nonlocal tree
         W.copy_(A)
-        _, tree = T.factor(W, b, s, R=R, tree=tree)
-        T.form_q(tree, Q)
+        _, hold["tree"] = T.factor(W, b, s, R=R, tree=hold["tree"])
+        T.form_q(hold["tree"], Q)
         return Q
 
     t_ts, _ = timed(tsqr)
@@ -81,4 +80,4 @@ for e in range(0, 16, 2):
     t_c2, (Q2, R2) = timed(chol2)
     c2 = "   breakdown" if Q2 is None else f"  {metrics(A, Q2, R2)[0]:9.2e} {t_c2:7.3f}"
     print(f"{kappa:8.0e} | {o_ts:9.2e} {r_ts:9.2e} {t_ts:7.3f} |{cq} |{c2}")
-    tree.free()
+    hold["tree"].free()
