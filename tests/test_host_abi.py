@@ -130,3 +130,31 @@ def test_apply_validation_without_gpu():
     assert L.tsqr_form_q(None, None, 0, None) == 1
     assert L.tsqr_cross_factor(None, 1, None, None, 0, None) == 1
     assert L.tsqr_tree_free(None) == 0
+    assert L.tsqr_apply_q(None, None, 0, 0, None) == 1
+    assert L.tsqr_cross_apply_q(None, 1, None, 0, None, None, 0, 0, None) == 1
+    assert L.tsqr_cross_factor_gathered(None, None, None, 0, None) == 1
+
+
+def test_caqr_validation_without_gpu():
+    L = _lib.lib()
+    fake = ctypes.c_void_p(0x1000)
+    h = ctypes.c_void_p(None)
+    o = T.api.opts(block_rows=256, tile_rows=128)
+
+    def st(m, N, A, lda, panel, R, ldr, opts=o):
+        return L.tsqr_caqr_factor(m, N, A, lda, panel, R, ldr, ctypes.byref(opts), None, ctypes.byref(h))
+
+    assert st(100, 200, fake, 100, 32, fake, 200) == 2                  # m < N
+    assert st(1000, 0, fake, 1000, 32, fake, 1) == 2                    # N < 1
+    assert st(1000, 100, None, 1000, 32, fake, 100) == 1                # null A
+    assert st(1000, 100, fake, 1000, 32, None, 100) == 1                # null R
+    assert st(1000, 100, fake, 999, 32, fake, 100) == 1                 # lda < m
+    assert st(1000, 100, fake, 1000, 32, fake, 99) == 1                 # ldr < N
+    assert st(1000, 100, fake, 1000, 0, fake, 100) == 1                 # panel < 1
+    assert st(1000, 100, fake, 1000, 257, fake, 100) == 3               # panel > TSQR_MAX_N
+    assert st(1000, 100, fake, 1000, 32, fake, 100, T.api.opts(block_rows=256, nranks=2)) == 3
+    assert h.value is None                                              # nothing created
+    assert L.tsqr_caqr_apply_qt(None, None, 0, 0, None) == 1
+    assert L.tsqr_caqr_apply_q(None, None, 0, 0, None) == 1
+    assert L.tsqr_caqr_form_q(None, None, 0, None) == 1
+    assert L.tsqr_caqr_free(None) == 0
