@@ -245,6 +245,34 @@ def node_y1(f: Factor, k: int) -> np.ndarray:
     return f.Y1[k].reshape(n, n, order="F")
 
 
+# -------------------------------------------------- sequential (streamed) TSQR
+def slab_ranges(m: int, n: int, slab_rows: int):
+    """Row slabs of the streamed TSQR: slab_rows each from row 0; a remainder of fewer than n
+    rows is merged into the last slab (the row-block rule of reading R6 at slab granularity)."""
+    full, rem = divmod(m, slab_rows)
+    if full == 0:
+        return [(0, m)]
+    out = [(k * slab_rows, slab_rows) for k in range(full)]
+    if rem >= n:
+        out.append((full * slab_rows, rem))
+    elif rem:
+        out[-1] = (out[-1][0], slab_rows + rem)
+    return out
+
+
+def sequential_tsqr_r(A, slab_rows: int, b: int, s: int | None = None, c: int = 0) -> np.ndarray:
+    """R of A by sequential TSQR over row slabs (flat tree; [TR] Alg. sequential TSQR
+    P:1725-1753, flat tree P:954-993): each slab's R by the (parallel) TSQR of its rows with
+    the plan (b, s, c), then R <- structured QR of [R; R_slab] (Alg. QR:qnxn with q = 2)."""
+    F = np.asarray(A, dtype=np.float64)
+    m, n = F.shape
+    R = None
+    for r0, rows in slab_ranges(m, n, slab_rows):
+        f = tsqr_factor(np.array(F[r0:r0 + rows], order="F"), plan(rows, n, b, s, 1, c))
+        R = f.R if R is None else combine(R, f.R)[0]
+    return R
+
+
 # ------------------------------------------------------------------- CAQR
 @dataclass
 class CaqrFactor:

@@ -469,3 +469,25 @@ def test_caqr_single_panel_is_tsqr():
     f = orc.tsqr_factor(A.copy(order="F"), orc.plan(900, 24, 300, 100, 1, 0))
     assert np.array_equal(cf.R, f.R)
     assert np.array_equal(orc.caqr_form_q(cf), orc.tsqr_form_q(f))
+
+
+# ------------------------------------------------------ sequential (streamed) TSQR
+def test_slab_ranges():
+    assert orc.slab_ranges(1000, 10, 300) == [(0, 300), (300, 300), (600, 300), (900, 100)]
+    assert orc.slab_ranges(905, 10, 300) == [(0, 300), (300, 300), (600, 305)]
+    assert orc.slab_ranges(200, 10, 300) == [(0, 200)]
+
+
+@pytest.mark.parametrize("m,n,slab,b,s,c", [(3000, 20, 700, 350, 175, 0), (2500, 40, 1000, 500, 250, 16),
+                                             (1200, 100, 500, 500, 500, 0)])
+def test_sequential_tsqr_pins(m, n, slab, b, s, c):
+    """Flat tree over slabs pinned to LAPACK's R (unique up to signs, full rank) and to
+    R^T R = A^T A; one slab is exactly the parallel TSQR (bitwise)."""
+    A = np.asfortranarray(np.random.default_rng(6).standard_normal((m, n)))
+    R = orc.sequential_tsqr_r(A, slab, b, s, c)
+    assert np.all(np.tril(R, -1) == 0.0)
+    Rl = scipy.linalg.qr(A, mode="r")[0][:n]
+    assert orc.rel_fro(orc.sign_normalise(R), orc.sign_normalise(Rl)) <= 1e-12
+    assert np.linalg.norm(R.T @ R - A.T @ A) / np.linalg.norm(A) ** 2 <= 1e-14
+    one = orc.sequential_tsqr_r(A, m, b, s, c)
+    assert np.array_equal(one, orc.tsqr_factor(A.copy(order="F"), orc.plan(m, n, b, s, 1, c)).R)
