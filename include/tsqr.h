@@ -199,6 +199,23 @@ tsqr_status_t tsqr_cross_apply_q(tsqr_tree_t tree, int32_t round, double *top, i
  * cross-rank node factors are replicated on every rank. */
 tsqr_status_t tsqr_form_q(tsqr_tree_t tree, double *Q, int64_t ldq, void *stream);
 
+/* Sequential (out-of-HBM) TSQR: R of a HOST-resident m x n matrix streamed
+ * through the GPU in row slabs -- a flat tree over the slabs ([TR] Alg.
+ * sequential TSQR P:1725-1753; flat tree P:954-993; model Eq. 6).
+ * Slab k (rows k*slab_rows .., a remainder of fewer than n rows joins the last
+ * slab) is copied to the device (cudaMemcpy2DAsync on an internal copy stream,
+ * overlapping the previous slab's factorization; page-locked A makes the copy
+ * asynchronous), factored by tsqr_factor with opts (nranks must be 0 or 1), and
+ * the running R absorbs it by the structured combine of [R; R_slab] (Alg.
+ * QR:qnxn, q = 2).  A (host, lda >= m) is read only.  Y (host, ldy >= m, may be
+ * NULL) receives every factored slab (its tiles' reflectors below their
+ * diagonals, as tsqr_factor leaves A).  R (device, n x n, ldr >= n) receives R,
+ * exact zeros below.  Device memory: two slabs plus O(n^2).  Synchronous: returns
+ * after `stream` has completed the factorization. */
+tsqr_status_t tsqr_factor_streamed(int64_t m, int64_t n, const double *A, int64_t lda, int64_t slab_rows,
+                                   double *Y, int64_t ldy, double *R, int64_t ldr,
+                                   const tsqr_opts_t *opts, void *stream);
+
 /* ---------------------------------------------------------------- CAQR
  * Right-looking QR of an m x N matrix (N may exceed TSQR_MAX_N) with TSQR
  * panels: "CAQR simply implements the right-looking QR factorization using ...

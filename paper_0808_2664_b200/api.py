@@ -21,10 +21,12 @@ def _stream_ptr(stream=None) -> int:
     return s.cuda_stream
 
 
-def _colmajor(t: torch.Tensor, name: str):
+def _colmajor(t: torch.Tensor, name: str, host: bool = False):
     if t.dtype != torch.float64:
         raise TypeError(f"{name} must be float64")
-    if not t.is_cuda:
+    if host and t.is_cuda:
+        raise TypeError(f"{name} must be a host (CPU) tensor")
+    if not host and not t.is_cuda:
         raise TypeError(f"{name} must be a CUDA tensor (the product path has no CPU fallback)")
     if t.dim() != 2 or (t.shape[1] > 1 and t.stride(1) != 1):
         raise ValueError(f"{name} must be column-major: shape (ncols, nrows) with stride(1) == 1")
@@ -168,6 +170,24 @@ def cross_apply_q(tree: Tree, rnd: int, top: torch.Tensor, partner_top: torch.Te
     check(lib().tsqr_cross_apply_q(tree.handle, rnd, ptop, ldtop, partner_top.data_ptr(), pc, ldc, k,
                                    _stream_ptr(stream)), "tsqr_cross_apply_q")
     return top
+
+
+def factor_streamed(A_host: torch.Tensor, slab_rows: int, block_rows: int = 0, tile_rows: int = 0,
+                    R: torch.Tensor | None = None, Y_host: torch.Tensor | None = None, device=None,
+                    stream=None) -> torch.Tensor:
+    """R of a host-resident A (CPU tensor, column-major m x n; pin it for overlapped copies)
+    streamed through the GPU in slabs of slab_rows (sequential TSQR).  Returns R on the device."""
+    pa, m, n, lda = _colmajor(A_host, "A", host=True)
+    if R is None:
+        R = torch.empty((n, n), dtype=torch.float64, device=device or "cuda")
+    pr, _, _, ldr = _colmajor(R, "R")
+    py, ldy = None, 0
+    if Y_host is not None:
+        py, _, _, ldy = _colmajor(Y_host, "Y", host=True)
+    o = opts(block_rows, tile_rows)
+    check(lib().tsqr_factor_streamed(m, n, pa, lda, slab_rows, py, ldy, pr, ldr, ctypes.byref(o),
+                                     _stream_ptr(stream)), "tsqr_factor_streamed")
+    return R
 
 
 # ------------------------------------------------------------------- CAQR
