@@ -131,6 +131,14 @@ __device__ __forceinline__ House house_bf(double alpha, double s2) {
     return h;
 }
 
+// 16 < n <= 32 (variants: -DTSQR_KM32=<row blocks> -DTSQR_NW32=<warps>, plan.cpp TSQR_C32 = 8 KM)
+#ifndef TSQR_KM32
+#define TSQR_KM32 8
+#endif
+#ifndef TSQR_NW32
+#define TSQR_NW32 8
+#endif
+#define TSQR_CFG32 4, TSQR_KM32, TSQR_NW32
 template <int NCB_, int KM_, int NW_, int NBUF_ = 2>
 struct Cfg {
     // NBUF: R buffers; with 2 the tiles of a CTA alternate and the next tile's head

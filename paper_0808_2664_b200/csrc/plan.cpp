@@ -22,8 +22,11 @@ int64_t default_tile_rows(int64_t n) { return n > 64 ? 2048 : 32 * (int64_t)chun
 // as tall as the register file and the staging buffers allow at 8 warps/SM:
 // KM = 8 (64 rows) for n <= 32, 6 (48) for n <= 48, 5 (40) for n <= 64 (for
 // 56 < n <= 64 with a single R buffer, tsqr_chain.cu)
+#ifndef TSQR_C32
+#define TSQR_C32 64
+#endif
 int chunk_rows_for(int64_t n) {
-    return n <= 32 ? 64 : (n <= 48 ? 48 : (n <= 64 ? 40 : 0));   // 0: one chunk per tile
+    return n <= 16 ? 64 : (n <= 32 ? TSQR_C32 : (n <= 48 ? 48 : (n <= 64 ? 40 : 0)));   // 0: one chunk per tile
 }
 
 static int64_t block_count(int64_t m, int64_t n, int64_t b, int64_t *last_rows) {

@@ -152,7 +152,7 @@ static cudaError_t chain_dispatch(int n, F &&fn) {
     const int ncb = (n + 7) / 8;
     switch (ncb) {
         case 1: case 2: return fn(Cfg<2, 8, 8>());
-        case 3: case 4: return fn(Cfg<4, 8, 8>());
+        case 3: case 4: return fn(Cfg<TSQR_CFG32>());
         case 5: case 6: return fn(Cfg<6, 6, 8>());
         case 7: return fn(Cfg<7, 5, 8>());
         default: return fn(Cfg<8, 5, 8, 1>());          // one R buffer: room for 40-row chunks

@@ -270,7 +270,7 @@ static cudaError_t chain_cfg_dispatch(int n, F &&fn) {
     const int ncb = (n + 7) / 8;
     switch (ncb) {
         case 1: case 2: return fn(chunk::Cfg<2, 8, 8>());
-        case 3: case 4: return fn(chunk::Cfg<4, 8, 8>());
+        case 3: case 4: return fn(chunk::Cfg<TSQR_CFG32>());
         case 5: case 6: return fn(chunk::Cfg<6, 6, 8>());
         case 7: return fn(chunk::Cfg<7, 5, 8>());
         default: return fn(chunk::Cfg<8, 5, 8, 1>());
