@@ -1003,7 +1003,10 @@ static size_t apply_leaf_smem(int max_rows, int slots) {
 template <int KM>
 static cudaError_t launch_leaves_km(double *A, int64_t lda, int n, const int64_t *row0, const int *rows, int L,
                                    int max_rows, double *tau, double *tcache, double *tpair, cudaStream_t st) {
-    const size_t bytes = LeafSmem<KM>::bytes(max_rows);
+    size_t bytes = LeafSmem<KM>::bytes(max_rows);
+#ifdef TSQR_WIDE_MIN_SMEM
+    if (bytes < TSQR_WIDE_MIN_SMEM) bytes = TSQR_WIDE_MIN_SMEM;     // variant: cap resident CTAs per SM
+#endif
     cudaError_t e = cudaFuncSetAttribute((const void *)k_wide_leaves<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)bytes);
     if (e != cudaSuccess) return e;
