@@ -112,6 +112,27 @@ def combine(Ra, Rb):
     return np.triu(a), np.triu(b), tau, fl.value
 
 
+def combine_q(Rs):
+    """Alg. QR:qnxn ([TR] P:1957-1979): structured Householder QR of q stacked n x n upper
+    triangles [R_1; ...; R_q], column by column: I_j = {j} U {rows 0..j of R_2} U ... U
+    {rows 0..j of R_q}; w = A(I_j, j); [tau_j, v] = House(w) (v(1) = 1); A(I_j, j+1:n) :=
+    (I - tau_j v v^T) A(I_j, j+1:n); v(2:end) scattered back into A(I_j \ {j}, j).
+    Returns (R, [Y_2, ..., Y_q] (upper triangles holding the v parts), tau); (2/3)(q-1)n^3 flops."""
+    q = len(Rs)
+    n = Rs[0].shape[0]
+    A = np.vstack([np.triu(np.asarray(R, dtype=np.float64)) for R in Rs])
+    tau = np.zeros(n)
+    for j in range(n):
+        I = [j] + [i * n + r for i in range(1, q) for r in range(j + 1)]
+        v, t, beta = house(A[I, j])
+        X = A[np.ix_(I, range(j + 1, n))]
+        A[np.ix_(I, range(j + 1, n))] = X - t * np.outer(v, v @ X)
+        A[I[1:], j] = v[1:]
+        A[j, j] = beta
+        tau[j] = t
+    return np.triu(A[:n]), [np.triu(A[i * n:(i + 1) * n]) for i in range(1, q)], tau
+
+
 def build_t(Y, tau):
     """T (k x k) with H_0...H_{k-1} = I - Y T Y^T, Y unit lower trapezoidal."""
     Y = _fortran(Y)

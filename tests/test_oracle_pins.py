@@ -491,3 +491,32 @@ def test_sequential_tsqr_pins(m, n, slab, b, s, c):
     assert np.linalg.norm(R.T @ R - A.T @ A) / np.linalg.norm(A) ** 2 <= 1e-14
     one = orc.sequential_tsqr_r(A, m, b, s, c)
     assert np.array_equal(one, orc.tsqr_factor(A.copy(order="F"), orc.plan(m, n, b, s, 1, c)).R)
+
+
+# ------------------------------------------------------------- q-ary combine
+def _q_from_combine(Ys, tau, n):
+    """Explicit Q (qn x n) of Alg. QR:qnxn: the reflectors applied to [I_n; 0] in reverse."""
+    q = len(Ys) + 1
+    Q = np.zeros((q * n, n))
+    Q[:n] = np.eye(n)
+    for j in range(n - 1, -1, -1):
+        I = [j] + [i * n + r for i in range(1, q) for r in range(j + 1)]
+        v = np.concatenate([[1.0]] + [Ys[i - 1][:j + 1, j] for i in range(1, q)])
+        Q[I] -= tau[j] * np.outer(v, v @ Q[I])
+    return Q
+
+
+@pytest.mark.parametrize("q,n", [(2, 5), (3, 8), (4, 17), (8, 33), (5, 64)])
+def test_combine_q_pins(q, n):
+    rng = np.random.default_rng(q * 100 + n)
+    Rs = [np.triu(rng.standard_normal((n, n))) for _ in range(q)]
+    R, Ys, tau = orc.combine_q(Rs)
+    S = np.vstack(Rs)
+    Rl = scipy.linalg.qr(S, mode="r")[0][:n]
+    assert orc.rel_fro(orc.sign_normalise(R), orc.sign_normalise(Rl)) <= 1e-13
+    Q = _q_from_combine(Ys, tau, n)
+    assert np.linalg.norm(Q @ R - S) / np.linalg.norm(S) <= 1e-14
+    assert np.linalg.norm(Q.T @ Q - np.eye(n)) <= 1e-13
+    if q == 2:                                            # the binary combine (C oracle)
+        Rb, Y1, tb, _ = orc.combine(Rs[0], Rs[1])
+        assert orc.rel_fro(R, Rb) <= 1e-14 and orc.rel_fro(Ys[0], Y1) <= 1e-14 and orc.rel_fro(tau, tb) <= 1e-14
