@@ -116,7 +116,7 @@ def combine_q(Rs):
     """Alg. QR:qnxn ([TR] P:1957-1979): structured Householder QR of q stacked n x n upper
     triangles [R_1; ...; R_q], column by column: I_j = {j} U {rows 0..j of R_2} U ... U
     {rows 0..j of R_q}; w = A(I_j, j); [tau_j, v] = House(w) (v(1) = 1); A(I_j, j+1:n) :=
-    (I - tau_j v v^T) A(I_j, j+1:n); v(2:end) scattered back into A(I_j \ {j}, j).
+    (I - tau_j v v^T) A(I_j, j+1:n); v(2:end) scattered back into A(I_j minus {j}, j).
     Returns (R, [Y_2, ..., Y_q] (upper triangles holding the v parts), tau); (2/3)(q-1)n^3 flops."""
     q = len(Rs)
     n = Rs[0].shape[0]
