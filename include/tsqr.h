@@ -216,6 +216,15 @@ tsqr_status_t tsqr_factor_streamed(int64_t m, int64_t n, const double *A, int64_
                                    double *Y, int64_t ldy, double *R, int64_t ldr,
                                    const tsqr_opts_t *opts, void *stream);
 
+/* q-ary structured combine, Alg. QR:qnxn ([TR] P:1957-1979): the QR of q stacked
+ * n x n upper triangles [R_1; ...; R_q], reflector j acting on {row j of R_1} U
+ * {rows 0..j of R_2..R_q} ((2/3)(q-1)n^3 flops; q = 2 is the tree's
+ * binary node).  packed (device, q * n(n+1)/2 words, triangle i at offset
+ * i*n(n+1)/2, each packed column by column as tsqr_pack_r): IN R_1..R_q, OUT R in
+ * slot 0 and the reflectors' v parts Y_2..Y_q (upper triangles, v(1) = 1
+ * implicit) in slots 1..q-1.  tau (device, n): OUT.  One CTA; asynchronous. */
+tsqr_status_t tsqr_combine_stacked(int32_t q, int64_t n, double *packed, double *tau, void *stream);
+
 /* ---------------------------------------------------------------- CAQR
  * Right-looking QR of an m x N matrix (N may exceed TSQR_MAX_N) with TSQR
  * panels: "CAQR simply implements the right-looking QR factorization using ...

@@ -8,7 +8,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtsqr.so")
-SOURCES = ["tsqr_api.cu", "tsqr_wy.cu", "tsqr_chain.cu", "tsqr_cs.cu", "tsqr_wide.cu", "tsqr_tree.cu", "tsqr_caqr.cu", "tsqr_stream.cu", "plan.cpp"]
+SOURCES = ["tsqr_api.cu", "tsqr_wy.cu", "tsqr_chain.cu", "tsqr_cs.cu", "tsqr_wide.cu", "tsqr_tree.cu", "tsqr_caqr.cu", "tsqr_stream.cu", "tsqr_combine.cu", "plan.cpp"]
 HEADERS = ["wy.cuh", "chunk.cuh", "tsqr_kernels.h", "plan.h", os.path.join("..", "..", "include", "tsqr.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -20,7 +20,7 @@ SYMBOLS = ["tsqr_status_string", "tsqr_last_error", "tsqr_slab", "tsqr_plan_info
            "tsqr_cross_partner", "tsqr_factor", "tsqr_pack_r", "tsqr_cross_factor", "tsqr_cross_factor_gathered", "tsqr_apply_qt",
            "tsqr_cross_apply_qt", "tsqr_apply_q", "tsqr_cross_apply_q", "tsqr_form_q", "tsqr_tree_free", "tsqr_tree_export_tau",
            "tsqr_tree_stage_ms", "tsqr_caqr_factor", "tsqr_caqr_apply_qt", "tsqr_caqr_apply_q",
-           "tsqr_caqr_form_q", "tsqr_caqr_free", "tsqr_factor_streamed"]
+           "tsqr_caqr_form_q", "tsqr_caqr_free", "tsqr_factor_streamed", "tsqr_combine_stacked"]
 
 
 class TsqrError(RuntimeError):
@@ -84,6 +84,7 @@ def lib():
         "tsqr_caqr_apply_q": [_vp, _vp, _i64, _i64, _vp],
         "tsqr_caqr_form_q": [_vp, _vp, _i64, _vp],
         "tsqr_caqr_free": [_vp],
+        "tsqr_combine_stacked": [_i32, _i64, _vp, _vp, _vp],
         "tsqr_factor_streamed": [_i64, _i64, _vp, _i64, _i64, _vp, _i64, _vp, _i64, ctypes.POINTER(Opts), _vp],
     }
     for name, args in sig.items():

@@ -190,6 +190,18 @@ def factor_streamed(A_host: torch.Tensor, slab_rows: int, block_rows: int = 0, t
     return R
 
 
+def combine_stacked(packed: torch.Tensor, q: int, n: int, tau: torch.Tensor | None = None, stream=None):
+    """Alg. QR:qnxn on q packed triangles (device, q*n(n+1)/2, in place): slot 0 becomes R,
+    slots 1.. the reflectors' v parts.  Returns tau (n)."""
+    if not packed.is_cuda or packed.dtype != torch.float64 or packed.numel() != q * n * (n + 1) // 2:
+        raise ValueError("packed must be a CUDA float64 tensor of q*n(n+1)/2 words")
+    if tau is None:
+        tau = torch.empty(n, dtype=torch.float64, device=packed.device)
+    check(lib().tsqr_combine_stacked(q, n, packed.data_ptr(), tau.data_ptr(), _stream_ptr(stream)),
+          "tsqr_combine_stacked")
+    return tau
+
+
 # ------------------------------------------------------------------- CAQR
 class Caqr:
     """Right-looking CAQR with TSQR panels (tsqr_caqr_*): one panel tree per panel_cols
