@@ -52,6 +52,10 @@ struct tsqr_tree_s {
     std::vector<int> step_off;   // top-down: groups [step_off[g], step_off[g+1])
 };
 
+void tsqr::set_last_error(const char *where, cudaError_t e) {
+    g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+}
+
 static tsqr_status_t cuda_fail(cudaError_t e, const char *where) {
     g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
     return TSQR_ERR_CUDA;

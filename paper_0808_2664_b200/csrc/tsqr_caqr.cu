@@ -6,6 +6,7 @@
 // small fill kernels; every panel factor and trailing update runs in the TSQR
 // kernels.
 #include "../../include/tsqr.h"
+#include "tsqr_kernels.h"
 
 #include <cuda_runtime.h>
 
@@ -91,7 +92,11 @@ tsqr_status_t tsqr_caqr_factor(int64_t m, int64_t N, double *A, int64_t lda, int
             // zero block below the diagonal block, then line 3 (+ the tree stages): Q_j^T on the
             // trailing columns; rows 0..w-1 of the result are R's row block
             k_caqr_zero_below<<<grid_for((N - c0 - w) * w), 256, 0, st>>>(R, ldr, N, c0, w);
-            if (cudaGetLastError() != cudaSuccess) s = TSQR_ERR_CUDA;
+            const cudaError_t e = cudaGetLastError();
+            if (e != cudaSuccess) {
+                tsqr::set_last_error("tsqr_caqr_factor", e);
+                s = TSQR_ERR_CUDA;
+            }
             if (s == TSQR_OK)
                 s = tsqr_apply_qt(c->trees[j], A + c0 + (c0 + w) * lda, lda, N - c0 - w, R + c0 + (c0 + w) * ldr,
                                   ldr, stream);
@@ -138,7 +143,11 @@ tsqr_status_t tsqr_caqr_form_q(tsqr_caqr_t c, double *Q, int64_t ldq, void *stre
     if (!c || !c->A || !Q || ldq < c->m) return TSQR_ERR_INVALID;
     cudaStream_t st = (cudaStream_t)stream;
     k_caqr_eye<<<grid_for(c->m * c->N), 256, 0, st>>>(Q, ldq, c->m, c->N);
-    if (cudaGetLastError() != cudaSuccess) return TSQR_ERR_CUDA;
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        tsqr::set_last_error("tsqr_caqr_form_q", e);
+        return TSQR_ERR_CUDA;
+    }
     // Q = Q_1 ... Q_p [I_N; 0]: Q_j acts on rows c0_j.. where only columns >= c0_j are nonzero
     for (size_t j = c->trees.size(); j-- > 0;) {
         const int64_t c0 = (int64_t)j * c->panel;

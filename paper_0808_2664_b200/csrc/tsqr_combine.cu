@@ -7,6 +7,7 @@
 // butterfly), one CTA, the triangles staged in shared memory when they fit.
 // Product code.
 #include "../../include/tsqr.h"
+#include "tsqr_kernels.h"
 
 #include <cuda_runtime.h>
 
@@ -108,11 +109,16 @@ extern "C" tsqr_status_t tsqr_combine_stacked(int32_t q, int64_t n, double *pack
     const size_t bytes = sizeof(double) * (size_t)q * (size_t)(n * (n + 1) / 2);
     const int staged = bytes <= 200 * 1024;
     cudaStream_t st = (cudaStream_t)stream;
-    if (staged && cudaFuncSetAttribute((const void *)k_combine_q, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)bytes) != cudaSuccess) {
-        cudaGetLastError();
+    cudaError_t e = staged ? cudaFuncSetAttribute((const void *)k_combine_q,
+                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes)
+                           : cudaSuccess;
+    if (e == cudaSuccess) {
+        k_combine_q<<<1, CT, staged ? bytes : 0, st>>>(packed, q, (int)n, tau, staged);
+        e = cudaGetLastError();
+    }
+    if (e != cudaSuccess) {
+        tsqr::set_last_error("tsqr_combine_stacked", e);
         return TSQR_ERR_CUDA;
     }
-    k_combine_q<<<1, CT, staged ? bytes : 0, st>>>(packed, q, (int)n, tau, staged);
-    return cudaGetLastError() == cudaSuccess ? TSQR_OK : TSQR_ERR_CUDA;
+    return TSQR_OK;
 }

@@ -8,12 +8,13 @@
 
 namespace tsqr {
 
-
+// The text tsqr_last_error() returns (tsqr_api.cu); for the C-ABI entry points in other files.
+void set_last_error(const char *where, cudaError_t e);
 
 // Leaf stage on the chunk engine (tsqr_chain.cu).
 struct ChainArgs {
     double *A; int64_t lda; int n;
-    int chunk_rows;              // 32 or 64 (chain_chunk_rows(n))
+    int chunk_rows;              // the plan's c (chain_chunk_rows(n))
     const int64_t *tile_row0; const int *tile_rows; const int64_t *tile_chunk0;
     const int *cta_tile0; int grid;
     double *tau;                 // [chunks][n]

@@ -63,6 +63,7 @@ struct Res {
         cudaError_t _e = (expr);                             \
         if (_e != cudaSuccess) {                             \
             cudaGetLastError();                              \
+            set_last_error("tsqr_factor_streamed", _e);      \
             return _e == cudaErrorMemoryAllocation ? TSQR_ERR_ALLOC : TSQR_ERR_CUDA; \
         }                                                    \
     } while (0)
