@@ -208,23 +208,57 @@ int chain_grid(int n) {
     return sms * occ;
 }
 
-// Balanced split of the tiles over `grid` CTAs by chunk count (contiguous runs).
+// Split of the tiles over `grid` CTAs in contiguous runs that minimises the
+// largest run's chunk count (the kernel ends with its busiest CTA): binary
+// search on the capacity, runs filled greedily.
 void chain_partition(const std::vector<int64_t> &tile_rows, int chunk_rows, int grid, std::vector<int> &cta_tile0) {
     const int L = (int)tile_rows.size();
+    std::vector<int64_t> w(L);
+    int64_t lo = 0, hi = 0;
+    for (int t = 0; t < L; ++t) {
+        w[t] = (tile_rows[t] + chunk_rows - 1) / chunk_rows;
+        lo = std::max(lo, w[t]);
+        hi += w[t];
+    }
+    auto runs = [&](int64_t cap) {
+        int k = 0;
+        int64_t acc = 0;
+        for (int t = 0; t < L; ++t) {
+            if (k == 0 || acc + w[t] > cap) { ++k; acc = 0; }
+            acc += w[t];
+        }
+        return k;
+    };
+#ifdef TSQR_PARTITION_NEAREST
+    // variant: cuts at the tile nearest to each equal-share target
     std::vector<int64_t> pre(L + 1, 0);
-    for (int t = 0; t < L; ++t) pre[t + 1] = pre[t] + (tile_rows[t] + chunk_rows - 1) / chunk_rows;
+    for (int t = 0; t < L; ++t) pre[t + 1] = pre[t] + w[t];
     cta_tile0.assign(grid + 1, L);
     cta_tile0[0] = 0;
     int t = 0;
     for (int i = 1; i < grid; ++i) {
         const int64_t target = (pre[L] * i + grid - 1) / grid;
         while (t < L && pre[t] < target) ++t;
-        // choose the closer cut of t-1 / t
         if (t > 0 && t < L && (target - pre[t - 1]) < (pre[t] - target)) --t;
         t = std::max(t, cta_tile0[i - 1]);
         cta_tile0[i] = t;
     }
     cta_tile0[grid] = L;
+    return;
+#endif
+    while (lo < hi) {
+        const int64_t mid = lo + (hi - lo) / 2;
+        if (runs(mid) <= grid) hi = mid;
+        else lo = mid + 1;
+    }
+    cta_tile0.assign(grid + 1, L);
+    cta_tile0[0] = 0;
+    int k = 0;
+    int64_t acc = 0;
+    for (int t = 0; t < L; ++t) {
+        if (t > 0 && acc + w[t] > lo) { cta_tile0[++k] = t; acc = 0; }
+        acc += w[t];
+    }
 }
 
 }  // namespace tsqr
