@@ -5,6 +5,8 @@
 #include "plan.h"
 #include "tsqr_kernels.h"
 
+#include <nvtx3/nvToolsExt.h>
+
 #include <algorithm>
 #include <cstring>
 #include <new>
@@ -14,6 +16,15 @@
 using namespace tsqr;
 
 static thread_local std::string g_last_error;
+
+// NVTX range over a device entry point (named in nsys / ncu --nvtx timelines; a no-op
+// without a tool attached)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 struct tsqr_tree_s {
     Plan plan;
@@ -315,6 +326,7 @@ static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t 
 
 tsqr_status_t tsqr_factor(int64_t m_local, int64_t n, double *A, int64_t lda, double *R, int64_t ldr,
                           const tsqr_opts_t *opts, void *stream, tsqr_tree_t *tree) {
+    NvtxRange nvtx_("tsqr_factor");
     if (!tree || !A) return TSQR_ERR_INVALID;
     if (n < 1 || m_local < n) return TSQR_ERR_SHAPE;
     if (lda < m_local) return TSQR_ERR_INVALID;
@@ -398,6 +410,7 @@ tsqr_status_t tsqr_factor(int64_t m_local, int64_t n, double *A, int64_t lda, do
 }
 
 tsqr_status_t tsqr_pack_r(tsqr_tree_t t, double *packed, void *stream) {
+    NvtxRange nvtx_("tsqr_pack_r");
     if (!t || !t->A || !packed) return TSQR_ERR_INVALID;
     CUDA_TRY(launch_pack_r(t->A, t->lda, (int)t->plan.n, packed, (cudaStream_t)stream), "tsqr_pack_r");
     t->stream = (cudaStream_t)stream;
@@ -406,6 +419,7 @@ tsqr_status_t tsqr_pack_r(tsqr_tree_t t, double *packed, void *stream) {
 
 tsqr_status_t tsqr_cross_factor(tsqr_tree_t t, int32_t round, const double *partner_packed, double *R,
                                 int64_t ldr, void *stream) {
+    NvtxRange nvtx_("tsqr_cross_factor");
     if (!t || !t->A || !partner_packed) return TSQR_ERR_INVALID;
     if (round != t->cross_done + 1 || round > t->cross_rounds) return TSQR_ERR_INVALID;
     if (R && ldr < t->plan.n) return TSQR_ERR_INVALID;
@@ -468,6 +482,7 @@ static tsqr_status_t gathered_group_r(tsqr_tree_s *t, const double *all, int r, 
 
 tsqr_status_t tsqr_cross_factor_gathered(tsqr_tree_t t, const double *all_packed, double *R, int64_t ldr,
                                          void *stream) {
+    NvtxRange nvtx_("tsqr_cross_factor_gathered");
     if (!t || !t->A || !all_packed) return TSQR_ERR_INVALID;
     if (t->cross_done != 0) return TSQR_ERR_INVALID;
     if (R && ldr < t->plan.n) return TSQR_ERR_INVALID;
@@ -502,6 +517,7 @@ tsqr_status_t tsqr_cross_factor_gathered(tsqr_tree_t t, const double *all_packed
 
 tsqr_status_t tsqr_apply_qt(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, double *top, int64_t ldtop,
                             void *stream) {
+    NvtxRange nvtx_("tsqr_apply_qt");
     if (!t || !t->A) return TSQR_ERR_INVALID;
     if (k < 0 || k > INT32_MAX) return TSQR_ERR_INVALID;
     if (k == 0) return TSQR_OK;
@@ -544,6 +560,7 @@ tsqr_status_t tsqr_apply_qt(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, do
 
 tsqr_status_t tsqr_cross_apply_qt(tsqr_tree_t t, int32_t round, double *top, int64_t ldtop,
                                   const double *partner_top, double *C, int64_t ldc, int64_t k, void *stream) {
+    NvtxRange nvtx_("tsqr_cross_apply_qt");
     if (!t || !t->A || !top || !partner_top) return TSQR_ERR_INVALID;
     if (round < 1 || round > t->cross_done) return TSQR_ERR_INVALID;
     if (k < 0 || k > INT32_MAX || ldtop < t->plan.n) return TSQR_ERR_INVALID;
@@ -573,6 +590,7 @@ tsqr_status_t tsqr_cross_apply_qt(tsqr_tree_t t, int32_t round, double *top, int
 
 tsqr_status_t tsqr_cross_apply_q(tsqr_tree_t t, int32_t round, double *top, int64_t ldtop,
                                  const double *partner_top, double *C, int64_t ldc, int64_t k, void *stream) {
+    NvtxRange nvtx_("tsqr_cross_apply_q");
     if (!t || !t->A || !top || !partner_top) return TSQR_ERR_INVALID;
     if (round < 1 || round > t->cross_done) return TSQR_ERR_INVALID;
     if (k < 0 || k > INT32_MAX || ldtop < t->plan.n) return TSQR_ERR_INVALID;
@@ -602,6 +620,7 @@ tsqr_status_t tsqr_cross_apply_q(tsqr_tree_t t, int32_t round, double *top, int6
 }
 
 tsqr_status_t tsqr_apply_q(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, void *stream) {
+    NvtxRange nvtx_("tsqr_apply_q");
     if (!t || !t->A) return TSQR_ERR_INVALID;
     if (k < 0 || k > INT32_MAX) return TSQR_ERR_INVALID;
     if (k == 0) return TSQR_OK;
@@ -632,6 +651,7 @@ tsqr_status_t tsqr_apply_q(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, voi
 }
 
 tsqr_status_t tsqr_form_q(tsqr_tree_t t, double *Q, int64_t ldq, void *stream) {
+    NvtxRange nvtx_("tsqr_form_q");
     if (!t || !t->A || !Q) return TSQR_ERR_INVALID;
     if (ldq < t->plan.m_local) return TSQR_ERR_INVALID;
     if (t->cross_done != t->cross_rounds) return TSQR_ERR_INVALID;
