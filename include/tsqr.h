@@ -30,7 +30,9 @@ typedef enum {
     TSQR_ERR_UNSUPPORTED = 3,  /* n > TSQR_MAX_N, tile_rows above the kernel capacity,
                                   nranks not a power of two                             */
     TSQR_ERR_ALLOC = 4,        /* device or host allocation failed                      */
-    TSQR_ERR_CUDA = 5          /* a CUDA runtime error (message: tsqr_last_error())     */
+    TSQR_ERR_CUDA = 5,         /* a CUDA runtime error (message: tsqr_last_error())     */
+    TSQR_ERR_NCCL = 6          /* an NCCL error or a failed exchange of a butterfly
+                                  round (message: tsqr_last_error())                    */
 } tsqr_status_t;
 
 #define TSQR_MAX_N 256         /* widest n the kernels support: n <= 64 on the
@@ -277,6 +279,96 @@ tsqr_status_t tsqr_tree_export_tau(tsqr_tree_t tree, double *tau_tile_host, doub
  * recorded on the factor's stream when opts.flags bit 1 was set (else
  * TSQR_ERR_INVALID).  Either pointer may be NULL.  Waits for the last event. */
 tsqr_status_t tsqr_tree_stage_ms(tsqr_tree_t tree, float *leaf_ms, float *tree_ms);
+
+/* ---------------------------------------------------------------- communicator
+ * Row-sharded multi-GPU TSQR as ONE collective call per operation:
+ * Alg. TSQR:par ([TR] P:1667-1707) with the butterfly indexing of [TR]
+ * each rank factors its slab (tsqr_factor), then log2(nranks)
+ * rounds, each one grouped ncclSend/ncclRecv of the packed R (n(n+1)/2 words,
+ * the Cor. 2 minimum) with partner rank XOR 2^(k-1) on the caller's
+ * stream followed by the structured combine; R ends replicated.
+ * Everything is enqueued on `stream` (no host synchronisation), so the calls
+ * can be captured in a CUDA graph.  One context per process (= per GPU).
+ * Every ctx call on a context with nranks > 1 is COLLECTIVE over its ranks, with
+ * the same n, k and plan options on every rank; m_local, A, C and Q are the
+ * rank's slab (tsqr_slab); R and top are replicated.  SURVEY 8(b) writes
+ * tsqr_factor(ctx, ...): that is tsqr_ctx_factor below; tsqr_factor without a
+ * context is its local (one-rank) layer. */
+typedef struct tsqr_ctx_s *tsqr_ctx_t;
+
+/* A context on CUDA device `device` (nranks = 1 until a communicator is set). */
+tsqr_status_t tsqr_ctx_create(int device, tsqr_ctx_t *out);
+
+/* ncclGetUniqueId into uid128 (host, 128 bytes): rank 0 calls it and hands the
+ * bytes to every rank (any host channel, e.g. torch.distributed). */
+tsqr_status_t tsqr_get_unique_id(void *uid128);
+
+/* ncclCommInitRank(nranks, uid, rank) on the context's device (collective and
+ * blocking across the ranks).  nranks must be a power of two (the butterfly;
+ * TSQR_ERR_UNSUPPORTED otherwise).  Replaces an earlier communicator. */
+tsqr_status_t tsqr_ctx_set_comm(tsqr_ctx_t ctx, const void *uid128, int32_t nranks, int32_t rank);
+
+/* Test transport: the ranks of one process exchange through a host mailbox
+ * (each side synchronises its stream, then copies its partner's message) instead
+ * of NCCL -- kernels of one rank never wait on another's.  hub from
+ * tsqr_loopback_create(nranks); ctx takes rank `rank` of it. */
+typedef struct tsqr_loopback_s *tsqr_loopback_t;
+tsqr_status_t tsqr_loopback_create(int32_t nranks, tsqr_loopback_t *out);
+tsqr_status_t tsqr_loopback_destroy(tsqr_loopback_t hub);
+tsqr_status_t tsqr_ctx_set_loopback(tsqr_ctx_t ctx, tsqr_loopback_t hub, int32_t rank);
+
+/* Ranks and rank of the context. */
+tsqr_status_t tsqr_ctx_info(tsqr_ctx_t ctx, int32_t *nranks, int32_t *rank);
+
+/* Release the communicator and the context's exchange buffers. */
+tsqr_status_t tsqr_ctx_destroy(tsqr_ctx_t ctx);
+
+/* Collective factor: tsqr_factor of this rank's slab (opts' nranks and rank are
+ * taken from the context), then every butterfly round inside the call.  R (device,
+ * n x n, ldr >= n, may be NULL) receives the replicated R.  *tree as tsqr_factor. */
+tsqr_status_t tsqr_ctx_factor(tsqr_ctx_t ctx, int64_t m_local, int64_t n, double *A, int64_t lda,
+                              double *R, int64_t ldr, const tsqr_opts_t *opts, void *stream,
+                              tsqr_tree_t *tree);
+
+/* Collective C <- Q^T C: the local tree (tsqr_apply_qt), then per round one
+ * exchange of the n x k R coordinates (n k words, Table 1) and the
+ * round's node reflectors on [top_lower; top_upper] (eq. localQTupdate
+ * P:2193-2212).  C (device, m_local x k, ldc) ends in tree order (rank 0's rows
+ * 0..n-1 = Q_thin^T C); top (device, n x k, ldtop >= n, may be NULL) receives the
+ * replicated Q_thin^T C on every rank. */
+tsqr_status_t tsqr_ctx_apply_qt(tsqr_ctx_t ctx, tsqr_tree_t tree, double *C, int64_t ldc, int64_t k,
+                                double *top, int64_t ldtop, void *stream);
+
+/* Collective C <- Q C (C in tree order), the inverse of tsqr_ctx_apply_qt: the
+ * rounds top-down between the two group heads of each round, then the local tree. */
+tsqr_status_t tsqr_ctx_apply_q(tsqr_ctx_t ctx, tsqr_tree_t tree, double *C, int64_t ldc, int64_t k, void *stream);
+
+/* Explicit thin Q rows of this rank: no communication (the butterfly replicates
+ * every cross-rank node factor, [TR] P:1919-1925); = tsqr_form_q. */
+tsqr_status_t tsqr_ctx_form_q(tsqr_ctx_t ctx, tsqr_tree_t tree, double *Q, int64_t ldq, void *stream);
+
+/* ---------------------------------------------------------------- host
+ * End-to-end QR with HOST buffers on one GPU (the e2e path of bench.py): A (host,
+ * m x n, lda >= m) is copied to the device, factored (tsqr_factor with opts;
+ * nranks must be 0 or 1), R (host, n x n, ldr >= n) receives R (zeros below);
+ * if Q (host, ldq >= m) is non-NULL it receives the explicit thin Q (tsqr_form_q);
+ * if k > 0, C (host, m x k, ldc >= m) is replaced by Q^T C in tree order
+ * (tsqr_apply_qt).  Every copy and kernel is enqueued on `stream`; page-locked
+ * host buffers make the copies asynchronous DMA.  Returns after the outputs
+ * have landed in host memory (synchronises `stream`).  *ws: device workspace
+ * and tree, created on first use (pass a NULL-initialised handle) and reused
+ * while (m, n) match; release with tsqr_host_ws_free. */
+typedef struct tsqr_host_ws_s *tsqr_host_ws_t;
+tsqr_status_t tsqr_qr_host(tsqr_host_ws_t *ws, int64_t m, int64_t n, const double *A, int64_t lda,
+                           double *R, int64_t ldr, double *Q, int64_t ldq, double *C, int64_t ldc,
+                           int64_t k, const tsqr_opts_t *opts, void *stream);
+tsqr_status_t tsqr_host_ws_free(tsqr_host_ws_t ws);
+
+/* ---------------------------------------------------------------- measurement
+ * FP64 pipe peak of the current device (TFLOP/s, best of 3): DMMA.8x8x4 chains and
+ * DFMA chains on every SM (the roofline denominator of SURVEY 8(d)).  Synchronises
+ * `stream`.  Not on the TSQR path. */
+tsqr_status_t tsqr_measure_fp64_peak(double *dmma_tflops, double *dfma_tflops, void *stream);
 
 #ifdef __cplusplus
 }

@@ -29,7 +29,7 @@ def build(force: bool = False) -> str:
     newest = max(os.path.getmtime(_SRC), os.path.getmtime(_HDR))
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < newest:
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.run(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"], check=True)
+        subprocess.run(["gcc", *CFLAGS, "-pthread", "-o", tmp, _SRC, "-lm"], check=True)
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -223,16 +223,23 @@ def _plan_args(p: Plan):
             _i64(p.nnodes), _i(p.node_a), _i(p.node_b))
 
 
-def tsqr_factor(A, p: Plan) -> Factor:
-    F = _fortran(A)
+def tsqr_factor(A, p: Plan, threads: int = 1, overwrite: bool = False, keep_y1: bool = True) -> Factor:
+    """TSQR over the plan p.  threads > 1 runs the leaf QRs (Eq. 1, independent per
+    leaf) on that many host threads (orc_tsqr_factor_mt, bitwise the same result);
+    overwrite=True factors A itself (a Fortran-ordered float64 array) instead of a
+    copy, keep_y1=False skips the node factors (nnodes x n^2 words) -- both for
+    full-size checks whose matrices are GBs."""
+    F = A if (overwrite and isinstance(A, np.ndarray) and A.dtype == np.float64 and A.flags.f_contiguous) \
+        else _fortran(A)
     m, n = F.shape
     assert m == p.m and n == p.n
     tau_tile = np.zeros((int(p.tile_chunk0[-1]), n))
-    Y1 = np.zeros((max(p.nnodes, 1), n * n))
+    Y1 = np.zeros((max(p.nnodes, 1), n * n)) if keep_y1 else None
     tau_node = np.zeros((max(p.nnodes, 1), n))
     R = np.zeros((n, n), order="F")
-    lib().orc_tsqr_factor(_i64(m), _i64(n), _d(F), _i64(_ld(F)), _i64(p.c), *_plan_args(p),
-                          _d(tau_tile), _d(Y1), _d(tau_node), _d(R), _i64(n))
+    lib().orc_tsqr_factor_mt(_i64(m), _i64(n), _d(F), _i64(_ld(F)), _i64(p.c), *_plan_args(p),
+                             _d(tau_tile), _d(Y1) if keep_y1 else None, _d(tau_node), _d(R), _i64(n),
+                             _i64(max(1, int(threads))))
     return Factor(p, F, tau_tile, Y1, tau_node, R)
 
 

@@ -7,6 +7,7 @@
  */
 #include "oracle.h"
 #include <math.h>
+#include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -340,33 +341,75 @@ int orc_plan_fill(int64_t m, int64_t n, int64_t b, int64_t s, int64_t G,
 
 /* Eqs. 1-4: every tile A_i = Q_i R_i, then stacked pairs of R's
  * are re-factored up the tree; the implicit Q is the tree of local factors. */
+/* Eq. 1 for tiles [t0, t1): the leaf QRs, independent of one another. */
+typedef struct {
+    int64_t n, lda, c, t0, t1;
+    double *A, *tau_tile, *Rsub;
+    const int64_t *tile_row0, *tile_rows, *chunk0;
+} leaf_job;
+
+static void *leaf_range(void *arg)
+{
+    const leaf_job *J = (const leaf_job *)arg;
+    const size_t nn = (size_t)(J->n * J->n);
+    for (int64_t t = J->t0; t < J->t1; ++t) {
+        double *At = J->A + J->tile_row0[t];
+        orc_chain_qr(J->tile_rows[t], J->n, At, J->lda, J->c, J->tau_tile + J->chunk0[t] * J->n);
+        for (int64_t j = 0; j < J->n; ++j)
+            for (int64_t i = 0; i <= j; ++i) AT(J->Rsub + t * nn, i, j, J->n) = AT(At, i, j, J->lda);
+    }
+    return NULL;
+}
+
+void orc_tsqr_factor_mt(int64_t m, int64_t n, double *A, int64_t lda, int64_t c,
+                        int64_t ntiles, const int64_t *tile_row0, const int64_t *tile_rows,
+                        int64_t nnodes, const int64_t *node_a, const int64_t *node_b,
+                        double *tau_tile, double *Y1, double *tau_node,
+                        double *R, int64_t ldr, int64_t nthreads)
+{
+    (void)m;
+    size_t nn = (size_t)(n * n);
+    double *Rsub = (double *)calloc((size_t)ntiles * nn, sizeof(double));
+    int64_t *chunk0 = (int64_t *)malloc(sizeof(int64_t) * (size_t)(ntiles + 1));
+    chunk0[0] = 0;
+    for (int64_t t = 0; t < ntiles; ++t) chunk0[t + 1] = chunk0[t] + chunks_of(tile_rows[t], c);
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > ntiles) nthreads = ntiles;
+    leaf_job *jobs = (leaf_job *)malloc(sizeof(leaf_job) * (size_t)nthreads);
+    pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)nthreads);
+    for (int64_t w = 0; w < nthreads; ++w) {                     /* Eq. 1: contiguous runs of leaves */
+        leaf_job J = {n, lda, c, ntiles * w / nthreads, ntiles * (w + 1) / nthreads,
+                      A, tau_tile, Rsub, tile_row0, tile_rows, chunk0};
+        jobs[w] = J;
+    }
+    for (int64_t w = 1; w < nthreads; ++w) pthread_create(&th[w], NULL, leaf_range, &jobs[w]);
+    leaf_range(&jobs[0]);
+    for (int64_t w = 1; w < nthreads; ++w) pthread_join(th[w], NULL);
+    for (int64_t k = 0; k < nnodes; ++k) {                       /* Eqs. 2-3, in plan order */
+        double *Ra = Rsub + node_a[k] * nn, *Rb = Rsub + node_b[k] * nn;
+        orc_combine(n, Ra, n, Rb, n, tau_node + k * n, NULL);
+        if (Y1) {
+            double *Yk = Y1 + k * nn;
+            for (int64_t j = 0; j < n; ++j)
+                for (int64_t i = 0; i < n; ++i) AT(Yk, i, j, n) = (i <= j) ? AT(Rb, i, j, n) : 0.0;
+        }
+    }
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i < n; ++i) AT(R, i, j, ldr) = (i <= j) ? AT(Rsub, i, j, n) : 0.0;
+    free(th);
+    free(jobs);
+    free(chunk0);
+    free(Rsub);
+}
+
 void orc_tsqr_factor(int64_t m, int64_t n, double *A, int64_t lda, int64_t c,
                      int64_t ntiles, const int64_t *tile_row0, const int64_t *tile_rows,
                      int64_t nnodes, const int64_t *node_a, const int64_t *node_b,
                      double *tau_tile, double *Y1, double *tau_node,
                      double *R, int64_t ldr)
 {
-    (void)m;
-    size_t nn = (size_t)(n * n);
-    double *Rsub = (double *)calloc((size_t)ntiles * nn, sizeof(double));
-    int64_t ch0 = 0;
-    for (int64_t t = 0; t < ntiles; ++t) {                       /* Eq. 1 */
-        double *At = A + tile_row0[t];
-        orc_chain_qr(tile_rows[t], n, At, lda, c, tau_tile + ch0 * n);
-        ch0 += chunks_of(tile_rows[t], c);
-        for (int64_t j = 0; j < n; ++j)
-            for (int64_t i = 0; i <= j; ++i) AT(Rsub + t * nn, i, j, n) = AT(At, i, j, lda);
-    }
-    for (int64_t k = 0; k < nnodes; ++k) {                       /* Eqs. 2-3 */
-        double *Ra = Rsub + node_a[k] * nn, *Rb = Rsub + node_b[k] * nn;
-        orc_combine(n, Ra, n, Rb, n, tau_node + k * n, NULL);
-        double *Yk = Y1 + k * nn;
-        for (int64_t j = 0; j < n; ++j)
-            for (int64_t i = 0; i < n; ++i) AT(Yk, i, j, n) = (i <= j) ? AT(Rb, i, j, n) : 0.0;
-    }
-    for (int64_t j = 0; j < n; ++j)
-        for (int64_t i = 0; i < n; ++i) AT(R, i, j, ldr) = (i <= j) ? AT(Rsub, i, j, n) : 0.0;
-    free(Rsub);
+    orc_tsqr_factor_mt(m, n, A, lda, c, ntiles, tile_row0, tile_rows, nnodes, node_a, node_b,
+                       tau_tile, Y1, tau_node, R, ldr, 1);
 }
 
 /* reflector j of a tile chunk (rows from chain_rows, vector tail stored in

@@ -127,6 +127,18 @@ void orc_tsqr_factor(int64_t m, int64_t n, double *A, int64_t lda, int64_t c,
                      double *tau_tile, double *Y1, double *tau_node,
                      double *R, int64_t ldr);
 
+/* The same factorization with the leaf QRs (Eq. 1, independent per leaf)
+ * spread over nthreads host threads (contiguous runs of tiles); the nodes run
+ * in plan order on the calling thread.  Bitwise equal to orc_tsqr_factor (each
+ * tile's arithmetic is unchanged; only which thread runs it differs).  Y1 may
+ * be NULL.  The only parallelism in the oracle ("parallel over
+ * leaves"), used to time it on all host cores and to check full-size configs. */
+void orc_tsqr_factor_mt(int64_t m, int64_t n, double *A, int64_t lda, int64_t c,
+                        int64_t ntiles, const int64_t *tile_row0, const int64_t *tile_rows,
+                        int64_t nnodes, const int64_t *node_a, const int64_t *node_b,
+                        double *tau_tile, double *Y1, double *tau_node,
+                        double *R, int64_t ldr, int64_t nthreads);
+
 /* C <- Q^T C in "tree order" (leaves first, then nodes in factor order;
  * reading R4): tile stage [TR] P:1915-1938, node stage eq. localQTupdate
  * applied reflector by reflector.  Global rows 0..n-1 end

@@ -8,11 +8,24 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libtsqr.so")
-SOURCES = ["tsqr_api.cu", "tsqr_wy.cu", "tsqr_chain.cu", "tsqr_cs.cu", "tsqr_wide.cu", "tsqr_tree.cu", "tsqr_caqr.cu", "tsqr_stream.cu", "tsqr_combine.cu", "plan.cpp"]
+SOURCES = ["tsqr_api.cu", "tsqr_wy.cu", "tsqr_chain.cu", "tsqr_cs.cu", "tsqr_wide.cu", "tsqr_tree.cu", "tsqr_caqr.cu",
+           "tsqr_stream.cu", "tsqr_combine.cu", "tsqr_comm.cu", "tsqr_peak.cu", "tsqr_host.cu", "plan.cpp"]
 HEADERS = ["wy.cuh", "chunk.cuh", "tsqr_kernels.h", "plan.h", os.path.join("..", "..", "include", "tsqr.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+
+
+def _nccl_dir() -> str:
+    """The NCCL that torch loads (nvidia-nccl-cu12 wheel, 2.28): the communicator layer
+    links the same libnccl.so.2, so one NCCL lives in the process."""
+    import nvidia.nccl
+    return list(nvidia.nccl.__path__)[0]
+
+
+NCCL = _nccl_dir()
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC,-O2", "-shared", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+         "-Xcompiler", "-fPIC,-O2", "-shared", "--expt-relaxed-constexpr", "-Xptxas", "-v",
+         "-I", os.path.join(NCCL, "include")]
+EXTRA = os.environ.get("TSQR_NVCC_EXTRA", "").split()       # developer A/B variants (-D...)
 
 
 def _newest_input() -> float:
@@ -25,7 +38,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
-    cflags = [f for f in FLAGS if f != "-shared"]
+    cflags = [f for f in FLAGS if f != "-shared"] + EXTRA
     procs, objs, log = [], [], ""
     for src in SOURCES:                       # one nvcc per translation unit, in parallel
         obj = os.path.join(objdir, src + f".{os.getpid()}.o")
@@ -39,7 +52,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         ok = ok and pr.returncode == 0
     tmp = LIB + f".tmp{os.getpid()}"
     if ok:
-        cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, "-lcudart"]
+        nlib = os.path.join(NCCL, "lib")
+        cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs, "-lcudart",
+               "-L", nlib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={nlib}"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         log += " ".join(cmd) + "\n" + res.stdout + res.stderr
         ok = res.returncode == 0

@@ -12,7 +12,7 @@ LIB_PATH = os.environ.get("TSQR_LIBRARY", os.path.join(HERE, "libtsqr.so"))
 
 TSQR_OK = 0
 STATUS = {0: "TSQR_OK", 1: "TSQR_ERR_INVALID", 2: "TSQR_ERR_SHAPE", 3: "TSQR_ERR_UNSUPPORTED",
-          4: "TSQR_ERR_ALLOC", 5: "TSQR_ERR_CUDA"}
+          4: "TSQR_ERR_ALLOC", 5: "TSQR_ERR_CUDA", 6: "TSQR_ERR_NCCL"}
 MAX_N = 256
 
 # every symbol include/tsqr.h declares
@@ -20,7 +20,11 @@ SYMBOLS = ["tsqr_status_string", "tsqr_last_error", "tsqr_slab", "tsqr_plan_info
            "tsqr_cross_partner", "tsqr_factor", "tsqr_pack_r", "tsqr_cross_factor", "tsqr_cross_factor_gathered", "tsqr_apply_qt",
            "tsqr_cross_apply_qt", "tsqr_apply_q", "tsqr_cross_apply_q", "tsqr_form_q", "tsqr_tree_free", "tsqr_tree_export_tau",
            "tsqr_tree_stage_ms", "tsqr_caqr_factor", "tsqr_caqr_apply_qt", "tsqr_caqr_apply_q",
-           "tsqr_caqr_form_q", "tsqr_caqr_free", "tsqr_factor_streamed", "tsqr_combine_stacked"]
+           "tsqr_caqr_form_q", "tsqr_caqr_free", "tsqr_factor_streamed", "tsqr_combine_stacked",
+           "tsqr_ctx_create", "tsqr_get_unique_id", "tsqr_ctx_set_comm", "tsqr_loopback_create",
+           "tsqr_loopback_destroy", "tsqr_ctx_set_loopback", "tsqr_ctx_info", "tsqr_ctx_destroy", "tsqr_ctx_factor",
+           "tsqr_ctx_apply_qt", "tsqr_ctx_apply_q", "tsqr_ctx_form_q", "tsqr_measure_fp64_peak",
+           "tsqr_qr_host", "tsqr_host_ws_free"]
 
 
 class TsqrError(RuntimeError):
@@ -86,6 +90,22 @@ def lib():
         "tsqr_caqr_free": [_vp],
         "tsqr_combine_stacked": [_i32, _i64, _vp, _vp, _vp],
         "tsqr_factor_streamed": [_i64, _i64, _vp, _i64, _i64, _vp, _i64, _vp, _i64, ctypes.POINTER(Opts), _vp],
+        "tsqr_ctx_create": [ctypes.c_int, ctypes.POINTER(_vp)],
+        "tsqr_get_unique_id": [_vp],
+        "tsqr_ctx_set_comm": [_vp, _vp, _i32, _i32],
+        "tsqr_loopback_create": [_i32, ctypes.POINTER(_vp)],
+        "tsqr_loopback_destroy": [_vp],
+        "tsqr_ctx_set_loopback": [_vp, _vp, _i32],
+        "tsqr_ctx_info": [_vp, _pi32, _pi32],
+        "tsqr_ctx_destroy": [_vp],
+        "tsqr_ctx_factor": [_vp, _i64, _i64, _vp, _i64, _vp, _i64, ctypes.POINTER(Opts), _vp, ctypes.POINTER(_vp)],
+        "tsqr_ctx_apply_qt": [_vp, _vp, _vp, _i64, _i64, _vp, _i64, _vp],
+        "tsqr_ctx_apply_q": [_vp, _vp, _vp, _i64, _i64, _vp],
+        "tsqr_ctx_form_q": [_vp, _vp, _vp, _i64, _vp],
+        "tsqr_measure_fp64_peak": [_pd, _pd, _vp],
+        "tsqr_qr_host": [ctypes.POINTER(_vp), _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64,
+                         ctypes.POINTER(Opts), _vp],
+        "tsqr_host_ws_free": [_vp],
     }
     for name, args in sig.items():
         fn = getattr(L, name)
@@ -97,5 +117,5 @@ def lib():
 
 def check(status: int, where: str) -> None:
     if status != TSQR_OK:
-        detail = lib().tsqr_last_error().decode() if status == 5 else ""
+        detail = lib().tsqr_last_error().decode() if status in (5, 6) else ""
         raise TsqrError(status, where, detail)

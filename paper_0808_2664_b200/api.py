@@ -202,6 +202,114 @@ def combine_stacked(packed: torch.Tensor, q: int, n: int, tau: torch.Tensor | No
     return tau
 
 
+# ------------------------------------------------------------ communicator
+class Ctx:
+    """A libtsqr communicator context (one per process / GPU): the collective
+    tsqr_ctx_* calls run every butterfly round inside the C library (NCCL grouped
+    send/recv on the call's stream, or the in-process loopback of the tests)."""
+
+    def __init__(self, device: int | None = None):
+        self.handle = ctypes.c_void_p(None)
+        self.device = torch.cuda.current_device() if device is None else device
+        check(lib().tsqr_ctx_create(self.device, ctypes.byref(self.handle)), "tsqr_ctx_create")
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        check(lib().tsqr_get_unique_id(buf), "tsqr_get_unique_id")
+        return buf.raw
+
+    def set_comm(self, uid: bytes, nranks: int, rank: int):
+        if len(uid) != 128:
+            raise ValueError("uid must be the 128 bytes of tsqr_get_unique_id")
+        check(lib().tsqr_ctx_set_comm(self.handle, ctypes.create_string_buffer(uid, 128), nranks, rank),
+              "tsqr_ctx_set_comm")
+        return self
+
+    def set_loopback(self, hub: "Loopback", rank: int):
+        check(lib().tsqr_ctx_set_loopback(self.handle, hub.handle, rank), "tsqr_ctx_set_loopback")
+        self._hub = hub                           # keep the hub alive
+        return self
+
+    def info(self):
+        nr, rk = ctypes.c_int32(), ctypes.c_int32()
+        check(lib().tsqr_ctx_info(self.handle, ctypes.byref(nr), ctypes.byref(rk)), "tsqr_ctx_info")
+        return nr.value, rk.value
+
+    def factor(self, A: torch.Tensor, block_rows: int = 0, tile_rows: int = 0, R: torch.Tensor | None = None,
+               tree: Tree | None = None, stream=None, debug: bool = False, stage_timing: bool = False):
+        """Collective factor of this rank's slab; R replicated.  Returns (R, tree)."""
+        pa, m, n, lda = _colmajor(A, "A")
+        if R is None:
+            R = torch.empty((n, n), dtype=torch.float64, device=A.device)
+        pr, _, _, ldr = _colmajor(R, "R")
+        nr, rk = self.info()
+        o = opts(block_rows, tile_rows, nr, rk, debug, stage_timing)
+        t = tree if tree is not None else Tree()
+        h = t.handle
+        check(lib().tsqr_ctx_factor(self.handle, m, n, pa, lda, pr, ldr, ctypes.byref(o), _stream_ptr(stream),
+                                    ctypes.byref(h)), "tsqr_ctx_factor")
+        t.handle = h
+        t.A, t.m_local, t.n, t.opts = A, m, n, o
+        return R, t
+
+    def apply_qt(self, tree: Tree, C: torch.Tensor, top: torch.Tensor | None = None, stream=None):
+        pc, m, k, ldc = _colmajor(C, "C")
+        ptop, ldtop = None, 0
+        if top is not None:
+            ptop, _, _, ldtop = _colmajor(top, "top")
+        check(lib().tsqr_ctx_apply_qt(self.handle, tree.handle, pc, ldc, k, ptop, ldtop, _stream_ptr(stream)),
+              "tsqr_ctx_apply_qt")
+        return C, top
+
+    def apply_q(self, tree: Tree, C: torch.Tensor, stream=None):
+        pc, m, k, ldc = _colmajor(C, "C")
+        check(lib().tsqr_ctx_apply_q(self.handle, tree.handle, pc, ldc, k, _stream_ptr(stream)), "tsqr_ctx_apply_q")
+        return C
+
+    def form_q(self, tree: Tree, Q: torch.Tensor | None = None, stream=None):
+        if Q is None:
+            Q = torch.empty((tree.n, tree.m_local), dtype=torch.float64, device=tree.A.device)
+        pq, _, _, ldq = _colmajor(Q, "Q")
+        check(lib().tsqr_ctx_form_q(self.handle, tree.handle, pq, ldq, _stream_ptr(stream)), "tsqr_ctx_form_q")
+        return Q
+
+    def free(self):
+        if self.handle:
+            lib().tsqr_ctx_destroy(self.handle)
+            self.handle = ctypes.c_void_p(None)
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+class Loopback:
+    """In-process exchange hub for G contexts of one process (tests): each rank's call
+    synchronises its own stream before posting, so no kernel waits on another rank."""
+
+    def __init__(self, nranks: int):
+        self.handle = ctypes.c_void_p(None)
+        check(lib().tsqr_loopback_create(nranks, ctypes.byref(self.handle)), "tsqr_loopback_create")
+
+    def __del__(self):
+        try:
+            if self.handle:
+                lib().tsqr_loopback_destroy(self.handle)
+        except Exception:
+            pass
+
+
+def measure_fp64_peak(stream=None):
+    """(DMMA, DFMA) TFLOP/s of this GPU, measured now (tsqr_measure_fp64_peak)."""
+    a, b = ctypes.c_double(), ctypes.c_double()
+    check(lib().tsqr_measure_fp64_peak(ctypes.byref(a), ctypes.byref(b), _stream_ptr(stream)),
+          "tsqr_measure_fp64_peak")
+    return a.value, b.value
+
+
 # ------------------------------------------------------------------- CAQR
 class Caqr:
     """Right-looking CAQR with TSQR panels (tsqr_caqr_*): one panel tree per panel_cols
@@ -303,14 +411,49 @@ def cross_partner(nranks: int, rank: int, rnd: int):
 
 
 # ----------------------------------------------------------------- end to end
-def tsqr(A_host: torch.Tensor, block_rows: int = 0, tile_rows: int = 0, want_q: bool = True,
-         device="cuda", stream=None):
-    """End-to-end convenience call with HOST tensors: copies A (column-major (n, m), ideally
-    pinned) to the device, factors it, forms Q, and copies R (and Q) back to host memory."""
-    A = A_host.to(device, non_blocking=True)
-    R, tree = factor(A, block_rows, tile_rows, stream=stream)
-    Q = form_q(tree, stream=stream) if want_q else None
-    R_h = R.to("cpu", non_blocking=False)
-    Q_h = Q.to("cpu", non_blocking=False) if want_q else None
-    tree.free()
-    return R_h, Q_h
+class HostQR:
+    """End-to-end QR of HOST matrices through one C call (tsqr_qr_host): copies in,
+    factor, form Q / apply Q^T, copies out, on one GPU; the device workspace and tree
+    are kept between calls of the same shape."""
+
+    def __init__(self):
+        self.ws = ctypes.c_void_p(None)
+
+    def __call__(self, A_host: torch.Tensor, block_rows: int = 0, tile_rows: int = 0, R_host=None, Q_host=None,
+                 C_host=None, want_q: bool = True, stream=None):
+        pa, m, n, lda = _colmajor(A_host, "A", host=True)
+        if R_host is None:
+            R_host = torch.empty((n, n), dtype=torch.float64).pin_memory()
+        pr, _, _, ldr = _colmajor(R_host, "R", host=True)
+        pq, ldq = None, 0
+        if want_q:
+            if Q_host is None:
+                Q_host = torch.empty((n, m), dtype=torch.float64).pin_memory()
+            pq, _, _, ldq = _colmajor(Q_host, "Q", host=True)
+        pc, ldc, k = None, 0, 0
+        if C_host is not None:
+            pc, _, k, ldc = _colmajor(C_host, "C", host=True)
+        o = opts(block_rows, tile_rows)
+        check(lib().tsqr_qr_host(ctypes.byref(self.ws), m, n, pa, lda, pr, ldr, pq, ldq, pc, ldc, k,
+                                 ctypes.byref(o), _stream_ptr(stream)), "tsqr_qr_host")
+        return R_host, Q_host, C_host
+
+    def free(self):
+        if self.ws:
+            lib().tsqr_host_ws_free(self.ws)
+            self.ws = ctypes.c_void_p(None)
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def tsqr(A_host: torch.Tensor, block_rows: int = 0, tile_rows: int = 0, want_q: bool = True, stream=None):
+    """End-to-end convenience call with HOST tensors (column-major (n, m), ideally pinned):
+    returns (R, Q) in host memory (Q None unless want_q)."""
+    h = HostQR()
+    R, Q, _ = h(A_host, block_rows, tile_rows, want_q=want_q, stream=stream)
+    h.free()
+    return R, Q

@@ -84,20 +84,45 @@ struct Sync {
     int *row, *tr;
     int s;
 };
-// Shared-memory accesses of one warp are performed in issue order, so a hand-off
-// needs only compiler barriers: the data stores precede the counter store in
-// program order (publish), and no load of the guarded data is hoisted above
-// the spin (wait).  No MEMBAR: a fence.cta would also wait for the warp's
-// outstanding global stores.
-__device__ __forceinline__ void sync_wait(const int *c, int v) {
-    while (*reinterpret_cast<const volatile int *>(c) < v) {
-    }
+// Memory model of a hand-off (PTX memory model, scope cta): the publisher's lanes
+// store the data, __syncwarp() orders those stores before lane 0's counter store,
+// which is a RELEASE (st.release.cta); the waiter reads the counter with an ACQUIRE
+// (ld.acquire.cta) and reads the data only after it, so a counter value that
+// satisfies the wait makes every store released before it visible (release /
+// acquire synchronisation; the warp barrier gives the cumulativity over the
+// publisher's other lanes).  Build with -DTSQR_HANDOFF_RELAXED for the round-1
+// variant (volatile accesses and compiler barriers only, relying on a warp's
+// shared-memory accesses being performed in issue order, which the model does
+// not promise) -- kept only to measure what the ordering costs.
+__device__ __forceinline__ int ld_acquire_cta(const int *c) {
+#ifdef TSQR_HANDOFF_RELAXED
+    const int v = *reinterpret_cast<const volatile int *>(c);
     asm volatile("" ::: "memory");
+    return v;
+#else
+    int v;
+    const unsigned a = (unsigned)__cvta_generic_to_shared(c);
+    asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+#endif
+}
+__device__ __forceinline__ void st_release_cta(int *c, int v) {
+#ifdef TSQR_HANDOFF_RELAXED
+    asm volatile("" ::: "memory");
+    *reinterpret_cast<volatile int *>(c) = v;
+#else
+    const unsigned a = (unsigned)__cvta_generic_to_shared(c);
+    asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+#endif
+}
+__device__ __forceinline__ void sync_wait(const int *c, int v) {
+    while (ld_acquire_cta(c) < v) {
+    }
 }
 __device__ __forceinline__ void sync_publish(int *c, int v) {
     asm volatile("" ::: "memory");
     __syncwarp();
-    if ((threadIdx.x & 31) == 0) *reinterpret_cast<volatile int *>(c) = v;
+    if ((threadIdx.x & 31) == 0) st_release_cta(c, v);
 }
 
 // dlarfg scalars (readings R1/R2/R19), branch-free: beta = -sign(alpha) N with
@@ -195,6 +220,40 @@ __device__ __forceinline__ void quad_sums(double &d, double &s2, double pd, doub
     dmma(s2, s1, ps, 1.0);
 }
 
+// Rescaled step (reading R23, wy::house_unsafe): the sums of a Householder step
+// redone on s x for the register layouts in which every lane of a q group holds
+// the same rows of the pivot column's tail (x[k][e] = row 8k + 2q + e) and
+// a(k, e) is this lane's column l4 on those rows.  Every input is warp-uniform
+// except a, so d (column l4's dot) and s2 are what the unscaled sums would be
+// for s x; sc = s.  Taken only when y = alpha^2 + sigma^2 left [2^-900, 2^900].
+template <int K, class AF>
+__device__ __forceinline__ void rescaled_sums(const double (&x)[K][2], AF a, double alpha, double &d, double &s2,
+                                              double &sc) {
+    double mx = fabs(alpha);
+#pragma unroll
+    for (int k = 0; k < K; ++k) mx = fmax(mx, fmax(fabs(x[k][0]), fabs(x[k][1])));
+    mx = fmax(mx, __shfl_xor_sync(FULL, mx, 1));
+    mx = fmax(mx, __shfl_xor_sync(FULL, mx, 2));
+    sc = wy::pow2_scale(mx);
+    double d0 = 0.0, d1 = 0.0, s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const double x0 = sc * x[k][0], x1 = sc * x[k][1];
+        d0 = fma(x0, a(k, 0), d0);
+        d1 = fma(x1, a(k, 1), d1);
+        s0 = fma(x0, x0, s0);
+        s1 = fma(x1, x1, s1);
+    }
+    d0 += d1;
+    s0 += s1;
+    d0 += __shfl_xor_sync(FULL, d0, 1);
+    s0 += __shfl_xor_sync(FULL, s0, 1);
+    d0 += __shfl_xor_sync(FULL, d0, 2);
+    s0 += __shfl_xor_sync(FULL, s0, 2);
+    d = d0;
+    s2 = s0;
+}
+
 // Columns past n are padding: their Householder steps would be identities
 // (tau = 0, zero reflector), so the panels stop after column n-1 and give the
 // remaining columns tau = 0 and zero Gram entries, which makes their rows and
@@ -252,15 +311,13 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
         double d, s2;
         quad_sums(d, s2, d0 + d1, s0 + s1);
         PROBE(3);
-        // R row j released by the previous chunk: the counter and the row are
-        // read together (a warp's shared-memory accesses are performed in
-        // issue order, so a row read issued after a counter read that sees
-        // the release sees the row); only if the counter is short do we spin
-        // and read the row again
+        // R row j released by the previous chunk: the row is read right after an
+        // acquire of its counter (ordered after it); only if the counter is
+        // short do we spin and read the row again
         double alpha, rj;                                            // R(j, j), R(j, 8P + l4)
         {
             const volatile double *rr = Rb + j * C::LDR;
-            const int c0 = *reinterpret_cast<const volatile int *>(sy.row + j);
+            const int c0 = ld_acquire_cta(sy.row + j);
             alpha = rr[j];
             rj = rr[8 * P + l4];
             if (c0 < sy.s) {
@@ -270,13 +327,20 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
             }
         }
         PROBE(4);
-        const House h = house_bf(alpha, s2);
+        House h = house_bf(alpha, s2);
+        double sc = 1.0;
+        if (wy::house_unsafe(alpha, s2)) {                          // warp-uniform, R23
+            rescaled_sums<C::KM>(x, [&](int k, int e) { return ch.a[k][P][e]; }, alpha, d, s2, sc);
+            h = house_bf(sc * alpha, s2);
+            h.beta = h.beta / sc;
+        }
+        const double sx = h.scale * sc;                              // scale of the unscaled x
         const double w = fma(h.scale, d, rj);                        // v^T [R(j,c); a_c]
         // a <- a - u x (u = tau scale w) for the trailing columns; the pivot
         // column becomes v = scale x, formed as scale x + (a - x) with a - x
         // exactly 0 (a - (1 - scale) x would cancel when scale << 1)
-        const double u = (l4 > jj) ? h.tau * h.scale * w : (l4 == jj ? 1.0 : 0.0);
-        const double g = (l4 == jj) ? h.scale : 0.0;
+        const double u = (l4 > jj) ? h.tau * sx * w : (l4 == jj ? 1.0 : 0.0);
+        const double g = (l4 == jj) ? sx : 0.0;
         // hand R row j to the next chunk first (its step j waits for it), then
         // update this chunk's panel
         const double rnew = (l4 == jj) ? h.beta : fma(-h.tau, w, rj);
@@ -340,10 +404,17 @@ __device__ __forceinline__ void panel_dense(Chunk<C> &ch, int kb, double *Gs, do
         }
         double d, s2;
         quad_sums(d, s2, d0 + d1, s0 + s1);
-        const House h = house_bf(alpha, s2);
+        House h = house_bf(alpha, s2);
+        double sc = 1.0;
+        if (wy::house_unsafe(alpha, s2)) {                          // warp-uniform, R23
+            rescaled_sums<C::KM>(x, [&](int k, int e) { return ch.a[k][P][e]; }, alpha, d, s2, sc);
+            h = house_bf(sc * alpha, s2);
+            h.beta = h.beta / sc;
+        }
+        const double sx = h.scale * sc;
         const double w = fma(h.scale, d, rj);
-        const double u = (l4 > jj) ? h.tau * h.scale * w : (l4 == jj ? 1.0 : 0.0);
-        const double g = (l4 == jj) ? h.scale : 0.0;                 // pivot column: v = scale x exactly
+        const double u = (l4 > jj) ? h.tau * sx * w : (l4 == jj ? 1.0 : 0.0);
+        const double g = (l4 == jj) ? sx : 0.0;                      // pivot column: v = scale x exactly
 #pragma unroll
         for (int k = 0; k < C::KM; ++k) {
             ch.a[k][P][0] = fma(g, x[k][0], fma(-u, x[k][0], ch.a[k][P][0]));
@@ -453,7 +524,7 @@ __device__ __forceinline__ void factor_panel(Chunk<C> &ch, int kind, int kb, dou
         sync_wait(sy.tr + P, sy.s);
         if (kind == 2) {
             if (lane < 8 && 8 * P + lane < n) tau_out[8 * P + lane] = 0.0;
-            if (lane < 8) sy.row[8 * P + lane] = sy.s + 1;
+            if (lane < 8) st_release_cta(sy.row + 8 * P + lane, sy.s + 1);
             if (!defer) sync_publish(sy.tr + P, sy.s + 1);
             return;
         }
@@ -502,7 +573,7 @@ __device__ __forceinline__ void factor_panel(Chunk<C> &ch, int kind, int kb, dou
             }
         asm volatile("" ::: "memory");
         __syncwarp();
-        if (lane < 8) sy.row[8 * P + lane] = sy.s + 1;
+        if (lane < 8) st_release_cta(sy.row + 8 * P + lane, sy.s + 1);
         if (!defer) sync_publish(sy.tr + P, sy.s + 1);
     }
     __syncwarp();

@@ -46,6 +46,10 @@ struct tsqr_tree_s {
     int pipe_count = 0, pipe_root = -1;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};   // stage timing (opts.flags bit 1)
     bool ev_recorded = false;
+    // completion of the last call on the tree (recorded on its stream): a call on another
+    // stream first waits for it, so the handle may move between streams
+    cudaEvent_t done = nullptr;
+    bool done_valid = false;
     // chunk-chain leaf stage
     int64_t *d_tile_chunk0 = nullptr;
     int *d_cta_tile0 = nullptr, *d_apply_cta_tile0 = nullptr;
@@ -67,6 +71,18 @@ void tsqr::set_last_error(const char *where, cudaError_t e) {
     g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
 }
 
+void tsqr::set_last_error_text(const char *text) { g_last_error = text; }
+
+bool tsqr::tree_shape(const tsqr_tree_s *t, int64_t *m_local, int64_t *n, int *nranks, int *rank, int *rounds_done) {
+    if (!t) return false;
+    *m_local = t->plan.m_local;
+    *n = t->plan.n;
+    *nranks = t->opts.nranks;
+    *rank = t->opts.rank;
+    *rounds_done = t->cross_done;
+    return true;
+}
+
 static tsqr_status_t cuda_fail(cudaError_t e, const char *where) {
     g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
     return TSQR_ERR_CUDA;
@@ -82,24 +98,51 @@ static tsqr_status_t debug_sync(const tsqr_tree_s *t, cudaStream_t st, const cha
     if (t->opts.flags & 1) CUDA_TRY(cudaStreamSynchronize(st), where);
     return TSQR_OK;
 }
+static tsqr_status_t leave(tsqr_tree_s *t, cudaStream_t st);
+static tsqr_status_t enter(tsqr_tree_s *t, cudaStream_t st);
+static tsqr_status_t finish(tsqr_tree_s *t, cudaStream_t st, const char *where) {
+    tsqr_status_t s = leave(t, st);
+    return s != TSQR_OK ? s : debug_sync(t, st, where);
+}
+#define ENTER(t, st)                                   \
+    do {                                               \
+        tsqr_status_t _s = enter((t), (st));           \
+        if (_s != TSQR_OK) return _s;                  \
+    } while (0)
 
-static void free_tree_memory(tsqr_tree_s *t) {
+// Stream ordering of a tree's calls: every device entry point runs enter() before its
+// first launch and leave() after its last one.
+static tsqr_status_t enter(tsqr_tree_s *t, cudaStream_t st) {
+    if (t->done_valid && st != t->stream) CUDA_TRY(cudaStreamWaitEvent(st, t->done, 0), "stream order");
+    return TSQR_OK;
+}
+static tsqr_status_t leave(tsqr_tree_s *t, cudaStream_t st) {
+    if (!t->done) CUDA_TRY(cudaEventCreateWithFlags(&t->done, cudaEventDisableTiming), "stream order");
+    CUDA_TRY(cudaEventRecord(t->done, st), "stream order");
+    t->stream = st;
+    t->done_valid = true;
+    return TSQR_OK;
+}
+
+// Device memory of a tree is stream-ordered (cudaMallocAsync / cudaFreeAsync on the
+// call's stream): nothing here synchronises the host.
+static void free_tree_memory(tsqr_tree_s *t, cudaStream_t st) {
     void *ptrs[] = {t->d_row0, t->d_rows, t->d_node_a,
                     t->d_tau_node, t->d_cross_y1, t->d_cross_tau, t->d_xbuf,
                     t->d_step_ids, t->d_pipe_nodes, t->d_prod_l, t->d_prod_r, t->d_pipe_flags,
                     t->d_tile_chunk0, t->d_cta_tile0, t->d_apply_cta_tile0, t->d_tau_chunk, t->d_tcache,
                     t->d_tcache_node, t->d_cross_tcache, t->d_wtmp, t->d_tcache_pair, t->d_gather};
     for (void *p : ptrs)
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, st);
 }
 
 // The wide path's stacking buffer (2n x max(n, cols) doubles), grown on demand.
-static tsqr_status_t wide_tmp(tsqr_tree_s *t, int64_t cols) {
+static tsqr_status_t wide_tmp(tsqr_tree_s *t, int64_t cols, cudaStream_t st) {
     const int64_t need = 2 * t->plan.n * std::max<int64_t>(cols, t->plan.n);
     if (t->d_wtmp && t->wtmp_size >= need) return TSQR_OK;
-    if (t->d_wtmp) cudaFree(t->d_wtmp);
+    if (t->d_wtmp) cudaFreeAsync(t->d_wtmp, st);
     t->d_wtmp = nullptr;
-    if (cudaMalloc((void **)&t->d_wtmp, sizeof(double) * need) != cudaSuccess) {
+    if (cudaMallocAsync((void **)&t->d_wtmp, sizeof(double) * need, st) != cudaSuccess) {
         cudaGetLastError();
         t->wtmp_size = 0;
         return TSQR_ERR_ALLOC;
@@ -124,6 +167,7 @@ const char *tsqr_status_string(tsqr_status_t s) {
         case TSQR_ERR_UNSUPPORTED: return "unsupported (n > TSQR_MAX_N, tile_rows above capacity, or nranks not a power of two)";
         case TSQR_ERR_ALLOC: return "allocation failed";
         case TSQR_ERR_CUDA: return "CUDA error";
+        case TSQR_ERR_NCCL: return "NCCL error or failed butterfly exchange";
     }
     return "unknown status";
 }
@@ -211,7 +255,7 @@ tsqr_status_t tsqr_cross_partner(int32_t nranks, int32_t rank, int32_t round, in
 }
 
 static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t lda, const tsqr_opts_t *opts,
-                                 tsqr_tree_s **out) {
+                                 cudaStream_t st, tsqr_tree_s **out) {
     tsqr_tree_s *t = new (std::nothrow) tsqr_tree_s();
     if (!t) return TSQR_ERR_ALLOC;
     tsqr_opts_t ro;
@@ -234,7 +278,7 @@ static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t 
     t->cross_rounds = ilog2(ro.nranks);
     cudaError_t e = cudaSuccess;
     auto alloc = [&](void **ptr, size_t bytes) {
-        if (e == cudaSuccess) e = cudaMalloc(ptr, bytes < 16 ? 16 : bytes);
+        if (e == cudaSuccess) e = cudaMallocAsync(ptr, bytes < 16 ? 16 : bytes, st);
     };
     alloc((void **)&t->d_row0, sizeof(int64_t) * L);
     alloc((void **)&t->d_rows, sizeof(int) * L);
@@ -292,31 +336,31 @@ static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t 
     }
     t->nchunks = nchunks;
     if (e != cudaSuccess) {
-        free_tree_memory(t);
+        free_tree_memory(t, st);
         delete t;
         g_last_error = std::string("tsqr_factor alloc: ") + cudaGetErrorString(e);
         cudaGetLastError();
         return TSQR_ERR_ALLOC;
     }
+    // plan arrays: stream-ordered copies on the call's stream (pageable sources are
+    // staged by the driver before cudaMemcpyAsync returns, so the vectors may go)
     std::vector<int> rows(p.tile_rows.begin(), p.tile_rows.end());
-    e = cudaMemcpy(t->d_row0, p.tile_row0.data(), sizeof(int64_t) * L, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(t->d_rows, rows.data(), sizeof(int) * L, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(t->d_node_a, p.node_a.data(), sizeof(int) * L, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess && !ids.empty())
-        e = cudaMemcpy(t->d_step_ids, ids.data(), sizeof(int) * ids.size(), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess && !pipe.empty())
-        e = cudaMemcpy(t->d_pipe_nodes, pipe.data(), sizeof(int) * pipe.size(), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(t->d_prod_l, prod_l.data(), sizeof(int) * L, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(t->d_prod_r, prod_r.data(), sizeof(int) * L, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess)
-        e = cudaMemcpy(t->d_tile_chunk0, p.tile_chunk0.data(), sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess)
-        e = cudaMemcpy(t->d_cta_tile0, cta_tile0.data(), sizeof(int) * (grid + 1), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess)
-        e = cudaMemcpy(t->d_apply_cta_tile0, apply_tile0.data(), sizeof(int) * (agrid + 1), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemset(t->d_tau_node, 0, sizeof(double) * L * n);
+    auto h2d = [&](void *dst, const void *src, size_t bytes) {
+        if (e == cudaSuccess && bytes) e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st);
+    };
+    h2d(t->d_row0, p.tile_row0.data(), sizeof(int64_t) * L);
+    h2d(t->d_rows, rows.data(), sizeof(int) * L);
+    h2d(t->d_node_a, p.node_a.data(), sizeof(int) * L);
+    h2d(t->d_step_ids, ids.data(), sizeof(int) * ids.size());
+    h2d(t->d_pipe_nodes, pipe.data(), sizeof(int) * pipe.size());
+    h2d(t->d_prod_l, prod_l.data(), sizeof(int) * L);
+    h2d(t->d_prod_r, prod_r.data(), sizeof(int) * L);
+    h2d(t->d_tile_chunk0, p.tile_chunk0.data(), sizeof(int64_t) * (L + 1));
+    h2d(t->d_cta_tile0, cta_tile0.data(), sizeof(int) * (grid + 1));
+    h2d(t->d_apply_cta_tile0, apply_tile0.data(), sizeof(int) * (agrid + 1));
+    if (e == cudaSuccess) e = cudaMemsetAsync(t->d_tau_node, 0, sizeof(double) * L * n, st);
     if (e != cudaSuccess) {
-        free_tree_memory(t);
+        free_tree_memory(t, st);
         delete t;
         return cuda_fail(e, "tsqr_factor setup");
     }
@@ -346,11 +390,21 @@ tsqr_status_t tsqr_factor(int64_t m_local, int64_t n, double *A, int64_t lda, do
                        t->opts.rank == ro.rank;
     if (!reuse) {
         tsqr_tree_s *nt = nullptr;
-        tsqr_status_t s = create_tree(m_local, n, A, lda, opts, &nt);
+        if (t) {                                  // the old tree's last work precedes the new one's
+            tsqr_status_t s0 = enter(t, (cudaStream_t)stream);
+            if (s0 != TSQR_OK) return s0;
+        }
+        tsqr_status_t s = create_tree(m_local, n, A, lda, opts, (cudaStream_t)stream, &nt);
         if (s != TSQR_OK) return s;
-        if (t) { tsqr_tree_free(t); }
+        if (t) {
+            t->stream = (cudaStream_t)stream;     // stream-ordered release behind the new tree's setup
+            tsqr_tree_free(t);
+        }
         t = nt;
         *tree = t;
+    } else {
+        tsqr_status_t s0 = enter(t, (cudaStream_t)stream);
+        if (s0 != TSQR_OK) return s0;
     }
     t->opts.flags = ro.flags;
     t->A = A;
@@ -391,7 +445,7 @@ tsqr_status_t tsqr_factor(int64_t m_local, int64_t n, double *A, int64_t lda, do
         if (R) CUDA_TRY(launch_extract_r(A, lda, (int)n, R, ldr, t->stream), "tsqr_factor R");
         CUDA_TRY(mark(2), "tsqr_factor events");
         t->ev_recorded = timed;
-        return debug_sync(t, t->stream, "tsqr_factor");
+        return finish(t, t->stream, "tsqr_factor");
     }
     CUDA_TRY(mark(0), "tsqr_factor events");
     CUDA_TRY(launch_chain_factor(ca, t->stream), "tsqr_factor leaves");
@@ -406,15 +460,15 @@ tsqr_status_t tsqr_factor(int64_t m_local, int64_t n, double *A, int64_t lda, do
     }
     CUDA_TRY(mark(2), "tsqr_factor events");
     t->ev_recorded = timed;
-    return debug_sync(t, t->stream, "tsqr_factor");
+    return finish(t, t->stream, "tsqr_factor");
 }
 
 tsqr_status_t tsqr_pack_r(tsqr_tree_t t, double *packed, void *stream) {
     NvtxRange nvtx_("tsqr_pack_r");
     if (!t || !t->A || !packed) return TSQR_ERR_INVALID;
+    ENTER(t, (cudaStream_t)stream);
     CUDA_TRY(launch_pack_r(t->A, t->lda, (int)t->plan.n, packed, (cudaStream_t)stream), "tsqr_pack_r");
-    t->stream = (cudaStream_t)stream;
-    return debug_sync(t, t->stream, "tsqr_pack_r");
+    return finish(t, (cudaStream_t)stream, "tsqr_pack_r");
 }
 
 tsqr_status_t tsqr_cross_factor(tsqr_tree_t t, int32_t round, const double *partner_packed, double *R,
@@ -426,9 +480,10 @@ tsqr_status_t tsqr_cross_factor(tsqr_tree_t t, int32_t round, const double *part
     int32_t partner, lower, role;
     if (tsqr_cross_partner(t->opts.nranks, t->opts.rank, round, &partner, &lower, &role) != TSQR_OK)
         return TSQR_ERR_INVALID;
+    ENTER(t, (cudaStream_t)stream);
     const int n = (int)t->plan.n;
     if (t->wide) {
-        tsqr_status_t ws = wide_tmp(t, n);
+        tsqr_status_t ws = wide_tmp(t, n, (cudaStream_t)stream);
         if (ws != TSQR_OK) return ws;
         CUDA_TRY(launch_wide_cross_factor(t->A, t->lda, n, partner_packed, lower, t->d_wtmp,
                                           t->d_cross_y1 + (int64_t)(round - 1) * n * n,
@@ -443,8 +498,7 @@ tsqr_status_t tsqr_cross_factor(tsqr_tree_t t, int32_t round, const double *part
                  "tsqr_cross_factor");
     }
     t->cross_done = round;
-    t->stream = (cudaStream_t)stream;
-    return debug_sync(t, t->stream, "tsqr_cross_factor");
+    return finish(t, (cudaStream_t)stream, "tsqr_cross_factor");
 }
 
 // Packed R of rank group g at butterfly level r (ranks g*2^r .. (g+1)*2^r - 1) from the
@@ -488,20 +542,21 @@ tsqr_status_t tsqr_cross_factor_gathered(tsqr_tree_t t, const double *all_packed
     if (R && ldr < t->plan.n) return TSQR_ERR_INVALID;
     const int n = (int)t->plan.n, G = t->opts.nranks;
     cudaStream_t st = (cudaStream_t)stream;
+    ENTER(t, st);
     if (t->cross_rounds == 0) {
         if (R) CUDA_TRY(launch_extract_r(t->A, t->lda, n, R, ldr, st), "tsqr_cross_factor_gathered");
-        return debug_sync(t, st, "tsqr_cross_factor_gathered");
+        return finish(t, st, "tsqr_cross_factor_gathered");
     }
     if (!t->d_gather) {
         const size_t words = (size_t)n * n + (size_t)G * n * (n + 1) / 2;
-        if (cudaMalloc((void **)&t->d_gather, sizeof(double) * words) != cudaSuccess) {
+        if (cudaMallocAsync((void **)&t->d_gather, sizeof(double) * words, st) != cudaSuccess) {
             cudaGetLastError();
             t->d_gather = nullptr;
             return TSQR_ERR_ALLOC;
         }
     }
     if (t->wide) {
-        tsqr_status_t ws = wide_tmp(t, n);
+        tsqr_status_t ws = wide_tmp(t, n, st);
         if (ws != TSQR_OK) return ws;
     }
     for (int r = 1; r <= t->cross_rounds; ++r) {
@@ -524,6 +579,7 @@ tsqr_status_t tsqr_apply_qt(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, do
     if (!C || ldc < t->plan.m_local) return TSQR_ERR_INVALID;
     if (top && ldtop < t->plan.n) return TSQR_ERR_INVALID;
     cudaStream_t st = (cudaStream_t)stream;
+    ENTER(t, st);
     ChainApplyArgs ca;
     ca.A = t->A; ca.lda = t->lda; ca.n = (int)t->plan.n; ca.chunk_rows = t->plan.c;
     ca.tile_row0 = t->d_row0; ca.tile_rows = t->d_rows; ca.tile_chunk0 = t->d_tile_chunk0;
@@ -554,8 +610,7 @@ tsqr_status_t tsqr_apply_qt(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, do
         }
     }
     if (top) CUDA_TRY(launch_copy_block(C, ldc, top, ldtop, (int)t->plan.n, (int)k, st), "tsqr_apply_qt top");
-    t->stream = st;
-    return debug_sync(t, st, "tsqr_apply_qt");
+    return finish(t, st, "tsqr_apply_qt");
 }
 
 tsqr_status_t tsqr_cross_apply_qt(tsqr_tree_t t, int32_t round, double *top, int64_t ldtop,
@@ -569,9 +624,10 @@ tsqr_status_t tsqr_cross_apply_qt(tsqr_tree_t t, int32_t round, double *top, int
         return TSQR_ERR_INVALID;
     if (role != 0 && (!C || ldc < t->plan.m_local)) return TSQR_ERR_INVALID;
     if (k == 0) return TSQR_OK;
+    ENTER(t, (cudaStream_t)stream);
     const int n = (int)t->plan.n;
     if (t->wide) {
-        tsqr_status_t ws = wide_tmp(t, k);
+        tsqr_status_t ws = wide_tmp(t, k, (cudaStream_t)stream);
         if (ws != TSQR_OK) return ws;
         CUDA_TRY(launch_wide_cross_apply(t->d_cross_y1 + (int64_t)(round - 1) * n * n,
                                          t->d_cross_tcache + (int64_t)(round - 1) * t->npan * 64, top, ldtop,
@@ -584,8 +640,7 @@ tsqr_status_t tsqr_cross_apply_qt(tsqr_tree_t t, int32_t round, double *top, int
                                     C, ldc, n, (int)k, 1, (cudaStream_t)stream),
                  "tsqr_cross_apply_qt");
     }
-    t->stream = (cudaStream_t)stream;
-    return debug_sync(t, t->stream, "tsqr_cross_apply_qt");
+    return finish(t, (cudaStream_t)stream, "tsqr_cross_apply_qt");
 }
 
 tsqr_status_t tsqr_cross_apply_q(tsqr_tree_t t, int32_t round, double *top, int64_t ldtop,
@@ -600,9 +655,10 @@ tsqr_status_t tsqr_cross_apply_q(tsqr_tree_t t, int32_t round, double *top, int6
         return TSQR_ERR_INVALID;
     if (role == 0) return TSQR_ERR_INVALID;        // only the group heads take part in this round
     if (k == 0) return TSQR_OK;
+    ENTER(t, (cudaStream_t)stream);
     const int n = (int)t->plan.n;
     if (t->wide) {
-        tsqr_status_t ws = wide_tmp(t, k);
+        tsqr_status_t ws = wide_tmp(t, k, (cudaStream_t)stream);
         if (ws != TSQR_OK) return ws;
         CUDA_TRY(launch_wide_cross_apply(t->d_cross_y1 + (int64_t)(round - 1) * n * n,
                                          t->d_cross_tcache + (int64_t)(round - 1) * t->npan * 64, top, ldtop,
@@ -615,8 +671,7 @@ tsqr_status_t tsqr_cross_apply_q(tsqr_tree_t t, int32_t round, double *top, int6
                                     C, ldc, n, (int)k, 0, (cudaStream_t)stream),
                  "tsqr_cross_apply_q");
     }
-    t->stream = (cudaStream_t)stream;
-    return debug_sync(t, t->stream, "tsqr_cross_apply_q");
+    return finish(t, (cudaStream_t)stream, "tsqr_cross_apply_q");
 }
 
 tsqr_status_t tsqr_apply_q(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, void *stream) {
@@ -627,6 +682,7 @@ tsqr_status_t tsqr_apply_q(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, voi
     if (!C || ldc < t->plan.m_local) return TSQR_ERR_INVALID;
     const int n = (int)t->plan.n;
     cudaStream_t st = (cudaStream_t)stream;
+    ENTER(t, st);
     for (size_t g = 0; g + 1 < t->step_off.size(); ++g) {             // tree steps top-down
         const int cnt = t->step_off[g + 1] - t->step_off[g];
         if (cnt == 0) continue;
@@ -646,8 +702,7 @@ tsqr_status_t tsqr_apply_q(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, voi
         ca.C = C; ca.ldc = ldc; ca.k = (int)k; ca.forward = 0; ca.xbuf = nullptr;
         CUDA_TRY(launch_cs_apply(ca, st), "tsqr_apply_q leaves");
     }
-    t->stream = st;
-    return debug_sync(t, st, "tsqr_apply_q");
+    return finish(t, st, "tsqr_apply_q");
 }
 
 tsqr_status_t tsqr_form_q(tsqr_tree_t t, double *Q, int64_t ldq, void *stream) {
@@ -658,8 +713,9 @@ tsqr_status_t tsqr_form_q(tsqr_tree_t t, double *Q, int64_t ldq, void *stream) {
     const int n = (int)t->plan.n;
     const int L = t->plan.ntiles();
     cudaStream_t st = (cudaStream_t)stream;
+    ENTER(t, st);
     if (!t->d_xbuf) {
-        cudaError_t e = cudaMalloc((void **)&t->d_xbuf, sizeof(double) * (size_t)L * n * n);
+        cudaError_t e = cudaMallocAsync((void **)&t->d_xbuf, sizeof(double) * (size_t)L * n * n, st);
         if (e != cudaSuccess) {
             t->d_xbuf = nullptr;
             cudaGetLastError();
@@ -668,7 +724,7 @@ tsqr_status_t tsqr_form_q(tsqr_tree_t t, double *Q, int64_t ldq, void *stream) {
         }
     }
     if (t->wide) {
-        tsqr_status_t ws = wide_tmp(t, n);
+        tsqr_status_t ws = wide_tmp(t, n, st);
         if (ws != TSQR_OK) return ws;
         CUDA_TRY(cudaMemsetAsync(t->d_xbuf, 0, sizeof(double) * (size_t)L * n * n, st), "tsqr_form_q");
         CUDA_TRY(launch_wide_cross_root_x(t->d_cross_y1, t->d_cross_tcache, (int64_t)t->npan * 64, t->cross_rounds,
@@ -685,8 +741,7 @@ tsqr_status_t tsqr_form_q(tsqr_tree_t t, double *Q, int64_t ldq, void *stream) {
         CUDA_TRY(launch_wide_apply_leaves(t->A, t->lda, n, t->d_row0, t->d_rows, L, (int)t->plan.max_rows,
                                           t->d_tcache, t->d_tcache_pair, Q, ldq, n, 0, st),
                  "tsqr_form_q leaves");
-        t->stream = st;
-        return debug_sync(t, st, "tsqr_form_q");
+        return finish(t, st, "tsqr_form_q");
     }
     // root X of this rank: I (one GPU) or the butterfly path (no communication)
     // the node stages read X_b = 0 below every subtree's X ([X; 0])
@@ -709,16 +764,17 @@ tsqr_status_t tsqr_form_q(tsqr_tree_t t, double *Q, int64_t ldq, void *stream) {
     ca.cta_tile0 = t->d_apply_cta_tile0; ca.grid = t->apply_grid; ca.tcache = t->d_tcache;
     ca.C = Q; ca.ldc = ldq; ca.k = n; ca.forward = 0; ca.xbuf = t->d_xbuf;
     CUDA_TRY(launch_cs_apply(ca, st), "tsqr_form_q leaves");
-    t->stream = st;
-    return debug_sync(t, st, "tsqr_form_q");
+    return finish(t, st, "tsqr_form_q");
 }
 
 tsqr_status_t tsqr_tree_free(tsqr_tree_t t) {
     if (!t) return TSQR_OK;
-    if (t->stream) cudaStreamSynchronize(t->stream);
+    // stream-ordered: the memory is released behind the tree's last call on its stream
+    // (no host synchronisation); events are destroyed once their work completes
     for (cudaEvent_t &e : t->ev)
         if (e) cudaEventDestroy(e);
-    free_tree_memory(t);
+    if (t->done) cudaEventDestroy(t->done);
+    free_tree_memory(t, t->stream);
     delete t;
     return TSQR_OK;
 }

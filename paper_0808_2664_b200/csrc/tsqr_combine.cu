@@ -8,6 +8,7 @@
 // Product code.
 #include "../../include/tsqr.h"
 #include "tsqr_kernels.h"
+#include "wy.cuh"
 
 #include <cuda_runtime.h>
 
@@ -35,6 +36,19 @@ __device__ double block_sum(double v, double *red) {
     return s;
 }
 
+__device__ double block_max(double v, double *red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < CW; ++w) s = fmax(s, red[w]);
+    __syncthreads();
+    return s;
+}
+
 __global__ void __launch_bounds__(CT) k_combine_q(double *g, int q, int n, double *tau_out, int staged) {
     extern __shared__ __align__(16) double sm[];
     __shared__ double red[CW];
@@ -52,17 +66,30 @@ __global__ void __launch_bounds__(CT) k_combine_q(double *g, int q, int n, doubl
             const double x = P.at(1 + e / (j + 1), e % (j + 1), j);
             s = fma(x, x, s);
         }
-        const double sigma2 = block_sum(s, red);
+        double sigma2 = block_sum(s, red);
+        double sc = 1.0;
+        if (tsqr::wy::house_unsafe(P.at(0, j, j), sigma2)) {      // block-uniform: dlarfg's rescaling (R23)
+            double mx = 0.0;
+            for (int e = threadIdx.x; e < len; e += CT) mx = fmax(mx, fabs(P.at(1 + e / (j + 1), e % (j + 1), j)));
+            sc = tsqr::wy::pow2_scale(fmax(block_max(mx, red), fabs(P.at(0, j, j))));
+            s = 0.0;
+            for (int e = threadIdx.x; e < len; e += CT) {
+                const double x = sc * P.at(1 + e / (j + 1), e % (j + 1), j);
+                s = fma(x, x, s);
+            }
+            sigma2 = block_sum(s, red);                        // of s w
+        }
         if (threadIdx.x == 0) {
             // House(w), LAPACK dlarfg: beta = -sign(alpha)||w||, tau = (beta - alpha)/beta,
-            // v = w / (alpha - beta), v(1) = 1; w with nothing to annihilate gives H = I
-            const double alpha = P.at(0, j, j);
+            // v = w / (alpha - beta), v(1) = 1; w with nothing to annihilate gives H = I;
+            // computed on s w (s = 1 unless rescaled): beta = beta_s / s, 1/(alpha - beta) = s/(alpha_s - beta_s)
+            const double alpha = sc * P.at(0, j, j);
             if (sigma2 == 0.0) {
-                hh[0] = 0.0; hh[1] = alpha; hh[2] = 0.0;
+                hh[0] = 0.0; hh[1] = alpha / sc; hh[2] = 0.0;
             } else {
                 const double nrm = sqrt(fma(alpha, alpha, sigma2));
                 const double beta = alpha >= 0.0 ? -nrm : nrm;
-                hh[0] = (beta - alpha) / beta; hh[1] = beta; hh[2] = 1.0 / (alpha - beta);
+                hh[0] = (beta - alpha) / beta; hh[1] = beta / sc; hh[2] = sc / (alpha - beta);
             }
         }
         __syncthreads();

@@ -10,6 +10,12 @@ namespace tsqr {
 
 // The text tsqr_last_error() returns (tsqr_api.cu); for the C-ABI entry points in other files.
 void set_last_error(const char *where, cudaError_t e);
+void set_last_error_text(const char *text);
+}  // namespace tsqr
+struct tsqr_tree_s;
+namespace tsqr {
+// Shape of a tree handle (tsqr_api.cu), for the communicator layer (tsqr_comm.cu).
+bool tree_shape(const tsqr_tree_s *t, int64_t *m_local, int64_t *n, int *nranks, int *rank, int *rounds_done);
 
 // Leaf stage on the chunk engine (tsqr_chain.cu).
 struct ChainArgs {

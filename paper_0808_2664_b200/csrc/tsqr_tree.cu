@@ -119,10 +119,17 @@ __device__ __forceinline__ void node_panel(NodeRegs<C> &rg, double *Ahead_a, dou
         chunk::quad_sums(d, s2, d0 + d1, s0 + s1);
         const double alpha = Ra[jj * C::LDA + 8 * P + jj];
         const double rj = Ra[jj * C::LDA + 8 * P + l4];
-        const House h = house_bf(alpha, s2);
+        House h = house_bf(alpha, s2);
+        double sc = 1.0;
+        if (wy::house_unsafe(alpha, s2)) {                          // warp-uniform, R23
+            chunk::rescaled_sums<P + 1>(x, [&](int k, int e) { return rg.a[k][P][e]; }, alpha, d, s2, sc);
+            h = house_bf(sc * alpha, s2);
+            h.beta = h.beta / sc;
+        }
+        const double sx = h.scale * sc;
         const double w = fma(h.scale, d, rj);
-        const double u = (l4 > jj) ? h.tau * h.scale * w : (l4 == jj ? 1.0 : 0.0);
-        const double g = (l4 == jj) ? h.scale : 0.0;
+        const double u = (l4 > jj) ? h.tau * sx * w : (l4 == jj ? 1.0 : 0.0);
+        const double g = (l4 == jj) ? sx : 0.0;
         const double rnew = (l4 == jj) ? h.beta : fma(-h.tau, w, rj);
 #pragma unroll
         for (int k = 0; k <= P; ++k) {
@@ -443,10 +450,49 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                 SPROBE(2);
                 const double alpha = RaP[8 * jj + jj];
                 const double rj = RaP[8 * l4 + jj];
-                const House h = house_bf(alpha, s2);
+                House h = house_bf(alpha, s2);
+                double sc = 1.0;
+                if (wy::house_unsafe(alpha, s2)) {              // block-uniform, rescaled step (R23)
+                    double mx = fabs(alpha);
+                    for (int k = warp; k <= P; k += NT / 32) {
+                        const double2 x = *reinterpret_cast<const double2 *>(xr + 8 * k + 2 * q);
+                        mx = fmax(mx, fmax(fabs(x.x), fabs(x.y)));
+                    }
+                    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+                    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+                    __syncthreads();                             // every warp has read the sums
+                    if (lane == 0) part[warp * 9] = mx;
+                    __syncthreads();
+                    for (int w2 = 0; w2 < NT / 32; ++w2) mx = fmax(mx, part[w2 * 9]);
+                    sc = wy::pow2_scale(mx);
+                    __syncthreads();                             // every warp has read the maxima
+                    d0 = d1 = s0 = s1 = 0.0;
+                    for (int k = warp; k <= P; k += NT / 32) {
+                        const double2 x = *reinterpret_cast<const double2 *>(xr + 8 * k + 2 * q);
+                        const double2 v = *reinterpret_cast<const double2 *>(Wb + 64 * k + 8 * l4 + 2 * q);
+                        d0 = fma(sc * x.x, v.x, d0);
+                        d1 = fma(sc * x.y, v.y, d1);
+                        s0 = fma(sc * x.x, sc * x.x, s0);
+                        s1 = fma(sc * x.y, sc * x.y, s1);
+                    }
+                    chunk::quad_sums(dw, sw, d0 + d1, s0 + s1);
+                    if (q == 0) part[warp * 9 + l4] = dw;
+                    if (lane == 0) part[warp * 9 + 8] = sw;
+                    __syncthreads();
+                    d = 0.0;
+                    s2 = 0.0;
+#pragma unroll
+                    for (int w2 = 0; w2 < NT / 32; ++w2) {
+                        d += part[w2 * 9 + l4];
+                        s2 += part[w2 * 9 + 8];
+                    }
+                    h = house_bf(sc * alpha, s2);
+                    h.beta = h.beta / sc;
+                }
+                const double sx = h.scale * sc;
                 const double w = fma(h.scale, d, rj);
-                const double u = (l4 > jj) ? h.tau * h.scale * w : (l4 == jj ? 1.0 : 0.0);
-                const double g = (l4 == jj) ? h.scale : 0.0;
+                const double u = (l4 > jj) ? h.tau * sx * w : (l4 == jj ? 1.0 : 0.0);
+                const double g = (l4 == jj) ? sx : 0.0;
                 const double rnew = (l4 == jj) ? h.beta : fma(-h.tau, w, rj);
                 SPROBE(3);
 #pragma unroll 4

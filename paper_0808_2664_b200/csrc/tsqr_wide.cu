@@ -157,10 +157,58 @@ __device__ void wide_qr(const Prob &P, int n, double *tau, double *tcache, Smem 
                 s2 += S.part[par][w][8];
             }
             const double rj = S.piv[par][l4], alpha = S.piv[par][jj];
-            const House h = house(alpha, s2);
+            House h = house(alpha, s2);
+            double sc = 1.0;
+            if (wy::house_unsafe(alpha, s2)) {                      // block-uniform, rescaled step (R23)
+                double mx = fabs(alpha);
+#pragma unroll
+                for (int k = 0; k < KMW; ++k) {
+                    const double2 xv = *reinterpret_cast<const double2 *>(xr + 8 * k + 2 * q);
+                    const int r = rbase + 8 * k + 2 * q;
+                    mx = fmax(mx, fmax(r > j ? fabs(xv.x) : 0.0, r + 1 > j ? fabs(xv.y) : 0.0));
+                }
+                mx = fmax(mx, __shfl_xor_sync(FULL, mx, 1));
+                mx = fmax(mx, __shfl_xor_sync(FULL, mx, 2));
+                // part[par ^ 1] is free: its last readers (step jj - 1) are past this step's barrier
+                if (lane == 0) S.part[par ^ 1][warp][8] = mx;
+                __syncthreads();
+                for (int w = 0; w < NW; ++w) mx = fmax(mx, S.part[par ^ 1][w][8]);
+                sc = wy::pow2_scale(mx);
+                __syncthreads();
+                double e0 = 0.0, e1 = 0.0, f0 = 0.0, f1 = 0.0;
+#pragma unroll
+                for (int k = 0; k < KMW; ++k) {
+                    const double2 xv = *reinterpret_cast<const double2 *>(xr + 8 * k + 2 * q);
+                    const int r = rbase + 8 * k + 2 * q;
+                    const double x0 = r > j ? sc * xv.x : 0.0, x1 = r + 1 > j ? sc * xv.y : 0.0;
+                    e0 = fma(x0, a[k][0], e0);
+                    e1 = fma(x1, a[k][1], e1);
+                    f0 = fma(x0, x0, f0);
+                    f1 = fma(x1, x1, f1);
+                }
+                dd = e0 + e1;
+                s2 = f0 + f1;
+                dd += __shfl_xor_sync(FULL, dd, 1);
+                s2 += __shfl_xor_sync(FULL, s2, 1);
+                dd += __shfl_xor_sync(FULL, dd, 2);
+                s2 += __shfl_xor_sync(FULL, s2, 2);
+                if (q == 0) S.part[par ^ 1][warp][l4] = dd;
+                if (lane == 0) S.part[par ^ 1][warp][8] = s2;
+                __syncthreads();
+                dd = 0.0;
+                s2 = 0.0;
+#pragma unroll
+                for (int w = 0; w < NW; ++w) {
+                    dd += S.part[par ^ 1][w][l4];
+                    s2 += S.part[par ^ 1][w][8];
+                }
+                h = house(sc * alpha, s2);
+                h.beta = h.beta / sc;
+            }
+            const double sx = h.scale * sc;
             const double wv = fma(h.scale, dd, rj);
-            const double u = (l4 > jj) ? h.tau * h.scale * wv : (l4 == jj ? 1.0 : 0.0);
-            const double g = (l4 == jj) ? h.scale : 0.0;             // pivot column: v = scale x exactly
+            const double u = (l4 > jj) ? h.tau * sx * wv : (l4 == jj ? 1.0 : 0.0);
+            const double g = (l4 == jj) ? sx : 0.0;             // pivot column: v = scale x exactly
             const double pnew = (l4 > jj) ? fma(-h.tau, wv, rj) : (l4 == jj ? h.beta : rj);
             double *xw = par ? xs0 : xs1;
 #pragma unroll
@@ -612,10 +660,58 @@ __device__ void wide_leaf_qr(double *At, int64_t lda, int H, int n, double *tau,
                 s2 += S.part[par][w][8];
             }
             const double rj = S.piv[par][l4], alpha = S.piv[par][jj];
-            const House h = house(alpha, s2);
+            House h = house(alpha, s2);
+            double sc = 1.0;
+            if (wy::house_unsafe(alpha, s2)) {                      // block-uniform, rescaled step (R23)
+                double mx = fabs(alpha);
+#pragma unroll
+                for (int k = 0; k < KM; ++k) {
+                    const double2 xv = *reinterpret_cast<const double2 *>(xr + 8 * k + 2 * q);
+                    const int r = rbase + 8 * k + 2 * q;
+                    mx = fmax(mx, fmax(r > j ? fabs(xv.x) : 0.0, r + 1 > j ? fabs(xv.y) : 0.0));
+                }
+                mx = fmax(mx, __shfl_xor_sync(FULL, mx, 1));
+                mx = fmax(mx, __shfl_xor_sync(FULL, mx, 2));
+                // part[par ^ 1] is free: its last readers (step jj - 1) are past this step's barrier
+                if (lane == 0) S.part[par ^ 1][warp][8] = mx;
+                __syncthreads();
+                for (int w = 0; w < NW; ++w) mx = fmax(mx, S.part[par ^ 1][w][8]);
+                sc = wy::pow2_scale(mx);
+                __syncthreads();
+                double e0 = 0.0, e1 = 0.0, f0 = 0.0, f1 = 0.0;
+#pragma unroll
+                for (int k = 0; k < KM; ++k) {
+                    const double2 xv = *reinterpret_cast<const double2 *>(xr + 8 * k + 2 * q);
+                    const int r = rbase + 8 * k + 2 * q;
+                    const double x0 = r > j ? sc * xv.x : 0.0, x1 = r + 1 > j ? sc * xv.y : 0.0;
+                    e0 = fma(x0, a[k][0], e0);
+                    e1 = fma(x1, a[k][1], e1);
+                    f0 = fma(x0, x0, f0);
+                    f1 = fma(x1, x1, f1);
+                }
+                dd = e0 + e1;
+                s2 = f0 + f1;
+                dd += __shfl_xor_sync(FULL, dd, 1);
+                s2 += __shfl_xor_sync(FULL, s2, 1);
+                dd += __shfl_xor_sync(FULL, dd, 2);
+                s2 += __shfl_xor_sync(FULL, s2, 2);
+                if (q == 0) S.part[par ^ 1][warp][l4] = dd;
+                if (lane == 0) S.part[par ^ 1][warp][8] = s2;
+                __syncthreads();
+                dd = 0.0;
+                s2 = 0.0;
+#pragma unroll
+                for (int w = 0; w < NW; ++w) {
+                    dd += S.part[par ^ 1][w][l4];
+                    s2 += S.part[par ^ 1][w][8];
+                }
+                h = house(sc * alpha, s2);
+                h.beta = h.beta / sc;
+            }
+            const double sx = h.scale * sc;
             const double wv = fma(h.scale, dd, rj);
-            const double u = (l4 > jj) ? h.tau * h.scale * wv : (l4 == jj ? 1.0 : 0.0);
-            const double g = (l4 == jj) ? h.scale : 0.0;
+            const double u = (l4 > jj) ? h.tau * sx * wv : (l4 == jj ? 1.0 : 0.0);
+            const double g = (l4 == jj) ? sx : 0.0;
             const double pnew = (l4 > jj) ? fma(-h.tau, wv, rj) : (l4 == jj ? h.beta : rj);
             double *xw = par ? xs0 : xs1;
 #pragma unroll

@@ -69,6 +69,30 @@ __device__ __forceinline__ House householder(double alpha, double sigma2) {
     return h;
 }
 
+// dlarfg's rescaling (LAPACK scales x by 1/safmin while |beta| < safmin; reading
+// R23).  The unscaled step forms sigma^2 = sum x_i^2 and the dots x^T a in plain
+// fp64 and takes 1/sqrt and 1/x from flush-to-zero MUFU seeds, so it needs
+// y = alpha^2 + sigma^2 inside [2^-900, 2^900]: no square or dot under- or
+// overflows there (entries of A around 1e-160 or 1e+155 leave it).  Outside it
+// (a warp- or block-uniform branch, never taken on ordinary data) the step is
+// redone on s x, s = 2^-e a power of two with s max(|alpha|, |x_i|) in [0.5, 1):
+// the scalars of the scaled column are (s beta, tau, scale / s), so the caller
+// keeps its formulas with
+//     w = rj + scale_s d_s      (d_s = (s x)^T a: the dot recomputed on s x),
+//     u = tau (s scale_s) w,    v = (s scale_s) x,    beta = beta_s / s.
+__device__ __forceinline__ bool house_unsafe(double alpha, double s2) {
+    const double y = fma(alpha, alpha, s2);
+    return !(y >= 0x1p-900 && y <= 0x1p+900);
+}
+// s = 2^-e with s mx in [0.5, 1); 1 for mx = 0, inf or NaN (nothing to rescale);
+// e clamped to [-1000, 1000] so that s and 1/s stay finite (a subnormal mx then
+// lands near 2^-74, far inside the safe range)
+__device__ __forceinline__ double pow2_scale(double mx) {
+    if (!(mx > 0.0) || isinf(mx)) return 1.0;
+    const int e = max(-1000, min(1000, ilogb(mx) + 1));
+    return ldexp(1.0, -e);
+}
+
 // Active 8-row blocks of panel p: dense (blocks p .. nrb-1) or structured node
 // (the pivot block piv holding row block p of R_a, then blocks na .. na+p of R_b).
 struct Rows {
@@ -121,9 +145,30 @@ __device__ __forceinline__ void panel_steps(double (*pv)[2], int p, int n, doubl
         const double rj = __shfl_sync(0xffffffffu, pj, 4 * cl + (jj >> 1));   // A(8p + jj, col)
         const double sig2 = __shfl_sync(0xffffffffu, d, 4 * jj);
         const double alpha = __shfl_sync(0xffffffffu, rj, 4 * jj);
-        const House h = householder(alpha, sig2);
+        House h = householder(alpha, sig2);
+        double sx = h.scale;                                 // the scale that multiplies the unscaled x
+        if (house_unsafe(alpha, sig2)) {                     // warp-uniform; rescaled step (R23)
+            double mx = fabs(alpha);
+#pragma unroll
+            for (int k = 0; k < KM; ++k) mx = fmax(mx, fmax(fabs(x[k][0]), fabs(x[k][1])));
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+            const double sc = pow2_scale(mx);
+            double e0 = 0.0, e1 = 0.0;
+#pragma unroll
+            for (int k = 0; k < KM; ++k) {
+                e0 = fma(sc * x[k][0], pv[k][0], e0);
+                e1 = fma(sc * x[k][1], pv[k][1], e1);
+            }
+            d = e0 + e1;
+            d += __shfl_xor_sync(0xffffffffu, d, 1);
+            d += __shfl_xor_sync(0xffffffffu, d, 2);
+            h = householder(sc * alpha, sc * __shfl_sync(0xffffffffu, d, 4 * jj));   // (s x)^T (s x)
+            sx = h.scale * sc;
+            h.beta = h.beta / sc;
+        }
         const double w = fma(d, h.scale, rj);                // v^T A(:, col)
-        const double u = (cl > jj && col < n) ? h.tau * h.scale * w : 0.0;
+        const double u = (cl > jj && col < n) ? h.tau * sx * w : 0.0;
 #pragma unroll
         for (int k = 0; k < KM; ++k) {
             pv[k][0] = fma(-x[k][0], u, pv[k][0]);
@@ -133,7 +178,7 @@ __device__ __forceinline__ void panel_steps(double (*pv)[2], int p, int n, doubl
         if (jj & 1) pv[0][1] -= dr;
         else pv[0][0] -= dr;
         if (Gs != nullptr && q == 0 && cl < jj) Gs[cl * 8 + jj] = scl * fma(h.scale, d, rj);
-        scl = (cl == jj) ? h.scale : scl;
+        scl = (cl == jj) ? sx : scl;
         if (lane == 0) {
             taus[8 * p + jj] = h.tau;
             betas[8 * p + jj] = h.beta;

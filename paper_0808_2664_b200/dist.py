@@ -11,10 +11,17 @@ R coordinates per round, apply Q (its inverse) the same between the group heads;
 form Q needs no communication (every rank holds the
 node factors on its root-to-leaf path).
 
-The round logic is written once (`RankState`) and driven either by
-torch.distributed (`factor`, `apply_qt`) or, for tests, by an in-process
-loopback over virtual ranks (`*_virtual`).  The arithmetic is the engine's:
-`CudaEngine` calls libtsqr.so; tests substitute an oracle-backed engine.
+Product path (NCCL process group, the default engine): a thin caller of the
+C-ABI's communicator layer -- rank 0's NCCL unique id is broadcast over the
+process group, every rank joins a libtsqr context (tsqr_ctx_set_comm), and each
+operation is ONE collective C call that runs every round inside the library
+(grouped ncclSend/ncclRecv on the call's stream; `CtxState`).
+
+Test path: the same round logic written in Python (`RankState`), driven by
+torch.distributed point-to-point (gloo, `factor`, `apply_qt`) or by an
+in-process loopback over virtual ranks (`*_virtual`), with the arithmetic of an
+engine: `CudaEngine` calls libtsqr.so's per-round entry points; the CPU tests
+substitute an oracle-backed engine.
 """
 from __future__ import annotations
 
@@ -145,6 +152,39 @@ class RankState:
         self.engine.cross_apply_q(self.tree, rnd, mine, recv, C)
 
 
+@dataclass
+class CtxState:
+    """A factor done by the C communicator layer (tsqr_ctx_factor): R replicated."""
+    ctx: object
+    tree: object
+    R: object
+    rank: int
+    nranks: int
+    top: object = None
+
+
+_CTX = {}
+
+
+def nccl_ctx(group=None):
+    """The libtsqr context of this process for `group` (NCCL backend), created once:
+    rank 0's ncclUniqueId is broadcast over the group, then every rank joins."""
+    import torch.distributed as dist
+    key = id(group)
+    if key not in _CTX:
+        rank, nranks = dist.get_rank(group), dist.get_world_size(group)
+        box = [api.Ctx.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0, group=group)
+        _CTX[key] = api.Ctx(torch.cuda.current_device()).set_comm(box[0], nranks, rank)
+    return _CTX[key]
+
+
+def _use_ctx(engine, group, cross) -> bool:
+    import torch.distributed as dist
+    return (engine is None or type(engine) is CudaEngine) and cross == "butterfly" and \
+        dist.get_backend(group) == "nccl"
+
+
 def _exchange(send: torch.Tensor, partner: int, group=None) -> torch.Tensor:
     import torch.distributed as dist
     if send.is_cuda and dist.get_backend(group) == "gloo":
@@ -180,6 +220,11 @@ def factor(A_local, block_rows: int, tile_rows: int = 0, engine=None, group=None
     packed leaf R's, the rounds recomputed locally; bitwise the same R and tree state)."""
     import torch.distributed as dist
     rank, nranks = dist.get_rank(group), dist.get_world_size(group)
+    if _use_ctx(engine, group, cross):             # product path: one collective C call
+        ctx = nccl_ctx(group)
+        R, t = ctx.factor(A_local, block_rows, tile_rows, tree=tree,
+                          stage_timing=bool(engine is not None and engine.stage_timing))
+        return CtxState(ctx, t, R, rank, nranks)
     st = RankState(engine or CudaEngine(), rank, nranks)
     st.factor_local(A_local, block_rows, tile_rows, tree)
     if cross == "allgather":
@@ -197,6 +242,10 @@ def factor(A_local, block_rows: int, tile_rows: int = 0, engine=None, group=None
 
 def apply_qt(st: RankState, C_local, group=None):
     """Collective: C_local <- rows of Q^T C (tree order); st.top = Q_thin^T C on every rank."""
+    if isinstance(st, CtxState):
+        st.top = torch.empty((C_local.shape[0], st.R.shape[0]), dtype=torch.float64, device=C_local.device)
+        st.ctx.apply_qt(st.tree, C_local, st.top)
+        return C_local, st.top
     st.apply_local(C_local)
     for rnd in range(1, rounds_of(st.nranks) + 1):
         partner = st.rank ^ (1 << (rnd - 1))
@@ -207,6 +256,8 @@ def apply_qt(st: RankState, C_local, group=None):
 
 def apply_q(st: RankState, C_local, group=None):
     """Collective: C_local <- rows of Q C, C in tree order (the inverse of apply_qt)."""
+    if isinstance(st, CtxState):
+        return st.ctx.apply_q(st.tree, C_local)
     for rnd in range(rounds_of(st.nranks), 0, -1):
         send = st.apply_q_send(rnd, C_local)
         if send is None:
@@ -219,6 +270,8 @@ def apply_q(st: RankState, C_local, group=None):
 
 def form_q(st: RankState):
     """Local (communication-free) explicit Q rows of this rank."""
+    if isinstance(st, CtxState):
+        return st.ctx.form_q(st.tree)
     return st.engine.form_q(st.tree)
 
 

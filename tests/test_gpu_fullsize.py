@@ -1,7 +1,9 @@
 """GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py
 times (its block rows b and tile rows s).  C2 and C3 are compared with the CPU
-oracle element by element (the oracle finishes them in seconds); C4 and C5
-(8.6 GB each) are checked through properties that hold at any size, computed
+oracle element by element (the oracle finishes them in seconds).  C4 and C5
+(8.6 GB each): R against the oracle run on every host core (leaves in parallel,
+orc_tsqr_factor_mt), both in the kernel's plan and in the paper's plain plan (one
+DGEQR2 per 4096-row block), plus properties that hold at any size, computed
 with plain PyTorch fp64 on the GPU from the untouched input:
   R^T R = A^T A (Cor. 1 identity), ||A - QR||/||A||, ||Q^T Q - I||,
   column norms of Q^T C equal those of C (Q orthogonal), and the thin part
@@ -39,6 +41,23 @@ def _cfg(name):
 
 def _c(m, n, b, s):
     return T.plan_info(m, n, block_rows=b, tile_rows=s)["chunk_rows"]
+
+
+THREADS = max(1, os.cpu_count() or 1)
+
+
+def _oracle_r_full(A_dev, p):
+    """R of the oracle's TSQR over plan p, on a host copy of A_dev (column-major (n, m)),
+    leaves in parallel on every host core; the copy is factored in place."""
+    Ah = A_dev.cpu().numpy().T                    # Fortran-ordered m x n view of the copy
+    f = orc.tsqr_factor(Ah, p, threads=THREADS, overwrite=True, keep_y1=False)
+    del Ah
+    return f.R
+
+
+def _sign_q(R, Q):
+    s = np.where(np.diag(R) < 0, -1.0, 1.0)
+    return Q * s[None, :]
 
 
 def _check_reflectors(F, tree, p, f, n):
@@ -104,6 +123,47 @@ def _gram_check(A, R):
     G = A @ A.T                                   # A^T A of the m x n matrix
     Rm = R.T                                      # the matrix R
     return (torch.linalg.norm(Rm.T @ Rm - G) / torch.linalg.norm(A) ** 2).item()
+
+
+def test_full_c2_plain_plan():
+    """C2 R and Q against the oracle's plain paper plan (one DGEQR2 per 4096-row block,
+    the binary tree over the 245 blocks): plan-independent."""
+    m, n, b, s, _ = _cfg("c2")
+    At = inputs.gaussian(m, n, 0)
+    A0 = _np(At).copy()
+    Ad = At.cuda()
+    R, tree = T.factor(Ad, b, s)
+    Q = T.form_q(tree)
+    torch.cuda.synchronize()
+    f = orc.tsqr_factor(A0, orc.plan(m, n, b, 0, 1, 0), threads=THREADS)
+    Rg, Qg = _np(R), _np(Q)
+    assert orc.rel_fro(orc.sign_normalise(Rg), orc.sign_normalise(f.R)) <= TOL_R
+    assert orc.rel_fro(_sign_q(Rg, Qg), _sign_q(f.R, orc.tsqr_form_q(f))) <= TOL_R
+    tree.free()
+
+
+@pytest.mark.parametrize("cfg", ["c4", "c5"])
+def test_full_r_parity_oracle(cfg):
+    """north_star: GPU R within 1e-11 (relative Frobenius, rows sign-normalised) of the
+    oracle's R at the full C4 (kappa = 1e10) and C5 sizes, in the kernel's plan and in
+    the plain plan."""
+    m, n, b, s, _ = _cfg(cfg)
+    if cfg == "c4":
+        A = inputs.conditioned_rows(0, m, n, 0, 1e10, 2, "cuda")
+    else:
+        A = inputs.gaussian_rows(0, m, n, 0, "cuda")
+    Ad = A.clone()
+    R, tree = T.factor(Ad, b, s)
+    torch.cuda.synchronize()
+    Rg = orc.sign_normalise(_np(R))
+    tree.free()
+    del Ad
+    torch.cuda.empty_cache()
+    for p in (orc.plan(m, n, b, s, 1, _c(m, n, b, s)), orc.plan(m, n, b, 0, 1, 0)):
+        Ro = _oracle_r_full(A, p)
+        err = orc.rel_fro(Rg, orc.sign_normalise(Ro))
+        print(f"{cfg} R vs oracle (c={p.c}, {p.ntiles} leaves): {err:.3e}")
+        assert err <= TOL_R
 
 
 def test_full_c4_invariants():

@@ -33,7 +33,7 @@ def test_library_is_sm100a():
 
 def test_status_strings():
     L = _lib.lib()
-    for s in range(6):
+    for s in range(7):
         assert len(L.tsqr_status_string(s)) > 0
 
 
