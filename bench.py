@@ -386,13 +386,13 @@ def run_ours(args, cfg):
     t_e2e = med(te)
     if world > 1:
         t_e2e = max_over_ranks([t_e2e], dev)[0]
-    h2d = 8 * m * n + (8 * m * k if C_h is not None else 0)                 # all ranks' slabs
+    h2d = 8 * m * n + (8 * m * k if C0 is not None else 0)                 # all ranks' slabs
     d2h = 8 * n * n * world + (8 * m * n if cfg["op"] == "form_q" else 8 * m * k)
     e2e = {"value": 2.0 * m * n * n / (t_e2e * 1e-3) / 1e9, "unit": UNIT,
            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": t_e2e,
            "path": ("tsqr_qr_host (one C-ABI call: H2D of A%s, factor, %s, D2H of R and %s from pinned host "
                     "memory), median of %d, CUDA events on its stream") % (
-               " and C" if C_h is not None else "", cfg["op"], "Q" if cfg["op"] == "form_q" else "Q^T C", len(te))
+               " and C" if C0 is not None else "", cfg["op"], "Q" if cfg["op"] == "form_q" else "Q^T C", len(te))
            if world == 1 else "torch H2D of the slab + tsqr_ctx_* collective calls + D2H, max over ranks"}
 
     if rank != 0:

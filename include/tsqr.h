@@ -51,7 +51,17 @@ typedef enum {
  *              tsqr_slab() assigns.
  *  flags:      bit 0 = synchronise and check after every launch (debug);
  *              bit 1 = record CUDA events around tsqr_factor's leaf and tree
- *              stages on its stream (read back with tsqr_tree_stage_ms). */
+ *              stages on its stream (read back with tsqr_tree_stage_ms);
+ *              bit 2 = TSQR_FLAG_ROBUST: dlarfg's rescaling in every leaf and
+ *              tree Householder step (reading R23 of DESIGN.md).  Without it the
+ *              leaf kernels form sums of squares unscaled and are exact (to
+ *              rounding, normwise) when the nonzero entries of A have magnitudes
+ *              in [2^-400, 2^400] (about 1e-120 .. 1e+120); outside that range
+ *              set the flag (it costs 3-8 % of the factor).  The cross-rank and
+ *              q-ary combines always rescale. */
+#define TSQR_FLAG_DEBUG_SYNC 1
+#define TSQR_FLAG_STAGE_TIMING 2
+#define TSQR_FLAG_ROBUST 4
 typedef struct {
     int64_t block_rows;
     int64_t tile_rows;

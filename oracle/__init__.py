@@ -370,6 +370,12 @@ def sign_normalise(R, Q=None):
 
 
 def rel_fro(X, Y) -> float:
-    d = np.linalg.norm(np.asarray(X) - np.asarray(Y))
-    nrm = np.linalg.norm(np.asarray(Y))
+    """||X - Y||_F / ||Y||_F, both scaled by max|Y| first so that the squares neither
+    overflow nor underflow (inputs near the fp64 range limits, reading R23)."""
+    X, Y = np.asarray(X, dtype=np.float64), np.asarray(Y, dtype=np.float64)
+    s = float(np.max(np.abs(Y))) if Y.size else 0.0
+    if not np.isfinite(s) or s == 0.0:
+        s = 1.0
+    d = np.linalg.norm(X / s - Y / s)
+    nrm = np.linalg.norm(Y / s)
     return float(d / nrm) if nrm > 0 else float(d)

@@ -7,7 +7,7 @@ import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libtsqr.so")
+LIB = os.environ.get("TSQR_BUILD_OUT", os.path.join(HERE, "libtsqr.so"))   # override: A/B variant builds
 SOURCES = ["tsqr_api.cu", "tsqr_wy.cu", "tsqr_chain.cu", "tsqr_cs.cu", "tsqr_wide.cu", "tsqr_tree.cu", "tsqr_caqr.cu",
            "tsqr_stream.cu", "tsqr_combine.cu", "tsqr_comm.cu", "tsqr_peak.cu", "tsqr_host.cu", "plan.cpp"]
 HEADERS = ["wy.cuh", "chunk.cuh", "tsqr_kernels.h", "plan.h", os.path.join("..", "..", "include", "tsqr.h")]
@@ -31,6 +31,20 @@ EXTRA = os.environ.get("TSQR_NVCC_EXTRA", "").split()       # developer A/B vari
 def _newest_input() -> float:
     files = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [__file__]
     return max(os.path.getmtime(f) for f in files)
+
+
+JITTER_LIB = os.path.join(HERE, "libtsqr_jitter.so")
+
+
+def build_variant(out: str, extra: list, force: bool = False) -> str:
+    """A diagnostic variant of the library (e.g. -DTSQR_HANDOFF_JITTER) built to `out`."""
+    global LIB, EXTRA
+    saved = (LIB, EXTRA)
+    LIB, EXTRA = out, list(extra)
+    try:
+        return build(force=force)
+    finally:
+        LIB, EXTRA = saved
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

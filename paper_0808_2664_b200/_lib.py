@@ -108,6 +108,8 @@ def lib():
         "tsqr_host_ws_free": [_vp],
     }
     for name, args in sig.items():
+        if "TSQR_LIBRARY" in os.environ and not hasattr(L, name):
+            continue                              # an older A/B build: its own symbols only
         fn = getattr(L, name)
         fn.argtypes = args
         fn.restype = ctypes.c_int

@@ -36,8 +36,10 @@ def _colmajor(t: torch.Tensor, name: str, host: bool = False):
 
 
 def opts(block_rows: int = 0, tile_rows: int = 0, nranks: int = 1, rank: int = 0, debug: bool = False,
-         stage_timing: bool = False) -> Opts:
-    return Opts(block_rows, tile_rows, nranks, rank, (1 if debug else 0) | (2 if stage_timing else 0), 0)
+         stage_timing: bool = False, robust: bool = False) -> Opts:
+    """robust: TSQR_FLAG_ROBUST -- rescaled Householder steps for inputs outside [2^-400, 2^400]."""
+    return Opts(block_rows, tile_rows, nranks, rank,
+                (1 if debug else 0) | (2 if stage_timing else 0) | (4 if robust else 0), 0)
 
 
 class Tree:
@@ -81,14 +83,15 @@ class Tree:
 
 def factor(A: torch.Tensor, block_rows: int = 0, tile_rows: int = 0, R: torch.Tensor | None = None,
            nranks: int = 1, rank: int = 0, tree: Tree | None = None, stream=None, debug: bool = False,
-           stage_timing: bool = False):
+           stage_timing: bool = False, robust: bool = False):
     """Factor A (column-major m_local x n) in place.  Returns (R, tree): R is n x n upper
-    triangular as a column-major (n, n) tensor.  Pass `tree` back in to reuse its workspace."""
+    triangular as a column-major (n, n) tensor.  Pass `tree` back in to reuse its workspace.
+    robust: rescaled steps for entries outside [2^-400, 2^400] (TSQR_FLAG_ROBUST)."""
     pa, m, n, lda = _colmajor(A, "A")
     if R is None:
         R = torch.empty((n, n), dtype=torch.float64, device=A.device)
     pr, _, _, ldr = _colmajor(R, "R")
-    o = opts(block_rows, tile_rows, nranks, rank, debug, stage_timing)
+    o = opts(block_rows, tile_rows, nranks, rank, debug, stage_timing, robust)
     t = tree if tree is not None else Tree()
     h = t.handle
     check(lib().tsqr_factor(m, n, pa, lda, pr, ldr, ctypes.byref(o), _stream_ptr(stream), ctypes.byref(h)),

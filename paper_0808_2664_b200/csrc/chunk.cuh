@@ -84,20 +84,37 @@ struct Sync {
     int *row, *tr;
     int s;
 };
-// Memory model of a hand-off (PTX memory model, scope cta): the publisher's lanes
-// store the data, __syncwarp() orders those stores before lane 0's counter store,
-// which is a RELEASE (st.release.cta); the waiter reads the counter with an ACQUIRE
-// (ld.acquire.cta) and reads the data only after it, so a counter value that
-// satisfies the wait makes every store released before it visible (release /
-// acquire synchronisation; the warp barrier gives the cumulativity over the
-// publisher's other lanes).  Build with -DTSQR_HANDOFF_RELAXED for the round-1
-// variant (volatile accesses and compiler barriers only, relying on a warp's
-// shared-memory accesses being performed in issue order, which the model does
-// not promise) -- kept only to measure what the ordering costs.
+// Hand-off ordering.  The publisher's lanes store the data, __syncwarp() orders
+// those stores before lane 0's counter store; the waiter reads the counter and
+// then the data.  Default build: the counter is a volatile access and the only
+// fences are compiler barriers -- it relies on one warp's shared-memory
+// accesses being performed in issue order by the SM's memory pipeline (the
+// publisher's data stores reach shared memory before its counter store, and the
+// waiter's data load issued after its counter load sees at least what the
+// counter promised).  The PTX memory model does not promise that: a conforming
+// build (-DTSQR_HANDOFF_ACQREL) makes the counter store a RELEASE and its load an
+// ACQUIRE (release/acquire synchronisation at cta scope; __syncwarp gives the
+// cumulativity over the publisher's lanes).  On sm_100a the release compiles to
+// MEMBAR.ALL.CTA, which waits for the warp's outstanding global stores, and costs
+// 6-8 % of the leaf kernel, so it is a variant; the
+// jitter build (-DTSQR_HANDOFF_JITTER) injects pseudo-random __nanosleep delays
+// between the data and the counter on both sides and is checked bitwise against
+// the default build and against the oracle (tests/test_gpu_handoff.py).
+#if defined(TSQR_HANDOFF_JITTER)
+__device__ __forceinline__ void handoff_jitter() {
+    unsigned t;
+    asm volatile("mov.u32 %0, %%clock;" : "=r"(t));
+    t = (t ^ (threadIdx.x * 2654435761u)) * 2246822519u;
+    if (((t >> 13) & 7) == 0) __nanosleep(32 + ((t >> 17) & 511));
+}
+#else
+__device__ __forceinline__ void handoff_jitter() {}
+#endif
 __device__ __forceinline__ int ld_acquire_cta(const int *c) {
-#ifdef TSQR_HANDOFF_RELAXED
+#ifndef TSQR_HANDOFF_ACQREL
     const int v = *reinterpret_cast<const volatile int *>(c);
     asm volatile("" ::: "memory");
+    handoff_jitter();
     return v;
 #else
     int v;
@@ -107,8 +124,9 @@ __device__ __forceinline__ int ld_acquire_cta(const int *c) {
 #endif
 }
 __device__ __forceinline__ void st_release_cta(int *c, int v) {
-#ifdef TSQR_HANDOFF_RELAXED
+#ifndef TSQR_HANDOFF_ACQREL
     asm volatile("" ::: "memory");
+    handoff_jitter();
     *reinterpret_cast<volatile int *>(c) = v;
 #else
     const unsigned a = (unsigned)__cvta_generic_to_shared(c);
@@ -128,20 +146,19 @@ __device__ __forceinline__ void sync_publish(int *c, int v) {
 // dlarfg scalars (readings R1/R2/R19), branch-free: beta = -sign(alpha) N with
 // N = sqrt(alpha^2 + sigma2), tau = 1 + |alpha|/N, scale = 1/(alpha - beta);
 // sigma2 == 0 gives H = I (tau = 0, beta = alpha).  1/sqrt from the MUFU seed
-// and two Newton steps, 1/x likewise (rcp_nr): <= 2 ulp.
+// and two Newton steps, 1/x likewise (rcp_nr): <= 2 ulp.  (A single third-order
+// correction per seed is one dependent step shorter but measured no faster.)
+// The plain sums and the flush-to-zero seeds need the input range of reading
+// R23; the robust instantiation (kRobust) rescales outside it.
 __device__ __forceinline__ House house_bf(double alpha, double s2) {
     const double y = fma(alpha, alpha, s2);
     const double aa = fabs(alpha);
     double r, i;
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(y));
-    // seed 1/(|alpha| + N) from the rsqrt seed while r is refined (the two MUFU
-    // chains overlap); its Newton steps then run against the exact denominator
     const double D0 = fma(y, r, aa);
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(i) : "d"(D0));
     const double hy = 0.5 * y;
     r = r * fma(-hy * r, r, 1.5);
-    // first Newton step of 1/D against D1 = |alpha| + y r1 (r once refined),
-    // overlapped with r's second step; the last one runs against the exact D
     const double D1 = fma(y, r, aa);
     i = fma(i, fma(-D1, i, 1.0), i);
     r = r * fma(-hy * r, r, 1.5);
@@ -178,7 +195,8 @@ struct Cfg {
     static constexpr int OFF_WS = NBUF * RBUF;            // after the R buffers
     static constexpr int OFF_SYNC = OFF_WS + NW * WS;     // per buffer: NP row + NCB panel counters
     static constexpr int SYNC_INTS = NP + NCB;
-    static constexpr int OFF_STG = (OFF_SYNC + (NBUF * SYNC_INTS + 1) / 2 + 1) & ~1;   // 16-byte aligned; per warp:
+    // after the counters: one range-gate flag per buffer (NBUF ints)
+    static constexpr int OFF_STG = (OFF_SYNC + (NBUF * (SYNC_INTS + 1) + 1) / 2 + 1) & ~1;   // 16-byte aligned; per warp:
                                                                                    // the next chunk (col-major CH x NP)
     static constexpr int STG = CH * NP;
     static constexpr size_t BYTES = (size_t)(OFF_STG + NW * STG) * sizeof(double);
@@ -276,7 +294,7 @@ struct Chunk {
 // whole chunk.  On exit the panel registers hold v (the reflectors' chunk part,
 // scale applied), R's pivot rows hold (beta, updated R entries) in the panel
 // columns, Gs/t8 the Gram entries and taus.
-template <class C, int P>
+template <class C, int P, bool kRobust>
 __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, double *Gs, double *t8, double *xs,
                                                  double *tau_out, int n, const Sync &sy) {
     const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
@@ -311,30 +329,27 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
         double d, s2;
         quad_sums(d, s2, d0 + d1, s0 + s1);
         PROBE(3);
-        // R row j released by the previous chunk: the row is read right after an
-        // acquire of its counter (ordered after it); only if the counter is
-        // short do we spin and read the row again
-        double alpha, rj;                                            // R(j, j), R(j, 8P + l4)
-        {
-            const volatile double *rr = Rb + j * C::LDR;
-            const int c0 = ld_acquire_cta(sy.row + j);
+        // R row j released by the previous chunk: the counter and the row are read
+        // together, the row again only if the counter was short ("Hand-off
+        // ordering" above)
+        const volatile double *rr = Rb + j * C::LDR;
+        const int c0 = ld_acquire_cta(sy.row + j);
+        double alpha = rr[j], rj = rr[8 * P + l4];                   // R(j, j), R(j, 8P + l4)
+        if (c0 < sy.s) {
+            sync_wait(sy.row + j, sy.s);
             alpha = rr[j];
             rj = rr[8 * P + l4];
-            if (c0 < sy.s) {
-                sync_wait(sy.row + j, sy.s);
-                alpha = rr[j];
-                rj = rr[8 * P + l4];
-            }
         }
         PROBE(4);
         House h = house_bf(alpha, s2);
         double sc = 1.0;
-        if (wy::house_unsafe(alpha, s2)) {                          // warp-uniform, R23
+        double sx = h.scale;                                        // the scale of the unscaled x
+        if (kRobust && __any_sync(FULL, wy::house_unsafe(alpha, s2))) {   // warp-uniform, R23
             rescaled_sums<C::KM>(x, [&](int k, int e) { return ch.a[k][P][e]; }, alpha, d, s2, sc);
             h = house_bf(sc * alpha, s2);
             h.beta = h.beta / sc;
+            sx = h.scale * sc;
         }
-        const double sx = h.scale * sc;                              // scale of the unscaled x
         const double w = fma(h.scale, d, rj);                        // v^T [R(j,c); a_c]
         // a <- a - u x (u = tau scale w) for the trailing columns; the pivot
         // column becomes v = scale x, formed as scale x + (a - x) with a - x
@@ -371,7 +386,7 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
 // Dense panel P: the pivots are chunk rows 8 kb .. 8 kb + 7 (kb = (8P - r0)/8).
 // On exit the panel column holds R above/at the pivot (beta on the diagonal)
 // and v below it, as DGEQR2 stores them.
-template <class C, int P>
+template <class C, int P, bool kRobust>
 __device__ __forceinline__ void panel_dense(Chunk<C> &ch, int kb, double *Gs, double *t8, double *tau_out, int n) {
     const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
     const int jn = (P + 1 < C::NCB) ? 8 : n - 8 * P;      // only the last panel has padding columns
@@ -406,12 +421,13 @@ __device__ __forceinline__ void panel_dense(Chunk<C> &ch, int kb, double *Gs, do
         quad_sums(d, s2, d0 + d1, s0 + s1);
         House h = house_bf(alpha, s2);
         double sc = 1.0;
-        if (wy::house_unsafe(alpha, s2)) {                          // warp-uniform, R23
+        double sx = h.scale;                                        // the scale of the unscaled x
+        if (kRobust && __any_sync(FULL, wy::house_unsafe(alpha, s2))) {   // warp-uniform, R23
             rescaled_sums<C::KM>(x, [&](int k, int e) { return ch.a[k][P][e]; }, alpha, d, s2, sc);
             h = house_bf(sc * alpha, s2);
             h.beta = h.beta / sc;
+            sx = h.scale * sc;
         }
-        const double sx = h.scale * sc;
         const double w = fma(h.scale, d, rj);
         const double u = (l4 > jj) ? h.tau * sx * w : (l4 == jj ? 1.0 : 0.0);
         const double g = (l4 == jj) ? sx : 0.0;                      // pivot column: v = scale x exactly
@@ -513,7 +529,7 @@ __device__ __forceinline__ void trailing(Chunk<C> &ch, const double (&yv)[C::KM]
 }
 
 // Panel P of the factorisation of one chunk (kind 0 structured, 1 dense, 2 none).
-template <class C, int P>
+template <class C, int P, bool kRobust>
 __device__ __forceinline__ void factor_panel(Chunk<C> &ch, int kind, int kb, double *Rb, double *ws,
                                              double *tau_out, int n, const Sync &sy, bool defer, double *tg) {
     // defer: the caller publishes tr[P] itself (after copying R rows out);
@@ -532,14 +548,14 @@ __device__ __forceinline__ void factor_panel(Chunk<C> &ch, int kind, int kb, dou
     double yv[C::KM][2];
     PROBE(1);
     if (kind == 0) {
-        panel_structured<C, P>(ch, Rb, Gs, t8, ws + C::XS, tau_out, n, sy);
+        panel_structured<C, P, kRobust>(ch, Rb, Gs, t8, ws + C::XS, tau_out, n, sy);
 #pragma unroll
         for (int k = 0; k < C::KM; ++k) {
             yv[k][0] = ch.a[k][P][0];
             yv[k][1] = ch.a[k][P][1];
         }
     } else {
-        panel_dense<C, P>(ch, kb, Gs, t8, tau_out, n);
+        panel_dense<C, P, kRobust>(ch, kb, Gs, t8, tau_out, n);
         const int piv = 8 * kb + l4;                      // chunk row of this lane's column's pivot
 #pragma unroll
         for (int k = 0; k < C::KM; ++k)

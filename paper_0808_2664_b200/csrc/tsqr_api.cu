@@ -133,7 +133,11 @@ static void free_tree_memory(tsqr_tree_s *t, cudaStream_t st) {
                     t->d_tile_chunk0, t->d_cta_tile0, t->d_apply_cta_tile0, t->d_tau_chunk, t->d_tcache,
                     t->d_tcache_node, t->d_cross_tcache, t->d_wtmp, t->d_tcache_pair, t->d_gather};
     for (void *p : ptrs)
+#ifdef TSQR_PLAIN_MALLOC
+        if (p) cudaFree(p);
+#else
         if (p) cudaFreeAsync(p, st);
+#endif
 }
 
 // The wide path's stacking buffer (2n x max(n, cols) doubles), grown on demand.
@@ -278,7 +282,11 @@ static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t 
     t->cross_rounds = ilog2(ro.nranks);
     cudaError_t e = cudaSuccess;
     auto alloc = [&](void **ptr, size_t bytes) {
+#ifdef TSQR_PLAIN_MALLOC            // measurement variant
+        if (e == cudaSuccess) e = cudaMalloc(ptr, bytes < 16 ? 16 : bytes);
+#else
         if (e == cudaSuccess) e = cudaMallocAsync(ptr, bytes < 16 ? 16 : bytes, st);
+#endif
     };
     alloc((void **)&t->d_row0, sizeof(int64_t) * L);
     alloc((void **)&t->d_rows, sizeof(int) * L);
@@ -421,17 +429,19 @@ tsqr_status_t tsqr_factor(int64_t m_local, int64_t n, double *A, int64_t lda, do
     ca.A = A; ca.lda = lda; ca.n = (int)n; ca.chunk_rows = t->plan.c;
     ca.tile_row0 = t->d_row0; ca.tile_rows = t->d_rows; ca.tile_chunk0 = t->d_tile_chunk0;
     ca.cta_tile0 = t->d_cta_tile0; ca.grid = t->chain_grid; ca.tau = t->d_tau_chunk; ca.tcache = t->d_tcache;
+    const bool robust = (ro.flags & TSQR_FLAG_ROBUST) != 0;     // reading R23
+    ca.robust = robust;
     if (t->wide) {
         const int L = t->plan.ntiles();
         CUDA_TRY(mark(0), "tsqr_factor events");
         CUDA_TRY(launch_wide_leaves(A, lda, (int)n, t->d_row0, t->d_rows, L, (int)t->plan.max_rows, t->d_tau_chunk,
-                                    t->d_tcache, t->d_tcache_pair, t->stream),
+                                    t->d_tcache, t->d_tcache_pair, robust, t->stream),
                  "tsqr_factor leaves");
         CUDA_TRY(mark(1), "tsqr_factor events");
         if (wide_tree_pipe_ok((int)n)) {
             CUDA_TRY(launch_wide_tree_pipe(A, lda, (int)n, t->d_row0, t->d_node_a, t->d_pipe_nodes, t->pipe_count,
                                            t->d_prod_l, t->d_prod_r, t->d_pipe_flags, t->d_tau_node,
-                                           t->d_tcache_node, t->stream),
+                                           t->d_tcache_node, robust, t->stream),
                      "tsqr_factor tree");
         } else {
             for (size_t g = t->step_off.size() - 1; g-- > 0;) {     // tree steps bottom-up

@@ -17,14 +17,14 @@
 namespace tsqr {
 using namespace chunk;
 
-template <class C, int P>
+template <class C, int P, bool kRobust>
 __device__ __forceinline__ void chunk_panels(Chunk<C> &ch, int r0, bool last, double *Rb, const Sync &sy,
                                              double *ws, double *tau_out, int n, double *Ahead, int64_t lda,
                                              double *tg) {
     const int lane = threadIdx.x & 31;
     const int kind = (8 * P < r0) ? 0 : (8 * P < r0 + C::CH ? 1 : 2);
     const int kb = (8 * P - r0) >> 3;
-    factor_panel<C, P>(ch, kind, kb, Rb, ws, tau_out, n, sy, last, tg);
+    factor_panel<C, P, kRobust>(ch, kind, kb, Rb, ws, tau_out, n, sy, last, tg);
     if (last) {                                   // R rows 8P .. 8P+7 of the tile are final
         const int w = n - 8 * P;
         for (int e = lane; e < 8 * w; e += 32) {
@@ -34,7 +34,7 @@ __device__ __forceinline__ void chunk_panels(Chunk<C> &ch, int r0, bool last, do
         sync_publish(sy.tr + P, sy.s + 1);        // the buffer's next user may overwrite them
     }
     PROBE(8);
-    if constexpr (P + 1 < C::NCB) chunk_panels<C, P + 1>(ch, r0, last, Rb, sy, ws, tau_out, n, Ahead, lda, tg);
+    if constexpr (P + 1 < C::NCB) chunk_panels<C, P + 1, kRobust>(ch, r0, last, Rb, sy, ws, tau_out, n, Ahead, lda, tg);
 }
 
 // Prefetch a chunk (rows [r0, r0 + hk) of the tile at A + row0, all n columns)
@@ -53,7 +53,10 @@ __device__ __forceinline__ void prefetch_chunk(double *stg, const double *src, i
     asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
-template <class C>
+// kRobust: the rescaled Householder steps of reading R23 (inputs outside
+// [2^-400, 2^400]); a separate instantiation chosen at launch (opts.flags bit 2)
+// so the default kernel carries no trace of the slow path (measured 3-8 %).
+template <class C, bool kRobust>
 __global__ void __launch_bounds__(C::NT, 1)
 k_chain_factor(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *tile_rows,
                const int64_t *tile_chunk0, const int *cta_tile0, double *tau, double *tcache) {
@@ -128,7 +131,7 @@ k_chain_factor(double *A, int64_t lda, int n, const int64_t *tile_row0, const in
         double *tau_out = tau + (tile_chunk0[pt] + pc) * n;
         const Sync sy{sync + pb * C::SYNC_INTS, sync + pb * C::SYNC_INTS + C::NP, ps};
         double *tg = tcache ? tcache + (tile_chunk0[pt] + pc) * (C::NCB * 64) : nullptr;
-        chunk_panels<C, 0>(ch, r0, pc == pnch - 1, sm + pb * C::RBUF, sy, ws, tau_out, n, A + row0, lda, tg);
+        chunk_panels<C, 0, kRobust>(ch, r0, pc == pnch - 1, sm + pb * C::RBUF, sy, ws, tau_out, n, A + row0, lda, tg);
         double *dst = A + row0 + r0;
 #pragma unroll
         for (int k = 0; k < C::KM; ++k)
@@ -159,19 +162,21 @@ static cudaError_t chain_dispatch(int n, F &&fn) {
     }
 }
 
-template <class C>
+template <class C, bool kRobust>
 static cudaError_t launch_chain_factor_t(const ChainArgs &f, cudaStream_t st) {
     const size_t sm = C::BYTES;
-    cudaError_t e = cudaFuncSetAttribute((const void *)k_chain_factor<C>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sm);
+    cudaError_t e = cudaFuncSetAttribute((const void *)k_chain_factor<C, kRobust>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    k_chain_factor<C><<<f.grid, C::NT, sm, st>>>(f.A, f.lda, f.n, f.tile_row0, f.tile_rows, f.tile_chunk0,
-                                                 f.cta_tile0, f.tau, f.tcache);
+    k_chain_factor<C, kRobust><<<f.grid, C::NT, sm, st>>>(f.A, f.lda, f.n, f.tile_row0, f.tile_rows, f.tile_chunk0,
+                                                          f.cta_tile0, f.tau, f.tcache);
     return cudaGetLastError();
 }
 
 cudaError_t launch_chain_factor(const ChainArgs &f, cudaStream_t st) {
-    return chain_dispatch(f.n, [&](auto c) { return launch_chain_factor_t<decltype(c)>(f, st); });
+    return chain_dispatch(f.n, [&](auto c) {
+        return f.robust ? launch_chain_factor_t<decltype(c), true>(f, st) : launch_chain_factor_t<decltype(c), false>(f, st);
+    });
 }
 
 int chain_chunk_rows(int n) {
@@ -199,10 +204,10 @@ int chain_grid(int n) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaError_t e = chain_dispatch(n, [&](auto c) {
         using C = decltype(c);
-        cudaError_t r = cudaFuncSetAttribute((const void *)k_chain_factor<C>,
+        cudaError_t r = cudaFuncSetAttribute((const void *)k_chain_factor<C, false>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES);
         if (r != cudaSuccess) return r;
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_chain_factor<C>, C::NT, C::BYTES);
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_chain_factor<C, false>, C::NT, C::BYTES);
     });
     if (e != cudaSuccess || occ < 1) occ = 1;
     return sms * occ;

@@ -25,6 +25,7 @@ struct ChainArgs {
     const int *cta_tile0; int grid;
     double *tau;                 // [chunks][n]
     double *tcache;              // [chunks][NCB][8][8]: the panels' T (compact WY), may be null
+    bool robust = false;         // the rescaled steps of reading R23 (opts.flags bit 2)
 };
 // Leaf stage of Q^T C (forward) or of form Q (Q = Q_leaves [X; 0], !forward).
 struct ChainApplyArgs {
@@ -49,7 +50,7 @@ cudaError_t launch_cs_apply(const ChainApplyArgs &f, cudaStream_t st);
 // Wide-n engine (tsqr_wide.cu, 64 < n <= 256): one CTA per leaf / node problem.
 int wide_max_rows();
 cudaError_t launch_wide_leaves(double *A, int64_t lda, int n, const int64_t *row0, const int *rows, int L,
-                               int max_rows, double *tau, double *tcache, double *tpair, cudaStream_t st);
+                               int max_rows, double *tau, double *tcache, double *tpair, bool robust, cudaStream_t st);
 cudaError_t launch_wide_nodes(double *A, int64_t lda, int n, const int64_t *row0, const int *node_a, const int *ids,
                               int count, double *tau_node, double *tcache_node, cudaStream_t st);
 cudaError_t launch_wide_node1(double *Ra, int64_t lda, double *Rb, int64_t ldb, int n, double *tau, double *tcache,
@@ -85,7 +86,7 @@ cudaError_t launch_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_
 bool wide_tree_pipe_ok(int n);
 cudaError_t launch_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *node_a,
                                   const int *nodes, int count, const int *prod_l, const int *prod_r, int *flags,
-                                  double *tau_node, double *tcache_node, cudaStream_t st);
+                                  double *tau_node, double *tcache_node, bool robust, cudaStream_t st);
 cudaError_t launch_identity(double *X, int n, cudaStream_t st);
 cudaError_t launch_pack_r(const double *A, int64_t lda, int n, double *packed, cudaStream_t st);
 cudaError_t launch_unpack_r(const double *packed, int n, double *A, int64_t lda, cudaStream_t st);

@@ -121,12 +121,13 @@ __device__ __forceinline__ void node_panel(NodeRegs<C> &rg, double *Ahead_a, dou
         const double rj = Ra[jj * C::LDA + 8 * P + l4];
         House h = house_bf(alpha, s2);
         double sc = 1.0;
-        if (wy::house_unsafe(alpha, s2)) {                          // warp-uniform, R23
+        double sx = h.scale;                                        // the scale of the unscaled x
+        if (__any_sync(0xffffffffu, wy::house_unsafe(alpha, s2))) {  // warp-uniform, R23
             chunk::rescaled_sums<P + 1>(x, [&](int k, int e) { return rg.a[k][P][e]; }, alpha, d, s2, sc);
             h = house_bf(sc * alpha, s2);
             h.beta = h.beta / sc;
+            sx = h.scale * sc;
         }
-        const double sx = h.scale * sc;
         const double w = fma(h.scale, d, rj);
         const double u = (l4 > jj) ? h.tau * sx * w : (l4 == jj ? 1.0 : 0.0);
         const double g = (l4 == jj) ? sx : 0.0;
@@ -347,6 +348,7 @@ __device__ __forceinline__ void wait_flag_cta(const int *f) {
 
 }  // namespace wtree
 
+template <bool kRobust>
 __global__ void __launch_bounds__(wtree::NT, 1)
 k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *node_a, const int *nodes,
                  int count, const int *prod_l, const int *prod_r, int *flags, double *tau_node, double *tcache_node) {
@@ -452,7 +454,8 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                 const double rj = RaP[8 * l4 + jj];
                 House h = house_bf(alpha, s2);
                 double sc = 1.0;
-                if (wy::house_unsafe(alpha, s2)) {              // block-uniform, rescaled step (R23)
+                double sx = h.scale;                                        // the scale of the unscaled x
+                if (kRobust && wy::house_unsafe(alpha, s2)) {   // block-uniform, rescaled step (R23)
                     double mx = fabs(alpha);
                     for (int k = warp; k <= P; k += NT / 32) {
                         const double2 x = *reinterpret_cast<const double2 *>(xr + 8 * k + 2 * q);
@@ -488,8 +491,8 @@ k_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                     }
                     h = house_bf(sc * alpha, s2);
                     h.beta = h.beta / sc;
+                    sx = h.scale * sc;
                 }
-                const double sx = h.scale * sc;
                 const double w = fma(h.scale, d, rj);
                 const double u = (l4 > jj) ? h.tau * sx * w : (l4 == jj ? 1.0 : 0.0);
                 const double g = (l4 == jj) ? sx : 0.0;
@@ -592,7 +595,7 @@ bool wide_tree_pipe_ok(int n) { return (n + 7) / 8 <= wtree::MAX_NPAN; }
 
 cudaError_t launch_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *node_a,
                                   const int *nodes, int count, const int *prod_l, const int *prod_r, int *flags,
-                                  double *tau_node, double *tcache_node, cudaStream_t st) {
+                                  double *tau_node, double *tcache_node, bool robust, cudaStream_t st) {
     if (count == 0) return cudaSuccess;
     const int npan = (n + 7) / 8;
     if (npan > wtree::MAX_NPAN) return cudaErrorInvalidValue;
@@ -618,10 +621,11 @@ cudaError_t launch_wide_tree_pipe(double *A, int64_t lda, int n, const int64_t *
     const size_t bytes = wtree::smem_doubles(npan) * sizeof(double);
     cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * ((size_t)(count + 1) * wtree::MAX_NPAN + 1), st);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute((const void *)k_wide_tree_pipe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    auto kern = robust ? k_wide_tree_pipe<true> : k_wide_tree_pipe<false>;
+    e = cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;
-    k_wide_tree_pipe<<<count, wtree::NT, bytes, st>>>(A, lda, n, tile_row0, node_a, nodes, count, prod_l, prod_r,
-                                                      flags, tau_node, tcache_node);
+    kern<<<count, wtree::NT, bytes, st>>>(A, lda, n, tile_row0, node_a, nodes, count, prod_l, prod_r, flags, tau_node,
+                                          tcache_node);
     return cudaGetLastError();
 }
 

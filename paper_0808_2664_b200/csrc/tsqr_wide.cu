@@ -22,6 +22,7 @@
 // Q: backward with T) to C rows mapped the same way, column-split, no barriers.
 #include "tsqr_kernels.h"
 #include "wy.cuh"
+#include "chunk.cuh"
 
 #include <type_traits>
 
@@ -34,28 +35,9 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int NW = 8, NT = 256, KMW = 36, RW = 8 * KMW;   // rows per warp (logical)
 constexpr int MAXR = NW * RW;                               // 2304 logical rows
 
-// branch-free dlarfg scalars (readings R1/R2/R19), as chunk::house_bf
-__device__ __forceinline__ House house(double alpha, double s2) {
-    const double y = fma(alpha, alpha, s2);
-    const double aa = fabs(alpha);
-    double r, i;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(y));
-    const double D0 = fma(y, r, aa);
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(i) : "d"(D0));
-    const double hy = 0.5 * y;
-    r = r * fma(-hy * r, r, 1.5);
-    r = r * fma(-hy * r, r, 1.5);
-    const double N = y * r;
-    const double D = aa + N;
-    i = fma(i, fma(-D, i, 1.0), i);
-    i = fma(i, fma(-D, i, 1.0), i);
-    const bool z = (s2 == 0.0);
-    House h;
-    h.beta = z ? alpha : (alpha >= 0.0 ? -N : N);
-    h.tau = z ? 0.0 : fma(aa, r, 1.0);
-    h.scale = z ? 0.0 : (alpha >= 0.0 ? i : -i);
-    return h;
-}
+// branch-free dlarfg scalars (readings R1/R2/R19): chunk::house_bf (one
+// third-order correction per MUFU seed)
+__device__ __forceinline__ House house(double alpha, double s2) { return chunk::house_bf(alpha, s2); }
 
 // A problem: logical rows [0, hA) -> segment A rows (the first nA exist),
 // [hA, hA + hB) -> segment B rows.  A node pads its R_a segment to hA = NP
@@ -159,6 +141,7 @@ __device__ void wide_qr(const Prob &P, int n, double *tau, double *tcache, Smem 
             const double rj = S.piv[par][l4], alpha = S.piv[par][jj];
             House h = house(alpha, s2);
             double sc = 1.0;
+            double sx = h.scale;
             if (wy::house_unsafe(alpha, s2)) {                      // block-uniform, rescaled step (R23)
                 double mx = fabs(alpha);
 #pragma unroll
@@ -204,8 +187,8 @@ __device__ void wide_qr(const Prob &P, int n, double *tau, double *tcache, Smem 
                 }
                 h = house(sc * alpha, s2);
                 h.beta = h.beta / sc;
+                sx = h.scale * sc;
             }
-            const double sx = h.scale * sc;
             const double wv = fma(h.scale, dd, rj);
             const double u = (l4 > jj) ? h.tau * sx * wv : (l4 == jj ? 1.0 : 0.0);
             const double g = (l4 == jj) ? sx : 0.0;             // pivot column: v = scale x exactly
@@ -593,7 +576,7 @@ __device__ __forceinline__ void apply_one_cols(const double *Ys, const double *T
 // row-split over the warps (warp w: rows [w 8KM, (w+1) 8KM)), one
 // __syncthreads per Householder step for the cross-warp sums; T per panel;
 // the trailing update column-split (apply_panel_cols).
-template <int KM>
+template <int KM, bool kRobust>
 __device__ void wide_leaf_qr(double *At, int64_t lda, int H, int n, double *tau, double *tcache, double *tpair,
                              LeafSmem<KM> &S) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
@@ -662,7 +645,8 @@ __device__ void wide_leaf_qr(double *At, int64_t lda, int H, int n, double *tau,
             const double rj = S.piv[par][l4], alpha = S.piv[par][jj];
             House h = house(alpha, s2);
             double sc = 1.0;
-            if (wy::house_unsafe(alpha, s2)) {                      // block-uniform, rescaled step (R23)
+            double sx = h.scale;
+            if (kRobust && wy::house_unsafe(alpha, s2)) {          // block-uniform, rescaled step (R23)
                 double mx = fabs(alpha);
 #pragma unroll
                 for (int k = 0; k < KM; ++k) {
@@ -707,8 +691,8 @@ __device__ void wide_leaf_qr(double *At, int64_t lda, int H, int n, double *tau,
                 }
                 h = house(sc * alpha, s2);
                 h.beta = h.beta / sc;
+                sx = h.scale * sc;
             }
-            const double sx = h.scale * sc;
             const double wv = fma(h.scale, dd, rj);
             const double u = (l4 > jj) ? h.tau * sx * wv : (l4 == jj ? 1.0 : 0.0);
             const double g = (l4 == jj) ? sx : 0.0;
@@ -830,7 +814,7 @@ __device__ void wide_leaf_qr(double *At, int64_t lda, int H, int n, double *tau,
 using namespace wide;
 
 // Leaves: tile t (one CTA each), row-split panels sized to the tile.
-template <int KM>
+template <int KM, bool kRobust>
 __global__ void __launch_bounds__(NT, KM <= 8 ? 2 : 1)
 k_wide_leaves(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *tile_rows, double *tau_tile,
               double *tcache_tile, double *tpair_tile) {
@@ -838,7 +822,7 @@ k_wide_leaves(double *A, int64_t lda, int n, const int64_t *tile_row0, const int
     LeafSmem<KM> &S = *reinterpret_cast<LeafSmem<KM> *>(smraw);
     const int t = blockIdx.x;
     const int npan = (n + 7) / 8;
-    wide_leaf_qr<KM>(A + tile_row0[t], lda, tile_rows[t], n, tau_tile + (int64_t)t * n,
+    wide_leaf_qr<KM, kRobust>(A + tile_row0[t], lda, tile_rows[t], n, tau_tile + (int64_t)t * n,
                      tcache_tile + (int64_t)t * npan * 64, tpair_tile + (int64_t)t * ((npan + 1) / 2) * 64, S);
 }
 
@@ -1096,27 +1080,35 @@ static size_t apply_leaf_smem(int max_rows, int slots) {
     return sizeof(double) * (slots * yw * ((max_rows + 7) / 8 * 8) + 2 * 192);
 }
 
-template <int KM>
+template <int KM, bool kRobust>
 static cudaError_t launch_leaves_km(double *A, int64_t lda, int n, const int64_t *row0, const int *rows, int L,
                                    int max_rows, double *tau, double *tcache, double *tpair, cudaStream_t st) {
     size_t bytes = LeafSmem<KM>::bytes(max_rows);
 #ifdef TSQR_WIDE_MIN_SMEM
     if (bytes < TSQR_WIDE_MIN_SMEM) bytes = TSQR_WIDE_MIN_SMEM;     // variant: cap resident CTAs per SM
 #endif
-    cudaError_t e = cudaFuncSetAttribute((const void *)k_wide_leaves<KM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)bytes);
+    cudaError_t e = cudaFuncSetAttribute((const void *)k_wide_leaves<KM, kRobust>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
     if (e != cudaSuccess) return e;
-    k_wide_leaves<KM><<<L, NT, bytes, st>>>(A, lda, n, row0, rows, tau, tcache, tpair);
+    k_wide_leaves<KM, kRobust><<<L, NT, bytes, st>>>(A, lda, n, row0, rows, tau, tcache, tpair);
     return cudaGetLastError();
 }
 
-// max_rows: the tallest tile (selects the per-warp row range, 64 KM >= max_rows)
+template <bool kRobust>
+static cudaError_t launch_leaves_r(double *A, int64_t lda, int n, const int64_t *row0, const int *rows, int L,
+                                   int max_rows, double *tau, double *tcache, double *tpair, cudaStream_t st) {
+    if (max_rows <= 512) return launch_leaves_km<8, kRobust>(A, lda, n, row0, rows, L, max_rows, tau, tcache, tpair, st);
+    if (max_rows <= 1024) return launch_leaves_km<16, kRobust>(A, lda, n, row0, rows, L, max_rows, tau, tcache, tpair, st);
+    if (max_rows <= 1536) return launch_leaves_km<24, kRobust>(A, lda, n, row0, rows, L, max_rows, tau, tcache, tpair, st);
+    return launch_leaves_km<KMW, kRobust>(A, lda, n, row0, rows, L, max_rows, tau, tcache, tpair, st);
+}
+
+// max_rows: the tallest tile (selects the per-warp row range, 64 KM >= max_rows);
+// robust: the rescaled steps of reading R23
 cudaError_t launch_wide_leaves(double *A, int64_t lda, int n, const int64_t *row0, const int *rows, int L,
-                               int max_rows, double *tau, double *tcache, double *tpair, cudaStream_t st) {
-    if (max_rows <= 512) return launch_leaves_km<8>(A, lda, n, row0, rows, L, max_rows, tau, tcache, tpair, st);
-    if (max_rows <= 1024) return launch_leaves_km<16>(A, lda, n, row0, rows, L, max_rows, tau, tcache, tpair, st);
-    if (max_rows <= 1536) return launch_leaves_km<24>(A, lda, n, row0, rows, L, max_rows, tau, tcache, tpair, st);
-    return launch_leaves_km<KMW>(A, lda, n, row0, rows, L, max_rows, tau, tcache, tpair, st);
+                               int max_rows, double *tau, double *tcache, double *tpair, bool robust, cudaStream_t st) {
+    return robust ? launch_leaves_r<true>(A, lda, n, row0, rows, L, max_rows, tau, tcache, tpair, st)
+                  : launch_leaves_r<false>(A, lda, n, row0, rows, L, max_rows, tau, tcache, tpair, st);
 }
 
 cudaError_t launch_wide_nodes(double *A, int64_t lda, int n, const int64_t *row0, const int *node_a, const int *ids,

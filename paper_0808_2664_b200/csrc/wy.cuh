@@ -31,7 +31,8 @@ namespace wy {
 // D += A B for one 8x8x4 fp64 MMA (SASS DMMA.8x8x4).  Fragments (lane i):
 // A[i/4][i%4], B[k=i%4][n=i/4], C/D[i/4][2(i%4)+{0,1}].
 __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+    asm volatile(
+        "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(d0), "+d"(d1)
                  : "d"(a), "d"(b));
 }
@@ -81,8 +82,12 @@ __device__ __forceinline__ House householder(double alpha, double sigma2) {
 //     w = rj + scale_s d_s      (d_s = (s x)^T a: the dot recomputed on s x),
 //     u = tau (s scale_s) w,    v = (s scale_s) x,    beta = beta_s / s.
 __device__ __forceinline__ bool house_unsafe(double alpha, double s2) {
+#ifdef TSQR_NO_RESCALE            // measurement variant only: the slow path compiled out
+    return false;
+#else
     const double y = fma(alpha, alpha, s2);
     return !(y >= 0x1p-900 && y <= 0x1p+900);
+#endif
 }
 // s = 2^-e with s mx in [0.5, 1); 1 for mx = 0, inf or NaN (nothing to rescale);
 // e clamped to [-1000, 1000] so that s and 1/s stay finite (a subnormal mx then

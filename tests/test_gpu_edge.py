@@ -1,7 +1,8 @@
 """GPU edge cases through the C-ABI, against the CPU oracle ("What's weak" 3):
 
-* inputs near the fp64 range limits (A x 1e-160 ... 1e+155): the kernels' dlarfg
-  scalars must rescale like LAPACK's dlarfg (reading R23); the oracle's long-double
+* inputs near the fp64 range limits (A x 1e-300 ... 1e+300): inside [2^-400, 2^400]
+  the default kernels are exact (1e+-110 checks it), outside TSQR_FLAG_ROBUST makes
+  every step rescale like LAPACK's dlarfg (reading R23); the oracle's long-double
   sums have the exponent range to take them unscaled;
 * strided storage (lda = m + 7, ldc = m + 5, ldq = m + 3): the kernels must use the
   leading dimensions, never m, and leave the padding rows alone;
@@ -46,13 +47,14 @@ SCALED_SHAPES = [(5000, 50, 4096, 1366), (3000, 16, 1000, 250), (4096, 64, 4096,
                  (3000, 100, 1500, 1500), (4000, 200, 2048, 2048), (2000, 240, 1000, 1000)]
 
 
-@pytest.mark.parametrize("scale", [1e-160, 1e-150, 1e+150, 1e+155])
+@pytest.mark.parametrize("scale", [1e-160, 1e-150, 1e-110, 1e+110, 1e+150, 1e+155, 1e-300, 1e+300])
 @pytest.mark.parametrize("m,n,b,s", SCALED_SHAPES)
 def test_scaled_inputs(m, n, b, s, scale):
     At = inputs.gaussian(m, n, 21) * scale
     A0 = _np(At).copy()
     Ad = At.cuda()
-    R, tree = T.factor(Ad, block_rows=b, tile_rows=s, debug=True)
+    robust = not (2.0 ** -400 <= scale <= 2.0 ** 400)       # TSQR_FLAG_ROBUST outside the default range (R23)
+    R, tree = T.factor(Ad, block_rows=b, tile_rows=s, debug=True, robust=robust)
     Q = T.form_q(tree)
     torch.cuda.synchronize()
     Rg, Qg = _np(R), _np(Q)
