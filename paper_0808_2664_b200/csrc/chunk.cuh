@@ -145,26 +145,39 @@ __device__ __forceinline__ void sync_publish(int *c, int v) {
 
 // dlarfg scalars (readings R1/R2/R19), branch-free: beta = -sign(alpha) N with
 // N = sqrt(alpha^2 + sigma2), tau = 1 + |alpha|/N, scale = 1/(alpha - beta);
-// sigma2 == 0 gives H = I (tau = 0, beta = alpha).  1/sqrt from the MUFU seed
-// and two Newton steps, 1/x likewise (rcp_nr): <= 2 ulp.  (A single third-order
-// correction per seed is one dependent step shorter but measured no faster.)
+// sigma2 == 0 gives H = I (tau = 0, beta = alpha).  1/sqrt(y) and 1/(|alpha| + N)
+// from the MUFU seeds and two Newton steps each: <= 2 ulp; the reciprocal is
+// seeded from |alpha| + y r0 so its MUFU runs while the root is refined.
+// (-DTSQR_HOUSE3: one third-order correction per seed, one dependent step
+// shorter -- measured no faster on the full kernel.)
 // The plain sums and the flush-to-zero seeds need the input range of reading
 // R23; the robust instantiation (kRobust) rescales outside it.
 __device__ __forceinline__ House house_bf(double alpha, double s2) {
     const double y = fma(alpha, alpha, s2);
     const double aa = fabs(alpha);
-    double r, i;
-    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(y));
-    const double D0 = fma(y, r, aa);
-    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(i) : "d"(D0));
+    double r0, i0;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(y));
+    const double D0 = fma(y, r0, aa);
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(i0) : "d"(D0));
+#ifndef TSQR_HOUSE3
     const double hy = 0.5 * y;
-    r = r * fma(-hy * r, r, 1.5);
+    double r = r0 * fma(-hy * r0, r0, 1.5);
     const double D1 = fma(y, r, aa);
-    i = fma(i, fma(-D1, i, 1.0), i);
+    double i = fma(i0, fma(-D1, i0, 1.0), i0);
     r = r * fma(-hy * r, r, 1.5);
     const double N = y * r;
     const double D = aa + N;
     i = fma(i, fma(-D, i, 1.0), i);
+#else
+    // one third-order correction per seed: r = r0 (1 + e/2 + 3e^2/8), e = 1 - y r0^2;
+    // i = i0 (1 + e' + e'^2), e' = 1 - D i0 (seed errors ~2^-20 -> O(2^-60))
+    const double e = fma(-(y * r0), r0, 1.0);
+    const double r = fma(r0 * e, fma(0.375, e, 0.5), r0);
+    const double N = y * r;
+    const double D = aa + N;
+    const double ei = fma(-D, i0, 1.0);
+    const double i = fma(i0 * ei, 1.0 + ei, i0);
+#endif
     const bool z = (s2 == 0.0);
     House h;
     h.beta = z ? alpha : (alpha >= 0.0 ? -N : N);
@@ -307,6 +320,10 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
     }
     __syncwarp();
     const int jn = (P + 1 < C::NCB) ? 8 : n - 8 * P;      // only the last panel has padding columns
+    // A finished pivot column keeps x; its reflector v = scl x is formed once after
+    // the panel (scl: this lane's column's scale), so each step updates with one
+    // FMA per value: the pivot and finished columns get u = 0.
+    double scl = 1.0;
 #pragma unroll 1
     for (int jj = 0; jj < jn; ++jj) {
         const int j = 8 * P + jj;
@@ -318,16 +335,18 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
             x[k][0] = v.x;
             x[k][1] = v.y;
         }
-        double d0 = 0.0, d1 = 0.0, s0 = 0.0, s1 = 0.0;
+        // sigma^2 = the pivot column's own dot x^T x (its lanes hold x), read from
+        // lane 4 jj: no separate sum of squares (half the step's FMAs)
+        double dk[2][2] = {{0.0, 0.0}, {0.0, 0.0}};                 // four partial dots: shorter chains
 #pragma unroll
         for (int k = 0; k < C::KM; ++k) {
-            d0 = fma(x[k][0], ch.a[k][P][0], d0);
-            d1 = fma(x[k][1], ch.a[k][P][1], d1);
-            s0 = fma(x[k][0], x[k][0], s0);
-            s1 = fma(x[k][1], x[k][1], s1);
+            dk[k & 1][0] = fma(x[k][0], ch.a[k][P][0], dk[k & 1][0]);
+            dk[k & 1][1] = fma(x[k][1], ch.a[k][P][1], dk[k & 1][1]);
         }
-        double d, s2;
-        quad_sums(d, s2, d0 + d1, s0 + s1);
+        double d, s2, dz = 0.0;
+        d = 0.0;
+        dmma(d, dz, (dk[0][0] + dk[1][0]) + (dk[0][1] + dk[1][1]), 1.0);
+        s2 = __shfl_sync(FULL, d, 4 * jj);
         PROBE(3);
         // R row j released by the previous chunk: the counter and the row are read
         // together, the row again only if the counter was short ("Hand-off
@@ -351,11 +370,9 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
             sx = h.scale * sc;
         }
         const double w = fma(h.scale, d, rj);                        // v^T [R(j,c); a_c]
-        // a <- a - u x (u = tau scale w) for the trailing columns; the pivot
-        // column becomes v = scale x, formed as scale x + (a - x) with a - x
-        // exactly 0 (a - (1 - scale) x would cancel when scale << 1)
-        const double u = (l4 > jj) ? h.tau * sx * w : (l4 == jj ? 1.0 : 0.0);
-        const double g = (l4 == jj) ? sx : 0.0;
+        // a <- a - u x (u = tau scale w) for the trailing columns only
+        const double u = (l4 > jj) ? h.tau * sx * w : 0.0;
+        if (l4 == jj) scl = sx;
         // hand R row j to the next chunk first (its step j waits for it), then
         // update this chunk's panel
         const double rnew = (l4 == jj) ? h.beta : fma(-h.tau, w, rj);
@@ -364,8 +381,8 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
         sync_publish(sy.row + j, sy.s + 1);
 #pragma unroll
         for (int k = 0; k < C::KM; ++k) {
-            ch.a[k][P][0] = fma(g, x[k][0], fma(-u, x[k][0], ch.a[k][P][0]));
-            ch.a[k][P][1] = fma(g, x[k][1], fma(-u, x[k][1], ch.a[k][P][1]));
+            ch.a[k][P][0] = fma(-u, x[k][0], ch.a[k][P][0]);
+            ch.a[k][P][1] = fma(-u, x[k][1], ch.a[k][P][1]);
         }
         if (l4 == jj + 1) {                                          // next pivot column -> the other row
             double *xw = xs + ((jj + 1) & 1) * C::CH;
@@ -373,10 +390,15 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
             for (int k = 0; k < C::KM; ++k)
                 *reinterpret_cast<double2 *>(xw + 8 * k + 2 * q) = make_double2(ch.a[k][P][0], ch.a[k][P][1]);
         }
-        if (q == 0 && l4 < jj) Gs[l4 * 8 + jj] = h.scale * d;       // G(l, jj) = v_l^T v_jj
+        if (q == 0 && l4 < jj) Gs[l4 * 8 + jj] = scl * (h.scale * d);   // G(l, jj) = v_l^T v_jj, v_l = scl x_l
         if (lane == 0) t8[jj] = h.tau;
         __syncwarp();                                                // xs of the next step
         PROBE(2);
+    }
+#pragma unroll
+    for (int k = 0; k < C::KM; ++k) {                                // v = scl x (exactly the former scale x + 0)
+        ch.a[k][P][0] *= scl;
+        ch.a[k][P][1] *= scl;
     }
     pad_steps(Gs, t8, jn);
     __syncwarp();
