@@ -209,10 +209,13 @@ struct Cfg {
     static constexpr int OFF_SYNC = OFF_WS + NW * WS;     // per buffer: NP row + NCB panel counters
     static constexpr int SYNC_INTS = NP + NCB;
     // after the counters: one range-gate flag per buffer (NBUF ints)
-    static constexpr int OFF_STG = (OFF_SYNC + (NBUF * (SYNC_INTS + 1) + 1) / 2 + 1) & ~1;   // 16-byte aligned; per warp:
-                                                                                   // the next chunk (col-major CH x NP)
+    // per warp: the next chunk (col-major CH x NP), 128-byte aligned (TMA destination)
+    static constexpr int OFF_STG = (OFF_SYNC + (NBUF * (SYNC_INTS + 1) + 1) / 2 + 15) & ~15;
     static constexpr int STG = CH * NP;
-    static constexpr size_t BYTES = (size_t)(OFF_STG + NW * STG) * sizeof(double);
+    static_assert((STG * 8) % 128 == 0, "TMA staging slots must stay 128-byte aligned");
+    static constexpr int OFF_BAR = OFF_STG + NW * STG;    // one mbarrier per warp (TMA completion)
+    static constexpr size_t BYTES = (size_t)(OFF_BAR + NW) * sizeof(double);
+    static_assert(BYTES <= 232448, "exceeds 227 KB of shared memory per CTA");
 };
 
 // T (8x8, row-major) of one panel from its Gram entries G(l, c), l < c

@@ -54,6 +54,7 @@ struct tsqr_tree_s {
     int64_t *d_tile_chunk0 = nullptr;
     int *d_cta_tile0 = nullptr, *d_apply_cta_tile0 = nullptr;
     int chain_grid = 0, apply_grid = 0;
+    bool rows_even = false;           // every tile starts on an even row (TMA boxes need 16-byte aligned starts)
     double *d_tau_chunk = nullptr;
     double *d_tcache = nullptr;       // [chunks][NCB][8][8] panel T factors (compact WY)
     int64_t nchunks = 0;
@@ -343,6 +344,7 @@ static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t 
         alloc((void **)&t->d_tcache_pair, sizeof(double) * L * ((t->npan + 1) / 2) * 64);
     }
     t->nchunks = nchunks;
+    t->rows_even = std::all_of(p.tile_row0.begin(), p.tile_row0.end(), [](int64_t r) { return (r & 1) == 0; });
     if (e != cudaSuccess) {
         free_tree_memory(t, st);
         delete t;
@@ -426,7 +428,7 @@ tsqr_status_t tsqr_factor(int64_t m_local, int64_t n, double *A, int64_t lda, do
             if (!e) CUDA_TRY(cudaEventCreate(&e), "tsqr_factor events");
     auto mark = [&](int i) -> cudaError_t { return timed ? cudaEventRecord(t->ev[i], t->stream) : cudaSuccess; };
     ChainArgs ca;
-    ca.A = A; ca.lda = lda; ca.n = (int)n; ca.chunk_rows = t->plan.c;
+    ca.A = A; ca.lda = lda; ca.n = (int)n; ca.m = t->rows_even ? m_local : 0; ca.chunk_rows = t->plan.c;
     ca.tile_row0 = t->d_row0; ca.tile_rows = t->d_rows; ca.tile_chunk0 = t->d_tile_chunk0;
     ca.cta_tile0 = t->d_cta_tile0; ca.grid = t->chain_grid; ca.tau = t->d_tau_chunk; ca.tcache = t->d_tcache;
     const bool robust = (ro.flags & TSQR_FLAG_ROBUST) != 0;     // reading R23

@@ -10,12 +10,26 @@
 //      of a tile writes the tile's R into the upper triangle of its head rows.
 #include "tsqr_kernels.h"
 #include "chunk.cuh"
+#include "tma.cuh"
+
+#include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 namespace tsqr {
 using namespace chunk;
+
+// TSQR_NO_TMA=1 in the environment: the per-element cp.async staging everywhere (A/B checks)
+static bool chain_no_tma() {
+    static const int v = [] {
+        const char *e = std::getenv("TSQR_NO_TMA");
+        return (e && *e == '1') ? 1 : 0;
+    }();
+    return v != 0;
+}
 
 template <class C, int P, bool kRobust>
 __device__ __forceinline__ void chunk_panels(Chunk<C> &ch, int r0, bool last, double *Rb, const Sync &sy,
@@ -56,19 +70,48 @@ __device__ __forceinline__ void prefetch_chunk(double *stg, const double *src, i
 // kRobust: the rescaled Householder steps of reading R23 (inputs outside
 // [2^-400, 2^400]); a separate instantiation chosen at launch (opts.flags bit 2)
 // so the default kernel carries no trace of the slow path (measured 3-8 %).
-template <class C, bool kRobust>
+// kTma: the next chunk is staged by one TMA box copy (tensor map `tmap` of A,
+// box CH x n, rows past the matrix zero-filled, the slot's padding columns
+// n..NP-1 zeroed once; rows past the tile are zeroed on the register load)
+// completing on the warp's mbarrier;
+// otherwise by per-element cp.async (any lda / alignment).
+template <class C, bool kRobust, bool kTma>
 __global__ void __launch_bounds__(C::NT, 1)
 k_chain_factor(double *A, int64_t lda, int n, const int64_t *tile_row0, const int *tile_rows,
-               const int64_t *tile_chunk0, const int *cta_tile0, double *tau, double *tcache) {
-    extern __shared__ __align__(16) double sm[];
+               const int64_t *tile_chunk0, const int *cta_tile0, double *tau, double *tcache,
+               const __grid_constant__ CUtensorMap tmap) {
+    extern __shared__ __align__(128) double sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int q = lane & 3, l4 = lane >> 2;
     int *sync = reinterpret_cast<int *>(sm + C::OFF_SYNC);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(sm + C::OFF_BAR) + warp;
     for (int i = threadIdx.x; i < C::NBUF * C::SYNC_INTS; i += C::NT) sync[i] = 0;
+    if (kTma && lane == 0) {
+        tma::mbar_init(bar, 1);
+        tma::fence_mbar_init();
+        tma::prefetch_map(&tmap);
+    }
     PROBE_INIT();
     __syncthreads();
     double *ws = sm + C::OFF_WS + warp * C::WS;
     double *stg = sm + C::OFF_STG + warp * C::STG;
+    unsigned phase = 0;
+    if constexpr (kTma) {                                 // the box is CH x n: padding columns stay zero
+        for (int i = lane; i < (C::NP - n) * C::CH; i += 32) stg[n * C::CH + i] = 0.0;
+        __syncwarp();
+    }
+    // stream rows [r0, r0 + hk) of tile t into the staging slot
+    auto stage = [&](int t, int r0, int hk) {
+        if constexpr (kTma) {
+            if (lane == 0) {
+                tma::fence_proxy_async_smem();        // the slot's generic reads precede the async write
+                tma::mbar_arrive_expect_tx(bar, C::CH * n * (unsigned)sizeof(double));
+                tma::load_2d(stg, &tmap, (int)(tile_row0[t] + r0), 0, bar);
+            }
+        } else {
+            prefetch_chunk<C>(stg, A + tile_row0[t] + r0, lda, hk, n);
+        }
+    };
     const int tb = cta_tile0[blockIdx.x], te = cta_tile0[blockIdx.x + 1];
     // Walk the CTA's chunk sequence (all warps identically); this warp owns
     // every NW-th chunk.  When the warp finds its next chunk it computes the
@@ -102,7 +145,7 @@ k_chain_factor(double *A, int64_t lda, int n, const int64_t *tile_row0, const in
         if (pt < 0) {                                     // first chunk: stream it in
             if (nt < 0) break;
             const int r0 = ncix * C::CH;
-            prefetch_chunk<C>(stg, A + tile_row0[nt] + r0, lda, min(C::CH, tile_rows[nt] - r0), n);
+            stage(nt, r0, min(C::CH, tile_rows[nt] - r0));
             pt = nt; pc = ncix; ps = ns; pb = nb;
             continue;
         }
@@ -111,7 +154,12 @@ k_chain_factor(double *A, int64_t lda, int n, const int64_t *tile_row0, const in
         const int pnch = (h + C::CH - 1) / C::CH;
         const int64_t row0 = tile_row0[pt];
         const int r0 = pc * C::CH, hk = min(C::CH, h - r0);
-        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        if constexpr (kTma) {
+            tma::mbar_wait(bar, phase);
+            phase ^= 1;
+        } else {
+            asm volatile("cp.async.wait_all;\n" ::: "memory");
+        }
         __syncwarp();
         Chunk<C> ch;
 #pragma unroll
@@ -122,10 +170,19 @@ k_chain_factor(double *A, int64_t lda, int n, const int64_t *tile_row0, const in
                 ch.a[k][cb][0] = v.x;
                 ch.a[k][cb][1] = v.y;
             }
+        if (kTma && hk < C::CH) {                         // the box ran into the next tile: zero those rows
+#pragma unroll
+            for (int k = 0; k < C::KM; ++k)
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                    if (8 * k + 2 * q + e >= hk)
+#pragma unroll
+                        for (int cb = 0; cb < C::NCB; ++cb) ch.a[k][cb][e] = 0.0;
+        }
         __syncwarp();
         if (nt >= 0) {                                    // the next chunk streams in meanwhile
             const int r0n = ncix * C::CH;
-            prefetch_chunk<C>(stg, A + tile_row0[nt] + r0n, lda, min(C::CH, tile_rows[nt] - r0n), n);
+            stage(nt, r0n, min(C::CH, tile_rows[nt] - r0n));
         }
         PROBE(0);
         double *tau_out = tau + (tile_chunk0[pt] + pc) * n;
@@ -162,20 +219,53 @@ static cudaError_t chain_dispatch(int n, F &&fn) {
     }
 }
 
-template <class C, bool kRobust>
-static cudaError_t launch_chain_factor_t(const ChainArgs &f, cudaStream_t st) {
+// Tensor map of an m x n column-major fp64 matrix (tma.cuh), through the driver
+// entry point (no libcuda link dependency).
+bool make_tmap_colmajor(CUtensorMap *map, const double *base, int64_t m, int64_t n, int64_t ld, int box_rows,
+                        int box_cols) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    static bool looked = false;
+    if (!looked) {
+        looked = true;
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult qr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &qr) == cudaSuccess &&
+            qr == cudaDriverEntryPointSuccess)
+            encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+        cudaGetLastError();
+    }
+    if (!encode || m < 1 || n < 1 || m > INT32_MAX || n > INT32_MAX) return false;
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * 8) & 15) || ld >= (int64_t(1) << 37)) return false;
+    const cuuint64_t dims[2] = {(cuuint64_t)m, (cuuint64_t)n};
+    const cuuint64_t strides[1] = {(cuuint64_t)(ld * 8)};
+    const cuuint32_t box[2] = {(cuuint32_t)box_rows, (cuuint32_t)box_cols};
+    const cuuint32_t estr[2] = {1, 1};
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <class C, bool kRobust, bool kTma>
+static cudaError_t launch_chain_factor_t(const ChainArgs &f, const CUtensorMap &map, cudaStream_t st) {
     const size_t sm = C::BYTES;
-    cudaError_t e = cudaFuncSetAttribute((const void *)k_chain_factor<C, kRobust>,
+    cudaError_t e = cudaFuncSetAttribute((const void *)k_chain_factor<C, kRobust, kTma>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
-    k_chain_factor<C, kRobust><<<f.grid, C::NT, sm, st>>>(f.A, f.lda, f.n, f.tile_row0, f.tile_rows, f.tile_chunk0,
-                                                          f.cta_tile0, f.tau, f.tcache);
+    k_chain_factor<C, kRobust, kTma><<<f.grid, C::NT, sm, st>>>(f.A, f.lda, f.n, f.tile_row0, f.tile_rows,
+                                                               f.tile_chunk0, f.cta_tile0, f.tau, f.tcache, map);
     return cudaGetLastError();
 }
 
 cudaError_t launch_chain_factor(const ChainArgs &f, cudaStream_t st) {
     return chain_dispatch(f.n, [&](auto c) {
-        return f.robust ? launch_chain_factor_t<decltype(c), true>(f, st) : launch_chain_factor_t<decltype(c), false>(f, st);
+        using C = decltype(c);
+        CUtensorMap map;
+        std::memset(&map, 0, sizeof(map));
+        // the robust instantiation keeps the cp.async staging (one fewer kernel per configuration)
+        const bool tma = !f.robust && f.m > 0 && !chain_no_tma() &&
+                         make_tmap_colmajor(&map, f.A, f.m, f.n, f.lda, C::CH, f.n);
+        if (f.robust) return launch_chain_factor_t<C, true, false>(f, map, st);
+        return tma ? launch_chain_factor_t<C, false, true>(f, map, st) : launch_chain_factor_t<C, false, false>(f, map, st);
     });
 }
 
@@ -204,10 +294,10 @@ int chain_grid(int n) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaError_t e = chain_dispatch(n, [&](auto c) {
         using C = decltype(c);
-        cudaError_t r = cudaFuncSetAttribute((const void *)k_chain_factor<C, false>,
+        cudaError_t r = cudaFuncSetAttribute((const void *)k_chain_factor<C, false, false>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::BYTES);
         if (r != cudaSuccess) return r;
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_chain_factor<C, false>, C::NT, C::BYTES);
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_chain_factor<C, false, false>, C::NT, C::BYTES);
     });
     if (e != cudaSuccess || occ < 1) occ = 1;
     return sms * occ;

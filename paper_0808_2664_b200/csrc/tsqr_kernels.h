@@ -20,6 +20,7 @@ bool tree_shape(const tsqr_tree_s *t, int64_t *m_local, int64_t *n, int *nranks,
 // Leaf stage on the chunk engine (tsqr_chain.cu).
 struct ChainArgs {
     double *A; int64_t lda; int n;
+    int64_t m = 0;               // rows of A (the TMA tensor map's extent; 0 = no TMA)
     int chunk_rows;              // the plan's c (chain_chunk_rows(n))
     const int64_t *tile_row0; const int *tile_rows; const int64_t *tile_chunk0;
     const int *cta_tile0; int grid;

@@ -13,7 +13,7 @@ import paper_0808_2664_b200 as T  # noqa: E402
 lib = os.environ.get("TSQR_LIBRARY", "default")
 for name in sys.argv[1:]:
     cfg = bench.CONFIGS[name]
-    m, n, b, s, k = cfg["m"], cfg["n"], cfg["b"], cfg["s"], cfg["k"]
+    m, n, b, s, k = cfg["m"], cfg["n"], cfg["b"], int(os.environ.get("AB_S", cfg["s"])), cfg["k"]
     A0 = bench.make_slab(cfg, 0, m, "cuda")
     A = torch.empty_like(A0)
     Q = torch.empty_like(A0) if cfg["op"] == "form_q" else None
@@ -40,7 +40,7 @@ for name in sys.argv[1:]:
             ts.append(e1.elapsed_time(e2))
             tl.append(tree.stage_ms()[0])
     med = statistics.median
-    print(f"{os.path.basename(lib):28s} {name}: factor {med(tf):8.3f} ms (leaf {med(tl):8.3f})  second op {med(ts):8.3f} ms",
+    print(f"{os.path.basename(lib):28s} {name} s={s}: factor {med(tf):8.3f} ms (leaf {med(tl):8.3f})  second op {med(ts):8.3f} ms",
           flush=True)
     tree.free()
     del A0, A, Q, C0, C
