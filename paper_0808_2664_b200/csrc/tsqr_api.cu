@@ -593,7 +593,7 @@ tsqr_status_t tsqr_apply_qt(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, do
     cudaStream_t st = (cudaStream_t)stream;
     ENTER(t, st);
     ChainApplyArgs ca;
-    ca.A = t->A; ca.lda = t->lda; ca.n = (int)t->plan.n; ca.chunk_rows = t->plan.c;
+    ca.A = t->A; ca.lda = t->lda; ca.n = (int)t->plan.n; ca.chunk_rows = t->plan.c; ca.bulk = t->rows_even;
     ca.tile_row0 = t->d_row0; ca.tile_rows = t->d_rows; ca.tile_chunk0 = t->d_tile_chunk0;
     ca.cta_tile0 = t->d_apply_cta_tile0; ca.grid = t->apply_grid; ca.tcache = t->d_tcache;
     ca.C = C; ca.ldc = ldc; ca.k = (int)k; ca.forward = 1; ca.xbuf = nullptr;
@@ -708,7 +708,7 @@ tsqr_status_t tsqr_apply_q(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, voi
                  "tsqr_apply_q leaves");
     } else {
         ChainApplyArgs ca;
-        ca.A = t->A; ca.lda = t->lda; ca.n = n; ca.chunk_rows = t->plan.c;
+        ca.A = t->A; ca.lda = t->lda; ca.n = n; ca.chunk_rows = t->plan.c; ca.bulk = t->rows_even; ca.bulk = t->rows_even;
         ca.tile_row0 = t->d_row0; ca.tile_rows = t->d_rows; ca.tile_chunk0 = t->d_tile_chunk0;
         ca.cta_tile0 = t->d_apply_cta_tile0; ca.grid = t->apply_grid; ca.tcache = t->d_tcache;
         ca.C = C; ca.ldc = ldc; ca.k = (int)k; ca.forward = 0; ca.xbuf = nullptr;
@@ -771,7 +771,7 @@ tsqr_status_t tsqr_form_q(tsqr_tree_t t, double *Q, int64_t ldq, void *stream) {
                  "tsqr_form_q nodes");
     }
     ChainApplyArgs ca;
-    ca.A = t->A; ca.lda = t->lda; ca.n = n; ca.chunk_rows = t->plan.c;
+    ca.A = t->A; ca.lda = t->lda; ca.n = n; ca.chunk_rows = t->plan.c; ca.bulk = t->rows_even;
     ca.tile_row0 = t->d_row0; ca.tile_rows = t->d_rows; ca.tile_chunk0 = t->d_tile_chunk0;
     ca.cta_tile0 = t->d_apply_cta_tile0; ca.grid = t->apply_grid; ca.tcache = t->d_tcache;
     ca.C = Q; ca.ldc = ldq; ca.k = n; ca.forward = 0; ca.xbuf = t->d_xbuf;

@@ -2,12 +2,23 @@
 // factor's representation (chunk.cuh).  Product code.
 #include "tsqr_kernels.h"
 #include "chunk.cuh"
+#include "tma.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 namespace tsqr {
 using namespace chunk;
+
+// TSQR_NO_TMA=1: per-element cp.async staging here too (A/B checks)
+static bool apply_no_bulk() {
+    static const int v = [] {
+        const char *e = std::getenv("TSQR_NO_TMA");
+        return (e && *e == '1') ? 1 : 0;
+    }();
+    return v != 0;
+}
 
 // ============================================================ apply / form Q
 // k_cs_apply<C, kFwd, kX>: the leaf stage of C <- Q^T C (kFwd, (a7)), of the
@@ -32,8 +43,47 @@ struct ApplyCs {
     static constexpr int LDY = C::NP + 2, LDT = C::CH + 2;
     static constexpr int OFF_YT = C::CH * LDY, OFF_T = OFF_YT + C::NP * LDT;
     static constexpr int YS = OFF_T + C::NCB * 64;
-    static constexpr size_t BYTES = (size_t)2 * YS * sizeof(double);
+    static_assert(LDT % 2 == 0 && OFF_YT % 2 == 0 && OFF_T % 2 == 0 && YS % 2 == 0, "bulk copy targets 16-byte aligned");
+    static constexpr size_t BYTES = (size_t)2 * YS * sizeof(double) + 2 * sizeof(uint64_t);   // + two mbarriers
 };
+
+__device__ __forceinline__ void bulk_g2s(double *dst, const double *src, unsigned bytes, uint64_t *bar) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst), b = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(d),
+                 "l"(src), "r"(bytes), "r"(b)
+                 : "memory");
+}
+
+// Bulk staging (even row starts, even lda, hk even): each of Y's n columns (hk rows,
+// 16-byte aligned both sides) is one cp.async.bulk into the column-major copy Yt,
+// the T's one more; all complete on the slot's mbarrier.  After the wait,
+// finish_bulk_stage() zeroes what the factor stores but Y does not contain (rows past
+// the tile, the R entries on/above the pivots of a head chunk), sets the unit
+// diagonal and writes the row-major copy Yr.
+template <class C>
+__device__ __forceinline__ void stage_chunk_bulk(double *slot, const double *Ak, int64_t lda, int hk, int n,
+                                                 const double *tch, uint64_t *bar) {
+    using AC = ApplyCs<C>;
+    if (threadIdx.x == 0)
+        tma::mbar_arrive_expect_tx(bar, (unsigned)(n * hk + C::NCB * 64) * (unsigned)sizeof(double));
+    tma::fence_proxy_async_smem();
+    for (int col = threadIdx.x; col <= n; col += blockDim.x) {
+        if (col < n) bulk_g2s(slot + AC::OFF_YT + col * AC::LDT, Ak + (int64_t)col * lda, (unsigned)hk * 8u, bar);
+        else bulk_g2s(slot + AC::OFF_T, tch, C::NCB * 64 * 8u, bar);
+    }
+}
+template <class C>
+__device__ __forceinline__ void finish_bulk_stage(double *slot, int hk, int n, int r0) {
+    using AC = ApplyCs<C>;
+    const bool fix = hk < C::CH || r0 < C::NP;            // ragged or head chunk: Yt changes too
+    for (int i = threadIdx.x; i < C::CH * C::NP; i += blockDim.x) {
+        const int col = i / C::CH, row = i - col * C::CH;
+        const double v = slot[AC::OFF_YT + col * AC::LDT + row];
+        const double y = (col < n && row < hk && row > col - r0) ? v : ((col < n && row == col - r0) ? 1.0 : 0.0);
+        slot[row * AC::LDY + col] = y;
+        if (fix) slot[AC::OFF_YT + col * AC::LDT + row] = y;
+    }
+}
 
 __device__ __forceinline__ void cp8(double *sm, const double *g, bool ok) {
     const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(sm));
@@ -65,8 +115,8 @@ __device__ __forceinline__ void fix_dense(double *slot, int n, int r0) {
         }
 }
 
-template <class C, bool kFwd>
-__device__ __forceinline__ void cs_apply_panel(double (&cc)[C::KM][2], double (&cr)[C::NCB][2], int p, int r0,
+template <class C, bool kFwd, int p>
+__device__ __forceinline__ void cs_apply_panel(double (&cc)[C::KM][2], double (&cr)[C::NCB][2], int r0,
                                                const double *slot, bool &czero) {
     // czero (form Q only): the chunk's rows of C are still all zero -- they become
     // nonzero with the first panel applied to the chunk -- so W^T = C^T Y is skipped
@@ -78,12 +128,7 @@ __device__ __forceinline__ void cs_apply_panel(double (&cc)[C::KM][2], double (&
     const double *ys = slot + 8 * p;
     const double *Tg = slot + ApplyCs<C>::OFF_T + 64 * p;
     const double *yt = slot + ApplyCs<C>::OFF_YT + 8 * p * LDT;       // Yt column 8p
-    double crp0 = 0.0, crp1 = 0.0;
-#pragma unroll
-    for (int i = 0; i < C::NCB; ++i) {
-        crp0 = (i == p) ? cr[i][0] : crp0;
-        crp1 = (i == p) ? cr[i][1] : crp1;
-    }
+    double crp0 = cr[p][0], crp1 = cr[p][1];
     if (!kFwd && dense) {                     // Q: the pivot rows take their R-row coordinates back
 #pragma unroll
         for (int k = 0; k < KM; ++k) {
@@ -128,11 +173,22 @@ __device__ __forceinline__ void cs_apply_panel(double (&cc)[C::KM][2], double (&
             crp1 = (k == kb) ? cc[k][1] : crp1;
         }
     }
-#pragma unroll
-    for (int i = 0; i < C::NCB; ++i) {
-        cr[i][0] = (i == p) ? crp0 : cr[i][0];
-        cr[i][1] = (i == p) ? crp1 : cr[i][1];
+    cr[p][0] = crp0;
+    cr[p][1] = crp1;
+}
+
+// the chunk's panels in order (Q^T: 0 .. np-1) or reverse (Q: np-1 .. 0), the
+// panel index a compile-time constant so C_R's row block is a plain register
+template <class C, bool kFwd, int I>
+__device__ __forceinline__ void cs_apply_panels(double (&cc)[C::KM][2], double (&cr)[C::NCB][2], int r0, int np,
+                                                const double *slot, bool &czero) {
+    if constexpr (kFwd) {
+        if (I < np) cs_apply_panel<C, kFwd, I>(cc, cr, r0, slot, czero);
+    } else {
+        constexpr int p = C::NCB - 1 - I;
+        if (p < np) cs_apply_panel<C, kFwd, p>(cc, cr, r0, slot, czero);
     }
+    if constexpr (I + 1 < C::NCB) cs_apply_panels<C, kFwd, I + 1>(cc, cr, r0, np, slot, czero);
 }
 
 // this lane's slab of C (column col, rows 8kk+2q+{0,1}) for chunk c of a tile
@@ -153,9 +209,35 @@ template <class C, bool kFwd, bool kX>
 __global__ void __launch_bounds__(256, 2)
 k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const int *tile_rows,
            const int64_t *tile_chunk0, const int *cta_tile0, const double *tcache, double *Cm, int64_t ldc, int k,
-           const double *xbuf) {
+           const double *xbuf, int bulk) {
     using AC = ApplyCs<C>;
     extern __shared__ __align__(16) double sm[];
+    uint64_t *bars = reinterpret_cast<uint64_t *>(sm + 2 * AC::YS);
+    if (bulk) {                                                   // padding columns of Yt stay zero
+        for (int i = threadIdx.x; i < 2 * (C::NP - n) * AC::LDT; i += blockDim.x) {
+            const int sl = i / ((C::NP - n) * AC::LDT), j = i - sl * (C::NP - n) * AC::LDT;
+            sm[sl * AC::YS + AC::OFF_YT + n * AC::LDT + j] = 0.0;
+        }
+        if (threadIdx.x == 0) {
+            tma::mbar_init(bars, 1);
+            tma::mbar_init(bars + 1, 1);
+            tma::fence_mbar_init();
+        }
+        __syncthreads();
+    }
+    unsigned phase = 0u, sbulk = 0u;                              // per slot (bit i): mbarrier parity, bulk-staged
+    auto stage = [&](int slot_i, int t_, int c_, int hk_, int r0_) {
+        const double *Ak = A + tile_row0[t_] + r0_;
+        const double *tch = tcache + (tile_chunk0[t_] + c_) * (C::NCB * 64);
+        const bool bk = bulk && !(hk_ & 1);
+        sbulk = bk ? (sbulk | (1u << slot_i)) : (sbulk & ~(1u << slot_i));
+        if (bk) {
+            stage_chunk_bulk<C>(sm + slot_i * AC::YS, Ak, lda, hk_, n, tch, bars + slot_i);
+            asm volatile("cp.async.commit_group;\n" ::: "memory");    // an empty group: wait_group counts stay aligned
+        } else {
+            stage_chunk<C>(sm + slot_i * AC::YS, Ak, lda, hk_, n, tch, r0_);
+        }
+    };
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
     const int tb = cta_tile0[blockIdx.x], te = cta_tile0[blockIdx.x + 1];
     const int pw = blockDim.x >> 2;                               // columns per pass (8 per warp)
@@ -199,9 +281,7 @@ k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                 const int c = chunk_of(t, cc_);
                 const int r0 = c * C::CH, hk = min(C::CH, h - r0);
                 const bool dense = r0 < C::NP;                    // a head chunk (holds pivots)
-                if (!staged)
-                    stage_chunk<C>(sm + cur * AC::YS, A + row0 + r0, lda, hk, n,
-                                   tcache + (tile_chunk0[t] + c) * (C::NCB * 64), r0);
+                if (!staged) stage(cur, t, c, hk, r0);
                 // prefetch the next chunk of the work list: Y/T into the other
                 // slot, C into registers
                 int tn = t, pn = pass, cn = cc_ + 1;
@@ -209,8 +289,7 @@ k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                 double ccn[C::KM][2];
                 if (tn < te) {
                     const int cnn = chunk_of(tn, cn), hn = tile_rows[tn], r0n = cnn * C::CH;
-                    stage_chunk<C>(sm + (cur ^ 1) * AC::YS, A + tile_row0[tn] + r0n, lda, min(C::CH, hn - r0n), n,
-                                   tcache + (tile_chunk0[tn] + cnn) * (C::NCB * 64), r0n);
+                    stage(cur ^ 1, tn, cnn, min(C::CH, hn - r0n), r0n);
                     if (!kX) load_cslab<C>(ccn, Cm, ldc, k, tile_row0[tn], hn, cnn, pw * pn + 8 * warp + l4, q);
                     asm volatile("cp.async.wait_group 1;\n" ::: "memory");
                     staged = true;
@@ -222,17 +301,22 @@ k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const 
 #pragma unroll
                     for (int kk = 0; kk < C::KM; ++kk) ccv[kk][0] = ccv[kk][1] = 0.0;
                 }
-                __syncthreads();
                 double *slot = sm + cur * AC::YS;
-                if (dense) {
-                    fix_dense<C>(slot, n, r0);
+                if ((sbulk >> cur) & 1u) {
+                    tma::mbar_wait(bars + cur, (phase >> cur) & 1u);
+                    phase ^= 1u << cur;
+                    finish_bulk_stage<C>(slot, hk, n, r0);
                     __syncthreads();
+                } else {
+                    __syncthreads();
+                    if (dense) {
+                        fix_dense<C>(slot, n, r0);
+                        __syncthreads();
+                    }
                 }
                 double *Ck = Cm + row0 + r0;
                 bool czero = kX;
-#pragma unroll 1
-                for (int pp = 0; pp < np; ++pp)
-                    cs_apply_panel<C, kFwd>(ccv, cr, kFwd ? pp : np - 1 - pp, r0, slot, czero);
+                cs_apply_panels<C, kFwd, 0>(ccv, cr, r0, np, slot, czero);
 #pragma unroll
                 for (int kk = 0; kk < C::KM; ++kk)
 #pragma unroll
@@ -303,8 +387,10 @@ cudaError_t launch_cs_apply(const ChainApplyArgs &f, cudaStream_t st) {
                                              (int)AC::BYTES);
         if (e != cudaSuccess) return e;
         const int nw = f.k >= 64 ? 8 : (f.k + 7) / 8;           // one warp per 8-column slab
+        const bool bulk = f.bulk && !apply_no_bulk() && !(reinterpret_cast<uintptr_t>(f.A) & 15) && !(f.lda & 1) &&
+                          !(reinterpret_cast<uintptr_t>(f.tcache) & 15);
         kern<<<f.grid, 32 * (nw < 1 ? 1 : nw), AC::BYTES, st>>>(f.A, f.lda, f.n, f.tile_row0, f.tile_rows, f.tile_chunk0, f.cta_tile0,
-                                                f.tcache, f.C, f.ldc, f.k, f.xbuf);
+                                                f.tcache, f.C, f.ldc, f.k, f.xbuf, bulk ? 1 : 0);
         return cudaGetLastError();
     });
 }

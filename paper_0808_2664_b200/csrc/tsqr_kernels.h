@@ -39,6 +39,7 @@ struct ChainApplyArgs {
     int forward;
     const double *xbuf;          // !forward: per-tile X (n x n) from the node stage (form Q);
                                  // nullptr: C <- Q C in place (the head rows hold C_R)
+    bool bulk = false;           // Y / T staged by bulk copies (every tile starts on an even row)
 };
 // Chain engine (tsqr_chain.cu): chunk rows, column blocks, persistent grid, factor.
 int chain_chunk_rows(int n);
