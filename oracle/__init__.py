@@ -46,6 +46,7 @@ def lib():
         _lib = ctypes.CDLL(build())
         _lib.orc_plan_count.restype = ctypes.c_int
         _lib.orc_plan_fill.restype = ctypes.c_int
+        _lib.orc_cholqr.restype = ctypes.c_int
     return _lib
 
 
@@ -159,6 +160,17 @@ def mgs_ld(A):
     R = np.zeros((n, n), order="F")
     lib().orc_mgs_ld(_i64(m), _i64(n), _d(A), _i64(m), _d(Q), _i64(m), _d(R), _i64(n))
     return Q, R
+
+
+def cholqr(A, want_q: bool = True):
+    """Alg. CholeskyQR (the comparison method, orc_cholqr).  Returns (info, R, Q or None)."""
+    A = _fortran(A)
+    m, n = A.shape
+    R = np.zeros((n, n), order="F")
+    Q = np.zeros((m, n), order="F") if want_q else None
+    info = lib().orc_cholqr(_i64(m), _i64(n), _d(A), _i64(m), _d(R), _i64(n),
+                            _d(Q) if want_q else None, _i64(m))
+    return int(info), R, Q
 
 
 # ------------------------------------------------------------------- plan

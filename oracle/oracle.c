@@ -537,3 +537,43 @@ void orc_mgs_ld(int64_t m, int64_t n, const double *A, int64_t lda,
         for (int64_t i = 0; i < m; ++i) AT(Q, i, j, ldq) = (double)V[i + j * m];
     free(V);
 }
+
+/* Alg. CholeskyQR ([TR] P:1410-1419), see oracle.h. */
+int orc_cholqr(int64_t m, int64_t n, const double *A, int64_t lda, double *R, int64_t ldr,
+               double *Q, int64_t ldq)
+{
+    /* line 1: W := A^T A */
+    double *W = (double *)malloc((size_t)(n * n) * sizeof(double));
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = 0; j < n; ++j) {
+            long double s = 0.0L;
+            for (int64_t r = 0; r < m; ++r) s += (long double)AT(A, r, i, lda) * AT(A, r, j, lda);
+            W[i + j * n] = (double)s;
+        }
+    /* line 2: W = R^T R, R upper triangular, row j from rows 0..j-1 */
+    for (int64_t j = 0; j < n; ++j)
+        for (int64_t i = 0; i < n; ++i) AT(R, i, j, ldr) = 0.0;
+    for (int64_t j = 0; j < n; ++j) {
+        long double d = W[j + j * n];
+        for (int64_t k = 0; k < j; ++k) d -= (long double)AT(R, k, j, ldr) * AT(R, k, j, ldr);
+        if (!(d > 0.0L)) { free(W); return (int)(j + 1); }
+        const double rjj = (double)sqrtl(d);
+        AT(R, j, j, ldr) = rjj;
+        for (int64_t c = j + 1; c < n; ++c) {
+            long double s = W[j + c * n];
+            for (int64_t k = 0; k < j; ++k) s -= (long double)AT(R, k, j, ldr) * AT(R, k, c, ldr);
+            AT(R, j, c, ldr) = (double)(s / rjj);
+        }
+    }
+    free(W);
+    /* line 3: Q := A R^{-1}, row by row (R^T q_i = a_i, forward substitution) */
+    if (Q) {
+        for (int64_t r = 0; r < m; ++r)
+            for (int64_t j = 0; j < n; ++j) {
+                long double s = AT(A, r, j, lda);
+                for (int64_t l = 0; l < j; ++l) s -= (long double)AT(Q, r, l, ldq) * AT(R, l, j, ldr);
+                AT(Q, r, j, ldq) = (double)(s / AT(R, j, j, ldr));
+            }
+    }
+    return 0;
+}

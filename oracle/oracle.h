@@ -169,6 +169,22 @@ void orc_tsqr_form_q(int64_t m, int64_t n, const double *A, int64_t lda, int64_t
 void orc_mgs_ld(int64_t m, int64_t n, const double *A, int64_t lda,
                 double *Q, int64_t ldq, double *R, int64_t ldr);
 
+/* CholeskyQR, Alg. CholeskyQR ([TR] P:1410-1419) -- the comparison method of
+ * SURVEY 8(f) row 4, NOT part of TSQR:
+ *   line 1  W := A^T A        (each entry an inner product, long double sum, then
+ *                              rounded to double: the fp64 W of the algorithm)
+ *   line 2  W = L L^T         (Cholesky, row by row; R := L^T, positive diagonal)
+ *   line 3  Q := A L^{-T}     (Q = A R^{-1}: forward substitution q_i^T R = a_i^T
+ *                              for every row i)
+ * Returns 0, or j+1 when the leading minor of order j+1 of the computed W is not
+ * positive (R, Q then incomplete).  Q may be NULL (R only).
+ * Pinned by: a hand-worked 2x2 example (golden cholqr_2x2.txt); R vs LAPACK's
+ * Householder R (uniqueness modulo signs); Q vs an independent
+ * triangular solve; orthonormal A -> R = I, Q = A; a zero column -> breakdown at
+ * that column; the loss of orthogonality growing as kappa^2. */
+int orc_cholqr(int64_t m, int64_t n, const double *A, int64_t lda, double *R, int64_t ldr,
+               double *Q, int64_t ldq);
+
 #ifdef __cplusplus
 }
 #endif

@@ -520,3 +520,75 @@ def test_combine_q_pins(q, n):
     if q == 2:                                            # the binary combine (C oracle)
         Rb, Y1, tb, _ = orc.combine(Rs[0], Rs[1])
         assert orc.rel_fro(R, Rb) <= 1e-14 and orc.rel_fro(Ys[0], Y1) <= 1e-14 and orc.rel_fro(tau, tb) <= 1e-14
+
+
+# ------------------------------------------------------- CholeskyQR (8(f) row 4)
+def test_cholqr_worked_example(golden_dir):
+    """Alg. CholeskyQR ([TR] P:1410-1419) on the hand-worked 2x2 case."""
+    (row,) = _golden_rows(os.path.join(golden_dir, "cholqr_2x2.txt"))
+    v = [float(x) for x in row]
+    A = np.array([[v[0], v[1]], [v[2], v[3]]])
+    info, R, Q = orc.cholqr(A)
+    assert info == 0
+    np.testing.assert_allclose(R, [[v[4], v[5]], [0.0, v[6]]], rtol=0, atol=4 * EPS * 5)
+    # q2 = (a2 - 2.2 q1) / 0.4 cancels (1 - 1.32) and divides by 0.4: ~10 eps of rounding
+    np.testing.assert_allclose(Q, [[v[7], v[8]], [v[9], v[10]]], rtol=0, atol=32 * EPS)
+
+
+@pytest.mark.parametrize("m,n,seed", [(200, 8, 0), (1000, 16, 1), (3000, 33, 2)])
+def test_cholqr_matches_lapack_householder_r(m, n, seed):
+    """kappa(A) ~ 1: CholeskyQR's R is the QR factor's R with a positive diagonal (R is
+    unique up to the signs of its rows), so it equals LAPACK's Householder R
+    after sign normalisation; Q = A R^{-1} equals an independent triangular solve."""
+    A = _rng(seed).standard_normal((m, n))
+    info, R, Q = orc.cholqr(A)
+    assert info == 0
+    assert np.all(np.diag(R) > 0) and np.all(np.tril(R, -1) == 0)
+    Rl = np.linalg.qr(A, mode="r")
+    Rl = Rl * np.sign(np.diag(Rl))[:, None]
+    assert np.linalg.norm(R - Rl) / np.linalg.norm(Rl) <= 1e-13
+    Qs = scipy.linalg.solve_triangular(R, A.T, trans="T", lower=False).T     # R^T Q^T = A^T
+    assert np.linalg.norm(Q - Qs) <= 1e-13 * np.sqrt(n)
+    assert np.linalg.norm(Q.T @ Q - np.eye(n)) <= 1e-13
+
+
+def test_cholqr_orthonormal_input():
+    """A with orthonormal columns: W = I exactly up to rounding, so R = I and Q = A."""
+    A, _ = np.linalg.qr(_rng(5).standard_normal((500, 12)))
+    info, R, Q = orc.cholqr(A)
+    assert info == 0
+    assert np.linalg.norm(R - np.eye(12)) <= 1e-14
+    assert np.linalg.norm(Q - A) <= 1e-14
+
+
+def test_cholqr_breakdown_on_zero_column():
+    """A zero column makes the leading minor of that order of W = A^T A zero: Alg.
+    CholeskyQR line 2 breaks down exactly there (info = column + 1)."""
+    A = _rng(6).standard_normal((100, 6))
+    A[:, 3] = 0.0
+    info, _, _ = orc.cholqr(A)
+    assert info == 4
+
+
+def test_cholqr_orthogonality_degrades_as_kappa_squared():
+    """"the Q factor computed by CholeskyQR loses orthogonality proportionally to
+    kappa_2(A)^2", while Householder QR's Q stays orthogonal: on the C4
+    recipe (sigma log-spaced 1 .. 1/kappa, reading R15) the orthogonality error grows by
+    >= 1e5 from kappa = 1e2 to 1e5 (kappa^2 grows 1e6) and stays within c kappa^2 eps."""
+    import torch
+    from paper_0808_2664_b200 import inputs
+    errs = {}
+    for kappa in (1e2, 1e5):
+        A = inputs.to_numpy_colmajor(inputs.conditioned(4096, 16, seed=0, kappa=kappa))
+        info, R, Q = orc.cholqr(A)
+        assert info == 0
+        errs[kappa] = np.linalg.norm(Q.T @ Q - np.eye(16))
+        assert errs[kappa] <= 50 * kappa ** 2 * EPS
+        # and the factorisation itself is still backward stable: ||A - QR|| small
+        assert np.linalg.norm(A - Q @ R) / np.linalg.norm(A) <= 1e-12
+    assert errs[1e5] >= 1e5 * errs[1e2]
+    F = A.copy(order="F")
+    tau = np.zeros(16)
+    orc.lib().orc_hqr(orc._i64(4096), orc._i64(16), orc._d(F), orc._i64(4096), orc._d(tau))
+    Qh = _explicit_tile_q(F, tau, 4096, 16)[:, :16]
+    assert np.linalg.norm(Qh.T @ Qh - np.eye(16)) <= 1e-13
