@@ -357,6 +357,32 @@ tsqr_status_t tsqr_ctx_apply_q(tsqr_ctx_t ctx, tsqr_tree_t tree, double *C, int6
  * every cross-rank node factor, [TR] P:1919-1925); = tsqr_form_q. */
 tsqr_status_t tsqr_ctx_form_q(tsqr_ctx_t ctx, tsqr_tree_t tree, double *Q, int64_t ldq, void *stream);
 
+/* ---------------------------------------------------------------- CholeskyQR
+ * The comparison method of SURVEY 8(f) row 4 -- NOT the TSQR path.  Alg.
+ * CholeskyQR ([TR] P:1410-1419): W := A^T A (line 1), W = L L^T (line 2),
+ * Q := A L^{-T} (line 3); R = L^T.  Its Q "loses orthogonality proportionally
+ * to kappa_2(A)^2" where TSQR's stays orthogonal: the stability
+ * half of "only parallel TSQR is simultaneously fastest and stable"
+ * (P:1347-1354).  A^T A and A R^{-1} run on FP64 DMMA.
+ * A (device, m x n, lda >= m) is read only.  R (device, n x n, ldr >= n)
+ * receives the upper triangular factor with a positive diagonal (zeros below).
+ * Q (device, m x n, ldq >= m, may be NULL: R only) receives A R^{-1}.
+ * info (DEVICE int) receives 0, or j + 1 when the computed W's leading minor of
+ * order j + 1 is not positive (Cholesky breakdown -- kappa(A)^2 beyond 1/eps);
+ * R and Q are then unspecified.  Workspace is stream-ordered (cudaMallocAsync
+ * on `stream`); TSQR_ERR_ALLOC if it cannot be had.  n <= TSQR_MAX_N. */
+tsqr_status_t tsqr_cholqr(int64_t m, int64_t n, const double *A, int64_t lda, double *R, int64_t ldr,
+                          double *Q, int64_t ldq, int *info, void *stream);
+
+/* Collective CholeskyQR over the context's ranks (row slabs as tsqr_ctx_factor):
+ * each rank's A_i^T A_i, then the all-reduction of line 1 as log2(nranks)
+ * butterfly rounds of n^2 words (lower rank's W + upper rank's W in that order,
+ * so W -- hence R -- is bitwise identical on every rank; Table "CholeskyQR
+ * counts": log P messages), then lines 2-3 locally.  R replicated;
+ * Q = this rank's rows. */
+tsqr_status_t tsqr_ctx_cholqr(tsqr_ctx_t ctx, int64_t m_local, int64_t n, const double *A, int64_t lda,
+                              double *R, int64_t ldr, double *Q, int64_t ldq, int *info, void *stream);
+
 /* ---------------------------------------------------------------- host
  * End-to-end QR with HOST buffers on one GPU (the e2e path of bench.py): A (host,
  * m x n, lda >= m) is copied to the device, factored (tsqr_factor with opts;

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.environ.get("TSQR_BUILD_OUT", os.path.join(HERE, "libtsqr.so"))   # override: A/B variant builds
 SOURCES = ["tsqr_api.cu", "tsqr_wy.cu", "tsqr_chain.cu", "tsqr_cs.cu", "tsqr_wide.cu", "tsqr_tree.cu", "tsqr_caqr.cu",
-           "tsqr_stream.cu", "tsqr_combine.cu", "tsqr_comm.cu", "tsqr_peak.cu", "tsqr_host.cu", "plan.cpp"]
+           "tsqr_stream.cu", "tsqr_combine.cu", "tsqr_comm.cu", "tsqr_peak.cu", "tsqr_host.cu", "tsqr_cholqr.cu", "plan.cpp"]
 HEADERS = ["wy.cuh", "chunk.cuh", "tma.cuh", "tsqr_kernels.h", "plan.h", os.path.join("..", "..", "include", "tsqr.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 

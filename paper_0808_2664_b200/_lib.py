@@ -24,7 +24,7 @@ SYMBOLS = ["tsqr_status_string", "tsqr_last_error", "tsqr_slab", "tsqr_plan_info
            "tsqr_ctx_create", "tsqr_get_unique_id", "tsqr_ctx_set_comm", "tsqr_loopback_create",
            "tsqr_loopback_destroy", "tsqr_ctx_set_loopback", "tsqr_ctx_info", "tsqr_ctx_destroy", "tsqr_ctx_factor",
            "tsqr_ctx_apply_qt", "tsqr_ctx_apply_q", "tsqr_ctx_form_q", "tsqr_measure_fp64_peak",
-           "tsqr_qr_host", "tsqr_host_ws_free"]
+           "tsqr_qr_host", "tsqr_host_ws_free", "tsqr_cholqr", "tsqr_ctx_cholqr"]
 
 
 class TsqrError(RuntimeError):
@@ -106,6 +106,8 @@ def lib():
         "tsqr_qr_host": [ctypes.POINTER(_vp), _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i64,
                          ctypes.POINTER(Opts), _vp],
         "tsqr_host_ws_free": [_vp],
+        "tsqr_cholqr": [_i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp],
+        "tsqr_ctx_cholqr": [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp],
     }
     for name, args in sig.items():
         if "TSQR_LIBRARY" in os.environ and not hasattr(L, name):

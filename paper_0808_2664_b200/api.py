@@ -277,6 +277,12 @@ class Ctx:
         check(lib().tsqr_ctx_form_q(self.handle, tree.handle, pq, ldq, _stream_ptr(stream)), "tsqr_ctx_form_q")
         return Q
 
+    def cholqr(self, A: torch.Tensor, R: torch.Tensor | None = None, Q: torch.Tensor | None = None,
+               want_q: bool = True, stream=None):
+        """Collective CholeskyQR (tsqr_ctx_cholqr): R replicated, Q this rank's rows.
+        Returns (R, Q or None, info) with info a device int32 tensor (0 = ok, j+1 = breakdown)."""
+        return _cholqr(A, R, Q, want_q, stream, ctx=self)
+
     def free(self):
         if self.handle:
             lib().tsqr_ctx_destroy(self.handle)
@@ -303,6 +309,33 @@ class Loopback:
                 lib().tsqr_loopback_destroy(self.handle)
         except Exception:
             pass
+
+
+def _cholqr(A, R, Q, want_q, stream, ctx=None):
+    pa, m, n, lda = _colmajor(A, "A")
+    if R is None:
+        R = torch.empty((n, n), dtype=torch.float64, device=A.device)
+    pr, _, _, ldr = _colmajor(R, "R")
+    pq, ldq = None, 0
+    if want_q:
+        if Q is None:
+            Q = torch.empty((n, m), dtype=torch.float64, device=A.device)
+        pq, _, _, ldq = _colmajor(Q, "Q")
+    info = torch.zeros(1, dtype=torch.int32, device=A.device)
+    if ctx is None:
+        check(lib().tsqr_cholqr(m, n, pa, lda, pr, ldr, pq, ldq, info.data_ptr(), _stream_ptr(stream)), "tsqr_cholqr")
+    else:
+        check(lib().tsqr_ctx_cholqr(ctx.handle, m, n, pa, lda, pr, ldr, pq, ldq, info.data_ptr(), _stream_ptr(stream)),
+              "tsqr_ctx_cholqr")
+    return R, (Q if want_q else None), info
+
+
+def cholqr(A: torch.Tensor, R: torch.Tensor | None = None, Q: torch.Tensor | None = None, want_q: bool = True,
+           stream=None):
+    """CholeskyQR (tsqr_cholqr; Alg. CholeskyQR [TR] P:1410-1419) -- the comparison method
+    of SURVEY 8(f) row 4, not TSQR.  A is read only.  Returns (R, Q or None, info) with
+    info a device int32 tensor: 0, or j+1 when the Cholesky of A^T A broke down at j."""
+    return _cholqr(A, R, Q, want_q, stream)
 
 
 def measure_fp64_peak(stream=None):

@@ -348,4 +348,37 @@ tsqr_status_t tsqr_ctx_form_q(tsqr_ctx_t c, tsqr_tree_t tree, double *Q, int64_t
     return tsqr_form_q(tree, Q, ldq, stream);
 }
 
+tsqr_status_t tsqr_ctx_cholqr(tsqr_ctx_t c, int64_t m_local, int64_t n, const double *A, int64_t lda, double *R,
+                              int64_t ldr, double *Q, int64_t ldq, int *info, void *stream) {
+    if (!valid(c) || !A || !R || !info) return TSQR_ERR_INVALID;
+    if (n < 1 || m_local < n) return TSQR_ERR_SHAPE;
+    if (n > TSQR_MAX_N) return TSQR_ERR_UNSUPPORTED;
+    if (lda < m_local || ldr < n || (Q && ldq < m_local)) return TSQR_ERR_INVALID;
+    DeviceGuard g(c->device);
+    if (g.err != cudaSuccess) return cuda_fail(g.err, "tsqr_ctx_cholqr");
+    const int rounds = ilog2(c->nranks);
+    cudaStream_t st = (cudaStream_t)stream;
+    tsqr_status_t s = rounds ? ensure_buffers(c, n * n, st) : TSQR_OK;
+    if (s != TSQR_OK) return s;
+    CholqrWs w;
+    cudaError_t e = cholqr_alloc(w, m_local, (int)n, st);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return TSQR_ERR_ALLOC;
+    }
+    e = cholqr_gram(A, lda, m_local, (int)n, w, st);                       // line 1, this rank's A_i^T A_i
+    for (int r = 1; r <= rounds && e == cudaSuccess && s == TSQR_OK; ++r) {  // line 1's all-reduction
+        const int partner = c->rank ^ (1 << (r - 1));
+        e = cudaMemcpyAsync(c->send, w.W, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, st);
+        if (e == cudaSuccess) s = exchange(c, c->send, c->recv, n * n, partner, st);
+        if (e == cudaSuccess && s == TSQR_OK) e = cholqr_add_ordered(w.W, c->recv, n * n, c->rank < partner, st);
+    }
+    if (e == cudaSuccess && s == TSQR_OK) e = cholqr_finish(A, lda, m_local, (int)n, w, R, ldr, Q, ldq, info, st);
+    cholqr_free(w, st);
+    if (rounds) c->buf_stream = st;
+    if (s != TSQR_OK) return s;
+    return e == cudaSuccess ? TSQR_OK : cuda_fail(e, "tsqr_ctx_cholqr");
+}
+
 }  // extern "C"
+

@@ -102,4 +102,18 @@ cudaError_t launch_cross_apply(int NP, const double *Y1, const double *tau, doub
 cudaError_t launch_cross_root_x(int NP, const double *Y1s, const double *taus, int rounds, int rank, int n,
                                 double *X0, cudaStream_t st);
 
+
+// CholeskyQR comparison path (tsqr_cholqr.cu): workspace and stages.
+struct CholqrWs {
+    double *base = nullptr, *W = nullptr, *Rinv = nullptr, *part = nullptr;
+    int nsplit = 1;
+    int64_t rows_per_split = 0;
+    ~CholqrWs();
+};
+cudaError_t cholqr_alloc(CholqrWs &w, int64_t m, int n, cudaStream_t st);
+void cholqr_free(CholqrWs &w, cudaStream_t st);
+cudaError_t cholqr_gram(const double *A, int64_t lda, int64_t m, int n, CholqrWs &w, cudaStream_t st);   // w.W = A^T A
+cudaError_t cholqr_add_ordered(double *W, const double *P, int64_t count, int is_lower, cudaStream_t st);
+cudaError_t cholqr_finish(const double *A, int64_t lda, int64_t m, int n, CholqrWs &w, double *R, int64_t ldr,
+                          double *Q, int64_t ldq, int *info, cudaStream_t st);
 }  // namespace tsqr
