@@ -228,6 +228,31 @@ tsqr_status_t tsqr_factor_streamed(int64_t m, int64_t n, const double *A, int64_
                                    double *Y, int64_t ldy, double *R, int64_t ldr,
                                    const tsqr_opts_t *opts, void *stream);
 
+/* The streamed factor with its implicit Q kept ([TR] Alg. sequential TSQR
+ * P:1725-1753 writes every slab's Q factors to slow memory): as
+ * tsqr_factor_streamed, Y (host, ldy >= m) REQUIRED -- it receives the reflectors
+ * and is borrowed by the handle until tsqr_stream_tree_free -- and *out receives a
+ * handle holding, in page-locked host memory, each slab tree's taus and cached T's
+ * and each flat-tree node's factors (O(mn/c + S n^2) words).  Then, slab by slab
+ * through the GPU (device memory: one slab of Y and of C plus O(n k)), with HOST
+ * matrices:
+ *   tsqr_streamed_apply_qt  C (m x k, ldc >= m) <- Q^T C in the streamed tree's
+ *                           order (rows 0..n-1 = Q_thin^T C; top, host n x k,
+ *                           ldtop >= n, may be NULL, receives it too);
+ *   tsqr_streamed_apply_q   C <- Q C (C in that order): the exact inverse;
+ *   tsqr_streamed_form_q    Q (m x n, ldq >= m) <- the explicit thin Q.
+ * Synchronous (they return after `stream` has finished).  Page-locked C / Q make
+ * the copies asynchronous DMA. */
+typedef struct tsqr_stream_tree_s *tsqr_stream_tree_t;
+tsqr_status_t tsqr_factor_streamed_q(int64_t m, int64_t n, const double *A, int64_t lda, int64_t slab_rows,
+                                     double *Y, int64_t ldy, double *R, int64_t ldr, const tsqr_opts_t *opts,
+                                     void *stream, tsqr_stream_tree_t *out);
+tsqr_status_t tsqr_streamed_apply_qt(tsqr_stream_tree_t t, double *C, int64_t ldc, int64_t k, double *top,
+                                     int64_t ldtop, void *stream);
+tsqr_status_t tsqr_streamed_apply_q(tsqr_stream_tree_t t, double *C, int64_t ldc, int64_t k, void *stream);
+tsqr_status_t tsqr_streamed_form_q(tsqr_stream_tree_t t, double *Q, int64_t ldq, void *stream);
+tsqr_status_t tsqr_stream_tree_free(tsqr_stream_tree_t t);
+
 /* q-ary structured combine, Alg. QR:qnxn ([TR] P:1957-1979): the QR of q stacked
  * n x n upper triangles [R_1; ...; R_q], reflector j acting on {row j of R_1} U
  * {rows 0..j of R_2..R_q} ((2/3)(q-1)n^3 flops; q = 2 is the tree's

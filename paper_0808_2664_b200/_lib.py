@@ -24,7 +24,9 @@ SYMBOLS = ["tsqr_status_string", "tsqr_last_error", "tsqr_slab", "tsqr_plan_info
            "tsqr_ctx_create", "tsqr_get_unique_id", "tsqr_ctx_set_comm", "tsqr_loopback_create",
            "tsqr_loopback_destroy", "tsqr_ctx_set_loopback", "tsqr_ctx_info", "tsqr_ctx_destroy", "tsqr_ctx_factor",
            "tsqr_ctx_apply_qt", "tsqr_ctx_apply_q", "tsqr_ctx_form_q", "tsqr_measure_fp64_peak",
-           "tsqr_qr_host", "tsqr_host_ws_free", "tsqr_cholqr", "tsqr_ctx_cholqr"]
+           "tsqr_qr_host", "tsqr_host_ws_free", "tsqr_cholqr", "tsqr_ctx_cholqr",
+           "tsqr_factor_streamed_q", "tsqr_streamed_apply_qt", "tsqr_streamed_apply_q", "tsqr_streamed_form_q",
+           "tsqr_stream_tree_free"]
 
 
 class TsqrError(RuntimeError):
@@ -108,6 +110,12 @@ def lib():
         "tsqr_host_ws_free": [_vp],
         "tsqr_cholqr": [_i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp],
         "tsqr_ctx_cholqr": [_vp, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _vp],
+        "tsqr_factor_streamed_q": [_i64, _i64, _vp, _i64, _i64, _vp, _i64, _vp, _i64, ctypes.POINTER(Opts), _vp,
+                                   ctypes.POINTER(_vp)],
+        "tsqr_streamed_apply_qt": [_vp, _vp, _i64, _i64, _vp, _i64, _vp],
+        "tsqr_streamed_apply_q": [_vp, _vp, _i64, _i64, _vp],
+        "tsqr_streamed_form_q": [_vp, _vp, _i64, _vp],
+        "tsqr_stream_tree_free": [_vp],
     }
     for name, args in sig.items():
         if "TSQR_LIBRARY" in os.environ and not hasattr(L, name):

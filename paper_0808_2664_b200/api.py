@@ -193,6 +193,69 @@ def factor_streamed(A_host: torch.Tensor, slab_rows: int, block_rows: int = 0, t
     return R
 
 
+class StreamTree:
+    """Implicit Q of a streamed factor (tsqr_factor_streamed_q): slab trees' taus / T's and the
+    flat-tree nodes in pinned host memory; borrows the host Y (the reflectors) until freed."""
+
+    def __init__(self):
+        self.handle = ctypes.c_void_p(None)
+        self.Y = None
+        self.m = self.n = 0
+
+    def free(self):
+        if self.handle:
+            lib().tsqr_stream_tree_free(self.handle)
+            self.handle = ctypes.c_void_p(None)
+        self.Y = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def factor_streamed_q(A_host: torch.Tensor, slab_rows: int, Y_host: torch.Tensor, block_rows: int = 0,
+                      tile_rows: int = 0, R: torch.Tensor | None = None, device=None, stream=None):
+    """Streamed factor keeping Q: returns (R on the device, StreamTree)."""
+    pa, m, n, lda = _colmajor(A_host, "A", host=True)
+    if R is None:
+        R = torch.empty((n, n), dtype=torch.float64, device=device or "cuda")
+    pr, _, _, ldr = _colmajor(R, "R")
+    py, _, _, ldy = _colmajor(Y_host, "Y", host=True)
+    o = opts(block_rows, tile_rows)
+    st = StreamTree()
+    h = st.handle
+    check(lib().tsqr_factor_streamed_q(m, n, pa, lda, slab_rows, py, ldy, pr, ldr, ctypes.byref(o),
+                                       _stream_ptr(stream), ctypes.byref(h)), "tsqr_factor_streamed_q")
+    st.handle, st.Y, st.m, st.n = h, Y_host, m, n
+    return R, st
+
+
+def streamed_apply_qt(t: StreamTree, C_host: torch.Tensor, top: torch.Tensor | None = None, stream=None):
+    pc, m, k, ldc = _colmajor(C_host, "C", host=True)
+    ptop, ldtop = None, 0
+    if top is not None:
+        ptop, _, _, ldtop = _colmajor(top, "top", host=True)
+    check(lib().tsqr_streamed_apply_qt(t.handle, pc, ldc, k, ptop, ldtop, _stream_ptr(stream)),
+          "tsqr_streamed_apply_qt")
+    return C_host
+
+
+def streamed_apply_q(t: StreamTree, C_host: torch.Tensor, stream=None):
+    pc, m, k, ldc = _colmajor(C_host, "C", host=True)
+    check(lib().tsqr_streamed_apply_q(t.handle, pc, ldc, k, _stream_ptr(stream)), "tsqr_streamed_apply_q")
+    return C_host
+
+
+def streamed_form_q(t: StreamTree, Q_host: torch.Tensor | None = None, stream=None):
+    if Q_host is None:
+        Q_host = torch.empty((t.n, t.m), dtype=torch.float64).pin_memory()
+    pq, _, _, ldq = _colmajor(Q_host, "Q", host=True)
+    check(lib().tsqr_streamed_form_q(t.handle, pq, ldq, _stream_ptr(stream)), "tsqr_streamed_form_q")
+    return Q_host
+
+
 def combine_stacked(packed: torch.Tensor, q: int, n: int, tau: torch.Tensor | None = None, stream=None):
     """Alg. QR:qnxn on q packed triangles (device, q*n(n+1)/2, in place): slot 0 becomes R,
     slots 1.. the reflectors' v parts.  Returns tau (n)."""

@@ -813,3 +813,96 @@ tsqr_status_t tsqr_tree_export_tau(tsqr_tree_t t, double *tau_tile_host, double 
 }
 
 }  // extern "C"
+
+// --------------------------------------------------- tree state (streamed Q)
+// The device arrays that, with the reflectors in A, make up a local tree's implicit
+// Q (everything tsqr_apply_qt / tsqr_apply_q / tsqr_form_q read): chunk and node taus
+// and the cached panel T's.  tsqr_stream.cu keeps them in host memory per slab
+// ([TR] Alg. sequential TSQR P:1725-1753: "write Q factors to slow memory").
+namespace {
+struct StateArr {
+    double *p;
+    size_t words;
+};
+// the chain engine's chunk T cache (a fifth of Y's size at n = 64) is left out of the
+// compact state: tree_rebuild_tcache recomputes it from Y and the chunk taus
+std::vector<StateArr> state_arrays(const tsqr_tree_s *t, bool full) {
+    const int64_t L = t->plan.ntiles(), n = t->plan.n;
+    const int ncb_cache = t->wide ? t->npan : chain_ncb((int)n);
+    std::vector<StateArr> v = {{t->d_tau_chunk, (size_t)(t->nchunks * n)},
+                               {t->d_tau_node, (size_t)(L * n)},
+                               {t->d_tcache_node, (size_t)(L * t->npan * 64)}};
+    if (full || t->wide) v.push_back({t->d_tcache, (size_t)(t->nchunks * ncb_cache * 64)});
+    if (t->wide) v.push_back({t->d_tcache_pair, (size_t)(L * ((t->npan + 1) / 2) * 64)});
+    return v;
+}
+}  // namespace
+
+size_t tsqr::tree_state_words(const tsqr_tree_s *t, bool full) {
+    size_t w = 0;
+    for (const StateArr &a : state_arrays(t, full)) w += a.words;
+    return w;
+}
+
+tsqr_status_t tsqr::tree_state_words_for(int64_t m_local, int64_t n, const tsqr_opts_t *opts, bool full,
+                                         size_t *words) {
+    Plan p;
+    tsqr_opts_t ro;
+    int rc;
+    try { rc = plan_for(m_local, n, opts, &p, &ro); } catch (const std::bad_alloc &) { return TSQR_ERR_ALLOC; }
+    if (rc) return (tsqr_status_t)rc;
+    const int64_t L = p.ntiles(), nchunks = p.tile_chunk0[L], npan = (n + 7) / 8;
+    const bool wide = n > 64;
+    const int64_t ncb_cache = wide ? npan : chain_ncb((int)n);
+    size_t w = (size_t)(nchunks * n + L * n + L * npan * 64);
+    if (full || wide) w += (size_t)(nchunks * ncb_cache * 64);
+    if (wide) w += (size_t)(L * ((npan + 1) / 2) * 64);
+    *words = w;
+    return TSQR_OK;
+}
+
+cudaError_t tsqr::tree_state_copy(tsqr_tree_s *t, double *host, bool to_host, bool full, cudaStream_t st) {
+    size_t off = 0;
+    for (const StateArr &a : state_arrays(t, full)) {
+        const cudaError_t e = to_host
+            ? cudaMemcpyAsync(host + off, a.p, sizeof(double) * a.words, cudaMemcpyDeviceToHost, st)
+            : cudaMemcpyAsync(a.p, host + off, sizeof(double) * a.words, cudaMemcpyHostToDevice, st);
+        if (e != cudaSuccess) return e;
+        off += a.words;
+    }
+    return cudaSuccess;
+}
+
+cudaError_t tsqr::tree_rebuild_tcache(tsqr_tree_s *t, cudaStream_t st) {
+    if (t->wide) return cudaSuccess;                // the compact state of a wide tree is complete
+    return launch_chain_rebuild_t(t->A, t->lda, (int)t->plan.n, t->d_row0, t->d_rows, t->d_tile_chunk0,
+                                  t->plan.ntiles(), t->nchunks, t->d_tau_chunk, t->d_tcache, st);
+}
+
+tsqr_status_t tsqr::tree_bind(int64_t m_local, int64_t n, double *A, int64_t lda, const tsqr_opts_t *opts,
+                              cudaStream_t st, tsqr_tree_s **tree) {
+    // a tree for the plan of (m_local, n, opts) bound to the reflectors in A, without
+    // factoring (its state is imported next); an existing handle of the same plan is kept
+    tsqr_tree_s *t = *tree;
+    const tsqr_opts_t ro = resolve_opts(m_local, opts);
+    const bool reuse = t && t->plan.m_local == m_local && t->plan.n == n && t->opts.block_rows == ro.block_rows &&
+                       (ro.tile_rows == 0 || t->plan.s == ro.tile_rows) && t->opts.nranks == ro.nranks;
+    if (!reuse) {
+        if (t) {
+            t->stream = st;
+            tsqr_tree_free(t);
+        }
+        t = nullptr;
+        const tsqr_status_t s = create_tree(m_local, n, A, lda, opts, st, &t);
+        if (s != TSQR_OK) return s;
+        *tree = t;
+    } else {
+        ENTER(t, st);
+    }
+    t->A = A;
+    t->lda = lda;
+    t->stream = st;
+    t->cross_done = 0;
+    return TSQR_OK;
+}
+

@@ -356,4 +356,99 @@ void chain_partition(const std::vector<int64_t> &tile_rows, int chunk_rows, int 
     }
 }
 
+// ================================================================ T rebuild
+// k_chain_rebuild_t: the factor's T cache (tcache[chunk][panel] = the 8 x 8 T of
+// the panel's reflectors, row-major, LAPACK sign, reading R3) recomputed from the
+// stored reflectors and taus alone -- the streamed factor keeps only Y and tau
+// as its Q factors in host memory ([TR] Alg. TSQR:seq P:1725-1753 writes Y and
+// tau; T is derived data, Alg. YT:scaled P:2007-2028).  One warp per (chunk,
+// panel): the chunk-local part of each reflector is
+//     structured column j < r0:   y_j(i) = A(r0 + i, j), i < hk   (its R-row part
+//                                 e_j is orthogonal to the others' in the panel)
+//     dense column r0 <= j:       1 at i = j - r0, A(r0 + i, j) below, 0 above,
+// (a panel never mixes the two: CH is a multiple of 8); the lanes split the rows
+// for the 28 Gram entries G(l, c) = v_l^T v_c (l < c), a warp reduction, then T by
+// the recurrence T(r,c) = -tau_c sum_{l=r}^{c-1} T(r,l) G(l,c).  Absent columns
+// (tau = 0) give zero rows/columns, as in the factor.
+__global__ void __launch_bounds__(256)
+k_chain_rebuild_t(const double *A, int64_t lda, int n, int ch, int ncb, const int64_t *tile_row0, const int *tile_rows,
+                  const int64_t *tile_chunk0, int ntiles, const double *tau, double *tcache) {
+    const int lane = threadIdx.x & 31;
+    const int64_t nchunks = tile_chunk0[ntiles];
+    const int64_t task = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (task >= nchunks * ncb) return;
+    const int64_t g = task / ncb;
+    const int P = (int)(task - g * ncb);
+    int lo = 0, hi = ntiles - 1;                          // tile of chunk g
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (tile_chunk0[mid] <= g) lo = mid;
+        else hi = mid - 1;
+    }
+    const int t = lo;
+    const int r0 = (int)(g - tile_chunk0[t]) * ch;
+    const int hk = min(ch, tile_rows[t] - r0);
+    const double *Ak = A + tile_row0[t] + r0;
+    double gs[28];
+#pragma unroll
+    for (int i = 0; i < 28; ++i) gs[i] = 0.0;
+    for (int i = lane; i < hk; i += 32) {
+        double v[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const int j = 8 * P + c;
+            double x = 0.0;
+            if (j < n) {
+                if (j < r0) x = Ak[i + (int64_t)j * lda];
+                else x = (i == j - r0) ? 1.0 : (i > j - r0 ? Ak[i + (int64_t)j * lda] : 0.0);
+            }
+            v[c] = x;
+        }
+        int e = 0;
+#pragma unroll
+        for (int c = 1; c < 8; ++c)
+#pragma unroll
+            for (int l = 0; l < c; ++l) {
+                gs[e] = fma(v[l], v[c], gs[e]);
+                ++e;
+            }
+    }
+#pragma unroll
+    for (int i = 0; i < 28; ++i)
+#pragma unroll
+        for (int o = 16; o; o >>= 1) gs[i] += __shfl_xor_sync(0xffffffffu, gs[i], o);
+    const double *tp = tau + g * n;
+    const int r = lane & 7;
+    double row[8], tt[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) tt[c] = (8 * P + c < n) ? tp[8 * P + c] : 0.0;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) row[c] = (c == r) ? tt[r] : 0.0;
+    int e = 0;
+#pragma unroll
+    for (int c = 1; c < 8; ++c) {
+        double s2 = 0.0;
+#pragma unroll
+        for (int l = 0; l < c; ++l) s2 = fma(row[l], gs[e + l], s2);
+        e += c;
+        row[c] = (r < c) ? -tt[c] * s2 : row[c];
+    }
+    if (lane < 8) {
+        double *dst = tcache + (g * ncb + P) * 64 + r * 8;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) dst[c] = row[c];
+    }
+}
+
+cudaError_t launch_chain_rebuild_t(const double *A, int64_t lda, int n, const int64_t *tile_row0, const int *tile_rows,
+                                   const int64_t *tile_chunk0, int ntiles, int64_t nchunks, const double *tau,
+                                   double *tcache, cudaStream_t st) {
+    const int ch = chain_chunk_rows(n), ncb = chain_ncb(n);
+    const int64_t tasks = nchunks * ncb;
+    if (tasks == 0) return cudaSuccess;
+    k_chain_rebuild_t<<<(unsigned)((tasks + 7) / 8), 256, 0, st>>>(A, lda, n, ch, ncb, tile_row0, tile_rows, tile_chunk0,
+                                                                   ntiles, tau, tcache);
+    return cudaGetLastError();
+}
+
 }  // namespace tsqr

@@ -1,6 +1,8 @@
 // Host-side declarations of the kernel launchers (tsqr_chain.cu, tsqr_cs.cu,
 // tsqr_tree.cu, tsqr_wide.cu, tsqr_wy.cu), called by the C-ABI in tsqr_api.cu.
 #pragma once
+#include "../../include/tsqr.h"
+
 #include <cstdint>
 #include <cuda_runtime.h>
 #include <vector>
@@ -16,6 +18,20 @@ struct tsqr_tree_s;
 namespace tsqr {
 // Shape of a tree handle (tsqr_api.cu), for the communicator layer (tsqr_comm.cu).
 bool tree_shape(const tsqr_tree_s *t, int64_t *m_local, int64_t *n, int *nranks, int *rank, int *rounds_done);
+// A local tree's implicit-Q state besides the reflectors in A (taus, cached T's):
+// its size in doubles, and a packed stream-ordered copy to / from host memory
+// (tsqr_api.cu; used by the streamed factor's Q, tsqr_stream.cu).
+// full = false: the compact state (the chain engine's chunk T cache left out and rebuilt
+// from Y and the taus on import -- the tree must already be bound to its reflectors).
+size_t tree_state_words(const tsqr_tree_s *t, bool full);
+tsqr_status_t tree_state_words_for(int64_t m_local, int64_t n, const tsqr_opts_t *opts, bool full, size_t *words);
+cudaError_t tree_state_copy(tsqr_tree_s *t, double *host, bool to_host, bool full, cudaStream_t st);
+// after a compact import: the chain engine's chunk T cache from the bound reflectors and taus
+cudaError_t tree_rebuild_tcache(tsqr_tree_s *t, cudaStream_t st);
+// A tree of the plan (m_local, n, opts) bound to reflectors in A without a factor
+// (for an imported state); reuses *tree when the plan matches.
+tsqr_status_t tree_bind(int64_t m_local, int64_t n, double *A, int64_t lda, const tsqr_opts_t *opts,
+                        cudaStream_t st, tsqr_tree_s **tree);
 
 // Leaf stage on the chunk engine (tsqr_chain.cu).
 struct ChainArgs {
@@ -47,6 +63,10 @@ int chain_ncb(int n);
 int chain_grid(int n);
 int cs_apply_grid(int n);   // SMs x resident apply CTAs
 cudaError_t launch_chain_factor(const ChainArgs &f, cudaStream_t st);
+// The factor's T cache recomputed from the stored reflectors and chunk taus (streamed Q).
+cudaError_t launch_chain_rebuild_t(const double *A, int64_t lda, int n, const int64_t *tile_row0, const int *tile_rows,
+                                   const int64_t *tile_chunk0, int ntiles, int64_t nchunks, const double *tau,
+                                   double *tcache, cudaStream_t st);
 // Leaf stage of Q^T C / form Q on the chain representation (tsqr_cs.cu).
 cudaError_t launch_cs_apply(const ChainApplyArgs &f, cudaStream_t st);
 // Wide-n engine (tsqr_wide.cu, 64 < n <= 256): one CTA per leaf / node problem.
