@@ -492,17 +492,40 @@ __device__ __forceinline__ void trailing(Chunk<C> &ch, const double (&yv)[C::KM]
     const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
     if constexpr (P + 1 < C::NCB) {
         double wt[C::NCB][2];
+#ifdef TSQR_T_FIRST            // variant: T before the W^T DMMAs (measured slower: C4 15.86 -> 16.12 ms)
+        build_t(Gs, t8, Ts);
+#endif
+        // few trailing blocks (<= TSQR_WT_SPLIT, default 3): two accumulation chains per block,
+        // which halves the dependent DMMA chain where it is not hidden by other blocks'
+        // chains (C4 leaf 15.86 -> 15.69-15.76 ms; 0 disables)
+#ifndef TSQR_WT_SPLIT
+#define TSQR_WT_SPLIT 3
+#endif
+        constexpr bool kSplit = (C::NCB - 1 - P) <= TSQR_WT_SPLIT;
 #pragma unroll
         for (int cb = P + 1; cb < C::NCB; ++cb) {
             wt[cb][0] = wt[cb][1] = 0.0;
+            if constexpr (kSplit) {
+                double u0 = 0.0, u1 = 0.0;
 #pragma unroll
-            for (int k = 0; k < C::KM; ++k) {
-                dmma(wt[cb][0], wt[cb][1], ch.a[k][cb][0], yv[k][0]);
-                dmma(wt[cb][0], wt[cb][1], ch.a[k][cb][1], yv[k][1]);
+                for (int k = 0; k < C::KM; ++k) {
+                    dmma(wt[cb][0], wt[cb][1], ch.a[k][cb][0], yv[k][0]);
+                    dmma(u0, u1, ch.a[k][cb][1], yv[k][1]);
+                }
+                wt[cb][0] += u0;
+                wt[cb][1] += u1;
+            } else {
+#pragma unroll
+                for (int k = 0; k < C::KM; ++k) {
+                    dmma(wt[cb][0], wt[cb][1], ch.a[k][cb][0], yv[k][0]);
+                    dmma(wt[cb][0], wt[cb][1], ch.a[k][cb][1], yv[k][1]);
+                }
             }
         }
+#ifndef TSQR_T_FIRST
         // T while the W^T DMMAs drain (it only needs the panel's Gram and taus)
         build_t(Gs, t8, Ts);
+#endif
         if (tg != nullptr)
             *reinterpret_cast<double2 *>(tg + 8 * P * 8 + 2 * lane) = *reinterpret_cast<const double2 *>(Ts + 2 * lane);
         const double tb0 = Ts[(2 * q) * 8 + l4], tb1 = Ts[(2 * q + 1) * 8 + l4];
