@@ -265,10 +265,18 @@ static int build_plan(int64_t m, int64_t n, int64_t b, int64_t s, int64_t G, pla
         int64_t t = (s == 0) ? 1 : (h + s - 1) / s;   /* s = 0: one tile per block */
         if (t > h / n) t = h / n;                      /* never a tile shorter than n */
         if (t < 1) t = 1;
+        /* near-equal tiles of EVEN height: the block's row pairs are split near-equally
+         * (the first (h/2 mod t) tiles one pair taller), the last tile takes what is left
+         * (one row more when h is odd); if that would leave a tile shorter than n, plain
+         * near-equal heights (the first h mod t tiles one row taller) */
         int64_t base = h / t, extra = h - base * t;
+        const int64_t pb = (h / 2) / t, pe = (h / 2) - pb * t;
+        const int64_t last_even = h - 2 * (pb * (t - 1) + (pe < t - 1 ? pe : t - 1));
+        const int even = t > 1 && 2 * pb >= n && last_even >= n;
         int64_t r0 = blk_row0[k];
         for (int64_t i = 0; i < t; ++i) {
             int64_t rows = base + (i < extra ? 1 : 0);
+            if (even) rows = (i < t - 1) ? 2 * (pb + (i < pe ? 1 : 0)) : last_even;
             if (rows < n) { free(blk_row0); free(blk_rows); free(blk_tile0); return -1; }
             if (!p->count_only) { p->tile_row0[nt] = r0; p->tile_rows[nt] = rows; }
             r0 += rows;

@@ -98,8 +98,11 @@ void orc_build_t_node(int64_t n, const double *Y1, int64_t ldy, const double *ta
  * Ranks: contiguous runs of whole blocks, the first (nblocks mod G) ranks get
  * one extra block.
  * Tiles: a block of h rows is split into t = min(ceil(h/s), floor(h/n)) (at
- * least 1) tiles of near-equal height, the first (h mod t) tiles one row
- * taller; s = 0 means one tile per block (the paper's plan, tiles = row blocks).
+ * least 1) tiles of near-equal EVEN height: the floor(h/2) row pairs split
+ * near-equally (the first (floor(h/2) mod t) tiles one pair taller), the last
+ * tile taking the rest; when that leaves a tile shorter than n, plain
+ * near-equal heights (the first (h mod t) tiles one row taller); s = 0 means
+ * one tile per block (the paper's plan, tiles = row blocks).
  * Nodes are listed in execution order: level by level inside every block,
  * then level by level over the blocks of each rank, then the rank levels.
  * A node is the pair (a, b) of the leftmost tiles of its left and right

@@ -327,7 +327,11 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
     // the panel (scl: this lane's column's scale), so each step updates with one
     // FMA per value: the pivot and finished columns get u = 0.
     double scl = 1.0;
+#ifdef TSQR_UNROLL_STEPS          // variant: the panel's 8 structured steps unrolled
+#pragma unroll
+#else
 #pragma unroll 1
+#endif
     for (int jj = 0; jj < jn; ++jj) {
         const int j = 8 * P + jj;
         const double *xr = xs + (jj & 1) * C::CH;

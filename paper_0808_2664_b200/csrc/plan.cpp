@@ -86,8 +86,15 @@ int build_plan(int64_t m_local, int64_t n, int64_t block_rows, int64_t tile_rows
         // tiles of near-equal height, never shorter than n
         const int64_t t = std::max<int64_t>(1, std::min<int64_t>((h + s - 1) / s, h / n));
         p->blk_tile0.push_back((int)p->tile_row0.size());
+        // even heights when every tile keeps >= n rows (row pairs split near-equally, the
+        // last tile takes the rest): with an even block start every tile then starts on an
+        // even row, as the leaf kernel's TMA staging needs
+        const int64_t pb = (h / 2) / t, pe = (h / 2) % t;
+        const int64_t last_even = h - 2 * (pb * (t - 1) + std::min<int64_t>(pe, t - 1));
+        const bool even = t > 1 && 2 * pb >= n && last_even >= n;
         for (int64_t i = 0; i < t; ++i) {
-            const int64_t rows = h / t + (i < h % t ? 1 : 0);
+            const int64_t rows = even ? (i < t - 1 ? 2 * (pb + (i < pe ? 1 : 0)) : last_even)
+                                      : h / t + (i < h % t ? 1 : 0);
             if (rows < n) return TSQR_ERR_SHAPE;
             if (rows > cap) return TSQR_ERR_UNSUPPORTED;
             p->tile_row0.push_back(row);

@@ -265,8 +265,16 @@ def test_plan_remainder_rules():
     # remainder >= n becomes its own block; < n merges into the last block (reading R6)
     p = orc.plan(1000 + 10, 16, 500)
     assert list(p.tile_rows) == [500, 510]
+    # tiles of even height: 250 row pairs over 3 tiles -> 84, 83, rest
     p = orc.plan(1000 + 10, 16, 500, 200)
-    assert list(p.tile_rows) == [167, 167, 166, 170, 170, 170]
+    assert list(p.tile_rows) == [168, 166, 166, 170, 170, 170]
+    assert all(r0 % 2 == 0 for r0 in p.tile_row0)
+    # an odd block: the last tile takes the odd row
+    p = orc.plan(1011, 16, 500, 200)
+    assert list(p.tile_rows) == [168, 166, 166, 170, 170, 171]
+    # even heights would leave a tile shorter than n: plain near-equal heights
+    p = orc.plan(99, 49, 99, 50)
+    assert list(p.tile_rows) == [50, 49]
     p = orc.plan(1000 + 16, 16, 500)
     assert list(p.tile_rows) == [500, 500, 16]
     # s < n: tiles are never shorter than n (t = min(ceil(h/s), floor(h/n)))
