@@ -95,12 +95,20 @@ def test_strided_storage(m, n, b, s, k):
     assert orc.rel_fro(orc.sign_normalise(Rg), orc.sign_normalise(f.R)) <= TOL_R
     assert orc.rel_fro(_np(C), orc.tsqr_apply_qt(f, C0)) <= TOL_R
     assert orc.rel_fro(_np(Q), orc.tsqr_form_q(f)) <= TOL_R
-    # the stored reflectors: the same bytes a contiguous factor leaves
+    # the stored reflectors, Q^T C and Q: the same bytes a contiguous factor gives.  The odd
+    # lda (m + 7) stages chunks by per-element cp.async, the contiguous even-lda copy by TMA /
+    # bulk copies wherever tiles start on even rows, so this also pins
+    # the two staging paths to each other bit for bit.
     A2 = At.cuda()
-    T.factor(A2, block_rows=b, tile_rows=s)
+    _, tree2 = T.factor(A2, block_rows=b, tile_rows=s)
+    C2 = Ct.cuda()
+    T.apply_qt(tree2, C2)
+    Q2 = T.form_q(tree2)
     torch.cuda.synchronize()
     assert torch.equal(A, A2)
+    assert torch.equal(C, C2) and torch.equal(Q, Q2)
     tree.free()
+    tree2.free()
 
 
 def test_first_factor_on_fresh_stream():
