@@ -334,6 +334,25 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
 #endif
     for (int jj = 0; jj < jn; ++jj) {
         const int j = 8 * P + jj;
+        // Where R row j (released by the previous chunk) is read, measured per configuration:
+        // for 56 < n <= 64 (one R buffer, 40-row chunks) counter and entries are read -- and
+        // waited for -- at the top of the step, so their latency overlaps the dots (C4 leaf
+        // 15.83 -> 15.27 ms); for the other configurations after the dots, where an early
+        // wait costs more than it hides (C2 0.818 -> 0.836 ms, C5 10.47 -> 10.71 ms).
+        constexpr bool kEarlyR = C::NCB == 8;
+        const volatile double *rr = Rb + j * C::LDR;
+        int c0 = 0;
+        double alpha = 0.0, rj = 0.0;
+        if constexpr (kEarlyR) {
+            c0 = ld_acquire_cta(sy.row + j);
+            alpha = rr[j];                                           // R(j, j)
+            rj = rr[8 * P + l4];                                     // R(j, 8P + l4)
+            if (c0 < sy.s) {
+                sync_wait(sy.row + j, sy.s);
+                alpha = rr[j];
+                rj = rr[8 * P + l4];
+            }
+        }
         const double *xr = xs + (jj & 1) * C::CH;
         double x[C::KM][2];
 #pragma unroll
@@ -355,16 +374,17 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
         dmma(d, dz, (dk[0][0] + dk[1][0]) + (dk[0][1] + dk[1][1]), 1.0);
         s2 = __shfl_sync(FULL, d, 4 * jj);
         PROBE(3);
-        // R row j released by the previous chunk: the counter and the row are read
-        // together, the row again only if the counter was short ("Hand-off
-        // ordering" above)
-        const volatile double *rr = Rb + j * C::LDR;
-        const int c0 = ld_acquire_cta(sy.row + j);
-        double alpha = rr[j], rj = rr[8 * P + l4];                   // R(j, j), R(j, 8P + l4)
-        if (c0 < sy.s) {
-            sync_wait(sy.row + j, sy.s);
+        if constexpr (!kEarlyR) {
+            // the counter and the row read together, the row again only if the counter was
+            // short ("Hand-off ordering" above)
+            c0 = ld_acquire_cta(sy.row + j);
             alpha = rr[j];
             rj = rr[8 * P + l4];
+            if (c0 < sy.s) {
+                sync_wait(sy.row + j, sy.s);
+                alpha = rr[j];
+                rj = rr[8 * P + l4];
+            }
         }
         PROBE(4);
         House h = house_bf(alpha, s2);
