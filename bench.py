@@ -69,12 +69,14 @@ def kernel_launches(info, n, op, world):
     """Kernels of this repo launched per step (tsqr_api.cu's dispatch): factor, then the second op."""
     multi = info["ntiles"] > 1
     rounds = info["cross_rounds"] if world > 1 else 0
+    # the node stages of apply / form Q are one pipelined launch for n <= 224 (else one per step)
+    nodes = (1 if multi else 0) if n <= 224 else info["depth"]
     if n <= 64:
         fac = 1 + 1                                   # chain leaves + pipelined tree (or R extraction)
-        second = (1 + multi) if op == "apply_qt" else (info["depth"] + 2)   # leaves+nodes | identity+node steps+leaves
+        second = (1 + nodes) if op == "apply_qt" else (2 + nodes)   # leaves+nodes | identity+nodes+leaves
     else:
         fac = 1 + multi + 1                           # leaves + pipelined tree + R extraction
-        second = (1 + info["depth"]) if op == "apply_qt" else (info["depth"] + 4)
+        second = (1 + nodes) if op == "apply_qt" else (3 + nodes)   # | identity+nodes+[X;0]+leaves
     # butterfly rounds: pack + combine per round on the factor; apply: one combine per round + top copy
     cross = 2 * rounds + (2 * rounds if op == "apply_qt" else 0)
     return fac + second + cross

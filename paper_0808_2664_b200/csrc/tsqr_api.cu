@@ -43,6 +43,7 @@ struct tsqr_tree_s {
     double *d_xbuf = nullptr;
     int *d_step_ids = nullptr;
     int *d_pipe_nodes = nullptr, *d_prod_l = nullptr, *d_prod_r = nullptr, *d_pipe_flags = nullptr;
+    int *d_parent = nullptr, *d_node_flags = nullptr;   // the one-launch node stages of apply / form Q
     int pipe_count = 0, pipe_root = -1;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};   // stage timing (opts.flags bit 1)
     bool ev_recorded = false;
@@ -130,7 +131,8 @@ static tsqr_status_t leave(tsqr_tree_s *t, cudaStream_t st) {
 static void free_tree_memory(tsqr_tree_s *t, cudaStream_t st) {
     void *ptrs[] = {t->d_row0, t->d_rows, t->d_node_a,
                     t->d_tau_node, t->d_cross_y1, t->d_cross_tau, t->d_xbuf,
-                    t->d_step_ids, t->d_pipe_nodes, t->d_prod_l, t->d_prod_r, t->d_pipe_flags,
+                    t->d_step_ids, t->d_pipe_nodes, t->d_prod_l, t->d_prod_r, t->d_pipe_flags, t->d_parent,
+                    t->d_node_flags,
                     t->d_tile_chunk0, t->d_cta_tile0, t->d_apply_cta_tile0, t->d_tau_chunk, t->d_tcache,
                     t->d_tcache_node, t->d_cross_tcache, t->d_wtmp, t->d_tcache_pair, t->d_gather};
     for (void *p : ptrs)
@@ -160,6 +162,45 @@ static int ilog2(int x) {
     int r = 0;
     while ((1 << r) < x) ++r;
     return r;
+}
+
+// The node stages of Q^T C (forward: bottom-up, after the leaves) or of Q C / form Q
+// (top-down, before the leaves) on C's tile heads (xbuf_mode: the per-tile X blocks):
+// one pipelined launch over the whole tree when the node kernel fits (n <= 224), else
+// one launch per tree step.
+static cudaError_t node_stages(tsqr_tree_s *t, double *C, int64_t ldc, int k, bool forward, int xbuf_mode,
+                               cudaStream_t st) {
+    const int n = (int)t->plan.n, L = t->plan.ntiles();
+    const int count = t->step_off.back();
+    if (count == 0) return cudaSuccess;
+    if ((n + 7) / 8 <= 28) {
+        return forward ? launch_node_apply_pipe(t->A, t->lda, n, t->d_row0, t->d_node_a, t->d_pipe_nodes, count,
+                                                t->d_prod_l, t->d_prod_r, t->d_node_flags, L, t->d_tcache_node, C,
+                                                ldc, k, 1, xbuf_mode, st)
+                       : launch_node_apply_pipe(t->A, t->lda, n, t->d_row0, t->d_node_a, t->d_step_ids, count,
+                                                t->d_parent, nullptr, t->d_node_flags, L, t->d_tcache_node, C, ldc,
+                                                k, 0, xbuf_mode, st);
+    }
+    if (forward) {
+        for (size_t g = t->step_off.size() - 1; g-- > 0;) {             // tree steps bottom-up
+            const int cnt = t->step_off[g + 1] - t->step_off[g];
+            if (cnt == 0) continue;
+            const cudaError_t e = launch_node_apply(t->A, t->lda, n, t->d_row0, t->d_node_a,
+                                                    t->d_step_ids + t->step_off[g], cnt, t->d_tcache_node, C, ldc,
+                                                    k, 1, xbuf_mode, st);
+            if (e != cudaSuccess) return e;
+        }
+    } else {
+        for (size_t g = 0; g + 1 < t->step_off.size(); ++g) {             // tree steps top-down
+            const int cnt = t->step_off[g + 1] - t->step_off[g];
+            if (cnt == 0) continue;
+            const cudaError_t e = launch_node_apply(t->A, t->lda, n, t->d_row0, t->d_node_a,
+                                                    t->d_step_ids + t->step_off[g], cnt, t->d_tcache_node, C, ldc,
+                                                    k, 0, xbuf_mode, st);
+            if (e != cudaSuccess) return e;
+        }
+    }
+    return cudaSuccess;
 }
 
 extern "C" {
@@ -310,6 +351,15 @@ static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t 
     alloc((void **)&t->d_prod_l, sizeof(int) * L);
     alloc((void **)&t->d_prod_r, sizeof(int) * L);
     alloc((void **)&t->d_pipe_flags, sizeof(int) * (L * 32 + 1));   // L x panels (<= 28 wide, 8 narrow) + ticket
+    // top-down dependency of the node stages: each node's parent (the node that writes the
+    // head block this node reads); bottom-up it is prod_l / prod_r
+    std::vector<int> parent(L, -1);
+    for (int b : pipe) {
+        if (prod_l[b] >= 0) parent[prod_l[b]] = b;
+        if (prod_r[b] >= 0) parent[prod_r[b]] = b;
+    }
+    alloc((void **)&t->d_parent, sizeof(int) * L);
+    alloc((void **)&t->d_node_flags, sizeof(int) * (L + 1));
     const int64_t nchunks = p.tile_chunk0[L];
     t->wide = n > 64;
     t->npan = (int)((n + 7) / 8);
@@ -365,6 +415,7 @@ static tsqr_status_t create_tree(int64_t m_local, int64_t n, double *A, int64_t 
     h2d(t->d_pipe_nodes, pipe.data(), sizeof(int) * pipe.size());
     h2d(t->d_prod_l, prod_l.data(), sizeof(int) * L);
     h2d(t->d_prod_r, prod_r.data(), sizeof(int) * L);
+    h2d(t->d_parent, parent.data(), sizeof(int) * L);
     h2d(t->d_tile_chunk0, p.tile_chunk0.data(), sizeof(int64_t) * (L + 1));
     h2d(t->d_cta_tile0, cta_tile0.data(), sizeof(int) * (grid + 1));
     h2d(t->d_apply_cta_tile0, apply_tile0.data(), sizeof(int) * (agrid + 1));
@@ -603,23 +654,10 @@ tsqr_status_t tsqr_apply_qt(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, do
                                           (int)t->plan.max_rows, t->d_tcache, t->d_tcache_pair, C, ldc, (int)k, 1,
                                           st),
                  "tsqr_apply_qt leaves");
-        for (size_t g = t->step_off.size() - 1; g-- > 0;) {         // tree steps bottom-up
-            const int cnt = t->step_off[g + 1] - t->step_off[g];
-            if (cnt == 0) continue;
-            CUDA_TRY(launch_node_apply(t->A, t->lda, n, t->d_row0, t->d_node_a, t->d_step_ids + t->step_off[g],
-                                             cnt, t->d_tcache_node, C, ldc, (int)k, 1, 0, st),
-                     "tsqr_apply_qt nodes");
-        }
+        CUDA_TRY(node_stages(t, C, ldc, (int)k, true, 0, st), "tsqr_apply_qt nodes");
     } else {
         CUDA_TRY(launch_cs_apply(ca, st), "tsqr_apply_qt leaves");
-        for (size_t g = t->step_off.size() - 1; g-- > 0;) {         // tree steps bottom-up
-            const int cnt = t->step_off[g + 1] - t->step_off[g];
-            if (cnt == 0) continue;
-            CUDA_TRY(launch_node_apply(t->A, t->lda, (int)t->plan.n, t->d_row0, t->d_node_a,
-                                             t->d_step_ids + t->step_off[g], cnt, t->d_tcache_node, C, ldc, (int)k, 1,
-                                             0, st),
-                     "tsqr_apply_qt nodes");
-        }
+        CUDA_TRY(node_stages(t, C, ldc, (int)k, true, 0, st), "tsqr_apply_qt nodes");
     }
     if (top) CUDA_TRY(launch_copy_block(C, ldc, top, ldtop, (int)t->plan.n, (int)k, st), "tsqr_apply_qt top");
     return finish(t, st, "tsqr_apply_qt");
@@ -695,13 +733,7 @@ tsqr_status_t tsqr_apply_q(tsqr_tree_t t, double *C, int64_t ldc, int64_t k, voi
     const int n = (int)t->plan.n;
     cudaStream_t st = (cudaStream_t)stream;
     ENTER(t, st);
-    for (size_t g = 0; g + 1 < t->step_off.size(); ++g) {             // tree steps top-down
-        const int cnt = t->step_off[g + 1] - t->step_off[g];
-        if (cnt == 0) continue;
-        CUDA_TRY(launch_node_apply(t->A, t->lda, n, t->d_row0, t->d_node_a, t->d_step_ids + t->step_off[g], cnt,
-                                   t->d_tcache_node, C, ldc, (int)k, 0, 0, st),
-                 "tsqr_apply_q nodes");
-    }
+    CUDA_TRY(node_stages(t, C, ldc, (int)k, false, 0, st), "tsqr_apply_q nodes");
     if (t->wide) {
         CUDA_TRY(launch_wide_apply_leaves(t->A, t->lda, n, t->d_row0, t->d_rows, t->plan.ntiles(),
                                           (int)t->plan.max_rows, t->d_tcache, t->d_tcache_pair, C, ldc, (int)k, 0, st),
@@ -742,13 +774,7 @@ tsqr_status_t tsqr_form_q(tsqr_tree_t t, double *Q, int64_t ldq, void *stream) {
         CUDA_TRY(launch_wide_cross_root_x(t->d_cross_y1, t->d_cross_tcache, (int64_t)t->npan * 64, t->cross_rounds,
                                           t->opts.rank, n, t->d_wtmp, t->d_xbuf, st),
                  "tsqr_form_q root");
-        for (size_t g = 0; g + 1 < t->step_off.size(); ++g) {         // tree steps top-down
-            const int cnt = t->step_off[g + 1] - t->step_off[g];
-            if (cnt == 0) continue;
-            CUDA_TRY(launch_node_apply(t->A, t->lda, n, t->d_row0, t->d_node_a, t->d_step_ids + t->step_off[g],
-                                             cnt, t->d_tcache_node, t->d_xbuf, n, n, 0, 1, st),
-                     "tsqr_form_q nodes");
-        }
+        CUDA_TRY(node_stages(t, t->d_xbuf, n, n, false, 1, st), "tsqr_form_q nodes");
         CUDA_TRY(launch_wide_formq_init(t->d_row0, t->d_rows, L, n, t->d_xbuf, Q, ldq, st), "tsqr_form_q");
         CUDA_TRY(launch_wide_apply_leaves(t->A, t->lda, n, t->d_row0, t->d_rows, L, (int)t->plan.max_rows,
                                           t->d_tcache, t->d_tcache_pair, Q, ldq, n, 0, st),
@@ -763,13 +789,7 @@ tsqr_status_t tsqr_form_q(tsqr_tree_t t, double *Q, int64_t ldq, void *stream) {
         CUDA_TRY(launch_cross_root_x(t->NP, t->d_cross_y1, t->d_cross_tau, t->cross_rounds, t->opts.rank, n,
                                      t->d_xbuf, st),
                  "tsqr_form_q root");
-    for (size_t g = 0; g + 1 < t->step_off.size(); ++g) {         // tree steps top-down
-        const int cnt = t->step_off[g + 1] - t->step_off[g];
-        if (cnt == 0) continue;
-        CUDA_TRY(launch_node_apply(t->A, t->lda, n, t->d_row0, t->d_node_a, t->d_step_ids + t->step_off[g],
-                                         cnt, t->d_tcache_node, t->d_xbuf, n, n, 0, 1, st),
-                 "tsqr_form_q nodes");
-    }
+    CUDA_TRY(node_stages(t, t->d_xbuf, n, n, false, 1, st), "tsqr_form_q nodes");
     ChainApplyArgs ca;
     ca.A = t->A; ca.lda = t->lda; ca.n = n; ca.chunk_rows = t->plan.c; ca.bulk = t->rows_even;
     ca.tile_row0 = t->d_row0; ca.tile_rows = t->d_rows; ca.tile_chunk0 = t->d_tile_chunk0;

@@ -83,6 +83,10 @@ cudaError_t launch_wide_apply_leaves(const double *A, int64_t lda, int n, const 
 cudaError_t launch_node_apply(const double *A, int64_t lda, int n, const int64_t *row0, const int *node_a,
                                     const int *ids, int count, const double *tcache_node, double *C, int64_t ldc,
                                     int k, int forward, int xbuf_mode, cudaStream_t st);
+cudaError_t launch_node_apply_pipe(const double *A, int64_t lda, int n, const int64_t *row0, const int *node_a,
+                                   const int *ids, int count, const int *dep0, const int *dep1, int *flags, int L,
+                                   const double *tcache_node, double *C, int64_t ldc, int k, int forward,
+                                   int xbuf_mode, cudaStream_t st);
 cudaError_t launch_wide_apply_node1(const double *Y1, int64_t ldy, int n, const double *tcache, double *Ca,
                                     int64_t ldca, double *Cb, int64_t ldcb, int k, int forward, cudaStream_t st);
 cudaError_t launch_wide_formq_init(const int64_t *row0, const int *rows, int L, int n, const double *xbuf, double *Q,

@@ -924,20 +924,35 @@ k_wide_apply_nodes(const double *A, int64_t lda, int n, const int64_t *tile_row0
     wide_apply<kFwd>(P, Cp, n, k, tcache_node + (int64_t)b * npan * 64);
 }
 
-// Q^T / Q of one tree step's nodes for npan <= 28: the node's Y1 (upper
-// block triangle of the right subtree's head, 8x8 column-major blocks) and
-// its panels' T are staged in shared memory once; every warp then owns an
-// 8-column slab of C and runs all panels alone: C_b's head rows (n x 8) in
-// registers, C_a's row block P read and written back per panel (the identity
-// part of the node's reflectors).  No barrier after the staging.
+// Q^T / Q of tree nodes for npan <= 28: the node's Y1 (upper block triangle of
+// the right subtree's head, 8x8 column-major blocks) and its panels' T are
+// staged in shared memory once; every warp then owns an 8-column slab of C and
+// runs all panels alone: C_b's head rows (n x 8) in registers, C_a's row block P
+// read and written back per panel (the identity part of the node's reflectors).
+// No barrier after the staging.
+// Launched either per tree step (ids = the step's nodes, one CTA each) or, with
+// `flags`, once for the whole tree: ids is every node in dependency order
+// (bottom-up for Q^T, top-down for Q), each CTA takes the next node from a ticket
+// counter (flags[L]) when it starts -- so it only ever waits on nodes taken
+// earlier, which are resident or done -- stages the node's factors, waits until
+// the nodes it depends on (dep0/dep1: the producers of its two C head blocks
+// bottom-up, its parent top-down; -1 none) have set their flags, applies the
+// node and sets its own flag.  Levels overlap: the critical path is the tree's
+// depth in node latencies instead of one launch per step.
 constexpr int NPAN_NODE = 28;
 template <bool kFwd, int NPAN_NODE>
 __global__ void __launch_bounds__(NT, 1)
 k_node_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const int *node_a,
-                       const int *ids, const double *tcache_node, double *C, int64_t ldc, int k, int xbuf_mode) {
+                       const int *ids, const double *tcache_node, double *C, int64_t ldc, int k, int xbuf_mode,
+                       int *flags, int L, const int *dep0, const int *dep1) {
     extern __shared__ __align__(16) double smraw[];
+    __shared__ int s_idx;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
-    const int b = ids[blockIdx.x], a = node_a[b];
+    if (flags) {
+        if (threadIdx.x == 0) s_idx = atomicAdd(flags + L, 1);
+        __syncthreads();
+    }
+    const int b = ids[flags ? s_idx : blockIdx.x], a = node_a[b];
     const int npan = (n + 7) / 8;
     const int nb = npan * (npan + 1) / 2;
     double *Yb = smraw, *Tn = smraw + 64 * nb;
@@ -955,6 +970,14 @@ k_node_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, cons
     }
     const double *tc = tcache_node + (int64_t)b * npan * 64;
     for (int e = threadIdx.x; e < 64 * npan; e += NT) cp_async8(Tn + e, tc + e, true);
+    if (flags && threadIdx.x == 0) {                  // the producers of this node's inputs
+        const int d0 = dep0[b], d1 = dep1 ? dep1[b] : -1;
+        if (d0 >= 0)
+            while (*reinterpret_cast<volatile int *>(flags + d0) == 0) __nanosleep(64);
+        if (d1 >= 0)
+            while (*reinterpret_cast<volatile int *>(flags + d1) == 0) __nanosleep(64);
+        __threadfence();
+    }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncthreads();
     double *Ca, *Cb;
@@ -1043,6 +1066,13 @@ k_node_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, cons
                 const int r = 8 * kk + 2 * q + e;
                 if (okc && kk < npan && r < n) Cb[r + co] = cb[kk][e];
             }
+    }
+    if (flags) {                                      // this node's C blocks are final
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            *reinterpret_cast<volatile int *>(flags + b) = 1;
+        }
     }
 }
 
@@ -1158,7 +1188,7 @@ cudaError_t launch_node_apply(const double *A, int64_t lda, int n, const int64_t
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
             if (e != cudaSuccess) return e;
             k_node_apply<F, NPM><<<count, NT, bytes, st>>>(A, lda, n, row0, node_a, ids, tcache_node, C, ldc,
-                                                                     k, xbuf_mode);
+                                                                     k, xbuf_mode, nullptr, 0, nullptr, nullptr);
             return cudaGetLastError();
         };
         using T8 = std::integral_constant<int, 8>;
@@ -1171,6 +1201,34 @@ cudaError_t launch_node_apply(const double *A, int64_t lda, int n, const int64_t
     else
         k_wide_apply_nodes<false><<<count, NT, 0, st>>>(A, lda, n, row0, node_a, ids, tcache_node, C, ldc, k, xbuf_mode);
     return cudaGetLastError();
+}
+
+// The whole tree's node stage in one launch (k_node_apply with flags), npan <= 28:
+// ids = every node in dependency order; flags[L + 1] scratch (zeroed here).
+cudaError_t launch_node_apply_pipe(const double *A, int64_t lda, int n, const int64_t *row0, const int *node_a,
+                                   const int *ids, int count, const int *dep0, const int *dep1, int *flags, int L,
+                                   const double *tcache_node, double *C, int64_t ldc, int k, int forward,
+                                   int xbuf_mode, cudaStream_t st) {
+    const int npan = (n + 7) / 8;
+    if (npan > NPAN_NODE) return cudaErrorNotSupported;
+    if (count == 0) return cudaSuccess;
+    cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (L + 1), st);
+    if (e != cudaSuccess) return e;
+    const size_t bytes = sizeof(double) * 64 * (npan * (npan + 1) / 2 + npan);
+    auto go = [&](auto kf, auto np) -> cudaError_t {
+        constexpr bool F = decltype(kf)::value;
+        constexpr int NPM = decltype(np)::value;
+        cudaError_t r = cudaFuncSetAttribute((const void *)k_node_apply<F, NPM>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+        if (r != cudaSuccess) return r;
+        k_node_apply<F, NPM><<<count, NT, bytes, st>>>(A, lda, n, row0, node_a, ids, tcache_node, C, ldc, k,
+                                                       xbuf_mode, flags, L, dep0, dep1);
+        return cudaGetLastError();
+    };
+    using T8 = std::integral_constant<int, 8>;
+    using T28 = std::integral_constant<int, NPAN_NODE>;
+    if (forward) return npan <= 8 ? go(std::true_type(), T8()) : go(std::true_type(), T28());
+    return npan <= 8 ? go(std::false_type(), T8()) : go(std::false_type(), T28());
 }
 
 cudaError_t launch_wide_apply_node1(const double *Y1, int64_t ldy, int n, const double *tcache, double *Ca,
