@@ -158,3 +158,28 @@ def test_plain_plan_parity(m, n, b, s, kind):
     assert np.linalg.norm(A0 - Qg @ Rg) / np.linalg.norm(A0) <= TOL_INV
     assert np.linalg.norm(Qg.T @ Qg - np.eye(n)) <= TOL_INV
     tree.free()
+
+
+@pytest.mark.parametrize("m,n,b,s", [(200_000, 50, 4096, 1024), (60_000, 100, 2048, 400), (100_000, 64, 4096, 4096)])
+def test_rank_deficient_full_engines(m, n, b, s):
+    """Rank-deficient input at scale on both leaf engines (chain n <= 64, wide n > 64): a
+    duplicated column and a zero column.  R is not unique past a dependent column (its later
+    rows are set by rounding), so the invariants are checked: A = QR, Q^T Q = I (the Householder
+    Q stays orthogonal whatever the rank), exact zeros below R's diagonal, and the dependent
+    columns' diagonal entries at rounding level."""
+    At = inputs.gaussian(m, n, 31)
+    At[10] = At[3]                       # column 10 = column 3 (tensor rows are matrix columns)
+    At[20] = 0.0
+    A0 = _np(At).copy()
+    A = At.cuda()
+    R, tree = T.factor(A, block_rows=b, tile_rows=s)
+    Q = T.form_q(tree)
+    torch.cuda.synchronize()
+    Rg, Qg = _np(R), _np(Q)
+    assert np.all(np.isfinite(Rg)) and np.all(np.isfinite(Qg))
+    assert np.all(np.tril(Rg, -1) == 0.0)
+    nA = np.linalg.norm(A0)
+    assert np.linalg.norm(A0 - Qg @ Rg) / nA <= TOL_INV
+    assert np.linalg.norm(Qg.T @ Qg - np.eye(n)) <= TOL_INV
+    assert abs(Rg[10, 10]) <= 1e-13 * nA and abs(Rg[20, 20]) <= 1e-13 * nA
+    tree.free()
