@@ -327,11 +327,7 @@ __device__ __forceinline__ void panel_structured(Chunk<C> &ch, double *Rb, doubl
     // the panel (scl: this lane's column's scale), so each step updates with one
     // FMA per value: the pivot and finished columns get u = 0.
     double scl = 1.0;
-#ifdef TSQR_UNROLL_STEPS          // variant: the panel's 8 structured steps unrolled
-#pragma unroll
-#else
-#pragma unroll 1
-#endif
+#pragma unroll 1                  // unrolled, the kernel's code grows 1.5x and runs 27 % slower (C4)
     for (int jj = 0; jj < jn; ++jj) {
         const int j = 8 * P + jj;
         // Where R row j (released by the previous chunk) is read, measured per configuration:
@@ -516,9 +512,6 @@ __device__ __forceinline__ void trailing(Chunk<C> &ch, const double (&yv)[C::KM]
     const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
     if constexpr (P + 1 < C::NCB) {
         double wt[C::NCB][2];
-#ifdef TSQR_T_FIRST            // variant: T before the W^T DMMAs (measured slower: C4 15.86 -> 16.12 ms)
-        build_t(Gs, t8, Ts);
-#endif
         // few trailing blocks (<= TSQR_WT_SPLIT, default 3): two accumulation chains per block,
         // which halves the dependent DMMA chain where it is not hidden by other blocks'
         // chains (C4 leaf 15.86 -> 15.69-15.76 ms; 0 disables)
@@ -546,10 +539,9 @@ __device__ __forceinline__ void trailing(Chunk<C> &ch, const double (&yv)[C::KM]
                 }
             }
         }
-#ifndef TSQR_T_FIRST
-        // T while the W^T DMMAs drain (it only needs the panel's Gram and taus)
+        // T while the W^T DMMAs drain (it only needs the panel's Gram and taus; built before
+        // them, or one column per step inside the steps, it measured slower)
         build_t(Gs, t8, Ts);
-#endif
         if (tg != nullptr)
             *reinterpret_cast<double2 *>(tg + 8 * P * 8 + 2 * lane) = *reinterpret_cast<const double2 *>(Ts + 2 * lane);
         const double tb0 = Ts[(2 * q) * 8 + l4], tb1 = Ts[(2 * q + 1) * 8 + l4];
