@@ -9,18 +9,19 @@
 #include "chunk.cuh"
 
 #include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 using namespace tsqr;
 using namespace tsqr::chunk;
 
 template <class C, bool kTrail>
-__global__ void __launch_bounds__(256, 1) k_probe(int iters, int n, unsigned long long *out, double *sink) {
+__global__ void __launch_bounds__(C::NT, 1) k_probe(int iters, int n, unsigned long long *out, double *sink) {
     extern __shared__ __align__(16) double sm[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     double *Rb = sm;                               // one R buffer for all warps (timing only)
     double *ws = sm + C::RBUF + warp * C::WS;
-    int *cnt = reinterpret_cast<int *>(sm + C::RBUF + 8 * C::WS) + warp * C::SYNC_INTS;
+    int *cnt = reinterpret_cast<int *>(sm + C::RBUF + 16 * C::WS) + warp * C::SYNC_INTS;
     PROBE_INIT();
     for (int i = lane; i < C::RBUF; i += 32) Rb[i] = (i % (C::LDR + 1) == 0) ? 3.0 : 0.01 * (i % 7);
     for (int i = lane; i < C::SYNC_INTS; i += 32) cnt[i] = 1 << 30;
@@ -42,7 +43,7 @@ __global__ void __launch_bounds__(256, 1) k_probe(int iters, int n, unsigned lon
         else panel_structured<C, 0, false>(ch, Rb, ws + C::GS, ws + C::T8, ws + C::XS, tau, n, sy);
     }
     const unsigned long long t1 = clock64();
-    if (lane == 0) out[blockIdx.x * 8 + warp] = t1 - t0;
+    if (lane == 0) out[blockIdx.x * 16 + warp] = t1 - t0;
     PROBE_FLUSH();
     double s = 0.0;
 #pragma unroll
@@ -62,9 +63,9 @@ void run(const char *name, int warps) {
     const int n = 8 * C::NCB, sms = 148;
     unsigned long long *out;
     double *sink;
-    cudaMalloc(&out, sizeof(unsigned long long) * sms * 8);
+    cudaMalloc(&out, sizeof(unsigned long long) * sms * 16);
     cudaMalloc(&sink, 8 * 256);
-    const size_t bytes = (size_t)(C::RBUF + 8 * C::WS + 8 * C::SYNC_INTS) * 8;
+    const size_t bytes = (size_t)(C::RBUF + 16 * C::WS + 16 * C::SYNC_INTS) * 8;
     cudaFuncSetAttribute((const void *)k_probe<C, kTrail>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
 #ifdef TSQR_PROBE
     unsigned long long *pb;
@@ -82,11 +83,11 @@ void run(const char *name, int warps) {
     cudaError_t err = cudaDeviceSynchronize();
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
-    std::vector<unsigned long long> h(sms * 8);
+    std::vector<unsigned long long> h(sms * 16);
     cudaMemcpy(h.data(), out, 8 * h.size(), cudaMemcpyDeviceToHost);
     double avg = 0;
     for (int b = 0; b < sms; ++b)
-        for (int w = 0; w < warps; ++w) avg += h[b * 8 + w];
+        for (int w = 0; w < warps; ++w) avg += h[b * 16 + w];
     avg /= sms * warps;
     // per chunk-panel: useful FMAs of the panel's steps (+ trailing): c rows x 8 cols x 2 x 8 steps
     // (dots + updates), + trailing c x 8 x nt x 2 x 2 (W and C update)
@@ -121,6 +122,16 @@ void run(const char *name, int warps) {
 }
 
 int main() {
+    const char *only = std::getenv("PROBE_ONLY");
+    if (only && only[0] == 'h') {     // half-chunk (32-column) chains at 8 and 12 warps vs the n64 chunk at 8
+        run<Cfg<8, 5, 8, 1>, false>("n64 c40 steps", 8);
+        run<Cfg<8, 5, 8, 1>, true>("n64 c40 steps+trail", 8);
+        run<Cfg<4, 5, 12>, false>("n32 c40 steps", 8);
+        run<Cfg<4, 5, 12>, true>("n32 c40 steps+trail", 8);
+        run<Cfg<4, 5, 12>, false>("n32 c40 steps", 12);
+        run<Cfg<4, 5, 12>, true>("n32 c40 steps+trail", 12);
+        return 0;
+    }
     for (int w : {1, 4, 8}) {
         run<Cfg<8, 5, 8, 1>, false>("n64 c40 steps", w);
         run<Cfg<8, 5, 8, 1>, true>("n64 c40 steps+trail", w);
