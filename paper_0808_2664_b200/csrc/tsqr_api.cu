@@ -44,6 +44,11 @@ struct tsqr_tree_s {
     int *d_step_ids = nullptr;
     int *d_pipe_nodes = nullptr, *d_prod_l = nullptr, *d_prod_r = nullptr, *d_pipe_flags = nullptr;
     int *d_parent = nullptr, *d_node_flags = nullptr;   // the one-launch node stages of apply / form Q
+    // the pipelined host path (tsqr_qr_host): per-slab CTA partitions of the leaf and form-Q
+    // kernels, slab k's at d_slab_part + slab_off[k] (leaves) / + slab_off[S + k] (form Q)
+    int slab_S = 0;
+    std::vector<int> slab_t0, slab_grid, slab_off;
+    int *d_slab_part = nullptr;
     int pipe_count = 0, pipe_root = -1;
     cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};   // stage timing (opts.flags bit 1)
     bool ev_recorded = false;
@@ -132,7 +137,7 @@ static void free_tree_memory(tsqr_tree_s *t, cudaStream_t st) {
     void *ptrs[] = {t->d_row0, t->d_rows, t->d_node_a,
                     t->d_tau_node, t->d_cross_y1, t->d_cross_tau, t->d_xbuf,
                     t->d_step_ids, t->d_pipe_nodes, t->d_prod_l, t->d_prod_r, t->d_pipe_flags, t->d_parent,
-                    t->d_node_flags,
+                    t->d_node_flags, t->d_slab_part,
                     t->d_tile_chunk0, t->d_cta_tile0, t->d_apply_cta_tile0, t->d_tau_chunk, t->d_tcache,
                     t->d_tcache_node, t->d_cross_tcache, t->d_wtmp, t->d_tcache_pair, t->d_gather};
     for (void *p : ptrs)
@@ -926,3 +931,141 @@ tsqr_status_t tsqr::tree_bind(int64_t m_local, int64_t n, double *A, int64_t lda
     return TSQR_OK;
 }
 
+
+// ------------------------------------------------- pipelined host path (e2e)
+// tsqr_qr_host with a HOST A and the explicit Q (n <= 64, one rank): the tiles are cut
+// into S slabs of whole tiles; slab k's rows go host->device on `up` and its leaves are
+// factored on `st` as soon as they land (the leaf QRs are independent, Eq. 1),
+// so the copy-in hides the leaf stage; then the tree and the form-Q node stages; then slab
+// k's form-Q leaves and its Q rows device->host on `down`, so the copy-out hides the
+// leaf stage of form Q.  Same kernels, same plan, same results as tsqr_factor +
+// tsqr_form_q (the CTA partition of the leaf kernels is per slab; no kernel's arithmetic
+// depends on it).
+tsqr_status_t tsqr::qr_host_pipelined(tsqr_tree_s **tree, int64_t m, int64_t n, const double *A, int64_t lda,
+                                      double *dA, double *dR, double *dQ, double *R, int64_t ldr, double *Q,
+                                      int64_t ldq, const tsqr_opts_t *opts, cudaStream_t st, cudaStream_t up,
+                                      cudaStream_t down, int S) {
+    if (n > 64 || (opts && opts->nranks > 1)) return TSQR_ERR_UNSUPPORTED;
+    // the tree of the plan, bound to dA (lda = m), exactly as tsqr_factor prepares it
+    {
+        Plan p;
+        tsqr_opts_t ro;
+        int rc;
+        try { rc = plan_for(m, n, opts, &p, &ro); } catch (const std::bad_alloc &) { return TSQR_ERR_ALLOC; }
+        if (rc) return (tsqr_status_t)rc;
+    }
+    tsqr_status_t s = tree_bind(m, n, dA, m, opts, st, tree);
+    if (s != TSQR_OK) return s;
+    tsqr_tree_s *t = *tree;
+    const int L = t->plan.ntiles();
+    S = std::max(1, std::min(S, L));
+    const Plan &p = t->plan;
+    if (t->slab_S != S || !t->d_slab_part) {       // the slabs' CTA partitions, once per (tree, S)
+        t->slab_t0.assign(S + 1, L);
+        const int64_t per = (m + S - 1) / S;
+        int tt = 0;
+        for (int k = 0; k < S; ++k) {
+            t->slab_t0[k] = tt;
+            while (tt < L && (p.tile_row0[tt] + p.tile_rows[tt] <= (int64_t)(k + 1) * per || k == S - 1)) ++tt;
+        }
+        t->slab_t0[S] = L;
+        std::vector<int> all;
+        t->slab_grid.assign(2 * S, 0);
+        t->slab_off.assign(2 * S, 0);
+        for (int pass = 0; pass < 2; ++pass)
+            for (int k = 0; k < S; ++k) {
+                const int a = t->slab_t0[k], b = t->slab_t0[k + 1];
+                std::vector<int64_t> rows(p.tile_rows.begin() + a, p.tile_rows.begin() + b);
+                const int g = std::max(1, std::min(b - a, pass == 0 ? chain_grid((int)n) : cs_apply_grid((int)n)));
+                std::vector<int> part;
+                if (b > a) chain_partition(rows, p.c, g, part);
+                else part.assign(g + 1, 0);
+                t->slab_grid[pass * S + k] = b > a ? g : 0;
+                t->slab_off[pass * S + k] = (int)all.size();
+                for (int v : part) all.push_back(v + a);
+            }
+        if (t->d_slab_part) cudaFreeAsync(t->d_slab_part, st);
+        t->d_slab_part = nullptr;
+        CUDA_TRY(cudaMallocAsync((void **)&t->d_slab_part, sizeof(int) * all.size(), st), "tsqr_qr_host slabs");
+        CUDA_TRY(cudaMemcpyAsync(t->d_slab_part, all.data(), sizeof(int) * all.size(), cudaMemcpyHostToDevice, st),
+                 "tsqr_qr_host slabs");
+        CUDA_TRY(cudaStreamSynchronize(st), "tsqr_qr_host slabs");   // the pageable source goes out of scope
+        t->slab_S = S;
+    }
+    std::vector<cudaEvent_t> ev(2 * S + 1, nullptr);
+    struct EvGuard {
+        std::vector<cudaEvent_t> &v;
+        ~EvGuard() {
+            for (cudaEvent_t e : v)
+                if (e) cudaEventDestroy(e);
+        }
+    } guard{ev};
+    for (cudaEvent_t &e : ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "tsqr_qr_host events");
+    const size_t D = sizeof(double);
+    // the side streams start behind the work already on st (allocations, the partition upload)
+    CUDA_TRY(cudaEventRecord(ev[2 * S], st), "tsqr_qr_host");
+    CUDA_TRY(cudaStreamWaitEvent(up, ev[2 * S], 0), "tsqr_qr_host");
+    CUDA_TRY(cudaStreamWaitEvent(down, ev[2 * S], 0), "tsqr_qr_host");
+    auto slab_rows = [&](int k, int64_t *r0, int64_t *rows) {
+        const int a = t->slab_t0[k], b = t->slab_t0[k + 1];
+        *r0 = a < L ? p.tile_row0[a] : m;
+        *rows = (b > a) ? p.tile_row0[b - 1] + p.tile_rows[b - 1] - *r0 : 0;
+    };
+    for (int k = 0; k < S; ++k) {                  // copy-in, slab by slab
+        int64_t r0, rows;
+        slab_rows(k, &r0, &rows);
+        if (rows > 0)
+            CUDA_TRY(cudaMemcpy2DAsync(dA + r0, D * m, A + r0, D * lda, D * rows, n, cudaMemcpyHostToDevice, up),
+                     "tsqr_qr_host copy in");
+        CUDA_TRY(cudaEventRecord(ev[k], up), "tsqr_qr_host");
+    }
+    t->opts.flags = resolve_opts(m, opts).flags & ~2;
+    t->ev_recorded = false;
+    ChainArgs ca;
+    ca.A = dA; ca.lda = m; ca.n = (int)n; ca.m = t->rows_even ? m : 0; ca.chunk_rows = p.c;
+    ca.tile_row0 = t->d_row0; ca.tile_rows = t->d_rows; ca.tile_chunk0 = t->d_tile_chunk0;
+    ca.tau = t->d_tau_chunk; ca.tcache = t->d_tcache; ca.robust = (t->opts.flags & TSQR_FLAG_ROBUST) != 0;
+    for (int k = 0; k < S; ++k) {                  // each slab's leaves as soon as it has landed
+        CUDA_TRY(cudaStreamWaitEvent(st, ev[k], 0), "tsqr_qr_host");
+        if (t->slab_grid[k] == 0) continue;
+        ca.cta_tile0 = t->d_slab_part + t->slab_off[k];
+        ca.grid = t->slab_grid[k];
+        CUDA_TRY(launch_chain_factor(ca, st), "tsqr_qr_host leaves");
+    }
+    if (t->pipe_count == 0) CUDA_TRY(launch_extract_r(dA, m, (int)n, dR, n, st), "tsqr_qr_host R");
+    else
+        CUDA_TRY(launch_tree_pipe(dA, m, (int)n, t->d_row0, t->d_node_a, t->d_pipe_nodes, t->pipe_count, t->d_prod_l,
+                                  t->d_prod_r, t->d_pipe_flags, t->d_tau_node, t->pipe_root, dR, n, t->d_tcache_node,
+                                  st),
+                 "tsqr_qr_host tree");
+    // form Q: the root X = I, the node stages, then slab by slab the leaves and the copy-out
+    if (!t->d_xbuf) CUDA_TRY(cudaMallocAsync((void **)&t->d_xbuf, D * (size_t)L * n * n, st), "tsqr_qr_host xbuf");
+    if (L > 1) CUDA_TRY(cudaMemsetAsync(t->d_xbuf, 0, D * (size_t)L * n * n, st), "tsqr_qr_host");
+    CUDA_TRY(launch_identity(t->d_xbuf, (int)n, st), "tsqr_qr_host identity");
+    CUDA_TRY(node_stages(t, t->d_xbuf, n, (int)n, false, 1, st), "tsqr_qr_host nodes");
+    ChainApplyArgs qa;
+    qa.A = dA; qa.lda = m; qa.n = (int)n; qa.chunk_rows = p.c; qa.bulk = t->rows_even;
+    qa.tile_row0 = t->d_row0; qa.tile_rows = t->d_rows; qa.tile_chunk0 = t->d_tile_chunk0; qa.tcache = t->d_tcache;
+    qa.C = dQ; qa.ldc = m; qa.k = (int)n; qa.forward = 0; qa.xbuf = t->d_xbuf;
+    for (int k = 0; k < S; ++k) {
+        int64_t r0, rows;
+        slab_rows(k, &r0, &rows);
+        if (t->slab_grid[S + k] > 0) {
+            qa.cta_tile0 = t->d_slab_part + t->slab_off[S + k];
+            qa.grid = t->slab_grid[S + k];
+            CUDA_TRY(launch_cs_apply(qa, st), "tsqr_qr_host form Q leaves");
+        }
+        CUDA_TRY(cudaEventRecord(ev[S + k], st), "tsqr_qr_host");
+        CUDA_TRY(cudaStreamWaitEvent(down, ev[S + k], 0), "tsqr_qr_host");
+        if (rows > 0)
+            CUDA_TRY(cudaMemcpy2DAsync(Q + r0, D * ldq, dQ + r0, D * m, D * rows, n, cudaMemcpyDeviceToHost, down),
+                     "tsqr_qr_host copy out");
+    }
+    CUDA_TRY(cudaMemcpy2DAsync(R, D * ldr, dR, D * n, D * n, n, cudaMemcpyDeviceToHost, st), "tsqr_qr_host R out");
+    CUDA_TRY(cudaEventRecord(ev[2 * S], down), "tsqr_qr_host");
+    CUDA_TRY(cudaStreamWaitEvent(st, ev[2 * S], 0), "tsqr_qr_host");
+    s = leave(t, st);
+    if (s != TSQR_OK) return s;
+    CUDA_TRY(cudaStreamSynchronize(st), "tsqr_qr_host");
+    return TSQR_OK;
+}

@@ -6,6 +6,7 @@
 #include "../../include/tsqr.h"
 #include "tsqr_kernels.h"
 
+#include <algorithm>
 #include <new>
 
 struct tsqr_host_ws_s {
@@ -14,6 +15,7 @@ struct tsqr_host_ws_s {
     double *A = nullptr, *R = nullptr, *Q = nullptr, *C = nullptr;
     tsqr_tree_t tree = nullptr;
     cudaStream_t st = nullptr;
+    cudaStream_t up = nullptr, down = nullptr;   // the pipelined path's copy streams
 };
 
 namespace {
@@ -24,6 +26,13 @@ tsqr_status_t fail(cudaError_t e, const char *where) {
 }
 
 void release(tsqr_host_ws_s *w) {
+    for (cudaStream_t *sp : {&w->up, &w->down}) {
+        if (*sp) {
+            cudaStreamSynchronize(*sp);
+            cudaStreamDestroy(*sp);
+        }
+        *sp = nullptr;
+    }
     if (w->tree) tsqr_tree_free(w->tree);
     w->tree = nullptr;
     for (double **p : {&w->A, &w->R, &w->Q, &w->C}) {
@@ -75,6 +84,17 @@ tsqr_status_t tsqr_qr_host(tsqr_host_ws_t *ws, int64_t m, int64_t n, const doubl
     }
     w->st = st;
     const size_t d = sizeof(double);
+    if (Q && k == 0 && n <= 64) {
+        // factor + explicit Q pipelined over slabs of tiles: the copy-in hides the leaf stage
+        // and the copy-out the form-Q leaves (tsqr::qr_host_pipelined); slabs of >= 128 MB
+        const int S = (int)std::max<int64_t>(1, std::min<int64_t>(8, (int64_t)(d * m * n) >> 27));
+        cudaError_t e = cudaSuccess;
+        if (!w->up) e = cudaStreamCreateWithFlags(&w->up, cudaStreamNonBlocking);
+        if (e == cudaSuccess && !w->down) e = cudaStreamCreateWithFlags(&w->down, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return fail(e, "tsqr_qr_host streams");
+        return tsqr::qr_host_pipelined(&w->tree, m, n, A, lda, w->A, w->R, w->Q, R, ldr, Q, ldq, opts, st, w->up,
+                                       w->down, S);
+    }
     cudaError_t e = cudaMemcpy2DAsync(w->A, d * m, A, d * lda, d * m, n, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess && k) e = cudaMemcpy2DAsync(w->C, d * m, C, d * ldc, d * m, k, cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return fail(e, "tsqr_qr_host copy in");

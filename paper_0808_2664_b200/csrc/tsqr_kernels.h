@@ -32,6 +32,11 @@ cudaError_t tree_rebuild_tcache(tsqr_tree_s *t, cudaStream_t st);
 // (for an imported state); reuses *tree when the plan matches.
 tsqr_status_t tree_bind(int64_t m_local, int64_t n, double *A, int64_t lda, const tsqr_opts_t *opts,
                         cudaStream_t st, tsqr_tree_s **tree);
+// The host-buffer QR + explicit Q pipelined over S slabs of tiles (tsqr_api.cu; n <= 64, one
+// rank; TSQR_ERR_UNSUPPORTED otherwise, before anything is enqueued).
+tsqr_status_t qr_host_pipelined(tsqr_tree_s **tree, int64_t m, int64_t n, const double *A, int64_t lda, double *dA,
+                                double *dR, double *dQ, double *R, int64_t ldr, double *Q, int64_t ldq,
+                                const tsqr_opts_t *opts, cudaStream_t st, cudaStream_t up, cudaStream_t down, int S);
 
 // Leaf stage on the chunk engine (tsqr_chain.cu).
 struct ChainArgs {
