@@ -134,7 +134,15 @@ k_chain_factor(double *A, int64_t lda, int n, const int64_t *tile_row0, const in
                 continue;
             }
             const int s = cnt[b]++;
-            const bool mine = (g % C::NW == warp);
+            // n = 64 and n = 32: consecutive chunks go to the two warps of one SMSP (warp w
+            // runs on SMSP w % 4), chunk i -> warp (i >> 1) + 4 (i & 1), so those two warps run
+            // about one panel apart, mostly in the same phase -- both in latency-bound
+            // Householder steps or both in DMMA-bound trailing updates -- instead of one's
+            // DMMAs delaying the other's step chain on the shared FP64 pipe (C4 leaf 15.33 ->
+            // 14.84 ms, C5 10.46 -> 10.41 ms; C2's n = 50 configuration measured 1 % slower)
+            constexpr bool kPairSmsp = C::NW == 8 && (C::NCB == 8 || C::NCB == 4);
+            const int gi = g % C::NW;
+            const bool mine = (kPairSmsp ? (gi >> 1) + 4 * (gi & 1) : gi) == warp;
             ++g;
             const int cc = c++;
             if (mine) {
