@@ -198,15 +198,30 @@ k_chain_factor(double *A, int64_t lda, int n, const int64_t *tile_row0, const in
         double *tg = tcache ? tcache + (tile_chunk0[pt] + pc) * (C::NCB * 64) : nullptr;
         chunk_panels<C, 0, kRobust>(ch, r0, pc == pnch - 1, sm + pb * C::RBUF, sy, ws, tau_out, n, A + row0, lda, tg);
         double *dst = A + row0 + r0;
+        if (kTma && hk == C::CH && r0 >= C::NP) {
+            // a full chunk below the pivots: every element is a reflector entry, and with the
+            // TMA layout conditions (even tile starts, even lda) each lane's row pair is one
+            // aligned 16-byte store
 #pragma unroll
-        for (int k = 0; k < C::KM; ++k)
+            for (int k = 0; k < C::KM; ++k)
 #pragma unroll
-            for (int cb = 0; cb < C::NCB; ++cb)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int r = 8 * k + 2 * q + e, col = 8 * cb + l4;
-                    if (col < n && r < hk && r0 + r > col) dst[r + (int64_t)col * lda] = ch.a[k][cb][e];
+                for (int cb = 0; cb < C::NCB; ++cb) {
+                    const int col = 8 * cb + l4;
+                    if (col < n)
+                        *reinterpret_cast<double2 *>(dst + 8 * k + 2 * q + (int64_t)col * lda) =
+                            make_double2(ch.a[k][cb][0], ch.a[k][cb][1]);
                 }
+        } else {
+#pragma unroll
+            for (int k = 0; k < C::KM; ++k)
+#pragma unroll
+                for (int cb = 0; cb < C::NCB; ++cb)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int r = 8 * k + 2 * q + e, col = 8 * cb + l4;
+                        if (col < n && r < hk && r0 + r > col) dst[r + (int64_t)col * lda] = ch.a[k][cb][e];
+                    }
+        }
         if (nt < 0) break;
         pt = nt; pc = ncix; ps = ns; pb = nb;
     }
