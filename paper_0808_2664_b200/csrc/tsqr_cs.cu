@@ -192,11 +192,21 @@ __device__ __forceinline__ void cs_apply_panels(double (&cc)[C::KM][2], double (
 }
 
 // this lane's slab of C (column col, rows 8kk+2q+{0,1}) for chunk c of a tile
+// (vec: C's rows pairs 16-byte aligned -- even tile starts, even ldc, aligned base)
 template <class C>
 __device__ __forceinline__ void load_cslab(double (&v)[C::KM][2], const double *Cm, int64_t ldc, int k, int64_t row0,
-                                           int h, int c, int col, int q) {
+                                           int h, int c, int col, int q, bool vec) {
     const int r0 = c * C::CH, hk = min(C::CH, h - r0);
     const double *Ck = Cm + row0 + r0 + (int64_t)(col < k ? col : 0) * ldc;
+    if (vec && hk == C::CH) {
+#pragma unroll
+        for (int kk = 0; kk < C::KM; ++kk) {
+            const double2 x = col < k ? *reinterpret_cast<const double2 *>(Ck + 8 * kk + 2 * q) : make_double2(0.0, 0.0);
+            v[kk][0] = x.x;
+            v[kk][1] = x.y;
+        }
+        return;
+    }
 #pragma unroll
     for (int kk = 0; kk < C::KM; ++kk) {
         const int r = 8 * kk + 2 * q;
@@ -209,7 +219,7 @@ template <class C, bool kFwd, bool kX>
 __global__ void __launch_bounds__(256, 2)
 k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const int *tile_rows,
            const int64_t *tile_chunk0, const int *cta_tile0, const double *tcache, double *Cm, int64_t ldc, int k,
-           const double *xbuf, int bulk) {
+           const double *xbuf, int bulk, int vecc) {
     using AC = ApplyCs<C>;
     extern __shared__ __align__(16) double sm[];
     uint64_t *bars = reinterpret_cast<uint64_t *>(sm + 2 * AC::YS);
@@ -251,7 +261,7 @@ k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const 
         return kFwd ? cc_ : nch - 1 - cc_;
     };
     double ccv[C::KM][2];
-    if (!kX && tb < te) load_cslab<C>(ccv, Cm, ldc, k, tile_row0[tb], tile_rows[tb], chunk_of(tb, 0), 8 * warp + l4, q);
+    if (!kX && tb < te) load_cslab<C>(ccv, Cm, ldc, k, tile_row0[tb], tile_rows[tb], chunk_of(tb, 0), 8 * warp + l4, q, vecc);
     for (int t = tb; t < te; ++t) {
         const int h = tile_rows[t];
         const int nch = (h + C::CH - 1) / C::CH;
@@ -290,7 +300,7 @@ k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                 if (tn < te) {
                     const int cnn = chunk_of(tn, cn), hn = tile_rows[tn], r0n = cnn * C::CH;
                     stage(cur ^ 1, tn, cnn, min(C::CH, hn - r0n), r0n);
-                    if (!kX) load_cslab<C>(ccn, Cm, ldc, k, tile_row0[tn], hn, cnn, pw * pn + 8 * warp + l4, q);
+                    if (!kX) load_cslab<C>(ccn, Cm, ldc, k, tile_row0[tn], hn, cnn, pw * pn + 8 * warp + l4, q, vecc);
                     asm volatile("cp.async.wait_group 1;\n" ::: "memory");
                     staged = true;
                 } else {
@@ -317,13 +327,22 @@ k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                 double *Ck = Cm + row0 + r0;
                 bool czero = kX;
                 cs_apply_panels<C, kFwd, 0>(ccv, cr, r0, np, slot, czero);
+                if (vecc && hk == C::CH && (!kFwd || r0 >= C::NP)) {   // aligned row pairs, every row stored
+                    if (okc) {
 #pragma unroll
-                for (int kk = 0; kk < C::KM; ++kk)
-#pragma unroll
-                    for (int e = 0; e < 2; ++e) {
-                        const int r = 8 * kk + 2 * q + e;
-                        if (okc && r < hk && (!kFwd || r0 + r >= n)) Ck[r + (int64_t)col * ldc] = ccv[kk][e];
+                        for (int kk = 0; kk < C::KM; ++kk)
+                            *reinterpret_cast<double2 *>(Ck + 8 * kk + 2 * q + (int64_t)col * ldc) =
+                                make_double2(ccv[kk][0], ccv[kk][1]);
                     }
+                } else {
+#pragma unroll
+                    for (int kk = 0; kk < C::KM; ++kk)
+#pragma unroll
+                        for (int e = 0; e < 2; ++e) {
+                            const int r = 8 * kk + 2 * q + e;
+                            if (okc && r < hk && (!kFwd || r0 + r >= n)) Ck[r + (int64_t)col * ldc] = ccv[kk][e];
+                        }
+                }
                 if (!kX && tn < te) {
 #pragma unroll
                     for (int kk = 0; kk < C::KM; ++kk) {
@@ -389,8 +408,10 @@ cudaError_t launch_cs_apply(const ChainApplyArgs &f, cudaStream_t st) {
         const int nw = f.k >= 64 ? 8 : (f.k + 7) / 8;           // one warp per 8-column slab
         const bool bulk = f.bulk && !apply_no_bulk() && !(reinterpret_cast<uintptr_t>(f.A) & 15) && !(f.lda & 1) &&
                           !(reinterpret_cast<uintptr_t>(f.tcache) & 15);
+        // C's row pairs aligned: even tile starts (f.bulk), even ldc, 16-byte aligned base
+        const bool vecc = f.bulk && !(f.ldc & 1) && !(reinterpret_cast<uintptr_t>(f.C) & 15);
         kern<<<f.grid, 32 * (nw < 1 ? 1 : nw), AC::BYTES, st>>>(f.A, f.lda, f.n, f.tile_row0, f.tile_rows, f.tile_chunk0, f.cta_tile0,
-                                                f.tcache, f.C, f.ldc, f.k, f.xbuf, bulk ? 1 : 0);
+                                                f.tcache, f.C, f.ldc, f.k, f.xbuf, bulk ? 1 : 0, vecc ? 1 : 0);
         return cudaGetLastError();
     });
 }
