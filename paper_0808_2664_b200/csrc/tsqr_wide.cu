@@ -21,6 +21,8 @@
 // k_wide_apply applies the stored reflectors (Q^T: panels forward with T^T;
 // Q: backward with T) to C rows mapped the same way, column-split, no barriers.
 #include "tsqr_kernels.h"
+
+#include <cstdint>
 #include "wy.cuh"
 #include "chunk.cuh"
 
@@ -345,16 +347,33 @@ __device__ __forceinline__ void cp_async8(double *sm, const double *g, bool ok) 
 // blocks of loads in flight per lane.
 constexpr int UNR = 8;
 
+// a lane's row pair (r, r+1) of a C column, r even: one 16-byte access when the column
+// pointer is 16-byte aligned (even tile starts and an even ldc make every pair aligned)
+__device__ __forceinline__ void ld_pair(double &x0, double &x1, const double *cp, bool okc, int r, int H) {
+    if (okc && r + 1 < H && !(reinterpret_cast<uintptr_t>(cp) & 15)) {
+        const double2 v = *reinterpret_cast<const double2 *>(cp + r);
+        x0 = v.x;
+        x1 = v.y;
+    } else {
+        x0 = (okc && r < H) ? cp[r] : 0.0;
+        x1 = (okc && r + 1 < H) ? cp[r + 1] : 0.0;
+    }
+}
+__device__ __forceinline__ void st_pair(double *cp, bool okc, int r, int H, double x0, double x1) {
+    if (okc && r + 1 < H && !(reinterpret_cast<uintptr_t>(cp) & 15)) {
+        *reinterpret_cast<double2 *>(cp + r) = make_double2(x0, x1);
+    } else {
+        if (okc && r < H) cp[r] = x0;
+        if (okc && r + 1 < H) cp[r + 1] = x1;
+    }
+}
+
 // one group of U row blocks of this lane's column of C (rows 8k+2q+{0,1})
 template <int U>
 __device__ __forceinline__ void load_grp(double (&cv)[U][2], const double *cp, bool okc, int H, int k0) {
     const int q = threadIdx.x & 3;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-        const int r = 8 * (k0 + u) + 2 * q;
-        cv[u][0] = (okc && r < H) ? cp[r] : 0.0;
-        cv[u][1] = (okc && r + 1 < H) ? cp[r + 1] : 0.0;
-    }
+    for (int u = 0; u < U; ++u) ld_pair(cv[u][0], cv[u][1], cp, okc, 8 * (k0 + u) + 2 * q, H);
 }
 template <int U>
 __device__ __forceinline__ void w_grp(double (&w0)[2], double (&w1)[2], const double (&cv)[U][2], const double *Ys,
@@ -380,8 +399,7 @@ __device__ __forceinline__ void upd_grp(double (&cv)[U][2], double *cp, bool okc
             dmma(cv[u][0], cv[u][1], -p0, y.x);
             dmma(cv[u][0], cv[u][1], -p1, y.y);
             const int r = 8 * (k0 + u) + 2 * q;
-            if (okc && r < H) cp[r] = cv[u][0];
-            if (okc && r + 1 < H) cp[r + 1] = cv[u][1];
+            st_pair(cp, okc, r, H, cv[u][0], cv[u][1]);
         }
     }
 }
@@ -473,8 +491,7 @@ __device__ __forceinline__ void upd_grp16(double (&cv)[U][2], double *cp, bool o
             dmma(cv[u][0], cv[u][1], -r0, z.x);
             dmma(cv[u][0], cv[u][1], -r1, z.y);
             const int r = 8 * (k0 + u) + 2 * q;
-            if (okc && r < H) cp[r] = cv[u][0];
-            if (okc && r + 1 < H) cp[r + 1] = cv[u][1];
+            st_pair(cp, okc, r, H, cv[u][0], cv[u][1]);
         }
     }
 }
@@ -565,8 +582,7 @@ __device__ __forceinline__ void apply_one_cols(const double *Ys, const double *T
                     dmma(cv[u][0], cv[u][1], -p0, Ys[r8 * YW + 2 * q]);
                     dmma(cv[u][0], cv[u][1], -p1, Ys[r8 * YW + 2 * q + 1]);
                     const int r = 8 * (k0 + u) + 2 * q;
-                    if (okc && r < H) cp[r] = cv[u][0];
-                    if (okc && r + 1 < H) cp[r + 1] = cv[u][1];
+                    st_pair(cp, okc, r, H, cv[u][0], cv[u][1]);
                 }
         }
     }
@@ -592,12 +608,7 @@ __device__ void wide_leaf_qr(double *At, int64_t lda, int H, int n, double *tau,
         double *colp = At + (int64_t)(c < n ? c : 0) * lda;
         double a[KM][2];
 #pragma unroll
-        for (int k = 0; k < KM; ++k)
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int r = rbase + 8 * k + 2 * q + e;
-                a[k][e] = (c < n && r < H) ? colp[r] : 0.0;
-            }
+        for (int k = 0; k < KM; ++k) ld_pair(a[k][0], a[k][1], colp, c < n, rbase + 8 * k + 2 * q, H);
         double *xs0 = S.xs[warp][0], *xs1 = S.xs[warp][1];
         if (l4 == 0) {
 #pragma unroll
@@ -722,11 +733,12 @@ __device__ void wide_leaf_qr(double *At, int64_t lda, int H, int n, double *tau,
         }
         // write the panel back; Y of the panel -> Ys (rows >= 8p, zero past H)
 #pragma unroll
+        for (int k = 0; k < KM; ++k) st_pair(colp, c < n, rbase + 8 * k + 2 * q, H, a[k][0], a[k][1]);
+#pragma unroll
         for (int k = 0; k < KM; ++k)
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int r = rbase + 8 * k + 2 * q + e;
-                if (c < n && r < H) colp[r] = a[k][e];
                 if (r >= 8 * (TWO ? (p & ~1) : p) && r < Hp)     // a pair's Y1 is zero on Y0's first rows
                     S.Ys[r * YW + yo + l4] = (c >= n || r < c || r >= H) ? 0.0 : (r == c ? 1.0 : a[k][e]);
             }
