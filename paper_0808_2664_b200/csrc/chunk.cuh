@@ -595,9 +595,13 @@ __device__ __forceinline__ void trailing(Chunk<C> &ch, const double (&yv)[C::KM]
 // Panel P of the factorisation of one chunk (kind 0 structured, 1 dense, 2 none).
 template <class C, int P, bool kRobust>
 __device__ __forceinline__ void factor_panel(Chunk<C> &ch, int kind, int kb, double *Rb, double *ws,
-                                             double *tau_out, int n, const Sync &sy, bool defer, double *tg) {
+                                             double *tau_out, int n, const Sync &sy, bool defer, double *tg,
+                                             double *ydst = nullptr, int64_t ldy = 0) {
     // defer: the caller publishes tr[P] itself (after copying R rows out);
-    // tg: this chunk's T cache (NCB x 8 x 8, row-major per panel) or null
+    // tg: this chunk's T cache (NCB x 8 x 8, row-major per panel) or null;
+    // ydst: a full structured chunk whose rows and columns are all reflector entries, with
+    // 16-byte aligned row pairs: the panel's reflectors are stored as soon as its steps end
+    // (spread over the chunk instead of one burst after its last panel), or null
     const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
     double *Ys = ws + C::YS, *Gs = ws + C::GS, *Ts = ws + C::TS, *t8 = ws + C::T8;
     if (kind != 0) {                  // the previous chunk must be done with R rows 8P..8P+7
@@ -617,6 +621,12 @@ __device__ __forceinline__ void factor_panel(Chunk<C> &ch, int kind, int kb, dou
         for (int k = 0; k < C::KM; ++k) {
             yv[k][0] = ch.a[k][P][0];
             yv[k][1] = ch.a[k][P][1];
+        }
+        if (ydst != nullptr && 8 * P + l4 < n) {
+#pragma unroll
+            for (int k = 0; k < C::KM; ++k)
+                *reinterpret_cast<double2 *>(ydst + 8 * k + 2 * q + (int64_t)(8 * P + l4) * ldy) =
+                    make_double2(yv[k][0], yv[k][1]);
         }
     } else {
         panel_dense<C, P, kRobust>(ch, kb, Gs, t8, tau_out, n);
