@@ -10,10 +10,10 @@ done
 timeout -s KILL 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/r2f_bench_ref_c4.json 2> gpurun_out/r2f_bench_ref_c4.err
 timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'^k_' -c 400 --csv --log-file gpurun_out/r2f_launches_c4.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/r2f_ncu_launch.log 2>&1
 timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'^k_' -c 400 --csv --log-file gpurun_out/r2f_launches_c2.csv python bench.py --config c2 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/r2f_ncu_launch2.log 2>&1
-mkdir -p /tmp/rep
+rm -rf /tmp/rep; mkdir -p /tmp/rep
 prof() {
   local name=$1 k=$2; shift 2
-  timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:$k -c 1 -o /tmp/rep/$name python tools/prof_one.py "$@" > gpurun_out/r2f_$name.log 2>&1
+  timeout -s KILL 900 ncu -f --set full --clock-control none --import-source on -k regex:$k -c 1 -o /tmp/rep/$name python tools/prof_one.py "$@" > gpurun_out/r2f_$name.log 2>&1
   python tools/ncu_raw.py /tmp/rep/$name.ncu-rep > gpurun_out/r2f_${name}_raw.txt 2>&1
   python tools/ncu_groups.py /tmp/rep/$name.ncu-rep > gpurun_out/r2f_${name}_groups.txt 2>&1
   python tools/ncu_lines.py /tmp/rep/$name.ncu-rep 40 > gpurun_out/r2f_${name}_lines.txt 2>&1
