@@ -31,12 +31,12 @@ static bool chain_no_tma() {
     return v != 0;
 }
 
-template <class C, int P, bool kRobust>
+template <class C, int P, bool kRobust, bool kAllStruct>
 __device__ __forceinline__ void chunk_panels(Chunk<C> &ch, int r0, bool last, double *Rb, const Sync &sy,
                                              double *ws, double *tau_out, int n, double *Ahead, int64_t lda,
                                              double *tg, double *ydst) {
     const int lane = threadIdx.x & 31;
-    const int kind = (8 * P < r0) ? 0 : (8 * P < r0 + C::CH ? 1 : 2);
+    const int kind = kAllStruct ? 0 : ((8 * P < r0) ? 0 : (8 * P < r0 + C::CH ? 1 : 2));
     const int kb = (8 * P - r0) >> 3;
     factor_panel<C, P, kRobust>(ch, kind, kb, Rb, ws, tau_out, n, sy, last, tg, ydst, lda);
     if (last) {                                   // R rows 8P .. 8P+7 of the tile are final
@@ -49,7 +49,7 @@ __device__ __forceinline__ void chunk_panels(Chunk<C> &ch, int r0, bool last, do
     }
     PROBE(8);
     if constexpr (P + 1 < C::NCB)
-        chunk_panels<C, P + 1, kRobust>(ch, r0, last, Rb, sy, ws, tau_out, n, Ahead, lda, tg, ydst);
+        chunk_panels<C, P + 1, kRobust, kAllStruct>(ch, r0, last, Rb, sy, ws, tau_out, n, Ahead, lda, tg, ydst);
 }
 
 // Prefetch a chunk (rows [r0, r0 + hk) of the tile at A + row0, all n columns)
@@ -204,8 +204,21 @@ k_chain_factor(double *A, int64_t lda, int n, const int64_t *tile_row0, const in
         // over the chunk: C4 leaf 14.58 -> 14.06 ms, C2 0.810 -> 0.799 ms against one burst of
         // stores after the last panel).  Other chunks store after the last panel, masked.
         const bool full = kTma && hk == C::CH && r0 >= C::NP;
-        chunk_panels<C, 0, kRobust>(ch, r0, pc == pnch - 1, sm + pb * C::RBUF, sy, ws, tau_out, n, A + row0, lda, tg,
-                                    full ? dst : nullptr);
+        if constexpr (C::NCB <= 4) {
+            // n <= 32: a chunk below the pivots runs structured panels only, in its own
+            // instantiation, so its code is contiguous (the head chunks' dense / mixed path is
+            // laid out elsewhere): C5 leaf 10.25 -> 10.0 ms.  For n > 32 the same split measured
+            // slower (C4 +2.8 %, C2 +6 %; profiles/r02_split_paths_ab.txt).
+            if (__builtin_expect(r0 >= C::NP, 1))
+                chunk_panels<C, 0, kRobust, true>(ch, r0, pc == pnch - 1, sm + pb * C::RBUF, sy, ws, tau_out, n,
+                                                  A + row0, lda, tg, full ? dst : nullptr);
+            else
+                chunk_panels<C, 0, kRobust, false>(ch, r0, pc == pnch - 1, sm + pb * C::RBUF, sy, ws, tau_out, n,
+                                                   A + row0, lda, tg, nullptr);
+        } else {
+            chunk_panels<C, 0, kRobust, false>(ch, r0, pc == pnch - 1, sm + pb * C::RBUF, sy, ws, tau_out, n, A + row0,
+                                               lda, tg, full ? dst : nullptr);
+        }
         if (!full) {
 #pragma unroll
             for (int k = 0; k < C::KM; ++k)
