@@ -545,6 +545,62 @@ __device__ __forceinline__ void apply_pair_cols(const double *Ys, const double *
     }
 }
 
+// The same for ONE column block [c_lo, c_hi) (c_hi <= c_lo + 8) of a tile whose rows fit
+// KM row blocks per warp, split over the warps by rows instead of columns: warp w owns row
+// blocks rb0 + w, rb0 + w + 8, ...; all of its loads are in flight at once and stay in
+// registers for the update; the warps' partial W^T meet in gp (NW x 64, fixed summation
+// order), every warp forms W'^T = W^T T^T itself.  Column-split, this block was one warp's
+// work while the other seven waited at the panel's barrier (a lookahead step of a pair).
+template <int KM, int YW>
+__device__ __forceinline__ void apply_block_rows(const double *Ys, const double *Tg, double *C, int64_t ldc, int H,
+                                                 int rb0, int c_lo, int c_hi, double (*gp)[64]) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+    const double tb0 = Tg[(2 * q) * 8 + l4], tb1 = Tg[(2 * q + 1) * 8 + l4];
+    const int nrb = (H + 7) / 8;
+    const int col = c_lo + l4;
+    const bool okc = col < c_hi;
+    double *cp = C + (int64_t)(okc ? col : c_lo) * ldc;
+    double cv[KM][2];
+#pragma unroll
+    for (int u = 0; u < KM; ++u) {
+        const int k = rb0 + warp + NW * u;
+        if (k < nrb) ld_pair(cv[u][0], cv[u][1], cp, okc, 8 * k + 2 * q, H);
+        else cv[u][0] = cv[u][1] = 0.0;
+    }
+    double w0[2] = {0.0, 0.0}, w1[2] = {0.0, 0.0};
+#pragma unroll
+    for (int u = 0; u < KM; ++u) {
+        const int k = rb0 + warp + NW * u;
+        if (k < nrb) {
+            const int r = 8 * k + 2 * q;
+            dmma(w0[u & 1], w1[u & 1], cv[u][0], Ys[r * YW + l4]);
+            dmma(w0[u & 1], w1[u & 1], cv[u][1], Ys[(r + 1) * YW + l4]);
+        }
+    }
+    *reinterpret_cast<double2 *>(&gp[warp][2 * lane]) = make_double2(w0[0] + w0[1], w1[0] + w1[1]);
+    __syncthreads();
+    double wt0 = 0.0, wt1 = 0.0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        const double2 g = *reinterpret_cast<const double2 *>(&gp[w][2 * lane]);
+        wt0 += g.x;
+        wt1 += g.y;
+    }
+    double p0 = 0.0, p1 = 0.0;
+    dmma(p0, p1, wt0, tb0);
+    dmma(p0, p1, wt1, tb1);
+#pragma unroll
+    for (int u = 0; u < KM; ++u) {
+        const int k = rb0 + warp + NW * u;
+        if (k < nrb) {
+            const int r8 = 8 * k + l4;
+            dmma(cv[u][0], cv[u][1], -p0, Ys[r8 * YW + 2 * q]);
+            dmma(cv[u][0], cv[u][1], -p1, Ys[r8 * YW + 2 * q + 1]);
+            st_pair(cp, okc, 8 * k + 2 * q, H, cv[u][0], cv[u][1]);
+        }
+    }
+}
+
 // apply_panel_cols on a Y stored with row stride YW (one panel's 8 columns at Ys + off)
 template <int YW, bool kFwd = true>
 __device__ __forceinline__ void apply_one_cols(const double *Ys, const double *Tg, double *C, int64_t ldc, int H,
@@ -770,7 +826,8 @@ __device__ void wide_leaf_qr(double *At, int64_t lda, int H, int n, double *tau,
             if (p + 1 < npan) apply_one_cols<YW>(S.Ys, Tp, At, lda, H, p, 8 * (p + 1), n);
         } else if ((p & 1) == 0) {
             // first panel of a pair: update only the pair's second column block
-            if (p + 1 < npan) apply_one_cols<YW>(S.Ys, Tp, At, lda, H, p, 8 * (p + 1), min(n, 8 * (p + 2)));
+            // (row-split over the warps: C3 leaf 0.953 -> 0.928 ms against one warp's column slab)
+            if (p + 1 < npan) apply_block_rows<KM, YW>(S.Ys, Tp, At, lda, H, p, 8 * (p + 1), min(n, 8 * (p + 2)), S.gp);
         } else {
             // (also for the last pair: the apply / form-Q kernels use its T01)
             // second panel of a pair: T01 = -T0 (Y0^T Y1) T1, then the 16-reflector update
@@ -1139,6 +1196,9 @@ static cudaError_t launch_leaves_km(double *A, int64_t lda, int n, const int64_t
 template <bool kRobust>
 static cudaError_t launch_leaves_r(double *A, int64_t lda, int n, const int64_t *row0, const int *rows, int L,
                                    int max_rows, double *tau, double *tcache, double *tpair, cudaStream_t st) {
+    // 56 rows per warp for tiles of <= 448 rows (C3's 400): the steps and the row-split
+    // updates skip the 64-row padding of KM = 8 (C3 leaf 0.928 -> 0.878 ms)
+    if (max_rows <= 448) return launch_leaves_km<7, kRobust>(A, lda, n, row0, rows, L, max_rows, tau, tcache, tpair, st);
     if (max_rows <= 512) return launch_leaves_km<8, kRobust>(A, lda, n, row0, rows, L, max_rows, tau, tcache, tpair, st);
     if (max_rows <= 1024) return launch_leaves_km<16, kRobust>(A, lda, n, row0, rows, L, max_rows, tau, tcache, tpair, st);
     if (max_rows <= 1536) return launch_leaves_km<24, kRobust>(A, lda, n, row0, rows, L, max_rows, tau, tcache, tpair, st);
