@@ -1196,8 +1196,10 @@ static cudaError_t launch_leaves_km(double *A, int64_t lda, int n, const int64_t
 template <bool kRobust>
 static cudaError_t launch_leaves_r(double *A, int64_t lda, int n, const int64_t *row0, const int *rows, int L,
                                    int max_rows, double *tau, double *tcache, double *tpair, cudaStream_t st) {
-    // 56 rows per warp for tiles of <= 448 rows (C3's 400): the steps and the row-split
-    // updates skip the 64-row padding of KM = 8 (C3 leaf 0.928 -> 0.878 ms)
+    // 48 / 56 rows per warp for tiles of <= 384 / 448 rows: the steps and the row-split
+    // updates skip most of the padding of KM = 8 (C3's 342-row tiles at s = 400: leaf
+    // 0.928 -> 0.878 ms with KM = 7, 0.851 ms with KM = 6)
+    if (max_rows <= 384) return launch_leaves_km<6, kRobust>(A, lda, n, row0, rows, L, max_rows, tau, tcache, tpair, st);
     if (max_rows <= 448) return launch_leaves_km<7, kRobust>(A, lda, n, row0, rows, L, max_rows, tau, tcache, tpair, st);
     if (max_rows <= 512) return launch_leaves_km<8, kRobust>(A, lda, n, row0, rows, L, max_rows, tau, tcache, tpair, st);
     if (max_rows <= 1024) return launch_leaves_km<16, kRobust>(A, lda, n, row0, rows, L, max_rows, tau, tcache, tpair, st);
