@@ -29,7 +29,10 @@ using chunk::House;
 using chunk::house_bf;
 using wy::dmma;
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int NW = 8;
+#ifndef TSQR_TREE_NW
+#define TSQR_TREE_NW 4
+#endif
+constexpr int NW = TSQR_TREE_NW;   // nodes (warps) per block: 4 spreads a level over twice the SMs of 8 (C5 tree 0.229 -> 0.189 ms, C4 0.307 -> 0.293, C2 0.126 -> 0.121)
 
 template <int NCB_>
 struct TCfg {
