@@ -80,6 +80,10 @@ CASES = [
     (65, 65, 65, 65),            # n = 65 square
     (128, 64, 128, 64),          # tiles exactly n rows tall (two 64-row tiles)
     (7000, 128, 3500, 512),      # n = 128 (16 panels, pairs), tiles of 500 rows, two blocks
+    # wide-leaf instantiations by tile height: 48 / 56 / 64 rows per warp (KM = 6 / 7 / 8)
+    (3072, 96, 3072, 384),       # tiles of exactly 384 rows: the KM = 6 limit
+    (4400, 200, 2200, 440),      # tiles of 440 rows: KM = 7
+    (3600, 136, 3600, 450),      # tiles of 450 rows: KM = 8
 ]
 
 
