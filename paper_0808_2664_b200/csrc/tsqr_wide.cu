@@ -26,6 +26,7 @@
 #include "wy.cuh"
 #include "chunk.cuh"
 
+#include <cstdlib>
 #include <type_traits>
 
 namespace tsqr {
@@ -1013,7 +1014,7 @@ template <bool kFwd, int NPAN_NODE>
 __global__ void __launch_bounds__(NT, 1)
 k_node_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const int *node_a,
                        const int *ids, const double *tcache_node, double *C, int64_t ldc, int k, int xbuf_mode,
-                       int *flags, int L, const int *dep0, const int *dep1) {
+                       int *flags, int L, const int *dep0, const int *dep1, int *pflags) {
     extern __shared__ __align__(16) double smraw[];
     __shared__ int s_idx;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
@@ -1039,7 +1040,8 @@ k_node_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, cons
     }
     const double *tc = tcache_node + (int64_t)b * npan * 64;
     for (int e = threadIdx.x; e < 64 * npan; e += NT) cp_async8(Tn + e, tc + e, true);
-    if (flags && threadIdx.x == 0) {                  // the producers of this node's inputs
+    const bool ppipe = kFwd && flags && pflags;     // panel-level hand-offs (below)
+    if (flags && !ppipe && threadIdx.x == 0) {       // the producers of this node's inputs
         const int d0 = dep0[b], d1 = dep1 ? dep1[b] : -1;
         if (d0 >= 0)
             while (*reinterpret_cast<volatile int *>(flags + d0) == 0) __nanosleep(64);
@@ -1056,7 +1058,100 @@ k_node_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, cons
     } else {
         Ca = C + tile_row0[a]; Cb = C + tile_row0[b]; ld = ldc;
     }
-    for (int cbw = warp; 8 * cbw < k; cbw += NW) {
+    if (ppipe) {
+        // Q^T, whole tree in one launch, panel-level pipelining: this node's panel P needs only
+        // row block P of its two input head blocks (C_a: the left child's output, C_b: the
+        // right child's), final once that child has applied its own panel P; it publishes its
+        // output row block P (C_a's, read by its parent) with a per-(node, 8-column slab, panel)
+        // flag right after computing it.  The critical path is about depth + panels panel
+        // latencies instead of depth whole nodes.  Row blocks of C_b are loaded as their panel
+        // first needs them (panel P reads C_b row blocks <= P only).
+        const int nslab = (k + 7) / 8;
+        const int d0 = dep0[b], d1 = dep1 ? dep1[b] : -1;
+        for (int cbw = warp; cbw < nslab; cbw += NW) {
+            const int col = 8 * cbw + l4;
+            const bool okc = col < k;
+            const int64_t co = (int64_t)(okc ? col : 0) * ld;
+            const int *f0 = d0 >= 0 ? pflags + ((int64_t)d0 * nslab + cbw) * npan : nullptr;
+            const int *f1 = d1 >= 0 ? pflags + ((int64_t)d1 * nslab + cbw) * npan : nullptr;
+            int *fme = pflags + ((int64_t)b * nslab + cbw) * npan;
+            double cb[NPAN_NODE][2];
+#pragma unroll
+            for (int kk = 0; kk < NPAN_NODE; ++kk) cb[kk][0] = cb[kk][1] = 0.0;
+            for (int P = 0; P < npan; ++P) {
+                if (lane == 0) {
+                    if (f1) while (*reinterpret_cast<const volatile int *>(f1 + P) == 0) __nanosleep(32);
+                    if (f0) while (*reinterpret_cast<const volatile int *>(f0 + P) == 0) __nanosleep(32);
+                }
+                __syncwarp();
+                __threadfence();
+                const double *Tg = Tn + 64 * P;
+                const double tb0 = Tg[(2 * q) * 8 + l4], tb1 = Tg[(2 * q + 1) * 8 + l4];
+                const int ra = 8 * P + 2 * q;
+                const double nb0 = (okc && ra < n) ? __ldcg(Cb + ra + co) : 0.0;
+                const double nb1 = (okc && ra + 1 < n) ? __ldcg(Cb + ra + 1 + co) : 0.0;
+                const double ca0 = (okc && ra < n) ? __ldcg(Ca + ra + co) : 0.0;
+                const double ca1 = (okc && ra + 1 < n) ? __ldcg(Ca + ra + 1 + co) : 0.0;
+#pragma unroll
+                for (int kk = 0; kk < NPAN_NODE; ++kk)
+                    if (kk == P) {
+                        cb[kk][0] = nb0;
+                        cb[kk][1] = nb1;
+                    }
+                const double *yP = Yb + 64 * (P * (P + 1) / 2);
+                double w0[2] = {0.0, 0.0}, w1[2] = {0.0, 0.0};
+#pragma unroll
+                for (int g = 0; g < NPAN_NODE; g += 4) {
+                    if (g <= P) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int kk = g + u;
+                            if (kk < NPAN_NODE) {
+                                const bool ok = kk <= P;
+                                double2 y = *reinterpret_cast<const double2 *>(yP + 64 * (ok ? kk : P) + 8 * l4 + 2 * q);
+                                y.x = ok ? y.x : 0.0;
+                                y.y = ok ? y.y : 0.0;
+                                dmma(w0[u & 1], w1[u & 1], cb[kk][0], y.x);
+                                dmma(w0[u & 1], w1[u & 1], cb[kk][1], y.y);
+                            }
+                        }
+                    }
+                }
+                double p0 = 0.0, p1 = 0.0;
+                dmma(p0, p1, w0[0] + w0[1] + ca0, tb0);
+                dmma(p0, p1, w1[0] + w1[1] + ca1, tb1);
+                if (okc && ra < n) Ca[ra + co] = ca0 - p0;
+                if (okc && ra + 1 < n) Ca[ra + 1 + co] = ca1 - p1;
+                __threadfence();                      // this node's output row block P ...
+                __syncwarp();
+                if (lane == 0) *reinterpret_cast<volatile int *>(fme + P) = 1;   // ... is published
+#pragma unroll
+                for (int g = 0; g < NPAN_NODE; g += 4) {
+                    if (g <= P) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int kk = g + u;
+                            if (kk < NPAN_NODE) {
+                                const bool ok = kk <= P;
+                                const double *yb = yP + 64 * (ok ? kk : P);
+                                const double y0 = ok ? yb[8 * (2 * q) + l4] : 0.0, y1 = ok ? yb[8 * (2 * q + 1) + l4] : 0.0;
+                                dmma(cb[kk][0], cb[kk][1], -p0, y0);
+                                dmma(cb[kk][0], cb[kk][1], -p1, y1);
+                            }
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int kk = 0; kk < NPAN_NODE; ++kk)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int r = 8 * kk + 2 * q + e;
+                    if (okc && kk < npan && r < n) Cb[r + co] = cb[kk][e];
+                }
+        }
+    }
+    for (int cbw = warp; !ppipe && 8 * cbw < k; cbw += NW) {
         const int col = 8 * cbw + l4;
         const bool okc = col < k;
         const int64_t co = (int64_t)(okc ? col : 0) * ld;
@@ -1262,7 +1357,7 @@ cudaError_t launch_node_apply(const double *A, int64_t lda, int n, const int64_t
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
             if (e != cudaSuccess) return e;
             k_node_apply<F, NPM><<<count, NT, bytes, st>>>(A, lda, n, row0, node_a, ids, tcache_node, C, ldc,
-                                                                     k, xbuf_mode, nullptr, 0, nullptr, nullptr);
+                                                                     k, xbuf_mode, nullptr, 0, nullptr, nullptr, nullptr);
             return cudaGetLastError();
         };
         using T8 = std::integral_constant<int, 8>;
@@ -1277,6 +1372,8 @@ cudaError_t launch_node_apply(const double *A, int64_t lda, int n, const int64_t
     return cudaGetLastError();
 }
 
+bool node_ppipe_disabled();
+
 // The whole tree's node stage in one launch (k_node_apply with flags), npan <= 28:
 // ids = every node in dependency order; flags[L + 1] scratch (zeroed here).
 cudaError_t launch_node_apply_pipe(const double *A, int64_t lda, int n, const int64_t *row0, const int *node_a,
@@ -1288,6 +1385,16 @@ cudaError_t launch_node_apply_pipe(const double *A, int64_t lda, int n, const in
     if (count == 0) return cudaSuccess;
     cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (L + 1), st);
     if (e != cudaSuccess) return e;
+    // Q^T: per-(node, 8-column slab, panel) flags of the panel-level pipeline, stream-ordered;
+    // for npan > 8 only (C3 apply Q^T 0.852 -> 0.600 ms; with 4 panels, C5, the per-panel
+    // publish costs more than the overlap gains: 23.9 -> 24.3 ms)
+    int *pflags = nullptr;
+    const size_t pf_ints = forward && !xbuf_mode && npan > 8 ? (size_t)L * ((k + 7) / 8) * npan : 0;
+    if (pf_ints > 0 && !node_ppipe_disabled()) {
+        e = cudaMallocAsync((void **)&pflags, sizeof(int) * pf_ints, st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(pflags, 0, sizeof(int) * pf_ints, st);
+        if (e != cudaSuccess) return e;
+    }
     const size_t bytes = sizeof(double) * 64 * (npan * (npan + 1) / 2 + npan);
     auto go = [&](auto kf, auto np) -> cudaError_t {
         constexpr bool F = decltype(kf)::value;
@@ -1296,13 +1403,24 @@ cudaError_t launch_node_apply_pipe(const double *A, int64_t lda, int n, const in
                                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
         if (r != cudaSuccess) return r;
         k_node_apply<F, NPM><<<count, NT, bytes, st>>>(A, lda, n, row0, node_a, ids, tcache_node, C, ldc, k,
-                                                       xbuf_mode, flags, L, dep0, dep1);
+                                                       xbuf_mode, flags, L, dep0, dep1, pflags);
         return cudaGetLastError();
     };
     using T8 = std::integral_constant<int, 8>;
     using T28 = std::integral_constant<int, NPAN_NODE>;
-    if (forward) return npan <= 8 ? go(std::true_type(), T8()) : go(std::true_type(), T28());
-    return npan <= 8 ? go(std::false_type(), T8()) : go(std::false_type(), T28());
+    if (forward) e = npan <= 8 ? go(std::true_type(), T8()) : go(std::true_type(), T28());
+    else e = npan <= 8 ? go(std::false_type(), T8()) : go(std::false_type(), T28());
+    if (pflags) {
+        const cudaError_t f = cudaFreeAsync(pflags, st);
+        if (e == cudaSuccess) e = f;
+    }
+    return e;
+}
+
+// TSQR_NO_NODE_PPIPE=1 in the environment: node-level hand-offs only (A/B)
+bool node_ppipe_disabled() {
+    const char *v = std::getenv("TSQR_NO_NODE_PPIPE");
+    return v && *v == '1';
 }
 
 cudaError_t launch_wide_apply_node1(const double *Y1, int64_t ldy, int n, const double *tcache, double *Ca,
