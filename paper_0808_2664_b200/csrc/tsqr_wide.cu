@@ -1040,7 +1040,7 @@ k_node_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, cons
     }
     const double *tc = tcache_node + (int64_t)b * npan * 64;
     for (int e = threadIdx.x; e < 64 * npan; e += NT) cp_async8(Tn + e, tc + e, true);
-    const bool ppipe = kFwd && flags && pflags;     // panel-level hand-offs (below)
+    const bool ppipe = flags && pflags;             // panel-level hand-offs (below)
     if (flags && !ppipe && threadIdx.x == 0) {       // the producers of this node's inputs
         const int d0 = dep0[b], d1 = dep1 ? dep1[b] : -1;
         if (d0 >= 0)
@@ -1059,13 +1059,18 @@ k_node_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, cons
         Ca = C + tile_row0[a]; Cb = C + tile_row0[b]; ld = ldc;
     }
     if (ppipe) {
-        // Q^T, whole tree in one launch, panel-level pipelining: this node's panel P needs only
-        // row block P of its two input head blocks (C_a: the left child's output, C_b: the
-        // right child's), final once that child has applied its own panel P; it publishes its
-        // output row block P (C_a's, read by its parent) with a per-(node, 8-column slab, panel)
-        // flag right after computing it.  The critical path is about depth + panels panel
-        // latencies instead of depth whole nodes.  Row blocks of C_b are loaded as their panel
-        // first needs them (panel P reads C_b row blocks <= P only).
+        // Whole tree in one launch, panel-level pipelining.  Q^T (bottom-up, panels forward):
+        // this node's panel P needs only row block P of its two input head blocks (C_a: the
+        // left child's output, C_b: the right child's), final once that child has applied its
+        // own panel P; it publishes its output row block P (C_a's, read by its parent) with a
+        // per-(node, 8-column slab, panel) flag right after computing it, and loads C_b's row
+        // blocks as its panels first need them (panel P reads C_b row blocks <= P only).
+        // Q / form Q (top-down, panels backward): C_b is ready at the start (the input's head
+        // rows, or the zeroed X block); C_a's row block P comes from the parent, final once the
+        // parent has applied its panel P, and so are both of this node's outputs' row blocks P
+        // (C_a's at panel P, C_b's at its last update, panel P): they are stored and published
+        // there.  The critical path is about depth + panels panel latencies instead of depth
+        // whole nodes.
         const int nslab = (k + 7) / 8;
         const int d0 = dep0[b], d1 = dep1 ? dep1[b] : -1;
         for (int cbw = warp; cbw < nslab; cbw += NW) {
@@ -1077,8 +1082,14 @@ k_node_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, cons
             int *fme = pflags + ((int64_t)b * nslab + cbw) * npan;
             double cb[NPAN_NODE][2];
 #pragma unroll
-            for (int kk = 0; kk < NPAN_NODE; ++kk) cb[kk][0] = cb[kk][1] = 0.0;
-            for (int P = 0; P < npan; ++P) {
+            for (int kk = 0; kk < NPAN_NODE; ++kk)
+#pragma unroll
+                for (int e = 0; e < 2; ++e) {
+                    const int r = 8 * kk + 2 * q + e;
+                    cb[kk][e] = (!kFwd && okc && kk < npan && r < n) ? Cb[r + co] : 0.0;
+                }
+            for (int pp = 0; pp < npan; ++pp) {
+                const int P = kFwd ? pp : npan - 1 - pp;
                 if (lane == 0) {
                     if (f1) while (*reinterpret_cast<const volatile int *>(f1 + P) == 0) __nanosleep(32);
                     if (f0) while (*reinterpret_cast<const volatile int *>(f0 + P) == 0) __nanosleep(32);
@@ -1086,18 +1097,21 @@ k_node_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, cons
                 __syncwarp();
                 __threadfence();
                 const double *Tg = Tn + 64 * P;
-                const double tb0 = Tg[(2 * q) * 8 + l4], tb1 = Tg[(2 * q + 1) * 8 + l4];
+                const double tb0 = kFwd ? Tg[(2 * q) * 8 + l4] : Tg[l4 * 8 + 2 * q];
+                const double tb1 = kFwd ? Tg[(2 * q + 1) * 8 + l4] : Tg[l4 * 8 + 2 * q + 1];
                 const int ra = 8 * P + 2 * q;
-                const double nb0 = (okc && ra < n) ? __ldcg(Cb + ra + co) : 0.0;
-                const double nb1 = (okc && ra + 1 < n) ? __ldcg(Cb + ra + 1 + co) : 0.0;
                 const double ca0 = (okc && ra < n) ? __ldcg(Ca + ra + co) : 0.0;
                 const double ca1 = (okc && ra + 1 < n) ? __ldcg(Ca + ra + 1 + co) : 0.0;
+                if (kFwd) {
+                    const double nb0 = (okc && ra < n) ? __ldcg(Cb + ra + co) : 0.0;
+                    const double nb1 = (okc && ra + 1 < n) ? __ldcg(Cb + ra + 1 + co) : 0.0;
 #pragma unroll
-                for (int kk = 0; kk < NPAN_NODE; ++kk)
-                    if (kk == P) {
-                        cb[kk][0] = nb0;
-                        cb[kk][1] = nb1;
-                    }
+                    for (int kk = 0; kk < NPAN_NODE; ++kk)
+                        if (kk == P) {
+                            cb[kk][0] = nb0;
+                            cb[kk][1] = nb1;
+                        }
+                }
                 const double *yP = Yb + 64 * (P * (P + 1) / 2);
                 double w0[2] = {0.0, 0.0}, w1[2] = {0.0, 0.0};
 #pragma unroll
@@ -1122,9 +1136,11 @@ k_node_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, cons
                 dmma(p0, p1, w1[0] + w1[1] + ca1, tb1);
                 if (okc && ra < n) Ca[ra + co] = ca0 - p0;
                 if (okc && ra + 1 < n) Ca[ra + 1 + co] = ca1 - p1;
-                __threadfence();                      // this node's output row block P ...
-                __syncwarp();
-                if (lane == 0) *reinterpret_cast<volatile int *>(fme + P) = 1;   // ... is published
+                if (kFwd) {
+                    __threadfence();                  // this node's output row block P ...
+                    __syncwarp();
+                    if (lane == 0) *reinterpret_cast<volatile int *>(fme + P) = 1;   // ... is published
+                }
 #pragma unroll
                 for (int g = 0; g < NPAN_NODE; g += 4) {
                     if (g <= P) {
@@ -1141,14 +1157,27 @@ k_node_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, cons
                         }
                     }
                 }
-            }
+                if (!kFwd) {                          // C_b's row block P had its last update
 #pragma unroll
-            for (int kk = 0; kk < NPAN_NODE; ++kk)
-#pragma unroll
-                for (int e = 0; e < 2; ++e) {
-                    const int r = 8 * kk + 2 * q + e;
-                    if (okc && kk < npan && r < n) Cb[r + co] = cb[kk][e];
+                    for (int kk = 0; kk < NPAN_NODE; ++kk)
+                        if (kk == P) {
+                            if (okc && ra < n) Cb[ra + co] = cb[kk][0];
+                            if (okc && ra + 1 < n) Cb[ra + 1 + co] = cb[kk][1];
+                        }
+                    __threadfence();                  // both outputs' row blocks P ...
+                    __syncwarp();
+                    if (lane == 0) *reinterpret_cast<volatile int *>(fme + P) = 1;   // ... are published
                 }
+            }
+            if (kFwd) {
+#pragma unroll
+                for (int kk = 0; kk < NPAN_NODE; ++kk)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int r = 8 * kk + 2 * q + e;
+                        if (okc && kk < npan && r < n) Cb[r + co] = cb[kk][e];
+                    }
+            }
         }
     }
     for (int cbw = warp; !ppipe && 8 * cbw < k; cbw += NW) {
@@ -1385,11 +1414,13 @@ cudaError_t launch_node_apply_pipe(const double *A, int64_t lda, int n, const in
     if (count == 0) return cudaSuccess;
     cudaError_t e = cudaMemsetAsync(flags, 0, sizeof(int) * (L + 1), st);
     if (e != cudaSuccess) return e;
-    // Q^T: per-(node, 8-column slab, panel) flags of the panel-level pipeline, stream-ordered;
-    // for npan > 8 only (C3 apply Q^T 0.852 -> 0.600 ms; with 4 panels, C5, the per-panel
-    // publish costs more than the overlap gains: 23.9 -> 24.3 ms)
+    // per-(node, 8-column slab, panel) flags of the panel-level pipeline, stream-ordered; for
+    // npan > 8 only: C3 apply Q^T 0.852 -> 0.600 ms, form Q at n = 200 2.83 -> 1.96 ms, but
+    // with <= 8 panels the per-panel publish costs more than the overlap gains (C5 apply Q^T
+    // 23.9 -> 24.3 ms, C4 form Q 11.40 -> 11.68 ms, C2 0.816 -> 0.863 ms)
     int *pflags = nullptr;
-    const size_t pf_ints = forward && !xbuf_mode && npan > 8 ? (size_t)L * ((k + 7) / 8) * npan : 0;
+    const bool pp_on = npan > 8 && (forward ? !xbuf_mode : true);
+    const size_t pf_ints = pp_on ? (size_t)L * ((k + 7) / 8) * npan : 0;
     if (pf_ints > 0 && !node_ppipe_disabled()) {
         e = cudaMallocAsync((void **)&pflags, sizeof(int) * pf_ints, st);
         if (e == cudaSuccess) e = cudaMemsetAsync(pflags, 0, sizeof(int) * pf_ints, st);
