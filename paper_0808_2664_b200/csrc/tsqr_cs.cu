@@ -37,9 +37,11 @@ static bool apply_no_bulk() {
 template <class C>
 struct ApplyCs {
     static constexpr int NW = 8, NT = 256;
-    // Y twice, so that both DMMA operand reads are bank-conflict free: row-major Yr (CH x NP,
-    // row stride LDY = NP + 2) for W^T = C^T Y (rows 2q+e, column l4 of a lane) and column-major
-    // Yt (NP x CH, stride LDT = CH + 2) for C -= Y W' (rows l4, columns 2q+e); then the T's
+    // Y column-major (Yt: NP x CH, stride LDT = CH + 2), read bank-conflict free by both DMMA
+    // operand patterns: W^T = C^T Y (a lane's rows 2q, 2q+1 of column l4: one 16-byte load;
+    // LDT = 2 mod 4 doubles spreads the 8 columns over the banks) and C -= Y W' (rows l4,
+    // columns 2q+e); then the T's.  (The [0, OFF_YT) region held a row-major copy for the first
+    // pattern, written per chunk after the staging: dropped, the region stays unused.)
     static constexpr int LDY = C::NP + 2, LDT = C::CH + 2;
     static constexpr int OFF_YT = C::CH * LDY, OFF_T = OFF_YT + C::NP * LDT;
     static constexpr int YS = OFF_T + C::NCB * 64;
@@ -72,16 +74,15 @@ __device__ __forceinline__ void stage_chunk_bulk(double *slot, const double *Ak,
         else bulk_g2s(slot + AC::OFF_T, tch, C::NCB * 64 * 8u, bar);
     }
 }
+// (only for a ragged or head chunk: a full chunk below the pivots is Y as staged)
 template <class C>
 __device__ __forceinline__ void finish_bulk_stage(double *slot, int hk, int n, int r0) {
     using AC = ApplyCs<C>;
-    const bool fix = hk < C::CH || r0 < C::NP;            // ragged or head chunk: Yt changes too
     for (int i = threadIdx.x; i < C::CH * C::NP; i += blockDim.x) {
         const int col = i / C::CH, row = i - col * C::CH;
         const double v = slot[AC::OFF_YT + col * AC::LDT + row];
         const double y = (col < n && row < hk && row > col - r0) ? v : ((col < n && row == col - r0) ? 1.0 : 0.0);
-        slot[row * AC::LDY + col] = y;
-        if (fix) slot[AC::OFF_YT + col * AC::LDT + row] = y;
+        slot[AC::OFF_YT + col * AC::LDT + row] = y;
     }
 }
 
@@ -100,7 +101,6 @@ __device__ __forceinline__ void stage_chunk(double *slot, const double *Ak, int6
         const int col = i / C::CH, row = i % C::CH;
         const bool ok = row < hk && col < n && row > col - r0;
         const double *src = Ak + row + (int64_t)(ok ? col : 0) * lda;
-        cp8(slot + row * ApplyCs<C>::LDY + col, src, ok);
         cp8(slot + ApplyCs<C>::OFF_YT + col * ApplyCs<C>::LDT + row, src, ok);
     }
     for (int i = threadIdx.x; i < C::NCB * 64; i += blockDim.x) cp8(slot + ApplyCs<C>::OFF_T + i, tch + i, true);
@@ -109,10 +109,7 @@ __device__ __forceinline__ void stage_chunk(double *slot, const double *Ak, int6
 template <class C>
 __device__ __forceinline__ void fix_dense(double *slot, int n, int r0) {
     for (int c = threadIdx.x; c < C::NP; c += blockDim.x)
-        if (c < n && c >= r0 && c < r0 + C::CH) {
-            slot[(c - r0) * ApplyCs<C>::LDY + c] = 1.0;
-            slot[ApplyCs<C>::OFF_YT + c * ApplyCs<C>::LDT + (c - r0)] = 1.0;
-        }
+        if (c < n && c >= r0 && c < r0 + C::CH) slot[ApplyCs<C>::OFF_YT + c * ApplyCs<C>::LDT + (c - r0)] = 1.0;
 }
 
 template <class C, bool kFwd, int p>
@@ -121,11 +118,11 @@ __device__ __forceinline__ void cs_apply_panel(double (&cc)[C::KM][2], double (&
     // czero (form Q only): the chunk's rows of C are still all zero -- they become
     // nonzero with the first panel applied to the chunk -- so W^T = C^T Y is skipped
     const int lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
-    constexpr int KM = C::KM, NP = ApplyCs<C>::LDY, LDT = ApplyCs<C>::LDT;   // Yr / Yt strides
+    constexpr int KM = C::KM, LDT = ApplyCs<C>::LDT;                          // Yt stride
     if (8 * p >= r0 + C::CH) return;           // no reflector of panel p in this chunk
     const bool dense = 8 * p >= r0;            // pivots inside the chunk: row block kb
     const int kb = dense ? (8 * p - r0) >> 3 : -1;
-    const double *ys = slot + 8 * p;
+    const double *ycol = slot + ApplyCs<C>::OFF_YT + (8 * p + l4) * LDT;   // this lane's column of the panel
     const double *Tg = slot + ApplyCs<C>::OFF_T + 64 * p;
     const double *yt = slot + ApplyCs<C>::OFF_YT + 8 * p * LDT;       // Yt column 8p
     double crp0 = cr[p][0], crp1 = cr[p][1];
@@ -140,7 +137,8 @@ __device__ __forceinline__ void cs_apply_panel(double (&cc)[C::KM][2], double (&
     if (!(kFwd == false && czero && !dense)) {
 #pragma unroll
         for (int k = 0; k < KM; ++k) {
-            const double y0 = ys[(8 * k + 2 * q) * NP + l4], y1 = ys[(8 * k + 2 * q + 1) * NP + l4];
+            const double2 yv = *reinterpret_cast<const double2 *>(ycol + 8 * k + 2 * q);
+            const double y0 = yv.x, y1 = yv.y;
             dmma(w0[k & 1], w1[k & 1], cc[k][0], y0);
             dmma(w0[k & 1], w1[k & 1], cc[k][1], y1);
         }
@@ -315,8 +313,10 @@ k_cs_apply(const double *A, int64_t lda, int n, const int64_t *tile_row0, const 
                 if ((sbulk >> cur) & 1u) {
                     tma::mbar_wait(bars + cur, (phase >> cur) & 1u);
                     phase ^= 1u << cur;
-                    finish_bulk_stage<C>(slot, hk, n, r0);
-                    __syncthreads();
+                    if (hk < C::CH || r0 < C::NP) {       // ragged or head chunk: Yt is fixed up
+                        finish_bulk_stage<C>(slot, hk, n, r0);
+                        __syncthreads();
+                    }                                     // (else every thread waited on the TMA itself)
                 } else {
                     __syncthreads();
                     if (dense) {
