@@ -979,6 +979,134 @@ k_wide_apply_leaves(const double *A, int64_t lda, int n, const int64_t *tile_row
     }
 }
 
+// The same with the warp's 8-column slab of C resident in registers for the whole tile
+// (tiles of <= 8 MR rows, k <= 64: one slab per warp, pairs cached): C is read and written
+// once per tile instead of streamed through L2 twice per panel pair, and every pair's W^T
+// and update run on registers (the streamed version waited on L2 latency with 4-8 row blocks
+// in flight).  One CTA per SM (the slab takes 2 MR registers per lane).
+template <bool kFwd, int MR>
+__global__ void __launch_bounds__(NT, 1)
+k_wide_apply_leaves_reg(const double *A, int64_t lda, int n, const int64_t *tile_row0, const int *tile_rows,
+                        const double *tcache_tile, const double *tpair_tile, double *C, int64_t ldc, int k) {
+    extern __shared__ __align__(16) double smraw[];
+    const int t = blockIdx.x;
+    const int npan = (n + 7) / 8;
+    const int H = tile_rows[t];
+    const int Hp = 8 * ((H + 7) / 8);
+    const int nrb = Hp / 8;
+    double *Ts = smraw, *Ys = smraw + 2 * 192;                   // 2 slots: T0 T1 T01 | Y (H x 16)
+    const double *At = A + tile_row0[t];
+    const double *tc = tcache_tile + (int64_t)t * npan * 64;
+    const double *tp = tpair_tile + (int64_t)t * ((npan + 1) / 2) * 64;
+    const int ngrp = (npan + 1) / 2;
+    auto stage = [&](int g, int slot) {
+        double *Y = Ys + slot * Hp * 16, *T = Ts + slot * 192;
+        const int p0 = 2 * g, np = min(2, npan - p0), h0 = 8 * p0, hs = Hp - h0;
+        for (int e = threadIdx.x; e < 8 * np * hs; e += NT) {
+            const int r = h0 + e % hs, jj = e / hs, c = 8 * p0 + jj;
+            const bool ok = c < n && r > c && r < H;
+            cp_async8(Y + r * 16 + jj, At + (ok ? r + (int64_t)c * lda : 0), ok);
+        }
+        if (threadIdx.x < 64 * np) cp_async8(T + threadIdx.x, tc + 64 * p0 + threadIdx.x, true);
+        if (np == 2 && threadIdx.x < 64) cp_async8(T + 128 + threadIdx.x, tp + 64 * g + threadIdx.x, true);
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, q = lane & 3, l4 = lane >> 2;
+    const int col = 8 * warp + l4;
+    const bool okc = col < k;
+    double *cp = C + tile_row0[t] + (int64_t)(okc ? col : 0) * ldc;
+    stage(kFwd ? 0 : ngrp - 1, 0);
+    double c[MR][2];
+#pragma unroll
+    for (int kk = 0; kk < MR; ++kk) {
+        c[kk][0] = c[kk][1] = 0.0;
+        if (kk < nrb) ld_pair(c[kk][0], c[kk][1], cp, okc, 8 * kk + 2 * q, H);
+    }
+    for (int gg = 0; gg < ngrp; ++gg) {
+        const int g = kFwd ? gg : ngrp - 1 - gg, slot = gg & 1;
+        if (gg + 1 < ngrp) {
+            stage(kFwd ? g + 1 : g - 1, slot ^ 1);
+            asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+        } else {
+            asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+        }
+        __syncthreads();
+        const int p0 = 2 * g, np = min(2, npan - p0);
+        double *Y = Ys + slot * Hp * 16, *T = Ts + slot * 192;
+        if (threadIdx.x < 8 * np) {                             // the unit diagonals
+            const int cc = 8 * p0 + threadIdx.x;
+            if (cc < n && cc < H) Y[cc * 16 + threadIdx.x] = 1.0;
+        }
+        __syncthreads();
+        auto tb = [&](const double *Tm, int e) { return kFwd ? Tm[(2 * q + e) * 8 + l4] : Tm[l4 * 8 + 2 * q + e]; };
+        if (np == 2) {
+            const double a0 = tb(T, 0), a1 = tb(T, 1), b0 = tb(T + 64, 0), b1 = tb(T + 64, 1);
+            const double x0 = tb(T + 128, 0), x1 = tb(T + 128, 1);
+            double w0[2] = {0.0, 0.0}, w1[2] = {0.0, 0.0}, v0[2] = {0.0, 0.0}, v1[2] = {0.0, 0.0};
+#pragma unroll
+            for (int kk = 0; kk < MR; ++kk) {
+                if (kk >= p0 && kk < nrb) {
+                    const int r = 8 * kk + 2 * q;
+                    dmma(w0[kk & 1], w1[kk & 1], c[kk][0], Y[r * 16 + l4]);
+                    dmma(w0[kk & 1], w1[kk & 1], c[kk][1], Y[(r + 1) * 16 + l4]);
+                    dmma(v0[kk & 1], v1[kk & 1], c[kk][0], Y[r * 16 + 8 + l4]);
+                    dmma(v0[kk & 1], v1[kk & 1], c[kk][1], Y[(r + 1) * 16 + 8 + l4]);
+                }
+            }
+            const double we = w0[0] + w0[1], wo = w1[0] + w1[1], ve = v0[0] + v0[1], vo = v1[0] + v1[1];
+            double q0 = 0.0, q1 = 0.0, r0 = 0.0, r1 = 0.0;
+            dmma(q0, q1, we, a0);
+            dmma(q0, q1, wo, a1);
+            if (kFwd) {                                         // P1 = W0^T T01 + W1^T T1
+                dmma(r0, r1, we, x0);
+                dmma(r0, r1, wo, x1);
+            } else {                                            // P0 += W1^T T01^T
+                dmma(q0, q1, ve, x0);
+                dmma(q0, q1, vo, x1);
+            }
+            dmma(r0, r1, ve, b0);
+            dmma(r0, r1, vo, b1);
+#pragma unroll
+            for (int kk = 0; kk < MR; ++kk) {
+                if (kk >= p0 && kk < nrb) {
+                    const double2 y = *reinterpret_cast<const double2 *>(Y + (8 * kk + l4) * 16 + 2 * q);
+                    const double2 z = *reinterpret_cast<const double2 *>(Y + (8 * kk + l4) * 16 + 8 + 2 * q);
+                    dmma(c[kk][0], c[kk][1], -q0, y.x);
+                    dmma(c[kk][0], c[kk][1], -q1, y.y);
+                    dmma(c[kk][0], c[kk][1], -r0, z.x);
+                    dmma(c[kk][0], c[kk][1], -r1, z.y);
+                }
+            }
+        } else {                                                // the last, unpaired panel
+            const double t0 = tb(T, 0), t1 = tb(T, 1);
+            double w0[2] = {0.0, 0.0}, w1[2] = {0.0, 0.0};
+#pragma unroll
+            for (int kk = 0; kk < MR; ++kk) {
+                if (kk >= p0 && kk < nrb) {
+                    const int r = 8 * kk + 2 * q;
+                    dmma(w0[kk & 1], w1[kk & 1], c[kk][0], Y[r * 16 + l4]);
+                    dmma(w0[kk & 1], w1[kk & 1], c[kk][1], Y[(r + 1) * 16 + l4]);
+                }
+            }
+            double q0 = 0.0, q1 = 0.0;
+            dmma(q0, q1, w0[0] + w0[1], t0);
+            dmma(q0, q1, w1[0] + w1[1], t1);
+#pragma unroll
+            for (int kk = 0; kk < MR; ++kk) {
+                if (kk >= p0 && kk < nrb) {
+                    const int r8 = 8 * kk + l4;
+                    dmma(c[kk][0], c[kk][1], -q0, Y[r8 * 16 + 2 * q]);
+                    dmma(c[kk][0], c[kk][1], -q1, Y[r8 * 16 + 2 * q + 1]);
+                }
+            }
+        }
+        __syncthreads();                                        // the slot may be refilled
+    }
+#pragma unroll
+    for (int kk = 0; kk < MR; ++kk)
+        if (kk < nrb) st_pair(cp, okc, 8 * kk + 2 * q, H, c[kk][0], c[kk][1]);
+}
+
 // Q^T / Q of one tree step's nodes on C's head rows (or on xbuf blocks for form Q).
 template <bool kFwd>
 __global__ void __launch_bounds__(NT, 1)
@@ -1359,6 +1487,21 @@ cudaError_t launch_wide_apply_leaves(const double *A, int64_t lda, int n, const 
                                      int L, int max_rows, const double *tcache, const double *tpair, double *C,
                                      int64_t ldc, int k, int forward, cudaStream_t st) {
     const int pairs = max_rows <= 1024;                      // the factor cached T01 (wide_leaf_qr, KM <= 16)
+#ifndef TSQR_NO_APPLY_REG
+    constexpr int MR = 44;                                     // register-resident slab: tiles <= 352 rows
+    if (pairs && k <= 64 && max_rows <= 8 * MR) {
+        const size_t rb = sizeof(double) * (2 * 192 + 2 * (size_t)(8 * ((max_rows + 7) / 8)) * 16);
+        const void *fr = forward ? (const void *)k_wide_apply_leaves_reg<true, MR>
+                                 : (const void *)k_wide_apply_leaves_reg<false, MR>;
+        cudaError_t er = cudaFuncSetAttribute(fr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rb);
+        if (er != cudaSuccess) return er;
+        if (forward)
+            k_wide_apply_leaves_reg<true, MR><<<L, NT, rb, st>>>(A, lda, n, row0, rows, tcache, tpair, C, ldc, k);
+        else
+            k_wide_apply_leaves_reg<false, MR><<<L, NT, rb, st>>>(A, lda, n, row0, rows, tcache, tpair, C, ldc, k);
+        return cudaGetLastError();
+    }
+#endif
     const int slots = apply_leaf_smem(max_rows, 2) <= 227 * 1024 ? 2 : 1;   // prefetch the next group if it fits
     const size_t bytes = apply_leaf_smem(max_rows, slots);
     const void *fn = forward ? (const void *)k_wide_apply_leaves<true> : (const void *)k_wide_apply_leaves<false>;
