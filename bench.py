@@ -421,6 +421,22 @@ def run_ours(args, cfg):
             traffic_src = tj.get("source")
         except Exception:
             traffic = None
+    # the second op against its own roofline: form Q at DORGQR's count 2mn^2 - 2n^3/3 with Y read
+    # and Q written (16mn bytes), Q^T C at 4mnk with Y read and C read and written (8m(n + 2k))
+    t2 = ts - tf
+    second_roof = None
+    if t2 > 0:
+        if cfg["op"] == "form_q":
+            f2, b2 = 2.0 * m * n * n - 2.0 * n ** 3 / 3, 16.0 * m * n
+            models = ("2mn^2 - 2n^3/3", "16mn (Y in, Q out)")
+        else:
+            f2, b2 = 4.0 * m * n * k, 8.0 * m * (n + 2 * k)
+            models = ("4mnk", "8m(n + 2k) (Y in, C in and out)")
+        tf2, tb2 = f2 / (peak * 1e12), b2 / (bw * 1e9 * world)
+        second_roof = {"op": cfg["op"], "ms": t2, "flops_model": models[0], "bytes_model": models[1],
+                       "achieved_tflops": f2 / (t2 * 1e-3) / 1e12, "achieved_gbs": b2 / (t2 * 1e-3) / 1e9,
+                       "bound": "alu" if tf2 >= tb2 else "hbm", "frac": max(tf2, tb2) / (t2 * 1e-3),
+                       "timing": "median step minus median factor (CUDA events on the step's stream)"}
     launches_per_step = kernel_launches(info, n, cfg["op"], world)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -455,6 +471,7 @@ def run_ours(args, cfg):
         "ms_factor": tf, "ms_factor_min": tf_min, "ms_factor_mean": tf_mean, "second_op_ms": ts - tf,
         "second_op_gflops": (2.0 * m * n * n - 2.0 * n ** 3 / 3 if cfg["op"] == "form_q" else 4.0 * m * n * k)
         / ((ts - tf) * 1e-3) / 1e9 if ts > tf else None,
+        "second_op_roofline": second_roof,
         "timed_region_wall_ms": wall * 1e3,
         "clocks": clk, "gpu_launches": launches_per_step * args.steps,
         "e2e": e2e, "cpu_baseline": cpu,
