@@ -129,7 +129,11 @@ def test_form_q(m, n, b, s):
                                        (5000, 50, 4096, 192, 64), (4096, 64, 4096, 64, 200),
                                        (20000, 50, 4096, 704, 64), (40000, 32, 4096, 4096, 128),
                                        (1000, 50, 1000, 1000, 70), (20000, 200, 2048, 2048, 64),
-                                       (5000, 100, 2048, 2048, 13)])
+                                       (5000, 100, 2048, 2048, 13),
+                                       # wide: 19 column slabs (a warp takes several) through the
+                                       # panel-pipelined node stage; 352-row tiles with k = 64 (the
+                                       # register-resident leaf apply)
+                                       (6000, 136, 3000, 340, 150), (3520, 96, 3520, 352, 64)])
 def test_apply_qt(m, n, b, s, k):
     A0, Ad, R, tree, p, f = _run(m, n, b, s, seed=5)
     Ct = inputs.gaussian(m, k, seed=1)
@@ -220,7 +224,8 @@ def test_tree_reuse_and_repeat_determinism():
                                        (1500, 33, 400, 128, 130), (5000, 50, 4096, 192, 64), (777, 5, 100, 30, 1),
                                        (3003, 56, 3003, 1001, 20), (4000, 49, 4000, 1000, 9), (700, 57, 700, 100, 57),
                                        (50, 50, 50, 50, 8), (300, 9, 300, 40, 11), (5000, 100, 2048, 2048, 13),
-                                       (3000, 65, 1000, 1000, 65), (7000, 128, 3500, 512, 40), (300, 200, 300, 300, 7)])
+                                       (3000, 65, 1000, 1000, 65), (7000, 128, 3500, 512, 40), (300, 200, 300, 300, 7),
+                                       (6000, 136, 3000, 340, 150), (3520, 96, 3520, 352, 64)])
 def test_apply_q(m, n, b, s, k):
     """C <- Q C (the reverse traversal) against the oracle's apply_q on the same plan,
     the round trip Q (Q^T C) = C, and Q [I; 0] = the explicit Q of form_q."""
