@@ -350,11 +350,25 @@ constexpr int UNR = 8;
 
 // a lane's row pair (r, r+1) of a C column, r even: one 16-byte access when the column
 // pointer is 16-byte aligned (even tile starts and an even ldc make every pair aligned)
+#ifdef TSQR_WIDE_L2KEEP
+// variant: the row pairs of C carry an L2 evict_last policy (a tile's trailing columns are
+// re-streamed once per panel pair; keep them in L2 against the other tiles' traffic)
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+#endif
 __device__ __forceinline__ void ld_pair(double &x0, double &x1, const double *cp, bool okc, int r, int H) {
     if (okc && r + 1 < H && !(reinterpret_cast<uintptr_t>(cp) & 15)) {
+#ifdef TSQR_WIDE_L2KEEP
+        asm("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+            : "=d"(x0), "=d"(x1) : "l"(cp + r), "l"(l2_keep_policy()) : "memory");
+#else
         const double2 v = *reinterpret_cast<const double2 *>(cp + r);
         x0 = v.x;
         x1 = v.y;
+#endif
     } else {
         x0 = (okc && r < H) ? cp[r] : 0.0;
         x1 = (okc && r + 1 < H) ? cp[r + 1] : 0.0;
@@ -362,7 +376,12 @@ __device__ __forceinline__ void ld_pair(double &x0, double &x1, const double *cp
 }
 __device__ __forceinline__ void st_pair(double *cp, bool okc, int r, int H, double x0, double x1) {
     if (okc && r + 1 < H && !(reinterpret_cast<uintptr_t>(cp) & 15)) {
+#ifdef TSQR_WIDE_L2KEEP
+        asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;"
+                     :: "l"(cp + r), "d"(x0), "d"(x1), "l"(l2_keep_policy()) : "memory");
+#else
         *reinterpret_cast<double2 *>(cp + r) = make_double2(x0, x1);
+#endif
     } else {
         if (okc && r < H) cp[r] = x0;
         if (okc && r + 1 < H) cp[r + 1] = x1;

@@ -8,12 +8,12 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_0808_2664_b200 import _build  # noqa: E402
 
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-os.makedirs(os.path.join(root, "build_ab"), exist_ok=True)
+os.makedirs(os.path.join(root, os.environ.get("AB_DIR", "build_ab")), exist_ok=True)
 
 
 def one(spec):
     name, _, flags = spec.partition(":")
-    out = os.path.join(root, "build_ab", name + ".so")
+    out = os.path.join(root, os.environ.get("AB_DIR", "build_ab"), name + ".so")
     _build.build_variant(out, [f for f in flags.split(",") if f], force=True)
     return out
 
