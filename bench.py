@@ -42,7 +42,7 @@ sys.path.insert(0, ROOT)
 CONFIGS = {
     "c1": dict(m=4096, n=16, b=512, s=512, kind="gauss", op="form_q", k=0,
                desc="fp64 A 4096x16 N(0,1) seed 0, row blocks 512 (8-leaf binary tree): factor + form Q"),
-    "c2": dict(m=1_000_000, n=50, b=4096, s=1024, kind="gauss", op="form_q", k=0,
+    "c2": dict(m=1_000_000, n=50, b=4096, s=1366, kind="gauss", op="form_q", k=0,
                desc="fp64 A 1,000,000x50 N(0,1), row blocks 4096, binary tree: factor + form Q"),
     "c3": dict(m=100_000, n=200, b=2048, s=400, kind="gauss", op="apply_qt", k=64,
                desc="fp64 A 100,000x200 N(0,1), row blocks 2048 (blocked compact-WY leaves): factor + apply Q^T "
