@@ -96,7 +96,7 @@ struct Sync {
 // ACQUIRE (release/acquire synchronisation at cta scope; __syncwarp gives the
 // cumulativity over the publisher's lanes).  On sm_100a the release compiles to
 // MEMBAR.ALL.CTA, which waits for the warp's outstanding global stores, and costs
-// 6-8 % of the leaf kernel, so it is a variant; the
+// 6-16 % of the leaf kernel (C4 +16 % on the final code, profiles/r02j_house3_acqrel_ab.txt), so it is a variant; the
 // jitter build (-DTSQR_HANDOFF_JITTER) injects pseudo-random __nanosleep delays
 // between the data and the counter on both sides and is checked bitwise against
 // the default build and against the oracle (tests/test_gpu_handoff.py).
@@ -146,10 +146,11 @@ __device__ __forceinline__ void sync_publish(int *c, int v) {
 // dlarfg scalars (readings R1/R2/R19), branch-free: beta = -sign(alpha) N with
 // N = sqrt(alpha^2 + sigma2), tau = 1 + |alpha|/N, scale = 1/(alpha - beta);
 // sigma2 == 0 gives H = I (tau = 0, beta = alpha).  1/sqrt(y) and 1/(|alpha| + N)
-// from the MUFU seeds and two Newton steps each: <= 2 ulp; the reciprocal is
-// seeded from |alpha| + y r0 so its MUFU runs while the root is refined.
-// (-DTSQR_HOUSE3: one third-order correction per seed, one dependent step
-// shorter -- measured no faster on the full kernel.)
+// from the MUFU seeds, each refined by one third-order correction (seed errors
+// ~2^-22 -> O(2^-66) + rounding); the reciprocal is seeded from |alpha| + y r0
+// so its MUFU runs while the root is refined.  (-DTSQR_HOUSE_NEWTON2: two Newton
+// steps per seed, one dependent step longer: C4 leaf +0.5 %,
+// profiles/r02j_house3_acqrel_ab.txt.)
 // The plain sums and the flush-to-zero seeds need the input range of reading
 // R23; the robust instantiation (kRobust) rescales outside it.
 __device__ __forceinline__ House house_bf(double alpha, double s2) {
@@ -159,7 +160,7 @@ __device__ __forceinline__ House house_bf(double alpha, double s2) {
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r0) : "d"(y));
     const double D0 = fma(y, r0, aa);
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(i0) : "d"(D0));
-#ifndef TSQR_HOUSE3
+#ifdef TSQR_HOUSE_NEWTON2
     const double hy = 0.5 * y;
     double r = r0 * fma(-hy * r0, r0, 1.5);
     const double D1 = fma(y, r, aa);
