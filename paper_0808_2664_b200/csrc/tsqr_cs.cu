@@ -40,10 +40,14 @@ struct ApplyCs {
     // Y column-major (Yt: NP x CH, stride LDT = CH + 2), read bank-conflict free by both DMMA
     // operand patterns: W^T = C^T Y (a lane's rows 2q, 2q+1 of column l4: one 16-byte load;
     // LDT = 2 mod 4 doubles spreads the 8 columns over the banks) and C -= Y W' (rows l4,
-    // columns 2q+e); then the T's.  (The [0, OFF_YT) region held a row-major copy for the first
-    // pattern, written per chunk after the staging: dropped, the region stays unused.)
-    static constexpr int LDY = C::NP + 2, LDT = C::CH + 2;
-    static constexpr int OFF_YT = C::CH * LDY, OFF_T = OFF_YT + C::NP * LDT;
+    // columns 2q+e); then the T's.
+    static constexpr int LDT = C::CH + 2;
+#ifdef TSQR_APPLY_OLD_SLOT
+    static constexpr int OFF_YT = C::CH * (C::NP + 2);   // variant: the old row-major region kept, unused
+#else
+    static constexpr int OFF_YT = 0;
+#endif
+    static constexpr int OFF_T = OFF_YT + C::NP * LDT;
     static constexpr int YS = OFF_T + C::NCB * 64;
     static_assert(LDT % 2 == 0 && OFF_YT % 2 == 0 && OFF_T % 2 == 0 && YS % 2 == 0, "bulk copy targets 16-byte aligned");
     static constexpr size_t BYTES = (size_t)2 * YS * sizeof(double) + 2 * sizeof(uint64_t);   // + two mbarriers
